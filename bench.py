@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""bench.py — candidate plans scored/sec on B200 (metric of BASELINE.json).
+
+One step = score one batch of candidate topological orders of a training
+graph: per candidate the order-validity verdict (graph.cpp:239-254), lifetimes
+(schedule.cpp:33-50), resident bytes per step and the peak
+(schedule.cpp:69-88) and its first step (plan.cpp:135-141), plus the
+first-minimum argmin over the batch — one fused sm_100a kernel (K1+K3 with the
+argmin folded in). At N>1 every rank scores its own batch (weak scaling,
+disjoint candidate index ranges) and the best plan is chosen with ONE NCCL
+allreduce(min) on a packed (peak, index) key, inside the timed region.
+
+  python bench.py [--config c2|c4|c5] [--gpus N] [--steps K] [--warmup W]
+  python bench.py --impl reference ...   # the reference's own CPU scorer
+
+Default config c2 = ResNet-50 fwd+bwd+SGD training graph, batch 32
+(workloads/graphs/resnet50_b32.json.gz), 4,096 candidates per GPU.
+"""
+from __future__ import annotations
+
+import argparse
+import gzip
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_BYTES = 126 * 2**20
+CONFIGS = {
+    "c2": {"workload": "resnet50_b32_fwd_bwd_sgd", "graph": "resnet50_b32.json.gz",
+           "candidates": 4096},
+    "c3": {"workload": "bert_base_s512_fwd_bwd_sgd", "graph": "bert_base_s512.json.gz",
+           "candidates": 4096},
+    "c4": {"workload": "gpt2_medium_s1024_fwd_bwd_sgd", "graph": "gpt2_medium_s1024.json.gz",
+           "candidates": 8192},
+    "c5": {"workload": "training_like_L33333_100k_tensors", "generate": ("training_like", 33333, 8),
+           "candidates": 1024},
+}
+
+
+def load_graph(cfg):
+    import paper_2210_12924_b200 as mp
+    if "generate" in cfg:
+        return mp.generate_graph(*cfg["generate"])
+    with gzip.open(os.path.join(ROOT, "workloads", "graphs", cfg["graph"]), "rt") as f:
+        return mp.load_graph(f.read())
+
+
+# ---- clocks (NVML, sampled in a thread during the timed region) ----------------------
+class ClockSampler:
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting", 0x1: "gpu_idle"}
+
+    def __init__(self, torch_device):
+        self.samples = []
+        self.ok = False
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            props = torch.cuda.get_device_properties(torch_device)
+            bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+            try:
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(torch_device.index or 0)
+            self.nv = pynvml
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # no NVML: report nothing rather than guess
+            self.err = str(e)
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                try:
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.samples.append((time.perf_counter(), sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def start(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self._t:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self, t0, t1):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": "nvml unavailable"}
+        win = [s for s in self.samples if t0 <= s[0] <= t1]
+        note = "sampled during the timed region"
+        if not win:
+            win = self.samples[-5:]
+            note = "timed region shorter than one NVML sample; nearest samples"
+        reasons = set()
+        for _, _, r in win:
+            for bit, name in self.REASONS.items():
+                if r & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median([s[1] for s in win]) if win else None,
+                "sm_max_mhz": self.max_sm, "reasons": sorted(reasons), "samples": len(win),
+                "note": note}
+
+
+def measured_peak_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def profile_traffic(config):
+    """dram bytes per launch of the scoring kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", f"{config}_score_ncu.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ---- reference arm -------------------------------------------------------------------
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    import paper_2210_12924_b200 as mp
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/libmemplan_ref.so not built"}))
+        return 0
+    g = load_graph(cfg)
+    rg = O.RefGraph.load(mp.save_graph(g))
+    threads = os.cpu_count() or 1
+    orders = mp.random_topo_orders(g, min(cfg["candidates"], 4096), seed=12345)
+    # calibrate: bounded sample per step so the whole run ends within a few minutes
+    t = time.perf_counter()
+    rg.score_orders(orders[:threads], threads=threads)
+    per = (time.perf_counter() - t) / threads * threads  # seconds per `threads` candidates
+    budget = 90.0 / max(args.steps + args.warmup, 1)
+    m = int(max(threads, min(len(orders), threads * budget / max(per, 1e-9))))
+    sample = orders[:m]
+    for _ in range(args.warmup):
+        rg.score_orders(sample, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        peak, valid, best = rg.score_orders(sample, threads=threads)
+    dt = time.perf_counter() - t0
+    value = m * args.steps / dt
+    line = {
+        "impl": "reference", "metric": "candidate plans scored/sec", "value": value,
+        "unit": "plans/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "nodes": g.n, "edges": g.E,
+                   "candidates_per_step": m},
+        "cpu_baseline": {"value": value, "unit": "plans/s", "cores": threads, "kind": "reference",
+                         "sample": f"{m} random topological orders per step, memplan::"
+                                   f"peak_resident_bytes per order + first-min argmin, "
+                                   f"{threads} host threads"},
+        "e2e": {"value": value, "unit": "plans/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def cpu_baseline(g, orders, seconds=10.0):
+    """The reference (oracle/_ref) on this host's cores over a bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    import paper_2210_12924_b200 as mp
+    if not O.ref_available():
+        return None
+    rg = O.RefGraph.load(mp.save_graph(g))
+    threads = os.cpu_count() or 1
+    t = time.perf_counter()
+    k = min(len(orders), threads * 2)
+    rg.score_orders(orders[:k], threads=threads)
+    per = (time.perf_counter() - t) / k
+    m = int(min(len(orders), max(k, seconds / max(per, 1e-9))))
+    t = time.perf_counter()
+    rg.score_orders(orders[:m], threads=threads)
+    dt = time.perf_counter() - t
+    return {"value": m / dt, "unit": "plans/s", "cores": threads, "kind": "reference",
+            "sample": f"{m} of the step's candidate orders, reference memplan::peak_resident_bytes "
+                      f"(oracle/_ref, -O3) on {threads} host threads + first-min argmin"}
+
+
+# ---- our arm -------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2210_12924_b200 as mp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    g = load_graph(cfg)
+    C = cfg["candidates"]
+    n = g.n
+    planner = mp.Planner(local)
+    dg = planner.upload(g)
+    info = dg.info()
+    stream = torch.cuda.current_stream(dev)
+    planner.set_stream(stream.cuda_stream)
+
+    # Candidate batches: distinct seeded random topological orders, rotated so the
+    # bytes touched between reuses exceed L2 (inputs larger than L2 every step).
+    batch_bytes = C * n * 4
+    nb = max(1, -(-2 * L2_BYTES // batch_bytes))
+    host_batches = [mp.random_topo_orders(g, C, seed=1000 * rank + b) for b in range(nb)]
+    batches = [torch.from_numpy(hb).to(dev) for hb in host_batches]
+    peak = torch.zeros(C, dtype=torch.int64, device=dev)
+    step = torch.zeros(C, dtype=torch.int32, device=dev)
+    valid = torch.zeros(C, dtype=torch.uint8, device=dev)
+    key = torch.zeros(1, dtype=torch.int64, device=dev)
+    base = rank * C
+
+    def one_step(b):
+        key.fill_(-1)  # UINT64_MAX as the atomicMin identity
+        planner.score_orders_argmin_d(dg, batches[b % nb], C, peak, step, valid, key, base,
+                                      stream.cuda_stream)
+        if world > 1:
+            k = key.view(torch.int64)
+            dist.all_reduce(k, op=dist.ReduceOp.MIN)
+
+    for i in range(args.warmup):
+        one_step(i)
+    torch.cuda.synchronize()
+    # key semantics check on the last warm-up batch (the fused argmin is the product)
+    kk = int(key.cpu().numpy().view(np.uint64)[0])
+
+    clocks = ClockSampler(dev)
+    clocks.start()
+    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    start.record(stream)
+    for i in range(args.steps):
+        key.fill_(-1)
+        ev_s[i].record(stream)
+        planner.score_orders_argmin_d(dg, batches[i % nb], C, peak, step, valid, key, base,
+                                      stream.cuda_stream)
+        ev_e[i].record(stream)
+        if world > 1:
+            dist.all_reduce(key, op=dist.ReduceOp.MIN)
+    end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t1 = time.perf_counter()
+    clocks.stop()
+    total_ms = start.elapsed_time(end)
+    kern_ms = sum(a.elapsed_time(b) for a, b in zip(ev_s, ev_e)) / args.steps
+    t = torch.tensor([total_ms, kern_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, kern_ms = float(t[0]), float(t[1])
+    ms_per_step = total_ms / args.steps
+    value = world * C / (ms_per_step / 1e3)
+
+    # roofline of the scoring kernel: algorithmic bytes per launch
+    graph_bytes = (4 * (n + 1) + 4 * info["num_pred_pairs"] + 16 * n
+                   + 4 * (info["num_multi_sink"] + 1) + 12 * info["num_multi_sink"])
+    alg_bytes = C * (4 * n + 16) + graph_bytes
+    peak_gbs, peak_src = measured_peak_gbs()
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+
+    # e2e through the public host-buffer API: pinned orders in, results out, every step
+    e2e_steps = args.e2e_steps or min(args.steps, 50)
+    pinned = [torch.from_numpy(hb).pin_memory() for hb in host_batches[:2]]
+    h_peak = torch.zeros(C, dtype=torch.int64).pin_memory()
+    h_step = torch.zeros(C, dtype=torch.int32).pin_memory()
+    h_valid = torch.zeros(C, dtype=torch.uint8).pin_memory()
+    planner.set_stream(None)
+    for i in range(3):
+        planner.score_orders_into(dg, pinned[i % 2].numpy(), h_peak, h_step, h_valid)
+    if world > 1:
+        dist.barrier()
+    te0 = time.perf_counter()
+    for i in range(e2e_steps):
+        best = planner.score_orders_into(dg, pinned[i % 2].numpy(), h_peak, h_step, h_valid)
+        if world > 1:
+            kv = (int(h_peak[best]) << 20 | (best + base)) if best >= 0 else 2**63 - 1
+            bk = torch.tensor([kv], device=dev)
+            dist.all_reduce(bk, op=dist.ReduceOp.MIN)
+            bk.item()
+    te = torch.tensor([time.perf_counter() - te0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * C * e2e_steps / float(te[0])
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(g, host_batches[0])
+        line = {
+            "metric": "candidate plans scored/sec (peak bytes + validity + argmin)",
+            "value": value, "unit": "plans/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "nodes": n, "edges": g.E,
+                       "sinks": int(len(g.sinks)), "candidates_per_gpu": C,
+                       "candidate_source": "seeded random topological orders (randomised Kahn)",
+                       "l2": f"inputs larger than L2: {nb} rotating batches of "
+                             f"{batch_bytes / 2**20:.1f} MiB ({nb * batch_bytes / 2**20:.0f} MiB"
+                             " > 126 MiB L2)",
+                       "parallelism": f"dp{world} (candidates sharded, 1 allreduce-min)",
+                       "smem_resident": bool(info["smem_resident"])},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
+                         "frac": achieved / peak_gbs, "traffic": profile_traffic(args.config),
+                         "kernel": "score_kernel (K1+K3 fused + argmin)",
+                         "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": alg_bytes,
+                         "peak_source": peak_src},
+            "e2e": {"value": e2e_value, "unit": "plans/s", "h2d_bytes_per_step": batch_bytes,
+                    "d2h_bytes_per_step": C * 13 + 8,
+                    "path": "Planner.score_orders_into -> mp_score_orders_best (pinned host)"},
+            "gpu_launches": args.steps,
+            "clocks": clocks.summary(t0, t1),
+            "best_key_check": kk != 2**64 - 1,
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    planner.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,228 @@
+/* memplan_b200 — B200-native (sm_100a) data-parallel core of the OLLA memory
+ * planner (arXiv 2210.12924), behind a plain C ABI.
+ *
+ * This header is the drop-in boundary. Every entry point names the
+ * reference interface it replaces (file:line under /root/reference/proj).
+ * The reference has no FFI of its own (it is a static C++ library,
+ * CMakeLists.txt:10-25); INTEGRATION.md shows the C++ shim a maintainer adds
+ * so memplan's pipeline/CLI call these functions with their existing
+ * signatures, and the ctypes binding the Python tests use.
+ *
+ * Conventions
+ *   - Indices are int32 (memplan::NodeIndex / EdgeIndex are `int`,
+ *     graph.hpp:58-59); byte sizes and addresses are uint64.
+ *   - Timesteps are 1-based and intervals closed, as memplan::Interval
+ *     (analysis.hpp:28-37); an interval with lo > hi is empty.
+ *   - Functions without the `_d` suffix take HOST buffers and copy in/out.
+ *     `_d` variants take DEVICE pointers and a cudaStream_t (as void*), are
+ *     stream-ordered and never synchronise unless stated.
+ *   - No CPU fallback exists: with no usable sm_100 device every call that
+ *     computes returns MP_E_NO_DEVICE / MP_E_CUDA.
+ *   - Errors map 1:1 onto the reference's exception classes
+ *     (errors.hpp:24-76); mp_last_error() returns the reference-format
+ *     message ("InvalidOrder: sequence is not a topological order of the
+ *     graph", schedule.cpp:25-26).
+ */
+#ifndef MEMPLAN_B200_H_
+#define MEMPLAN_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MP_ABI_VERSION 1
+
+typedef enum {
+  MP_OK = 0,
+  MP_E_INVALID_ORDER = 1, /* memplan::InvalidOrder (schedule.cpp:25, plan.cpp:107) */
+  MP_E_BAD_GRAPH = 2,     /* DanglingEndpoint / InvalidStructure analogues (graph.cpp:64-141) */
+  MP_E_INVALID_ARG = 3,   /* null pointer, negative size, mismatched lengths */
+  MP_E_CUDA = 4,          /* CUDA runtime failure (message in mp_last_error) */
+  MP_E_OOM = 5,           /* device allocation failed */
+  MP_E_CAPACITY = 6,      /* caller buffer smaller than the result (count returned) */
+  MP_E_NO_DEVICE = 7      /* no sm_100 device: there is no CPU fallback */
+} mp_status;
+
+typedef struct mp_ctx mp_ctx;     /* one device + one stream + scratch */
+typedef struct mp_graph mp_graph; /* device-resident graph (CSR + derived tables) */
+
+/* Flattened memplan::Graph (graph.hpp:62-127): edge e is produced by
+ * edge_src[e] and consumed by sinks[sink_off[e] .. sink_off[e+1]).
+ * edge_size[e] == 0 marks a control edge (graph.cpp:89-93): it orders nodes
+ * but carries no bytes. Node order is program order. */
+typedef struct {
+  int32_t num_nodes;
+  int32_t num_edges;
+  const int32_t* edge_src;   /* [num_edges] */
+  const int64_t* sink_off;   /* [num_edges + 1] */
+  const int32_t* sinks;      /* [sink_off[num_edges]] */
+  const uint64_t* edge_size; /* [num_edges] */
+} mp_csr;
+
+typedef struct {
+  int32_t num_nodes;
+  int32_t num_edges;
+  int64_t num_sinks;
+  int64_t num_pred_pairs;  /* distinct (producer, consumer) node pairs checked for validity */
+  int32_t num_multi_sink;  /* data edges whose last consumer depends on the order */
+  int32_t smem_resident;   /* 1 when the fused scorer keeps per-candidate state in smem */
+  uint64_t total_bytes;    /* Graph::total_bytes() (graph.hpp:93) */
+} mp_graph_info;
+
+/* ---- context / graph lifetime --------------------------------------------- */
+int mp_abi_version(void);
+const char* mp_status_string(mp_status s);
+const char* mp_last_error(void); /* thread-local, reference-format message */
+
+mp_status mp_ctx_create(int device, mp_ctx** out);
+mp_status mp_ctx_destroy(mp_ctx* ctx);
+/* Use a caller stream (cudaStream_t as void*) instead of the context's own. */
+mp_status mp_ctx_set_stream(mp_ctx* ctx, void* stream);
+mp_status mp_ctx_synchronize(mp_ctx* ctx);
+
+/* Validates and uploads a graph once (the analogue of Graph::build,
+ * graph.cpp:64-141, for the checks the kernels rely on: endpoints in range,
+ * monotone sink offsets, no duplicate sink within one edge). */
+mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out);
+mp_status mp_graph_free(mp_graph* g);
+mp_status mp_graph_get_info(const mp_graph* g, mp_graph_info* info);
+
+/* ---- (a2/a3) lifetimes over one order ---------------------------------------
+ * memplan::lifetimes_from_order (schedule.cpp:33-50) incl. the
+ * is_topological_order verdict (graph.cpp:239-254): returns
+ * MP_E_INVALID_ORDER for a non-topological order. lo/hi: [num_edges]. */
+mp_status mp_lifetimes(mp_ctx* ctx, const mp_graph* g, const int32_t* order, int64_t order_len,
+                       int32_t* lo, int32_t* hi);
+mp_status mp_lifetimes_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_order,
+                         int64_t order_len, int32_t* d_lo, int32_t* d_hi, int32_t* d_valid,
+                         void* stream);
+
+/* ---- (a4) realized lifetimes -------------------------------------------------
+ * memplan::realized_lifetimes (plan.cpp:101-120). timestep_of[v] == 0 means
+ * node v has no timestep; the first such node met in edge order (source,
+ * then sinks) yields MP_E_INVALID_ORDER "node <id> has no timestep" — the
+ * node index is returned in *missing_node (ids live on the host side). */
+mp_status mp_realized_lifetimes(mp_ctx* ctx, const mp_graph* g, const int32_t* timestep_of,
+                                int32_t horizon, int32_t* lo, int32_t* hi,
+                                int32_t* missing_node);
+
+/* ---- (a8/a9/a10) resident bytes ---------------------------------------------
+ * resident_bytes_per_step / peak_resident_bytes (schedule.cpp:69-88). */
+mp_status mp_resident_bytes(mp_ctx* ctx, const mp_graph* g, const int32_t* order,
+                            int64_t order_len, uint64_t* bytes /* [num_nodes] */);
+mp_status mp_peak_resident_bytes(mp_ctx* ctx, const mp_graph* g, const int32_t* order,
+                                 int64_t order_len, uint64_t* peak);
+/* timeline_from_lifetimes (plan.cpp:122-143): bytes per step over
+ * 1..horizon (bytes may be NULL), peak_rs and peak_step (first strict
+ * maximum; 1 when all zero and horizon > 0; 0 when horizon == 0). */
+mp_status mp_timeline(mp_ctx* ctx, const mp_graph* g, const int32_t* lo, const int32_t* hi,
+                      int32_t horizon, uint64_t* bytes, uint64_t* peak_rs, int32_t* peak_step);
+
+/* ---- batched candidate scoring (K1+K3 fused) ----------------------------------
+ * For each candidate order c (row c of [num_orders][num_nodes] int32):
+ * valid[c] = is_topological_order (graph.cpp:239-254); when valid,
+ * peak[c] = peak_resident_bytes (schedule.cpp:81-88) and peak_step[c] the
+ * first step attaining it (plan.cpp:135-141); invalid candidates get
+ * peak = 0, peak_step = 0. The multi-order analogue of
+ * enumerate_min_peak's scoring (oracle.cpp:74-93). */
+mp_status mp_score_orders(mp_ctx* ctx, const mp_graph* g, const int32_t* orders,
+                          int64_t num_orders, uint64_t* peak, int32_t* peak_step,
+                          uint8_t* valid);
+mp_status mp_score_orders_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_orders,
+                            int64_t num_orders, uint64_t* d_peak, int32_t* d_peak_step,
+                            uint8_t* d_valid, void* stream);
+/* Scoring with the argmin fused in: *best = first-minimum index over valid
+ * candidates (-1 if none). One kernel on the device; host buffers. */
+mp_status mp_score_orders_best(mp_ctx* ctx, const mp_graph* g, const int32_t* orders,
+                               int64_t num_orders, uint64_t* peak, int32_t* peak_step,
+                               uint8_t* valid, int64_t* best);
+/* Device variant of the fused form: every valid candidate c does
+ * atomicMin(d_best_key, peak << 20 | (c + index_base)); the caller sets
+ * *d_best_key = UINT64_MAX beforehand (stream-ordered). Keys that do not fit
+ * (peak >= 2^43 or index >= 2^20) are recorded as UINT64_MAX - 1, telling
+ * the caller to fall back to mp_argmin_key_d. The minimum key across GPUs
+ * (one allreduce(min)) is the global first-minimum. */
+mp_status mp_score_orders_argmin_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_orders,
+                                   int64_t num_orders, uint64_t* d_peak, int32_t* d_peak_step,
+                                   uint8_t* d_valid, uint64_t* d_best_key, int64_t index_base,
+                                   void* stream);
+/* First-minimum argmin over valid candidates (oracle.cpp:78-81 keeps the
+ * first strictly smaller peak): *best = index or -1 when none is valid. */
+mp_status mp_argmin(mp_ctx* ctx, const uint64_t* peak, const uint8_t* valid, int64_t num_orders,
+                    int64_t* best);
+/* Device variant (one CTA): d_out3[0] = best index + index_base (or -1),
+ * d_out3[1] = its peak, d_out3[2] = packed key peak << 20 | index (UINT64_MAX
+ * when nothing is valid or the key does not fit: peak >= 2^43 or index >=
+ * 2^20). index_base makes keys of different GPU shards comparable. */
+mp_status mp_argmin_key_d(mp_ctx* ctx, const uint64_t* d_peak, const uint8_t* d_valid,
+                          int64_t num_orders, int64_t index_base, uint64_t* d_out3,
+                          void* stream);
+
+/* ---- (a6) liveness-overlap pairs --------------------------------------------
+ * The pair set of encode_addresses' loop (encode.cpp:347-367): i < j in
+ * edge-index order, size[i] > 0 and size[j] > 0 (encode.cpp:329-331), not
+ * both pinned (:351), closed intervals intersecting (:354). The
+ * edge_precedes filter (:355-357) removes nothing on lifetimes realized from
+ * a topological order, which is the contract here.
+ * pinned may be NULL. Two-phase: call with pairs == NULL for the count;
+ * pairs is [cap][2] int32 in lexicographic (i, j) order. */
+mp_status mp_overlap_pairs(mp_ctx* ctx, int32_t num_edges, const int32_t* lo, const int32_t* hi,
+                           const uint64_t* size, const uint8_t* pinned, int32_t* pairs,
+                           int64_t cap, int64_t* count);
+/* Device variant over a row range [row_begin, row_end) (for sharding rows
+ * across GPUs): d_row_off[row_end-row_begin+1] (int64) receives the
+ * exclusive offsets (relative to the range), pairs are written when d_pairs
+ * != NULL and the range total fits cap. */
+mp_status mp_overlap_pairs_d(mp_ctx* ctx, int32_t num_edges, const int32_t* d_lo,
+                             const int32_t* d_hi, const uint64_t* d_size,
+                             const uint8_t* d_pinned, int64_t row_begin, int64_t row_end,
+                             int64_t* d_row_off, int32_t* d_pairs, int64_t cap,
+                             int64_t* count, void* stream);
+
+/* ---- (a11/a12/a13) address-plan validation + fragmentation ---------------------
+ * Pairwise part of validate_plan (plan.cpp:390-404): among edges with
+ * size > 0 and has_addr != 0, pairs i < j whose closed lifetimes intersect
+ * and whose [addr, addr+size) ranges overlap. Violating pairs come back in
+ * (i, j) order (viol [cap][2], may be NULL for the count). */
+mp_status mp_validate_pairs(mp_ctx* ctx, int32_t num_edges, const int32_t* lo, const int32_t* hi,
+                            const uint64_t* size, const uint8_t* has_addr, const uint64_t* addr,
+                            int32_t* viol, int64_t cap, int64_t* num_viol);
+mp_status mp_validate_pairs_d(mp_ctx* ctx, int32_t num_edges, const int32_t* d_lo,
+                              const int32_t* d_hi, const uint64_t* d_size,
+                              const uint8_t* d_has_addr, const uint64_t* d_addr,
+                              int64_t row_begin, int64_t row_end, int64_t* d_row_off,
+                              int32_t* d_viol, int64_t cap, int64_t* num_viol, void* stream);
+/* addresses_feasible (pipeline.cpp:146-160): *feasible = 1 iff no
+ * conflicting pair among edges with has_addr. */
+mp_status mp_addresses_feasible(mp_ctx* ctx, int32_t num_edges, const int32_t* lo,
+                                const int32_t* hi, const uint64_t* size,
+                                const uint8_t* has_addr, const uint64_t* addr, int32_t* feasible);
+/* peak_mem = max(addr + size) over edges with an address (pipeline.cpp:270-275). */
+mp_status mp_peak_mem(mp_ctx* ctx, int32_t num_edges, const uint64_t* size,
+                      const uint8_t* has_addr, const uint64_t* addr, uint64_t* peak_mem);
+/* fragmentation (placement.cpp:64-67): (mr - rs) / mr, 0 when mr == 0. */
+double mp_fragmentation(uint64_t mr, uint64_t rs);
+
+/* ---- workload helpers (host C++, not on the measured path) ----------------------
+ * Deterministic graph families with the semantics of generate_graph
+ * (generate.cpp:45-158; chain = 0, fork_join = 1, training_like = 2).
+ * Two-phase: call with NULL arrays to get the dims. Node/edge ids are not
+ * produced (the CSR is id-free); training_like's naming is documented in
+ * paper_2210_12924_b200/graph.py. */
+mp_status mp_generate_graph(int kind, int32_t layers, uint64_t size, uint64_t seed,
+                            int32_t* num_nodes, int32_t* num_edges, int64_t* num_sinks,
+                            int32_t* edge_src, int64_t* sink_off, int32_t* sinks,
+                            uint64_t* edge_size, uint8_t* node_role);
+/* Seeded uniformly-random topological orders (randomised Kahn; candidate c
+ * uses a splitmix64 stream seeded from (seed, c)). out: [num_orders][n]. */
+mp_status mp_random_topo_orders(const mp_csr* csr, int64_t num_orders, uint64_t seed,
+                                int32_t num_threads, int32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MEMPLAN_B200_H_ */

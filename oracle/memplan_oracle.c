@@ -1,0 +1,226 @@
+/* TEST INFRASTRUCTURE ONLY — see memplan_oracle.h. Plain-C restatement of
+ * the reference planner's hot path; every function cites the reference
+ * file:line it restates. Compiled by oracle/Makefile into
+ * oracle/_build/liboracle.so. Deliberately scalar and literal: it mirrors
+ * the reference loops (including their complexity) rather than the GPU
+ * algorithms, so an agreement between the two is evidence, not tautology.
+ */
+#include "memplan_oracle.h"
+
+#include <stdlib.h>
+#include <string.h>
+
+/* graph.cpp:239-254: length n, each node once and in range, every sink of
+ * every edge (data and control) strictly after its source. */
+int or_is_topological_order(const or_graph* g, const int32_t* order, int64_t len) {
+  if (len != g->n) return 0;
+  int32_t* pos = (int32_t*)malloc(sizeof(int32_t) * (size_t)(g->n > 0 ? g->n : 1));
+  for (int32_t v = 0; v < g->n; ++v) pos[v] = -1;
+  int ok = 1;
+  for (int64_t i = 0; i < len && ok; ++i) {
+    int32_t v = order[i];
+    if (v < 0 || v >= g->n || pos[v] != -1) ok = 0;
+    else pos[v] = (int32_t)i;
+  }
+  for (int32_t e = 0; e < g->num_edges && ok; ++e) {
+    int32_t s0 = pos[g->edge_src[e]];
+    for (int64_t k = g->sink_off[e]; k < g->sink_off[e + 1]; ++k)
+      if (pos[g->sinks[k]] <= s0) { ok = 0; break; }
+  }
+  free(pos);
+  return ok;
+}
+
+/* schedule.cpp:23-31 */
+int or_positions_of(const or_graph* g, const int32_t* order, int64_t len, int32_t* pos) {
+  if (!or_is_topological_order(g, order, len)) return 1; /* InvalidOrder */
+  for (int32_t v = 0; v < g->n; ++v) pos[v] = 0;
+  for (int64_t i = 0; i < len; ++i) pos[order[i]] = (int32_t)i + 1;
+  return 0;
+}
+
+/* schedule.cpp:33-50 */
+int or_lifetimes_from_order(const or_graph* g, const int32_t* order, int64_t len,
+                            int32_t* lo, int32_t* hi) {
+  int32_t* pos = (int32_t*)malloc(sizeof(int32_t) * (size_t)(g->n > 0 ? g->n : 1));
+  if (or_positions_of(g, order, len, pos)) { free(pos); return 1; }
+  for (int32_t e = 0; e < g->num_edges; ++e) {
+    lo[e] = pos[g->edge_src[e]];
+    hi[e] = lo[e];
+    if (g->sink_off[e] == g->sink_off[e + 1]) {
+      hi[e] = g->n;
+    } else {
+      for (int64_t k = g->sink_off[e]; k < g->sink_off[e + 1]; ++k)
+        if (pos[g->sinks[k]] > hi[e]) hi[e] = pos[g->sinks[k]];
+    }
+  }
+  free(pos);
+  return 0;
+}
+
+/* schedule.cpp:69-79 — the literal per-timestep accumulation. */
+int or_resident_bytes_per_step(const or_graph* g, const int32_t* order, int64_t len,
+                               uint64_t* out) {
+  int32_t E = g->num_edges;
+  int32_t* lo = (int32_t*)malloc(sizeof(int32_t) * (size_t)(E > 0 ? E : 1));
+  int32_t* hi = (int32_t*)malloc(sizeof(int32_t) * (size_t)(E > 0 ? E : 1));
+  if (or_lifetimes_from_order(g, order, len, lo, hi)) { free(lo); free(hi); return 1; }
+  for (int32_t t = 0; t < g->n; ++t) out[t] = 0;
+  for (int32_t e = 0; e < E; ++e)
+    for (int32_t t = lo[e]; t <= hi[e]; ++t) out[t - 1] += g->edge_size[e];
+  free(lo);
+  free(hi);
+  return 0;
+}
+
+/* schedule.cpp:81-88 */
+int or_peak_resident_bytes(const or_graph* g, const int32_t* order, int64_t len,
+                           uint64_t* peak) {
+  uint64_t* rs = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(g->n > 0 ? g->n : 1));
+  if (or_resident_bytes_per_step(g, order, len, rs)) { free(rs); return 1; }
+  uint64_t best = 0;
+  for (int32_t t = 0; t < g->n; ++t) if (rs[t] > best) best = rs[t];
+  *peak = best;
+  free(rs);
+  return 0;
+}
+
+/* plan.cpp:122-143 (bytes, peak_rs, peak_step; the per-step live id lists
+ * are not restated). contains(t) is lo <= t <= hi (analysis.hpp:31-32). */
+void or_timeline_from_lifetimes(const or_graph* g, const int32_t* lo, const int32_t* hi,
+                                int32_t horizon, uint64_t* bytes, uint64_t* peak_rs,
+                                int32_t* peak_step) {
+  uint64_t best = 0;
+  int32_t best_t = 0;
+  for (int32_t t = 1; t <= horizon; ++t) {
+    uint64_t b = 0;
+    for (int32_t e = 0; e < g->num_edges; ++e)
+      if (lo[e] <= t && t <= hi[e]) b += g->edge_size[e];
+    if (bytes) bytes[t - 1] = b;
+    if (b > best) { best = b; best_t = t; }
+  }
+  if (horizon > 0 && best_t == 0) best_t = 1;
+  *peak_rs = best;
+  *peak_step = best_t;
+}
+
+/* plan.cpp:101-120: source first, then sinks in declaration order; the
+ * first node without a timestep raises InvalidOrder. */
+int or_realized_lifetimes(const or_graph* g, const int32_t* timestep_of, int32_t horizon,
+                          int32_t* lo, int32_t* hi, int32_t* missing) {
+  for (int32_t e = 0; e < g->num_edges; ++e) {
+    int32_t s = g->edge_src[e];
+    if (timestep_of[s] == 0) { *missing = s; return 1; }
+    int32_t l = timestep_of[s];
+    int32_t h = g->sink_off[e] == g->sink_off[e + 1] ? horizon : l;
+    for (int64_t k = g->sink_off[e]; k < g->sink_off[e + 1]; ++k) {
+      int32_t w = g->sinks[k];
+      if (timestep_of[w] == 0) { *missing = w; return 1; }
+      if (timestep_of[w] > h) h = timestep_of[w];
+    }
+    lo[e] = l;
+    hi[e] = h;
+  }
+  return 0;
+}
+
+/* analysis.hpp:28-37 */
+static int disjoint(int32_t alo, int32_t ahi, int32_t blo, int32_t bhi) {
+  return alo > ahi || blo > bhi || ahi < blo || bhi < alo;
+}
+
+static int pair_live(const int32_t* lo, const int32_t* hi, const uint64_t* size,
+                     const uint8_t* pinned, int32_t i, int32_t j) {
+  if (size[i] == 0 || size[j] == 0) return 0;             /* encode.cpp:329-331 */
+  if (pinned && pinned[i] && pinned[j]) return 0;          /* encode.cpp:351 */
+  return !disjoint(lo[i], hi[i], lo[j], hi[j]);            /* encode.cpp:354 */
+}
+
+/* encode.cpp:347-367 pair enumeration order: data edges a<b in edge-index
+ * order. */
+int64_t or_overlap_pairs(int32_t num_edges, const int32_t* lo, const int32_t* hi,
+                         const uint64_t* size, const uint8_t* pinned,
+                         int32_t* pairs, int64_t cap) {
+  int64_t count = 0;
+  for (int32_t i = 0; i < num_edges; ++i)
+    for (int32_t j = i + 1; j < num_edges; ++j) {
+      if (!pair_live(lo, hi, size, pinned, i, j)) continue;
+      if (pairs && count < cap) {
+        pairs[2 * count] = i;
+        pairs[2 * count + 1] = j;
+      }
+      ++count;
+    }
+  return count;
+}
+
+void or_overlap_row_stats(int32_t num_edges, const int32_t* lo, const int32_t* hi,
+                          const uint64_t* size, const uint8_t* pinned,
+                          int64_t row_begin, int64_t row_end,
+                          int64_t* row_count, uint64_t* row_hash) {
+  for (int64_t i = row_begin; i < row_end; ++i) {
+    int64_t c = 0;
+    uint64_t h = 1469598103934665603ull;
+    for (int32_t j = (int32_t)i + 1; j < num_edges; ++j) {
+      if (!pair_live(lo, hi, size, pinned, (int32_t)i, j)) continue;
+      ++c;
+      h = (h ^ (uint64_t)(uint32_t)j) * 1099511628211ull;
+    }
+    row_count[i - row_begin] = c;
+    row_hash[i - row_begin] = h;
+  }
+}
+
+/* plan.cpp:390-404 */
+int64_t or_validate_pairs(int32_t num_edges, const int32_t* lo, const int32_t* hi,
+                          const uint64_t* size, const uint8_t* has_addr,
+                          const uint64_t* addr, int32_t* viol, int64_t cap) {
+  int64_t count = 0;
+  for (int32_t i = 0; i < num_edges; ++i) {
+    if (size[i] == 0 || !has_addr[i]) continue;
+    for (int32_t j = i + 1; j < num_edges; ++j) {
+      if (size[j] == 0 || !has_addr[j]) continue;
+      if (disjoint(lo[i], hi[i], lo[j], hi[j])) continue;
+      uint64_t a_lo = addr[i], b_lo = addr[j];
+      if (a_lo < b_lo + size[j] && b_lo < a_lo + size[i]) {
+        if (viol && count < cap) {
+          viol[2 * count] = i;
+          viol[2 * count + 1] = j;
+        }
+        ++count;
+      }
+    }
+  }
+  return count;
+}
+
+/* pipeline.cpp:146-160 (iterates the address map, i.e. edges with an
+ * address in index order). */
+int or_addresses_feasible(int32_t num_edges, const int32_t* lo, const int32_t* hi,
+                          const uint64_t* size, const uint8_t* has_addr,
+                          const uint64_t* addr) {
+  for (int32_t i = 0; i < num_edges; ++i) {
+    if (!has_addr[i]) continue;
+    for (int32_t j = i + 1; j < num_edges; ++j) {
+      if (!has_addr[j]) continue;
+      if (disjoint(lo[i], hi[i], lo[j], hi[j])) continue;
+      if (addr[i] < addr[j] + size[j] && addr[j] < addr[i] + size[i]) return 0;
+    }
+  }
+  return 1;
+}
+
+/* placement.cpp:64-67 */
+double or_fragmentation(uint64_t mr, uint64_t rs) {
+  if (mr == 0) return 0.0;
+  return (double)(mr - rs) / (double)mr;
+}
+
+/* pipeline.cpp:270-275 */
+uint64_t or_peak_mem(int32_t num_edges, const uint64_t* size, const uint8_t* has_addr,
+                     const uint64_t* addr) {
+  uint64_t peak = 0;
+  for (int32_t e = 0; e < num_edges; ++e)
+    if (has_addr[e] && addr[e] + size[e] > peak) peak = addr[e] + size[e];
+  return peak;
+}

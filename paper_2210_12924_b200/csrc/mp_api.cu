@@ -1,0 +1,746 @@
+// C ABI of memplan_b200 (include/memplan_b200.h): contexts, graph upload
+// with the derived scoring tables, and the host-buffer / device-buffer entry
+// points that launch the kernels in k_score.cu, k_lifetimes.cu, k_pairs.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mp_internal.h"
+
+namespace mpb {
+
+namespace {
+thread_local std::string g_err;
+const char* kInvalidOrderMsg = "InvalidOrder: sequence is not a topological order of the graph";
+}  // namespace
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+mp_status cuda_status(cudaError_t e, const char* what) {
+  set_error(std::string("CUDA error: ") + cudaGetErrorString(e) + " (" + what + ")");
+  cudaGetLastError();  // clear sticky-free errors
+  return e == cudaErrorMemoryAllocation ? MP_E_OOM : MP_E_CUDA;
+}
+
+mp_status Scratch::reserve(size_t want) {
+  if (want <= bytes && ptr) return MP_OK;
+  if (ptr) {
+    cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  size_t b = want + want / 4 + 4096;
+  MP_CUDA(cudaMalloc(&ptr, b));
+  bytes = b;
+  return MP_OK;
+}
+
+Scratch::~Scratch() {
+  if (ptr) cudaFree(ptr);
+}
+
+// Bump allocator over one scratch slot (256-byte aligned pieces).
+struct Carver {
+  char* base;
+  size_t at = 0;
+  explicit Carver(void* p) : base(static_cast<char*>(p)) {}
+  template <typename T>
+  T* take(size_t count) {
+    T* p = reinterpret_cast<T*>(base + at);
+    at += (count * sizeof(T) + 255) & ~size_t(255);
+    return p;
+  }
+  static size_t size_of(std::initializer_list<size_t> bytes) {
+    size_t s = 0;
+    for (size_t b : bytes) s += (b + 255) & ~size_t(255);
+    return s + 256;
+  }
+};
+
+struct DeviceGuard {
+  explicit DeviceGuard(int dev) { cudaSetDevice(dev); }
+};
+
+mp_status invalid_order() {
+  set_error(kInvalidOrderMsg);
+  return MP_E_INVALID_ORDER;
+}
+
+mp_status invalid_arg(const std::string& what) {
+  set_error("InvalidArgument: " + what);
+  return MP_E_INVALID_ARG;
+}
+
+template <typename T>
+mp_status upload(T** dst, const T* src, size_t count, cudaStream_t st) {
+  *dst = nullptr;
+  if (count == 0) return MP_OK;
+  MP_CUDA(cudaMalloc(reinterpret_cast<void**>(dst), count * sizeof(T)));
+  MP_CUDA(cudaMemcpyAsync(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice, st));
+  return MP_OK;
+}
+
+}  // namespace mpb
+
+using namespace mpb;
+
+extern "C" {
+
+int mp_abi_version(void) { return MP_ABI_VERSION; }
+
+const char* mp_status_string(mp_status s) {
+  switch (s) {
+    case MP_OK: return "MP_OK";
+    case MP_E_INVALID_ORDER: return "MP_E_INVALID_ORDER";
+    case MP_E_BAD_GRAPH: return "MP_E_BAD_GRAPH";
+    case MP_E_INVALID_ARG: return "MP_E_INVALID_ARG";
+    case MP_E_CUDA: return "MP_E_CUDA";
+    case MP_E_OOM: return "MP_E_OOM";
+    case MP_E_CAPACITY: return "MP_E_CAPACITY";
+    case MP_E_NO_DEVICE: return "MP_E_NO_DEVICE";
+  }
+  return "MP_E_UNKNOWN";
+}
+
+const char* mp_last_error(void) { return g_err.c_str(); }
+
+mp_status mp_ctx_create(int device, mp_ctx** out) {
+  if (!out) return invalid_arg("out is null");
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    set_error("memplan_b200: no CUDA device visible; there is no CPU fallback");
+    return MP_E_NO_DEVICE;
+  }
+  if (device < 0 || device >= count) return invalid_arg("device index out of range");
+  cudaDeviceProp prop;
+  MP_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) {
+    set_error("memplan_b200: device " + std::to_string(device) + " is sm_" +
+              std::to_string(prop.major) + std::to_string(prop.minor) +
+              "; this library is built for sm_100a only");
+    return MP_E_NO_DEVICE;
+  }
+  DeviceGuard guard(device);
+  auto* ctx = new mp_ctx();
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  ctx->max_smem_optin = (size_t)optin;
+  cudaError_t ce = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+  if (ce == cudaSuccess) ce = cudaMalloc(reinterpret_cast<void**>(&ctx->d_small), 256);
+  if (ce != cudaSuccess) {
+    mp_status s = cuda_status(ce, "mp_ctx_create");
+    delete ctx;
+    return s;
+  }
+  ctx->stream = ctx->own_stream;
+  *out = ctx;
+  return MP_OK;
+}
+
+mp_status mp_ctx_destroy(mp_ctx* ctx) {
+  if (!ctx) return MP_OK;
+  DeviceGuard guard(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->d_small) cudaFree(ctx->d_small);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+  return MP_OK;
+}
+
+mp_status mp_ctx_set_stream(mp_ctx* ctx, void* stream) {
+  if (!ctx) return invalid_arg("ctx is null");
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  return MP_OK;
+}
+
+mp_status mp_ctx_synchronize(mp_ctx* ctx) {
+  if (!ctx) return invalid_arg("ctx is null");
+  DeviceGuard guard(ctx->device);
+  MP_CUDA(cudaStreamSynchronize(ctx->stream));
+  return MP_OK;
+}
+
+// ---- graph upload -----------------------------------------------------------
+mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
+  if (!ctx || !csr || !out) return invalid_arg("null argument");
+  *out = nullptr;
+  const int32_t n = csr->num_nodes, E = csr->num_edges;
+  if (n < 0 || E < 0) return invalid_arg("negative graph dimensions");
+  if (E > 0 && (!csr->edge_src || !csr->sink_off || !csr->edge_size))
+    return invalid_arg("edge arrays are null");
+  if (E > 0 && csr->sink_off[0] != 0) {
+    set_error("InvalidStructure: sink_off[0] must be 0");
+    return MP_E_BAD_GRAPH;
+  }
+  const int64_t S = E > 0 ? csr->sink_off[E] : 0;
+  if (S > 0 && !csr->sinks) return invalid_arg("sinks is null");
+
+  auto* g = new mp_graph();
+  g->ctx = ctx;
+  g->n = n;
+  g->E = E;
+  g->S = S;
+  g->h_edge_src.assign(csr->edge_src, csr->edge_src + E);
+  g->h_sink_off.assign(csr->sink_off, csr->sink_off + (E > 0 ? E + 1 : 0));
+  if (E == 0) g->h_sink_off.assign(1, 0);
+  g->h_sinks.assign(csr->sinks, csr->sinks + S);
+  g->h_edge_size.assign(csr->edge_size, csr->edge_size + E);
+
+  // Structural checks the kernels rely on (Graph::build, graph.cpp:82-128).
+  std::vector<std::vector<int32_t>> preds(n);
+  std::vector<uint64_t> alloc(n, 0), sfree(n, 0);
+  std::vector<int32_t> multi_off{0}, multi_sinks;
+  std::vector<uint64_t> multi_size;
+  uint64_t total = 0;
+  const uint64_t cap = uint64_t{1} << 62;
+  std::vector<int32_t> seen_stamp(n, -1);
+  for (int32_t e = 0; e < E; ++e) {
+    const int32_t s = g->h_edge_src[e];
+    const int64_t a = g->h_sink_off[e], b = g->h_sink_off[e + 1];
+    if (s < 0 || s >= n) {
+      set_error("DanglingEndpoint: edge #" + std::to_string(e) + " has unknown source");
+      delete g;
+      return MP_E_BAD_GRAPH;
+    }
+    if (b < a || b > S) {
+      set_error("InvalidStructure: sink offsets are not monotone");
+      delete g;
+      return MP_E_BAD_GRAPH;
+    }
+    for (int64_t k = a; k < b; ++k) {
+      const int32_t w = g->h_sinks[k];
+      if (w < 0 || w >= n) {
+        set_error("DanglingEndpoint: edge #" + std::to_string(e) + " has unknown sink");
+        delete g;
+        return MP_E_BAD_GRAPH;
+      }
+      if (seen_stamp[w] == e) {
+        set_error("InvalidStructure: edge #" + std::to_string(e) + " lists a sink twice");
+        delete g;
+        return MP_E_BAD_GRAPH;
+      }
+      seen_stamp[w] = e;
+      preds[w].push_back(s);
+    }
+    const uint64_t sz = g->h_edge_size[e];
+    if (sz >= cap || total + sz >= cap) {
+      set_error("InvalidStructure: total tensor bytes exceed the supported range");
+      delete g;
+      return MP_E_BAD_GRAPH;
+    }
+    total += sz;
+    if (sz == 0) continue;  // control edge: orders nodes, carries no bytes
+    alloc[s] += sz;
+    if (b - a == 1) {
+      sfree[g->h_sinks[a]] += sz;
+    } else if (b - a >= 2) {
+      for (int64_t k = a; k < b; ++k) multi_sinks.push_back(g->h_sinks[k]);
+      multi_off.push_back((int32_t)multi_sinks.size());
+      multi_size.push_back(sz);
+    }
+  }
+  g->total_bytes = total;
+  std::vector<int32_t> pred_off(n + 1, 0), pred_flat;
+  for (int32_t v = 0; v < n; ++v) {
+    auto& p = preds[v];
+    std::sort(p.begin(), p.end());
+    p.erase(std::unique(p.begin(), p.end()), p.end());
+    pred_flat.insert(pred_flat.end(), p.begin(), p.end());
+    pred_off[v + 1] = (int32_t)pred_flat.size();
+  }
+  g->D = (int64_t)pred_flat.size();
+  g->M = (int32_t)multi_size.size();
+  g->MS = (int64_t)multi_sinks.size();
+
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = ctx->stream;
+  mp_status s = MP_OK;
+  auto up = [&](mp_status r) {
+    if (s == MP_OK) s = r;
+  };
+  up(upload(&g->d_edge_src, g->h_edge_src.data(), (size_t)E, st));
+  up(upload(&g->d_sink_off, g->h_sink_off.data(), (size_t)E + 1, st));
+  up(upload(&g->d_sinks, g->h_sinks.data(), (size_t)S, st));
+  up(upload(&g->d_edge_size, g->h_edge_size.data(), (size_t)E, st));
+  up(upload(&g->d_pred_off, pred_off.data(), (size_t)n + 1, st));
+  up(upload(&g->d_preds, pred_flat.data(), pred_flat.size(), st));
+  up(upload(&g->d_node_alloc, alloc.data(), (size_t)n, st));
+  up(upload(&g->d_node_sfree, sfree.data(), (size_t)n, st));
+  up(upload(&g->d_multi_off, multi_off.data(), multi_off.size(), st));
+  up(upload(&g->d_multi_sinks, multi_sinks.data(), multi_sinks.size(), st));
+  up(upload(&g->d_multi_size, multi_size.data(), multi_size.size(), st));
+  if (s == MP_OK) up(score_configure(g));
+  if (s == MP_OK) {
+    cudaError_t ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) s = cuda_status(ce, "mp_graph_upload");
+  }
+  if (s != MP_OK) {
+    mp_graph_free(g);
+    return s;
+  }
+  *out = g;
+  return MP_OK;
+}
+
+mp_status mp_graph_free(mp_graph* g) {
+  if (!g) return MP_OK;
+  DeviceGuard guard(g->ctx->device);
+  void* ptrs[] = {g->d_edge_src,  g->d_sink_off,   g->d_sinks,      g->d_edge_size,
+                  g->d_pred_off,  g->d_preds,      g->d_node_alloc, g->d_node_sfree,
+                  g->d_multi_off, g->d_multi_sinks, g->d_multi_size};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete g;
+  return MP_OK;
+}
+
+mp_status mp_graph_get_info(const mp_graph* g, mp_graph_info* info) {
+  if (!g || !info) return invalid_arg("null argument");
+  info->num_nodes = g->n;
+  info->num_edges = g->E;
+  info->num_sinks = g->S;
+  info->num_pred_pairs = g->D;
+  info->num_multi_sink = g->M;
+  info->smem_resident = g->smem_resident ? 1 : 0;
+  info->total_bytes = g->total_bytes;
+  return MP_OK;
+}
+
+// ---- lifetimes ------------------------------------------------------------------
+mp_status mp_lifetimes_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_order, int64_t len,
+                         int32_t* d_lo, int32_t* d_hi, int32_t* d_valid, void* stream) {
+  if (!ctx || !g || (len > 0 && !d_order) || !d_valid) return invalid_arg("null argument");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  MP_TRY(ctx->scratch[2].reserve(sizeof(int32_t) * ((size_t)g->n + 1)));
+  return launch_lifetimes(g, d_order, len, d_lo, d_hi, d_valid,
+                          static_cast<int32_t*>(ctx->scratch[2].ptr), st);
+}
+
+mp_status mp_lifetimes(mp_ctx* ctx, const mp_graph* g, const int32_t* order, int64_t len,
+                       int32_t* lo, int32_t* hi) {
+  if (!ctx || !g || (len > 0 && !order) || (g->E > 0 && (!lo || !hi)))
+    return invalid_arg("null argument");
+  if (len != g->n) return invalid_order();
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const size_t n = (size_t)g->n, E = (size_t)g->E;
+  MP_TRY(ctx->scratch[0].reserve(Carver::size_of({4 * n, 4 * E, 4 * E, 4})));
+  Carver cv(ctx->scratch[0].ptr);
+  int32_t* d_order = cv.take<int32_t>(n);
+  int32_t* d_lo = cv.take<int32_t>(E);
+  int32_t* d_hi = cv.take<int32_t>(E);
+  int32_t* d_valid = cv.take<int32_t>(1);
+  if (n) MP_CUDA(cudaMemcpyAsync(d_order, order, 4 * n, cudaMemcpyHostToDevice, st));
+  MP_TRY(mp_lifetimes_d(ctx, g, d_order, len, d_lo, d_hi, d_valid, st));
+  int32_t valid = 0;
+  MP_CUDA(cudaMemcpyAsync(&valid, d_valid, 4, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaStreamSynchronize(st));
+  if (!valid) return invalid_order();
+  if (E) {
+    MP_CUDA(cudaMemcpyAsync(lo, d_lo, 4 * E, cudaMemcpyDeviceToHost, st));
+    MP_CUDA(cudaMemcpyAsync(hi, d_hi, 4 * E, cudaMemcpyDeviceToHost, st));
+    MP_CUDA(cudaStreamSynchronize(st));
+  }
+  return MP_OK;
+}
+
+mp_status mp_realized_lifetimes(mp_ctx* ctx, const mp_graph* g, const int32_t* timestep_of,
+                                int32_t horizon, int32_t* lo, int32_t* hi,
+                                int32_t* missing_node) {
+  if (!ctx || !g || (g->n > 0 && !timestep_of) || (g->E > 0 && (!lo || !hi)))
+    return invalid_arg("null argument");
+  if (missing_node) *missing_node = -1;
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const size_t n = (size_t)g->n, E = (size_t)g->E;
+  MP_TRY(ctx->scratch[0].reserve(Carver::size_of({4 * n, 4 * E, 4 * E, 4})));
+  Carver cv(ctx->scratch[0].ptr);
+  int32_t* d_ts = cv.take<int32_t>(n);
+  int32_t* d_lo = cv.take<int32_t>(E);
+  int32_t* d_hi = cv.take<int32_t>(E);
+  int32_t* d_bad = cv.take<int32_t>(1);
+  if (n) MP_CUDA(cudaMemcpyAsync(d_ts, timestep_of, 4 * n, cudaMemcpyHostToDevice, st));
+  const int32_t big = INT_MAX;
+  MP_CUDA(cudaMemcpyAsync(d_bad, &big, 4, cudaMemcpyHostToDevice, st));
+  MP_TRY(launch_realized(g, d_ts, horizon, d_lo, d_hi, d_bad, st));
+  int32_t bad = INT_MAX;
+  MP_CUDA(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaStreamSynchronize(st));
+  if (bad != INT_MAX) {
+    // Resolve the reference's first missing endpoint: source, then sinks
+    // (plan.cpp:111-116).
+    int32_t miss = g->h_edge_src[bad];
+    if (timestep_of[miss] != 0) {
+      for (int64_t k = g->h_sink_off[bad]; k < g->h_sink_off[bad + 1]; ++k)
+        if (timestep_of[g->h_sinks[k]] == 0) {
+          miss = g->h_sinks[k];
+          break;
+        }
+    }
+    if (missing_node) *missing_node = miss;
+    set_error("InvalidOrder: node #" + std::to_string(miss) + " has no timestep");
+    return MP_E_INVALID_ORDER;
+  }
+  if (E) {
+    MP_CUDA(cudaMemcpyAsync(lo, d_lo, 4 * E, cudaMemcpyDeviceToHost, st));
+    MP_CUDA(cudaMemcpyAsync(hi, d_hi, 4 * E, cudaMemcpyDeviceToHost, st));
+    MP_CUDA(cudaStreamSynchronize(st));
+  }
+  return MP_OK;
+}
+
+// ---- resident bytes / timeline ----------------------------------------------------
+static mp_status score_one(mp_ctx* ctx, const mp_graph* g, const int32_t* order, int64_t len,
+                           uint64_t* bytes, uint64_t* peak) {
+  if (!ctx || !g || (len > 0 && !order)) return invalid_arg("null argument");
+  if (len != g->n) return invalid_order();
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const size_t n = (size_t)g->n;
+  MP_TRY(ctx->scratch[0].reserve(Carver::size_of({4 * n, 8 * n, 8, 4, 1})));
+  Carver cv(ctx->scratch[0].ptr);
+  int32_t* d_order = cv.take<int32_t>(n);
+  uint64_t* d_bytes = cv.take<uint64_t>(n);
+  uint64_t* d_peak = cv.take<uint64_t>(1);
+  int32_t* d_step = cv.take<int32_t>(1);
+  uint8_t* d_valid = cv.take<uint8_t>(1);
+  if (n == 0) {
+    if (peak) *peak = 0;
+    return MP_OK;
+  }
+  MP_CUDA(cudaMemcpyAsync(d_order, order, 4 * n, cudaMemcpyHostToDevice, st));
+  MP_TRY(launch_score(g, d_order, 1, d_peak, d_step, d_valid, bytes ? d_bytes : nullptr,
+                       nullptr, 0, st));
+  uint8_t valid = 0;
+  uint64_t pk = 0;
+  MP_CUDA(cudaMemcpyAsync(&valid, d_valid, 1, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaMemcpyAsync(&pk, d_peak, 8, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaStreamSynchronize(st));
+  if (!valid) return invalid_order();
+  if (bytes) {
+    MP_CUDA(cudaMemcpyAsync(bytes, d_bytes, 8 * n, cudaMemcpyDeviceToHost, st));
+    MP_CUDA(cudaStreamSynchronize(st));
+  }
+  if (peak) *peak = pk;
+  return MP_OK;
+}
+
+mp_status mp_resident_bytes(mp_ctx* ctx, const mp_graph* g, const int32_t* order, int64_t len,
+                            uint64_t* bytes) {
+  if (g && g->n > 0 && !bytes) return invalid_arg("bytes is null");
+  return score_one(ctx, g, order, len, bytes, nullptr);
+}
+
+mp_status mp_peak_resident_bytes(mp_ctx* ctx, const mp_graph* g, const int32_t* order,
+                                 int64_t len, uint64_t* peak) {
+  if (!peak) return invalid_arg("peak is null");
+  return score_one(ctx, g, order, len, nullptr, peak);
+}
+
+mp_status mp_timeline(mp_ctx* ctx, const mp_graph* g, const int32_t* lo, const int32_t* hi,
+                      int32_t horizon, uint64_t* bytes, uint64_t* peak_rs, int32_t* peak_step) {
+  if (!ctx || !g || (g->E > 0 && (!lo || !hi)) || !peak_rs || !peak_step)
+    return invalid_arg("null argument");
+  if (horizon < 0) return invalid_arg("negative horizon");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const size_t E = (size_t)g->E, h = (size_t)horizon;
+  MP_TRY(ctx->scratch[0].reserve(Carver::size_of({4 * E, 4 * E, 8 * h, 8 * (h + 2), 8, 4})));
+  Carver cv(ctx->scratch[0].ptr);
+  int32_t* d_lo = cv.take<int32_t>(E);
+  int32_t* d_hi = cv.take<int32_t>(E);
+  uint64_t* d_bytes = cv.take<uint64_t>(h);
+  int64_t* d_diff = cv.take<int64_t>(h + 2);
+  uint64_t* d_peak = cv.take<uint64_t>(1);
+  int32_t* d_step = cv.take<int32_t>(1);
+  if (E) {
+    MP_CUDA(cudaMemcpyAsync(d_lo, lo, 4 * E, cudaMemcpyHostToDevice, st));
+    MP_CUDA(cudaMemcpyAsync(d_hi, hi, 4 * E, cudaMemcpyHostToDevice, st));
+  }
+  MP_TRY(launch_timeline(g->E, d_lo, d_hi, g->d_edge_size, horizon, bytes ? d_bytes : nullptr,
+                         d_peak, d_step, d_diff, st));
+  MP_CUDA(cudaMemcpyAsync(peak_rs, d_peak, 8, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaMemcpyAsync(peak_step, d_step, 4, cudaMemcpyDeviceToHost, st));
+  if (bytes && h) MP_CUDA(cudaMemcpyAsync(bytes, d_bytes, 8 * h, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaStreamSynchronize(st));
+  return MP_OK;
+}
+
+// ---- batched scoring --------------------------------------------------------------
+mp_status mp_score_orders_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_orders,
+                            int64_t C, uint64_t* d_peak, int32_t* d_step, uint8_t* d_valid,
+                            void* stream) {
+  return mp_score_orders_argmin_d(ctx, g, d_orders, C, d_peak, d_step, d_valid, nullptr, 0,
+                                  stream);
+}
+
+mp_status mp_score_orders_argmin_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_orders,
+                                   int64_t C, uint64_t* d_peak, int32_t* d_step,
+                                   uint8_t* d_valid, uint64_t* d_best_key, int64_t index_base,
+                                   void* stream) {
+  if (!ctx || !g || C < 0 || index_base < 0) return invalid_arg("null argument or negative count");
+  if (C > 0 && (!d_peak || !d_step || !d_valid || (g->n > 0 && !d_orders)))
+    return invalid_arg("null output");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  return launch_score(g, d_orders, C, d_peak, d_step, d_valid, nullptr, d_best_key, index_base,
+                      st);
+}
+
+mp_status mp_score_orders(mp_ctx* ctx, const mp_graph* g, const int32_t* orders, int64_t C,
+                          uint64_t* peak, int32_t* step, uint8_t* valid) {
+  return mp_score_orders_best(ctx, g, orders, C, peak, step, valid, nullptr);
+}
+
+mp_status mp_score_orders_best(mp_ctx* ctx, const mp_graph* g, const int32_t* orders, int64_t C,
+                               uint64_t* peak, int32_t* step, uint8_t* valid, int64_t* best) {
+  if (!ctx || !g || C < 0) return invalid_arg("null argument or negative count");
+  if (best) *best = -1;
+  if (C == 0) return MP_OK;
+  if (!peak || !step || !valid || (g->n > 0 && !orders)) return invalid_arg("null buffer");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const size_t n = (size_t)g->n, c = (size_t)C;
+  MP_TRY(ctx->scratch[0].reserve(Carver::size_of({4 * n * c, 8 * c, 4 * c, c, 24})));
+  Carver cv(ctx->scratch[0].ptr);
+  int32_t* d_orders = cv.take<int32_t>(n * c);
+  uint64_t* d_peak = cv.take<uint64_t>(c);
+  int32_t* d_step = cv.take<int32_t>(c);
+  uint8_t* d_valid = cv.take<uint8_t>(c);
+  uint64_t* d_key = cv.take<uint64_t>(3);
+  const bool fused = best && C <= (int64_t{1} << 20);
+  if (fused) MP_CUDA(cudaMemsetAsync(d_key, 0xff, 8, st));
+  if (n) MP_CUDA(cudaMemcpyAsync(d_orders, orders, 4 * n * c, cudaMemcpyHostToDevice, st));
+  MP_TRY(launch_score(g, d_orders, C, d_peak, d_step, d_valid, nullptr, fused ? d_key : nullptr,
+                      0, st));
+  uint64_t key = ~0ull;
+  if (fused) MP_CUDA(cudaMemcpyAsync(&key, d_key, 8, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaMemcpyAsync(peak, d_peak, 8 * c, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaMemcpyAsync(step, d_step, 4 * c, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaMemcpyAsync(valid, d_valid, c, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaStreamSynchronize(st));
+  if (best) {
+    if (key == ~0ull) {
+      *best = -1;                                   // no valid candidate
+    } else if (key != ~0ull - 1 && fused) {
+      *best = (int64_t)(key & ((1ull << 20) - 1));  // fused (peak, index) minimum
+    } else {                                        // key overflow: reduce on the device
+      MP_TRY(launch_argmin(d_peak, d_valid, C, 0, d_key, st));
+      uint64_t out0 = 0;
+      MP_CUDA(cudaMemcpyAsync(&out0, d_key, 8, cudaMemcpyDeviceToHost, st));
+      MP_CUDA(cudaStreamSynchronize(st));
+      *best = (int64_t)out0;
+    }
+  }
+  return MP_OK;
+}
+
+mp_status mp_argmin_key_d(mp_ctx* ctx, const uint64_t* d_peak, const uint8_t* d_valid,
+                          int64_t C, int64_t index_base, uint64_t* d_out3, void* stream) {
+  if (!ctx || !d_out3 || C < 0 || index_base < 0 || (C > 0 && (!d_peak || !d_valid)))
+    return invalid_arg("bad argument");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  return launch_argmin(d_peak, d_valid, C, index_base, d_out3, st);
+}
+
+mp_status mp_argmin(mp_ctx* ctx, const uint64_t* peak, const uint8_t* valid, int64_t C,
+                    int64_t* best) {
+  if (!ctx || !best || C < 0 || (C > 0 && (!peak || !valid))) return invalid_arg("bad argument");
+  *best = -1;
+  if (C == 0) return MP_OK;
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const size_t c = (size_t)C;
+  MP_TRY(ctx->scratch[1].reserve(Carver::size_of({8 * c, c, 24})));
+  Carver cv(ctx->scratch[1].ptr);
+  uint64_t* d_peak = cv.take<uint64_t>(c);
+  uint8_t* d_valid = cv.take<uint8_t>(c);
+  uint64_t* d_out = cv.take<uint64_t>(3);
+  MP_CUDA(cudaMemcpyAsync(d_peak, peak, 8 * c, cudaMemcpyHostToDevice, st));
+  MP_CUDA(cudaMemcpyAsync(d_valid, valid, c, cudaMemcpyHostToDevice, st));
+  MP_TRY(launch_argmin(d_peak, d_valid, C, 0, d_out, st));
+  uint64_t out[3];
+  MP_CUDA(cudaMemcpyAsync(out, d_out, 24, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaStreamSynchronize(st));
+  *best = (int64_t)out[0];
+  return MP_OK;
+}
+
+// ---- overlap pairs / validation ------------------------------------------------------
+static mp_status pair_sweep_d(mp_ctx* ctx, PairArgs a, int64_t* d_row_off, int32_t* d_out,
+                              int64_t cap, int64_t* count, cudaStream_t st) {
+  if (a.row_begin < 0 || a.row_end < a.row_begin || a.row_end > a.num_edges)
+    return invalid_arg("row range out of bounds");
+  MP_TRY(ctx->scratch[2].reserve(pairs_scratch_bytes(a, ctx->num_sms)));
+  int64_t total = 0;
+  MP_TRY(pairs_count(a, ctx->num_sms, ctx->scratch[2].ptr, d_row_off, &total, st));
+  *count = total;
+  if (!d_out) return MP_OK;
+  if (total > cap) {
+    set_error("Capacity: " + std::to_string(total) + " pairs exceed the buffer of " +
+              std::to_string(cap));
+    return MP_E_CAPACITY;
+  }
+  if (total > 0) MP_TRY(pairs_fill(a, ctx->num_sms, ctx->scratch[2].ptr, d_row_off, d_out, st));
+  return MP_OK;
+}
+
+static mp_status pair_sweep_h(mp_ctx* ctx, int mode, int32_t E, const int32_t* lo,
+                              const int32_t* hi, const uint64_t* size, const uint8_t* mask,
+                              const uint64_t* addr, int32_t* out, int64_t cap, int64_t* count) {
+  if (!ctx || !count || E < 0 || (E > 0 && (!lo || !hi || !size)))
+    return invalid_arg("null argument");
+  if (mode == 1 && E > 0 && (!mask || !addr)) return invalid_arg("null address arrays");
+  *count = 0;
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const size_t e = (size_t)E;
+  MP_TRY(ctx->scratch[0].reserve(Carver::size_of({4 * e, 4 * e, 8 * e, e, 8 * e, 8 * (e + 1)})));
+  Carver cv(ctx->scratch[0].ptr);
+  int32_t* d_lo = cv.take<int32_t>(e);
+  int32_t* d_hi = cv.take<int32_t>(e);
+  uint64_t* d_size = cv.take<uint64_t>(e);
+  uint8_t* d_mask = cv.take<uint8_t>(e);
+  uint64_t* d_addr = cv.take<uint64_t>(e);
+  int64_t* d_row_off = cv.take<int64_t>(e + 1);
+  if (E == 0) return MP_OK;
+  MP_CUDA(cudaMemcpyAsync(d_lo, lo, 4 * e, cudaMemcpyHostToDevice, st));
+  MP_CUDA(cudaMemcpyAsync(d_hi, hi, 4 * e, cudaMemcpyHostToDevice, st));
+  MP_CUDA(cudaMemcpyAsync(d_size, size, 8 * e, cudaMemcpyHostToDevice, st));
+  if (mask) MP_CUDA(cudaMemcpyAsync(d_mask, mask, e, cudaMemcpyHostToDevice, st));
+  if (addr) MP_CUDA(cudaMemcpyAsync(d_addr, addr, 8 * e, cudaMemcpyHostToDevice, st));
+  PairArgs a;
+  a.num_edges = E;
+  a.lo = d_lo;
+  a.hi = d_hi;
+  a.size = d_size;
+  a.mask = mask ? d_mask : nullptr;
+  a.addr = addr ? d_addr : nullptr;
+  a.mode = mode;
+  a.row_begin = 0;
+  a.row_end = E;
+  int64_t total = 0;
+  MP_TRY(ctx->scratch[2].reserve(pairs_scratch_bytes(a, ctx->num_sms)));
+  MP_TRY(pairs_count(a, ctx->num_sms, ctx->scratch[2].ptr, d_row_off, &total, st));
+  *count = total;
+  if (!out) return MP_OK;
+  if (total > cap) {
+    set_error("Capacity: " + std::to_string(total) + " pairs exceed the buffer of " +
+              std::to_string(cap));
+    return MP_E_CAPACITY;
+  }
+  if (total == 0) return MP_OK;
+  MP_TRY(ctx->scratch[1].reserve((size_t)total * 8 + 256));
+  int32_t* d_out = static_cast<int32_t*>(ctx->scratch[1].ptr);
+  MP_TRY(pairs_fill(a, ctx->num_sms, ctx->scratch[2].ptr, d_row_off, d_out, st));
+  MP_CUDA(cudaMemcpyAsync(out, d_out, (size_t)total * 8, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaStreamSynchronize(st));
+  return MP_OK;
+}
+
+mp_status mp_overlap_pairs(mp_ctx* ctx, int32_t E, const int32_t* lo, const int32_t* hi,
+                           const uint64_t* size, const uint8_t* pinned, int32_t* pairs,
+                           int64_t cap, int64_t* count) {
+  return pair_sweep_h(ctx, 0, E, lo, hi, size, pinned, nullptr, pairs, cap, count);
+}
+
+mp_status mp_overlap_pairs_d(mp_ctx* ctx, int32_t E, const int32_t* d_lo, const int32_t* d_hi,
+                             const uint64_t* d_size, const uint8_t* d_pinned, int64_t row_begin,
+                             int64_t row_end, int64_t* d_row_off, int32_t* d_pairs, int64_t cap,
+                             int64_t* count, void* stream) {
+  if (!ctx || !count || !d_row_off || E < 0 || (E > 0 && (!d_lo || !d_hi || !d_size)))
+    return invalid_arg("null argument");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  PairArgs a;
+  a.num_edges = E;
+  a.lo = d_lo;
+  a.hi = d_hi;
+  a.size = d_size;
+  a.mask = d_pinned;
+  a.mode = 0;
+  a.row_begin = row_begin;
+  a.row_end = row_end;
+  return pair_sweep_d(ctx, a, d_row_off, d_pairs, cap, count, st);
+}
+
+mp_status mp_validate_pairs(mp_ctx* ctx, int32_t E, const int32_t* lo, const int32_t* hi,
+                            const uint64_t* size, const uint8_t* has_addr, const uint64_t* addr,
+                            int32_t* viol, int64_t cap, int64_t* num_viol) {
+  return pair_sweep_h(ctx, 1, E, lo, hi, size, has_addr, addr, viol, cap, num_viol);
+}
+
+mp_status mp_validate_pairs_d(mp_ctx* ctx, int32_t E, const int32_t* d_lo, const int32_t* d_hi,
+                              const uint64_t* d_size, const uint8_t* d_has, const uint64_t* d_addr,
+                              int64_t row_begin, int64_t row_end, int64_t* d_row_off,
+                              int32_t* d_viol, int64_t cap, int64_t* num_viol, void* stream) {
+  if (!ctx || !num_viol || !d_row_off || E < 0 ||
+      (E > 0 && (!d_lo || !d_hi || !d_size || !d_has || !d_addr)))
+    return invalid_arg("null argument");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  PairArgs a;
+  a.num_edges = E;
+  a.lo = d_lo;
+  a.hi = d_hi;
+  a.size = d_size;
+  a.mask = d_has;
+  a.addr = d_addr;
+  a.mode = 1;
+  a.row_begin = row_begin;
+  a.row_end = row_end;
+  return pair_sweep_d(ctx, a, d_row_off, d_viol, cap, num_viol, st);
+}
+
+mp_status mp_addresses_feasible(mp_ctx* ctx, int32_t E, const int32_t* lo, const int32_t* hi,
+                                const uint64_t* size, const uint8_t* has_addr,
+                                const uint64_t* addr, int32_t* feasible) {
+  if (!feasible) return invalid_arg("feasible is null");
+  int64_t cnt = 0;
+  MP_TRY(pair_sweep_h(ctx, 1, E, lo, hi, size, has_addr, addr, nullptr, 0, &cnt));
+  *feasible = cnt == 0 ? 1 : 0;
+  return MP_OK;
+}
+
+mp_status mp_peak_mem(mp_ctx* ctx, int32_t E, const uint64_t* size, const uint8_t* has_addr,
+                      const uint64_t* addr, uint64_t* peak_mem) {
+  if (!ctx || !peak_mem || E < 0 || (E > 0 && (!size || !has_addr || !addr)))
+    return invalid_arg("null argument");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const size_t e = (size_t)E;
+  MP_TRY(ctx->scratch[0].reserve(Carver::size_of({8 * e, e, 8 * e, 8})));
+  Carver cv(ctx->scratch[0].ptr);
+  uint64_t* d_size = cv.take<uint64_t>(e);
+  uint8_t* d_has = cv.take<uint8_t>(e);
+  uint64_t* d_addr = cv.take<uint64_t>(e);
+  uint64_t* d_out = cv.take<uint64_t>(1);
+  if (e) {
+    MP_CUDA(cudaMemcpyAsync(d_size, size, 8 * e, cudaMemcpyHostToDevice, st));
+    MP_CUDA(cudaMemcpyAsync(d_has, has_addr, e, cudaMemcpyHostToDevice, st));
+    MP_CUDA(cudaMemcpyAsync(d_addr, addr, 8 * e, cudaMemcpyHostToDevice, st));
+  }
+  MP_TRY(launch_peak_mem(E, d_size, d_has, d_addr, d_out, st));
+  MP_CUDA(cudaMemcpyAsync(peak_mem, d_out, 8, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaStreamSynchronize(st));
+  return MP_OK;
+}
+
+double mp_fragmentation(uint64_t mr, uint64_t rs) {
+  // placement.cpp:64-67, the same expression on the host (one FP divide).
+  if (mr == 0) return 0.0;
+  return static_cast<double>(mr - rs) / static_cast<double>(mr);
+}
+
+}  // extern "C"

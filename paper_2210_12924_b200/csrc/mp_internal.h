@@ -1,0 +1,148 @@
+// Internal types shared by the memplan_b200 CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "memplan_b200.h"
+
+namespace mpb {
+
+// Thread-local error text behind mp_last_error().
+void set_error(const std::string& msg);
+
+// Returns MP_E_CUDA / MP_E_OOM with a message when `e` is an error.
+mp_status cuda_status(cudaError_t e, const char* what);
+
+#define MP_CUDA(expr)                                             \
+  do {                                                            \
+    cudaError_t _e = (expr);                                      \
+    if (_e != cudaSuccess) return ::mpb::cuda_status(_e, #expr);  \
+  } while (0)
+
+#define MP_TRY(expr)                    \
+  do {                                  \
+    mp_status _s = (expr);              \
+    if (_s != MP_OK) return _s;         \
+  } while (0)
+
+// Growable device scratch owned by a context (never shrinks).
+struct Scratch {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  mp_status reserve(size_t want);
+  ~Scratch();
+};
+
+}  // namespace mpb
+
+struct mp_ctx {
+  int device = 0;
+  int num_sms = 0;
+  size_t max_smem_optin = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;  // own_stream unless mp_ctx_set_stream
+  mpb::Scratch scratch[4];        // independent scratch slots per call site
+  mpb::Scratch host_pinned_dummy;
+  // small device buffer for per-call flags / counters
+  int64_t* d_small = nullptr;
+};
+
+// Device-resident graph tables. Built once by mp_graph_upload from the
+// reference-shaped CSR (memplan::Graph flattened).
+//
+// Scoring layout:
+//   pred_off/preds   distinct producer nodes of every node (validity:
+//                    graph.cpp:239-254 over data and control edges)
+//   node_alloc       bytes a node allocates at its own timestep (sum of its
+//                    data fanout sizes; schedule.cpp:37 lo = pos[src])
+//   node_sfree       bytes freed after a node's timestep by data edges whose
+//                    ONLY consumer is that node (hi = pos[sink])
+//   multi_*          data edges with >= 2 consumers: their last consumer
+//                    (hi = max pos[sink], schedule.cpp:46) depends on the order
+struct mp_graph {
+  mp_ctx* ctx = nullptr;
+  int32_t n = 0;
+  int32_t E = 0;
+  int64_t S = 0;
+  int64_t D = 0;       // pred pairs
+  int32_t M = 0;       // multi-consumer data edges
+  int64_t MS = 0;      // their total sinks
+  uint64_t total_bytes = 0;
+
+  // raw CSR (edge space)
+  int32_t* d_edge_src = nullptr;
+  int64_t* d_sink_off = nullptr;
+  int32_t* d_sinks = nullptr;
+  uint64_t* d_edge_size = nullptr;
+
+  // node space, derived
+  int32_t* d_pred_off = nullptr;   // [n+1]
+  int32_t* d_preds = nullptr;      // [D]
+  uint64_t* d_node_alloc = nullptr;  // [n]
+  uint64_t* d_node_sfree = nullptr;  // [n]
+  int32_t* d_multi_off = nullptr;  // [M+1] into d_multi_sinks
+  int32_t* d_multi_sinks = nullptr;  // [MS]
+  uint64_t* d_multi_size = nullptr;  // [M]
+
+  // first node that misses a timestep in realized_lifetimes is searched on
+  // the host in reference order; keep the CSR on the host too.
+  std::vector<int32_t> h_edge_src;
+  std::vector<int64_t> h_sink_off;
+  std::vector<int32_t> h_sinks;
+  std::vector<uint64_t> h_edge_size;
+
+  bool smem_resident = false;
+  size_t score_smem_bytes = 0;
+};
+
+namespace mpb {
+
+// Kernel launchers (k_*.cu). All stream-ordered, no synchronisation.
+mp_status launch_score(const mp_graph* g, const int32_t* d_orders, int64_t num_orders,
+                       uint64_t* d_peak, int32_t* d_peak_step, uint8_t* d_valid,
+                       uint64_t* d_bytes /* [C][n] or null */,
+                       uint64_t* d_key /* fused argmin key or null */, int64_t index_base,
+                       cudaStream_t st);
+size_t score_scratch_bytes(const mp_graph* g, int64_t num_orders);
+mp_status score_configure(mp_graph* g);
+
+mp_status launch_lifetimes(const mp_graph* g, const int32_t* d_order, int64_t order_len,
+                           int32_t* d_lo, int32_t* d_hi, int32_t* d_valid, int32_t* d_pos_scratch,
+                           cudaStream_t st);
+mp_status launch_realized(const mp_graph* g, const int32_t* d_timestep_of, int32_t horizon,
+                          int32_t* d_lo, int32_t* d_hi, int32_t* d_missing, cudaStream_t st);
+mp_status launch_timeline(int32_t num_edges, const int32_t* d_lo, const int32_t* d_hi,
+                          const uint64_t* d_size, int32_t horizon, uint64_t* d_bytes,
+                          uint64_t* d_peak_rs, int32_t* d_peak_step, int64_t* d_diff_scratch,
+                          cudaStream_t st);
+// out3 = {best index + base or -1, best peak, packed key or UINT64_MAX}
+mp_status launch_argmin(const uint64_t* d_peak, const uint8_t* d_valid, int64_t num_orders,
+                        int64_t index_base, uint64_t* d_out3, cudaStream_t st);
+
+// Pairwise sweeps. mode 0 = overlap pairs (a6), mode 1 = address conflicts (a11).
+struct PairArgs {
+  int32_t num_edges = 0;
+  const int32_t* lo = nullptr;
+  const int32_t* hi = nullptr;
+  const uint64_t* size = nullptr;
+  const uint8_t* mask = nullptr;   // pinned (mode 0) / has_addr (mode 1)
+  const uint64_t* addr = nullptr;  // mode 1
+  int mode = 0;
+  int64_t row_begin = 0;
+  int64_t row_end = 0;
+};
+size_t pairs_scratch_bytes(const PairArgs& a, int num_sms);
+// Count pass + scan: d_row_off[rows+1]; total copied to *h_total (sync).
+mp_status pairs_count(const PairArgs& a, int num_sms, void* d_scratch, int64_t* d_row_off,
+                      int64_t* h_total, cudaStream_t st);
+// Fill pass using d_row_off from pairs_count.
+mp_status pairs_fill(const PairArgs& a, int num_sms, void* d_scratch, const int64_t* d_row_off,
+                     int32_t* d_pairs, cudaStream_t st);
+mp_status launch_peak_mem(int32_t num_edges, const uint64_t* d_size, const uint8_t* d_has,
+                          const uint64_t* d_addr, uint64_t* d_out, cudaStream_t st);
+
+}  // namespace mpb

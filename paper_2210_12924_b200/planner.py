@@ -1,0 +1,512 @@
+"""The reference planner's hot-path API, executed by the sm_100a library.
+
+Each method keeps the reference function's name, argument meaning and error
+behaviour (raising the same exception class with the same message text) and
+cites the file:line it replaces. Host work here is limited to argument
+marshalling and report assembly; every data-parallel computation runs in
+``lib/libmemplan_b200.so`` through the C ABI (include/memplan_b200.h). There is
+no CPU fallback: without an sm_100 device the constructor raises DeviceError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from dataclasses import dataclass, field
+from typing import Mapping, Sequence
+
+import numpy as np
+
+from . import _native, errors
+from .graph import Graph
+
+_vp = C.c_void_p
+
+
+@dataclass
+class Interval:
+    """memplan::Interval (analysis.hpp:28-33): closed, 1-based, empty if lo > hi."""
+    lo: int = 1
+    hi: int = 0
+
+    def empty(self) -> bool:
+        return self.lo > self.hi
+
+    def contains(self, t: int) -> bool:
+        return self.lo <= t <= self.hi
+
+
+def intervals_disjoint(a: Interval, b: Interval) -> bool:
+    """analysis.hpp:35-37."""
+    return a.empty() or b.empty() or a.hi < b.lo or b.hi < a.lo
+
+
+@dataclass
+class ResidentTimeline:
+    """memplan::ResidentTimeline (plan.hpp:43-48) without the per-step id lists."""
+    bytes: np.ndarray
+    peak_rs: int
+    peak_step: int
+
+
+@dataclass
+class ScoreResult:
+    peak: np.ndarray       # uint64[C]; 0 for invalid candidates
+    peak_step: np.ndarray  # int32[C]; 0 for invalid candidates
+    valid: np.ndarray      # uint8[C]
+
+    def argmin(self) -> int:
+        """First minimum over valid candidates (-1 if none)."""
+        idx = np.flatnonzero(self.valid)
+        if idx.size == 0:
+            return -1
+        return int(idx[np.argmin(self.peak[idx], kind="stable")])
+
+
+@dataclass
+class ExecutionSequence:
+    steps: list = field(default_factory=list)
+    timestep_of: dict = field(default_factory=dict)
+
+
+@dataclass
+class MemoryPlan:
+    """memplan::MemoryPlan (plan.hpp:76-82); provenance kept as a dict."""
+    sequence: ExecutionSequence = field(default_factory=ExecutionSequence)
+    addresses: dict = field(default_factory=dict)
+    peak_mem: int = 0
+    timeline_bytes: list = field(default_factory=list)
+    peak_rs: int = 0
+    peak_step: int = 0
+    provenance: dict = field(default_factory=dict)
+
+
+def load_plan(text: str) -> MemoryPlan:
+    """Reads the canonical plan file (plan.cpp:233-305; strictness reduced to
+    the fields validate_plan consumes)."""
+    try:
+        doc = json.loads(text)
+    except json.JSONDecodeError as e:
+        raise errors.ParseError(f"plan file: {e}") from None
+    for key in ("sequence", "timesteps", "addresses", "peak_mem", "timeline", "provenance"):
+        if key not in doc:
+            raise errors.ParseError(f"plan file is missing field '{key}'")
+    plan = MemoryPlan()
+    plan.sequence.steps = list(doc["sequence"])
+    plan.sequence.timestep_of = {k: int(v) for k, v in doc["timesteps"].items()}
+    plan.addresses = {k: int(v) for k, v in doc["addresses"].items()}
+    plan.peak_mem = int(doc["peak_mem"])
+    plan.timeline_bytes = [int(b) for b in doc["timeline"]["bytes"]]
+    plan.peak_rs = int(doc["timeline"]["peak_rs"])
+    plan.peak_step = int(doc["timeline"]["peak_step"])
+    plan.provenance = dict(doc["provenance"])
+    return plan
+
+
+def fragmentation(mr: int, rs: int) -> float:
+    """placement.cpp:64-67 (the native library evaluates the same expression)."""
+    return float(_native.lib().mp_fragmentation(int(mr), int(rs)))
+
+
+class DeviceGraph:
+    """A graph uploaded to one context (mp_graph_upload)."""
+
+    def __init__(self, planner: "Planner", graph: Graph):
+        self.planner = planner
+        self.graph = graph
+        self._csr = graph.mp_csr()
+        h = _vp()
+        _native.check(_native.lib().mp_graph_upload(planner.ctx, C.byref(self._csr), C.byref(h)))
+        self.handle = h
+
+    def info(self) -> dict:
+        info = _native.MpGraphInfo()
+        _native.check(_native.lib().mp_graph_get_info(self.handle, C.byref(info)))
+        return {k: getattr(info, k) for k, _ in info._fields_}
+
+    def free(self):
+        if self.handle:
+            _native.lib().mp_graph_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, np.int32)
+
+
+class Planner:
+    """One device context (mp_ctx) plus the graphs uploaded to it."""
+
+    def __init__(self, device: int = 0):
+        L = _native.lib()
+        h = _vp()
+        _native.check(L.mp_ctx_create(device, C.byref(h)))
+        self.ctx = h
+        self.device = device
+        self._graphs: dict[int, DeviceGraph] = {}
+
+    def close(self):
+        for dg in self._graphs.values():
+            dg.free()
+        self._graphs.clear()
+        if self.ctx:
+            _native.lib().mp_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_ptr: int | None):
+        _native.check(_native.lib().mp_ctx_set_stream(self.ctx, stream_ptr))
+
+    def upload(self, graph: Graph) -> DeviceGraph:
+        dg = self._graphs.get(id(graph))
+        if dg is None or dg.graph is not graph:
+            dg = DeviceGraph(self, graph)
+            self._graphs[id(graph)] = dg
+        return dg
+
+    # ---- (a2/a3) ------------------------------------------------------------
+    def lifetimes_from_order(self, graph: Graph, order: Sequence[int]):
+        """schedule.cpp:33-50 -> (lo, hi) int32 arrays; InvalidOrder if not topological."""
+        dg = self.upload(graph)
+        o = _i32(order)
+        lo = np.zeros(max(graph.E, 1), np.int32)
+        hi = np.zeros(max(graph.E, 1), np.int32)
+        _native.check(_native.lib().mp_lifetimes(self.ctx, dg.handle, o.ctypes.data, o.size,
+                                                 lo.ctypes.data, hi.ctypes.data))
+        return lo[:graph.E], hi[:graph.E]
+
+    def positions_of(self, graph: Graph, order: Sequence[int]) -> np.ndarray:
+        """schedule.cpp:23-31: the device validates the order, pos is its inverse."""
+        self.lifetimes_from_order(graph, order)
+        pos = np.zeros(graph.n, np.int32)
+        pos[_i32(order)] = np.arange(1, graph.n + 1, dtype=np.int32)
+        return pos
+
+    # ---- (a4) ---------------------------------------------------------------
+    def realized_lifetimes(self, graph: Graph, timestep_of, horizon: int):
+        """plan.cpp:101-120. timestep_of: {node id: step} or int32[n] (0 = absent)."""
+        dg = self.upload(graph)
+        if isinstance(timestep_of, Mapping):
+            ts = np.zeros(graph.n, np.int32)
+            for k, v in timestep_of.items():
+                if graph.has_node(k):
+                    ts[graph.node_index(k)] = v
+        else:
+            ts = _i32(timestep_of)
+        lo = np.zeros(max(graph.E, 1), np.int32)
+        hi = np.zeros(max(graph.E, 1), np.int32)
+        miss = C.c_int32(-1)
+        st = _native.lib().mp_realized_lifetimes(self.ctx, dg.handle, ts.ctypes.data, int(horizon),
+                                                 lo.ctypes.data, hi.ctypes.data, C.byref(miss))
+        if st == _native.MP_E_INVALID_ORDER:
+            raise errors.InvalidOrder(f"node {graph.node_ids[miss.value]} has no timestep")
+        _native.check(st)
+        return lo[:graph.E], hi[:graph.E]
+
+    # ---- (a8/a9/a10) --------------------------------------------------------
+    def resident_bytes_per_step(self, graph: Graph, order) -> np.ndarray:
+        """schedule.cpp:69-79."""
+        dg = self.upload(graph)
+        o = _i32(order)
+        out = np.zeros(max(graph.n, 1), np.uint64)
+        _native.check(_native.lib().mp_resident_bytes(self.ctx, dg.handle, o.ctypes.data, o.size,
+                                                      out.ctypes.data))
+        return out[:graph.n]
+
+    def peak_resident_bytes(self, graph: Graph, order) -> int:
+        """schedule.cpp:81-88."""
+        dg = self.upload(graph)
+        o = _i32(order)
+        p = C.c_uint64()
+        _native.check(_native.lib().mp_peak_resident_bytes(self.ctx, dg.handle, o.ctypes.data,
+                                                           o.size, C.byref(p)))
+        return int(p.value)
+
+    def timeline_from_lifetimes(self, graph: Graph, lo, hi, horizon: int) -> ResidentTimeline:
+        """plan.cpp:122-143 (bytes, peak_rs, peak_step)."""
+        dg = self.upload(graph)
+        lo, hi = _i32(lo), _i32(hi)
+        b = np.zeros(max(horizon, 1), np.uint64)
+        pr, ps = C.c_uint64(), C.c_int32()
+        _native.check(_native.lib().mp_timeline(self.ctx, dg.handle, lo.ctypes.data, hi.ctypes.data,
+                                                int(horizon), b.ctypes.data, C.byref(pr),
+                                                C.byref(ps)))
+        return ResidentTimeline(b[:horizon], int(pr.value), int(ps.value))
+
+    # ---- batched scoring ------------------------------------------------------
+    def score_orders(self, graph: Graph, orders) -> ScoreResult:
+        """peak_resident_bytes over many candidate orders at once (+ verdicts)."""
+        dg = self.upload(graph)
+        o = _i32(orders)
+        if o.ndim == 1:
+            o = o.reshape(1, -1)
+        c = o.shape[0]
+        if o.shape[1] != graph.n:
+            # every candidate of the wrong length is invalid (graph.cpp:241)
+            return ScoreResult(np.zeros(c, np.uint64), np.zeros(c, np.int32), np.zeros(c, np.uint8))
+        peak = np.zeros(max(c, 1), np.uint64)
+        step = np.zeros(max(c, 1), np.int32)
+        valid = np.zeros(max(c, 1), np.uint8)
+        _native.check(_native.lib().mp_score_orders(self.ctx, dg.handle, o.ctypes.data, c,
+                                                    peak.ctypes.data, step.ctypes.data,
+                                                    valid.ctypes.data))
+        return ScoreResult(peak[:c], step[:c], valid[:c])
+
+    def score_orders_best(self, graph: Graph, orders) -> tuple[ScoreResult, int]:
+        """Scoring with the first-minimum argmin fused into the kernel."""
+        dg = self.upload(graph)
+        o = _i32(orders)
+        if o.ndim == 1:
+            o = o.reshape(1, -1)
+        c = o.shape[0]
+        if o.shape[1] != graph.n:
+            return ScoreResult(np.zeros(c, np.uint64), np.zeros(c, np.int32),
+                               np.zeros(c, np.uint8)), -1
+        peak = np.zeros(max(c, 1), np.uint64)
+        step = np.zeros(max(c, 1), np.int32)
+        valid = np.zeros(max(c, 1), np.uint8)
+        best = C.c_int64()
+        _native.check(_native.lib().mp_score_orders_best(self.ctx, dg.handle, o.ctypes.data, c,
+                                                         peak.ctypes.data, step.ctypes.data,
+                                                         valid.ctypes.data, C.byref(best)))
+        return ScoreResult(peak[:c], step[:c], valid[:c]), int(best.value)
+
+    def score_orders_into(self, dg: DeviceGraph, orders_host, peak, step, valid) -> int:
+        """Public host-buffer call for pre-allocated (e.g. pinned) buffers: H2D of the
+        orders, one fused scoring+argmin kernel, D2H of peak/step/valid; returns best."""
+        best = C.c_int64()
+        _native.check(_native.lib().mp_score_orders_best(
+            self.ctx, dg.handle, _native.ptr(orders_host), int(orders_host.shape[0]),
+            _native.ptr(peak), _native.ptr(step), _native.ptr(valid), C.byref(best)))
+        return int(best.value)
+
+    def argmin(self, peak, valid) -> int:
+        p = np.ascontiguousarray(peak, np.uint64)
+        v = np.ascontiguousarray(valid, np.uint8)
+        best = C.c_int64()
+        _native.check(_native.lib().mp_argmin(self.ctx, p.ctypes.data, v.ctypes.data, p.size,
+                                              C.byref(best)))
+        return int(best.value)
+
+    def score_orders_d(self, dg: DeviceGraph, d_orders, num_orders, d_peak, d_step, d_valid,
+                       stream: int | None = None):
+        """Device-pointer variant (torch tensors or raw pointers), stream-ordered."""
+        _native.check(_native.lib().mp_score_orders_d(
+            self.ctx, dg.handle, _native.ptr(d_orders), int(num_orders), _native.ptr(d_peak),
+            _native.ptr(d_step), _native.ptr(d_valid), stream))
+
+    def score_orders_argmin_d(self, dg: DeviceGraph, d_orders, num_orders, d_peak, d_step,
+                              d_valid, d_best_key, index_base=0, stream: int | None = None):
+        _native.check(_native.lib().mp_score_orders_argmin_d(
+            self.ctx, dg.handle, _native.ptr(d_orders), int(num_orders), _native.ptr(d_peak),
+            _native.ptr(d_step), _native.ptr(d_valid), _native.ptr(d_best_key), int(index_base),
+            stream))
+
+    def argmin_key_d(self, d_peak, d_valid, num_orders, index_base, d_out3,
+                     stream: int | None = None):
+        _native.check(_native.lib().mp_argmin_key_d(
+            self.ctx, _native.ptr(d_peak), _native.ptr(d_valid), int(num_orders),
+            int(index_base), _native.ptr(d_out3), stream))
+
+    # ---- (a6) overlap pairs -----------------------------------------------------
+    def encode_address_pairs(self, graph: Graph, lo, hi, preplaced: Mapping[int, int] | None = None,
+                             want_pairs: bool = True):
+        """Pair set of encode_addresses (encode.cpp:347-367) in emission order.
+
+        ``preplaced`` maps edge index -> offset; pairs of two preplaced edges are
+        skipped (:351). Returns int32[P, 2] (or the count with want_pairs=False);
+        the count equals constraint_counts["live_pair"].
+        """
+        lo, hi = _i32(lo), _i32(hi)
+        pin = None
+        if preplaced:
+            pin = np.zeros(graph.E, np.uint8)
+            pin[list(preplaced.keys())] = 1
+        return self.overlap_pairs(lo, hi, graph.edge_size, pin, want_pairs)
+
+    def overlap_pairs(self, lo, hi, size, pinned=None, want_pairs: bool = True):
+        lo, hi = _i32(lo), _i32(hi)
+        size = np.ascontiguousarray(size, np.uint64)
+        pin = None if pinned is None else np.ascontiguousarray(pinned, np.uint8)
+        E = lo.size
+        cnt = C.c_int64()
+        L = _native.lib()
+        _native.check(L.mp_overlap_pairs(self.ctx, E, lo.ctypes.data, hi.ctypes.data,
+                                         size.ctypes.data, _native.ptr(pin), None, 0,
+                                         C.byref(cnt)))
+        if not want_pairs:
+            return cnt.value
+        out = np.zeros((max(cnt.value, 1), 2), np.int32)
+        _native.check(L.mp_overlap_pairs(self.ctx, E, lo.ctypes.data, hi.ctypes.data,
+                                         size.ctypes.data, _native.ptr(pin), out.ctypes.data,
+                                         cnt.value, C.byref(cnt)))
+        return out[:cnt.value]
+
+    def overlap_pairs_d(self, num_edges, d_lo, d_hi, d_size, d_pinned, row_begin, row_end,
+                        d_row_off, d_pairs, cap, stream: int | None = None) -> int:
+        cnt = C.c_int64()
+        _native.check(_native.lib().mp_overlap_pairs_d(
+            self.ctx, int(num_edges), _native.ptr(d_lo), _native.ptr(d_hi), _native.ptr(d_size),
+            _native.ptr(d_pinned), int(row_begin), int(row_end), _native.ptr(d_row_off),
+            _native.ptr(d_pairs), int(cap), C.byref(cnt), stream))
+        return cnt.value
+
+    # ---- (a11/a12/a13) validation -----------------------------------------------
+    def conflicting_pairs(self, lo, hi, size, has_addr, addr) -> np.ndarray:
+        """Pairwise part of validate_plan (plan.cpp:390-404), in (i, j) order."""
+        lo, hi = _i32(lo), _i32(hi)
+        size = np.ascontiguousarray(size, np.uint64)
+        has = np.ascontiguousarray(has_addr, np.uint8)
+        ad = np.ascontiguousarray(addr, np.uint64)
+        E = lo.size
+        cnt = C.c_int64()
+        L = _native.lib()
+        _native.check(L.mp_validate_pairs(self.ctx, E, lo.ctypes.data, hi.ctypes.data,
+                                          size.ctypes.data, has.ctypes.data, ad.ctypes.data, None,
+                                          0, C.byref(cnt)))
+        out = np.zeros((max(cnt.value, 1), 2), np.int32)
+        if cnt.value:
+            _native.check(L.mp_validate_pairs(self.ctx, E, lo.ctypes.data, hi.ctypes.data,
+                                              size.ctypes.data, has.ctypes.data, ad.ctypes.data,
+                                              out.ctypes.data, cnt.value, C.byref(cnt)))
+        return out[:cnt.value]
+
+    def validate_pairs_d(self, num_edges, d_lo, d_hi, d_size, d_has, d_addr, row_begin, row_end,
+                         d_row_off, d_viol, cap, stream: int | None = None) -> int:
+        cnt = C.c_int64()
+        _native.check(_native.lib().mp_validate_pairs_d(
+            self.ctx, int(num_edges), _native.ptr(d_lo), _native.ptr(d_hi), _native.ptr(d_size),
+            _native.ptr(d_has), _native.ptr(d_addr), int(row_begin), int(row_end),
+            _native.ptr(d_row_off), _native.ptr(d_viol), int(cap), C.byref(cnt), stream))
+        return cnt.value
+
+    def addresses_feasible(self, graph: Graph, lo, hi, addresses: Mapping[int, int]) -> bool:
+        """pipeline.cpp:146-160 (addresses keyed by edge index)."""
+        has, ad = self._addr_arrays(graph, addresses)
+        f = C.c_int32()
+        lo, hi = _i32(lo), _i32(hi)
+        _native.check(_native.lib().mp_addresses_feasible(
+            self.ctx, graph.E, lo.ctypes.data, hi.ctypes.data, graph.edge_size.ctypes.data,
+            has.ctypes.data, ad.ctypes.data, C.byref(f)))
+        return bool(f.value)
+
+    def peak_mem(self, graph: Graph, addresses: Mapping[int, int]) -> int:
+        """max(addr + size) over placed edges (pipeline.cpp:270-275)."""
+        has, ad = self._addr_arrays(graph, addresses)
+        out = C.c_uint64()
+        _native.check(_native.lib().mp_peak_mem(self.ctx, graph.E, graph.edge_size.ctypes.data,
+                                                has.ctypes.data, ad.ctypes.data, C.byref(out)))
+        return int(out.value)
+
+    @staticmethod
+    def _addr_arrays(graph: Graph, addresses: Mapping[int, int]):
+        has = np.zeros(max(graph.E, 1), np.uint8)
+        ad = np.zeros(max(graph.E, 1), np.uint64)
+        for e, a in addresses.items():
+            has[e] = 1
+            ad[e] = a
+        return has, ad
+
+    def validate_plan(self, plan: MemoryPlan, graph: Graph) -> list[tuple[str, str]]:
+        """validate_plan (plan.cpp:315-419): the same violations in the same order.
+
+        Coverage / ordering / address-bound bookkeeping is host-side report
+        assembly over ids; realized lifetimes, the O(E^2) pairwise check and
+        the peak resident bytes run on the device.
+        """
+        out: list[tuple[str, str]] = []
+        fail = lambda tag, detail: out.append((tag, detail))  # noqa: E731
+        seen: dict[str, int] = {}
+        for sid in plan.sequence.steps:
+            if not graph.has_node(sid):
+                fail("create_once", f"sequence names unknown node '{sid}'")
+                continue
+            seen[sid] = seen.get(sid, 0) + 1
+            if seen[sid] == 2:
+                fail("create_once", f"node '{sid}' appears more than once")
+        for nid in graph.node_ids:
+            if nid not in seen:
+                fail("create_once", f"node '{nid}' is missing from the sequence")
+        horizon = graph.n
+        ts = plan.sequence.timestep_of
+        step_of = lambda k: ts.get(k, 0)  # noqa: E731
+        for sid in plan.sequence.steps:
+            t = step_of(sid)
+            if t <= 0:
+                fail("create_once", f"node '{sid}' has no timestep")
+            else:
+                horizon = max(horizon, t)
+        order_ok = True
+        node_ids = graph.node_ids
+        for e in range(graph.E):
+            src_id = node_ids[graph.source_of(e)]
+            t_src = step_of(src_id)
+            for w in graph.sinks_of(e):
+                t_sink = step_of(node_ids[w])
+                if t_src <= 0 or t_sink <= 0:
+                    continue
+                if t_sink <= t_src:
+                    fail("fanin_in_memory", f"edge '{graph.edge_ids[e]}': consumer '{node_ids[w]}'"
+                         f" does not run after producer '{src_id}'")
+                    order_ok = False
+        mask64 = (1 << 64) - 1
+        for aid in sorted(plan.addresses):
+            addr = plan.addresses[aid]
+            if not graph.has_edge(aid):
+                fail("peak_address", f"address for unknown tensor '{aid}'")
+                continue
+            end = (addr + int(graph.edge_size[graph.edge_index(aid)])) & mask64
+            if end > plan.peak_mem:
+                fail("peak_address", f"tensor '{aid}' ends at {end}, above peak_mem {plan.peak_mem}")
+        for e in range(graph.E):
+            if graph.edge_size[e] > 0 and graph.edge_ids[e] not in plan.addresses:
+                fail("peak_address", f"tensor '{graph.edge_ids[e]}' has no address")
+        if not order_ok:
+            return out
+        for nid in node_ids:
+            if step_of(nid) <= 0:
+                return out
+        lo, hi = self.realized_lifetimes(graph, ts, horizon)
+        has = np.zeros(max(graph.E, 1), np.uint8)
+        ad = np.zeros(max(graph.E, 1), np.uint64)
+        for e, eid in enumerate(graph.edge_ids):
+            if eid in plan.addresses:
+                has[e] = 1
+                ad[e] = plan.addresses[eid] & mask64
+        for i, j in self.conflicting_pairs(lo, hi, graph.edge_size, has[:graph.E],
+                                           ad[:graph.E]).tolist():
+            fail("below_above", f"tensors '{graph.edge_ids[i]}' and '{graph.edge_ids[j]}' are "
+                 "live together and overlap in memory")
+        peak_rs = self.timeline_from_lifetimes(graph, lo, hi, horizon).peak_rs
+        if plan.peak_mem < peak_rs:
+            fail("peak_mem", f"peak_mem {plan.peak_mem} is below the peak resident bytes {peak_rs}")
+        if plan.peak_rs != peak_rs:
+            fail("peak_mem", f"stored peak_rs {plan.peak_rs} differs from the recomputed {peak_rs}")
+        return out
+
+
+def format_report(violations: list[tuple[str, str]]) -> str:
+    """plan.cpp:421-427."""
+    if not violations:
+        return "ok\n"
+    return "".join(f"{tag}  {detail}\n" for tag, detail in violations)
+
+
+def random_topo_orders(graph: Graph, num_orders: int, seed: int = 0,
+                       threads: int = 0) -> np.ndarray:
+    """Seeded random topological orders (host C++ workload helper)."""
+    out = np.zeros((max(num_orders, 1), max(graph.n, 1)), np.int32)
+    csr = graph.mp_csr()
+    _native.check(_native.lib().mp_random_topo_orders(C.byref(csr), int(num_orders), int(seed),
+                                                      int(threads), out.ctypes.data))
+    return out[:num_orders, :graph.n]

@@ -1,0 +1,341 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's own
+outputs (tests/golden/golden.json) and the C restatement (oracle/), bit-exact.
+
+Every test here is @pytest.mark.gpu and runs on a B200 (`pytest -m gpu`).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2210_12924_b200 as mp
+from paper_2210_12924_b200 import errors
+
+pytestmark = pytest.mark.gpu
+
+
+def _graph(rec):
+    return mp.load_graph(rec["graph_json"])
+
+
+# ---- golden vectors from the reference --------------------------------------------
+def test_golden_orders(golden, planner):
+    checked = 0
+    for rec in golden["graphs"]:
+        g = _graph(rec)
+        for case in rec["orders"]:
+            order = case["order"]
+            if "error" in case:
+                with pytest.raises(errors.InvalidOrder) as ei:
+                    planner.lifetimes_from_order(g, order)
+                assert str(ei.value) == case["error"]
+                with pytest.raises(errors.InvalidOrder):
+                    planner.peak_resident_bytes(g, order)
+                with pytest.raises(errors.InvalidOrder):
+                    planner.resident_bytes_per_step(g, order)
+                continue
+            lo, hi = planner.lifetimes_from_order(g, order)
+            assert lo.tolist() == case["lo"] and hi.tolist() == case["hi"], rec["name"]
+            assert planner.resident_bytes_per_step(g, order).tolist() == case["bytes"]
+            assert planner.peak_resident_bytes(g, order) == case["peak"]
+            t = planner.timeline_from_lifetimes(g, lo, hi, g.n)
+            assert t.bytes.tolist() == case["timeline"]["bytes"]
+            assert (t.peak_rs, t.peak_step) == (case["timeline"]["peak_rs"],
+                                                case["timeline"]["peak_step"])
+            assert planner.encode_address_pairs(g, lo, hi).tolist() == case["pairs"], rec["name"]
+            checked += 1
+    assert checked >= 70
+
+
+def test_golden_batched_scoring(golden, planner):
+    for rec in golden["graphs"]:
+        g = _graph(rec)
+        rows = [c for c in rec["orders"] if len(c["order"]) == g.n]
+        if not rows:
+            continue
+        res = planner.score_orders(g, np.array([c["order"] for c in rows], np.int32))
+        for i, c in enumerate(rows):
+            if "error" in c:
+                assert res.valid[i] == 0 and res.peak[i] == 0 and res.peak_step[i] == 0
+            else:
+                assert res.valid[i] == 1
+                assert int(res.peak[i]) == c["peak"]
+                assert int(res.peak_step[i]) == c["timeline"]["peak_step"], rec["name"]
+
+
+def test_golden_pinned_pairs(golden, planner):
+    for rec in golden["graphs"]:
+        if "pinned" not in rec:
+            continue
+        g = _graph(rec)
+        lo, hi = planner.lifetimes_from_order(g, rec["orders"][0]["order"])
+        pin = {e: 0 for e, p in enumerate(rec["pinned"]["pinned"]) if p}
+        assert planner.encode_address_pairs(g, lo, hi, pin).tolist() == rec["pinned"]["pairs"]
+
+
+def test_golden_realized(golden, planner):
+    for rec in golden["graphs"]:
+        g = _graph(rec)
+        for case in rec.get("realized", []):
+            if "error" in case:
+                with pytest.raises(errors.InvalidOrder) as ei:
+                    planner.realized_lifetimes(g, case["timestep_of"], case["horizon"])
+                assert str(ei.value) == case["error"]
+            else:
+                lo, hi = planner.realized_lifetimes(g, case["timestep_of"], case["horizon"])
+                assert lo.tolist() == case["lo"] and hi.tolist() == case["hi"]
+
+
+def test_golden_validate_plan(golden, planner):
+    """Full validate_plan report (all tags, same order, same text) vs the reference."""
+    n_cases = 0
+    for rec in golden["graphs"]:
+        g = _graph(rec)
+        for pc in rec.get("plans", []):
+            plan = mp.MemoryPlan()
+            plan.sequence.steps = [g.node_ids[v] for v in pc["sequence"]]
+            plan.sequence.timestep_of = {g.node_ids[v]: t for v, t in enumerate(pc["timestep_of"])
+                                         if t != 0}
+            plan.addresses = {g.edge_ids[e]: a for e, (h, a) in
+                              enumerate(zip(pc["has_addr"], pc["addr"])) if h}
+            plan.peak_mem = pc["peak_mem"]
+            plan.peak_rs = pc["stored_peak_rs"]
+            got = planner.validate_plan(plan, g)
+            assert [list(v) for v in got] == pc["violations"], (rec["name"], pc["name"])
+            n_cases += 1
+    assert n_cases > 50
+
+
+def test_chain3_plan_file(golden, planner):
+    import json
+    plan = mp.load_plan(json.dumps(golden["plan_graph"]["chain3"]))
+    g = _graph([r for r in golden["graphs"] if r["name"] == "chain3"][0])
+    assert planner.validate_plan(plan, g) == []
+    assert mp.format_report([]) == "ok\n"
+    plan.addresses["e2"] = plan.addresses["e1"]           # test_plan.cpp:193-199
+    assert [t for t, _ in planner.validate_plan(plan, g)] == ["below_above"]
+    assert planner.peak_mem(g, {0: 0, 1: 4}) == 6
+    assert planner.addresses_feasible(g, [1, 2], [2, 3], {0: 0, 1: 4})
+    assert not planner.addresses_feasible(g, [1, 2], [2, 3], {0: 0, 1: 2})
+
+
+def _all_topo_orders_in_reference_dfs(g):
+    """Every topological order in enumerate_min_peak's DFS order (oracle.cpp:41-46, 74-93)."""
+    id_order = sorted(range(g.n), key=lambda v: g.node_ids[v])
+    preds = [set() for _ in range(g.n)]
+    for e in range(g.E):
+        for w in g.sinks_of(e):
+            preds[w].add(g.source_of(e))
+    out, prefix, done = [], [], [False] * g.n
+
+    def rec():
+        if len(prefix) == g.n:
+            out.append(list(prefix))
+            return
+        for v in id_order:
+            if done[v] or not all(done[u] for u in preds[v]):
+                continue
+            done[v] = True
+            prefix.append(v)
+            rec()
+            prefix.pop()
+            done[v] = False
+    rec()
+    return out
+
+
+def test_battery_argmin_matches_enumerate_min_peak(golden, planner):
+    """Batched scoring + first-minimum argmin reproduces enumerate_min_peak's
+    min_peak AND witness on >= 200 graphs (test_acceptance.cpp:69-88)."""
+    n = 0
+    for b in golden["battery"]:
+        if "spec" in b:
+            g = mp.generate_graph(*b["spec"])
+        else:
+            g = _graph([r for r in golden["graphs"] if r["name"] == b["fixture"]][0])
+        orders = np.array(_all_topo_orders_in_reference_dfs(g), np.int32)
+        res = planner.score_orders(g, orders)
+        assert res.valid.all()
+        best = planner.argmin(res.peak, res.valid)
+        assert best == res.argmin()
+        assert int(res.peak[best]) == b["min_peak"]
+        assert orders[best].tolist() == b["order"]
+        n += 1
+    assert n >= 200
+
+
+# ---- randomized parity against the C restatement / reference library ---------------
+CASES = [("fork_join", 40, 64, 3), ("fork_join", 400, 4096, 9), ("training_like", 60, 8, 0),
+         ("training_like", 700, 100, 0), ("chain", 300, 7, 0)]
+
+
+@pytest.mark.parametrize("kind,layers,size,seed", CASES)
+def test_random_orders_vs_oracle(planner, kind, layers, size, seed):
+    g = mp.generate_graph(kind, layers, size, seed)
+    orc = O.Oracle.from_csr(g.csr())
+    orders = mp.random_topo_orders(g, 48, seed=seed + 1)
+    rng = np.random.default_rng(seed)
+    bad = orders[:8].copy()
+    for i in range(8):                      # swaps / duplicates / out-of-range
+        a, b = rng.integers(0, g.n, 2)
+        if i % 3 == 0:
+            bad[i, [a, b]] = bad[i, [b, a]]
+        elif i % 3 == 1:
+            bad[i, a] = bad[i, b]
+        else:
+            bad[i, a] = g.n + a
+    allo = np.concatenate([orders, bad])
+    res = planner.score_orders(g, allo)
+    for i, o in enumerate(allo):
+        lt = orc.lifetimes_from_order(o)
+        if lt is None:
+            assert res.valid[i] == 0
+            continue
+        assert res.valid[i] == 1
+        b, pr, ps = orc.timeline_from_lifetimes(lt[0], lt[1], g.n)
+        assert (int(res.peak[i]), int(res.peak_step[i])) == (pr, ps)
+        if i < 4:
+            lo, hi = planner.lifetimes_from_order(g, o)
+            assert (lo == lt[0]).all() and (hi == lt[1]).all()
+            assert (planner.resident_bytes_per_step(g, o) == b).all()
+            pairs = planner.encode_address_pairs(g, lo, hi)
+            assert (pairs == O.overlap_pairs(lo, hi, g.edge_size)).all()
+
+
+def test_global_memory_path_large_graph(planner):
+    """n above the shared-memory budget (global-scratch variant of the scorer)."""
+    g = mp.generate_graph("training_like", 3000, 8)
+    dg = planner.upload(g)
+    assert dg.info()["smem_resident"] == 0
+    orc = O.Oracle.from_csr(g.csr())
+    orders = np.concatenate([g.program_order()[None, :], mp.random_topo_orders(g, 6, seed=2)])
+    res = planner.score_orders(g, orders)
+    for i, o in enumerate(orders):
+        lo, hi = orc.lifetimes_from_order(o)
+        _, pr, ps = orc.timeline_from_lifetimes(lo, hi, g.n)
+        assert res.valid[i] == 1 and (int(res.peak[i]), int(res.peak_step[i])) == (pr, ps)
+
+
+def test_c5_full_size(golden, planner):
+    """The 100k-tensor graph at full size: KAT peak + size-independent properties."""
+    g = mp.generate_graph("training_like", 33333, 8)
+    k = golden["kats"]["training_like_L33333"]
+    po = g.program_order()
+    assert planner.peak_resident_bytes(g, po) == k["program_peak"]
+    orders = mp.random_topo_orders(g, 3, seed=7)
+    res = planner.score_orders(g, np.concatenate([po[None, :], orders]))
+    assert res.valid.all() and int(res.peak[0]) == k["program_peak"]
+    orc = O.Oracle.from_csr(g.csr())
+    lo, hi = orc.lifetimes_from_order(orders[0])
+    glo, ghi = planner.lifetimes_from_order(g, orders[0])
+    assert (glo == lo).all() and (ghi == hi).all()
+    # resident bytes: sum over steps = sum of size * lifetime length (a checksum)
+    rs = planner.resident_bytes_per_step(g, orders[0])
+    assert int(rs.sum(dtype=np.uint64)) == int(
+        (g.edge_size * (hi - lo + 1).astype(np.uint64)).sum(dtype=np.uint64))
+    assert int(rs.max()) == int(res.peak[1]) and int(np.argmax(rs)) + 1 == int(res.peak_step[1])
+    # overlap pairs at full size: exact per-row counts and hashes on sampled rows
+    import torch
+    cnt = planner.encode_address_pairs(g, lo, hi, want_pairs=False)
+    total_c, _ = O.overlap_row_stats(lo, hi, g.edge_size)
+    assert cnt == int(total_c.sum())
+    d = torch.device("cuda:0")
+    dlo, dhi = torch.from_numpy(lo).to(d), torch.from_numpy(hi).to(d)
+    dsz = torch.from_numpy(g.edge_size.view(np.int64)).to(d)
+    for r in np.linspace(0, g.E - 1, 48).astype(np.int64).tolist():
+        c, h = O.overlap_row_stats(lo, hi, g.edge_size, rows=(r, r + 1))
+        off = torch.zeros(2, dtype=torch.int64, device=d)
+        k = planner.overlap_pairs_d(g.E, dlo, dhi, dsz, None, r, r + 1, off, None, 0)
+        assert k == int(c[0])
+        out = torch.zeros((max(k, 1), 2), dtype=torch.int32, device=d)
+        planner.overlap_pairs_d(g.E, dlo, dhi, dsz, None, r, r + 1, off, out, k)
+        js = out[:k, 1].cpu().numpy().astype(np.uint64)
+        hsh = np.uint64(1469598103934665603)
+        with np.errstate(over="ignore"):
+            for j in js:                                  # FNV-1a over the row's j list
+                hsh = (hsh ^ j) * np.uint64(1099511628211)
+        assert int(hsh) == int(h[0]) and (out[:k, 0].cpu().numpy() == r).all()
+
+
+def test_pairs_row_sharding_concatenates(planner):
+    """Row-range shards (multi-GPU partitioning) concatenate to the full list."""
+    import torch
+    g = mp.generate_graph("fork_join", 300, 50, 4)
+    lo, hi = planner.lifetimes_from_order(g, mp.random_topo_orders(g, 1, seed=3)[0])
+    full = planner.encode_address_pairs(g, lo, hi)
+    d = torch.device("cuda:0")
+    dlo, dhi = torch.from_numpy(lo).to(d), torch.from_numpy(hi).to(d)
+    dsz = torch.from_numpy(g.edge_size.view(np.int64)).to(d)
+    parts = []
+    bounds = [0, 17, 400, g.E // 2, g.E]
+    for r0, r1 in zip(bounds[:-1], bounds[1:]):
+        off = torch.zeros(r1 - r0 + 1, dtype=torch.int64, device=d)
+        cnt = planner.overlap_pairs_d(g.E, dlo, dhi, dsz, None, r0, r1, off, None, 0)
+        out = torch.zeros((max(cnt, 1), 2), dtype=torch.int32, device=d)
+        cnt2 = planner.overlap_pairs_d(g.E, dlo, dhi, dsz, None, r0, r1, off, out, cnt)
+        torch.cuda.synchronize()
+        assert cnt2 == cnt
+        parts.append(out[:cnt].cpu().numpy())
+    assert (np.concatenate(parts) == full).all()
+
+
+def test_validation_vs_oracle_random(planner):
+    g = mp.generate_graph("fork_join", 800, 1000, 5)
+    o = mp.random_topo_orders(g, 1, seed=11)[0]
+    lo, hi = planner.lifetimes_from_order(g, o)
+    rng = np.random.default_rng(0)
+    addr = rng.integers(0, 50_000, g.E).astype(np.uint64)
+    has = (rng.random(g.E) < 0.9).astype(np.uint8)
+    got = planner.conflicting_pairs(lo, hi, g.edge_size, has, addr)
+    exp = O.validate_pairs(lo, hi, g.edge_size, has, addr)
+    assert got.shape == exp.shape and (got == exp).all() and len(exp) > 0
+    placed = {e: int(addr[e]) for e in range(g.E) if has[e]}
+    assert planner.addresses_feasible(g, lo, hi, placed) == O.addresses_feasible(
+        lo, hi, g.edge_size, has, addr)
+    assert planner.peak_mem(g, placed) == O.peak_mem(g.edge_size, has, addr)
+
+
+def test_device_scoring_and_argmin_key(planner):
+    import torch
+    g = mp.generate_graph("fork_join", 200, 300, 1)
+    orders = mp.random_topo_orders(g, 1000, seed=4)
+    orders[5, 0], orders[5, 1] = orders[5, 1], orders[5, 0]
+    host = planner.score_orders(g, orders)
+    d = torch.device("cuda:0")
+    dg = planner.upload(g)
+    t_orders = torch.from_numpy(orders).to(d)
+    peak = torch.zeros(1000, dtype=torch.int64, device=d)
+    step = torch.zeros(1000, dtype=torch.int32, device=d)
+    valid = torch.zeros(1000, dtype=torch.uint8, device=d)
+    out3 = torch.zeros(3, dtype=torch.int64, device=d)
+    s = torch.cuda.current_stream().cuda_stream
+    planner.score_orders_d(dg, t_orders, 1000, peak, step, valid, s)
+    planner.argmin_key_d(peak, valid, 1000, 5000, out3, s)
+    torch.cuda.synchronize()
+    assert (peak.cpu().numpy().view(np.uint64) == host.peak).all()
+    assert (step.cpu().numpy() == host.peak_step).all()
+    assert (valid.cpu().numpy() == host.valid).all()
+    best = host.argmin()
+    o3 = out3.cpu().numpy().view(np.uint64)
+    assert int(o3[0]) == best + 5000 and int(o3[1]) == int(host.peak[best])
+    assert int(o3[2]) == (int(host.peak[best]) << 20) | (best + 5000)
+
+
+def test_edge_cases(planner):
+    empty = mp.load_graph('{"nodes": [], "edges": []}')
+    assert planner.peak_resident_bytes(empty, []) == 0
+    assert planner.resident_bytes_per_step(empty, []).tolist() == []
+    t = planner.timeline_from_lifetimes(empty, [], [], 0)
+    assert (t.peak_rs, t.peak_step) == (0, 0)
+    with pytest.raises(errors.InvalidOrder):
+        planner.lifetimes_from_order(empty, [0])
+    solo = mp.load_graph('{"nodes": [{"id": "a"}], "edges": []}')
+    res = planner.score_orders(solo, np.array([[0], [1], [-1]], np.int32))
+    assert res.valid.tolist() == [1, 0, 0] and res.peak_step.tolist() == [1, 0, 0]
+    t = planner.timeline_from_lifetimes(solo, [], [], 4)
+    assert t.bytes.tolist() == [0, 0, 0, 0] and (t.peak_rs, t.peak_step) == (0, 1)
+    g = mp.generate_graph("chain", 5, 3)
+    res = planner.score_orders(g, np.zeros((3, 4), np.int32))   # wrong length
+    assert res.valid.tolist() == [0, 0, 0]
+    assert planner.encode_address_pairs(g, [1, 1], [0, 0]).shape == (0, 2)
+    assert planner.argmin(np.array([5, 3, 3], np.uint64), np.array([1, 0, 1], np.uint8)) == 2
+    assert planner.argmin(np.array([5], np.uint64), np.array([0], np.uint8)) == -1

@@ -1,0 +1,118 @@
+"""CPU: the C restatement (oracle/memplan_oracle.c) against the reference's own
+outputs (tests/golden/golden.json, produced by the compiled reference) and the
+reference test suite's known answers."""
+import numpy as np
+import pytest
+
+import oracle as O
+
+
+def _oracle(rec):
+    c = rec["csr"]
+    return O.Oracle(c["n"], c["edge_src"], c["sink_off"], c["sinks"], c["edge_size"])
+
+
+def test_golden_orders(golden):
+    checked = 0
+    for rec in golden["graphs"]:
+        o = _oracle(rec)
+        for case in rec["orders"]:
+            lt = o.lifetimes_from_order(case["order"])
+            if "error" in case:
+                assert lt is None, (rec["name"], case["order"])
+                assert case["error"].startswith("InvalidOrder: ")
+                continue
+            lo, hi = lt
+            assert lo.tolist() == case["lo"] and hi.tolist() == case["hi"], rec["name"]
+            assert o.resident_bytes_per_step(case["order"]).tolist() == case["bytes"]
+            assert o.peak_resident_bytes(case["order"]) == case["peak"]
+            b, pr, ps = o.timeline_from_lifetimes(lo, hi, o.n)
+            assert b.tolist() == case["timeline"]["bytes"]
+            assert (pr, ps) == (case["timeline"]["peak_rs"], case["timeline"]["peak_step"])
+            pairs = O.overlap_pairs(lo, hi, o.size)
+            assert pairs.tolist() == case["pairs"], rec["name"]
+            assert len(pairs) == case["pairs_unfiltered_count"]
+            checked += 1
+    assert checked >= 70
+
+
+def test_golden_pinned_pairs(golden):
+    for rec in golden["graphs"]:
+        if "pinned" not in rec:
+            continue
+        o = _oracle(rec)
+        order = rec["orders"][0]["order"]
+        lo, hi = o.lifetimes_from_order(order)
+        got = O.overlap_pairs(lo, hi, o.size, np.asarray(rec["pinned"]["pinned"], np.uint8))
+        assert got.tolist() == rec["pinned"]["pairs"], rec["name"]
+
+
+def test_golden_validation_pairs(golden):
+    """Pairwise part of validate_plan: count of below_above violations."""
+    for rec in golden["graphs"]:
+        o = _oracle(rec)
+        for plan in rec.get("plans", []):
+            expect = [v for v in plan["violations"] if v[0] == "below_above"]
+            ts = np.asarray(plan["timestep_of"], np.int32)
+            if (ts <= 0).any() or any(v[0] == "fanin_in_memory" for v in plan["violations"]):
+                continue  # validate_plan returns before the pair loop
+            horizon = max(o.n, int(ts.max()) if ts.size else 0)
+            lo, hi = o.realized_lifetimes(ts, horizon)
+            got = O.validate_pairs(lo, hi, o.size, plan["has_addr"], plan["addr"])
+            assert len(got) == len(expect), (rec["name"], plan["name"])
+
+
+def test_golden_realized(golden):
+    for rec in golden["graphs"]:
+        o = _oracle(rec)
+        for case in rec.get("realized", []):
+            r = o.realized_lifetimes(case["timestep_of"], case["horizon"])
+            if "error" in case:
+                assert r[0] == "missing"
+                assert case["error"].startswith("InvalidOrder: node ")
+            else:
+                assert r[0].tolist() == case["lo"] and r[1].tolist() == case["hi"]
+
+
+def test_battery_min_peak_witnesses(golden):
+    """enumerate_min_peak's witness order attains min_peak (test_oracle.cpp:30-37)."""
+    assert len(golden["battery"]) >= 200
+    for b in golden["battery"]:
+        if "spec" not in b:
+            continue
+        kind, layers, size, seed = b["spec"]
+        if not O.ref_available():
+            pytest.skip("reference library not built")
+        g = O.RefGraph.generate(kind, layers, size, seed)
+        o = O.Oracle.from_csr(g.csr())
+        assert o.peak_resident_bytes(b["order"]) == b["min_peak"]
+
+
+def test_reference_known_answers(golden):
+    # test_plan.cpp:104-110 (chain3), :112-118 (order4 best order)
+    rec = {r["name"]: r for r in golden["graphs"]}
+    c3 = _oracle(rec["chain3"])
+    assert c3.resident_bytes_per_step([0, 1, 2]).tolist() == [4, 6, 2]
+    assert c3.timeline_from_lifetimes(*c3.lifetimes_from_order([0, 1, 2]), 3)[1:] == (6, 2)
+    o4 = _oracle(rec["order4"])
+    # node order in order4.json is v1, v3, v2, v4 -> best order v1 v2 v3 v4 = [0, 2, 1, 3]
+    assert o4.resident_bytes_per_step([0, 2, 1, 3]).tolist() == [20, 21, 21, 11]
+    assert o4.peak_resident_bytes([0, 1, 2, 3]) == 30   # program order (test_milp.cpp:103-108)
+    p3 = _oracle(rec["pack3"])
+    lo, hi = p3.lifetimes_from_order([0, 1, 2, 3])
+    assert list(zip(lo.tolist(), hi.tolist())) == [(1, 2), (1, 4), (3, 4)]
+    assert O.overlap_pairs(lo, hi, p3.size).tolist() == [[0, 1], [1, 2]]  # pack3_address.lp:4-9
+    for L, peak in ((2, 136), (3, 200), (4, 264)):                        # test_acceptance.cpp:235
+        assert golden["kats"][f"training_like_L{L}_program_peak"] == peak
+    for mr, rs, f in golden["kats"]["fragmentation"]:
+        assert O.fragmentation(mr, rs) == f
+    # sinkless edge to the horizon (test_plan.cpp:135-141)
+    one = O.Oracle(1, [0], [0, 0], [], [3])
+    assert one.realized_lifetimes([1], 5)[1].tolist() == [5]
+
+
+def test_chain3_plan_graph(golden):
+    plan = golden["plan_graph"]["chain3"]
+    assert plan["addresses"] == {"e1": 0, "e2": 4}
+    assert plan["peak_mem"] == 6 and plan["timeline"]["peak_rs"] == 6
+    assert O.peak_mem([4, 2], [1, 1], [0, 4]) == 6
