@@ -13,9 +13,11 @@
  *     graph.hpp:58-59); byte sizes and addresses are uint64.
  *   - Timesteps are 1-based and intervals closed, as memplan::Interval
  *     (analysis.hpp:28-37); an interval with lo > hi is empty.
- *   - Functions without the `_d` suffix take HOST buffers and copy in/out.
- *     `_d` variants take DEVICE pointers and a cudaStream_t (as void*), are
- *     stream-ordered and never synchronise unless stated.
+ *   - Functions without the `_d` suffix take HOST buffers and copy in/out on
+ *     the context's stream (mp_ctx_set_stream) and return when done.
+ *     `_d` variants take DEVICE pointers and a cudaStream_t (as void*; NULL
+ *     is the default stream, as in every CUDA API), are stream-ordered and
+ *     never synchronise unless stated (the pair/validation counts do).
  *   - No CPU fallback exists: with no usable sm_100 device every call that
  *     computes returns MP_E_NO_DEVICE / MP_E_CUDA.
  *   - Errors map 1:1 onto the reference's exception classes

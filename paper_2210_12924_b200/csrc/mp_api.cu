@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "mp_internal.h"
+#include "mp_prep.h"
 
 namespace mpb {
 
@@ -196,70 +197,44 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
   g->h_edge_size.assign(csr->edge_size, csr->edge_size + E);
 
   // Structural checks the kernels rely on (Graph::build, graph.cpp:82-128).
-  std::vector<std::vector<int32_t>> preds(n);
-  std::vector<uint64_t> alloc(n, 0), sfree(n, 0);
-  std::vector<int32_t> multi_off{0}, multi_sinks;
-  std::vector<uint64_t> multi_size;
   uint64_t total = 0;
   const uint64_t cap = uint64_t{1} << 62;
   std::vector<int32_t> seen_stamp(n, -1);
   for (int32_t e = 0; e < E; ++e) {
     const int32_t s = g->h_edge_src[e];
     const int64_t a = g->h_sink_off[e], b = g->h_sink_off[e + 1];
-    if (s < 0 || s >= n) {
-      set_error("DanglingEndpoint: edge #" + std::to_string(e) + " has unknown source");
-      delete g;
-      return MP_E_BAD_GRAPH;
-    }
-    if (b < a || b > S) {
-      set_error("InvalidStructure: sink offsets are not monotone");
-      delete g;
-      return MP_E_BAD_GRAPH;
-    }
-    for (int64_t k = a; k < b; ++k) {
+    std::string err;
+    if (s < 0 || s >= n) err = "DanglingEndpoint: edge #" + std::to_string(e) + " has unknown source";
+    else if (b < a || b > S) err = "InvalidStructure: sink offsets are not monotone";
+    for (int64_t k = a; err.empty() && k < b; ++k) {
       const int32_t w = g->h_sinks[k];
-      if (w < 0 || w >= n) {
-        set_error("DanglingEndpoint: edge #" + std::to_string(e) + " has unknown sink");
-        delete g;
-        return MP_E_BAD_GRAPH;
-      }
-      if (seen_stamp[w] == e) {
-        set_error("InvalidStructure: edge #" + std::to_string(e) + " lists a sink twice");
-        delete g;
-        return MP_E_BAD_GRAPH;
-      }
-      seen_stamp[w] = e;
-      preds[w].push_back(s);
+      if (w < 0 || w >= n) err = "DanglingEndpoint: edge #" + std::to_string(e) + " has unknown sink";
+      else if (seen_stamp[w] == e) err = "InvalidStructure: edge #" + std::to_string(e) + " lists a sink twice";
+      else seen_stamp[w] = e;
     }
     const uint64_t sz = g->h_edge_size[e];
-    if (sz >= cap || total + sz >= cap) {
-      set_error("InvalidStructure: total tensor bytes exceed the supported range");
+    if (err.empty() && (sz >= cap || total + sz >= cap))
+      err = "InvalidStructure: total tensor bytes exceed the supported range";
+    if (!err.empty()) {
+      set_error(err);
       delete g;
       return MP_E_BAD_GRAPH;
     }
     total += sz;
-    if (sz == 0) continue;  // control edge: orders nodes, carries no bytes
-    alloc[s] += sz;
-    if (b - a == 1) {
-      sfree[g->h_sinks[a]] += sz;
-    } else if (b - a >= 2) {
-      for (int64_t k = a; k < b; ++k) multi_sinks.push_back(g->h_sinks[k]);
-      multi_off.push_back((int32_t)multi_sinks.size());
-      multi_size.push_back(sz);
-    }
   }
   g->total_bytes = total;
-  std::vector<int32_t> pred_off(n + 1, 0), pred_flat;
-  for (int32_t v = 0; v < n; ++v) {
-    auto& p = preds[v];
-    std::sort(p.begin(), p.end());
-    p.erase(std::unique(p.begin(), p.end()), p.end());
-    pred_flat.insert(pred_flat.end(), p.begin(), p.end());
-    pred_off[v + 1] = (int32_t)pred_flat.size();
-  }
-  g->D = (int64_t)pred_flat.size();
-  g->M = (int32_t)multi_size.size();
-  g->MS = (int64_t)multi_sinks.size();
+
+  // Scoring tables (transitive reduction, static last consumers, gcd scale).
+  ScorePrep P;
+  prepare_scoring(n, E, g->h_edge_src.data(), g->h_sink_off.data(), g->h_sinks.data(),
+                  g->h_edge_size.data(), &P);
+  g->n_preds = (int64_t)P.preds.size();
+  g->n_dyn = (int32_t)P.dyn.size();
+  g->n_big = (int32_t)P.big_size.size();
+  g->n_dyn_edges = P.num_dyn_edges;
+  g->scale = P.scale;
+  g->narrow = P.narrow;
+  g->exact_reach = P.exact_reach;
 
   DeviceGuard guard(ctx->device);
   cudaStream_t st = ctx->stream;
@@ -271,16 +246,23 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
   up(upload(&g->d_sink_off, g->h_sink_off.data(), (size_t)E + 1, st));
   up(upload(&g->d_sinks, g->h_sinks.data(), (size_t)S, st));
   up(upload(&g->d_edge_size, g->h_edge_size.data(), (size_t)E, st));
-  up(upload(&g->d_pred_off, pred_off.data(), (size_t)n + 1, st));
-  up(upload(&g->d_preds, pred_flat.data(), pred_flat.size(), st));
-  up(upload(&g->d_node_alloc, alloc.data(), (size_t)n, st));
-  up(upload(&g->d_node_sfree, sfree.data(), (size_t)n, st));
-  up(upload(&g->d_multi_off, multi_off.data(), multi_off.size(), st));
-  up(upload(&g->d_multi_sinks, multi_sinks.data(), multi_sinks.size(), st));
-  up(upload(&g->d_multi_size, multi_size.data(), multi_size.size(), st));
-  if (s == MP_OK) up(score_configure(g));
+  up(upload(&g->d_pred_off, P.pred_off.data(), P.pred_off.size(), st));
+  up(upload(&g->d_preds, P.preds.data(), P.preds.size(), st));
+  up(upload(&g->d_node_alloc, P.alloc.data(), P.alloc.size(), st));
+  up(upload(&g->d_node_sfree, P.sfree.data(), P.sfree.size(), st));
+  up(upload(&g->d_dyn_off, P.dyn_off.data(), P.dyn_off.size(), st));
+  up(upload(reinterpret_cast<DynMember**>(&g->d_dyn), P.dyn.data(), P.dyn.size(), st));
+  up(upload(&g->d_big_off, P.big_off.data(), P.big_off.size(), st));
+  up(upload(&g->d_big_sinks, P.big_sinks.data(), P.big_sinks.size(), st));
+  up(upload(&g->d_big_size, P.big_size.data(), P.big_size.size(), st));
+  int max_pred = 0, max_dyn = 0;
+  for (int32_t v = 0; v < n; ++v) {
+    max_pred = std::max(max_pred, P.pred_off[v + 1] - P.pred_off[v]);
+    max_dyn = std::max(max_dyn, P.dyn_off[v + 1] - P.dyn_off[v]);
+  }
+  if (s == MP_OK) up(score_configure(g, max_pred, max_dyn));
   if (s == MP_OK) {
-    cudaError_t ce = cudaStreamSynchronize(st);
+    cudaError_t ce = cudaStreamSynchronize(st);  // host tables may go out of scope
     if (ce != cudaSuccess) s = cuda_status(ce, "mp_graph_upload");
   }
   if (s != MP_OK) {
@@ -294,9 +276,10 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
 mp_status mp_graph_free(mp_graph* g) {
   if (!g) return MP_OK;
   DeviceGuard guard(g->ctx->device);
-  void* ptrs[] = {g->d_edge_src,  g->d_sink_off,   g->d_sinks,      g->d_edge_size,
-                  g->d_pred_off,  g->d_preds,      g->d_node_alloc, g->d_node_sfree,
-                  g->d_multi_off, g->d_multi_sinks, g->d_multi_size};
+  void* ptrs[] = {g->d_edge_src, g->d_sink_off, g->d_sinks,     g->d_edge_size,
+                  g->d_pred_off, g->d_preds,    g->d_node_alloc, g->d_node_sfree,
+                  g->d_dyn_off,  g->d_dyn,      g->d_big_off,    g->d_big_sinks,
+                  g->d_big_size};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete g;
@@ -308,8 +291,8 @@ mp_status mp_graph_get_info(const mp_graph* g, mp_graph_info* info) {
   info->num_nodes = g->n;
   info->num_edges = g->E;
   info->num_sinks = g->S;
-  info->num_pred_pairs = g->D;
-  info->num_multi_sink = g->M;
+  info->num_pred_pairs = g->n_preds;
+  info->num_multi_sink = g->n_dyn_edges;
   info->smem_resident = g->smem_resident ? 1 : 0;
   info->total_bytes = g->total_bytes;
   return MP_OK;
@@ -320,7 +303,7 @@ mp_status mp_lifetimes_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_order,
                          int32_t* d_lo, int32_t* d_hi, int32_t* d_valid, void* stream) {
   if (!ctx || !g || (len > 0 && !d_order) || !d_valid) return invalid_arg("null argument");
   DeviceGuard guard(ctx->device);
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL: default stream
   MP_TRY(ctx->scratch[2].reserve(sizeof(int32_t) * ((size_t)g->n + 1)));
   return launch_lifetimes(g, d_order, len, d_lo, d_hi, d_valid,
                           static_cast<int32_t*>(ctx->scratch[2].ptr), st);
@@ -492,7 +475,7 @@ mp_status mp_score_orders_argmin_d(mp_ctx* ctx, const mp_graph* g, const int32_t
   if (C > 0 && (!d_peak || !d_step || !d_valid || (g->n > 0 && !d_orders)))
     return invalid_arg("null output");
   DeviceGuard guard(ctx->device);
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL: default stream
   return launch_score(g, d_orders, C, d_peak, d_step, d_valid, nullptr, d_best_key, index_base,
                       st);
 }
@@ -550,7 +533,7 @@ mp_status mp_argmin_key_d(mp_ctx* ctx, const uint64_t* d_peak, const uint8_t* d_
   if (!ctx || !d_out3 || C < 0 || index_base < 0 || (C > 0 && (!d_peak || !d_valid)))
     return invalid_arg("bad argument");
   DeviceGuard guard(ctx->device);
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL: default stream
   return launch_argmin(d_peak, d_valid, C, index_base, d_out3, st);
 }
 
@@ -662,7 +645,7 @@ mp_status mp_overlap_pairs_d(mp_ctx* ctx, int32_t E, const int32_t* d_lo, const 
   if (!ctx || !count || !d_row_off || E < 0 || (E > 0 && (!d_lo || !d_hi || !d_size)))
     return invalid_arg("null argument");
   DeviceGuard guard(ctx->device);
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL: default stream
   PairArgs a;
   a.num_edges = E;
   a.lo = d_lo;
@@ -689,7 +672,7 @@ mp_status mp_validate_pairs_d(mp_ctx* ctx, int32_t E, const int32_t* d_lo, const
       (E > 0 && (!d_lo || !d_hi || !d_size || !d_has || !d_addr)))
     return invalid_arg("null argument");
   DeviceGuard guard(ctx->device);
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL: default stream
   PairArgs a;
   a.num_edges = E;
   a.lo = d_lo;

@@ -54,23 +54,14 @@ struct mp_ctx {
 // Device-resident graph tables. Built once by mp_graph_upload from the
 // reference-shaped CSR (memplan::Graph flattened).
 //
-// Scoring layout:
-//   pred_off/preds   distinct producer nodes of every node (validity:
-//                    graph.cpp:239-254 over data and control edges)
-//   node_alloc       bytes a node allocates at its own timestep (sum of its
-//                    data fanout sizes; schedule.cpp:37 lo = pos[src])
-//   node_sfree       bytes freed after a node's timestep by data edges whose
-//                    ONLY consumer is that node (hi = pos[sink])
-//   multi_*          data edges with >= 2 consumers: their last consumer
-//                    (hi = max pos[sink], schedule.cpp:46) depends on the order
+// Scoring tables (see mp_prep.cpp and DESIGN.md §3): reduced validity
+// edges, per-node allocated / statically freed bytes, and the data edges
+// whose last consumer depends on the order.
 struct mp_graph {
   mp_ctx* ctx = nullptr;
   int32_t n = 0;
   int32_t E = 0;
   int64_t S = 0;
-  int64_t D = 0;       // pred pairs
-  int32_t M = 0;       // multi-consumer data edges
-  int64_t MS = 0;      // their total sinks
   uint64_t total_bytes = 0;
 
   // raw CSR (edge space)
@@ -79,14 +70,25 @@ struct mp_graph {
   int32_t* d_sinks = nullptr;
   uint64_t* d_edge_size = nullptr;
 
-  // node space, derived
-  int32_t* d_pred_off = nullptr;   // [n+1]
-  int32_t* d_preds = nullptr;      // [D]
+  // node space, derived by mp_prep.cpp (scaled by `scale`)
+  int64_t n_preds = 0;               // reduced validity edges
+  int32_t n_dyn = 0;                 // DynMember records
+  int32_t n_big = 0;                 // order-dependent edges with many candidates
+  int32_t n_dyn_edges = 0;
+  uint64_t scale = 1;
+  bool narrow = true;
+  bool exact_reach = false;
+  int32_t* d_pred_off = nullptr;     // [n+1]
+  int32_t* d_preds = nullptr;        // [n_preds]
   uint64_t* d_node_alloc = nullptr;  // [n]
   uint64_t* d_node_sfree = nullptr;  // [n]
-  int32_t* d_multi_off = nullptr;  // [M+1] into d_multi_sinks
-  int32_t* d_multi_sinks = nullptr;  // [MS]
-  uint64_t* d_multi_size = nullptr;  // [M]
+  int32_t* d_dyn_off = nullptr;      // [n+1]
+  void* d_dyn = nullptr;             // DynMember[n_dyn]
+  int32_t* d_big_off = nullptr;      // [n_big+1]
+  int32_t* d_big_sinks = nullptr;
+  uint64_t* d_big_size = nullptr;    // [n_big]
+  int score_j = 0;                   // nodes per thread held in registers (0 = global variant)
+  int score_threads = 1024;
 
   // first node that misses a timestep in realized_lifetimes is searched on
   // the host in reference order; keep the CSR on the host too.
@@ -108,7 +110,7 @@ mp_status launch_score(const mp_graph* g, const int32_t* d_orders, int64_t num_o
                        uint64_t* d_key /* fused argmin key or null */, int64_t index_base,
                        cudaStream_t st);
 size_t score_scratch_bytes(const mp_graph* g, int64_t num_orders);
-mp_status score_configure(mp_graph* g);
+mp_status score_configure(mp_graph* g, int max_pred_cnt, int max_dyn_cnt);
 
 mp_status launch_lifetimes(const mp_graph* g, const int32_t* d_order, int64_t order_len,
                            int32_t* d_lo, int32_t* d_hi, int32_t* d_valid, int32_t* d_pos_scratch,

@@ -59,7 +59,7 @@ class ScoreResult:
         idx = np.flatnonzero(self.valid)
         if idx.size == 0:
             return -1
-        return int(idx[np.argmin(self.peak[idx], kind="stable")])
+        return int(idx[np.argmin(self.peak[idx])])  # np.argmin returns the first minimum
 
 
 @dataclass
