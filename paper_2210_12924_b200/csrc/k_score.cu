@@ -13,26 +13,27 @@
 // position p(v): RS(p) = sum_{q<=p} (alloc_q - free_q) + free_p, where
 // alloc_q is the static fanout bytes of the node at q and free_q the bytes
 // whose last consumer is that node. Host preprocessing (mp_prep.cpp) makes
-// most frees static (single consumer, or every other consumer reaches this
-// one) and drops redundant validity edges, so per candidate the device does:
-//   phase 1 (order space)  pos[order[k]] = stamp|k                 n scatters
-//   phase 2 (node space)   stamp check = permutation check,        n sequential reads
-//                          producers-before-consumers,             |reduced preds| gathers
-//                          order-dependent last consumers,         few gathers
-//                          XF[p(v)] = (alloc - free, free)         n scatters
-//   phase 3 (order space)  two-pass warp scan + first argmax       sequential
-// Static per-node data lives in registers of the owning thread (node
-// v = tid + j*T, j < J) for the whole persistent loop; the next candidate's
-// order slice is prefetched into registers while the current one is scored.
-// Values are in units of gcd(sizes); 32-bit when total/gcd < 2^32 (every
-// RS then fits, and modular sums are exact).
+// most frees static (single consumer, or every other consumer reaches it) and
+// drops redundant validity edges. Per candidate the device then does:
+//   phase 1  (order space)  pos[order[k]] = stamp|k                      n scatters
+//   phase 2a (node space)   stamp check (= permutation check),          n sequential reads
+//                           first reduced producer before the node,     ~n gathers
+//                           XF[p(v)] = (x_v, f_v)                        n scatters
+//   phase 2b                remaining reduced producer pairs (flat)      few gathers
+//   phase 2c                order-dependent last consumers: max pos over
+//                           the candidate sinks, 2 smem atomics          few gathers
+//   phase 3  (order space)  blocked two-pass scan + first argmax        sequential
+// Static per-node data (x_v, f_v, first producer) lives in registers of the
+// owning thread (node v = tid + j*T, j < J) for the whole persistent loop;
+// the next candidate's order slice is prefetched into registers while the
+// current one is scored. Values are in units of gcd(sizes); 32-bit when
+// total/gcd < 2^32 (every RS then fits and modular sums are exact).
 #include <cuda_runtime.h>
 
 #include <climits>
 #include <cstdint>
 
 #include "mp_internal.h"
-#include "mp_prep.h"
 
 namespace mpb {
 namespace {
@@ -41,19 +42,19 @@ constexpr int kWarp = 32;
 
 struct ScoreTables {
   int32_t n;
-  int32_t npreds;
+  int32_t nextra;
   int32_t ndyn;
-  int32_t nbig;
+  int32_t ndyn_sinks;
+  int32_t P;  // scan chunk per thread (odd)
   uint64_t scale;
-  const int32_t* __restrict__ pred_off;
-  const int32_t* __restrict__ preds;
-  const uint64_t* __restrict__ alloc;
-  const uint64_t* __restrict__ sfree;
+  const uint64_t* __restrict__ node_x;
+  const uint64_t* __restrict__ node_f;
+  const int32_t* __restrict__ pred1;
+  const int32_t* __restrict__ extra_u;
+  const int32_t* __restrict__ extra_w;
   const int32_t* __restrict__ dyn_off;
-  const DynMember* __restrict__ dyn;
-  const int32_t* __restrict__ big_off;
-  const int32_t* __restrict__ big_sinks;
-  const uint64_t* __restrict__ big_size;
+  const int32_t* __restrict__ dyn_sinks;
+  const uint64_t* __restrict__ dyn_size;
 };
 
 // Position word: stamp in the high half, position in the low half. Within one
@@ -64,17 +65,19 @@ struct PosWord;
 template <>
 struct PosWord<uint32_t> {
   static constexpr uint32_t kMaxStamp = 0xffffu;
-  __device__ static uint32_t make(uint32_t stamp, int k) { return (stamp << 16) | (uint32_t)k; }
-  __device__ static uint32_t stamp(uint32_t w) { return w >> 16; }
+  __device__ static uint32_t tag(uint32_t stamp) { return stamp << 16; }
+  __device__ static bool fresh(uint32_t w, uint32_t tag) { return (w & 0xffff0000u) == tag; }
   __device__ static int pos(uint32_t w) { return (int)(w & 0xffffu); }
 };
 template <>
 struct PosWord<unsigned long long> {
   static constexpr uint32_t kMaxStamp = 0xffffffffu;
-  __device__ static unsigned long long make(uint32_t stamp, int k) {
-    return ((unsigned long long)stamp << 32) | (uint32_t)k;
+  __device__ static unsigned long long tag(uint32_t stamp) {
+    return (unsigned long long)stamp << 32;
   }
-  __device__ static uint32_t stamp(unsigned long long w) { return (uint32_t)(w >> 32); }
+  __device__ static bool fresh(unsigned long long w, unsigned long long tag) {
+    return (w & 0xffffffff00000000ull) == tag;
+  }
   __device__ static int pos(unsigned long long w) { return (int)(uint32_t)w; }
 };
 
@@ -121,15 +124,27 @@ struct BlockScratch {
   int widx[32];
 };
 
-// J > 0: static node data in registers (node v = tid + j*T, T <= 512),
-//        per-candidate buffers in shared memory.
-// J == 0: node data read from global (coalesced, L1/L2-resident) per
-//        candidate; buffers in shared memory (kSmem) or per-CTA global scratch.
-// Node ranges are packed as offset << 12 | count (count < 4096, checked on
-// the host; offsets < 2^20 in the shared-memory variants).
-constexpr int kCntBits = 12;
-constexpr int kCntMask = (1 << kCntBits) - 1;
+template <typename VT, typename PW>
+struct Layout {
+  // smem (or per-CTA global) layout: extra pairs, dyn tables, pos, XF
+  static size_t bytes(int n, int T, int P, int nextra, int ndyn, int ndyn_sinks, bool tables) {
+    size_t b = 0;
+    if (tables) {
+      b += ((size_t)nextra * 8 + 15) & ~size_t(15);
+      b += ((size_t)(ndyn + 1) * 4 + 15) & ~size_t(15);
+      b += ((size_t)ndyn_sinks * 4 + 15) & ~size_t(15);
+      b += ((size_t)ndyn * sizeof(VT) + 15) & ~size_t(15);
+    }
+    b += ((size_t)n * sizeof(PW) + 15) & ~size_t(15);
+    b += (size_t)T * P * sizeof(XFPair<VT>);
+    return b + 16;
+  }
+};
 
+// J > 0: node data in registers (node v = tid + j*T, T <= 512), buffers and
+//        flat tables in shared memory.
+// J == 0: node data read from global (coalesced) per candidate; buffers in
+//        shared memory (kSmem) or in a per-CTA global scratch slice.
 template <typename VT, typename PW, int J, bool kSmem>
 __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
     score_kernel(ScoreTables G, const int32_t* __restrict__ orders, int64_t C,
@@ -147,55 +162,58 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
   const int lane = tid & (kWarp - 1);
   const int warp = tid >> 5;
   const int nwarps = T >> 5;
+  const int P = G.P;
 
   // ---- buffers -------------------------------------------------------------
-  const int32_t* preds;
-  const DynMember* dyn;
-  PW* pos;
-  XFPair<VT>* XF;
+  const int32_t* ex_u = G.extra_u;
+  const int32_t* ex_w = G.extra_w;
+  const int32_t* dy_off = G.dyn_off;
+  const int32_t* dy_sinks = G.dyn_sinks;
+  const uint64_t* dy_size64 = G.dyn_size;
+  const VT* dy_size = nullptr;
+  char* p = kSmem ? smem : gscratch + (size_t)blockIdx.x * gstride;
   if (kSmem) {
-    char* p = smem;
-    int32_t* sp = reinterpret_cast<int32_t*>(p);
-    p += ((size_t)G.npreds * 4 + 15) & ~size_t(15);
-    DynMember* sd = reinterpret_cast<DynMember*>(p);
-    p += ((size_t)G.ndyn * sizeof(DynMember) + 15) & ~size_t(15);
-    pos = reinterpret_cast<PW*>(p);
-    p += ((size_t)n * sizeof(PW) + 15) & ~size_t(15);
-    XF = reinterpret_cast<XFPair<VT>*>(p);
-    for (int i = tid; i < G.npreds; i += T) sp[i] = G.preds[i];
-    const int32_t* gd = reinterpret_cast<const int32_t*>(G.dyn);
-    int32_t* sdw = reinterpret_cast<int32_t*>(sd);
-    for (int i = tid; i < G.ndyn * (int)(sizeof(DynMember) / 4); i += T) sdw[i] = gd[i];
-    preds = sp;
-    dyn = sd;
-  } else {
-    char* p = gscratch + (size_t)blockIdx.x * gstride;
-    pos = reinterpret_cast<PW*>(p);
-    p += ((size_t)n * sizeof(PW) + 255) & ~size_t(255);
-    XF = reinterpret_cast<XFPair<VT>*>(p);
-    preds = G.preds;
-    dyn = G.dyn;
+    int32_t* su = reinterpret_cast<int32_t*>(p);
+    int32_t* sw = su + G.nextra;
+    p += ((size_t)G.nextra * 8 + 15) & ~size_t(15);
+    int32_t* so = reinterpret_cast<int32_t*>(p);
+    p += ((size_t)(G.ndyn + 1) * 4 + 15) & ~size_t(15);
+    int32_t* ss = reinterpret_cast<int32_t*>(p);
+    p += ((size_t)G.ndyn_sinks * 4 + 15) & ~size_t(15);
+    VT* sz = reinterpret_cast<VT*>(p);
+    p += ((size_t)G.ndyn * sizeof(VT) + 15) & ~size_t(15);
+    for (int i = tid; i < G.nextra; i += T) {
+      su[i] = G.extra_u[i];
+      sw[i] = G.extra_w[i];
+    }
+    for (int i = tid; i <= G.ndyn; i += T) so[i] = G.dyn_off[i];
+    for (int i = tid; i < G.ndyn_sinks; i += T) ss[i] = G.dyn_sinks[i];
+    for (int i = tid; i < G.ndyn; i += T) sz[i] = (VT)G.dyn_size[i];
+    ex_u = su;
+    ex_w = sw;
+    dy_off = so;
+    dy_sinks = ss;
+    dy_size = sz;
   }
+  PW* pos = reinterpret_cast<PW*>(p);
+  p += ((size_t)n * sizeof(PW) + 15) & ~size_t(15);
+  XFPair<VT>* XF = reinterpret_cast<XFPair<VT>*>(p);
   for (int i = tid; i < n; i += T) pos[i] = 0;  // stamp 0 is never used
+  for (int i = n + tid; i < T * P; i += T) XF[i] = XFPair<VT>{0, 0};  // scan padding
 
   // ---- static per-node data in registers -------------------------------------
   constexpr int JR = J > 0 ? J : 1;
-  VT ra[JR], rf[JR];
-  uint32_t pr[JR], dr[JR];  // packed (offset << 12 | count)
-  int ov[JR];
+  VT rx[JR], rf[JR];
+  int rp[JR];  // first reduced producer, -1 if none
+  int ov[JR];  // next candidate's order slice
   if (J > 0) {
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const int v = tid + j * T;
       const bool in = v < n;
-      ra[j] = in ? (VT)G.alloc[v] : (VT)0;
-      rf[j] = in ? (VT)G.sfree[v] : (VT)0;
-      pr[j] = in ? ((uint32_t)G.pred_off[v] << kCntBits) |
-                       (uint32_t)(G.pred_off[v + 1] - G.pred_off[v])
-                 : 0u;
-      dr[j] = in ? ((uint32_t)G.dyn_off[v] << kCntBits) |
-                       (uint32_t)(G.dyn_off[v + 1] - G.dyn_off[v])
-                 : 0u;
+      rx[j] = in ? (VT)G.node_x[v] : (VT)0;
+      rf[j] = in ? (VT)G.node_f[v] : (VT)0;
+      rp[j] = in ? G.pred1[v] : -1;
       ov[j] = 0;
     }
     if ((int64_t)blockIdx.x < C) {
@@ -216,6 +234,7 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
       stamp = 1;
       __syncthreads();
     }
+    const PW tag = PWT::tag(stamp);
     bool bad = false;
 
     // ---- phase 1: inverse permutation (order space) ----------------------------
@@ -226,11 +245,10 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
         if (k < n) {
           const int v = ov[j];
           if ((unsigned)v >= (unsigned)n) bad = true;
-          else pos[v] = PWT::make(stamp, k);
+          else pos[v] = tag | (PW)k;
         }
       }
-      // prefetch the next candidate's slice; it lands while this one is scored
-      const int64_t cn = c + gridDim.x;
+      const int64_t cn = c + gridDim.x;  // prefetch: lands while this one is scored
       if (cn < C) {
         const int32_t* ord = orders + cn * n;
 #pragma unroll
@@ -244,53 +262,41 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
       for (int k = tid; k < n; k += T) {
         const int v = __ldg(ord + k);
         if ((unsigned)v >= (unsigned)n) bad = true;
-        else pos[v] = PWT::make(stamp, k);
+        else pos[v] = tag | (PW)k;
       }
     }
     __syncthreads();
 
-    // ---- phase 2: node space -----------------------------------------------------
-    auto node = [&](int v, VT a, VT sf, int q0, int q1, int e0, int e1) {
-      // q0..q1: reduced producers of v; e0..e1: v's order-dependent memberships
+    // ---- phase 2a: node space ------------------------------------------------------
+    auto node = [&](int v, VT x, VT f, int u) {
       const PW w = pos[v];
-      if (PWT::stamp(w) != stamp) bad = true;  // never written: not a permutation
-      for (int q = q0; q < q1; ++q)
-        if (pos[preds[q]] >= w) bad = true;    // a producer does not run before v
-      VT f = sf;
-      for (int e = e0; e < e1; ++e) {
-        const DynMember m = dyn[e];
-        bool last = true;
-        for (int i = 0; i < m.cnt; ++i) last &= pos[m.others[i]] < w;
-        if (last) f += (VT)m.size;
-      }
-      const int p = PWT::pos(w);
-      if (p < n) XF[p] = XFPair<VT>{(VT)(a - f), f};
+      bad |= !PWT::fresh(w, tag);           // never written: not a permutation
+      if (u >= 0) bad |= pos[u] >= w;       // producer not strictly before v
+      const int q = PWT::pos(w);
+      if (q < n) XF[q] = XFPair<VT>{x, f};
     };
     if (J > 0) {
 #pragma unroll
       for (int j = 0; j < J; ++j) {
         const int v = tid + j * T;
-        if (v < n) {
-          const int q0 = (int)(pr[j] >> kCntBits), e0 = (int)(dr[j] >> kCntBits);
-          node(v, ra[j], rf[j], q0, q0 + (int)(pr[j] & kCntMask), e0,
-               e0 + (int)(dr[j] & kCntMask));
-        }
+        if (v < n) node(v, rx[j], rf[j], rp[j]);
       }
     } else {
-      for (int v = tid; v < n; v += T)
-        node(v, (VT)G.alloc[v], (VT)G.sfree[v], G.pred_off[v], G.pred_off[v + 1], G.dyn_off[v],
-             G.dyn_off[v + 1]);
+      for (int v = tid; v < n; v += T) node(v, (VT)G.node_x[v], (VT)G.node_f[v], G.pred1[v]);
     }
-    if (G.nbig > 0) {  // order-dependent edges with many candidate consumers
-      __syncthreads();
-      for (int m = tid; m < G.nbig; m += T) {
+    // ---- phase 2b: remaining reduced producer pairs ----------------------------------
+    for (int i = tid; i < G.nextra; i += T) bad |= pos[ex_u[i]] >= pos[ex_w[i]];
+    // ---- phase 2c: order-dependent last consumers --------------------------------------
+    if (G.ndyn > 0) {
+      __syncthreads();  // XF written by phase 2a
+      for (int d = tid; d < G.ndyn; d += T) {
         PW h = 0;
-        for (int s = G.big_off[m]; s < G.big_off[m + 1]; ++s) h = max(h, pos[G.big_sinks[s]]);
-        const int p = PWT::pos(h);
-        if (p < n) {
-          const VT sz = (VT)G.big_size[m];
-          atomicAdd(&XF[p].f, sz);
-          atomicAdd(&XF[p].x, (VT)0 - sz);
+        for (int s = dy_off[d]; s < dy_off[d + 1]; ++s) h = max(h, pos[dy_sinks[s]]);
+        const int q = PWT::pos(h);
+        if (q < n) {
+          const VT sz = kSmem ? dy_size[d] : (VT)dy_size64[d];
+          atomicAdd(&XF[q].f, sz);
+          atomicAdd(&XF[q].x, (VT)0 - sz);
         }
       }
     }
@@ -303,33 +309,27 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
       continue;
     }
 
-    // ---- phase 3: order space, two-pass warp scan -------------------------------
-    const int chunks = (n + kWarp - 1) / kWarp;
-    const int per_warp = (chunks + nwarps - 1) / nwarps;
-    const int w_begin = warp * per_warp * kWarp;
-    const int w_end = min(n, w_begin + per_warp * kWarp);
-    VT part = 0;
-    for (int p = w_begin + lane; p < w_end; p += kWarp) part += XF[p].x;
-    part = warp_sum(part);
-    if (lane == 0) bs.wsum[warp] = part;
+    // ---- phase 3: blocked two-pass scan (chunk [tid*P, tid*P+P), P odd) ------------
+    const XFPair<VT>* mine = XF + tid * P;
+    VT total = 0;
+    for (int i = 0; i < P; ++i) total += mine[i].x;
+    const VT incl = warp_incl_scan(total, lane);
+    if (lane == kWarp - 1) bs.wsum[warp] = incl;
     __syncthreads();
-    VT carry = lane < warp ? bs.wsum[lane] : (VT)0;
-    carry = warp_sum(carry);
+    VT run = warp_sum(lane < warp ? bs.wsum[lane] : (VT)0) + incl - total;
     VT best = 0;
     int best_i = INT_MAX;
-    for (int base = w_begin; base < w_end; base += kWarp) {
-      const int p = base + lane;
-      const XFPair<VT> xf = p < w_end ? XF[p] : XFPair<VT>{0, 0};
-      const VT incl = warp_incl_scan(xf.x, lane) + carry;
-      const VT rs = incl + xf.f;
-      if (p < w_end) {
-        if (bytes_out) bytes_out[c * n + p] = (uint64_t)rs * G.scale;
-        if (rs > best || best_i == INT_MAX) {
-          best = rs;
-          best_i = p;
-        }
+    const int p0 = tid * P;
+    const int lim = min(P, n - p0);
+    for (int i = 0; i < lim; ++i) {
+      const XFPair<VT> xf = mine[i];
+      run += xf.x;
+      const VT rs = run + xf.f;
+      if (bytes_out) bytes_out[c * n + p0 + i] = (uint64_t)rs * G.scale;
+      if (rs > best || best_i == INT_MAX) {
+        best = rs;
+        best_i = p0 + i;
       }
-      carry = __shfl_sync(0xffffffffu, incl, kWarp - 1);
     }
     warp_argmax(best, best_i);
     if (lane == 0) {
@@ -355,34 +355,26 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
         }
       }
     }
-    // bs.wsum/wbest are rewritten only after two more barriers of the next
-    // candidate; XF after the next phase-1 barrier.
+    // bs.wsum is rewritten after >= 2 more barriers; XF after the next phase-1 barrier.
   }
-}
-
-template <typename VT>
-size_t smem_bytes(const mp_graph* g) {
-  return (((size_t)g->n_preds * 4 + 15) & ~size_t(15)) +
-         (((size_t)g->n_dyn * sizeof(DynMember) + 15) & ~size_t(15)) +
-         (((size_t)g->n * 4 + 15) & ~size_t(15)) + (size_t)g->n * 2 * sizeof(VT) + 64;
 }
 
 ScoreTables tables(const mp_graph* g) {
   ScoreTables G;
   G.n = g->n;
-  G.npreds = (int32_t)g->n_preds;
+  G.nextra = g->n_extra;
   G.ndyn = g->n_dyn;
-  G.nbig = g->n_big;
+  G.ndyn_sinks = g->n_dyn_sinks;
+  G.P = g->score_p;
   G.scale = g->scale;
-  G.pred_off = g->d_pred_off;
-  G.preds = g->d_preds;
-  G.alloc = g->d_node_alloc;
-  G.sfree = g->d_node_sfree;
+  G.node_x = g->d_node_x;
+  G.node_f = g->d_node_f;
+  G.pred1 = g->d_pred1;
+  G.extra_u = g->d_extra_u;
+  G.extra_w = g->d_extra_w;
   G.dyn_off = g->d_dyn_off;
-  G.dyn = reinterpret_cast<const DynMember*>(g->d_dyn);
-  G.big_off = g->d_big_off;
-  G.big_sinks = g->d_big_sinks;
-  G.big_size = g->d_big_size;
+  G.dyn_sinks = g->d_dyn_sinks;
+  G.dyn_size = g->d_dyn_size;
   return G;
 }
 
@@ -392,21 +384,22 @@ mp_status run(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d
               int64_t index_base, cudaStream_t st) {
   auto kern = score_kernel<VT, PW, J, kSmem>;
   const int T = g->score_threads;
+  const size_t per = Layout<VT, PW>::bytes(g->n, T, g->score_p, g->n_extra, g->n_dyn,
+                                           g->n_dyn_sinks, kSmem);
   size_t smem = 0;
   char* gs = nullptr;
   size_t gstride = 0;
   int64_t grid;
   if (kSmem) {
-    smem = smem_bytes<VT>(g);
+    smem = per;
     MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem));
     grid = (int64_t)g->ctx->num_sms * (per_sm > 0 ? per_sm : 1);
   } else {
     grid = (int64_t)g->ctx->num_sms * 2;
-    gstride = (((size_t)g->n * sizeof(PW) + 255) & ~size_t(255)) +
-              (((size_t)g->n * 2 * sizeof(VT) + 255) & ~size_t(255));
     if (grid > C) grid = C;
+    gstride = (per + 255) & ~size_t(255);
     MP_TRY(g->ctx->scratch[3].reserve(gstride * (size_t)(grid > 0 ? grid : 1)));
     gs = static_cast<char*>(g->ctx->scratch[3].ptr);
   }
@@ -425,6 +418,7 @@ mp_status dispatch(const mp_graph* g, const int32_t* o, int64_t C, uint64_t* pk,
   switch (g->score_j) {
     case 4: return run<VT, uint32_t, 4, true>(g, o, C, pk, stp, vl, by, key, base, st);
     case 8: return run<VT, uint32_t, 8, true>(g, o, C, pk, stp, vl, by, key, base, st);
+    case 16: return run<VT, uint32_t, 16, true>(g, o, C, pk, stp, vl, by, key, base, st);
     default:
       if (g->smem_resident)
         return run<VT, uint32_t, 0, true>(g, o, C, pk, stp, vl, by, key, base, st);
@@ -434,31 +428,40 @@ mp_status dispatch(const mp_graph* g, const int32_t* o, int64_t C, uint64_t* pk,
 
 }  // namespace
 
-mp_status score_configure(mp_graph* g, int max_pred_cnt, int max_dyn_cnt) {
-  // Register slice J (nodes per thread) with T = ceil(n / J) <= 512 threads
-  // when per-node counts fit the packed ranges; shared-memory buffers when
-  // they fit; otherwise node tables from global and/or global scratch.
+mp_status score_configure(mp_graph* g) {
+  // Register slice J (nodes per thread): the smallest of {4, 8, 16} giving
+  // T = ceil(n / J) <= 256 threads (512 for J = 16); shared-memory buffers
+  // when they fit; otherwise node tables from global and/or global scratch.
   const int n = g->n;
-  const size_t need = g->narrow ? smem_bytes<uint32_t>(g) : smem_bytes<unsigned long long>(g);
-  const bool smem = n < 65536 && need + 2048 <= g->ctx->max_smem_optin;
-  const bool packable = max_pred_cnt <= kCntMask && max_dyn_cnt <= kCntMask &&
-                        g->n_preds < (1 << 20) && g->n_dyn < (1 << 20);
   int J = 0, T = 1024;
-  if (smem && packable) {
-    for (int j : {4, 8}) {
-      const int t = ((n + j - 1) / j + 31) / 32 * 32;
-      if (t <= 512) {
-        J = j;
-        T = t < 32 ? 32 : t;
-        break;
-      }
+  for (int j : {4, 8, 16}) {
+    const int t = ((n + j - 1) / j + 31) / 32 * 32;
+    if (t <= (j == 16 ? 512 : 256)) {
+      J = j;
+      T = t < 32 ? 32 : t;
+      break;
     }
   }
-  if (J == 0 && smem) T = n <= 8192 ? 512 : 1024;
+  auto chunk = [&](int t) {
+    int p = (n + t - 1) / t;
+    if (p < 1) p = 1;
+    return p | 1;  // odd stride: conflict-free blocked LDS
+  };
+  auto need = [&](int t) {
+    return g->narrow ? Layout<uint32_t, uint32_t>::bytes(n, t, chunk(t), g->n_extra, g->n_dyn,
+                                                          g->n_dyn_sinks, true)
+                     : Layout<unsigned long long, uint32_t>::bytes(
+                           n, t, chunk(t), g->n_extra, g->n_dyn, g->n_dyn_sinks, true);
+  };
+  bool smem = n < 65536 && need(J > 0 ? T : 1024) + 2048 <= g->ctx->max_smem_optin;
+  if (!smem) J = 0;
+  if (J == 0) T = 1024;
+  if (J == 0 && !smem) smem = false;
   g->score_j = J;
   g->score_threads = T;
+  g->score_p = chunk(T);
   g->smem_resident = smem;
-  g->score_smem_bytes = smem ? need : 0;
+  g->score_smem_bytes = smem ? need(T) : 0;
   return MP_OK;
 }
 

@@ -228,10 +228,10 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
   ScorePrep P;
   prepare_scoring(n, E, g->h_edge_src.data(), g->h_sink_off.data(), g->h_sinks.data(),
                   g->h_edge_size.data(), &P);
-  g->n_preds = (int64_t)P.preds.size();
-  g->n_dyn = (int32_t)P.dyn.size();
-  g->n_big = (int32_t)P.big_size.size();
-  g->n_dyn_edges = P.num_dyn_edges;
+  g->n_preds = P.num_reduced_preds;
+  g->n_extra = (int32_t)P.extra_u.size();
+  g->n_dyn = (int32_t)P.dyn_size.size();
+  g->n_dyn_sinks = (int32_t)P.dyn_sinks.size();
   g->scale = P.scale;
   g->narrow = P.narrow;
   g->exact_reach = P.exact_reach;
@@ -246,21 +246,15 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
   up(upload(&g->d_sink_off, g->h_sink_off.data(), (size_t)E + 1, st));
   up(upload(&g->d_sinks, g->h_sinks.data(), (size_t)S, st));
   up(upload(&g->d_edge_size, g->h_edge_size.data(), (size_t)E, st));
-  up(upload(&g->d_pred_off, P.pred_off.data(), P.pred_off.size(), st));
-  up(upload(&g->d_preds, P.preds.data(), P.preds.size(), st));
-  up(upload(&g->d_node_alloc, P.alloc.data(), P.alloc.size(), st));
-  up(upload(&g->d_node_sfree, P.sfree.data(), P.sfree.size(), st));
+  up(upload(&g->d_node_x, P.node_x.data(), P.node_x.size(), st));
+  up(upload(&g->d_node_f, P.node_f.data(), P.node_f.size(), st));
+  up(upload(&g->d_pred1, P.pred1.data(), P.pred1.size(), st));
+  up(upload(&g->d_extra_u, P.extra_u.data(), P.extra_u.size(), st));
+  up(upload(&g->d_extra_w, P.extra_w.data(), P.extra_w.size(), st));
   up(upload(&g->d_dyn_off, P.dyn_off.data(), P.dyn_off.size(), st));
-  up(upload(reinterpret_cast<DynMember**>(&g->d_dyn), P.dyn.data(), P.dyn.size(), st));
-  up(upload(&g->d_big_off, P.big_off.data(), P.big_off.size(), st));
-  up(upload(&g->d_big_sinks, P.big_sinks.data(), P.big_sinks.size(), st));
-  up(upload(&g->d_big_size, P.big_size.data(), P.big_size.size(), st));
-  int max_pred = 0, max_dyn = 0;
-  for (int32_t v = 0; v < n; ++v) {
-    max_pred = std::max(max_pred, P.pred_off[v + 1] - P.pred_off[v]);
-    max_dyn = std::max(max_dyn, P.dyn_off[v + 1] - P.dyn_off[v]);
-  }
-  if (s == MP_OK) up(score_configure(g, max_pred, max_dyn));
+  up(upload(&g->d_dyn_sinks, P.dyn_sinks.data(), P.dyn_sinks.size(), st));
+  up(upload(&g->d_dyn_size, P.dyn_size.data(), P.dyn_size.size(), st));
+  if (s == MP_OK) up(score_configure(g));
   if (s == MP_OK) {
     cudaError_t ce = cudaStreamSynchronize(st);  // host tables may go out of scope
     if (ce != cudaSuccess) s = cuda_status(ce, "mp_graph_upload");
@@ -276,10 +270,9 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
 mp_status mp_graph_free(mp_graph* g) {
   if (!g) return MP_OK;
   DeviceGuard guard(g->ctx->device);
-  void* ptrs[] = {g->d_edge_src, g->d_sink_off, g->d_sinks,     g->d_edge_size,
-                  g->d_pred_off, g->d_preds,    g->d_node_alloc, g->d_node_sfree,
-                  g->d_dyn_off,  g->d_dyn,      g->d_big_off,    g->d_big_sinks,
-                  g->d_big_size};
+  void* ptrs[] = {g->d_edge_src, g->d_sink_off,  g->d_sinks,     g->d_edge_size,
+                  g->d_node_x,   g->d_node_f,    g->d_pred1,     g->d_extra_u,
+                  g->d_extra_w,  g->d_dyn_off,   g->d_dyn_sinks, g->d_dyn_size};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete g;
@@ -292,7 +285,7 @@ mp_status mp_graph_get_info(const mp_graph* g, mp_graph_info* info) {
   info->num_edges = g->E;
   info->num_sinks = g->S;
   info->num_pred_pairs = g->n_preds;
-  info->num_multi_sink = g->n_dyn_edges;
+  info->num_multi_sink = g->n_dyn;
   info->smem_resident = g->smem_resident ? 1 : 0;
   info->total_bytes = g->total_bytes;
   return MP_OK;

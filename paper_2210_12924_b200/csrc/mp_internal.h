@@ -71,24 +71,24 @@ struct mp_graph {
   uint64_t* d_edge_size = nullptr;
 
   // node space, derived by mp_prep.cpp (scaled by `scale`)
-  int64_t n_preds = 0;               // reduced validity edges
-  int32_t n_dyn = 0;                 // DynMember records
-  int32_t n_big = 0;                 // order-dependent edges with many candidates
-  int32_t n_dyn_edges = 0;
+  int64_t n_preds = 0;               // reduced validity edges (first + extra)
+  int32_t n_extra = 0;               // reduced pairs beyond each node's first producer
+  int32_t n_dyn = 0;                 // data edges whose last consumer depends on the order
+  int32_t n_dyn_sinks = 0;
   uint64_t scale = 1;
   bool narrow = true;
   bool exact_reach = false;
-  int32_t* d_pred_off = nullptr;     // [n+1]
-  int32_t* d_preds = nullptr;        // [n_preds]
-  uint64_t* d_node_alloc = nullptr;  // [n]
-  uint64_t* d_node_sfree = nullptr;  // [n]
-  int32_t* d_dyn_off = nullptr;      // [n+1]
-  void* d_dyn = nullptr;             // DynMember[n_dyn]
-  int32_t* d_big_off = nullptr;      // [n_big+1]
-  int32_t* d_big_sinks = nullptr;
-  uint64_t* d_big_size = nullptr;    // [n_big]
-  int score_j = 0;                   // nodes per thread held in registers (0 = global variant)
+  uint64_t* d_node_x = nullptr;      // [n] alloc - static free (scaled, modular)
+  uint64_t* d_node_f = nullptr;      // [n] static free (scaled)
+  int32_t* d_pred1 = nullptr;        // [n] first reduced producer or -1
+  int32_t* d_extra_u = nullptr;      // [n_extra]
+  int32_t* d_extra_w = nullptr;      // [n_extra]
+  int32_t* d_dyn_off = nullptr;      // [n_dyn+1]
+  int32_t* d_dyn_sinks = nullptr;    // [n_dyn_sinks]
+  uint64_t* d_dyn_size = nullptr;    // [n_dyn] scaled
+  int score_j = 0;                   // nodes per thread held in registers (0 = loop variant)
   int score_threads = 1024;
+  int score_p = 1;                   // blocked scan chunk per thread (odd)
 
   // first node that misses a timestep in realized_lifetimes is searched on
   // the host in reference order; keep the CSR on the host too.
@@ -110,7 +110,7 @@ mp_status launch_score(const mp_graph* g, const int32_t* d_orders, int64_t num_o
                        uint64_t* d_key /* fused argmin key or null */, int64_t index_base,
                        cudaStream_t st);
 size_t score_scratch_bytes(const mp_graph* g, int64_t num_orders);
-mp_status score_configure(mp_graph* g, int max_pred_cnt, int max_dyn_cnt);
+mp_status score_configure(mp_graph* g);
 
 mp_status launch_lifetimes(const mp_graph* g, const int32_t* d_order, int64_t order_len,
                            int32_t* d_lo, int32_t* d_hi, int32_t* d_valid, int32_t* d_pos_scratch,

@@ -97,8 +97,10 @@ void prepare_scoring(int32_t n, int32_t E, const int32_t* src, const int64_t* si
   };
   P->exact_reach = exact;
 
-  // Validity edges: drop u -> w when another successor of u reaches w.
-  P->pred_off.assign((size_t)n + 1, 0);
+  // Validity edges: drop u -> w when another successor of u reaches w. The
+  // first surviving producer of each node goes to the node's own record;
+  // the rest form a flat, evenly distributable pair list.
+  P->pred1.assign(n, -1);
   for (int32_t w = 0; w < n; ++w) {
     for (int32_t u : pred[w]) {
       bool redundant = false;
@@ -112,9 +114,15 @@ void prepare_scoring(int32_t n, int32_t E, const int32_t* src, const int64_t* si
           }
         }
       }
-      if (!redundant) P->preds.push_back(u);
+      if (redundant) continue;
+      ++P->num_reduced_preds;
+      if (P->pred1[w] < 0) {
+        P->pred1[w] = u;
+      } else {
+        P->extra_u.push_back(u);
+        P->extra_w.push_back(w);
+      }
     }
-    P->pred_off[w + 1] = (int32_t)P->preds.size();
   }
 
   // Byte tables.
@@ -127,13 +135,11 @@ void prepare_scoring(int32_t n, int32_t E, const int32_t* src, const int64_t* si
   if (g == 0) g = 1;
   P->scale = g;
   P->narrow = total / g < (uint64_t{1} << 32);
-  P->alloc.assign(n, 0);
-  P->sfree.assign(n, 0);
-  std::vector<std::vector<DynMember>> members(n);
+  std::vector<uint64_t> alloc(n, 0), sfree(n, 0);
   for (int32_t e = 0; e < E; ++e) {
     if (!size[e]) continue;
     const uint64_t s = size[e] / g;
-    P->alloc[src[e]] += s;
+    alloc[src[e]] += s;
     const int64_t a = sink_off[e], b = sink_off[e + 1];
     if (b == a) continue;  // sinkless: resident through the horizon
     std::vector<int32_t> cand;
@@ -146,28 +152,18 @@ void prepare_scoring(int32_t n, int32_t E, const int32_t* src, const int64_t* si
       if (!dominated) cand.push_back(x);
     }
     if (cand.size() == 1) {
-      P->sfree[cand[0]] += s;
-    } else if ((int)cand.size() <= kDynInline + 1) {
-      for (size_t i = 0; i < cand.size(); ++i) {
-        DynMember m{};
-        m.size = s;
-        m.cnt = 0;
-        for (size_t j = 0; j < cand.size(); ++j)
-          if (j != i) m.others[m.cnt++] = cand[j];
-        members[cand[i]].push_back(m);
-      }
-      ++P->num_dyn_edges;
+      sfree[cand[0]] += s;
     } else {
-      P->big_size.push_back(s);
-      P->big_sinks.insert(P->big_sinks.end(), cand.begin(), cand.end());
-      P->big_off.push_back((int32_t)P->big_sinks.size());
-      ++P->num_dyn_edges;
+      P->dyn_size.push_back(s);
+      P->dyn_sinks.insert(P->dyn_sinks.end(), cand.begin(), cand.end());
+      P->dyn_off.push_back((int32_t)P->dyn_sinks.size());
     }
   }
-  P->dyn_off.assign((size_t)n + 1, 0);
+  P->node_x.resize(n);
+  P->node_f.resize(n);
   for (int32_t v = 0; v < n; ++v) {
-    P->dyn.insert(P->dyn.end(), members[v].begin(), members[v].end());
-    P->dyn_off[v + 1] = (int32_t)P->dyn.size();
+    P->node_x[v] = alloc[v] - sfree[v];  // modular; exact after the prefix sum
+    P->node_f[v] = sfree[v];
   }
 }
 
