@@ -327,12 +327,12 @@ def main():
     h_valid = torch.zeros(C, dtype=torch.uint8).pin_memory()
     torch.cuda.synchronize()
     for i in range(3):
-        planner.score_orders_into(dg, pinned[i % 2].numpy(), h_peak, h_step, h_valid)
+        planner.score_orders_into(dg, pinned[i % len(pinned)].numpy(), h_peak, h_step, h_valid)
     if world > 1:
         dist.barrier()
     te0 = time.perf_counter()
     for i in range(e2e_steps):
-        best = planner.score_orders_into(dg, pinned[i % 2].numpy(), h_peak, h_step, h_valid)
+        best = planner.score_orders_into(dg, pinned[i % len(pinned)].numpy(), h_peak, h_step, h_valid)
         if world > 1:
             kv = (int(h_peak[best]) << 20 | (best + base)) if best >= 0 else 2**63 - 1
             bk = torch.tensor([kv], device=dev)

@@ -75,11 +75,19 @@ class Planner {
 
   mp_ctx* ctx() const { return ctx_; }
 
-  // The device copy of `g` (uploaded on first use).
+  // The device copy of `g` (uploaded on first use). Cached by address AND a
+  // structural fingerprint: a destroyed graph's address can be reused by the
+  // next one, which must not hit the stale upload.
   mp_graph* device_graph(const memplan::Graph& g) {
+    const std::uint64_t fp = fingerprint(g);
     auto it = graphs_.find(&g);
-    if (it != graphs_.end()) return it->second.handle;
+    if (it != graphs_.end()) {
+      if (it->second.fp == fp) return it->second.handle;
+      mp_graph_free(it->second.handle);
+      graphs_.erase(it);
+    }
     Uploaded u;
+    u.fp = fp;
     const int E = g.num_edges();
     u.src.resize(E);
     u.off.resize(E + 1, 0);
@@ -345,7 +353,21 @@ class Planner {
   }
 
  private:
+  static std::uint64_t fingerprint(const memplan::Graph& g) {
+    std::uint64_t h = 1469598103934665603ull;
+    auto mix = [&h](std::uint64_t x) { h = (h ^ x) * 1099511628211ull; };
+    mix((std::uint64_t)g.num_nodes());
+    mix((std::uint64_t)g.num_edges());
+    for (int e = 0; e < g.num_edges(); ++e) {
+      mix((std::uint64_t)g.source_of(e));
+      mix(g.edge(e).size);
+      for (int s : g.sinks_of(e)) mix((std::uint64_t)s + 0x9e3779b97f4a7c15ull);
+    }
+    return h;
+  }
+
   struct Uploaded {
+    std::uint64_t fp = 0;
     mp_graph* handle = nullptr;
     std::vector<int32_t> src, sinks;
     std::vector<int64_t> off;

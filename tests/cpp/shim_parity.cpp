@@ -115,6 +115,9 @@ static void check_graph(memplan_b200::Planner& dev, const Graph& g, std::mt19937
     const auto& o = orders[c];
     const std::string ref_err = error_of([&] { lifetimes_from_order(g, o); });
     const std::string dev_err = error_of([&] { dev.lifetimes_from_order(g, o); });
+    if (ref_err != dev_err)
+      std::printf("graph n=%d E=%d candidate %zu: ref='%s' dev='%s'\n", g.num_nodes(),
+                  g.num_edges(), c, ref_err.c_str(), dev_err.c_str());
     EXPECT(ref_err == dev_err, "lifetimes_from_order error text");
     EXPECT(scores[c].valid == ref_err.empty(), "score verdict");
     if (!ref_err.empty()) {
