@@ -232,6 +232,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2210_12924_b200 as mp
+    from paper_2210_12924_b200 import dist as D
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -264,7 +265,7 @@ def main():
     base = rank * C
 
     def one_step(b):
-        key.fill_(-1)  # UINT64_MAX as the atomicMin identity
+        key.fill_(D.NO_KEY)  # MP_KEY_NONE, the atomicMin identity
         planner.score_orders_argmin_d(dg, batches[b % nb], C, peak, step, valid, key, base,
                                       stream.cuda_stream)
         if world > 1:
@@ -275,7 +276,7 @@ def main():
         one_step(i)
     torch.cuda.synchronize()
     # key semantics check on the last warm-up batch (the fused argmin is the product)
-    kk = int(key.cpu().numpy().view(np.uint64)[0])
+    kk = D.check_device_key(int(key.item()))
 
     clocks = ClockSampler(dev)
     clocks.start()
@@ -289,7 +290,7 @@ def main():
     t0 = time.perf_counter()
     start.record(stream)
     for i in range(args.steps):
-        key.fill_(-1)
+        key.fill_(D.NO_KEY)
         ev_s[i].record(stream)
         planner.score_orders_argmin_d(dg, batches[i % nb], C, peak, step, valid, key, base,
                                       stream.cuda_stream)
@@ -334,7 +335,7 @@ def main():
     for i in range(e2e_steps):
         best = planner.score_orders_into(dg, pinned[i % len(pinned)].numpy(), h_peak, h_step, h_valid)
         if world > 1:
-            kv = (int(h_peak[best]) << 20 | (best + base)) if best >= 0 else 2**63 - 1
+            kv = D.pack_key(int(h_peak[best]), best + base) if best >= 0 else D.NO_KEY
             bk = torch.tensor([kv], device=dev)
             dist.all_reduce(bk, op=dist.ReduceOp.MIN)
             bk.item()
@@ -371,7 +372,7 @@ def main():
                     "path": "Planner.score_orders_into -> mp_score_orders_best (pinned host)"},
             "gpu_launches": args.steps,
             "clocks": clocks.summary(t0, t1),
-            "best_key_check": kk != 2**64 - 1,
+            "best_key_check": kk != D.NO_KEY,
         }
         if cpu:
             line["cpu_baseline"] = cpu

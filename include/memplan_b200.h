@@ -143,10 +143,13 @@ mp_status mp_score_orders_best(mp_ctx* ctx, const mp_graph* g, const int32_t* or
                                uint8_t* valid, int64_t* best);
 /* Device variant of the fused form: every valid candidate c does
  * atomicMin(d_best_key, peak << 20 | (c + index_base)); the caller sets
- * *d_best_key = UINT64_MAX beforehand (stream-ordered). Keys that do not fit
- * (peak >= 2^43 or index >= 2^20) are recorded as UINT64_MAX - 1, telling
- * the caller to fall back to mp_argmin_key_d. The minimum key across GPUs
- * (one allreduce(min)) is the global first-minimum. */
+ * *d_best_key = MP_KEY_NONE beforehand (stream-ordered). Keys that do not
+ * fit (peak >= 2^43 or index >= 2^20) are recorded as MP_KEY_OVERFLOW,
+ * telling the caller to fall back to mp_argmin_key_d. Keys are non-negative
+ * int64 values, so the minimum key across GPUs (one int64 allreduce(MIN))
+ * is the global first-minimum. */
+#define MP_KEY_NONE 0x7fffffffffffffffull
+#define MP_KEY_OVERFLOW 0x7ffffffffffffffeull
 mp_status mp_score_orders_argmin_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_orders,
                                    int64_t num_orders, uint64_t* d_peak, int32_t* d_peak_step,
                                    uint8_t* d_valid, uint64_t* d_best_key, int64_t index_base,
@@ -156,9 +159,9 @@ mp_status mp_score_orders_argmin_d(mp_ctx* ctx, const mp_graph* g, const int32_t
 mp_status mp_argmin(mp_ctx* ctx, const uint64_t* peak, const uint8_t* valid, int64_t num_orders,
                     int64_t* best);
 /* Device variant (one CTA): d_out3[0] = best index + index_base (or -1),
- * d_out3[1] = its peak, d_out3[2] = packed key peak << 20 | index (UINT64_MAX
- * when nothing is valid or the key does not fit: peak >= 2^43 or index >=
- * 2^20). index_base makes keys of different GPU shards comparable. */
+ * d_out3[1] = its peak, d_out3[2] = packed key peak << 20 | index
+ * (MP_KEY_NONE when nothing is valid, MP_KEY_OVERFLOW when peak >= 2^43 or
+ * index >= 2^20). index_base makes keys of different GPU shards comparable. */
 mp_status mp_argmin_key_d(mp_ctx* ctx, const uint64_t* d_peak, const uint8_t* d_valid,
                           int64_t num_orders, int64_t index_base, uint64_t* d_out3,
                           void* stream);

@@ -39,6 +39,10 @@ namespace mpb {
 namespace {
 
 constexpr int kWarp = 32;
+// Packed argmin keys stay non-negative as int64 so an NCCL int64 MIN works:
+// identity (no valid candidate) INT64_MAX, overflow marker INT64_MAX - 1.
+constexpr unsigned long long kKeyNone = 0x7fffffffffffffffull;
+constexpr unsigned long long kKeyOverflow = 0x7ffffffffffffffeull;
 
 struct ScoreTables {
   int32_t n;
@@ -350,7 +354,7 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
         if (best_key) {
           const uint64_t gi = (uint64_t)(c + index_base);
           const unsigned long long key =
-              (pk < (1ull << 43) && gi < (1ull << 20)) ? ((pk << 20) | gi) : ~0ull - 1;
+              (pk < (1ull << 43) && gi < (1ull << 20)) ? ((pk << 20) | gi) : kKeyOverflow;
           atomicMin(best_key, key);
         }
       }
@@ -523,7 +527,7 @@ __global__ void __launch_bounds__(1024)
       out[0] = (uint64_t)gi;
       out[1] = bp;
       const bool fits = gi >= 0 && gi < (1 << 20) && bp < (1ull << 43);
-      out[2] = fits ? ((bp << 20) | (uint64_t)gi) : ~0ull;
+      out[2] = gi < 0 ? kKeyNone : fits ? ((bp << 20) | (uint64_t)gi) : kKeyOverflow;
     }
   }
 }

@@ -495,20 +495,21 @@ mp_status mp_score_orders_best(mp_ctx* ctx, const mp_graph* g, const int32_t* or
   uint8_t* d_valid = cv.take<uint8_t>(c);
   uint64_t* d_key = cv.take<uint64_t>(3);
   const bool fused = best && C <= (int64_t{1} << 20);
-  if (fused) MP_CUDA(cudaMemsetAsync(d_key, 0xff, 8, st));
+  const uint64_t kNone = 0x7fffffffffffffffull, kOverflow = 0x7ffffffffffffffeull;
+  if (fused) MP_CUDA(cudaMemcpyAsync(d_key, &kNone, 8, cudaMemcpyHostToDevice, st));
   if (n) MP_CUDA(cudaMemcpyAsync(d_orders, orders, 4 * n * c, cudaMemcpyHostToDevice, st));
   MP_TRY(launch_score(g, d_orders, C, d_peak, d_step, d_valid, nullptr, fused ? d_key : nullptr,
                       0, st));
-  uint64_t key = ~0ull;
+  uint64_t key = kNone;
   if (fused) MP_CUDA(cudaMemcpyAsync(&key, d_key, 8, cudaMemcpyDeviceToHost, st));
   MP_CUDA(cudaMemcpyAsync(peak, d_peak, 8 * c, cudaMemcpyDeviceToHost, st));
   MP_CUDA(cudaMemcpyAsync(step, d_step, 4 * c, cudaMemcpyDeviceToHost, st));
   MP_CUDA(cudaMemcpyAsync(valid, d_valid, c, cudaMemcpyDeviceToHost, st));
   MP_CUDA(cudaStreamSynchronize(st));
   if (best) {
-    if (key == ~0ull) {
+    if (fused && key == kNone) {
       *best = -1;                                   // no valid candidate
-    } else if (key != ~0ull - 1 && fused) {
+    } else if (fused && key != kOverflow) {
       *best = (int64_t)(key & ((1ull << 20) - 1));  // fused (peak, index) minimum
     } else {                                        // key overflow: reduce on the device
       MP_TRY(launch_argmin(d_peak, d_valid, C, 0, d_key, st));

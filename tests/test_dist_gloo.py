@@ -1,0 +1,97 @@
+"""CPU, world size 2 over gloo: the multi-GPU host logic (candidate sharding +
+one allreduce-argmin, row sharding of the pair sweep) reproduces the serial
+reference semantics. The per-shard device work is replaced here by the C
+restatement of the same functions (this runs without a GPU)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp_
+
+from paper_2210_12924_b200 import dist as D
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, peaks, valid, lo, hi, size, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "oracle"))
+    import oracle as O
+    # --- candidate sharding + single allreduce(min) on the packed key
+    b, e = D.shard_range(len(peaks), world, rank)
+    best = -1
+    for c in range(b, e):
+        if valid[c] and (best < 0 or peaks[c] < peaks[best]):
+            best = c
+    key = torch.tensor([D.pack_key(int(peaks[best]), best) if best >= 0 else D.NO_KEY],
+                       dtype=torch.int64)
+    D.allreduce_argmin(key)
+    fallback = D.allgather_argmin(int(peaks[best]) if best >= 0 else 0, best)
+    # --- row-sharded pair generation, concatenated in rank order
+    ranges = D.balanced_row_ranges(D.triangular_row_work(len(lo)), world)
+    r0, r1 = ranges[rank]
+    pairs = O.overlap_pairs(lo, hi, size)
+    mine = pairs[(pairs[:, 0] >= r0) & (pairs[:, 0] < r1)] if len(pairs) else pairs
+    gathered = [None] * world
+    dist.all_gather_object(gathered, mine.tolist())
+    if rank == 0:
+        out_q.put((int(key.item()), fallback, gathered, ranges))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_two_rank_argmin_and_row_shards(world):
+    rng = np.random.default_rng(0)
+    C = 1000
+    peaks = rng.integers(1000, 1100, C).astype(np.int64)
+    valid = (rng.random(C) > 0.1).astype(np.uint8)
+    peaks[[17, 640]] = 999          # tie across the two shards: lowest index must win
+    valid[[17, 640]] = 1
+    E = 300
+    lo = rng.integers(1, 200, E).astype(np.int32)
+    hi = (lo + rng.integers(-3, 40, E)).astype(np.int32)
+    size = rng.integers(0, 3, E).astype(np.uint64)
+    ctx = mp_.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, peaks, valid, lo, hi, size, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    key, fallback, gathered, ranges = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert D.unpack_key(key) == (999, 17)
+    assert fallback == (999, 17)
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "oracle"))
+    import oracle as O
+    full = O.overlap_pairs(lo, hi, size).tolist()
+    assert sum(gathered, []) == full
+    assert ranges[0][0] == 0 and ranges[-1][1] == E and ranges[0][1] == ranges[1][0]
+
+
+def test_key_packing_edges():
+    assert D.unpack_key(D.pack_key(5, 3)) == (5, 3)
+    assert D.unpack_key(D.NO_KEY) == (0, -1)
+    assert D.pack_key(0, -1) == D.NO_KEY
+    with pytest.raises(OverflowError):
+        D.pack_key(1 << 43, 0)
+    with pytest.raises(OverflowError):
+        D.check_device_key(D.OVERFLOW_KEY)
+    assert D.check_device_key(D.NO_KEY) == D.NO_KEY
+    assert [D.shard_range(10, 3, r) for r in range(3)] == [(0, 3), (3, 6), (6, 10)]
+    assert D.balanced_row_ranges([], 2) == [(0, 0), (0, 0)]

@@ -356,6 +356,10 @@ def test_device_scoring_and_argmin_key(planner):
     o3 = out3.cpu().numpy().view(np.uint64)
     assert int(o3[0]) == best + 5000 and int(o3[1]) == int(host.peak[best])
     assert int(o3[2]) == (int(host.peak[best]) << 20) | (best + 5000)
+    key = torch.full((1,), (1 << 63) - 1, dtype=torch.int64, device=d)   # MP_KEY_NONE
+    planner.score_orders_argmin_d(dg, t_orders, 1000, peak, step, valid, key, 5000, s)
+    torch.cuda.synchronize()
+    assert int(key.item()) == int(o3[2])
 
 
 def test_edge_cases(planner):
