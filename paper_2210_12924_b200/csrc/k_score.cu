@@ -363,213 +363,7 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
   }
 }
 
-// ---- register-resident variant (n up to ~8k), branch-free per slot --------------
-// Slot j of a thread covers order position AND node k = (warp*J + j)*32 + lane:
-// warp-contiguous, so loads coalesce and per-slot offsets are immediates.
-// pos has two extra words: pos[n] absorbs the writes of padding slots (and of
-// out-of-range ids, which already flag the order) and pos[n+1] stays 0 = "no
-// producer" (always earlier). XF has T*P scanned entries (padding stays 0)
-// plus one garbage entry that absorbs scatters of stale (invalid) positions.
-template <typename VT, int J>
-__global__ void __launch_bounds__(512)
-    score_reg_kernel(ScoreTables G, const int32_t* __restrict__ orders, int64_t C,
-                     uint64_t* __restrict__ peak_out, int32_t* __restrict__ step_out,
-                     uint8_t* __restrict__ valid_out, uint64_t* __restrict__ bytes_out,
-                     unsigned long long* __restrict__ best_key, int64_t index_base) {
-  extern __shared__ __align__(16) char smem[];
-  __shared__ BlockScratch<VT> bs;
-
-  const int n = G.n;
-  const int T = blockDim.x;
-  const int tid = threadIdx.x;
-  const int lane = tid & (kWarp - 1);
-  const int warp = tid >> 5;
-  const int nwarps = T >> 5;
-  const int P = G.P;
-  const int TP = T * P;
-
-  // ---- shared memory: pos[n+2] | XF[TP+1] | extra pairs (u16|u16) | dyn tables
-  char* p = smem;
-  uint32_t* pos = reinterpret_cast<uint32_t*>(p);
-  p += ((size_t)(n + 2) * 4 + 15) & ~size_t(15);
-  XFPair<VT>* XF = reinterpret_cast<XFPair<VT>*>(p);
-  p += ((size_t)(TP + 1) * sizeof(XFPair<VT>) + 15) & ~size_t(15);
-  uint32_t* ex = reinterpret_cast<uint32_t*>(p);
-  p += ((size_t)G.nextra * 4 + 15) & ~size_t(15);
-  int32_t* dyo = reinterpret_cast<int32_t*>(p);
-  p += ((size_t)(G.ndyn + 1) * 4 + 15) & ~size_t(15);
-  int32_t* dys = reinterpret_cast<int32_t*>(p);
-  p += ((size_t)G.ndyn_sinks * 4 + 15) & ~size_t(15);
-  VT* dyz = reinterpret_cast<VT*>(p);
-  for (int i = tid; i < n + 2; i += T) pos[i] = 0;
-  for (int i = tid; i <= TP; i += T) XF[i] = XFPair<VT>{0, 0};
-  for (int i = tid; i < G.nextra; i += T)
-    ex[i] = (uint32_t)G.extra_u[i] | ((uint32_t)G.extra_w[i] << 16);
-  for (int i = tid; i <= G.ndyn; i += T) dyo[i] = G.dyn_off[i];
-  for (int i = tid; i < G.ndyn_sinks; i += T) dys[i] = G.dyn_sinks[i];
-  for (int i = tid; i < G.ndyn; i += T) dyz[i] = (VT)G.dyn_size[i];
-
-  // ---- per-slot registers ----------------------------------------------------
-  const int base = warp * J * kWarp + lane;  // slot j: k = base + 32*j
-  VT rx[J], rf[J];
-  int rpu[J];  // pos index of the first producer (n+1 if none)
-  int rpv[J];  // pos index of the node (n for padding)
-  int ov[J];               // next candidate's order values (-1 for padding)
-  uint32_t inmask = 0;
-#pragma unroll
-  for (int j = 0; j < J; ++j) {
-    const int v = base + kWarp * j;
-    const bool in = v < n;
-    inmask |= (in ? 1u : 0u) << j;
-    rx[j] = in ? (VT)G.node_x[v] : (VT)0;
-    rf[j] = in ? (VT)G.node_f[v] : (VT)0;
-    const int u = in ? G.pred1[v] : -1;
-    rpu[j] = u >= 0 ? u : n + 1;
-    rpv[j] = in ? v : n;
-    ov[j] = -1;
-  }
-  if ((int64_t)blockIdx.x < C) {
-    const int32_t* row = orders + (int64_t)blockIdx.x * n + base;
-#pragma unroll
-    for (int j = 0; j < J; ++j)
-      if (inmask >> j & 1) ov[j] = __ldg(row + kWarp * j);
-  }
-  __syncthreads();
-
-  const int garbage = TP;  // XF slot for stale positions
-  uint32_t stamp = 0;
-  for (int64_t c = blockIdx.x; c < C; c += gridDim.x) {
-    if (++stamp > 0xffffu) {
-      for (int i = tid; i < n + 2; i += T) pos[i] = 0;
-      stamp = 1;
-      __syncthreads();
-    }
-    const uint32_t tag = stamp << 16;
-    uint32_t bad = 0;
-
-    // ---- phase 1: pos[order[k]] = tag | k ------------------------------------------
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int v = ov[j];
-      const bool ok = (unsigned)v < (unsigned)n;
-      bad |= ((inmask >> j) & 1u) & (ok ? 0u : 1u);
-      pos[ok ? v : n] = tag + (uint32_t)(base + kWarp * j);
-    }
-    {
-      const int64_t cn = c + gridDim.x;  // prefetch the next candidate's slice
-      if (cn < C) {
-        const int32_t* row = orders + cn * n + base;
-#pragma unroll
-        for (int j = 0; j < J; ++j)
-          if (inmask >> j & 1) ov[j] = __ldg(row + kWarp * j);
-      }
-    }
-    __syncthreads();
-
-    // ---- phase 2a: node slots ---------------------------------------------------------
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const uint32_t w = pos[rpv[j]];
-      bad |= ((w & 0xffff0000u) != tag) ? 1u : 0u;  // not written: not a permutation
-      bad |= (pos[rpu[j]] >= w) ? 1u : 0u;           // producer not strictly earlier
-      const int q = (int)(w & 0xffffu);
-      XF[q < n ? q : garbage] = XFPair<VT>{rx[j], rf[j]};
-    }
-    // ---- phase 2b: remaining reduced producer pairs -----------------------------------
-    for (int i = tid; i < G.nextra; i += T) {
-      const uint32_t e = ex[i];
-      bad |= (pos[e & 0xffffu] >= pos[e >> 16]) ? 1u : 0u;
-    }
-    // ---- phase 2c: order-dependent last consumers -----------------------------------
-    if (G.ndyn > 0) {
-      __syncthreads();
-      for (int d = tid; d < G.ndyn; d += T) {
-        uint32_t h = 0;
-        for (int s = dyo[d]; s < dyo[d + 1]; ++s) h = max(h, pos[dys[s]]);
-        const int q = (int)(h & 0xffffu);
-        if (q < n) {
-          atomicAdd(&XF[q].f, dyz[d]);
-          atomicAdd(&XF[q].x, (VT)0 - dyz[d]);
-        }
-      }
-    }
-    if (__syncthreads_or(bad)) {
-      if (tid == 0) {
-        peak_out[c] = 0;
-        step_out[c] = 0;
-        valid_out[c] = 0;
-      }
-      continue;
-    }
-
-    // ---- phase 3: blocked two-pass scan over [tid*P, tid*P + P), P odd -------------
-    const XFPair<VT>* mine = XF + tid * P;
-    VT total = 0;
-    for (int i = 0; i < P; ++i) total += mine[i].x;
-    const VT incl = warp_incl_scan(total, lane);
-    if (lane == kWarp - 1) bs.wsum[warp] = incl;
-    __syncthreads();
-    VT run = warp_sum(lane < warp ? bs.wsum[lane] : (VT)0) + incl - total;
-    VT best = 0;
-    int best_i = INT_MAX;
-    const int p0 = tid * P;
-    if (bytes_out == nullptr) {
-      for (int i = 0; i < P; ++i) {  // padding entries are (0, 0): never a strict new max
-        const XFPair<VT> xf = mine[i];
-        run += xf.x;
-        const VT rs = run + xf.f;
-        const bool better = rs > best || best_i == INT_MAX;
-        best = better ? rs : best;
-        best_i = better ? p0 + i : best_i;
-      }
-      if (best_i >= n) best_i = INT_MAX;  // a chunk made only of padding
-    } else {
-      const int lim = min(P, n - p0);
-      for (int i = 0; i < lim; ++i) {
-        const XFPair<VT> xf = mine[i];
-        run += xf.x;
-        const VT rs = run + xf.f;
-        bytes_out[c * n + p0 + i] = (uint64_t)rs * G.scale;
-        if (rs > best || best_i == INT_MAX) {
-          best = rs;
-          best_i = p0 + i;
-        }
-      }
-    }
-    warp_argmax(best, best_i);
-    if (lane == 0) {
-      bs.wbest[warp] = best;
-      bs.widx[warp] = best_i;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      best = lane < nwarps ? bs.wbest[lane] : (VT)0;
-      best_i = lane < nwarps ? bs.widx[lane] : INT_MAX;
-      warp_argmax(best, best_i);
-      if (lane == 0) {
-        const bool empty = n == 0;
-        const uint64_t pk = empty ? 0 : (uint64_t)best * G.scale;
-        peak_out[c] = pk;
-        step_out[c] = empty ? 0 : best_i + 1;
-        valid_out[c] = 1;
-        if (best_key) {
-          const uint64_t gi = (uint64_t)(c + index_base);
-          const unsigned long long key =
-              (pk < (1ull << 43) && gi < (1ull << 20)) ? ((pk << 20) | gi) : kKeyOverflow;
-          atomicMin(best_key, key);
-        }
-      }
-    }
-  }
-}
-
-template <typename VT>
-size_t reg_smem_bytes(int n, int T, int P, int nextra, int ndyn, int ndyn_sinks) {
-  return (((size_t)(n + 2) * 4 + 15) & ~size_t(15)) +
-         (((size_t)(T * P + 1) * sizeof(XFPair<VT>) + 15) & ~size_t(15)) +
-         (((size_t)nextra * 4 + 15) & ~size_t(15)) + (((size_t)(ndyn + 1) * 4 + 15) & ~size_t(15)) +
-         (((size_t)ndyn_sinks * 4 + 15) & ~size_t(15)) + (size_t)ndyn * sizeof(VT) + 16;
-}
+#include "k_score_reg.cuh"
 
 ScoreTables tables(const mp_graph* g) {
   ScoreTables G;
@@ -667,7 +461,7 @@ mp_status score_configure(mp_graph* g) {
   int J = 0, T = 1024;
   for (int j : {4, 8, 16}) {
     const int t = ((n + j - 1) / j + 31) / 32 * 32;
-    if (t <= (j == 16 ? 512 : 256)) {
+    if (t <= (j == 16 ? 512 : 256)) {  // RegBounds<J>::kMaxT
       J = j;
       T = t < 32 ? 32 : t;
       break;
