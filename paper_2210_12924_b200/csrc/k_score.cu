@@ -59,6 +59,10 @@ struct ScoreTables {
   const int32_t* __restrict__ dyn_off;
   const int32_t* __restrict__ dyn_sinks;
   const uint64_t* __restrict__ dyn_size;
+  const uint32_t* __restrict__ node_xf32;
+  const uint64_t* __restrict__ node_xf64;
+  const int32_t* __restrict__ node_u;
+  const uint32_t* __restrict__ extra_packed;
 };
 
 // Position word: stamp in the high half, position in the low half. Within one
@@ -381,6 +385,10 @@ ScoreTables tables(const mp_graph* g) {
   G.dyn_off = g->d_dyn_off;
   G.dyn_sinks = g->d_dyn_sinks;
   G.dyn_size = g->d_dyn_size;
+  G.node_xf32 = g->d_node_xf32;
+  G.node_xf64 = g->d_node_xf64;
+  G.node_u = g->d_node_u;
+  G.extra_packed = g->d_extra_packed;
   return G;
 }
 

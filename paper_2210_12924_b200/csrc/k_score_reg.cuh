@@ -32,9 +32,7 @@ struct RegLayout {
            (((size_t)ndyn_sinks * 4 + 15) & ~size_t(15)) +
            (((size_t)ndyn * sizeof(VT) + 15) & ~size_t(15));
   }
-  __host__ __device__ size_t total() const {
-    return pos_bytes() + xf_bytes() + node_bytes() + table_bytes() + 16;
-  }
+  __host__ __device__ size_t total() const { return pos_bytes() + xf_bytes() + 16; }
 };
 
 // Register caps: J=4/8 run with T <= 256 and >= 4 CTAs per SM (<= 64 regs),
@@ -64,36 +62,22 @@ __global__ void __launch_bounds__(RegBounds<J>::kMaxT, RegBounds<J>::kMinBlocks)
   const int TP = T * P;
   const RegLayout<VT> L{n, T, P, G.nextra, G.ndyn, G.ndyn_sinks};
 
-  // ---- shared memory ----------------------------------------------------------
+  // ---- shared memory: only the per-candidate buffers; the static tables are
+  // read through L1 (prepared on the host in their final packed form, so a
+  // CTA that scores only a few candidates pays no copy-in).
   char* p = smem;
   uint32_t* pos = reinterpret_cast<uint32_t*>(p);
   p += L.pos_bytes();
   XFPair<VT>* XF = reinterpret_cast<XFPair<VT>*>(p);
-  p += L.xf_bytes();
-  XFPair<VT>* NXF = reinterpret_cast<XFPair<VT>*>(p);
-  p += ((size_t)(n + 1) * sizeof(XFPair<VT>) + 15) & ~size_t(15);
-  int32_t* NU = reinterpret_cast<int32_t*>(p);
-  p += ((size_t)(n + 1) * 4 + 15) & ~size_t(15);
-  uint32_t* ex = reinterpret_cast<uint32_t*>(p);
-  p += ((size_t)G.nextra * 4 + 15) & ~size_t(15);
-  int32_t* dyo = reinterpret_cast<int32_t*>(p);
-  p += ((size_t)(G.ndyn + 1) * 4 + 15) & ~size_t(15);
-  int32_t* dys = reinterpret_cast<int32_t*>(p);
-  p += ((size_t)G.ndyn_sinks * 4 + 15) & ~size_t(15);
-  VT* dyz = reinterpret_cast<VT*>(p);
+  const XFPair<VT>* __restrict__ NXF = reinterpret_cast<const XFPair<VT>*>(
+      sizeof(VT) == 4 ? (const void*)G.node_xf32 : (const void*)G.node_xf64);  // [n+1]
+  const int32_t* __restrict__ NU = G.node_u;        // [n+1], n+1 = no producer
+  const uint32_t* __restrict__ ex = G.extra_packed;  // u | w << 16
+  const int32_t* __restrict__ dyo = G.dyn_off;
+  const int32_t* __restrict__ dys = G.dyn_sinks;
+  const uint64_t* __restrict__ dyz = G.dyn_size;
   for (int i = tid; i < n + 2; i += T) pos[i] = 0;
   for (int i = tid; i <= TP; i += T) XF[i] = XFPair<VT>{0, 0};
-  for (int i = tid; i <= n; i += T) {  // NXF[n]/NU[n]: the padding node
-    const bool in = i < n;
-    NXF[i] = XFPair<VT>{in ? (VT)G.node_x[i] : (VT)0, in ? (VT)G.node_f[i] : (VT)0};
-    const int u = in ? G.pred1[i] : -1;
-    NU[i] = u >= 0 ? u : n + 1;
-  }
-  for (int i = tid; i < G.nextra; i += T)
-    ex[i] = (uint32_t)G.extra_u[i] | ((uint32_t)G.extra_w[i] << 16);
-  for (int i = tid; i <= G.ndyn; i += T) dyo[i] = G.dyn_off[i];
-  for (int i = tid; i < G.ndyn_sinks; i += T) dys[i] = G.dyn_sinks[i];
-  for (int i = tid; i < G.ndyn; i += T) dyz[i] = (VT)G.dyn_size[i];
 
   const int base = warp * J * kWarp + lane;  // slot j: k = base + 32*j
   uint32_t inmask = 0;
@@ -146,13 +130,13 @@ __global__ void __launch_bounds__(RegBounds<J>::kMaxT, RegBounds<J>::kMinBlocks)
       const int v = min(base + kWarp * j, n);        // padding slots -> node n
       const uint32_t w = pos[v];
       const XFPair<VT> nxf = NXF[v];
-      const uint32_t pu = pos[NU[v]];
+      const uint32_t pu = pos[__ldg(NU + v)];
       bad |= (w < tag || pu >= w) ? 1u : 0u;         // stale (not a permutation) / producer late
       XF[min((int)(w & 0xffffu), TP)] = nxf;
     }
     // ---- phase 2b: remaining reduced producer pairs -----------------------------------
     for (int i = tid; i < G.nextra; i += T) {
-      const uint32_t e = ex[i];
+      const uint32_t e = __ldg(ex + i);
       bad |= (pos[e & 0xffffu] >= pos[e >> 16]) ? 1u : 0u;
     }
     // ---- phase 2c: order-dependent last consumers -----------------------------------
@@ -160,11 +144,12 @@ __global__ void __launch_bounds__(RegBounds<J>::kMaxT, RegBounds<J>::kMinBlocks)
       __syncthreads();
       for (int d = tid; d < G.ndyn; d += T) {
         uint32_t h = 0;
-        for (int s = dyo[d]; s < dyo[d + 1]; ++s) h = max(h, pos[dys[s]]);
+        for (int s = __ldg(dyo + d); s < __ldg(dyo + d + 1); ++s) h = max(h, pos[__ldg(dys + s)]);
         const int q = (int)(h & 0xffffu);
         if (q < n) {
-          atomicAdd(&XF[q].f, dyz[d]);
-          atomicAdd(&XF[q].x, (VT)0 - dyz[d]);
+          const VT sz = (VT)__ldg(dyz + d);
+          atomicAdd(&XF[q].f, sz);
+          atomicAdd(&XF[q].x, (VT)0 - sz);
         }
       }
     }

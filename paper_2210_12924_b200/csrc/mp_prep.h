@@ -22,6 +22,11 @@ struct ScorePrep {
   std::vector<int32_t> dyn_off{0}, dyn_sinks;
   std::vector<uint64_t> dyn_size;   // scaled
   int64_t num_reduced_preds = 0;
+  // packed forms read by the register-slot scorer (index n = padding node):
+  std::vector<uint32_t> node_xf32;   // [2(n+1)] (x, f) pairs, 32-bit (narrow graphs)
+  std::vector<uint64_t> node_xf64;   // [2(n+1)] (x, f) pairs, 64-bit
+  std::vector<int32_t> node_u;       // [n+1] first producer, n+1 = none
+  std::vector<uint32_t> extra_packed;  // u | w << 16 (n < 65536)
 };
 
 void prepare_scoring(int32_t n, int32_t E, const int32_t* src, const int64_t* sink_off,
