@@ -432,8 +432,8 @@ mp_status run_reg(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_
                   int64_t index_base, cudaStream_t st) {
   auto kern = score_reg_kernel<VT, J>;
   const int T = g->score_threads;
-  const size_t smem = reg_smem_bytes<VT>(g->n, T, g->score_p, g->n_extra, g->n_dyn,
-                                         g->n_dyn_sinks);
+  const size_t smem = reg_smem_bytes<VT>(g->n, T, g->score_p, J);
+
   MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem));
@@ -469,7 +469,7 @@ mp_status score_configure(mp_graph* g) {
   int J = 0, T = 1024;
   for (int j : {4, 8, 16}) {
     const int t = ((n + j - 1) / j + 31) / 32 * 32;
-    if (t <= (j == 16 ? 512 : 256)) {  // RegBounds<J>::kMaxT
+    if (t <= (j == 4 ? 256 : j == 8 ? 384 : 512)) {  // RegBounds<J>::kMaxT
       J = j;
       T = t < 32 ? 32 : t;
       break;
@@ -487,10 +487,10 @@ mp_status score_configure(mp_graph* g) {
                            n, t, chunk(t), g->n_extra, g->n_dyn, g->n_dyn_sinks, true);
   };
   const size_t need_reg = J == 0 ? 0
-                         : g->narrow ? reg_smem_bytes<uint32_t>(n, T, chunk(T), g->n_extra,
-                                                                g->n_dyn, g->n_dyn_sinks)
-                                     : reg_smem_bytes<unsigned long long>(
-                                           n, T, chunk(T), g->n_extra, g->n_dyn, g->n_dyn_sinks);
+                         : g->narrow ? reg_smem_bytes<uint32_t>(n, T, chunk(T), J)
+                                     : reg_smem_bytes<unsigned long long>(n, T, chunk(T), J);
+
+
   if (J > 0 && need_reg + 2048 > g->ctx->max_smem_optin) J = 0;
   if (J > 0) T = ((n + J - 1) / J + 31) / 32 * 32, T = T < 32 ? 32 : T;
   bool smem = n < 65536 && need(J > 0 ? T : 1024) + 2048 <= g->ctx->max_smem_optin;

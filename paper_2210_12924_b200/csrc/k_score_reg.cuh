@@ -1,46 +1,39 @@
 // Register-slot variant of the fused scorer (n up to ~8k nodes), included by
 // k_score.cu inside namespace mpb::{anon}. See k_score.cu for the math.
 //
-// Slot j of a thread covers order position AND node k = (warp*J + j)*32 + lane:
-// warp-contiguous, so global loads coalesce, node-table reads are
-// conflict-free, and per-slot offsets are immediates. Only the next
-// candidate's order values live in registers (ov[J]); the static node tables
-// (x, f, first producer) sit in shared memory once per CTA.
+// Slot j of a thread covers order position AND node k = (warp*J + j)*32 + lane,
+// k < TJ = T*J: warp-contiguous, so global loads coalesce and every per-slot
+// shared-memory address is the thread's base plus an immediate. Per slot the
+// thread keeps in registers: the next candidate's order value ov, the node's
+// static bytes (x, f) and the pos index of its first reduced producer.
 //
-// Absorbing slots instead of branches:
-//   pos[n]    written by padding slots (k >= n) and by out-of-range ids
-//             (which already flag the order); padding node slots read it
-//   pos[n+1]  never written, stays 0: "no producer", always earlier
-//   XF[T*P]   garbage entry for scatters of stale (invalid-order) positions;
-//             XF[n .. T*P) is scan padding and stays (0, 0)
-// Permutation check: stamps only grow (until a wrap clears pos), so a word
-// is fresh iff w >= tag; n writes reaching all n nodes = a permutation.
+// Padding slots (k >= n) behave as inert nodes instead of branching: they
+// write pos[k] = tag|k in phase 1 (so they read back fresh), carry x = f = 0
+// (so their scatter leaves the scan padding at zero) and have "no producer"
+// (pos[TJ+1], never written, always 0). pos[TJ] absorbs out-of-range ids of
+// invalid orders. XF[n .. T*P) is scan padding (0, 0) and XF[T*P] absorbs
+// scatters of stale positions (invalid orders only).
+// Permutation check: stamps only grow (until a wrap clears pos), so a word is
+// fresh iff w >= tag; n writes reaching all n nodes = a permutation.
 
 template <typename VT>
 struct RegLayout {
-  int n, T, P, nextra, ndyn, ndyn_sinks;
-  __host__ __device__ size_t pos_bytes() const { return ((size_t)(n + 2) * 4 + 15) & ~size_t(15); }
+  int n, T, P, J;
+  __host__ __device__ int TJ() const { return T * J; }
+  __host__ __device__ size_t pos_words() const { return ((size_t)T * J + 2 + 3) & ~size_t(3); }
+  __host__ __device__ size_t pos_bytes() const { return pos_words() * 4; }
   __host__ __device__ size_t xf_bytes() const {
     return ((size_t)(T * P + 1) * sizeof(XFPair<VT>) + 15) & ~size_t(15);
-  }
-  __host__ __device__ size_t node_bytes() const {  // NXF[n+1] pairs + NU[n+1]
-    return (((size_t)(n + 1) * sizeof(XFPair<VT>) + 15) & ~size_t(15)) +
-           (((size_t)(n + 1) * 4 + 15) & ~size_t(15));
-  }
-  __host__ __device__ size_t table_bytes() const {
-    return (((size_t)nextra * 4 + 15) & ~size_t(15)) + (((size_t)(ndyn + 1) * 4 + 15) & ~size_t(15)) +
-           (((size_t)ndyn_sinks * 4 + 15) & ~size_t(15)) +
-           (((size_t)ndyn * sizeof(VT) + 15) & ~size_t(15));
   }
   __host__ __device__ size_t total() const { return pos_bytes() + xf_bytes() + 16; }
 };
 
-// Register caps: J=4/8 run with T <= 256 and >= 4 CTAs per SM (<= 64 regs),
-// J=16 with T <= 512 and >= 2 CTAs per SM.
+// Register budgets per slot count: J=4 -> T <= 256, 64 regs; J=8 -> T <= 384,
+// 85 regs; J=16 -> T <= 512, 128 regs (score_configure picks the smallest J).
 template <int J>
 struct RegBounds {
-  static constexpr int kMaxT = J <= 8 ? 256 : 512;
-  static constexpr int kMinBlocks = J <= 8 ? 4 : 2;
+  static constexpr int kMaxT = J == 4 ? 256 : J == 8 ? 384 : 512;
+  static constexpr int kMinBlocks = J == 4 ? 4 : J == 8 ? 2 : 1;
 };
 
 template <typename VT, int J>
@@ -60,44 +53,45 @@ __global__ void __launch_bounds__(RegBounds<J>::kMaxT, RegBounds<J>::kMinBlocks)
   const int nwarps = T >> 5;
   const int P = G.P;
   const int TP = T * P;
-  const RegLayout<VT> L{n, T, P, G.nextra, G.ndyn, G.ndyn_sinks};
+  const RegLayout<VT> L{n, T, P, J};
+  const int TJ = L.TJ();
 
-  // ---- shared memory: only the per-candidate buffers; the static tables are
-  // read through L1 (prepared on the host in their final packed form, so a
-  // CTA that scores only a few candidates pays no copy-in).
-  char* p = smem;
-  uint32_t* pos = reinterpret_cast<uint32_t*>(p);
-  p += L.pos_bytes();
-  XFPair<VT>* XF = reinterpret_cast<XFPair<VT>*>(p);
-  const XFPair<VT>* __restrict__ NXF = reinterpret_cast<const XFPair<VT>*>(
-      sizeof(VT) == 4 ? (const void*)G.node_xf32 : (const void*)G.node_xf64);  // [n+1]
-  const int32_t* __restrict__ NU = G.node_u;        // [n+1], n+1 = no producer
-  const uint32_t* __restrict__ ex = G.extra_packed;  // u | w << 16
-  const int32_t* __restrict__ dyo = G.dyn_off;
-  const int32_t* __restrict__ dys = G.dyn_sinks;
-  const uint64_t* __restrict__ dyz = G.dyn_size;
-  for (int i = tid; i < n + 2; i += T) pos[i] = 0;
-  for (int i = tid; i <= TP; i += T) XF[i] = XFPair<VT>{0, 0};
+  uint32_t* pos = reinterpret_cast<uint32_t*>(smem);
+  XFPair<VT>* XF = reinterpret_cast<XFPair<VT>*>(smem + L.pos_bytes());
+  {
+    uint4* z = reinterpret_cast<uint4*>(pos);  // pos = 0: stamp 0 is never used
+    for (int i = tid; i < (int)(L.pos_words() / 4); i += T) z[i] = make_uint4(0, 0, 0, 0);
+    for (int i = n + tid; i <= TP; i += T) XF[i] = XFPair<VT>{0, 0};  // scan padding
+  }
 
   const int base = warp * J * kWarp + lane;  // slot j: k = base + 32*j
-  uint32_t inmask = 0;
-#pragma unroll
-  for (int j = 0; j < J; ++j) inmask |= (base + kWarp * j < n ? 1u : 0u) << j;
+  uint32_t real = 0;                          // bit j: slot j is a real node / position
   int ov[J];
+  VT rx[J], rf[J];
+  int ru[J];
 #pragma unroll
-  for (int j = 0; j < J; ++j) ov[j] = -1;
+  for (int j = 0; j < J; ++j) {
+    const int k = base + kWarp * j;
+    const bool in = k < n;
+    real |= (in ? 1u : 0u) << j;
+    rx[j] = in ? (VT)__ldg(G.node_x + k) : (VT)0;
+    rf[j] = in ? (VT)__ldg(G.node_f + k) : (VT)0;
+    const int u = in ? __ldg(G.pred1 + k) : -1;
+    ru[j] = u >= 0 ? u : TJ + 1;
+    ov[j] = k;  // padding slots keep their own index forever
+  }
   if ((int64_t)blockIdx.x < C) {
     const int32_t* row = orders + (int64_t)blockIdx.x * n + base;
 #pragma unroll
     for (int j = 0; j < J; ++j)
-      if (inmask >> j & 1) ov[j] = __ldg(row + kWarp * j);
+      if (real >> j & 1) ov[j] = __ldg(row + kWarp * j);
   }
   __syncthreads();
 
   uint32_t stamp = 0;
   for (int64_t c = blockIdx.x; c < C; c += gridDim.x) {
     if (++stamp > 0xffffu) {
-      for (int i = tid; i < n + 2; i += T) pos[i] = 0;
+      for (int i = tid; i < (int)L.pos_words(); i += T) pos[i] = 0;
       stamp = 1;
       __syncthreads();
     }
@@ -109,9 +103,8 @@ __global__ void __launch_bounds__(RegBounds<J>::kMaxT, RegBounds<J>::kMinBlocks)
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const uint32_t v = (uint32_t)ov[j];
-      const bool ok = v < (uint32_t)n;                 // padding slots carry -1
-      bad |= (ok || !((inmask >> j) & 1u)) ? 0u : 1u;
-      pos[ok ? v : (uint32_t)n] = tagbase + kWarp * j;
+      bad |= ((real >> j) & 1u) & (v >= (uint32_t)n ? 1u : 0u);
+      pos[min(v, (uint32_t)TJ)] = tagbase + kWarp * j;
     }
     {
       const int64_t cn = c + gridDim.x;  // prefetch the next candidate's slice
@@ -119,7 +112,7 @@ __global__ void __launch_bounds__(RegBounds<J>::kMaxT, RegBounds<J>::kMinBlocks)
         const int32_t* row = orders + cn * n + base;
 #pragma unroll
         for (int j = 0; j < J; ++j)
-          if (inmask >> j & 1) ov[j] = __ldg(row + kWarp * j);
+          if (real >> j & 1) ov[j] = __ldg(row + kWarp * j);
       }
     }
     __syncthreads();
@@ -127,16 +120,14 @@ __global__ void __launch_bounds__(RegBounds<J>::kMaxT, RegBounds<J>::kMinBlocks)
     // ---- phase 2a: node slots -----------------------------------------------------------
 #pragma unroll
     for (int j = 0; j < J; ++j) {
-      const int v = min(base + kWarp * j, n);        // padding slots -> node n
-      const uint32_t w = pos[v];
-      const XFPair<VT> nxf = NXF[v];
-      const uint32_t pu = pos[__ldg(NU + v)];
-      bad |= (w < tag || pu >= w) ? 1u : 0u;         // stale (not a permutation) / producer late
-      XF[min((int)(w & 0xffffu), TP)] = nxf;
+      const uint32_t w = pos[base + kWarp * j];
+      const uint32_t pu = pos[ru[j]];
+      bad |= (w < tag || pu >= w) ? 1u : 0u;  // stale (not a permutation) / producer late
+      XF[min((int)(w & 0xffffu), TP)] = XFPair<VT>{rx[j], rf[j]};
     }
     // ---- phase 2b: remaining reduced producer pairs -----------------------------------
     for (int i = tid; i < G.nextra; i += T) {
-      const uint32_t e = __ldg(ex + i);
+      const uint32_t e = __ldg(G.extra_packed + i);
       bad |= (pos[e & 0xffffu] >= pos[e >> 16]) ? 1u : 0u;
     }
     // ---- phase 2c: order-dependent last consumers -----------------------------------
@@ -144,10 +135,11 @@ __global__ void __launch_bounds__(RegBounds<J>::kMaxT, RegBounds<J>::kMinBlocks)
       __syncthreads();
       for (int d = tid; d < G.ndyn; d += T) {
         uint32_t h = 0;
-        for (int s = __ldg(dyo + d); s < __ldg(dyo + d + 1); ++s) h = max(h, pos[__ldg(dys + s)]);
+        const int s1 = __ldg(G.dyn_off + d + 1);
+        for (int s = __ldg(G.dyn_off + d); s < s1; ++s) h = max(h, pos[__ldg(G.dyn_sinks + s)]);
         const int q = (int)(h & 0xffffu);
         if (q < n) {
-          const VT sz = (VT)__ldg(dyz + d);
+          const VT sz = (VT)__ldg(G.dyn_size + d);
           atomicAdd(&XF[q].f, sz);
           atomicAdd(&XF[q].x, (VT)0 - sz);
         }
@@ -170,22 +162,29 @@ __global__ void __launch_bounds__(RegBounds<J>::kMaxT, RegBounds<J>::kMinBlocks)
     if (lane == kWarp - 1) bs.wsum[warp] = incl;
     __syncthreads();
     VT run = warp_sum(lane < warp ? bs.wsum[lane] : (VT)0) + incl - total;
-    VT best = 0;
-    int best_i = INT_MAX;
     const int p0 = tid * P;
+    VT best;
+    int best_i;
     if (bytes_out == nullptr) {
-      // padding entries are (0, 0): their RS never exceeds RS(n-1), so a strict
-      // comparison never lets them replace a real position.
-      for (int i = 0; i < P; ++i) {
-        const XFPair<VT> xf = mine[i];
+      // First element initialises (best, index); strict > keeps the first
+      // maximum. Padding entries are (0, 0): their RS equals S(n-1) <= RS(n-1),
+      // so they never replace a real position.
+      XFPair<VT> xf = mine[0];
+      run += xf.x;
+      best = run + xf.f;
+      best_i = 0;
+      for (int i = 1; i < P; ++i) {
+        xf = mine[i];
         run += xf.x;
         const VT rs = run + xf.f;
-        const bool better = rs > best || best_i == INT_MAX;
+        const bool better = rs > best;
         best = better ? rs : best;
-        best_i = better ? p0 + i : best_i;
+        best_i = better ? i : best_i;
       }
-      if (best_i >= n) best_i = INT_MAX;  // a chunk made only of padding
+      best_i = p0 < n ? p0 + best_i : INT_MAX;  // a chunk made only of padding
     } else {
+      best = 0;
+      best_i = INT_MAX;
       const int lim = min(P, n - p0);
       for (int i = 0; i < lim; ++i) {
         const XFPair<VT> xf = mine[i];
@@ -226,6 +225,6 @@ __global__ void __launch_bounds__(RegBounds<J>::kMaxT, RegBounds<J>::kMinBlocks)
 }
 
 template <typename VT>
-size_t reg_smem_bytes(int n, int T, int P, int nextra, int ndyn, int ndyn_sinks) {
-  return RegLayout<VT>{n, T, P, nextra, ndyn, ndyn_sinks}.total();
+size_t reg_smem_bytes(int n, int T, int P, int J) {
+  return RegLayout<VT>{n, T, P, J}.total();
 }
