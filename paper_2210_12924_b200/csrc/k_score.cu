@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cstdlib>
 #include <cstdint>
 
 #include "mp_internal.h"
@@ -59,10 +60,10 @@ struct ScoreTables {
   const int32_t* __restrict__ dyn_off;
   const int32_t* __restrict__ dyn_sinks;
   const uint64_t* __restrict__ dyn_size;
-  const uint32_t* __restrict__ node_xf32;
-  const uint64_t* __restrict__ node_xf64;
-  const int32_t* __restrict__ node_u;
-  const uint32_t* __restrict__ extra_packed;
+  const uint4* __restrict__ node_rec32;      // (x, f, pred1, pred2), 32-bit graphs
+  const int2* __restrict__ node_u2;          // (pred1, pred2)
+  const uint32_t* __restrict__ extra3_packed;
+  int32_t nextra3;
 };
 
 // Position word: stamp in the high half, position in the low half. Within one
@@ -385,10 +386,10 @@ ScoreTables tables(const mp_graph* g) {
   G.dyn_off = g->d_dyn_off;
   G.dyn_sinks = g->d_dyn_sinks;
   G.dyn_size = g->d_dyn_size;
-  G.node_xf32 = g->d_node_xf32;
-  G.node_xf64 = g->d_node_xf64;
-  G.node_u = g->d_node_u;
-  G.extra_packed = g->d_extra_packed;
+  G.node_rec32 = reinterpret_cast<const uint4*>(g->d_node_rec32);
+  G.node_u2 = reinterpret_cast<const int2*>(g->d_node_u2);
+  G.extra3_packed = g->d_extra3_packed;
+  G.nextra3 = g->n_extra3;
   return G;
 }
 
@@ -467,7 +468,11 @@ mp_status score_configure(mp_graph* g) {
   // when they fit; otherwise node tables from global and/or global scratch.
   const int n = g->n;
   int J = 0, T = 1024;
+  // MP_SCORE_J=4|8|16 forces the slot count (tuning experiments only).
+  const char* force = std::getenv("MP_SCORE_J");
+  const int fj = force ? std::atoi(force) : 0;
   for (int j : {4, 8, 16}) {
+    if (fj && j != fj) continue;
     const int t = ((n + j - 1) / j + 31) / 32 * 32;
     if (t <= (j == 4 ? 256 : j == 8 ? 384 : 512)) {  // RegBounds<J>::kMaxT
       J = j;

@@ -68,28 +68,46 @@ __global__ void __launch_bounds__(RegBounds<J>::kMaxT, RegBounds<J>::kMinBlocks)
   uint32_t real = 0;                          // bit j: slot j is a real node / position
   int ov[J];
   VT rx[J], rf[J];
-  int ru[J];
+  int ru[J], ru2[J];  // pos indexes of the first two reduced producers (TJ+1: none)
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int k = base + kWarp * j;
     const bool in = k < n;
     real |= (in ? 1u : 0u) << j;
-    rx[j] = in ? (VT)__ldg(G.node_x + k) : (VT)0;
-    rf[j] = in ? (VT)__ldg(G.node_f + k) : (VT)0;
-    const int u = in ? __ldg(G.pred1 + k) : -1;
-    ru[j] = u >= 0 ? u : TJ + 1;
+    int u1 = -1, u2 = -1;
+    rx[j] = 0;
+    rf[j] = 0;
+    if (in) {
+      if constexpr (sizeof(VT) == 4) {
+        const uint4 rec = __ldg(G.node_rec32 + k);  // (x, f, pred1, pred2): one load
+        rx[j] = rec.x;
+        rf[j] = rec.y;
+        u1 = (int)rec.z;
+        u2 = (int)rec.w;
+      } else {
+        rx[j] = (VT)__ldg(G.node_x + k);
+        rf[j] = (VT)__ldg(G.node_f + k);
+        const int2 uu = __ldg(G.node_u2 + k);
+        u1 = uu.x;
+        u2 = uu.y;
+      }
+    }
+    ru[j] = u1 >= 0 ? u1 : TJ + 1;
+    ru2[j] = u2 >= 0 ? u2 : TJ + 1;
     ov[j] = k;  // padding slots keep their own index forever
   }
+  const int32_t* nrow = orders + (int64_t)blockIdx.x * n + base;  // row of the next candidate
+  const int64_t rowstep = (int64_t)gridDim.x * n;
   if ((int64_t)blockIdx.x < C) {
-    const int32_t* row = orders + (int64_t)blockIdx.x * n + base;
 #pragma unroll
     for (int j = 0; j < J; ++j)
-      if (real >> j & 1) ov[j] = __ldg(row + kWarp * j);
+      if (real >> j & 1) ov[j] = __ldg(nrow + kWarp * j);
   }
+  nrow += rowstep;
   __syncthreads();
 
   uint32_t stamp = 0;
-  for (int64_t c = blockIdx.x; c < C; c += gridDim.x) {
+  for (int64_t c = blockIdx.x; c < C; c += gridDim.x, nrow += rowstep) {
     if (++stamp > 0xffffu) {
       for (int i = tid; i < (int)L.pos_words(); i += T) pos[i] = 0;
       stamp = 1;
@@ -106,14 +124,10 @@ __global__ void __launch_bounds__(RegBounds<J>::kMaxT, RegBounds<J>::kMinBlocks)
       bad |= ((real >> j) & 1u) & (v >= (uint32_t)n ? 1u : 0u);
       pos[min(v, (uint32_t)TJ)] = tagbase + kWarp * j;
     }
-    {
-      const int64_t cn = c + gridDim.x;  // prefetch the next candidate's slice
-      if (cn < C) {
-        const int32_t* row = orders + cn * n + base;
+    if (c + gridDim.x < C) {  // prefetch the next candidate's slice
 #pragma unroll
-        for (int j = 0; j < J; ++j)
-          if (real >> j & 1) ov[j] = __ldg(row + kWarp * j);
-      }
+      for (int j = 0; j < J; ++j)
+        if (real >> j & 1) ov[j] = __ldg(nrow + kWarp * j);
     }
     __syncthreads();
 
@@ -122,12 +136,14 @@ __global__ void __launch_bounds__(RegBounds<J>::kMaxT, RegBounds<J>::kMinBlocks)
     for (int j = 0; j < J; ++j) {
       const uint32_t w = pos[base + kWarp * j];
       const uint32_t pu = pos[ru[j]];
-      bad |= (w < tag || pu >= w) ? 1u : 0u;  // stale (not a permutation) / producer late
+      const uint32_t pu2 = pos[ru2[j]];
+      // stale word (not a permutation) / a producer not strictly earlier
+      bad |= (w < tag || pu >= w || pu2 >= w) ? 1u : 0u;
       XF[min((int)(w & 0xffffu), TP)] = XFPair<VT>{rx[j], rf[j]};
     }
-    // ---- phase 2b: remaining reduced producer pairs -----------------------------------
-    for (int i = tid; i < G.nextra; i += T) {
-      const uint32_t e = __ldg(G.extra_packed + i);
+    // ---- phase 2b: 3rd+ reduced producer pairs (flat) ----------------------------------
+    for (int i = tid; i < G.nextra3; i += T) {
+      const uint32_t e = __ldg(G.extra3_packed + i);
       bad |= (pos[e & 0xffffu] >= pos[e >> 16]) ? 1u : 0u;
     }
     // ---- phase 2c: order-dependent last consumers -----------------------------------

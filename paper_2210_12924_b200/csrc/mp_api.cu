@@ -254,10 +254,10 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
   up(upload(&g->d_dyn_off, P.dyn_off.data(), P.dyn_off.size(), st));
   up(upload(&g->d_dyn_sinks, P.dyn_sinks.data(), P.dyn_sinks.size(), st));
   up(upload(&g->d_dyn_size, P.dyn_size.data(), P.dyn_size.size(), st));
-  up(upload(&g->d_node_xf32, P.node_xf32.data(), P.node_xf32.size(), st));
-  up(upload(&g->d_node_xf64, P.node_xf64.data(), P.node_xf64.size(), st));
-  up(upload(&g->d_node_u, P.node_u.data(), P.node_u.size(), st));
-  up(upload(&g->d_extra_packed, P.extra_packed.data(), P.extra_packed.size(), st));
+  up(upload(&g->d_node_rec32, P.node_rec32.data(), P.node_rec32.size(), st));
+  up(upload(&g->d_node_u2, P.node_u2.data(), P.node_u2.size(), st));
+  up(upload(&g->d_extra3_packed, P.extra3_packed.data(), P.extra3_packed.size(), st));
+  g->n_extra3 = (int32_t)P.extra3_packed.size();
   if (s == MP_OK) up(score_configure(g));
   if (s == MP_OK) {
     cudaError_t ce = cudaStreamSynchronize(st);  // host tables may go out of scope
@@ -277,7 +277,7 @@ mp_status mp_graph_free(mp_graph* g) {
   void* ptrs[] = {g->d_edge_src, g->d_sink_off,  g->d_sinks,     g->d_edge_size,
                   g->d_node_x,   g->d_node_f,    g->d_pred1,     g->d_extra_u,
                   g->d_extra_w,  g->d_dyn_off,   g->d_dyn_sinks, g->d_dyn_size,
-                  g->d_node_xf32, g->d_node_xf64, g->d_node_u,   g->d_extra_packed};
+                  g->d_node_rec32, g->d_node_u2, g->d_extra3_packed};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete g;

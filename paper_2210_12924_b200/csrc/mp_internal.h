@@ -86,10 +86,10 @@ struct mp_graph {
   int32_t* d_dyn_off = nullptr;      // [n_dyn+1]
   int32_t* d_dyn_sinks = nullptr;    // [n_dyn_sinks]
   uint64_t* d_dyn_size = nullptr;    // [n_dyn] scaled
-  uint32_t* d_node_xf32 = nullptr;   // [2(n+1)] packed (x, f), narrow graphs
-  uint64_t* d_node_xf64 = nullptr;   // [2(n+1)] packed (x, f)
-  int32_t* d_node_u = nullptr;       // [n+1] first producer, n+1 = none
-  uint32_t* d_extra_packed = nullptr;  // [n_extra] u | w << 16 (n < 65536)
+  uint32_t* d_node_rec32 = nullptr;    // [4n] (x, f, pred1, pred2), 32-bit graphs
+  int32_t* d_node_u2 = nullptr;        // [2n] (pred1, pred2)
+  uint32_t* d_extra3_packed = nullptr; // [n_extra3] 3rd+ producer pairs, u | w << 16
+  int32_t n_extra3 = 0;
   int score_j = 0;                   // nodes per thread held in registers (0 = loop variant)
   int score_threads = 1024;
   int score_p = 1;                   // blocked scan chunk per thread (odd)

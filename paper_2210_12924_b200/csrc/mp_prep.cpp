@@ -165,19 +165,29 @@ void prepare_scoring(int32_t n, int32_t E, const int32_t* src, const int64_t* si
     P->node_x[v] = alloc[v] - sfree[v];  // modular; exact after the prefix sum
     P->node_f[v] = sfree[v];
   }
-  P->node_xf32.assign(2 * ((size_t)n + 1), 0);
-  P->node_xf64.assign(2 * ((size_t)n + 1), 0);
-  P->node_u.assign((size_t)n + 1, n + 1);
-  for (int32_t v = 0; v < n; ++v) {
-    P->node_xf32[2 * v] = (uint32_t)P->node_x[v];
-    P->node_xf32[2 * v + 1] = (uint32_t)P->node_f[v];
-    P->node_xf64[2 * v] = P->node_x[v];
-    P->node_xf64[2 * v + 1] = P->node_f[v];
-    if (P->pred1[v] >= 0) P->node_u[v] = P->pred1[v];
+  // second producer per node; the rest (3rd+) as a flat packed list
+  P->pred2.assign(n, -1);
+  {
+    std::vector<int32_t> seen(n, 0);
+    for (size_t i = 0; i < P->extra_u.size(); ++i) {
+      const int32_t u = P->extra_u[i], w = P->extra_w[i];
+      if (seen[w]++ == 0) {
+        P->pred2[w] = u;
+      } else if (n < 65536) {
+        P->extra3_packed.push_back((uint32_t)u | ((uint32_t)w << 16));
+      }
+    }
   }
-  if (n < 65536)
-    for (size_t i = 0; i < P->extra_u.size(); ++i)
-      P->extra_packed.push_back((uint32_t)P->extra_u[i] | ((uint32_t)P->extra_w[i] << 16));
+  P->node_rec32.assign(4 * (size_t)n, 0);
+  P->node_u2.assign(2 * (size_t)n, -1);
+  for (int32_t v = 0; v < n; ++v) {
+    P->node_rec32[4 * v] = (uint32_t)P->node_x[v];
+    P->node_rec32[4 * v + 1] = (uint32_t)P->node_f[v];
+    P->node_rec32[4 * v + 2] = (uint32_t)P->pred1[v];
+    P->node_rec32[4 * v + 3] = (uint32_t)P->pred2[v];
+    P->node_u2[2 * v] = P->pred1[v];
+    P->node_u2[2 * v + 1] = P->pred2[v];
+  }
 }
 
 }  // namespace mpb

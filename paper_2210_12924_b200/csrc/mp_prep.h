@@ -22,11 +22,11 @@ struct ScorePrep {
   std::vector<int32_t> dyn_off{0}, dyn_sinks;
   std::vector<uint64_t> dyn_size;   // scaled
   int64_t num_reduced_preds = 0;
-  // packed forms read by the register-slot scorer (index n = padding node):
-  std::vector<uint32_t> node_xf32;   // [2(n+1)] (x, f) pairs, 32-bit (narrow graphs)
-  std::vector<uint64_t> node_xf64;   // [2(n+1)] (x, f) pairs, 64-bit
-  std::vector<int32_t> node_u;       // [n+1] first producer, n+1 = none
-  std::vector<uint32_t> extra_packed;  // u | w << 16 (n < 65536)
+  // packed forms read by the register-slot scorer:
+  std::vector<int32_t> pred2;          // second reduced producer of each node, -1 if none
+  std::vector<uint32_t> node_rec32;    // [4n] (x, f, pred1, pred2) for 32-bit graphs
+  std::vector<int32_t> node_u2;        // [2n] (pred1, pred2) for 64-bit graphs
+  std::vector<uint32_t> extra3_packed; // 3rd+ reduced producer pairs, u | w << 16 (n < 65536)
 };
 
 void prepare_scoring(int32_t n, int32_t E, const int32_t* src, const int64_t* sink_off,
