@@ -427,19 +427,20 @@ mp_status run(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d
   return MP_OK;
 }
 
-template <typename VT, int J>
+template <typename VT, int J, int KC>
 mp_status run_reg(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d_peak,
                   int32_t* d_step, uint8_t* d_valid, uint64_t* d_bytes, uint64_t* d_key,
                   int64_t index_base, cudaStream_t st) {
-  auto kern = score_reg_kernel<VT, J>;
+  auto kern = score_reg_kernel<VT, J, KC>;
   const int T = g->score_threads;
-  const size_t smem = reg_smem_bytes<VT>(g->n, T, g->score_p, J);
+  const size_t smem = reg_smem_bytes<VT>(g->n, T, g->score_p, J, KC);
 
   MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem));
   int64_t grid = (int64_t)g->ctx->num_sms * (per_sm > 0 ? per_sm : 1);
-  if (grid > C) grid = C;
+  const int64_t groups = (C + KC - 1) / KC;
+  if (grid > groups) grid = groups;
   kern<<<(unsigned)grid, T, smem, st>>>(tables(g), d_orders, C, d_peak, d_step, d_valid, d_bytes,
                                         reinterpret_cast<unsigned long long*>(d_key), index_base);
   MP_CUDA(cudaGetLastError());
@@ -450,9 +451,15 @@ template <typename VT>
 mp_status dispatch(const mp_graph* g, const int32_t* o, int64_t C, uint64_t* pk, int32_t* stp,
                    uint8_t* vl, uint64_t* by, uint64_t* key, int64_t base, cudaStream_t st) {
   switch (g->score_j) {
-    case 4: return run_reg<VT, 4>(g, o, C, pk, stp, vl, by, key, base, st);
-    case 8: return run_reg<VT, 8>(g, o, C, pk, stp, vl, by, key, base, st);
-    case 16: return run_reg<VT, 16>(g, o, C, pk, stp, vl, by, key, base, st);
+    case 4:
+      if (g->score_kc == 2) return run_reg<VT, 4, 2>(g, o, C, pk, stp, vl, by, key, base, st);
+      return run_reg<VT, 4, 1>(g, o, C, pk, stp, vl, by, key, base, st);
+    case 8:
+      if (g->score_kc == 2) return run_reg<VT, 8, 2>(g, o, C, pk, stp, vl, by, key, base, st);
+      return run_reg<VT, 8, 1>(g, o, C, pk, stp, vl, by, key, base, st);
+    case 16:
+      if (g->score_kc == 2) return run_reg<VT, 16, 2>(g, o, C, pk, stp, vl, by, key, base, st);
+      return run_reg<VT, 16, 1>(g, o, C, pk, stp, vl, by, key, base, st);
     default:
       if (g->smem_resident)
         return run<VT, uint32_t, 0, true>(g, o, C, pk, stp, vl, by, key, base, st);
@@ -491,9 +498,17 @@ mp_status score_configure(mp_graph* g) {
                      : Layout<unsigned long long, uint32_t>::bytes(
                            n, t, chunk(t), g->n_extra, g->n_dyn, g->n_dyn_sinks, true);
   };
-  const size_t need_reg = J == 0 ? 0
-                         : g->narrow ? reg_smem_bytes<uint32_t>(n, T, chunk(T), J)
-                                     : reg_smem_bytes<unsigned long long>(n, T, chunk(T), J);
+  // candidates scored together per CTA iteration (MP_SCORE_KC=1|2 forces it)
+  const char* fkc = std::getenv("MP_SCORE_KC");
+  int KC = fkc ? std::atoi(fkc) : 2;
+  if (KC != 1 && KC != 2) KC = 2;
+  auto reg_need = [&](int kc) {
+    return g->narrow ? reg_smem_bytes<uint32_t>(n, T, chunk(T), J, kc)
+                     : reg_smem_bytes<unsigned long long>(n, T, chunk(T), J, kc);
+  };
+  if (J > 0 && KC == 2 && reg_need(2) + 2048 > g->ctx->max_smem_optin) KC = 1;
+  if (J == 8 && KC == 2 && T > 320) KC = 1;  // RegBounds<8, 2>::kMaxT
+  const size_t need_reg = J == 0 ? 0 : reg_need(KC);
 
 
   if (J > 0 && need_reg + 2048 > g->ctx->max_smem_optin) J = 0;
@@ -503,6 +518,7 @@ mp_status score_configure(mp_graph* g) {
   if (J == 0) T = 1024;
   if (J == 0 && !smem) smem = false;
   g->score_j = J;
+  g->score_kc = KC;
   g->score_threads = T;
   g->score_p = chunk(T);
   g->smem_resident = smem;

@@ -4,8 +4,10 @@
 // Slot j of a thread covers order position AND node k = (warp*J + j)*32 + lane,
 // k < TJ = T*J: warp-contiguous, so global loads coalesce and every per-slot
 // shared-memory address is the thread's base plus an immediate. Per slot the
-// thread keeps in registers: the next candidate's order value ov, the node's
-// static bytes (x, f) and the pos index of its first reduced producer.
+// thread keeps in registers the node's static bytes (x, f) and the pos
+// indexes of its first two reduced producers - shared by KC candidates that
+// the CTA scores together (KC independent chains per barrier and per
+// instruction stream), each with its own order registers and smem buffers.
 //
 // Padding slots (k >= n) behave as inert nodes instead of branching: they
 // write pos[k] = tag|k in phase 1 (so they read back fresh), carry x = f = 0
@@ -25,25 +27,34 @@ struct RegLayout {
   __host__ __device__ size_t xf_bytes() const {
     return ((size_t)(T * P + 1) * sizeof(XFPair<VT>) + 15) & ~size_t(15);
   }
-  __host__ __device__ size_t total() const { return pos_bytes() + xf_bytes() + 16; }
+  __host__ __device__ size_t per_candidate() const { return pos_bytes() + xf_bytes(); }
 };
 
-// Register budgets per slot count: J=4 -> T <= 256, 64 regs; J=8 -> T <= 384,
-// 85 regs; J=16 -> T <= 512, 128 regs (score_configure picks the smallest J).
-template <int J>
+// Register budgets (65536 / (kMaxT * kMinBlocks) per thread):
+//   J=4: T <= 256, 64 regs (KC=1) / 85 (KC=2);  J=8: T <= 384, 85 (KC=1) / 102 (KC=2, T <= 320)
+//   J=16: T <= 512, 128.  score_configure picks T within kMaxT.
+template <int J, int KC>
 struct RegBounds {
-  static constexpr int kMaxT = J == 4 ? 256 : J == 8 ? 384 : 512;
-  static constexpr int kMinBlocks = J == 4 ? 4 : J == 8 ? 2 : 1;
+  static constexpr int kMaxT = J == 4 ? 256 : J == 8 ? (KC == 1 ? 384 : 320) : 512;
+  static constexpr int kMinBlocks = J == 4 ? (KC == 1 ? 4 : 3) : J == 8 ? 2 : 1;
 };
 
-template <typename VT, int J>
-__global__ void __launch_bounds__(RegBounds<J>::kMaxT, RegBounds<J>::kMinBlocks)
+template <typename VT, int KC>
+struct RegScratch {
+  VT wsum[KC][32];
+  VT wbest[KC][32];
+  int widx[KC][32];
+  uint32_t bad[2];  // per-iteration-parity bitmask of invalid candidates
+};
+
+template <typename VT, int J, int KC>
+__global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMinBlocks)
     score_reg_kernel(ScoreTables G, const int32_t* __restrict__ orders, int64_t C,
                      uint64_t* __restrict__ peak_out, int32_t* __restrict__ step_out,
                      uint8_t* __restrict__ valid_out, uint64_t* __restrict__ bytes_out,
                      unsigned long long* __restrict__ best_key, int64_t index_base) {
   extern __shared__ __align__(16) char smem[];
-  __shared__ BlockScratch<VT> bs;
+  __shared__ RegScratch<VT, KC> bs;
 
   const int n = G.n;
   const int T = blockDim.x;
@@ -56,184 +67,229 @@ __global__ void __launch_bounds__(RegBounds<J>::kMaxT, RegBounds<J>::kMinBlocks)
   const RegLayout<VT> L{n, T, P, J};
   const int TJ = L.TJ();
 
-  uint32_t* pos = reinterpret_cast<uint32_t*>(smem);
-  XFPair<VT>* XF = reinterpret_cast<XFPair<VT>*>(smem + L.pos_bytes());
-  {
-    uint4* z = reinterpret_cast<uint4*>(pos);  // pos = 0: stamp 0 is never used
+  uint32_t* pos[KC];
+  XFPair<VT>* XF[KC];
+#pragma unroll
+  for (int k = 0; k < KC; ++k) {
+    char* b = smem + k * L.per_candidate();
+    pos[k] = reinterpret_cast<uint32_t*>(b);
+    XF[k] = reinterpret_cast<XFPair<VT>*>(b + L.pos_bytes());
+    uint4* z = reinterpret_cast<uint4*>(pos[k]);  // pos = 0: stamp 0 is never used
     for (int i = tid; i < (int)(L.pos_words() / 4); i += T) z[i] = make_uint4(0, 0, 0, 0);
-    for (int i = n + tid; i <= TP; i += T) XF[i] = XFPair<VT>{0, 0};  // scan padding
+    for (int i = n + tid; i <= TP; i += T) XF[k][i] = XFPair<VT>{0, 0};  // scan padding
   }
+  if (tid < 2) bs.bad[tid] = 0;
 
   const int base = warp * J * kWarp + lane;  // slot j: k = base + 32*j
   uint32_t real = 0;                          // bit j: slot j is a real node / position
-  int ov[J];
   VT rx[J], rf[J];
   int ru[J], ru2[J];  // pos indexes of the first two reduced producers (TJ+1: none)
 #pragma unroll
   for (int j = 0; j < J; ++j) {
-    const int k = base + kWarp * j;
-    const bool in = k < n;
+    const int v = base + kWarp * j;
+    const bool in = v < n;
     real |= (in ? 1u : 0u) << j;
     int u1 = -1, u2 = -1;
     rx[j] = 0;
     rf[j] = 0;
     if (in) {
       if constexpr (sizeof(VT) == 4) {
-        const uint4 rec = __ldg(G.node_rec32 + k);  // (x, f, pred1, pred2): one load
+        const uint4 rec = __ldg(G.node_rec32 + v);  // (x, f, pred1, pred2): one load
         rx[j] = rec.x;
         rf[j] = rec.y;
         u1 = (int)rec.z;
         u2 = (int)rec.w;
       } else {
-        rx[j] = (VT)__ldg(G.node_x + k);
-        rf[j] = (VT)__ldg(G.node_f + k);
-        const int2 uu = __ldg(G.node_u2 + k);
+        rx[j] = (VT)__ldg(G.node_x + v);
+        rf[j] = (VT)__ldg(G.node_f + v);
+        const int2 uu = __ldg(G.node_u2 + v);
         u1 = uu.x;
         u2 = uu.y;
       }
     }
     ru[j] = u1 >= 0 ? u1 : TJ + 1;
     ru2[j] = u2 >= 0 ? u2 : TJ + 1;
-    ov[j] = k;  // padding slots keep their own index forever
   }
-  const int32_t* nrow = orders + (int64_t)blockIdx.x * n + base;  // row of the next candidate
-  const int64_t rowstep = (int64_t)gridDim.x * n;
-  if ((int64_t)blockIdx.x < C) {
+
+  // Candidate groups: group g covers candidates [g*KC, g*KC + KC).
+  const int64_t ngroups = (C + KC - 1) / KC;
+  int ov[KC][J];
+  auto load_group = [&](int64_t g) {
 #pragma unroll
-    for (int j = 0; j < J; ++j)
-      if (real >> j & 1) ov[j] = __ldg(nrow + kWarp * j);
-  }
-  nrow += rowstep;
+    for (int k = 0; k < KC; ++k) {
+      const int64_t c = g * KC + k;
+      const int32_t* row = orders + c * n + base;
+#pragma unroll
+      for (int j = 0; j < J; ++j)
+        ov[k][j] = ((real >> j & 1) && c < C) ? __ldg(row + kWarp * j) : base + kWarp * j;
+    }
+  };
+  if ((int64_t)blockIdx.x < ngroups) load_group(blockIdx.x);
   __syncthreads();
 
   uint32_t stamp = 0;
-  for (int64_t c = blockIdx.x; c < C; c += gridDim.x, nrow += rowstep) {
+  int parity = 0;
+  for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x, parity ^= 1) {
     if (++stamp > 0xffffu) {
-      for (int i = tid; i < (int)L.pos_words(); i += T) pos[i] = 0;
+      for (int k = 0; k < KC; ++k)
+        for (int i = tid; i < (int)L.pos_words(); i += T) pos[k][i] = 0;
       stamp = 1;
       __syncthreads();
     }
     const uint32_t tag = stamp << 16;
     const uint32_t tagbase = tag + (uint32_t)base;
-    uint32_t bad = 0;
+    uint32_t bad = 0;  // bit k: candidate k of the group is invalid
 
     // ---- phase 1: pos[order[k]] = tag | k --------------------------------------------
 #pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const uint32_t v = (uint32_t)ov[j];
-      bad |= ((real >> j) & 1u) & (v >= (uint32_t)n ? 1u : 0u);
-      pos[min(v, (uint32_t)TJ)] = tagbase + kWarp * j;
-    }
-    if (c + gridDim.x < C) {  // prefetch the next candidate's slice
+    for (int k = 0; k < KC; ++k)
 #pragma unroll
-      for (int j = 0; j < J; ++j)
-        if (real >> j & 1) ov[j] = __ldg(nrow + kWarp * j);
-    }
+      for (int j = 0; j < J; ++j) {
+        const uint32_t v = (uint32_t)ov[k][j];
+        bad |= (((real >> j) & 1u) & (v >= (uint32_t)n ? 1u : 0u)) << k;
+        pos[k][min(v, (uint32_t)TJ)] = tagbase + kWarp * j;
+      }
+    if (g + gridDim.x < ngroups) load_group(g + gridDim.x);  // lands while this group is scored
     __syncthreads();
 
     // ---- phase 2a: node slots -----------------------------------------------------------
 #pragma unroll
     for (int j = 0; j < J; ++j) {
-      const uint32_t w = pos[base + kWarp * j];
-      const uint32_t pu = pos[ru[j]];
-      const uint32_t pu2 = pos[ru2[j]];
-      // stale word (not a permutation) / a producer not strictly earlier
-      bad |= (w < tag || pu >= w || pu2 >= w) ? 1u : 0u;
-      XF[min((int)(w & 0xffffu), TP)] = XFPair<VT>{rx[j], rf[j]};
+      const int v = base + kWarp * j;
+#pragma unroll
+      for (int k = 0; k < KC; ++k) {
+        const uint32_t w = pos[k][v];
+        const uint32_t pu = pos[k][ru[j]];
+        const uint32_t pu2 = pos[k][ru2[j]];
+        // stale word (not a permutation) / a producer not strictly earlier
+        bad |= ((w < tag || pu >= w || pu2 >= w) ? 1u : 0u) << k;
+        XF[k][min((int)(w & 0xffffu), TP)] = XFPair<VT>{rx[j], rf[j]};
+      }
     }
     // ---- phase 2b: 3rd+ reduced producer pairs (flat) ----------------------------------
     for (int i = tid; i < G.nextra3; i += T) {
       const uint32_t e = __ldg(G.extra3_packed + i);
-      bad |= (pos[e & 0xffffu] >= pos[e >> 16]) ? 1u : 0u;
+#pragma unroll
+      for (int k = 0; k < KC; ++k)
+        bad |= ((pos[k][e & 0xffffu] >= pos[k][e >> 16]) ? 1u : 0u) << k;
     }
     // ---- phase 2c: order-dependent last consumers -----------------------------------
     if (G.ndyn > 0) {
       __syncthreads();
       for (int d = tid; d < G.ndyn; d += T) {
-        uint32_t h = 0;
+        uint32_t h[KC];
+#pragma unroll
+        for (int k = 0; k < KC; ++k) h[k] = 0;
         const int s1 = __ldg(G.dyn_off + d + 1);
-        for (int s = __ldg(G.dyn_off + d); s < s1; ++s) h = max(h, pos[__ldg(G.dyn_sinks + s)]);
-        const int q = (int)(h & 0xffffu);
-        if (q < n) {
-          const VT sz = (VT)__ldg(G.dyn_size + d);
-          atomicAdd(&XF[q].f, sz);
-          atomicAdd(&XF[q].x, (VT)0 - sz);
+        for (int s = __ldg(G.dyn_off + d); s < s1; ++s) {
+          const int x = __ldg(G.dyn_sinks + s);
+#pragma unroll
+          for (int k = 0; k < KC; ++k) h[k] = max(h[k], pos[k][x]);
+        }
+        const VT sz = (VT)__ldg(G.dyn_size + d);
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+          const int q = (int)(h[k] & 0xffffu);
+          if (q < n) {
+            atomicAdd(&XF[k][q].f, sz);
+            atomicAdd(&XF[k][q].x, (VT)0 - sz);
+          }
         }
       }
     }
-    if (__syncthreads_or(bad)) {
-      if (tid == 0) {
-        peak_out[c] = 0;
-        step_out[c] = 0;
-        valid_out[c] = 0;
-      }
-      continue;
+    // per-candidate verdicts: warp ballots, one atomicOr per warp that saw any
+    {
+      uint32_t wb = 0;
+#pragma unroll
+      for (int k = 0; k < KC; ++k) wb |= (__ballot_sync(0xffffffffu, (bad >> k) & 1u) ? 1u : 0u) << k;
+      if (lane == 0 && wb) atomicOr(&bs.bad[parity], wb);
     }
+    __syncthreads();
+    const uint32_t badmask = bs.bad[parity];
+    const int64_t c0 = g * KC;
 
     // ---- phase 3: blocked two-pass scan over [tid*P, tid*P + P), P odd -------------
-    const XFPair<VT>* mine = XF + tid * P;
-    VT total = 0;
-    for (int i = 0; i < P; ++i) total += mine[i].x;
-    const VT incl = warp_incl_scan(total, lane);
-    if (lane == kWarp - 1) bs.wsum[warp] = incl;
-    __syncthreads();
-    VT run = warp_sum(lane < warp ? bs.wsum[lane] : (VT)0) + incl - total;
+    VT run[KC], best[KC];
+    int best_i[KC];
     const int p0 = tid * P;
-    VT best;
-    int best_i;
-    if (bytes_out == nullptr) {
-      // First element initialises (best, index); strict > keeps the first
-      // maximum. Padding entries are (0, 0): their RS equals S(n-1) <= RS(n-1),
-      // so they never replace a real position.
-      XFPair<VT> xf = mine[0];
-      run += xf.x;
-      best = run + xf.f;
-      best_i = 0;
-      for (int i = 1; i < P; ++i) {
-        xf = mine[i];
-        run += xf.x;
-        const VT rs = run + xf.f;
-        const bool better = rs > best;
-        best = better ? rs : best;
-        best_i = better ? i : best_i;
-      }
-      best_i = p0 < n ? p0 + best_i : INT_MAX;  // a chunk made only of padding
-    } else {
-      best = 0;
-      best_i = INT_MAX;
-      const int lim = min(P, n - p0);
-      for (int i = 0; i < lim; ++i) {
-        const XFPair<VT> xf = mine[i];
-        run += xf.x;
-        const VT rs = run + xf.f;
-        bytes_out[c * n + p0 + i] = (uint64_t)rs * G.scale;
-        if (rs > best || best_i == INT_MAX) {
-          best = rs;
-          best_i = p0 + i;
-        }
-      }
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+      const XFPair<VT>* mine = XF[k] + p0;
+      VT total = 0;
+      for (int i = 0; i < P; ++i) total += mine[i].x;
+      const VT incl = warp_incl_scan(total, lane);
+      if (lane == kWarp - 1) bs.wsum[k][warp] = incl;
+      run[k] = incl - total;
     }
-    warp_argmax(best, best_i);
-    if (lane == 0) {
-      bs.wbest[warp] = best;
-      bs.widx[warp] = best_i;
+    __syncthreads();
+    if (tid == 0) bs.bad[parity ^ 1] = 0;  // next iteration's flags (last read a barrier ago)
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+      run[k] += warp_sum(lane < warp ? bs.wsum[k][lane] : (VT)0);
+      const XFPair<VT>* mine = XF[k] + p0;
+      if (bytes_out == nullptr) {
+        // First element initialises (best, index); strict > keeps the first
+        // maximum. Padding entries are (0, 0): their RS equals S(n-1) <= RS(n-1),
+        // so they never replace a real position.
+        XFPair<VT> xf = mine[0];
+        VT r = run[k] + xf.x;
+        VT b = r + xf.f;
+        int bi = 0;
+        for (int i = 1; i < P; ++i) {
+          xf = mine[i];
+          r += xf.x;
+          const VT rs = r + xf.f;
+          const bool better = rs > b;
+          b = better ? rs : b;
+          bi = better ? i : bi;
+        }
+        best[k] = b;
+        best_i[k] = p0 < n ? p0 + bi : INT_MAX;  // a chunk made only of padding
+      } else {
+        VT r = run[k], b = 0;
+        int bi = INT_MAX;
+        const int64_t c = c0 + k;
+        const int lim = min(P, n - p0);
+        for (int i = 0; i < lim; ++i) {
+          const XFPair<VT> xf = mine[i];
+          r += xf.x;
+          const VT rs = r + xf.f;
+          if (c < C) bytes_out[c * n + p0 + i] = (uint64_t)rs * G.scale;
+          if (rs > b || bi == INT_MAX) {
+            b = rs;
+            bi = p0 + i;
+          }
+        }
+        best[k] = b;
+        best_i[k] = bi;
+      }
+      warp_argmax(best[k], best_i[k]);
+      if (lane == 0) {
+        bs.wbest[k][warp] = best[k];
+        bs.widx[k][warp] = best_i[k];
+      }
     }
     __syncthreads();
     if (warp == 0) {
-      best = lane < nwarps ? bs.wbest[lane] : (VT)0;
-      best_i = lane < nwarps ? bs.widx[lane] : INT_MAX;
-      warp_argmax(best, best_i);
-      if (lane == 0) {
-        const bool empty = n == 0;
-        const uint64_t pk = empty ? 0 : (uint64_t)best * G.scale;
-        peak_out[c] = pk;
-        step_out[c] = empty ? 0 : best_i + 1;
-        valid_out[c] = 1;
-        if (best_key) {
-          const uint64_t gi = (uint64_t)(c + index_base);
-          const unsigned long long key =
-              (pk < (1ull << 43) && gi < (1ull << 20)) ? ((pk << 20) | gi) : kKeyOverflow;
-          atomicMin(best_key, key);
+#pragma unroll
+      for (int k = 0; k < KC; ++k) {
+        VT b = lane < nwarps ? bs.wbest[k][lane] : (VT)0;
+        int bi = lane < nwarps ? bs.widx[k][lane] : INT_MAX;
+        warp_argmax(b, bi);
+        const int64_t c = c0 + k;
+        if (lane == 0 && c < C) {
+          const bool ok = !((badmask >> k) & 1u);
+          const bool empty = n == 0;
+          const uint64_t pk = (!ok || empty) ? 0 : (uint64_t)b * G.scale;
+          peak_out[c] = pk;
+          step_out[c] = (!ok || empty) ? 0 : bi + 1;
+          valid_out[c] = ok ? 1 : 0;
+          if (best_key && ok) {
+            const uint64_t gi = (uint64_t)(c + index_base);
+            const unsigned long long key =
+                (pk < (1ull << 43) && gi < (1ull << 20)) ? ((pk << 20) | gi) : kKeyOverflow;
+            atomicMin(best_key, key);
+          }
         }
       }
     }
@@ -241,6 +297,6 @@ __global__ void __launch_bounds__(RegBounds<J>::kMaxT, RegBounds<J>::kMinBlocks)
 }
 
 template <typename VT>
-size_t reg_smem_bytes(int n, int T, int P, int J) {
-  return RegLayout<VT>{n, T, P, J}.total();
+size_t reg_smem_bytes(int n, int T, int P, int J, int KC) {
+  return RegLayout<VT>{n, T, P, J}.per_candidate() * KC + 16;
 }

@@ -92,6 +92,7 @@ struct mp_graph {
   int32_t n_extra3 = 0;
   int score_j = 0;                   // nodes per thread held in registers (0 = loop variant)
   int score_threads = 1024;
+  int score_kc = 1;                  // candidates per CTA iteration (register variant)
   int score_p = 1;                   // blocked scan chunk per thread (odd)
 
   // first node that misses a timestep in realized_lifetimes is searched on
