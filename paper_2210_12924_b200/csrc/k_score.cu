@@ -33,6 +33,7 @@
 #include <climits>
 #include <cstdlib>
 #include <cstdint>
+#include <string>
 
 #include "mp_internal.h"
 
@@ -369,6 +370,7 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
 }
 
 #include "k_score_reg.cuh"
+#include "k_score_warp.cuh"
 
 ScoreTables tables(const mp_graph* g) {
   ScoreTables G;
@@ -448,8 +450,31 @@ mp_status run_reg(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_
 }
 
 template <typename VT>
+mp_status run_warp(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d_peak,
+                   int32_t* d_step, uint8_t* d_valid, uint64_t* d_bytes, uint64_t* d_key,
+                   int64_t index_base, cudaStream_t st) {
+  auto kern = score_warp_kernel<VT>;
+  const int W = g->score_warps;
+  const size_t smem = warp_smem_bytes<VT>(g->n, g->score_wp, W);
+  MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * W, smem));
+  int64_t grid = (int64_t)g->ctx->num_sms * (per_sm > 0 ? per_sm : 1);
+  const int64_t need = (C + W - 1) / W;
+  if (grid > need) grid = need;
+  ScoreTables G = tables(g);
+  G.P = g->score_wp;
+  kern<<<(unsigned)grid, 32 * W, smem, st>>>(G, d_orders, C, d_peak, d_step, d_valid, d_bytes,
+                                             reinterpret_cast<unsigned long long*>(d_key),
+                                             index_base);
+  MP_CUDA(cudaGetLastError());
+  return MP_OK;
+}
+
+template <typename VT>
 mp_status dispatch(const mp_graph* g, const int32_t* o, int64_t C, uint64_t* pk, int32_t* stp,
                    uint8_t* vl, uint64_t* by, uint64_t* key, int64_t base, cudaStream_t st) {
+  if (g->score_warps > 0) return run_warp<VT>(g, o, C, pk, stp, vl, by, key, base, st);
   switch (g->score_j) {
     case 4:
       if (g->score_kc == 2) return run_reg<VT, 4, 2>(g, o, C, pk, stp, vl, by, key, base, st);
@@ -517,6 +542,23 @@ mp_status score_configure(mp_graph* g) {
   if (J > 0) smem = true;
   if (J == 0) T = 1024;
   if (J == 0 && !smem) smem = false;
+  // Warp-per-candidate variant for small graphs (MP_SCORE_MODE=cta|warp forces it):
+  // as many warps per CTA as the per-warp buffers allow, up to 16.
+  g->score_warps = 0;
+  const char* mode = std::getenv("MP_SCORE_MODE");
+  const bool want_warp = mode ? std::string(mode) == "warp" : n <= kWarpMaxNodes;
+  if (want_warp && n > 0 && n < 65535) {
+    const int wp = ((n + 31) / 32) | 1;
+    g->score_wp = wp;
+    for (int w = 16; w >= 1; --w) {
+      const size_t b = g->narrow ? warp_smem_bytes<uint32_t>(n, wp, w)
+                                 : warp_smem_bytes<unsigned long long>(n, wp, w);
+      if (b + 1024 <= g->ctx->max_smem_optin) {
+        g->score_warps = w;
+        break;
+      }
+    }
+  }
   g->score_j = J;
   g->score_kc = KC;
   g->score_threads = T;

@@ -93,6 +93,8 @@ struct mp_graph {
   int score_j = 0;                   // nodes per thread held in registers (0 = loop variant)
   int score_threads = 1024;
   int score_kc = 1;                  // candidates per CTA iteration (register variant)
+  int score_warps = 0;               // >0: warp-per-candidate variant, warps per CTA
+  int score_wp = 1;                  // its per-lane scan chunk (odd)
   int score_p = 1;                   // blocked scan chunk per thread (odd)
 
   // first node that misses a timestep in realized_lifetimes is searched on

@@ -228,6 +228,32 @@ def test_model_graphs_vs_oracle(planner, name):
     assert (b == orc.resident_bytes_per_step(orders[1])).all()
 
 
+@pytest.mark.parametrize("mode", ["warp", "cta"])
+@pytest.mark.parametrize("kind,layers,size,seed", [("training_like", 40, 8, 0),
+                                                   ("fork_join", 150, 1 << 34, 2),
+                                                   ("training_like", 300, 1000, 0)])
+def test_scorer_variants_small_graphs(planner, monkeypatch, mode, kind, layers, size, seed):
+    """Both small-graph scorer variants (warp-per-candidate, CTA register slots),
+    32-bit and 64-bit value paths, valid and invalid candidates, vs the oracle."""
+    monkeypatch.setenv("MP_SCORE_MODE", mode)
+    g = mp.generate_graph(kind, layers, size, seed)   # fresh object -> fresh upload
+    orc = O.Oracle.from_csr(g.csr())
+    orders = mp.random_topo_orders(g, 37, seed=seed + 5)
+    orders[3, [1, 2]] = orders[3, [2, 1]]
+    orders[7, 4] = orders[7, 9]
+    orders[9, 0] = g.n
+    res = planner.score_orders(g, orders)
+    for i, o in enumerate(orders):
+        lt = orc.lifetimes_from_order(o)
+        if lt is None:
+            assert res.valid[i] == 0
+            continue
+        _, pr, ps = orc.timeline_from_lifetimes(lt[0], lt[1], g.n)
+        assert res.valid[i] == 1 and (int(res.peak[i]), int(res.peak_step[i])) == (pr, ps), i
+    assert (planner.resident_bytes_per_step(g, orders[0]) ==
+            orc.resident_bytes_per_step(orders[0])).all()
+
+
 @pytest.mark.parametrize("layers,smem", [(3000, 1), (20000, 0)])
 def test_large_graph_variants(planner, layers, smem):
     """Graphs past the register-resident variant: node tables read per candidate,
