@@ -525,8 +525,8 @@ mp_status score_configure(mp_graph* g) {
   };
   // candidates scored together per CTA iteration (MP_SCORE_KC=1|2 forces it)
   const char* fkc = std::getenv("MP_SCORE_KC");
-  int KC = fkc ? std::atoi(fkc) : 2;
-  if (KC != 1 && KC != 2) KC = 2;
+  int KC = fkc ? std::atoi(fkc) : 1;
+  if (KC != 1 && KC != 2) KC = 1;
   auto reg_need = [&](int kc) {
     return g->narrow ? reg_smem_bytes<uint32_t>(n, T, chunk(T), J, kc)
                      : reg_smem_bytes<unsigned long long>(n, T, chunk(T), J, kc);

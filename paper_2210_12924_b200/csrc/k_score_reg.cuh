@@ -153,17 +153,22 @@ __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMi
     __syncthreads();
 
     // ---- phase 2a: node slots -----------------------------------------------------------
+    // all loads of the slots first, then the scatters (pos and XF alias as far
+    // as the compiler knows, so it would not hoist a load above a store)
 #pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int v = base + kWarp * j;
+    for (int k = 0; k < KC; ++k) {
+      uint32_t w[J], pu[J], pu2[J];
 #pragma unroll
-      for (int k = 0; k < KC; ++k) {
-        const uint32_t w = pos[k][v];
-        const uint32_t pu = pos[k][ru[j]];
-        const uint32_t pu2 = pos[k][ru2[j]];
+      for (int j = 0; j < J; ++j) {
+        w[j] = pos[k][base + kWarp * j];
+        pu[j] = pos[k][ru[j]];
+        pu2[j] = pos[k][ru2[j]];
+      }
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
         // stale word (not a permutation) / a producer not strictly earlier
-        bad |= ((w < tag || pu >= w || pu2 >= w) ? 1u : 0u) << k;
-        XF[k][min((int)(w & 0xffffu), TP)] = XFPair<VT>{rx[j], rf[j]};
+        bad |= ((w[j] < tag || pu[j] >= w[j] || pu2[j] >= w[j]) ? 1u : 0u) << k;
+        XF[k][min((int)(w[j] & 0xffffu), TP)] = XFPair<VT>{rx[j], rf[j]};
       }
     }
     // ---- phase 2b: 3rd+ reduced producer pairs (flat) ----------------------------------

@@ -99,30 +99,55 @@ __global__ void __launch_bounds__(512)
     __syncwarp();
 
     // ---- phase 1: pos[order[k]] = tag | k ------------------------------------------
-    for (int k = lane; k < n; k += 32) {
-      const uint32_t v = (uint32_t)buf[k];
-      bad |= v >= (uint32_t)n ? 1u : 0u;
-      pos[min(v, (uint32_t)n)] = tag | (uint32_t)k;
+    // Batches of kB: every load of a batch is issued before any store (the
+    // buffers alias as far as the compiler knows, so it would not reorder).
+    constexpr int kB = 8;
+    for (int k0 = lane; k0 < n; k0 += 32 * kB) {
+      uint32_t v[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int k = k0 + 32 * u;
+        v[u] = k < n ? (uint32_t)buf[k] : (uint32_t)n;  // past the end: absorb slot
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int k = k0 + 32 * u;
+        bad |= (k < n && v[u] >= (uint32_t)n) ? 1u : 0u;
+        pos[min(v[u], (uint32_t)n)] = tag | (uint32_t)k;
+      }
     }
     __syncwarp();  // buf consumed, pos written
     {
       const int64_t cn = c + wstride;  // prefetch the next candidate's row
       if (cn < C) {
         const int32_t* row = orders + cn * n;
+#pragma unroll 8
         for (int k = lane; k < n; k += 32) cp_async4(buf + k, row + k);
       }
       cp_async_commit();
     }
 
     // ---- phase 2a: node space ---------------------------------------------------------
-    for (int v = lane; v < n; v += 32) {
-      const uint32_t w = pos[v];
-      const uint32_t pp = NP[v];
-      const uint32_t a = pp & 0xffffu, b = pp >> 16;
-      const uint32_t pu = pos[a == 0xffffu ? none : a];
-      const uint32_t pu2 = pos[b == 0xffffu ? none : b];
-      bad |= (w < tag || pu >= w || pu2 >= w) ? 1u : 0u;
-      XF[min((int)(w & 0xffffu), TP)] = NX[v];
+    for (int v0 = lane; v0 < n; v0 += 32 * kB) {
+      uint32_t w[kB], pu[kB], pu2[kB];
+      XFPair<VT> nx[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int v = min(v0 + 32 * u, n);  // past the end: node n (pos[n] absorbs)
+        w[u] = pos[v];
+        const uint32_t pp = NP[v];
+        nx[u] = NX[v];
+        const uint32_t a = pp & 0xffffu, b = pp >> 16;
+        pu[u] = pos[a == 0xffffu ? none : a];
+        pu2[u] = pos[b == 0xffffu ? none : b];
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        if (v0 + 32 * u < n) {
+          bad |= (w[u] < tag || pu[u] >= w[u] || pu2[u] >= w[u]) ? 1u : 0u;
+          XF[min((int)(w[u] & 0xffffu), TP)] = nx[u];
+        }
+      }
     }
     // ---- phase 2b: 3rd+ reduced producer pairs ------------------------------------------
     for (int i = lane; i < G.nextra3; i += 32) {
@@ -150,6 +175,7 @@ __global__ void __launch_bounds__(512)
     // ---- phase 3: lane-blocked two-pass scan over [lane*P, lane*P + P), P odd -------
     const XFPair<VT>* ch = XF + lane * P;
     VT total = 0;
+#pragma unroll 8
     for (int i = 0; i < P; ++i) total += ch[i].x;
     const VT incl = warp_incl_scan(total, lane);
     VT r = incl - total;
@@ -161,6 +187,7 @@ __global__ void __launch_bounds__(512)
       r += xf.x;
       best = r + xf.f;
       int bi = 0;
+#pragma unroll 8
       for (int i = 1; i < P; ++i) {
         xf = ch[i];
         r += xf.x;
