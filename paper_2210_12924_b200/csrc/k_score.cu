@@ -542,11 +542,12 @@ mp_status score_configure(mp_graph* g) {
   if (J > 0) smem = true;
   if (J == 0) T = 1024;
   if (J == 0 && !smem) smem = false;
-  // Warp-per-candidate variant for small graphs (MP_SCORE_MODE=cta|warp forces it):
+  // Warp-per-candidate variant for small graphs, opt-in (MP_SCORE_MODE=warp): on
+  // the C2/C3 graphs it measured slower than the register-slot CTA variant.
   // as many warps per CTA as the per-warp buffers allow, up to 16.
   g->score_warps = 0;
   const char* mode = std::getenv("MP_SCORE_MODE");
-  const bool want_warp = mode ? std::string(mode) == "warp" : n <= kWarpMaxNodes;
+  const bool want_warp = mode && std::string(mode) == "warp" && n <= kWarpMaxNodes;
   if (want_warp && n > 0 && n < 65535) {
     const int wp = ((n + 31) / 32) | 1;
     g->score_wp = wp;
