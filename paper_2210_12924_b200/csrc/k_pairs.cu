@@ -46,53 +46,86 @@ __global__ void pack_kernel(int32_t E, const int32_t* __restrict__ lo,
   }
 }
 
-template <int MODE, bool PINNED>
-__device__ __forceinline__ bool pair_pred(const int2 a, const int2 b, const ulonglong2 aa,
-                                          const PairRec& R, int32_t j, bool pin_i) {
-  bool ok = b.x <= a.y && a.x <= b.y;
-  if (MODE == 0) {
-    if (PINNED) ok = ok && !(pin_i && R.pin[j]);
-  } else {
-    if (ok) {
-      const ulonglong2 bb = R.as[j];
-      ok = aa.x < bb.x + bb.y && bb.x < aa.x + aa.y;
-    }
-  }
-  return ok;
-}
+// Tiled sweep: a CTA owns RPW rows per warp (kept in registers) and streams
+// the columns j > first row through shared memory in tiles of kTileCols, so
+// every column record is read from L2 once per CTA instead of once per row.
+// Each lane evaluates its column of a 32-wide chunk against all of its warp's
+// rows (RPW ballots per loaded column); the count pass accumulates popc per
+// row, the fill pass writes each row's matches at off + popc(ballot & lt) in
+// increasing j (the reference's lexicographic order). Ineligible rows are
+// sentinels that match nothing.
+constexpr int kTileCols = 1024;
 
-// One warp per row i (rows interleaved over all warps of the grid so the
-// triangular work balances), 32 consecutive j per step.
-template <int MODE, bool PINNED, bool FILL>
+template <int MODE, bool PINNED, bool FILL, int RPW>
 __global__ void __launch_bounds__(kThreads)
-    pair_sweep_kernel(int32_t E, PairRec R, int64_t row_begin, int64_t row_end,
-                      int64_t* __restrict__ row_off, int2* __restrict__ out) {
+    pair_tile_kernel(int32_t E, PairRec R, int64_t row_begin, int64_t row_end,
+                     int64_t* __restrict__ row_off, int2* __restrict__ out) {
+  __shared__ int2 slh[kTileCols];
+  __shared__ ulonglong2 sas[MODE == 1 ? kTileCols : 1];
+  __shared__ uint8_t spin[PINNED ? kTileCols : 1];
   const int lane = threadIdx.x & 31;
-  const int64_t warp_global = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  const int64_t num_warps = (int64_t)gridDim.x * kWarpsPerBlock;
+  const int warp = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
-  for (int64_t r = row_begin + warp_global; r < row_end; r += num_warps) {
-    const int32_t i = (int32_t)r;
-    const int2 a = R.lh[i];
-    int64_t cnt = 0;
-    int64_t off = FILL ? row_off[r - row_begin] : 0;
-    if (a.x <= a.y) {
-      const ulonglong2 aa = MODE == 1 ? R.as[i] : make_ulonglong2(0, 0);
-      const bool pin_i = PINNED ? R.pin[i] != 0 : false;
-      for (int32_t j0 = i + 1; j0 < E; j0 += 32) {
-        const int32_t j = j0 + lane;
-        bool p = false;
-        if (j < E) p = pair_pred<MODE, PINNED>(a, R.lh[j], aa, R, j, pin_i);
-        const unsigned m = __ballot_sync(0xffffffffu, p);
-        if (FILL) {
-          if (p) out[off + __popc(m & lt_mask)] = make_int2(i, j);
-          off += __popc(m);
-        } else {
-          cnt += __popc(m);
+  const int64_t r0 = row_begin + (int64_t)blockIdx.x * kWarpsPerBlock * RPW;
+
+  int2 a[RPW];
+  ulonglong2 aa[RPW];
+  bool pin_i[RPW];
+  int64_t acc[RPW];  // FILL: running output offset; count: matches
+  int32_t ri[RPW];
+  bool any = false;
+#pragma unroll
+  for (int t = 0; t < RPW; ++t) {
+    const int64_t i = r0 + warp * RPW + t;
+    const bool in = i < row_end;
+    ri[t] = (int32_t)i;
+    a[t] = in ? R.lh[i] : make_int2(INT_MAX, INT_MIN);
+    any |= a[t].x <= a[t].y;
+    if (MODE == 1) aa[t] = in ? R.as[i] : make_ulonglong2(0, 0);
+    if (PINNED) pin_i[t] = in ? R.pin[i] != 0 : false;
+    acc[t] = (FILL && in) ? row_off[i - row_begin] : 0;
+  }
+  const bool warp_any = __any_sync(0xffffffffu, any);
+
+  for (int64_t j0 = r0 + 1; j0 < E; j0 += kTileCols) {
+    for (int q = threadIdx.x; q < kTileCols; q += kThreads) {
+      const int64_t j = j0 + q;
+      const bool in = j < E;
+      slh[q] = in ? R.lh[j] : make_int2(INT_MAX, INT_MIN);
+      if (MODE == 1) sas[q] = in ? R.as[j] : make_ulonglong2(0, 0);
+      if (PINNED) spin[q] = in ? R.pin[j] : 0;
+    }
+    __syncthreads();
+    if (warp_any) {
+      const int cols = (int)min((int64_t)kTileCols, E - j0);
+      for (int c = 0; c < cols; c += 32) {
+        const int q = c + lane;
+        const int32_t j = (int32_t)(j0 + q);
+        const int2 b = slh[q];
+        ulonglong2 bb;
+        if (MODE == 1) bb = sas[q];
+        const bool pj = PINNED ? spin[q] != 0 : false;
+#pragma unroll
+        for (int t = 0; t < RPW; ++t) {
+          bool p = b.x <= a[t].y && a[t].x <= b.y && j > ri[t];
+          if (MODE == 0 && PINNED) p = p && !(pin_i[t] && pj);
+          if (MODE == 1) p = p && aa[t].x < bb.x + bb.y && bb.x < aa[t].x + aa[t].y;
+          const unsigned m = __ballot_sync(0xffffffffu, p);
+          if (FILL) {
+            if (p) out[acc[t] + __popc(m & lt_mask)] = make_int2(ri[t], j);
+          }
+          acc[t] += __popc(m);
         }
       }
     }
-    if (!FILL && lane == 0) row_off[r - row_begin + 1] = cnt;
+    __syncthreads();
+  }
+  if (!FILL && lane == 0) {
+#pragma unroll
+    for (int t = 0; t < RPW; ++t) {
+      const int64_t i = r0 + warp * RPW + t;
+      if (i < row_end) row_off[i - row_begin + 1] = acc[t];
+    }
   }
 }
 
@@ -158,14 +191,6 @@ PairRec carve(const PairArgs& a, void* scratch) {
   return R;
 }
 
-unsigned sweep_grid(int64_t rows, int num_sms) {
-  int64_t want = (rows + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  int64_t cap = (int64_t)num_sms * 16;
-  if (want > cap) want = cap;
-  if (want < 1) want = 1;
-  return (unsigned)want;
-}
-
 mp_status pack(const PairArgs& a, const PairRec& R, cudaStream_t st) {
   if (a.num_edges == 0) return MP_OK;
   int64_t b = (a.num_edges + kThreads - 1) / kThreads;
@@ -176,22 +201,34 @@ mp_status pack(const PairArgs& a, const PairRec& R, cudaStream_t st) {
   return MP_OK;
 }
 
+template <int MODE, bool PINNED, bool FILL, int RPW>
+void launch_tile(const PairArgs& a, const PairRec& R, int64_t* row_off, int2* out,
+                 cudaStream_t st) {
+  const int64_t rows = a.row_end - a.row_begin;
+  const int64_t per_block = (int64_t)kWarpsPerBlock * RPW;
+  const unsigned grid = (unsigned)((rows + per_block - 1) / per_block);
+  pair_tile_kernel<MODE, PINNED, FILL, RPW>
+      <<<grid, kThreads, 0, st>>>(a.num_edges, R, a.row_begin, a.row_end, row_off, out);
+}
+
 template <bool FILL>
 mp_status sweep(const PairArgs& a, int num_sms, const PairRec& R, int64_t* row_off, int2* out,
                 cudaStream_t st) {
   const int64_t rows = a.row_end - a.row_begin;
   if (rows <= 0) return MP_OK;
-  const unsigned grid = sweep_grid(rows, num_sms);
+  // 8 rows per warp once there are enough rows to fill the GPU twice over
+  const bool big = rows >= (int64_t)num_sms * kWarpsPerBlock * 8 * 2;
   if (a.mode == 0) {
-    if (a.mask)
-      pair_sweep_kernel<0, true, FILL><<<grid, kThreads, 0, st>>>(a.num_edges, R, a.row_begin,
-                                                                  a.row_end, row_off, out);
-    else
-      pair_sweep_kernel<0, false, FILL><<<grid, kThreads, 0, st>>>(a.num_edges, R, a.row_begin,
-                                                                   a.row_end, row_off, out);
+    if (a.mask) {
+      big ? launch_tile<0, true, FILL, 8>(a, R, row_off, out, st)
+          : launch_tile<0, true, FILL, 1>(a, R, row_off, out, st);
+    } else {
+      big ? launch_tile<0, false, FILL, 8>(a, R, row_off, out, st)
+          : launch_tile<0, false, FILL, 1>(a, R, row_off, out, st);
+    }
   } else {
-    pair_sweep_kernel<1, false, FILL><<<grid, kThreads, 0, st>>>(a.num_edges, R, a.row_begin,
-                                                                 a.row_end, row_off, out);
+    big ? launch_tile<1, false, FILL, 8>(a, R, row_off, out, st)
+        : launch_tile<1, false, FILL, 1>(a, R, row_off, out, st);
   }
   MP_CUDA(cudaGetLastError());
   return MP_OK;
