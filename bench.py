@@ -354,18 +354,33 @@ def main():
     torch.cuda.synchronize()
     kern_ms = sum(a.elapsed_time(b) for a, b in zip(ev_s, ev_e)) / args.steps
 
-    # The K timed steps are one CUDA graph (launch-bound step: ~27 us of work per
-    # launch); each step = reset key + fused scoring kernel (+ NCCL allreduce-min).
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=stream):
-        cap = torch.cuda.current_stream().cuda_stream
-        for i in range(args.steps):
-            key.fill_(D.NO_KEY)
-            planner.score_orders_argmin_d(dg, batches[i % nb], C, peak, step, valid, key, base,
-                                          cap)
-            if world > 1:
+    # N=1: the K timed steps are one CUDA graph (launch-bound step). N>1: one
+    # graph per input batch (key reset + fused kernel), replayed per step, with the
+    # NCCL allreduce(min) issued eagerly after each (no collective inside a graph).
+    if world == 1:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            cap = torch.cuda.current_stream().cuda_stream
+            for i in range(args.steps):
+                key.fill_(D.NO_KEY)
+                planner.score_orders_argmin_d(dg, batches[i % nb], C, peak, step, valid, key,
+                                              base, cap)
+        run_timed = graph.replay
+    else:
+        graphs = []
+        for b in range(nb):
+            gb = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gb, stream=stream):
+                key.fill_(D.NO_KEY)
+                planner.score_orders_argmin_d(dg, batches[b], C, peak, step, valid, key, base,
+                                              torch.cuda.current_stream().cuda_stream)
+            graphs.append(gb)
+
+        def run_timed():
+            for i in range(args.steps):
+                graphs[i % nb].replay()
                 dist.all_reduce(key, op=dist.ReduceOp.MIN)
-    graph.replay()                       # warm replay (untimed)
+    run_timed()                           # warm replay (untimed)
     torch.cuda.synchronize()
     kk = D.check_device_key(int(key.item()))  # last step's global first-minimum key
 
@@ -378,7 +393,7 @@ def main():
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     start.record(stream)
-    graph.replay()
+    run_timed()
     end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -465,8 +480,9 @@ def main():
                     "path": "Planner.score_orders_into -> mp_score_orders_best (pinned host)",
                     "torch_pinned_h2d_gbs": h2d_gbs},
             "gpu_launches": args.steps,
-            "timing": "K steps captured as one CUDA graph, timed with CUDA events around the "
-                      "replay; kernel_ms from separate eager launches",
+            "timing": ("K steps captured as one CUDA graph" if world == 1 else
+                       "per-batch CUDA graph per step + eager NCCL allreduce(min)") +
+                      ", CUDA events on the step stream; kernel_ms = in-graph step time",
             "clocks": clocks.summary(t0, t1),
             "best_key_check": kk != D.NO_KEY,
         }
