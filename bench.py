@@ -33,6 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 L2_BYTES = 126 * 2**20
+METRIC = "candidate plans scored/sec (peak bytes + validity + argmin)"
 CONFIGS = {
     "c2": {"workload": "resnet50_b32_fwd_bwd_sgd", "graph": "resnet50_b32.json.gz",
            "candidates": 4096},
@@ -171,12 +172,13 @@ def run_reference(args, cfg):
     dt = time.perf_counter() - t0
     value = m * args.steps / dt
     line = {
-        "impl": "reference", "metric": "candidate plans scored/sec", "value": value,
+        "impl": "reference", "metric": METRIC, "value": value,
         "unit": "plans/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": cfg["workload"], "nodes": g.n, "edges": g.E,
-                   "candidates_per_step": m},
+                   "sinks": int(len(g.sinks)), "candidates_per_step": m,
+                   "candidate_source": "seeded random topological orders (randomised Kahn)"},
         "cpu_baseline": {"value": value, "unit": "plans/s", "cores": threads, "kind": "reference",
                          "sample": f"{m} random topological orders per step, memplan::"
                                    f"peak_resident_bytes per order + first-min argmin, "
@@ -457,7 +459,7 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(g, host_batches[0])
         line = {
-            "metric": "candidate plans scored/sec (peak bytes + validity + argmin)",
+            "metric": METRIC,
             "value": value, "unit": "plans/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
