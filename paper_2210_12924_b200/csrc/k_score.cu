@@ -268,11 +268,25 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
         }
       }
     } else {
+      // batches of kB: all loads of a batch before its stores (the compiler cannot
+      // reorder loads across stores to possibly aliasing buffers)
+      constexpr int kB = 8;
       const int32_t* ord = orders + c * n;
-      for (int k = tid; k < n; k += T) {
-        const int v = __ldg(ord + k);
-        if ((unsigned)v >= (unsigned)n) bad = true;
-        else pos[v] = tag | (PW)k;
+      for (int k0 = tid; k0 < n; k0 += T * kB) {
+        int vv[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int k = k0 + u * T;
+          vv[u] = k < n ? __ldg(ord + k) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int k = k0 + u * T;
+          if (k < n) {
+            if ((unsigned)vv[u] >= (unsigned)n) bad = true;
+            else pos[vv[u]] = tag | (PW)k;
+          }
+        }
       }
     }
     __syncthreads();
@@ -292,21 +306,68 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
         if (v < n) node(v, rx[j], rf[j], rp[j]);
       }
     } else {
-      for (int v = tid; v < n; v += T) node(v, (VT)G.node_x[v], (VT)G.node_f[v], G.pred1[v]);
+      constexpr int kB = 8;
+      for (int v0 = tid; v0 < n; v0 += T * kB) {
+        PW w[kB], pu[kB];
+        VT xx[kB], ff[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int v = v0 + u * T;
+          const bool in = v < n;
+          const int pr = in ? __ldg(G.pred1 + v) : -1;
+          w[u] = in ? pos[v] : tag;
+          xx[u] = in ? (VT)__ldg(G.node_x + v) : (VT)0;
+          ff[u] = in ? (VT)__ldg(G.node_f + v) : (VT)0;
+          pu[u] = pr >= 0 ? pos[pr] : (PW)0;
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          if (v0 + u * T < n) {
+            bad |= !PWT::fresh(w[u], tag) || pu[u] >= w[u];
+            const int q = PWT::pos(w[u]);
+            if (q < n) XF[q] = XFPair<VT>{xx[u], ff[u]};
+          }
+        }
+      }
     }
     // ---- phase 2b: remaining reduced producer pairs ----------------------------------
-    for (int i = tid; i < G.nextra; i += T) bad |= pos[ex_u[i]] >= pos[ex_w[i]];
+    {
+      constexpr int kB = 8;
+      for (int i0 = tid; i0 < G.nextra; i0 += T * kB) {
+        PW a[kB], b[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int i = i0 + u * T;
+          const bool in = i < G.nextra;
+          a[u] = in ? pos[ex_u[i]] : (PW)0;
+          b[u] = in ? pos[ex_w[i]] : (PW)1;
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) bad |= a[u] >= b[u];
+      }
+    }
     // ---- phase 2c: order-dependent last consumers --------------------------------------
     if (G.ndyn > 0) {
       __syncthreads();  // XF written by phase 2a
-      for (int d = tid; d < G.ndyn; d += T) {
-        PW h = 0;
-        for (int s = dy_off[d]; s < dy_off[d + 1]; ++s) h = max(h, pos[dy_sinks[s]]);
-        const int q = PWT::pos(h);
-        if (q < n) {
-          const VT sz = kSmem ? dy_size[d] : (VT)dy_size64[d];
-          atomicAdd(&XF[q].f, sz);
-          atomicAdd(&XF[q].x, (VT)0 - sz);
+      constexpr int kB = 4;
+      for (int d0 = tid; d0 < G.ndyn; d0 += T * kB) {
+        PW h[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {  // gathers of kB edges before any atomic
+          const int d = d0 + u * T;
+          h[u] = 0;
+          if (d < G.ndyn)
+            for (int s = dy_off[d]; s < dy_off[d + 1]; ++s) h[u] = max(h[u], pos[dy_sinks[s]]);
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int d = d0 + u * T;
+          const int q = PWT::pos(h[u]);
+          if (d < G.ndyn && q < n) {
+            const VT sz = kSmem ? dy_size[d] : (VT)dy_size64[d];
+            atomicAdd(&XF[q].f, sz);
+            atomicAdd(&XF[q].x, (VT)0 - sz);
+          }
         }
       }
     }
@@ -322,6 +383,7 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
     // ---- phase 3: blocked two-pass scan (chunk [tid*P, tid*P+P), P odd) ------------
     const XFPair<VT>* mine = XF + tid * P;
     VT total = 0;
+#pragma unroll 8
     for (int i = 0; i < P; ++i) total += mine[i].x;
     const VT incl = warp_incl_scan(total, lane);
     if (lane == kWarp - 1) bs.wsum[warp] = incl;
