@@ -79,6 +79,15 @@ struct PosWord<uint32_t> {
   __device__ static bool fresh(uint32_t w, uint32_t tag) { return (w & 0xffff0000u) == tag; }
   __device__ static int pos(uint32_t w) { return (int)(w & 0xffffu); }
 };
+// int32_t words: 24-bit position, 7-bit stamp (words stay non-negative, so
+// signed compares order them like the unsigned variants). n < 2^24.
+template <>
+struct PosWord<int32_t> {
+  static constexpr uint32_t kMaxStamp = 0x7fu;
+  __device__ static int32_t tag(uint32_t stamp) { return (int32_t)(stamp << 24); }
+  __device__ static bool fresh(int32_t w, int32_t tag) { return (w & 0x7f000000) == tag; }
+  __device__ static int pos(int32_t w) { return w & 0xffffff; }
+};
 template <>
 struct PosWord<unsigned long long> {
   static constexpr uint32_t kMaxStamp = 0xffffffffu;
@@ -476,7 +485,14 @@ mp_status run(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d
     MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem));
     grid = (int64_t)g->ctx->num_sms * (per_sm > 0 ? per_sm : 1);
   } else {
-    grid = (int64_t)g->ctx->num_sms * 2;
+    // per-CTA scratch slices are the working set of the random scatters: a
+    // grid of one CTA per SM keeps more of them L2-resident (MP_SCORE_GRID
+    // overrides, for tuning)
+    grid = (int64_t)g->ctx->num_sms;
+    if (const char* e = std::getenv("MP_SCORE_GRID")) {
+      const long v = std::atol(e);
+      if (v > 0) grid = v;
+    }
     if (grid > C) grid = C;
     gstride = (per + 255) & ~size_t(255);
     MP_TRY(g->ctx->scratch[3].reserve(gstride * (size_t)(grid > 0 ? grid : 1)));
@@ -550,6 +566,8 @@ mp_status dispatch(const mp_graph* g, const int32_t* o, int64_t C, uint64_t* pk,
     default:
       if (g->smem_resident)
         return run<VT, uint32_t, 0, true>(g, o, C, pk, stp, vl, by, key, base, st);
+      if (g->n < (1 << 24) && !std::getenv("MP_SCORE_POS64"))
+        return run<VT, int32_t, 0, false>(g, o, C, pk, stp, vl, by, key, base, st);
       return run<VT, unsigned long long, 0, false>(g, o, C, pk, stp, vl, by, key, base, st);
   }
 }

@@ -254,10 +254,13 @@ def test_scorer_variants_small_graphs(planner, monkeypatch, mode, kind, layers, 
             orc.resident_bytes_per_step(orders[0])).all()
 
 
-@pytest.mark.parametrize("layers,smem", [(3000, 1), (20000, 0)])
-def test_large_graph_variants(planner, layers, smem):
+@pytest.mark.parametrize("layers,smem,pos64", [(3000, 1, 0), (20000, 0, 0), (20000, 0, 1)])
+def test_large_graph_variants(planner, monkeypatch, layers, smem, pos64):
     """Graphs past the register-resident variant: node tables read per candidate,
-    buffers in shared memory (n=12k) or in global scratch (n=80k >= 65536)."""
+    buffers in shared memory (n=12k) or in global scratch (n=80k >= 65536),
+    with 32-bit (24-bit position) or 64-bit stamped position words."""
+    if pos64:
+        monkeypatch.setenv("MP_SCORE_POS64", "1")
     g = mp.generate_graph("training_like", layers, 8)
     dg = planner.upload(g)
     assert dg.info()["smem_resident"] == smem
@@ -273,6 +276,28 @@ def test_large_graph_variants(planner, layers, smem):
     for i, o in enumerate(orders):
         rs = orc.resident_bytes_per_step(o)
         assert (int(res.peak[i]), int(res.peak_step[i])) == (int(rs.max()), int(np.argmax(rs)) + 1)
+
+
+def test_global_scratch_stamp_wrap(planner, monkeypatch):
+    """One CTA scoring 300 candidates of an 80k-node graph: the 7-bit stamp of
+    the 32-bit position words wraps twice and every verdict and peak must hold."""
+    monkeypatch.setenv("MP_SCORE_GRID", "1")
+    g = mp.generate_graph("training_like", 20000, 8)
+    orc = O.Oracle.from_csr(g.csr())
+    orders = mp.random_topo_orders(g, 300, seed=11)
+    for i in (5, 130, 131, 290):          # invalid rows across the wraps
+        orders[i, [7, 8 + i]] = orders[i, [8 + i, 7]]
+    orders[200, 3] = orders[200, 4]
+    res = planner.score_orders(g, orders)
+    assert res.valid.tolist() == [int(orc.is_topological_order(o)) for o in orders]
+    for i in (0, 129, 257, 299):          # exact peaks on a few rows (O(sum of lifetimes) each)
+        if res.valid[i]:
+            rs = orc.resident_bytes_per_step(orders[i])
+            assert (int(res.peak[i]), int(res.peak_step[i])) == (int(rs.max()), int(np.argmax(rs)) + 1), i
+    monkeypatch.delenv("MP_SCORE_GRID")    # full grid (no wrap) must agree row for row
+    full = planner.score_orders(g, orders)
+    assert (full.peak == res.peak).all() and (full.peak_step == res.peak_step).all()
+    assert (full.valid == res.valid).all()
 
 
 def test_c5_full_size(golden, planner):
