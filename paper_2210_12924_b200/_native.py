@@ -13,6 +13,8 @@ import threading
 from . import errors
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libmemplan_b200.so")
+# MP_LIB selects a tuning build of the same sources (tools/gpu/variants.sh); never a fallback
+LIB_PATH = os.environ.get("MP_LIB", LIB_PATH)
 
 MP_OK = 0
 MP_E_INVALID_ORDER = 1

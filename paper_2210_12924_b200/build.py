@@ -37,29 +37,32 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(LIBDIR, exist_ok=True)
-    os.makedirs(OBJDIR, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB,
+          objdir: str = OBJDIR) -> str:
+    """Compile and link the library. ``defines``/``lib``/``objdir`` build tuning
+    variants (e.g. ``-DMP_J8_MAXT=320``) next to the product library."""
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    os.makedirs(objdir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(ROOT, "include", "memplan_b200.h"))
     common = ["-O3", "-std=c++17", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-              "-Xcompiler", "-fPIC,-Wall"]
+              "-Xcompiler", "-fPIC,-Wall", *defines]
     objs = []
     log = []
     for src in CU_SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJDIR, src + ".o")
+        o = os.path.join(objdir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
             log.append(_run([NVCC, *ARCH, "-lineinfo", "-Xptxas", "-v", *common, "-c", s, "-o", o]))
     for src in CPP_SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJDIR, src + ".o")
+        o = os.path.join(objdir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
             log.append(_run([NVCC, *ARCH, *common, "-c", s, "-o", o]))
-    if force or _stale(LIB, objs):
-        log.append(_run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs,
+    if force or _stale(lib, objs):
+        log.append(_run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs,
                          "-lpthread"]))
     text = "".join(log)
     if verbose:

@@ -213,6 +213,70 @@ __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMi
     const uint32_t badmask = bs.bad[parity];
     const int64_t c0 = g * KC;
 
+    if constexpr (sizeof(VT) == 8) {
+      if (bytes_out == nullptr) {
+        // ---- phase 3, 64-bit values: ONE pass over the chunk [p0, p0 + P) -----------
+        // x = alloc - free is exact as int64 (|x| <= total < 2^62), so chunk-relative
+        // RS values are exact: each thread finds its chunk's first maximum relative to
+        // the chunk start, a warp scan of the chunk sums makes it warp-relative, and
+        // warp 0 combines the per-warp (sum, best, index) triples after one barrier.
+        const int p0 = tid * P;
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+          const XFPair<VT>* mine = XF[k] + p0;
+          XFPair<VT> xf = mine[0];
+          long long l = (long long)xf.x;
+          long long lb = l + (long long)xf.f;
+          int li = 0;
+          for (int i = 1; i < P; ++i) {
+            xf = mine[i];
+            l += (long long)xf.x;
+            const long long rs = l + (long long)xf.f;
+            const bool better = rs > lb;
+            lb = better ? rs : lb;
+            li = better ? i : li;
+          }
+          const long long incl = warp_incl_scan(l, lane);
+          long long cand = incl - l + lb;
+          int ci = p0 < n ? p0 + li : INT_MAX;  // a chunk made only of padding
+          warp_argmax(cand, ci);
+          if (lane == 0) {
+            bs.wbest[k][warp] = (VT)cand;
+            bs.widx[k][warp] = ci;
+          }
+          if (lane == kWarp - 1) bs.wsum[k][warp] = (VT)incl;
+        }
+        __syncthreads();
+        if (tid == 0) bs.bad[parity ^ 1] = 0;  // next iteration's flags
+        if (warp == 0) {
+#pragma unroll
+          for (int k = 0; k < KC; ++k) {
+            const bool live = lane < nwarps;
+            const long long wt = live ? (long long)bs.wsum[k][lane] : 0;
+            const long long incl = warp_incl_scan(wt, lane);
+            long long b = live ? incl - wt + (long long)bs.wbest[k][lane] : LLONG_MIN;
+            int bi = live ? bs.widx[k][lane] : INT_MAX;
+            warp_argmax(b, bi);
+            const int64_t c = c0 + k;
+            if (lane == 0 && c < C) {
+              const bool ok = !((badmask >> k) & 1u);
+              const bool empty = n == 0;
+              const uint64_t pk = (!ok || empty) ? 0 : (uint64_t)b * G.scale;
+              peak_out[c] = pk;
+              step_out[c] = (!ok || empty) ? 0 : bi + 1;
+              valid_out[c] = ok ? 1 : 0;
+              if (best_key && ok) {
+                const uint64_t gi = (uint64_t)(c + index_base);
+                const unsigned long long key =
+                    (pk < (1ull << 43) && gi < (1ull << 20)) ? ((pk << 20) | gi) : kKeyOverflow;
+                atomicMin(best_key, key);
+              }
+            }
+          }
+        }
+        continue;
+      }
+    }
     // ---- phase 3: blocked two-pass scan over [tid*P, tid*P + P), P odd -------------
     VT run[KC], best[KC];
     int best_i[KC];
