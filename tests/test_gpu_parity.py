@@ -254,13 +254,17 @@ def test_scorer_variants_small_graphs(planner, monkeypatch, mode, kind, layers, 
             orc.resident_bytes_per_step(orders[0])).all()
 
 
-@pytest.mark.parametrize("layers,smem,pos64", [(3000, 1, 0), (20000, 0, 0), (20000, 0, 1)])
-def test_large_graph_variants(planner, monkeypatch, layers, smem, pos64):
+@pytest.mark.parametrize("layers,smem,mode", [(3000, 1, ""), (20000, 0, ""), (20000, 0, "tile"),
+                                              (20000, 0, "scratch64"), (3000, 1, "tile")])
+def test_large_graph_variants(planner, monkeypatch, layers, smem, mode):
     """Graphs past the register-resident variant: node tables read per candidate,
-    buffers in shared memory (n=12k) or in global scratch (n=80k >= 65536),
-    with 32-bit (24-bit position) or 64-bit stamped position words."""
-    if pos64:
+    buffers in shared memory (n=12k); at n=80k >= 65536 the node-space kernel with
+    global scratch and 32-bit (24-bit position, default) or 64-bit stamped position
+    words, or the tile scorer; the tile scorer forced on the 12k graph too."""
+    if mode == "scratch64":
         monkeypatch.setenv("MP_SCORE_POS64", "1")
+    if mode == "tile":
+        monkeypatch.setenv("MP_SCORE_MODE", "tile")
     g = mp.generate_graph("training_like", layers, 8)
     dg = planner.upload(g)
     assert dg.info()["smem_resident"] == smem
@@ -278,9 +282,13 @@ def test_large_graph_variants(planner, monkeypatch, layers, smem, pos64):
         assert (int(res.peak[i]), int(res.peak_step[i])) == (int(rs.max()), int(np.argmax(rs)) + 1)
 
 
-def test_global_scratch_stamp_wrap(planner, monkeypatch):
-    """One CTA scoring 300 candidates of an 80k-node graph: the 7-bit stamp of
-    the 32-bit position words wraps twice and every verdict and peak must hold."""
+@pytest.mark.parametrize("tile", [0, 1])
+def test_global_scratch_stamp_wrap(planner, monkeypatch, tile):
+    """One CTA scoring 300 candidates of an 80k-node graph: the stamp of the
+    32-bit position words wraps (7-bit node-space scratch: twice; 8-bit tile
+    scorer: once) and every verdict and peak must hold."""
+    if tile:
+        monkeypatch.setenv("MP_SCORE_MODE", "tile")
     monkeypatch.setenv("MP_SCORE_GRID", "1")
     g = mp.generate_graph("training_like", 20000, 8)
     orc = O.Oracle.from_csr(g.csr())
@@ -298,6 +306,35 @@ def test_global_scratch_stamp_wrap(planner, monkeypatch):
     full = planner.score_orders(g, orders)
     assert (full.peak == res.peak).all() and (full.peak_step == res.peak_step).all()
     assert (full.valid == res.valid).all()
+
+
+@pytest.mark.parametrize("name", ["resnet50_b32", "bert_base_s512", "gpt2_medium_s1024"])
+def test_tile_scorer_model_graphs(planner, monkeypatch, name):
+    """The tile scorer forced on the traced model graphs: order-dependent frees
+    (57/234/364 dynamic edges), 32- and 64-bit values, invalid rows, twice in a
+    row (stamps persist across launches), vs the oracle."""
+    monkeypatch.setenv("MP_SCORE_MODE", "tile")
+    import gzip
+    import os
+    path = os.path.join(os.path.dirname(__file__), "..", "workloads", "graphs", name + ".json.gz")
+    with gzip.open(path, "rt") as fh:
+        g = mp.load_graph(fh.read())
+    orc = O.Oracle.from_csr(g.csr())
+    orders = mp.random_topo_orders(g, 24, seed=3)
+    orders[2, [5, 6]] = orders[2, [6, 5]]
+    orders[4, 11] = orders[4, 12]
+    orders[6, -1] = -1
+    for _ in range(2):
+        res = planner.score_orders(g, orders)
+        for i, o in enumerate(orders):
+            lt = orc.lifetimes_from_order(o)
+            if lt is None:
+                assert res.valid[i] == 0, i
+                continue
+            _, pr, ps = orc.timeline_from_lifetimes(lt[0], lt[1], g.n)
+            assert res.valid[i] == 1 and (int(res.peak[i]), int(res.peak_step[i])) == (pr, ps), i
+    rs = planner.resident_bytes_per_step(g, orders[0])
+    assert (rs == orc.resident_bytes_per_step(orders[0])).all()
 
 
 def test_c5_full_size(golden, planner):
