@@ -211,6 +211,35 @@ mp_status mp_peak_mem(mp_ctx* ctx, int32_t num_edges, const uint64_t* size,
 /* fragmentation (placement.cpp:64-67): (mr - rs) / mr, 0 when mr == 0. */
 double mp_fragmentation(uint64_t mr, uint64_t rs);
 
+/* ---- (§8f-2) placement heuristics: the producers of the plans K4 validates ----
+ * preallocate_pyramid (placement.cpp:25-62) and greedy_pack
+ * (placement.cpp:182-204) over num_problems lifetime vectors that share the
+ * edge sizes (problem b: lo/hi [b*num_edges ..], e.g. one per candidate order),
+ * plus peak_mem = max(addr + size) of the result (pipeline.cpp:270-275).
+ * flags: MP_PLACE_PYRAMID      the preplaced map is preallocate_pyramid's
+ *                              (pipeline.cpp:248-249); fixed must be NULL
+ *        MP_PLACE_PYRAMID_ONLY stop after the pyramid (PrePlacement.assigned)
+ * fixed / fixed_addr [num_edges]: the caller's preplaced map (may be NULL).
+ * id_rank [num_edges]: rank of each edge id in byte-lexicographic order, the
+ * pyramid's last tie-break (placement.cpp:48-50); NULL = edge index order.
+ * Outputs: addr / has_addr [num_problems][num_edges] (has_addr = the edge is in
+ * the returned map), peak_mem [num_problems] and pyramid_base
+ * [num_problems] (PrePlacement.reserved_base), both optional.
+ * At most 8192 edges per problem (the placed set lives in shared memory):
+ * larger graphs return MP_E_CAPACITY. */
+#define MP_PLACE_PYRAMID 1u
+#define MP_PLACE_PYRAMID_ONLY 2u
+mp_status mp_place(mp_ctx* ctx, int32_t num_edges, int64_t num_problems, const int32_t* lo,
+                   const int32_t* hi, const uint64_t* size, const int32_t* id_rank,
+                   const uint8_t* fixed, const uint64_t* fixed_addr, uint32_t flags,
+                   uint64_t* addr, uint8_t* has_addr, uint64_t* peak_mem,
+                   uint64_t* pyramid_base);
+mp_status mp_place_d(mp_ctx* ctx, int32_t num_edges, int64_t num_problems, const int32_t* d_lo,
+                     const int32_t* d_hi, const uint64_t* d_size, const int32_t* d_id_rank,
+                     const uint8_t* d_fixed, const uint64_t* d_fixed_addr, uint32_t flags,
+                     uint64_t* d_addr, uint8_t* d_has_addr, uint64_t* d_peak_mem,
+                     uint64_t* d_pyramid_base, void* stream);
+
 /* ---- workload helpers (host C++, not on the measured path) ----------------------
  * Deterministic graph families with the semantics of generate_graph
  * (generate.cpp:45-158; chain = 0, fork_join = 1, training_like = 2).

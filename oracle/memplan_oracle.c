@@ -224,3 +224,73 @@ uint64_t or_peak_mem(int32_t num_edges, const uint64_t* size, const uint8_t* has
     if (has_addr[e] && addr[e] + size[e] > peak) peak = addr[e] + size[e];
   return peak;
 }
+
+/* placement.cpp:25-62, literally: repeatedly the longest-lived data edge whose
+ * lifetime fits strictly inside the window (ties: larger size, then smaller id),
+ * stacked at the next base; the window shrinks to its lifetime. */
+uint64_t or_preallocate_pyramid(int32_t num_edges, const int32_t* lo, const int32_t* hi,
+                                const uint64_t* size, const int32_t* id_rank, uint8_t* taken,
+                                uint64_t* addr) {
+  uint64_t base = 0;
+  int64_t min_start = 0, max_end = INT64_MAX;
+  for (int32_t e = 0; e < num_edges; ++e) taken[e] = 0;
+  while (max_end > min_start) {
+    int32_t pick = -1;
+    for (int32_t e = 0; e < num_edges; ++e) {
+      if (taken[e] || size[e] == 0) continue;
+      if (lo[e] <= min_start || hi[e] >= max_end) continue;
+      if (pick < 0) {
+        pick = e;
+        continue;
+      }
+      const int d_new = hi[e] - lo[e], d_old = hi[pick] - lo[pick];
+      if (d_new != d_old) {
+        if (d_new > d_old) pick = e;
+      } else if (size[e] != size[pick]) {
+        if (size[e] > size[pick]) pick = e;
+      } else if (id_rank[e] < id_rank[pick]) {
+        pick = e;
+      }
+    }
+    if (pick < 0) break;
+    taken[pick] = 1;
+    addr[pick] = base;
+    base += size[pick];
+    min_start = lo[pick];
+    max_end = hi[pick];
+  }
+  return base;
+}
+
+/* analysis.hpp:28-37 */
+static int or_disjoint(int32_t alo, int32_t ahi, int32_t blo, int32_t bhi) {
+  return alo > ahi || blo > bhi || ahi < blo || bhi < alo;
+}
+
+/* placement.cpp:182-204, literally: for each data edge not preplaced, in edge
+ * order, start at 0 and bump past every placed, lifetime-overlapping tensor
+ * whose range intersects, until a full pass moves nothing. `placed` is a
+ * std::map, iterated in edge-index order. */
+void or_greedy_pack(int32_t num_edges, const int32_t* lo, const int32_t* hi, const uint64_t* size,
+                    const uint8_t* fixed, uint64_t* addr, uint8_t* has) {
+  for (int32_t e = 0; e < num_edges; ++e) has[e] = fixed && fixed[e] ? 1 : 0;
+  for (int32_t e = 0; e < num_edges; ++e) {
+    if (size[e] == 0 || has[e]) continue;
+    uint64_t at = 0;
+    int moved = 1;
+    while (moved) {
+      moved = 0;
+      for (int32_t w = 0; w < num_edges; ++w) {
+        if (!has[w]) continue;
+        if (or_disjoint(lo[e], hi[e], lo[w], hi[w])) continue;
+        const uint64_t w_top = addr[w] + size[w];
+        if (at < w_top && addr[w] < at + size[e]) {
+          at = w_top;
+          moved = 1;
+        }
+      }
+    }
+    addr[e] = at;
+    has[e] = 1;
+  }
+}

@@ -79,6 +79,17 @@ double or_fragmentation(uint64_t mr, uint64_t rs);
 uint64_t or_peak_mem(int32_t num_edges, const uint64_t* size, const uint8_t* has_addr,
                      const uint64_t* addr);
 
+/* preallocate_pyramid (placement.cpp:25-62): taken[e] = 1 and addr[e] = its base
+ * for the picked edges; returns reserved_base. id_rank[e] orders edge ids
+ * (byte-lexicographic) for the last tie-break (placement.cpp:48-50). */
+uint64_t or_preallocate_pyramid(int32_t num_edges, const int32_t* lo, const int32_t* hi,
+                                const uint64_t* size, const int32_t* id_rank, uint8_t* taken,
+                                uint64_t* addr);
+/* greedy_pack (placement.cpp:182-204) with the preplaced map given as
+ * fixed[e] / addr[e] (in/out): on return has[e] = 1 for every placed edge. */
+void or_greedy_pack(int32_t num_edges, const int32_t* lo, const int32_t* hi, const uint64_t* size,
+                    const uint8_t* fixed, uint64_t* addr, uint8_t* has);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,6 +36,10 @@ def build(quiet: bool = True) -> None:
         print(out.stdout)
 
 
+def _c(a, dt):
+    return np.ascontiguousarray(a, dt)
+
+
 def _opt_ptr(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
@@ -84,6 +88,9 @@ def olib():
         lib.or_fragmentation.restype = C.c_double
         lib.or_peak_mem.argtypes = [C.c_int32, _u64p, _u8p, _u64p]
         lib.or_peak_mem.restype = C.c_uint64
+        lib.or_preallocate_pyramid.argtypes = [C.c_int32, _i32p, _i32p, _u64p, _i32p, _u8p, _u64p]
+        lib.or_preallocate_pyramid.restype = C.c_uint64
+        lib.or_greedy_pack.argtypes = [C.c_int32, _i32p, _i32p, _u64p, _vp, _u64p, _u8p]
         _olib = lib
     return _olib
 
@@ -197,6 +204,29 @@ def addresses_feasible(lo, hi, size, has_addr, addr):
         np.ascontiguousarray(addr, np.uint64)))
 
 
+def preallocate_pyramid(lo, hi, size, id_rank):
+    """placement.cpp:25-62 -> (taken u8[E], addr u64[E], reserved_base)."""
+    E = len(size)
+    taken = np.zeros(max(E, 1), np.uint8)
+    addr = np.zeros(max(E, 1), np.uint64)
+    base = olib().or_preallocate_pyramid(E, _c(lo, np.int32), _c(hi, np.int32),
+                                         _c(size, np.uint64), _c(id_rank, np.int32), taken, addr)
+    return taken[:E], addr[:E], int(base)
+
+
+def greedy_pack(lo, hi, size, fixed=None, fixed_addr=None):
+    """placement.cpp:182-204 -> (addr u64[E], has u8[E]); fixed = preplaced map."""
+    E = len(size)
+    addr = np.zeros(max(E, 1), np.uint64)
+    has = np.zeros(max(E, 1), np.uint8)
+    if fixed is not None:
+        addr[:E] = fixed_addr
+    fx = None if fixed is None else _c(fixed, np.uint8)
+    olib().or_greedy_pack(E, _c(lo, np.int32), _c(hi, np.int32), _c(size, np.uint64),
+                          _opt_ptr(fx), addr, has)
+    return addr[:E], has[:E]
+
+
 def fragmentation(mr, rs):
     return float(olib().or_fragmentation(int(mr), int(rs)))
 
@@ -254,6 +284,11 @@ def rlib():
                                           C.c_uint64, C.c_int32, _vp, C.c_int64,
                                           C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
         lib.ref_greedy_pack.argtypes = [_vp, _i32p, _i32p, _u64p]
+        lib.ref_preallocate_pyramid.argtypes = [_vp, _i32p, _i32p, _u8p, _u64p,
+                                                C.POINTER(C.c_uint64)]
+        lib.ref_greedy_pack_fixed.argtypes = [_vp, _i32p, _i32p, _vp, _vp, _u64p, _u8p]
+        lib.ref_run_baseline.argtypes = [_vp, _i32p, C.c_int64, C.c_int, C.POINTER(C.c_uint64),
+                                         C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
         lib.ref_fragmentation.argtypes = [C.c_uint64, C.c_uint64]
         lib.ref_fragmentation.restype = C.c_double
         lib.ref_enumerate_min_peak.argtypes = [_vp, C.POINTER(C.c_uint64), _i32p]
@@ -423,6 +458,33 @@ class RefGraph:
         _check(rlib().ref_greedy_pack(self._h, np.ascontiguousarray(lo, np.int32),
                                       np.ascontiguousarray(hi, np.int32), out))
         return out[: self.E]
+
+    def preallocate_pyramid(self, lo, hi):
+        """-> (taken u8[E], addr u64[E], reserved_base) from the reference."""
+        taken = np.zeros(max(self.E, 1), np.uint8)
+        addr = np.zeros(max(self.E, 1), np.uint64)
+        base = C.c_uint64()
+        _check(rlib().ref_preallocate_pyramid(self._h, _c(lo, np.int32), _c(hi, np.int32), taken,
+                                              addr, C.byref(base)))
+        return taken[: self.E], addr[: self.E], base.value
+
+    def greedy_pack_fixed(self, lo, hi, fixed=None, fixed_addr=None):
+        """greedy_pack with a preplaced map -> (addr u64[E], has u8[E])."""
+        addr = np.zeros(max(self.E, 1), np.uint64)
+        has = np.zeros(max(self.E, 1), np.uint8)
+        fx = None if fixed is None else _c(fixed, np.uint8)
+        fa = None if fixed is None else _c(fixed_addr, np.uint64)
+        _check(rlib().ref_greedy_pack_fixed(self._h, _c(lo, np.int32), _c(hi, np.int32),
+                                            _opt_ptr(fx), _opt_ptr(fa), addr, has))
+        return addr[: self.E], has[: self.E]
+
+    def run_baseline(self, order, best_fit=False):
+        """run_baseline (placement.cpp:150-180) -> (mr_peak, rs_at_peak, fragmentation)."""
+        mr, rs, fr = C.c_uint64(), C.c_uint64(), C.c_double()
+        o = _c(order, np.int32)
+        _check(rlib().ref_run_baseline(self._h, o, len(o), int(best_fit), C.byref(mr),
+                                       C.byref(rs), C.byref(fr)))
+        return mr.value, rs.value, fr.value
 
     def enumerate_min_peak(self):
         p = C.c_uint64()

@@ -387,6 +387,67 @@ int ref_greedy_pack(const void* gp, const int32_t* lo, const int32_t* hi,
   }
 }
 
+// preallocate_pyramid (placement.cpp:25-62): taken/addr per edge, reserved_base
+int ref_preallocate_pyramid(const void* gp, const int32_t* lo, const int32_t* hi, uint8_t* taken,
+                            uint64_t* addr, uint64_t* reserved_base) {
+  try {
+    const Graph& g = *static_cast<const Graph*>(gp);
+    PrePlacement pre = preallocate_pyramid(g, to_intervals(lo, hi, g.num_edges()));
+    for (int e = 0; e < g.num_edges(); ++e) {
+      taken[e] = 0;
+      addr[e] = 0;
+    }
+    for (const auto& [e, a] : pre.assigned) {
+      taken[e] = 1;
+      addr[e] = a;
+    }
+    *reserved_base = pre.reserved_base;
+    return REF_OK;
+  } catch (...) {
+    return fail_from_current();
+  }
+}
+
+// greedy_pack with a preplaced map (fixed[e] != 0 -> fixed_addr[e]); has[e] = in the result
+int ref_greedy_pack_fixed(const void* gp, const int32_t* lo, const int32_t* hi,
+                          const uint8_t* fixed, const uint64_t* fixed_addr, uint64_t* addr,
+                          uint8_t* has) {
+  try {
+    const Graph& g = *static_cast<const Graph*>(gp);
+    std::map<EdgeIndex, std::uint64_t> pre;
+    for (int e = 0; e < g.num_edges(); ++e)
+      if (fixed && fixed[e]) pre[e] = fixed_addr[e];
+    auto placed = greedy_pack(g, to_intervals(lo, hi, g.num_edges()), pre);
+    for (int e = 0; e < g.num_edges(); ++e) {
+      addr[e] = 0;
+      has[e] = 0;
+    }
+    for (const auto& [e, a] : placed) {
+      addr[e] = a;
+      has[e] = 1;
+    }
+    return REF_OK;
+  } catch (...) {
+    return fail_from_current();
+  }
+}
+
+// run_baseline (placement.cpp:150-180)
+int ref_run_baseline(const void* gp, const int32_t* order, int64_t len, int best_fit,
+                     uint64_t* mr_peak, uint64_t* rs_at_peak, double* frag) {
+  try {
+    const Graph& g = *static_cast<const Graph*>(gp);
+    BaselineResult r = run_baseline(g, to_order(order, len),
+                                    best_fit ? FitPolicy::kBestFit : FitPolicy::kFirstFit);
+    *mr_peak = r.mr_peak;
+    *rs_at_peak = r.rs_at_peak;
+    *frag = r.fragmentation;
+    return REF_OK;
+  } catch (...) {
+    return fail_from_current();
+  }
+}
+
 double ref_fragmentation(uint64_t mr, uint64_t rs) {
   return fragmentation(mr, rs);
 }

@@ -37,6 +37,7 @@ EXPORTS = [
     "mp_overlap_pairs", "mp_overlap_pairs_d",
     "mp_validate_pairs", "mp_validate_pairs_d", "mp_addresses_feasible", "mp_peak_mem",
     "mp_fragmentation", "mp_generate_graph", "mp_random_topo_orders",
+    "mp_place", "mp_place_d",
 ]
 
 
@@ -115,6 +116,10 @@ def lib():
             "mp_addresses_feasible": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, P(i32)]),
             "mp_peak_mem": (C.c_int, [vp, i32, vp, vp, vp, P(u64)]),
             "mp_fragmentation": (C.c_double, [u64, u64]),
+            "mp_place": (C.c_int, [vp, i32, i64, vp, vp, vp, vp, vp, vp, C.c_uint32, vp, vp,
+                                   vp, vp]),
+            "mp_place_d": (C.c_int, [vp, i32, i64, vp, vp, vp, vp, vp, vp, C.c_uint32, vp, vp,
+                                     vp, vp, vp]),
             "mp_generate_graph": (C.c_int, [C.c_int, i32, u64, u64, P(i32), P(i32), P(i64), vp,
                                             vp, vp, vp, vp]),
             "mp_random_topo_orders": (C.c_int, [P(MpCsr), i64, u64, i32, vp]),

@@ -1,0 +1,337 @@
+// K5 - placement heuristics over realized lifetimes, batched over problems:
+//   preallocate_pyramid (placement.cpp:25-62) and greedy_pack
+//   (placement.cpp:182-204), plus peak_mem = max(addr + size)
+//   (pipeline.cpp:270-275) of the resulting address plan.
+//
+// One CTA per problem (a problem = one lifetime vector over the shared edge
+// sizes, e.g. one candidate order). Both heuristics are sequential over edges,
+// so the parallelism inside a CTA is over the already-placed tensors:
+//
+// greedy_pack places edge e at the lowest offset x >= 0 with no placed,
+// lifetime-overlapping tensor w such that x < top_w && addr_w < x + size_e
+// (the reference's bump loop reaches exactly that x: every offset it skips is
+// covered by the tensor that made it jump, and it stops at a free one). In
+// terms of L_w = addr_w - size_e and R_w = top_w the forbidden offsets are the
+// open intervals (L_w, R_w); with the placed tensors kept sorted by address
+// (hence by L), x is the first gap of their union: M = max(0, R over the
+// prefix) up to the first conflicting w with L_w >= M. A CTA evaluates that
+// with one block-wide exclusive prefix-max over per-thread chunks, a chunk
+// sweep and a block min, then inserts e at its sorted position. Tensors stay
+// in append-only slots; the address order is an index array `ord` that each
+// thread shifts from its registers (4 bytes per entry). Per edge: O(placed/T)
+// work and five barriers.
+//
+// preallocate_pyramid is a block-wide arg-max per pick (duration, then size,
+// then the edge id's rank in byte order), the window narrowing each time.
+//
+// Shared memory: the placed set, 28 bytes per tensor (address, top, lifetime,
+// order index), so up to kPlaceMaxEntries tensors per problem.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "mp_internal.h"
+
+namespace mpb {
+namespace {
+
+constexpr int kChMax = 16;    // entries per thread in registers
+static_assert(512 * kChMax == kPlaceMaxEntries, "placed-set capacity");
+
+// Threads per problem: the smallest of 128/256/512 whose chunks hold every
+// tensor (16 per thread), so small graphs fit several problems per SM.
+template <int kPT>
+struct PlaceScratch {
+  long long wmax[kPT / 32];
+  int stop;
+  int pos;
+  long long x;
+  long long allmax;
+  int pick;
+  // pyramid arg-max per warp
+  int wd[kPT / 32];
+  unsigned long long ws[kPT / 32];
+  int wr[kPT / 32];
+  int we[kPT / 32];
+};
+
+__device__ __forceinline__ bool disjoint(int alo, int ahi, int blo, int bhi) {
+  return alo > ahi || blo > bhi || ahi < blo || bhi < alo;  // analysis.hpp:28-37
+}
+
+// pyramid order: longer lifetime, then larger size, then smaller id rank
+__device__ __forceinline__ bool pyr_better(int d, unsigned long long s, int r, int d2,
+                                           unsigned long long s2, int r2) {
+  if (d != d2) return d > d2;
+  if (s != s2) return s > s2;
+  return r < r2;
+}
+
+template <int kPT>
+__global__ void __launch_bounds__(kPT, 512 / kPT)
+    place_kernel(PlaceArgs a) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ PlaceScratch<kPT> ps;
+  const int E = a.num_edges;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kW = kPT / 32;
+  const int cap = a.cap;
+  unsigned long long* e_addr = reinterpret_cast<unsigned long long*>(smem);  // by slot
+  unsigned long long* e_top = e_addr + cap;
+  int2* e_life = reinterpret_cast<int2*>(e_top + cap);
+  int* ord = reinterpret_cast<int*>(e_life + cap);          // slots in address order
+  uint8_t* flag = reinterpret_cast<uint8_t*>(ord + cap);    // [E] fixed / taken
+
+  for (int64_t b = blockIdx.x; b < a.num_problems; b += gridDim.x) {
+    const int32_t* lo = a.lo + b * (int64_t)E;
+    const int32_t* hi = a.hi + b * (int64_t)E;
+    uint64_t* out_addr = a.addr + b * (int64_t)E;
+    uint8_t* out_has = a.has_addr + b * (int64_t)E;
+    int k = 0;                // placed tensors
+    unsigned long long peak = 0;
+    for (int e = tid; e < E; e += kPT) {
+      flag[e] = 0;
+      out_has[e] = 0;
+      out_addr[e] = 0;
+    }
+    __syncthreads();
+
+    // Place one tensor (size s, lifetime [elo, ehi]) at x, or - when `search` -
+    // at greedy_pack's lowest feasible offset; returns the offset.
+    auto place = [&](bool search, unsigned long long x, unsigned long long s, int elo,
+                     int ehi) -> unsigned long long {
+      const int ch = (k + kPT - 1) / kPT;
+      const int i0 = tid * ch;
+      int o[kChMax];
+#pragma unroll
+      for (int q = 0; q < kChMax; ++q) o[q] = (q < ch && i0 + q < k) ? ord[i0 + q] : -1;
+      if (search) {
+        long long cm = LLONG_MIN;  // max top over this chunk's conflicting tensors
+#pragma unroll
+        for (int q = 0; q < kChMax; ++q)
+          if (o[q] >= 0) {
+            const int2 l = e_life[o[q]];
+            if (!disjoint(elo, ehi, l.x, l.y)) {
+              const long long t = (long long)e_top[o[q]];
+              cm = t > cm ? t : cm;
+            }
+          }
+        // block exclusive prefix-max of cm (chunks are in address order)
+        long long incl = cm;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const long long v = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= d && v > incl) incl = v;
+        }
+        if (lane == 31) ps.wmax[warp] = incl;
+        if (tid == 0) ps.stop = INT_MAX;
+        __syncthreads();
+        long long before = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) before = LLONG_MIN;
+        for (int w = 0; w < warp; ++w) before = ps.wmax[w] > before ? ps.wmax[w] : before;
+        // sweep the chunk: the first conflicting tensor with L >= M leaves a gap at M
+        long long M = before > 0 ? before : 0;
+        int stop = INT_MAX;
+        long long xs = 0;
+#pragma unroll
+        for (int q = 0; q < kChMax; ++q)
+          if (stop == INT_MAX && o[q] >= 0) {
+            const int2 l = e_life[o[q]];
+            if (!disjoint(elo, ehi, l.x, l.y)) {
+              const long long L = (long long)e_addr[o[q]] - (long long)s;
+              const long long t = (long long)e_top[o[q]];
+              if (L >= M) {
+                stop = i0 + q;
+                xs = M;
+              } else if (t > M) {
+                M = t;
+              }
+            }
+          }
+        if (stop != INT_MAX) atomicMin(&ps.stop, stop);
+        if (tid == kPT - 1) {
+          long long all = incl;  // inclusive prefix at the last thread = max over all
+          for (int w = 0; w < warp; ++w) all = ps.wmax[w] > all ? ps.wmax[w] : all;
+          ps.allmax = all > 0 ? all : 0;
+        }
+        __syncthreads();
+        if (stop != INT_MAX && stop == ps.stop) ps.x = xs;
+        __syncthreads();
+        x = ps.stop != INT_MAX ? (unsigned long long)ps.x : (unsigned long long)ps.allmax;
+      }
+      // insert at the first address-order index whose address is >= x
+      int cnt = 0;
+#pragma unroll
+      for (int q = 0; q < kChMax; ++q)
+        if (o[q] >= 0) cnt += e_addr[o[q]] < x;
+      if (tid == 0) ps.pos = 0;
+      __syncthreads();
+      cnt = __reduce_add_sync(0xffffffffu, cnt);
+      if (lane == 0 && cnt) atomicAdd(&ps.pos, cnt);
+      __syncthreads();
+      const int p = ps.pos;
+#pragma unroll
+      for (int q = 0; q < kChMax; ++q)
+        if (o[q] >= 0 && i0 + q >= p) ord[i0 + q + 1] = o[q];
+      if (tid == 0) {
+        ord[p] = k;
+        e_addr[k] = x;
+        e_top[k] = x + s;
+        e_life[k] = make_int2(elo, ehi);
+      }
+      __syncthreads();
+      ++k;
+      return x;
+    };
+
+    // ---- fixed tensors: caller's preplaced map, or preallocate_pyramid ------------
+    if (a.pyramid) {
+      long long min_start = 0, max_end = LLONG_MAX;
+      unsigned long long base = 0;
+      while (max_end > min_start) {
+        int bd = INT_MIN, br = INT_MAX, be = -1;
+        unsigned long long bsz = 0;
+        for (int e = tid; e < E; e += kPT) {
+          const unsigned long long s = a.size[e];
+          if (flag[e] || s == 0) continue;
+          const int l = lo[e], h = hi[e];
+          if (l <= min_start || h >= max_end) continue;
+          const int d = h - l, r = a.id_rank ? a.id_rank[e] : e;
+          if (be < 0 || pyr_better(d, s, r, bd, bsz, br)) {
+            bd = d;
+            bsz = s;
+            br = r;
+            be = e;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const int d2 = __shfl_xor_sync(0xffffffffu, bd, o);
+          const unsigned long long s2 = __shfl_xor_sync(0xffffffffu, bsz, o);
+          const int r2 = __shfl_xor_sync(0xffffffffu, br, o);
+          const int e2 = __shfl_xor_sync(0xffffffffu, be, o);
+          if (e2 >= 0 && (be < 0 || pyr_better(d2, s2, r2, bd, bsz, br))) {
+            bd = d2;
+            bsz = s2;
+            br = r2;
+            be = e2;
+          }
+        }
+        if (lane == 0) {
+          ps.wd[warp] = bd;
+          ps.ws[warp] = bsz;
+          ps.wr[warp] = br;
+          ps.we[warp] = be;
+        }
+        __syncthreads();
+        if (warp == 0) {
+          bd = lane < kW ? ps.wd[lane] : INT_MIN;
+          bsz = lane < kW ? ps.ws[lane] : 0;
+          br = lane < kW ? ps.wr[lane] : INT_MAX;
+          be = lane < kW ? ps.we[lane] : -1;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const int d2 = __shfl_xor_sync(0xffffffffu, bd, o);
+            const unsigned long long s2 = __shfl_xor_sync(0xffffffffu, bsz, o);
+            const int r2 = __shfl_xor_sync(0xffffffffu, br, o);
+            const int e2 = __shfl_xor_sync(0xffffffffu, be, o);
+            if (e2 >= 0 && (be < 0 || pyr_better(d2, s2, r2, bd, bsz, br))) {
+              bd = d2;
+              bsz = s2;
+              br = r2;
+              be = e2;
+            }
+          }
+          if (lane == 0) ps.pick = be;
+        }
+        __syncthreads();
+        const int pick = ps.pick;
+        if (pick < 0) break;
+        const unsigned long long s = a.size[pick];
+        if (tid == 0) {
+          flag[pick] = 1;
+          out_addr[pick] = base;
+          out_has[pick] = 1;
+        }
+        place(false, base, s, lo[pick], hi[pick]);
+        base += s;
+        peak = base > peak ? base : peak;
+        min_start = lo[pick];
+        max_end = hi[pick];
+      }
+      if (tid == 0 && a.pyramid_base) a.pyramid_base[b] = base;
+    } else if (a.fixed) {
+      for (int e = 0; e < E; ++e) {  // uniform loop: preplaced maps are small
+        if (!a.fixed[e]) continue;
+        const unsigned long long x = a.fixed_addr[e], s = a.size[e];
+        if (tid == 0) {
+          flag[e] = 1;
+          out_addr[e] = x;
+          out_has[e] = 1;
+        }
+        place(false, x, s, lo[e], hi[e]);
+        peak = x + s > peak ? x + s : peak;
+      }
+    }
+    __syncthreads();
+
+    // ---- greedy_pack over the remaining data edges, in edge order -----------------
+    if (!a.pyramid_only) {
+      // the next edge's (size, lifetime) is loaded one step ahead (uniform loads)
+      unsigned long long s_nx = E > 0 ? a.size[0] : 0;
+      int lo_nx = E > 0 ? lo[0] : 0, hi_nx = E > 0 ? hi[0] : 0;
+      for (int e = 0; e < E; ++e) {
+        const unsigned long long s = s_nx;
+        const int elo = lo_nx, ehi = hi_nx;
+        if (e + 1 < E) {
+          s_nx = a.size[e + 1];
+          lo_nx = lo[e + 1];
+          hi_nx = hi[e + 1];
+        }
+        if (s == 0 || flag[e]) continue;  // uniform: flags were fixed before this loop
+        const unsigned long long x = place(true, 0, s, elo, ehi);
+        if (tid == 0) {
+          out_addr[e] = x;
+          out_has[e] = 1;
+        }
+        peak = x + s > peak ? x + s : peak;
+      }
+    }
+    if (tid == 0 && a.peak_mem) a.peak_mem[b] = peak;
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+size_t place_smem_bytes(int num_edges) {
+  const int cap = num_edges < kPlaceMaxEntries ? num_edges + 1 : kPlaceMaxEntries;
+  return (size_t)cap * (8 + 8 + 8 + 4) + (size_t)num_edges + 16;
+}
+
+template <int kPT>
+mp_status launch_place_t(const PlaceArgs& in, const mp_ctx* ctx, cudaStream_t st) {
+  PlaceArgs a = in;
+  a.cap = in.num_edges < kPlaceMaxEntries ? in.num_edges + 1 : kPlaceMaxEntries;
+  const size_t smem = place_smem_bytes(in.num_edges);
+  auto kern = place_kernel<kPT>;
+  MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPT, smem));
+  int64_t grid = (int64_t)ctx->num_sms * (per_sm > 0 ? per_sm : 1);
+  if (grid > in.num_problems) grid = in.num_problems;
+  kern<<<(unsigned)grid, kPT, smem, st>>>(a);
+  MP_CUDA(cudaGetLastError());
+  return MP_OK;
+}
+
+mp_status launch_place(const PlaceArgs& in, const mp_ctx* ctx, cudaStream_t st) {
+  if (in.num_problems <= 0 || in.num_edges == 0) return MP_OK;
+  // + preplaced entries never exceed num_edges: the placed set holds <= E tensors
+  if (in.num_edges <= 128 * kChMax) return launch_place_t<128>(in, ctx, st);
+  if (in.num_edges <= 256 * kChMax) return launch_place_t<256>(in, ctx, st);
+  return launch_place_t<512>(in, ctx, st);
+}
+
+}  // namespace mpb

@@ -697,6 +697,99 @@ mp_status mp_validate_pairs_d(mp_ctx* ctx, int32_t E, const int32_t* d_lo, const
   return pair_sweep_d(ctx, a, d_row_off, d_viol, cap, num_viol, st);
 }
 
+// ---- placement (K5) ---------------------------------------------------------------
+static mp_status place_check(int32_t E, int64_t B, uint32_t flags, const void* fixed) {
+  if (E < 0 || B < 0) return invalid_arg("negative size");
+  if ((flags & (MP_PLACE_PYRAMID | MP_PLACE_PYRAMID_ONLY)) && fixed)
+    return invalid_arg("a preplaced map and MP_PLACE_PYRAMID are exclusive");
+  if (E > kPlaceMaxEntries) {
+    set_error("Capacity: " + std::to_string(E) + " edges exceed the placement kernel's " +
+              std::to_string(kPlaceMaxEntries) + " per problem");
+    return MP_E_CAPACITY;
+  }
+  return MP_OK;
+}
+
+mp_status mp_place_d(mp_ctx* ctx, int32_t E, int64_t B, const int32_t* d_lo, const int32_t* d_hi,
+                     const uint64_t* d_size, const int32_t* d_id_rank, const uint8_t* d_fixed,
+                     const uint64_t* d_fixed_addr, uint32_t flags, uint64_t* d_addr,
+                     uint8_t* d_has_addr, uint64_t* d_peak_mem, uint64_t* d_pyramid_base,
+                     void* stream) {
+  if (!ctx) return invalid_arg("null context");
+  MP_TRY(place_check(E, B, flags, d_fixed));
+  if (E > 0 && B > 0 && (!d_lo || !d_hi || !d_size || !d_addr || !d_has_addr))
+    return invalid_arg("null argument");
+  if (d_fixed && !d_fixed_addr) return invalid_arg("fixed without fixed_addr");
+  DeviceGuard guard(ctx->device);
+  PlaceArgs a;
+  a.num_edges = E;
+  a.num_problems = B;
+  a.lo = d_lo;
+  a.hi = d_hi;
+  a.size = d_size;
+  a.id_rank = d_id_rank;
+  a.fixed = d_fixed;
+  a.fixed_addr = d_fixed_addr;
+  a.pyramid = (flags & (MP_PLACE_PYRAMID | MP_PLACE_PYRAMID_ONLY)) ? 1 : 0;
+  a.pyramid_only = (flags & MP_PLACE_PYRAMID_ONLY) ? 1 : 0;
+  a.addr = d_addr;
+  a.has_addr = d_has_addr;
+  a.peak_mem = d_peak_mem;
+  a.pyramid_base = d_pyramid_base;
+  return launch_place(a, ctx, static_cast<cudaStream_t>(stream));
+}
+
+mp_status mp_place(mp_ctx* ctx, int32_t E, int64_t B, const int32_t* lo, const int32_t* hi,
+                   const uint64_t* size, const int32_t* id_rank, const uint8_t* fixed,
+                   const uint64_t* fixed_addr, uint32_t flags, uint64_t* addr, uint8_t* has_addr,
+                   uint64_t* peak_mem, uint64_t* pyramid_base) {
+  if (!ctx) return invalid_arg("null context");
+  MP_TRY(place_check(E, B, flags, fixed));
+  if (E == 0 || B == 0) {
+    for (int64_t b = 0; b < B; ++b) {
+      if (peak_mem) peak_mem[b] = 0;
+      if (pyramid_base) pyramid_base[b] = 0;
+    }
+    return MP_OK;
+  }
+  if (!lo || !hi || !size || !addr || !has_addr) return invalid_arg("null argument");
+  if (fixed && !fixed_addr) return invalid_arg("fixed without fixed_addr");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const size_t e = (size_t)E, be = (size_t)B * e, b = (size_t)B;
+  MP_TRY(ctx->scratch[0].reserve(
+      Carver::size_of({4 * be, 4 * be, 8 * e, 4 * e, e, 8 * e, 8 * be, be, 8 * b, 8 * b})));
+  Carver cv(ctx->scratch[0].ptr);
+  int32_t* d_lo = cv.take<int32_t>(be);
+  int32_t* d_hi = cv.take<int32_t>(be);
+  uint64_t* d_size = cv.take<uint64_t>(e);
+  int32_t* d_rank = cv.take<int32_t>(e);
+  uint8_t* d_fixed = cv.take<uint8_t>(e);
+  uint64_t* d_faddr = cv.take<uint64_t>(e);
+  uint64_t* d_addr = cv.take<uint64_t>(be);
+  uint8_t* d_has = cv.take<uint8_t>(be);
+  uint64_t* d_peak = cv.take<uint64_t>(b);
+  uint64_t* d_base = cv.take<uint64_t>(b);
+  MP_CUDA(cudaMemcpyAsync(d_lo, lo, 4 * be, cudaMemcpyHostToDevice, st));
+  MP_CUDA(cudaMemcpyAsync(d_hi, hi, 4 * be, cudaMemcpyHostToDevice, st));
+  MP_CUDA(cudaMemcpyAsync(d_size, size, 8 * e, cudaMemcpyHostToDevice, st));
+  if (id_rank) MP_CUDA(cudaMemcpyAsync(d_rank, id_rank, 4 * e, cudaMemcpyHostToDevice, st));
+  if (fixed) {
+    MP_CUDA(cudaMemcpyAsync(d_fixed, fixed, e, cudaMemcpyHostToDevice, st));
+    MP_CUDA(cudaMemcpyAsync(d_faddr, fixed_addr, 8 * e, cudaMemcpyHostToDevice, st));
+  }
+  MP_TRY(mp_place_d(ctx, E, B, d_lo, d_hi, d_size, id_rank ? d_rank : nullptr,
+                    fixed ? d_fixed : nullptr, fixed ? d_faddr : nullptr, flags, d_addr, d_has,
+                    d_peak, d_base, st));
+  MP_CUDA(cudaMemcpyAsync(addr, d_addr, 8 * be, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaMemcpyAsync(has_addr, d_has, be, cudaMemcpyDeviceToHost, st));
+  if (peak_mem) MP_CUDA(cudaMemcpyAsync(peak_mem, d_peak, 8 * b, cudaMemcpyDeviceToHost, st));
+  if (pyramid_base)
+    MP_CUDA(cudaMemcpyAsync(pyramid_base, d_base, 8 * b, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaStreamSynchronize(st));
+  return MP_OK;
+}
+
 mp_status mp_addresses_feasible(mp_ctx* ctx, int32_t E, const int32_t* lo, const int32_t* hi,
                                 const uint64_t* size, const uint8_t* has_addr,
                                 const uint64_t* addr, int32_t* feasible) {

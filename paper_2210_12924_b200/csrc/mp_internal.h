@@ -164,6 +164,27 @@ mp_status pairs_count(const PairArgs& a, int num_sms, void* d_scratch, int64_t* 
 // Fill pass using d_row_off from pairs_count.
 mp_status pairs_fill(const PairArgs& a, int num_sms, void* d_scratch, const int64_t* d_row_off,
                      int32_t* d_pairs, cudaStream_t st);
+// K5 placement (k_place.cu): preallocate_pyramid / greedy_pack / peak_mem per problem.
+constexpr int kPlaceMaxEntries = 8192;  // placed tensors per problem (shared memory)
+struct PlaceArgs {
+  int32_t num_edges = 0;
+  int64_t num_problems = 0;
+  const int32_t* lo = nullptr;         // [B][E]
+  const int32_t* hi = nullptr;         // [B][E]
+  const uint64_t* size = nullptr;      // [E]
+  const int32_t* id_rank = nullptr;    // [E] or null (edge index order)
+  const uint8_t* fixed = nullptr;      // [E] preplaced map or null
+  const uint64_t* fixed_addr = nullptr;
+  int pyramid = 0;                     // fixed = preallocate_pyramid(lifetimes)
+  int pyramid_only = 0;                // stop after the pyramid
+  uint64_t* addr = nullptr;            // [B][E]
+  uint8_t* has_addr = nullptr;         // [B][E]
+  uint64_t* peak_mem = nullptr;        // [B] or null
+  uint64_t* pyramid_base = nullptr;    // [B] or null
+  int cap = 0;                         // set by launch_place
+};
+size_t place_smem_bytes(int num_edges);
+mp_status launch_place(const PlaceArgs& a, const mp_ctx* ctx, cudaStream_t st);
 mp_status launch_peak_mem(int32_t num_edges, const uint64_t* d_size, const uint8_t* d_has,
                           const uint64_t* d_addr, uint64_t* d_out, cudaStream_t st);
 

@@ -257,6 +257,16 @@ class Graph:
             out[s].append(e)
         return out
 
+    def id_rank(self) -> np.ndarray:
+        """Rank of each edge id in byte-lexicographic order (std::string's
+        operator<, the pyramid tie-break at placement.cpp:48-50)."""
+        if getattr(self, "_id_rank", None) is None or len(self._id_rank) != self.E:
+            r = np.zeros(max(self.E, 1), np.int32)
+            for k, e in enumerate(sorted(range(self.E), key=lambda e: self.edge_ids[e].encode())):
+                r[e] = k
+            self._id_rank = r
+        return self._id_rank
+
     def csr(self) -> dict:
         return {"n": self.n, "edge_src": self.edge_src, "sink_off": self.sink_off,
                 "sinks": self.sinks, "edge_size": self.edge_size}

@@ -12,7 +12,7 @@ from __future__ import annotations
 import ctypes as C
 import json
 from dataclasses import dataclass, field
-from typing import Mapping, Sequence
+from typing import Mapping, Optional, Sequence
 
 import numpy as np
 
@@ -100,6 +100,14 @@ def load_plan(text: str) -> MemoryPlan:
     plan.peak_step = int(doc["timeline"]["peak_step"])
     plan.provenance = dict(doc["provenance"])
     return plan
+
+
+@dataclass
+class PrePlacement:
+    """memplan::PrePlacement (placement.hpp:26-30)."""
+    assigned: dict
+    remaining: list
+    reserved_base: int = 0
 
 
 def fragmentation(mr: int, rs: int) -> float:
@@ -407,6 +415,60 @@ class Planner:
         _native.check(_native.lib().mp_peak_mem(self.ctx, graph.E, graph.edge_size.ctypes.data,
                                                 has.ctypes.data, ad.ctypes.data, C.byref(out)))
         return int(out.value)
+
+    # ---- placement heuristics (K5, k_place.cu) ---------------------------------------
+    PLACE_PYRAMID = 1
+    PLACE_PYRAMID_ONLY = 2
+
+    def place_batch(self, graph: Graph, lo, hi, pyramid: bool = True, pyramid_only: bool = False,
+                    preplaced: Optional[Mapping[int, int]] = None):
+        """Batched placement over B lifetime vectors (lo/hi [B][E]): the
+        preplaced map (preallocate_pyramid's when ``pyramid``) then greedy_pack
+        (placement.cpp:25-62, 182-204). Returns (addr u64[B][E], has u8[B][E],
+        peak_mem u64[B], pyramid_base u64[B])."""
+        lo = np.ascontiguousarray(np.atleast_2d(lo), np.int32)
+        hi = np.ascontiguousarray(np.atleast_2d(hi), np.int32)
+        B, E = lo.shape[0], graph.E
+        if lo.shape != (B, E) or hi.shape != (B, E):
+            raise ValueError("lo/hi must be [B][num_edges]")
+        flags = (self.PLACE_PYRAMID if pyramid else 0) | (self.PLACE_PYRAMID_ONLY if pyramid_only
+                                                           else 0)
+        fx = fa = None
+        if preplaced:
+            fx, fa = self._addr_arrays(graph, preplaced)
+        addr = np.zeros((B, max(E, 1)), np.uint64)
+        has = np.zeros((B, max(E, 1)), np.uint8)
+        peak = np.zeros(max(B, 1), np.uint64)
+        base = np.zeros(max(B, 1), np.uint64)
+        _native.check(_native.lib().mp_place(
+            self.ctx, E, B, lo.ctypes.data, hi.ctypes.data, graph.edge_size.ctypes.data,
+            graph.id_rank().ctypes.data, None if fx is None else fx.ctypes.data,
+            None if fa is None else fa.ctypes.data, flags, addr.ctypes.data, has.ctypes.data,
+            peak.ctypes.data, base.ctypes.data))
+        return addr[:, :E], has[:, :E], peak[:B], base[:B]
+
+    def place_batch_d(self, num_edges, num_problems, d_lo, d_hi, d_size, d_id_rank, flags,
+                      d_addr, d_has, d_peak=None, d_base=None, d_fixed=None, d_fixed_addr=None,
+                      stream: int | None = None) -> None:
+        """Device-pointer form of place_batch (mp_place_d), stream-ordered."""
+        _native.check(_native.lib().mp_place_d(
+            self.ctx, int(num_edges), int(num_problems), _native.ptr(d_lo), _native.ptr(d_hi),
+            _native.ptr(d_size), _native.ptr(d_id_rank), _native.ptr(d_fixed),
+            _native.ptr(d_fixed_addr), int(flags), _native.ptr(d_addr), _native.ptr(d_has),
+            _native.ptr(d_peak), _native.ptr(d_base), stream))
+
+    def preallocate_pyramid(self, graph: Graph, lo, hi) -> "PrePlacement":
+        """preallocate_pyramid (placement.cpp:25-62) -> PrePlacement."""
+        addr, has, _, base = self.place_batch(graph, lo, hi, pyramid=True, pyramid_only=True)
+        assigned = {int(e): int(addr[0, e]) for e in np.nonzero(has[0])[0]}
+        remaining = [e for e in range(graph.E) if graph.edge_size[e] > 0 and e not in assigned]
+        return PrePlacement(assigned, remaining, int(base[0]))
+
+    def greedy_pack(self, graph: Graph, lo, hi,
+                    preplaced: Optional[Mapping[int, int]] = None) -> dict:
+        """greedy_pack (placement.cpp:182-204): {edge index: address} incl. preplaced."""
+        addr, has, _, _ = self.place_batch(graph, lo, hi, pyramid=False, preplaced=preplaced or {})
+        return {int(e): int(addr[0, e]) for e in np.nonzero(has[0])[0]}
 
     @staticmethod
     def _addr_arrays(graph: Graph, addresses: Mapping[int, int]):

@@ -105,6 +105,16 @@ def order_case(g: "O.RefGraph", order):
     c["pairs"] = g.encode_address_pairs(lo, hi, filter_pairs=True).tolist()
     c["pairs_unfiltered_count"] = g.encode_address_pairs(lo, hi, filter_pairs=False,
                                                          want_pairs=False)
+    # placement heuristics (placement.cpp:25-62, 182-204) and the arena baseline (:150-180)
+    taken, paddr, base = g.preallocate_pyramid(lo, hi)
+    ga, gh = g.greedy_pack_fixed(lo, hi, taken, paddr)
+    pa, ph = g.greedy_pack_fixed(lo, hi)
+    c["placement"] = {"pyramid_taken": taken.tolist(), "pyramid_addr": [int(x) for x in paddr],
+                      "pyramid_base": int(base),
+                      "greedy_pyramid_addr": [int(x) for x in ga], "greedy_pyramid_has": gh.tolist(),
+                      "greedy_addr": [int(x) for x in pa], "greedy_has": ph.tolist()}
+    c["baseline"] = {"first_fit": list(g.run_baseline(order, best_fit=False)),
+                     "best_fit": list(g.run_baseline(order, best_fit=True))}
     return c
 
 

@@ -116,3 +116,33 @@ def test_chain3_plan_graph(golden):
     assert plan["addresses"] == {"e1": 0, "e2": 4}
     assert plan["peak_mem"] == 6 and plan["timeline"]["peak_rs"] == 6
     assert O.peak_mem([4, 2], [1, 1], [0, 4]) == 6
+
+
+def _id_rank(rec):
+    import paper_2210_12924_b200 as mp
+    return mp.load_graph(rec["graph_json"]).id_rank()
+
+
+def test_golden_placement(golden):
+    """or_preallocate_pyramid / or_greedy_pack vs the reference's own outputs
+    (placement.cpp:25-62, 182-204), plain and on top of the pyramid."""
+    checked = 0
+    for rec in golden["graphs"]:
+        size = np.asarray(rec["csr"]["edge_size"], np.uint64)
+        rank = _id_rank(rec)
+        for case in rec["orders"]:
+            if "placement" not in case:
+                continue
+            p = case["placement"]
+            taken, addr, base = O.preallocate_pyramid(case["lo"], case["hi"], size, rank)
+            assert taken.tolist() == p["pyramid_taken"], rec["name"]
+            assert [int(a) if t else 0 for a, t in zip(addr, taken)] == p["pyramid_addr"]
+            assert base == p["pyramid_base"]
+            ga, gh = O.greedy_pack(case["lo"], case["hi"], size, taken, addr)
+            assert gh.tolist() == p["greedy_pyramid_has"]
+            assert [int(a) if h else 0 for a, h in zip(ga, gh)] == p["greedy_pyramid_addr"]
+            pa, ph = O.greedy_pack(case["lo"], case["hi"], size)
+            assert ph.tolist() == p["greedy_has"]
+            assert [int(a) if h else 0 for a, h in zip(pa, ph)] == p["greedy_addr"]
+            checked += 1
+    assert checked >= 70
