@@ -368,6 +368,75 @@ def run_place(args, cfg):
     return 0
 
 
+def run_arena(args, cfg):
+    """Arena baseline (K6): run_baseline (placement.cpp:150-180) - the free-list
+    allocator replayed over every candidate order, one warp per candidate, orders
+    resident in HBM - beside the reference's own run_baseline on the host cores."""
+    import torch
+    import paper_2210_12924_b200 as mp
+    from concurrent.futures import ThreadPoolExecutor
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    g = load_graph(cfg)
+    planner = mp.Planner(0)
+    dg = planner.upload(g)
+    B = cfg["candidates"]
+    orders = mp.random_topo_orders(g, B, seed=31)
+    d_o = torch.from_numpy(orders).to(dev)
+    d_mr = torch.zeros(B, dtype=torch.int64, device=dev)
+    d_rs = torch.zeros(B, dtype=torch.int64, device=dev)
+    d_fr = torch.zeros(B, dtype=torch.float64, device=dev)
+    d_v = torch.zeros(B, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+
+    def run():
+        planner.run_baseline_d(dg, d_o, B, False, d_mr, d_rs, d_fr, d_v, stream=st)
+
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    reps = max(1, min(args.steps, 10))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        run()
+    b.record()
+    b.synchronize()
+    t = a.elapsed_time(b) / reps / 1e3
+    orc = O.Oracle.from_csr(g.csr())
+    mr = d_mr.cpu().numpy().view(np.uint64)
+    for i in range(0, B, max(1, B // 8)):   # parity spot check vs the C restatement
+        assert (int(mr[i]),) == orc.run_baseline(orders[i])[:1], i
+    cpu = None
+    if O.ref_available():
+        rg = O.RefGraph.load(mp.save_graph(g))
+        cores = os.cpu_count() or 1
+        sample = min(B, 16 * cores)
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(cores) as ex:
+            list(ex.map(lambda i: rg.run_baseline(orders[i]), range(sample)))
+        tr = time.perf_counter() - t0
+        cpu = {"value": sample / tr, "unit": "orders/s", "cores": cores, "kind": "reference",
+               "sample": f"{sample} candidate orders, memplan::run_baseline (first fit, "
+                         f"oracle/_ref -O3) on {cores} host threads"}
+    line = {
+        "metric": "candidate orders replayed through the arena baseline/sec (run_baseline)",
+        "value": B / t, "unit": "orders/s", "n_gpus": 1, "steps": reps, "warmup": 3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic",
+        "config": {"workload": cfg["workload"], "nodes": g.n, "edges": g.E, "orders": B,
+                   "policy": "first_fit"},
+        "ms_per_step": t * 1e3, "gpu_launches": reps, "cpu_baseline": cpu,
+        "bound": "latency: sequential replay per order, warp-cooperative list operations",
+        "timing": "CUDA events around stream-ordered mp_run_baseline_d launches",
+    }
+    print(json.dumps(line))
+    planner.close()
+    return 0
+
+
 # ---- our arm -------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
@@ -377,7 +446,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--place-batch", type=int, default=4096)
-    ap.add_argument("--mode", default="score", choices=["score", "pairs", "place"],
+    ap.add_argument("--mode", default="score", choices=["score", "pairs", "place", "arena"],
                     help="score: candidate scoring (the headline); pairs: overlap-pair "
                          "generation (K2) + address-plan validation (K4) on one lifetime set")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -391,6 +460,8 @@ def main():
         return run_pairs(args, cfg)
     if args.mode == "place":
         return run_place(args, cfg)
+    if args.mode == "arena":
+        return run_arena(args, cfg)
 
     import torch
     import torch.distributed as dist

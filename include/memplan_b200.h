@@ -240,6 +240,22 @@ mp_status mp_place_d(mp_ctx* ctx, int32_t num_edges, int64_t num_problems, const
                      uint64_t* d_addr, uint8_t* d_has_addr, uint64_t* d_peak_mem,
                      uint64_t* d_pyramid_base, void* stream);
 
+/* ---- (§8f-4) arena baseline: run_baseline over candidate orders ---------------
+ * run_baseline (placement.cpp:150-180): the free-list Arena (placement.cpp:69-148,
+ * first fit, or best fit when best_fit != 0) replayed over every order of
+ * orders [num_orders][n]: mr_peak (allocator high-water mark), rs_at_peak (live
+ * bytes when it was set) and fragmentation (placement.cpp:64-67, computed in
+ * double as the reference does). valid[c] = 0 where the reference throws
+ * InvalidOrder (the other outputs are then 0). Returns MP_E_CAPACITY when the
+ * per-candidate state (about 4 n + 20 num_edges bytes) exceeds shared memory. */
+mp_status mp_run_baseline(mp_ctx* ctx, const mp_graph* g, const int32_t* orders,
+                          int64_t num_orders, int best_fit, uint64_t* mr_peak,
+                          uint64_t* rs_at_peak, double* fragmentation, uint8_t* valid);
+mp_status mp_run_baseline_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_orders,
+                            int64_t num_orders, int best_fit, uint64_t* d_mr_peak,
+                            uint64_t* d_rs_at_peak, double* d_fragmentation, uint8_t* d_valid,
+                            void* stream);
+
 /* ---- workload helpers (host C++, not on the measured path) ----------------------
  * Deterministic graph families with the semantics of generate_graph
  * (generate.cpp:45-158; chain = 0, fork_join = 1, training_like = 2).

@@ -294,3 +294,137 @@ void or_greedy_pack(int32_t num_edges, const int32_t* lo, const int32_t* hi, con
     has[e] = 1;
   }
 }
+
+/* ---- run_baseline (placement.cpp:69-180) ------------------------------------ */
+typedef struct {
+  uint64_t addr, size;
+  int free_;
+  int32_t edge;
+} or_block;
+
+typedef struct {
+  or_block* b;
+  int64_t n, cap;
+} or_arena;
+
+static void or_arena_insert(or_arena* a, int64_t at, or_block blk) {
+  if (a->n == a->cap) {
+    a->cap = a->cap ? 2 * a->cap : 16;
+    a->b = (or_block*)realloc(a->b, (size_t)a->cap * sizeof(or_block));
+  }
+  memmove(a->b + at + 1, a->b + at, (size_t)(a->n - at) * sizeof(or_block));
+  a->b[at] = blk;
+  ++a->n;
+}
+
+static void or_arena_erase(or_arena* a, int64_t at) {
+  memmove(a->b + at, a->b + at + 1, (size_t)(a->n - at - 1) * sizeof(or_block));
+  --a->n;
+}
+
+static uint64_t or_arena_top(const or_arena* a) {
+  return a->n ? a->b[a->n - 1].addr + a->b[a->n - 1].size : 0;
+}
+
+/* Arena::allocate (placement.cpp:80-101) and grow (:117-128) */
+static void or_arena_allocate(or_arena* a, int32_t edge, uint64_t size, int best_fit) {
+  int64_t pick = -1;
+  for (int64_t i = 0; i < a->n; ++i) {
+    if (!a->b[i].free_ || a->b[i].size < size) continue;
+    if (!best_fit) {
+      pick = i;
+      break;
+    }
+    if (pick < 0 || a->b[i].size < a->b[pick].size) pick = i;
+  }
+  if (pick < 0) {
+    if (a->n && a->b[a->n - 1].free_) {
+      or_block* last = &a->b[a->n - 1];
+      last->size = size;
+      last->free_ = 0;
+      last->edge = edge;
+      return;
+    }
+    or_block nb = {or_arena_top(a), size, 0, edge};
+    or_arena_insert(a, a->n, nb);
+    return;
+  }
+  const uint64_t addr = a->b[pick].addr;
+  if (a->b[pick].size > size) {
+    or_block rest = {addr + size, a->b[pick].size - size, 1, -1};
+    a->b[pick].size = size;
+    or_arena_insert(a, pick + 1, rest);
+  }
+  a->b[pick].free_ = 0;
+  a->b[pick].edge = edge;
+}
+
+/* Arena::release (:103-111) + coalesce (:130-139) */
+static void or_arena_release(or_arena* a, int32_t edge) {
+  for (int64_t i = 0; i < a->n; ++i) {
+    if (a->b[i].free_ || a->b[i].edge != edge) continue;
+    a->b[i].free_ = 1;
+    a->b[i].edge = -1;
+    if (i + 1 < a->n && a->b[i + 1].free_) {
+      a->b[i].size += a->b[i + 1].size;
+      or_arena_erase(a, i + 1);
+    }
+    if (i > 0 && a->b[i - 1].free_) {
+      a->b[i - 1].size += a->b[i].size;
+      or_arena_erase(a, i);
+    }
+    return;
+  }
+}
+
+int or_run_baseline(const or_graph* g, const int32_t* order, int64_t len, int best_fit,
+                    uint64_t* mr_peak, uint64_t* rs_at_peak, double* frag) {
+  const int32_t n = g->n, E = g->num_edges;
+  int32_t* lo = (int32_t*)malloc(sizeof(int32_t) * (E ? E : 1));
+  int32_t* hi = (int32_t*)malloc(sizeof(int32_t) * (E ? E : 1));
+  if (or_lifetimes_from_order(g, order, len, lo, hi)) {
+    free(lo);
+    free(hi);
+    return 1;
+  }
+  /* frees[t]: data edges whose hi + 1 == t, in edge order (placement.cpp:155-158) */
+  int64_t* off = (int64_t*)calloc((size_t)n + 3, sizeof(int64_t));
+  int32_t* lst = (int32_t*)malloc(sizeof(int32_t) * (E ? E : 1));
+  for (int32_t e = 0; e < E; ++e)
+    if (g->edge_size[e] > 0) ++off[hi[e] + 1 + 1];
+  for (int32_t t = 0; t <= n + 1; ++t) off[t + 1] += off[t];
+  {
+    int64_t* cur = (int64_t*)malloc(sizeof(int64_t) * ((size_t)n + 2));
+    memcpy(cur, off, sizeof(int64_t) * ((size_t)n + 2));
+    for (int32_t e = 0; e < E; ++e)
+      if (g->edge_size[e] > 0) lst[cur[hi[e] + 1]++] = e;
+    free(cur);
+  }
+  or_arena a = {0, 0, 0};
+  uint64_t live = 0, mr = 0, rs = 0;
+  for (int32_t t = 1; t <= n; ++t) {
+    for (int64_t q = off[t]; q < off[t + 1]; ++q) {
+      or_arena_release(&a, lst[q]);
+      live -= g->edge_size[lst[q]];
+    }
+    const int32_t v = order[t - 1];
+    for (int32_t e = 0; e < E; ++e) {  /* fanout(v) in edge order */
+      if (g->edge_src[e] != v || g->edge_size[e] == 0) continue;
+      or_arena_allocate(&a, e, g->edge_size[e], best_fit);
+      live += g->edge_size[e];
+      if (or_arena_top(&a) > mr) {
+        mr = or_arena_top(&a);
+        rs = live;
+      }
+    }
+  }
+  *mr_peak = mr;
+  *rs_at_peak = rs;
+  *frag = or_fragmentation(mr, rs);
+  free(a.b);
+  free(off);
+  free(lst);
+  free(lo);
+  free(hi);
+  return 0;
+}

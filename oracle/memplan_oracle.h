@@ -90,6 +90,12 @@ uint64_t or_preallocate_pyramid(int32_t num_edges, const int32_t* lo, const int3
 void or_greedy_pack(int32_t num_edges, const int32_t* lo, const int32_t* hi, const uint64_t* size,
                     const uint8_t* fixed, uint64_t* addr, uint8_t* has);
 
+/* run_baseline (placement.cpp:150-180) with the free-list Arena of
+ * placement.cpp:69-148, literally. best_fit: FitPolicy::kBestFit. Returns 0, or
+ * 1 for InvalidOrder (lifetimes_from_order throws). */
+int or_run_baseline(const or_graph* g, const int32_t* order, int64_t len, int best_fit,
+                    uint64_t* mr_peak, uint64_t* rs_at_peak, double* frag);
+
 #ifdef __cplusplus
 }
 #endif

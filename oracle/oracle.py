@@ -91,6 +91,8 @@ def olib():
         lib.or_preallocate_pyramid.argtypes = [C.c_int32, _i32p, _i32p, _u64p, _i32p, _u8p, _u64p]
         lib.or_preallocate_pyramid.restype = C.c_uint64
         lib.or_greedy_pack.argtypes = [C.c_int32, _i32p, _i32p, _u64p, _vp, _u64p, _u8p]
+        lib.or_run_baseline.argtypes = [gp, _i32p, C.c_int64, C.c_int, C.POINTER(C.c_uint64),
+                                        C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
         _olib = lib
     return _olib
 
@@ -146,6 +148,15 @@ class Oracle:
         olib().or_timeline_from_lifetimes(C.byref(self._g), lo, hi, int(horizon), _opt_ptr(b),
                                           C.byref(pr), C.byref(ps))
         return (b[:horizon] if want_bytes else None), int(pr.value), int(ps.value)
+
+    def run_baseline(self, order, best_fit=False):
+        """placement.cpp:150-180 -> (mr_peak, rs_at_peak, fragmentation) or None (invalid)."""
+        mr, rs, fr = C.c_uint64(), C.c_uint64(), C.c_double()
+        o = _c(order, np.int32)
+        if olib().or_run_baseline(C.byref(self._g), o, len(o), int(best_fit), C.byref(mr), C.byref(rs),
+                                  C.byref(fr)):
+            return None
+        return mr.value, rs.value, fr.value
 
     def realized_lifetimes(self, timestep_of, horizon):
         ts = np.ascontiguousarray(timestep_of, np.int32)
@@ -409,6 +420,15 @@ class RefGraph:
                                                   b.ctypes.data_as(C.c_void_p), C.byref(pr),
                                                   C.byref(ps)))
         return b[:horizon], int(pr.value), int(ps.value)
+
+    def run_baseline(self, order, best_fit=False):
+        """placement.cpp:150-180 -> (mr_peak, rs_at_peak, fragmentation) or None (invalid)."""
+        mr, rs, fr = C.c_uint64(), C.c_uint64(), C.c_double()
+        o = _c(order, np.int32)
+        if olib().or_run_baseline(C.byref(self._g), o, len(o), int(best_fit), C.byref(mr), C.byref(rs),
+                                  C.byref(fr)):
+            return None
+        return mr.value, rs.value, fr.value
 
     def realized_lifetimes(self, timestep_of, horizon):
         ts = np.ascontiguousarray(timestep_of, np.int32)

@@ -6,7 +6,7 @@ Public surface (mirrors the reference memplan API for the hot path):
   Planner: lifetimes_from_order, realized_lifetimes, resident_bytes_per_step,
            peak_resident_bytes, timeline_from_lifetimes, score_orders, argmin,
            encode_address_pairs, validate_plan, addresses_feasible, peak_mem,
-           preallocate_pyramid, greedy_pack, place_batch
+           preallocate_pyramid, greedy_pack, place_batch, run_baseline
   fragmentation, format_report, random_topo_orders      (planner.py)
 The compute path is the native library lib/libmemplan_b200.so (C ABI in
 include/memplan_b200.h); there is no CPU fallback.
@@ -14,12 +14,12 @@ include/memplan_b200.h); there is no CPU fallback.
 from . import errors
 from .graph import (EdgeKind, Graph, Node, NodeRole, TensorEdge, generate_graph,
                     graph_from_lists, load_graph, load_graph_file, save_graph)
-from .planner import (DeviceGraph, ExecutionSequence, Interval, MemoryPlan, Planner,
+from .planner import (BaselineResult, DeviceGraph, ExecutionSequence, Interval, MemoryPlan, Planner,
                       PrePlacement, ResidentTimeline, ScoreResult, format_report, fragmentation,
                       intervals_disjoint, load_plan, random_topo_orders)
 
 __all__ = [
-    "errors", "EdgeKind", "Graph", "Node", "NodeRole", "TensorEdge", "generate_graph",
+    "BaselineResult", "errors", "EdgeKind", "Graph", "Node", "NodeRole", "TensorEdge", "generate_graph",
     "graph_from_lists", "load_graph", "load_graph_file", "save_graph", "DeviceGraph",
     "ExecutionSequence", "Interval", "MemoryPlan", "Planner", "PrePlacement", "ResidentTimeline",
     "ScoreResult",

@@ -1,0 +1,369 @@
+// K6 - the arena baseline run_baseline (placement.cpp:150-180), batched over
+// candidate orders: the free-list allocator (placement.cpp:69-148) replayed
+// over each order, reporting the allocator high-water mark (mr_peak), the live
+// bytes when it was set (rs_at_peak) and their fragmentation (placement.cpp:64-67).
+//
+// One warp per candidate, its state in shared memory:
+//   pos[n]            1-based position of each node (order validity, lifetimes)
+//   fstart[n+3]       frees bucketed by timestep (hi + 1), stable in edge order,
+//   flist[E]          as placement.cpp:155-158 builds them
+//   blocks[cap]       the arena: (size, edge or -1 when free), address-sorted and
+//                     contiguous, so addresses are implicit and top() is a sum
+// The block list gets kArenaCap entries first (the live-block count is far
+// below its 2E + 2 bound on real graphs); a candidate that would overflow it is
+// marked and replayed again by a second launch with the full bound. pos and
+// the block list share storage (pos is dead once the frees are bucketed).
+// Each allocate / release is warp-cooperative over the block list: a ballot
+// finds the first fit (or an arg-min the best fit) or the released edge, and
+// splits / coalescing shift the list 32 entries per step. The replay itself is
+// sequential in time, as the reference's is; the GPU's parallelism is the
+// candidates (thousands of orders at once) and the 32 lanes per operation.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+#include <cstdlib>
+
+#include "mp_internal.h"
+
+namespace mpb {
+namespace {
+
+constexpr int kArenaWarps = 1;  // candidates per CTA (shared memory bound)
+constexpr uint8_t kOverflow = 2;  // valid[] marker: replay again with the full block list
+
+struct ArenaLayout {
+  int n, E, cap;
+  __host__ __device__ size_t fstart_off() const { return 0; }
+  __host__ __device__ size_t flist_off() const {
+    return align(fstart_off() + 4 * ((size_t)n + 3));
+  }
+  // pos [n] and the block list (size [cap], edge [cap]) share this region
+  __host__ __device__ size_t pos_off() const { return align(flist_off() + 4 * (size_t)E); }
+  __host__ __device__ size_t bsize_off() const { return pos_off(); }
+  __host__ __device__ size_t bedge_off() const { return align(bsize_off() + 8 * (size_t)cap); }
+  __host__ __device__ size_t bytes() const {
+    const size_t blocks = align(bedge_off() + 4 * (size_t)cap);
+    const size_t p = align(pos_off() + 4 * (size_t)n);
+    return blocks > p ? blocks : p;
+  }
+  __host__ __device__ static size_t align(size_t x) { return (x + 15) & ~size_t(15); }
+};
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__global__ void __launch_bounds__(32 * kArenaWarps)
+    arena_kernel(ArenaArgs a) {
+  extern __shared__ __align__(16) char smem[];
+  const int n = a.n, E = a.E;
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const ArenaLayout Lo{n, E, a.cap};
+  char* base = smem + (size_t)wid * Lo.bytes();
+  int* pos = reinterpret_cast<int*>(base + Lo.pos_off());
+  int* fstart = reinterpret_cast<int*>(base + Lo.fstart_off());
+  int* flist = reinterpret_cast<int*>(base + Lo.flist_off());
+  unsigned long long* bsz = reinterpret_cast<unsigned long long*>(base + Lo.bsize_off());
+  int* bed = reinterpret_cast<int*>(base + Lo.bedge_off());
+
+  for (int64_t c = (int64_t)blockIdx.x * kArenaWarps + wid; c < a.num_orders;
+       c += (int64_t)gridDim.x * kArenaWarps) {
+    if (a.retry && a.valid[c] != kOverflow) continue;  // uniform per warp
+    const int32_t* order = a.orders + c * n;
+    // ---- positions: a permutation of [0, n) (duplicates via the returned word)
+    for (int v = lane; v < n; v += 32) pos[v] = 0;
+    __syncwarp();
+    bool bad = false;
+    for (int k = lane; k < n; k += 32) {
+      const int v = order[k];
+      if ((unsigned)v >= (unsigned)n) bad = true;
+      else bad |= atomicExch(&pos[v], k + 1) != 0;
+    }
+    __syncwarp();
+    // ---- lifetimes hi[e] (schedule.cpp:33-50) and validity (graph.cpp:239-254);
+    //      count the frees per timestep hi + 1 (placement.cpp:155-158)
+    for (int t = lane; t < n + 3; t += 32) fstart[t] = 0;
+    __syncwarp();
+    for (int e = lane; e < E; e += 32) {
+      const int lo = bad ? 0 : pos[a.edge_src[e]];
+      int hi = lo;
+      const int64_t s0 = a.sink_off[e], s1 = a.sink_off[e + 1];
+      for (int64_t q = s0; q < s1; ++q) {
+        const int ps = bad ? 0 : pos[a.sinks[q]];
+        bad |= ps <= lo;
+        hi = ps > hi ? ps : hi;
+      }
+      if (s1 == s0) hi = n;
+      if (!bad && a.edge_size[e] > 0) atomicAdd(&fstart[hi + 2], 1);
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    if (bad) {
+      if (lane == 0) {
+        a.mr_peak[c] = 0;
+        a.rs_at_peak[c] = 0;
+        a.frag[c] = 0.0;
+        a.valid[c] = 0;
+      }
+      __syncwarp();
+      continue;
+    }
+    __syncwarp();
+    // exclusive scan: fstart[t + 1] = first free at timestep t (t = 0 .. n + 1)
+    {
+      int carry = 0;
+      for (int t0 = 0; t0 < n + 3; t0 += 32) {
+        const int t = t0 + lane;
+        int v = t < n + 3 ? fstart[t] : 0;
+        int incl = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int o = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= d) incl += o;
+        }
+        __syncwarp();
+        if (t < n + 3) fstart[t] = carry + incl - v;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+    __syncwarp();
+    // stable fill in edge order: within a 32-edge chunk, rank lanes with the same t
+    for (int e0 = 0; e0 < E; e0 += 32) {
+      const int e = e0 + lane;
+      int t = -1;
+      if (e < E && a.edge_size[e] > 0) {
+        const int32_t* sk = a.sinks + a.sink_off[e];
+        const int64_t ns = a.sink_off[e + 1] - a.sink_off[e];
+        int hi = ns == 0 ? n : pos[a.edge_src[e]];
+        for (int64_t q = 0; q < ns; ++q) hi = pos[sk[q]] > hi ? pos[sk[q]] : hi;
+        t = hi + 1;
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, t);
+      const int rank = __popc(peers & lanemask_lt());
+      int at = 0;
+      if (t >= 0) at = fstart[t + 1] + rank;
+      __syncwarp();
+      if (t >= 0) {
+        flist[at] = e;
+        if (rank == 0) fstart[t + 1] += __popc(peers);
+      }
+      __syncwarp();
+    }
+    // fstart[t + 1] now points past bucket t; bucket t = [fstart[t], fstart[t + 1])
+    // ---- replay (placement.cpp:160-177) ------------------------------------------
+    int nb = 0;
+    bool overflow = false;  // warp-uniform
+    unsigned long long top = 0, live = 0, mr = 0, rs = 0;
+    for (int t = 1; t <= n && !overflow; ++t) {
+      const int f0 = fstart[t], f1 = fstart[t + 1];
+      for (int q = f0; q < f1; ++q) {  // Arena::release (placement.cpp:103-111)
+        const int e = flist[q];
+        int b = -1;
+        for (int i0 = 0; i0 < nb && b < 0; i0 += 32) {
+          const unsigned m = __ballot_sync(0xffffffffu, i0 + lane < nb && bed[i0 + lane] == e);
+          if (m) b = i0 + __ffs(m) - 1;
+        }
+        live -= a.edge_size[e];
+        if (b < 0) continue;
+        __syncwarp();
+        if (lane == 0) bed[b] = -1;
+        // coalesce (placement.cpp:130-139): the next block, then the previous one
+        int erase = -1;
+        if (b + 1 < nb && bed[b + 1] == -1) {
+          if (lane == 0) bsz[b] += bsz[b + 1];
+          erase = b + 1;
+        }
+        __syncwarp();
+        if (erase >= 0) {  // shift [erase + 1, nb) left by one
+          for (int i0 = erase + 1; i0 < nb; i0 += 32) {
+            const int i = i0 + lane;
+            unsigned long long sz = 0;
+            int ed = 0;
+            if (i < nb) {
+              sz = bsz[i];
+              ed = bed[i];
+            }
+            __syncwarp();
+            if (i < nb) {
+              bsz[i - 1] = sz;
+              bed[i - 1] = ed;
+            }
+            __syncwarp();
+          }
+          --nb;
+        }
+        if (b > 0 && bed[b - 1] == -1) {
+          if (lane == 0) bsz[b - 1] += bsz[b];
+          __syncwarp();
+          for (int i0 = b + 1; i0 < nb; i0 += 32) {
+            const int i = i0 + lane;
+            unsigned long long sz = 0;
+            int ed = 0;
+            if (i < nb) {
+              sz = bsz[i];
+              ed = bed[i];
+            }
+            __syncwarp();
+            if (i < nb) {
+              bsz[i - 1] = sz;
+              bed[i - 1] = ed;
+            }
+            __syncwarp();
+          }
+          --nb;
+        }
+        __syncwarp();
+      }
+      const int v = order[t - 1];
+      const int o0 = a.out_off[v], o1 = a.out_off[v + 1];
+      for (int q = o0; q < o1; ++q) {  // fanout(v) in edge order
+        const int e = a.out_edges[q];
+        const unsigned long long s = a.edge_size[e];
+        if (s == 0) continue;
+        // Arena::allocate (placement.cpp:80-101): first fit, or the smallest fit
+        int pick = -1;
+        if (!a.best_fit) {
+          for (int i0 = 0; i0 < nb && pick < 0; i0 += 32) {
+            const int i = i0 + lane;
+            const unsigned m =
+                __ballot_sync(0xffffffffu, i < nb && bed[i] == -1 && bsz[i] >= s);
+            if (m) pick = i0 + __ffs(m) - 1;
+          }
+        } else {
+          unsigned long long best = ULLONG_MAX;
+          int bi = INT_MAX;
+          for (int i0 = 0; i0 < nb; i0 += 32) {
+            const int i = i0 + lane;
+            if (i < nb && bed[i] == -1 && bsz[i] >= s && bsz[i] < best) {
+              best = bsz[i];
+              bi = i;
+            }
+          }
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) {
+            const unsigned long long b2 = __shfl_xor_sync(0xffffffffu, best, d);
+            const int i2 = __shfl_xor_sync(0xffffffffu, bi, d);
+            if (b2 < best || (b2 == best && i2 < bi)) {
+              best = b2;
+              bi = i2;
+            }
+          }
+          pick = bi == INT_MAX ? -1 : bi;
+        }
+        __syncwarp();
+        if (pick < 0) {  // grow (placement.cpp:117-128)
+          if (nb > 0 && bed[nb - 1] == -1) {
+            const unsigned long long old = bsz[nb - 1];
+            __syncwarp();
+            if (lane == 0) {
+              bsz[nb - 1] = s;
+              bed[nb - 1] = e;
+            }
+            top = top - old + s;
+          } else {
+            if (nb == a.cap) {
+              overflow = true;
+              break;
+            }
+            if (lane == 0) {
+              bsz[nb] = s;
+              bed[nb] = e;
+            }
+            ++nb;
+            top += s;
+          }
+        } else {
+          const unsigned long long bsize = bsz[pick];
+          __syncwarp();
+          if (bsize > s && nb == a.cap) {
+            overflow = true;
+            break;
+          }
+          if (bsize > s) {  // split: the rest stays free right after (shift right)
+            for (int i0 = ((nb - 1 - (pick + 1)) / 32) * 32 + pick + 1; i0 >= pick + 1;
+                 i0 -= 32) {
+              const int i = i0 + lane;
+              unsigned long long sz = 0;
+              int ed = 0;
+              if (i < nb) {
+                sz = bsz[i];
+                ed = bed[i];
+              }
+              __syncwarp();
+              if (i < nb) {
+                bsz[i + 1] = sz;
+                bed[i + 1] = ed;
+              }
+              __syncwarp();
+            }
+            if (lane == 0) {
+              bsz[pick + 1] = bsize - s;
+              bed[pick + 1] = -1;
+            }
+            ++nb;
+          }
+          if (lane == 0) {
+            bsz[pick] = s;
+            bed[pick] = e;
+          }
+        }
+        __syncwarp();
+        live += s;
+        if (top > mr) {
+          mr = top;
+          rs = live;
+        }
+      }
+    }
+    if (lane == 0) {
+      a.mr_peak[c] = overflow ? 0 : mr;
+      a.rs_at_peak[c] = overflow ? 0 : rs;
+      a.frag[c] = (overflow || mr == 0) ? 0.0 : (double)(mr - rs) / (double)mr;  // :64-67
+      a.valid[c] = overflow ? kOverflow : 1;
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+size_t arena_smem_bytes(int n, int E, int cap) {
+  return ArenaLayout{n, E, cap}.bytes() * kArenaWarps;
+}
+
+mp_status launch_arena_pass(const ArenaArgs& in, const mp_ctx* ctx, cudaStream_t st) {
+  const size_t smem = arena_smem_bytes(in.n, in.E, in.cap);
+  MP_CUDA(cudaFuncSetAttribute(arena_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+  int per_sm = 0;
+  MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arena_kernel, 32 * kArenaWarps,
+                                                        smem));
+  int64_t grid = (int64_t)ctx->num_sms * (per_sm > 0 ? per_sm : 1);
+  const int64_t need = (in.num_orders + kArenaWarps - 1) / kArenaWarps;
+  if (grid > need) grid = need;
+  arena_kernel<<<(unsigned)grid, 32 * kArenaWarps, smem, st>>>(in);
+  MP_CUDA(cudaGetLastError());
+  return MP_OK;
+}
+
+mp_status launch_arena(const ArenaArgs& in, const mp_ctx* ctx, cudaStream_t st) {
+  if (in.num_orders <= 0) return MP_OK;
+  const int full = 2 * in.E + 2;  // used + free blocks never exceed this
+  ArenaArgs a = in;
+  int first = kArenaCap;
+  if (const char* e = std::getenv("MP_ARENA_CAP")) first = std::atoi(e) > 0 ? std::atoi(e) : first;
+  a.cap = full < first ? full : first;  // MP_ARENA_CAP: tests of the overflow path
+  a.retry = 0;
+  MP_TRY(launch_arena_pass(a, ctx, st));
+  if (a.cap < full) {  // candidates whose block list overflowed, with the full bound
+    a.cap = full;
+    a.retry = 1;
+    MP_TRY(launch_arena_pass(a, ctx, st));
+  }
+  return MP_OK;
+}
+
+}  // namespace mpb

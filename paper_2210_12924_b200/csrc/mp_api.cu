@@ -263,6 +263,8 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
   g->n_extra3w = (int32_t)P.extra3_u.size();
   up(upload(&g->d_node_dyn_off, P.node_dyn_off.data(), P.node_dyn_off.size(), st));
   up(upload(&g->d_node_dyn, P.node_dyn.data(), P.node_dyn.size(), st));
+  up(upload(&g->d_out_off, P.out_off.data(), P.out_off.size(), st));
+  up(upload(&g->d_out_edges, P.out_edges.data(), P.out_edges.size(), st));
   up(upload(&g->d_tile_zw, P.tile_zw.data(), P.tile_zw.size(), st));
   up(upload(&g->d_tile_rec32, P.tile_rec32.data(), P.tile_rec32.size(), st));
   up(upload(&g->d_tile_moff, P.tile_moff.data(), P.tile_moff.size(), st));
@@ -289,7 +291,7 @@ mp_status mp_graph_free(mp_graph* g) {
                   g->d_extra_w,  g->d_dyn_off,   g->d_dyn_sinks, g->d_dyn_size,
                   g->d_node_rec32, g->d_node_u2, g->d_extra3_packed, g->d_extra3_u,
                   g->d_extra3_w, g->d_node_dyn_off, g->d_node_dyn, g->d_tile_pos,
-                  g->d_tile_zw, g->d_tile_rec32, g->d_tile_moff, g->d_tile_mother, g->d_tile_medge};
+                  g->d_out_off, g->d_out_edges, g->d_tile_zw, g->d_tile_rec32, g->d_tile_moff, g->d_tile_mother, g->d_tile_medge};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete g;
@@ -695,6 +697,64 @@ mp_status mp_validate_pairs_d(mp_ctx* ctx, int32_t E, const int32_t* d_lo, const
   a.row_begin = row_begin;
   a.row_end = row_end;
   return pair_sweep_d(ctx, a, d_row_off, d_viol, cap, num_viol, st);
+}
+
+// ---- arena baseline (K6) -----------------------------------------------------------
+mp_status mp_run_baseline_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_orders, int64_t B,
+                            int best_fit, uint64_t* d_mr, uint64_t* d_rs, double* d_frag,
+                            uint8_t* d_valid, void* stream) {
+  if (!ctx || !g || B < 0) return invalid_arg("null argument");
+  if (B == 0) return MP_OK;
+  if (!d_orders || !d_mr || !d_rs || !d_frag || !d_valid) return invalid_arg("null argument");
+  ArenaArgs a;
+  a.n = g->n;
+  a.E = g->E;
+  if (arena_smem_bytes(g->n, g->E, 2 * g->E + 2) > (size_t)ctx->max_smem_optin) {
+    set_error("Capacity: run_baseline state for " + std::to_string(g->n) + " nodes / " +
+              std::to_string(g->E) + " edges exceeds shared memory");
+    return MP_E_CAPACITY;
+  }
+  DeviceGuard guard(ctx->device);
+  a.num_orders = B;
+  a.orders = d_orders;
+  a.edge_src = g->d_edge_src;
+  a.sink_off = g->d_sink_off;
+  a.sinks = g->d_sinks;
+  a.edge_size = g->d_edge_size;
+  a.out_off = g->d_out_off;
+  a.out_edges = g->d_out_edges;
+  a.best_fit = best_fit ? 1 : 0;
+  a.mr_peak = d_mr;
+  a.rs_at_peak = d_rs;
+  a.frag = d_frag;
+  a.valid = d_valid;
+  return launch_arena(a, ctx, static_cast<cudaStream_t>(stream));
+}
+
+mp_status mp_run_baseline(mp_ctx* ctx, const mp_graph* g, const int32_t* orders, int64_t B,
+                          int best_fit, uint64_t* mr, uint64_t* rs, double* frag,
+                          uint8_t* valid) {
+  if (!ctx || !g || B < 0) return invalid_arg("null argument");
+  if (B == 0) return MP_OK;
+  if (!orders || !mr || !rs || !frag || !valid) return invalid_arg("null argument");
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const size_t b = (size_t)B, on = b * (size_t)g->n;
+  MP_TRY(ctx->scratch[0].reserve(Carver::size_of({4 * on, 8 * b, 8 * b, 8 * b, b})));
+  Carver cv(ctx->scratch[0].ptr);
+  int32_t* d_o = cv.take<int32_t>(on);
+  uint64_t* d_mr = cv.take<uint64_t>(b);
+  uint64_t* d_rs = cv.take<uint64_t>(b);
+  double* d_fr = cv.take<double>(b);
+  uint8_t* d_v = cv.take<uint8_t>(b);
+  if (on) MP_CUDA(cudaMemcpyAsync(d_o, orders, 4 * on, cudaMemcpyHostToDevice, st));
+  MP_TRY(mp_run_baseline_d(ctx, g, d_o, B, best_fit, d_mr, d_rs, d_fr, d_v, st));
+  MP_CUDA(cudaMemcpyAsync(mr, d_mr, 8 * b, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaMemcpyAsync(rs, d_rs, 8 * b, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaMemcpyAsync(frag, d_fr, 8 * b, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaMemcpyAsync(valid, d_v, b, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaStreamSynchronize(st));
+  return MP_OK;
 }
 
 // ---- placement (K5) ---------------------------------------------------------------

@@ -95,6 +95,8 @@ struct mp_graph {
   int32_t n_extra3w = 0;
   int32_t* d_node_dyn_off = nullptr;   // [n+1]
   int32_t* d_node_dyn = nullptr;       // [n_dyn_sinks]
+  int32_t* d_out_off = nullptr;        // [n+1] fanout(v), edge order
+  int32_t* d_out_edges = nullptr;      // [E]
   uint32_t* d_tile_zw = nullptr;       // [2n] tile scorer producer words (mp_prep.h)
   uint32_t* d_tile_rec32 = nullptr;    // [4n] (x, f, z, w), 32-bit graphs
   int32_t* d_tile_moff = nullptr;      // [n]
@@ -185,6 +187,27 @@ struct PlaceArgs {
 };
 size_t place_smem_bytes(int num_edges);
 mp_status launch_place(const PlaceArgs& a, const mp_ctx* ctx, cudaStream_t st);
+// K6 arena baseline (k_arena.cu): run_baseline per candidate order.
+struct ArenaArgs {
+  int32_t n = 0, E = 0, cap = 0;       // cap: block-list capacity (set by launch_arena)
+  int retry = 0;                       // second pass: only candidates marked overflowed
+  int64_t num_orders = 0;
+  const int32_t* orders = nullptr;     // [B][n]
+  const int32_t* edge_src = nullptr;
+  const int64_t* sink_off = nullptr;
+  const int32_t* sinks = nullptr;
+  const uint64_t* edge_size = nullptr;
+  const int32_t* out_off = nullptr;    // fanout lists
+  const int32_t* out_edges = nullptr;
+  int best_fit = 0;
+  uint64_t* mr_peak = nullptr;         // [B]
+  uint64_t* rs_at_peak = nullptr;      // [B]
+  double* frag = nullptr;              // [B]
+  uint8_t* valid = nullptr;            // [B]
+};
+constexpr int kArenaCap = 1024;       // first-pass block-list capacity
+size_t arena_smem_bytes(int n, int E, int cap);
+mp_status launch_arena(const ArenaArgs& a, const mp_ctx* ctx, cudaStream_t st);
 mp_status launch_peak_mem(int32_t num_edges, const uint64_t* d_size, const uint8_t* d_has,
                           const uint64_t* d_addr, uint64_t* d_out, cudaStream_t st);
 

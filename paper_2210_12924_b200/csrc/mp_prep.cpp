@@ -193,6 +193,15 @@ void prepare_scoring(int32_t n, int32_t E, const int32_t* src, const int64_t* si
       for (int32_t k = P->dyn_off[d]; k < P->dyn_off[d + 1]; ++k)
         P->node_dyn[cnt[P->dyn_sinks[k]]++] = d;
   }
+  // fanout lists in edge order (Graph::fanout, graph.cpp:100)
+  {
+    P->out_off.assign((size_t)n + 1, 0);
+    for (int32_t e = 0; e < E; ++e) ++P->out_off[src[e] + 1];
+    for (int32_t v = 0; v < n; ++v) P->out_off[v + 1] += P->out_off[v];
+    std::vector<int32_t> cur(P->out_off.begin(), P->out_off.end() - 1);
+    P->out_edges.assign(E, 0);
+    for (int32_t e = 0; e < E; ++e) P->out_edges[cur[src[e]]++] = e;
+  }
   // tile scorer words and memberships (only meaningful for n < 2^24)
   if (n < (1 << 24)) {
     P->tile_zw.assign(2 * (size_t)n, 0);

@@ -34,6 +34,8 @@ struct ScorePrep {
   // tile scorer node words (n < 2^24): z = pred1 (kNoNode if none) | min(#memberships,
   // 255) << 24, w = pred2 (kNoNode); memberships = (node v, dynamic edge d) pairs
   std::vector<uint32_t> tile_zw;             // [2n]
+  std::vector<int32_t> out_off{0};           // [n+1] fanout(v) (graph.hpp:91), edge order
+  std::vector<int32_t> out_edges;            // [E]
   std::vector<uint32_t> tile_rec32;          // [4n] (x, f, z, w) for 32-bit graphs
   std::vector<int32_t> tile_moff;            // [n] first membership of v
   std::vector<int32_t> tile_mother;          // [4 * m] other candidate sinks (kNoNode pad;

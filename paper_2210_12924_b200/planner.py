@@ -103,6 +103,14 @@ def load_plan(text: str) -> MemoryPlan:
 
 
 @dataclass
+class BaselineResult:
+    """memplan::BaselineResult (placement.hpp:44-48)."""
+    mr_peak: int = 0
+    rs_at_peak: int = 0
+    fragmentation: float = 0.0
+
+
+@dataclass
 class PrePlacement:
     """memplan::PrePlacement (placement.hpp:26-30)."""
     assigned: dict
@@ -415,6 +423,45 @@ class Planner:
         _native.check(_native.lib().mp_peak_mem(self.ctx, graph.E, graph.edge_size.ctypes.data,
                                                 has.ctypes.data, ad.ctypes.data, C.byref(out)))
         return int(out.value)
+
+    # ---- arena baseline (K6, k_arena.cu) ----------------------------------------------
+    def run_baseline_batch(self, graph: Graph, orders, best_fit: bool = False):
+        """run_baseline (placement.cpp:150-180) over many orders at once ->
+        (mr_peak u64[B], rs_at_peak u64[B], fragmentation f64[B], valid u8[B])."""
+        dg = self.upload(graph)
+        o = _i32(orders)
+        if o.ndim == 1:
+            o = o.reshape(1, -1)
+        c = o.shape[0]
+        mr = np.zeros(max(c, 1), np.uint64)
+        rs = np.zeros(max(c, 1), np.uint64)
+        fr = np.zeros(max(c, 1), np.float64)
+        valid = np.zeros(max(c, 1), np.uint8)
+        if o.shape[1] != graph.n:  # wrong length: not a topological order (graph.cpp:241)
+            return mr[:c], rs[:c], fr[:c], valid[:c]
+        _native.check(_native.lib().mp_run_baseline(self.ctx, dg.handle, o.ctypes.data, c,
+                                                    int(best_fit), mr.ctypes.data, rs.ctypes.data,
+                                                    fr.ctypes.data, valid.ctypes.data))
+        return mr[:c], rs[:c], fr[:c], valid[:c]
+
+    def run_baseline(self, graph: Graph, order: Sequence[int],
+                     policy: str = "first_fit") -> "BaselineResult":
+        """run_baseline (placement.cpp:150-180); InvalidOrder for a non-topological order."""
+        if policy not in ("first_fit", "best_fit"):
+            raise ValueError("policy is 'first_fit' or 'best_fit' (FitPolicy, placement.hpp:40)")
+        mr, rs, fr, valid = self.run_baseline_batch(graph, [list(order)] if len(order) else
+                                                    np.zeros((1, 0), np.int32),
+                                                    best_fit=policy == "best_fit")
+        if not valid[0]:
+            raise errors.InvalidOrder("sequence is not a topological order of the graph")
+        return BaselineResult(int(mr[0]), int(rs[0]), float(fr[0]))
+
+    def run_baseline_d(self, dg: "DeviceGraph", d_orders, num_orders, best_fit, d_mr, d_rs,
+                       d_frag, d_valid, stream: int | None = None) -> None:
+        _native.check(_native.lib().mp_run_baseline_d(
+            self.ctx, dg.handle, _native.ptr(d_orders), int(num_orders), int(best_fit),
+            _native.ptr(d_mr), _native.ptr(d_rs), _native.ptr(d_frag), _native.ptr(d_valid),
+            stream))
 
     # ---- placement heuristics (K5, k_place.cu) ---------------------------------------
     PLACE_PYRAMID = 1

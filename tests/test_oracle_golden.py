@@ -146,3 +146,25 @@ def test_golden_placement(golden):
             assert [int(a) if h else 0 for a, h in zip(pa, ph)] == p["greedy_addr"]
             checked += 1
     assert checked >= 70
+
+
+def test_golden_run_baseline(golden):
+    """or_run_baseline (the free-list arena, placement.cpp:69-180) vs the
+    reference's outputs, first fit and best fit, plus its known answers:
+    pack3 program order 0.2, chain3 0.0 (test_placement.cpp:88-101)."""
+    checked = 0
+    for rec in golden["graphs"]:
+        o = _oracle(rec)
+        for case in rec["orders"]:
+            if "baseline" not in case:
+                assert o.run_baseline(case["order"]) is None or "error" not in case
+                continue
+            for key, bf in (("first_fit", False), ("best_fit", True)):
+                mr, rs, fr = o.run_baseline(case["order"], best_fit=bf)
+                assert [mr, rs, fr] == case["baseline"][key], (rec["name"], key)
+            checked += 1
+        if rec["name"] == "pack3":
+            assert o.run_baseline(rec["orders"][0]["order"])[2] == pytest.approx(0.2)
+        if rec["name"] == "chain3":
+            assert o.run_baseline(rec["orders"][0]["order"])[2] == 0.0
+    assert checked >= 70
