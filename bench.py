@@ -437,6 +437,71 @@ def run_arena(args, cfg):
     return 0
 
 
+def run_lp(args, cfg):
+    """Non-overlap row emission (K7): the external-ILP placement model text
+    (write_lp(encode_addresses(...)), lp_format.cpp:88-121) through the public
+    host call - lifetimes in, LP text in host memory out - beside the reference's
+    encode_addresses + write_lp on the host."""
+    import torch
+    import paper_2210_12924_b200 as mp
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    torch.cuda.set_device(0)
+    g = load_graph(cfg)
+    planner = mp.Planner(0)
+    lo, hi = planner.lifetimes_from_order(g, mp.random_topo_orders(g, 1, seed=99)[0])
+    text, counts = planner.encode_addresses_lp(g, lo, hi, want_counts=True)   # warm-up
+    reps = max(1, min(args.steps, 5))
+    # the C call itself into a caller-owned (pinned) host buffer, text length known
+    import ctypes as C
+    ids = [x.encode() for x in g.edge_ids]
+    blob = b"".join(ids)
+    off = np.zeros(g.E + 1, np.int64)
+    off[1:] = np.cumsum([len(x) for x in ids])
+    hbuf = torch.empty(len(text) + 1, dtype=torch.uint8, pin_memory=True)
+    n = C.c_int64()
+    L = mp._native.lib()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        mp._native.check(L.mp_encode_addresses_lp(
+            planner.ctx, g.E, lo.ctypes.data, hi.ctypes.data, g.edge_size.ctypes.data, None, None,
+            blob, off.ctypes.data, hbuf.data_ptr(), len(text) + 1, C.byref(n), None))
+    t = (time.perf_counter() - t0) / reps
+    assert bytes(hbuf[:n.value].numpy()) == text.encode()
+    t1 = time.perf_counter()
+    text = planner.encode_addresses_lp(g, lo, hi)      # the Python mirror (two-phase + str)
+    t_py = time.perf_counter() - t1
+    cpu = None
+    if O.ref_available():
+        rg = O.RefGraph.load(mp.save_graph(g))
+        t0 = time.perf_counter()
+        ref = rg.encode_addresses_lp(lo, hi)
+        tr = time.perf_counter() - t0
+        assert ref == text, "LP text differs from the reference"
+        cpu = {"value": counts["live_pair"] / tr, "unit": "pairs/s", "cores": 1,
+               "kind": "reference", "seconds": tr,
+               "sample": "one lifetime set, memplan::encode_addresses + write_lp "
+                         "(oracle/_ref -O3, single-threaded as the reference is)"}
+    peak_gbs, _ = measured_peak_gbs()
+    line = {
+        "metric": "non-overlap rows emitted as LP text/sec (live_pair+below+above per pair)",
+        "value": counts["live_pair"] / t, "unit": "pairs/s", "n_gpus": 1, "steps": reps,
+        "warmup": 1, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "edges": g.E, "pairs": counts["live_pair"],
+                   "text_bytes": len(text), "order": "one seeded random topological order"},
+        "seconds_per_model": t, "text_gbs_end_to_end": len(text) / t / 1e9,
+        "python_mirror_seconds": t_py,
+        "hbm_peak_gbs": peak_gbs, "cpu_baseline": cpu, "identical_to_reference": cpu is not None,
+        "timing": "wall clock around mp_encode_addresses_lp into a pinned host buffer (pairs, "
+                  "lengths, scan, format, D2H of the text); python_mirror_seconds adds the "
+                  "two-phase length call and the str conversion",
+    }
+    print(json.dumps(line))
+    planner.close()
+    return 0
+
+
 # ---- our arm -------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
@@ -446,7 +511,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--place-batch", type=int, default=4096)
-    ap.add_argument("--mode", default="score", choices=["score", "pairs", "place", "arena"],
+    ap.add_argument("--mode", default="score", choices=["score", "pairs", "place", "arena", "lp"],
                     help="score: candidate scoring (the headline); pairs: overlap-pair "
                          "generation (K2) + address-plan validation (K4) on one lifetime set")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -462,6 +527,8 @@ def main():
         return run_place(args, cfg)
     if args.mode == "arena":
         return run_arena(args, cfg)
+    if args.mode == "lp":
+        return run_lp(args, cfg)
 
     import torch
     import torch.distributed as dist

@@ -240,6 +240,24 @@ mp_status mp_place_d(mp_ctx* ctx, int32_t num_edges, int64_t num_problems, const
                      uint64_t* d_addr, uint8_t* d_has_addr, uint64_t* d_peak_mem,
                      uint64_t* d_pyramid_base, void* stream);
 
+/* ---- (§8f-1) non-overlap rows: the external-ILP model text from the GPU pair list ----
+ * write_lp(encode_addresses(graph, lifetimes, preplaced)) (lp_format.cpp:88-121,
+ * encode.cpp:320-377) as text: per overlapping pair (the K2 pair set, i.e.
+ * filter_pairs on realized lifetimes) the live_pair / below /
+ * above rows and its two binaries, formatted on the GPU; the O(num_edges)
+ * sections (objective, peak_address rows, Bounds, Generals) on the host.
+ * ids: the edge ids concatenated, id_off [num_edges + 1] byte offsets (the
+ * variable names, sanitized as lp_format.cpp:30-36). pinned / pinned_addr: the
+ * preplaced map (may be NULL). Two-phase: out == NULL returns *len only.
+ * counts [4] (optional): rows tagged live_pair, below, above, peak_address.
+ * Ids that sanitize ambiguously (where lp_names would append "_2") are
+ * refused with MP_E_INVALID_ARG. */
+mp_status mp_encode_addresses_lp(mp_ctx* ctx, int32_t num_edges, const int32_t* lo,
+                                 const int32_t* hi, const uint64_t* size, const uint8_t* pinned,
+                                 const uint64_t* pinned_addr, const char* ids,
+                                 const int64_t* id_off, char* out, int64_t cap, int64_t* len,
+                                 int64_t* counts);
+
 /* ---- (§8f-4) arena baseline: run_baseline over candidate orders ---------------
  * run_baseline (placement.cpp:150-180): the free-list Arena (placement.cpp:69-148,
  * first fit, or best fit when best_fit != 0) replayed over every order of

@@ -295,6 +295,8 @@ def rlib():
                                           C.c_uint64, C.c_int32, _vp, C.c_int64,
                                           C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
         lib.ref_greedy_pack.argtypes = [_vp, _i32p, _i32p, _u64p]
+        lib.ref_encode_addresses_lp.argtypes = [_vp, _i32p, _i32p, _vp, _vp, C.c_int, _vp,
+                                                C.c_int64, C.POINTER(C.c_int64)]
         lib.ref_preallocate_pyramid.argtypes = [_vp, _i32p, _i32p, _u8p, _u64p,
                                                 C.POINTER(C.c_uint64)]
         lib.ref_greedy_pack_fixed.argtypes = [_vp, _i32p, _i32p, _vp, _vp, _u64p, _u8p]
@@ -453,6 +455,13 @@ class RefGraph:
                                                int(filter_pairs), out.ctypes.data_as(C.c_void_p),
                                                cnt.value, C.byref(cnt)))
         return out[: cnt.value]
+
+    def encode_addresses_lp(self, lo, hi, pinned=None, pinned_addr=None, filter_pairs=True):
+        """write_lp(encode_addresses(...)) from the reference, as text."""
+        pin = None if pinned is None else _c(pinned, np.uint8)
+        pa = None if pinned_addr is None else _c(pinned_addr, np.uint64)
+        return _text_call(rlib().ref_encode_addresses_lp, self._h, _c(lo, np.int32),
+                          _c(hi, np.int32), _opt_ptr(pin), _opt_ptr(pa), int(filter_pairs))
 
     def validate_plan(self, sequence, timestep_of, has_addr, addr, peak_mem, stored_peak_rs,
                       stored_peak_step=0):

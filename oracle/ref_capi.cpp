@@ -38,6 +38,7 @@
 #include "memplan/generate.hpp"
 #include "memplan/graph.hpp"
 #include "memplan/graph_io.hpp"
+#include "memplan/lp_format.hpp"
 #include "memplan/milp.hpp"
 #include "memplan/oracle.hpp"
 #include "memplan/pipeline.hpp"
@@ -332,6 +333,26 @@ int ref_encode_address_pairs(const void* gp, const int32_t* lo,
     }
     *count = at;
     return REF_OK;
+  } catch (...) {
+    return fail_from_current();
+  }
+}
+
+// write_lp(encode_addresses(...)) (lp_format.cpp:88-121): the model text
+int ref_encode_addresses_lp(const void* gp, const int32_t* lo, const int32_t* hi,
+                            const uint8_t* pinned, const uint64_t* pinned_addr, int filter,
+                            char* buf, int64_t cap, int64_t* len) {
+  try {
+    const Graph& g = *static_cast<const Graph*>(gp);
+    std::map<EdgeIndex, std::uint64_t> pre;
+    if (pinned)
+      for (int e = 0; e < g.num_edges(); ++e)
+        if (pinned[e]) pre[e] = pinned_addr ? pinned_addr[e] : 0;
+    EncodeOptions opts;
+    opts.filter_pairs = filter != 0;
+    const std::string text =
+        write_lp(encode_addresses(g, to_intervals(lo, hi, g.num_edges()), pre, opts));
+    return copy_text(text, buf, cap, len);
   } catch (...) {
     return fail_from_current();
   }

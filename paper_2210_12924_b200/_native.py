@@ -37,7 +37,7 @@ EXPORTS = [
     "mp_overlap_pairs", "mp_overlap_pairs_d",
     "mp_validate_pairs", "mp_validate_pairs_d", "mp_addresses_feasible", "mp_peak_mem",
     "mp_fragmentation", "mp_generate_graph", "mp_random_topo_orders",
-    "mp_place", "mp_place_d", "mp_run_baseline", "mp_run_baseline_d",
+    "mp_place", "mp_place_d", "mp_run_baseline", "mp_run_baseline_d", "mp_encode_addresses_lp",
 ]
 
 
@@ -116,6 +116,8 @@ def lib():
             "mp_addresses_feasible": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, P(i32)]),
             "mp_peak_mem": (C.c_int, [vp, i32, vp, vp, vp, P(u64)]),
             "mp_fragmentation": (C.c_double, [u64, u64]),
+            "mp_encode_addresses_lp": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, i64,
+                                                 P(i64), vp]),
             "mp_run_baseline": (C.c_int, [vp, vp, vp, i64, C.c_int, vp, vp, vp, vp]),
             "mp_run_baseline_d": (C.c_int, [vp, vp, vp, i64, C.c_int, vp, vp, vp, vp, vp]),
             "mp_place": (C.c_int, [vp, i32, i64, vp, vp, vp, vp, vp, vp, C.c_uint32, vp, vp,

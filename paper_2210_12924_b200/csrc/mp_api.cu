@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <unordered_set>
+#include <cctype>
 #include <climits>
 #include <cstring>
 #include <string>
@@ -697,6 +699,221 @@ mp_status mp_validate_pairs_d(mp_ctx* ctx, int32_t E, const int32_t* d_lo, const
   a.row_begin = row_begin;
   a.row_end = row_end;
   return pair_sweep_d(ctx, a, d_row_off, d_viol, cap, num_viol, st);
+}
+
+// ---- LP row emission (K7) ---------------------------------------------------------
+namespace {
+// lp_format.cpp:30-36: every non-alphanumeric byte becomes '_'
+std::string lp_sanitize(const char* s, size_t n) {
+  std::string out(s, n);
+  for (char& c : out)
+    if (!std::isalnum(static_cast<unsigned char>(c))) c = '_';
+  return out;
+}
+
+// lp_names (lp_format.cpp:75-86) suffixes duplicate sanitized names; this path
+// supports graphs whose names need no suffix and says so otherwise.
+bool lp_names_unique(const std::vector<std::string>& data_ids) {
+  std::unordered_set<std::string> d(data_ids.begin(), data_ids.end());
+  if (d.size() != data_ids.size()) return false;  // two ids, one sanitized name
+  // below_<A>_<B>_ == below_<A'>_<B'>_ needs A' = A_X and B = X_B' with A, B' ids
+  std::unordered_set<std::string> xs;
+  for (const std::string& a2 : data_ids)
+    for (size_t p = 0; p < a2.size(); ++p)
+      if (a2[p] == '_' && d.count(a2.substr(0, p))) xs.insert(a2.substr(p + 1));
+  if (xs.empty()) return true;
+  for (const std::string& b : data_ids)
+    for (size_t q = 0; q < b.size(); ++q)
+      if (b[q] == '_' && xs.count(b.substr(0, q)) && d.count(b.substr(q + 1))) return false;
+  return true;
+}
+}  // namespace
+
+mp_status mp_encode_addresses_lp(mp_ctx* ctx, int32_t E, const int32_t* lo, const int32_t* hi,
+                                 const uint64_t* size, const uint8_t* pinned,
+                                 const uint64_t* pinned_addr, const char* ids,
+                                 const int64_t* id_off, char* out, int64_t cap, int64_t* len,
+                                 int64_t* counts) {
+  if (!ctx || !len || E < 0 || (E > 0 && (!lo || !hi || !size || !ids || !id_off)))
+    return invalid_arg("null argument");
+  if (pinned && !pinned_addr) return invalid_arg("pinned without pinned_addr");
+  *len = 0;
+  // names, M and the host-side sections (O(E))
+  std::vector<std::string> sid(E);
+  std::vector<std::string> data_ids;
+  std::string names;
+  std::vector<int64_t> name_off(E + 1, 0);
+  long long M = 0;
+  for (int32_t e = 0; e < E; ++e) {
+    sid[e] = lp_sanitize(ids + id_off[e], (size_t)(id_off[e + 1] - id_off[e]));
+    names += sid[e];
+    name_off[e + 1] = (int64_t)names.size();
+    M += (long long)size[e];  // Graph::total_bytes (encode.cpp:325)
+    if (size[e] > 0) data_ids.push_back(sid[e]);
+  }
+  if (!lp_names_unique(data_ids)) {
+    set_error("InvalidArgument: edge ids are ambiguous once sanitized for LP "
+              "(lp_format.cpp:75-86 would suffix them); not supported by this path");
+    return MP_E_INVALID_ARG;
+  }
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = ctx->stream;
+  const size_t e = (size_t)E;
+  MP_TRY(ctx->scratch[0].reserve(Carver::size_of(
+      {4 * e, 4 * e, 8 * e, e, 8 * e, 8 * (e + 1), names.size() + 1, 8 * (e + 1), 8 * 4})));
+  Carver cv(ctx->scratch[0].ptr);
+  int32_t* d_lo = cv.take<int32_t>(e);
+  int32_t* d_hi = cv.take<int32_t>(e);
+  uint64_t* d_size = cv.take<uint64_t>(e);
+  uint8_t* d_pin = cv.take<uint8_t>(e);
+  uint64_t* d_paddr = cv.take<uint64_t>(e);
+  int64_t* d_row_off = cv.take<int64_t>(e + 1);
+  char* d_names = cv.take<char>(names.size() + 1);
+  int64_t* d_name_off = cv.take<int64_t>(e + 1);
+  int64_t* d_tot = cv.take<int64_t>(4);
+  int64_t P = 0;
+  int32_t* d_pairs = nullptr;
+  if (E > 0) {
+    MP_CUDA(cudaMemcpyAsync(d_lo, lo, 4 * e, cudaMemcpyHostToDevice, st));
+    MP_CUDA(cudaMemcpyAsync(d_hi, hi, 4 * e, cudaMemcpyHostToDevice, st));
+    MP_CUDA(cudaMemcpyAsync(d_size, size, 8 * e, cudaMemcpyHostToDevice, st));
+    if (pinned) {
+      MP_CUDA(cudaMemcpyAsync(d_pin, pinned, e, cudaMemcpyHostToDevice, st));
+      MP_CUDA(cudaMemcpyAsync(d_paddr, pinned_addr, 8 * e, cudaMemcpyHostToDevice, st));
+    }
+    if (!names.empty())
+      MP_CUDA(cudaMemcpyAsync(d_names, names.data(), names.size(), cudaMemcpyHostToDevice, st));
+    MP_CUDA(cudaMemcpyAsync(d_name_off, name_off.data(), 8 * (e + 1), cudaMemcpyHostToDevice,
+                            st));
+    // the pair list (K2): encode.cpp:347-357 in (i, j) order
+    PairArgs pa;
+    pa.num_edges = E;
+    pa.lo = d_lo;
+    pa.hi = d_hi;
+    pa.size = d_size;
+    pa.mask = pinned ? d_pin : nullptr;
+    pa.mode = 0;
+    pa.row_begin = 0;
+    pa.row_end = E;
+    MP_TRY(ctx->scratch[2].reserve(pairs_scratch_bytes(pa, ctx->num_sms)));
+    MP_TRY(pairs_count(pa, ctx->num_sms, ctx->scratch[2].ptr, d_row_off, &P, st));
+    if (P > 0) {
+      MP_TRY(ctx->scratch[4].reserve(Carver::size_of(
+          {8 * (size_t)P, 8 * (size_t)P, 8 * (size_t)P, 8 * (size_t)P, 8 * (size_t)P,
+           lp_scan_scratch(P)})));
+      Carver c4(ctx->scratch[4].ptr);
+      d_pairs = c4.take<int32_t>(2 * (size_t)P);
+      int64_t* d_rl = c4.take<int64_t>((size_t)P);
+      int64_t* d_bl = c4.take<int64_t>((size_t)P);
+      int64_t* d_ro = c4.take<int64_t>((size_t)P);
+      int64_t* d_bo = c4.take<int64_t>((size_t)P);
+      int64_t* d_sums = reinterpret_cast<int64_t*>(c4.take<char>(lp_scan_scratch(P)));
+      MP_TRY(pairs_fill(pa, ctx->num_sms, ctx->scratch[2].ptr, d_row_off, d_pairs, st));
+      LpArgs la;
+      la.E = E;
+      la.P = P;
+      la.pairs = reinterpret_cast<const int2*>(d_pairs);
+      la.size = d_size;
+      la.pinned = pinned ? d_pin : nullptr;
+      la.pinned_addr = pinned ? d_paddr : nullptr;
+      la.names = d_names;
+      la.name_off = d_name_off;
+      la.M = M;
+      la.row_len = d_rl;
+      la.bin_len = d_bl;
+      la.row_off = d_ro;
+      la.bin_off = d_bo;
+      MP_TRY(launch_lp_len(la, ctx->num_sms, st));
+      MP_TRY(scan_exclusive_i64(d_rl, P, d_ro, d_sums, d_tot, st));
+      MP_TRY(scan_exclusive_i64(d_bl, P, d_bo, d_sums, d_tot + 1, st));
+      int64_t tot[2];
+      MP_CUDA(cudaMemcpyAsync(tot, d_tot, 16, cudaMemcpyDeviceToHost, st));
+      MP_CUDA(cudaStreamSynchronize(st));
+      // host sections (O(E)) and the total length
+      std::string head = "Minimize\n obj: peak_mem\nSubject To\n";
+      std::string peak, bounds = "Bounds\n 0 <= peak_mem <= " + std::to_string(M) + "\n",
+                        gens = "Generals\n peak_mem\n";
+      int64_t q = 0;
+      for (int32_t x = 0; x < E; ++x) {
+        if (size[x] == 0) continue;
+        const bool pin = pinned && pinned[x];
+        const long long v = pin ? (long long)pinned_addr[x] : 0;
+        peak += " c" + std::to_string(3 * P + q) + "_peak_address:";
+        if (!pin) peak += " +1 addr_" + sid[x] + "_";
+        peak += " -1 peak_mem <= " + std::to_string(-(long long)size[x] - v) + "\n";
+        if (!pin) {
+          bounds += " 0 <= addr_" + sid[x] + "_ <= " + std::to_string(M) + "\n";
+          gens += " addr_" + sid[x] + "_\n";
+        }
+        ++q;
+      }
+      const std::string bin_head = "Binaries\n", end = "End\n";
+      const int64_t o_rows = (int64_t)head.size();
+      const int64_t o_peak = o_rows + tot[0];
+      const int64_t o_bounds = o_peak + (int64_t)peak.size();
+      const int64_t o_gens = o_bounds + (int64_t)bounds.size();
+      const int64_t o_binh = o_gens + (int64_t)gens.size();
+      const int64_t o_bins = o_binh + (int64_t)bin_head.size();
+      const int64_t o_end = o_bins + tot[1];
+      *len = o_end + (int64_t)end.size();
+      if (counts) {
+        counts[0] = counts[1] = counts[2] = P;
+        counts[3] = q;
+      }
+      if (!out) return MP_OK;
+      if (*len > cap) {
+        set_error("Capacity: the LP text of " + std::to_string(*len) +
+                  " bytes exceeds the buffer of " + std::to_string(cap));
+        return MP_E_CAPACITY;
+      }
+      MP_TRY(ctx->scratch[5].reserve((size_t)(tot[0] + tot[1]) + 16));
+      char* d_text = static_cast<char*>(ctx->scratch[5].ptr);
+      MP_TRY(launch_lp_write(la, d_text, d_text + tot[0], ctx->num_sms, st));
+      MP_CUDA(cudaMemcpyAsync(out + o_rows, d_text, (size_t)tot[0], cudaMemcpyDeviceToHost, st));
+      MP_CUDA(cudaMemcpyAsync(out + o_bins, d_text + tot[0], (size_t)tot[1],
+                              cudaMemcpyDeviceToHost, st));
+      std::memcpy(out, head.data(), head.size());
+      std::memcpy(out + o_peak, peak.data(), peak.size());
+      std::memcpy(out + o_bounds, bounds.data(), bounds.size());
+      std::memcpy(out + o_gens, gens.data(), gens.size());
+      std::memcpy(out + o_binh, bin_head.data(), bin_head.size());
+      std::memcpy(out + o_end, end.data(), end.size());
+      MP_CUDA(cudaStreamSynchronize(st));
+      return MP_OK;
+    }
+  }
+  // no overlapping pairs: every section is host-sized (O(E))
+  std::string text = "Minimize\n obj: peak_mem\nSubject To\n";
+  std::string bounds = "Bounds\n 0 <= peak_mem <= " + std::to_string(M) + "\n",
+              gens = "Generals\n peak_mem\n";
+  int64_t q = 0;
+  for (int32_t x = 0; x < E; ++x) {
+    if (size[x] == 0) continue;
+    const bool pin = pinned && pinned[x];
+    const long long v = pin ? (long long)pinned_addr[x] : 0;
+    text += " c" + std::to_string(q) + "_peak_address:";
+    if (!pin) text += " +1 addr_" + sid[x] + "_";
+    text += " -1 peak_mem <= " + std::to_string(-(long long)size[x] - v) + "\n";
+    if (!pin) {
+      bounds += " 0 <= addr_" + sid[x] + "_ <= " + std::to_string(M) + "\n";
+      gens += " addr_" + sid[x] + "_\n";
+    }
+    ++q;
+  }
+  text += bounds + gens + "Binaries\nEnd\n";
+  *len = (int64_t)text.size();
+  if (counts) {
+    counts[0] = counts[1] = counts[2] = 0;
+    counts[3] = q;
+  }
+  if (!out) return MP_OK;
+  if (*len > cap) {
+    set_error("Capacity: the LP text of " + std::to_string(*len) + " bytes exceeds the buffer of " +
+              std::to_string(cap));
+    return MP_E_CAPACITY;
+  }
+  std::memcpy(out, text.data(), text.size());
+  return MP_OK;
 }
 
 // ---- arena baseline (K6) -----------------------------------------------------------

@@ -45,7 +45,7 @@ struct mp_ctx {
   size_t max_smem_optin = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;  // own_stream unless mp_ctx_set_stream
-  mpb::Scratch scratch[4];        // independent scratch slots per call site
+  mpb::Scratch scratch[6];        // independent scratch slots per call site
   mpb::Scratch host_pinned_dummy;
   // small device buffer for per-call flags / counters
   int64_t* d_small = nullptr;
@@ -187,6 +187,29 @@ struct PlaceArgs {
 };
 size_t place_smem_bytes(int num_edges);
 mp_status launch_place(const PlaceArgs& a, const mp_ctx* ctx, cudaStream_t st);
+// K7 LP row emission (k_lp.cu): write_lp text of encode_addresses' pair rows.
+struct LpArgs {
+  int32_t E = 0;
+  int64_t P = 0;                        // overlapping pairs
+  const int2* pairs = nullptr;          // [P] (i, j), i < j
+  const uint64_t* size = nullptr;       // [E]
+  const uint8_t* pinned = nullptr;      // [E] or null
+  const uint64_t* pinned_addr = nullptr;
+  const char* names = nullptr;          // sanitized edge ids, concatenated
+  const int64_t* name_off = nullptr;    // [E+1]
+  long long M = 0;                      // big-M = Graph::total_bytes (encode.cpp:325)
+  int64_t* row_len = nullptr;           // [P]
+  int64_t* bin_len = nullptr;           // [P]
+  const int64_t* row_off = nullptr;     // [P] exclusive scan of row_len
+  const int64_t* bin_off = nullptr;
+};
+mp_status launch_lp_len(const LpArgs& a, int num_sms, cudaStream_t st);
+mp_status launch_lp_write(const LpArgs& a, char* d_rows, char* d_bins, int num_sms,
+                          cudaStream_t st);
+size_t lp_scan_scratch(int64_t n);
+mp_status scan_exclusive_i64(const int64_t* d_in, int64_t n, int64_t* d_out, int64_t* d_sums,
+                             int64_t* d_total, cudaStream_t st);
+
 // K6 arena baseline (k_arena.cu): run_baseline per candidate order.
 struct ArenaArgs {
   int32_t n = 0, E = 0, cap = 0;       // cap: block-list capacity (set by launch_arena)

@@ -424,6 +424,38 @@ class Planner:
                                                 has.ctypes.data, ad.ctypes.data, C.byref(out)))
         return int(out.value)
 
+    # ---- non-overlap rows as LP text (K7, k_lp.cu) ------------------------------------
+    def encode_addresses_lp(self, graph: Graph, lo, hi,
+                            preplaced: Optional[Mapping[int, int]] = None,
+                            want_counts: bool = False):
+        """write_lp(encode_addresses(graph, lifetimes, preplaced)) (lp_format.cpp:88-121,
+        encode.cpp:320-377): the external-ILP placement model as text, its pair rows
+        built on the GPU from the K2 pair list. With want_counts also returns the
+        constraint_counts of the model."""
+        lo, hi = _i32(lo), _i32(hi)
+        ids = [s.encode() for s in graph.edge_ids]
+        blob = b"".join(ids) or b"\0"
+        off = np.zeros(graph.E + 1, np.int64)
+        off[1:] = np.cumsum([len(x) for x in ids]) if ids else []
+        pin = pa = None
+        if preplaced:
+            pin, pa = self._addr_arrays(graph, preplaced)
+        n = C.c_int64()
+        counts = np.zeros(4, np.int64)
+        args = [self.ctx, graph.E, lo.ctypes.data, hi.ctypes.data, graph.edge_size.ctypes.data,
+                None if pin is None else pin.ctypes.data, None if pa is None else pa.ctypes.data,
+                blob, off.ctypes.data]
+        _native.check(_native.lib().mp_encode_addresses_lp(*args, None, 0, C.byref(n),
+                                                           counts.ctypes.data))
+        buf = C.create_string_buffer(n.value + 1)
+        _native.check(_native.lib().mp_encode_addresses_lp(*args, buf, n.value + 1, C.byref(n),
+                                                           None))
+        text = buf.raw[: n.value].decode()
+        if want_counts:
+            return text, {"live_pair": int(counts[0]), "below": int(counts[1]),
+                          "above": int(counts[2]), "peak_address": int(counts[3])}
+        return text
+
     # ---- arena baseline (K6, k_arena.cu) ----------------------------------------------
     def run_baseline_batch(self, graph: Graph, orders, best_fit: bool = False):
         """run_baseline (placement.cpp:150-180) over many orders at once ->

@@ -213,6 +213,10 @@ def graph_record(name, g: "O.RefGraph", rng, n_random=3, plans=True):
                 pin[e] = 1
         rec["pinned"] = {"pinned": pin.tolist(),
                          "pairs": g.encode_address_pairs(lo, hi, pin, np.zeros(g.E, np.uint64)).tolist()}
+        # the external-ILP placement model as LP text (encode.cpp:320-377, lp_format.cpp:88-121)
+        paddr = np.array([1000 * e + 8 for e in range(g.E)], np.uint64)
+        rec["lp"] = {"text": g.encode_addresses_lp(lo, hi), "pinned_addr": paddr.tolist(),
+                     "text_pinned": g.encode_addresses_lp(lo, hi, pin, paddr)}
         if plans:
             rec["plans"] = plan_cases(g, po, rng)
         rec["realized"] = realized_cases(g, po, rng)
