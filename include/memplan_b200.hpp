@@ -17,6 +17,10 @@
 //   memplan_b200::validate_plan            <- memplan::validate_plan (plan.cpp:315-419)
 //   memplan_b200::addresses_feasible       <- addresses_feasible (pipeline.cpp:146-160)
 //   memplan_b200::score_orders / best_order   batched peak_resident_bytes + first-min argmin
+//   memplan_b200::preallocate_pyramid      <- memplan::preallocate_pyramid (placement.cpp:25-62)
+//   memplan_b200::greedy_pack              <- memplan::greedy_pack (placement.cpp:182-204)
+//   memplan_b200::run_baseline             <- memplan::run_baseline (placement.cpp:150-180)
+//   memplan_b200::write_address_lp         <- write_lp(encode_addresses(...)) (lp_format.cpp:88-121)
 //
 // One Planner per device; graphs are uploaded once per Planner and cached by
 // address (a memplan::Graph is immutable after build, graph.hpp:61).
@@ -35,6 +39,7 @@
 #include "memplan/errors.hpp"
 #include "memplan/graph.hpp"
 #include "memplan/milp.hpp"
+#include "memplan/placement.hpp"
 #include "memplan/plan.hpp"
 #include "memplan_b200.h"
 
@@ -230,6 +235,82 @@ class Planner {
     return out;
   }
 
+  // ---- placement.hpp: the producers of the plans validate_plan checks -------------
+  memplan::PrePlacement preallocate_pyramid(const memplan::Graph& g,
+                                            const std::vector<memplan::Interval>& lt) {
+    std::vector<uint64_t> addr;
+    std::vector<uint8_t> has;
+    uint64_t base = 0;
+    place(g, lt, {}, MP_PLACE_PYRAMID_ONLY, &addr, &has, &base);
+    memplan::PrePlacement out;
+    for (int e = 0; e < g.num_edges(); ++e) {
+      if (has[e]) out.assigned[e] = addr[e];
+      else if (g.edge(e).size > 0) out.remaining.push_back(e);
+    }
+    out.reserved_base = base;
+    return out;
+  }
+
+  std::map<memplan::EdgeIndex, std::uint64_t> greedy_pack(
+      const memplan::Graph& g, const std::vector<memplan::Interval>& lt,
+      const std::map<memplan::EdgeIndex, std::uint64_t>& preplaced) {
+    std::vector<uint64_t> addr;
+    std::vector<uint8_t> has;
+    place(g, lt, preplaced, 0, &addr, &has, nullptr);
+    std::map<memplan::EdgeIndex, std::uint64_t> out;
+    for (int e = 0; e < g.num_edges(); ++e)
+      if (has[e]) out[e] = addr[e];
+    return out;
+  }
+
+  memplan::BaselineResult run_baseline(const memplan::Graph& g,
+                                       const std::vector<memplan::NodeIndex>& order,
+                                       memplan::FitPolicy policy = memplan::FitPolicy::kFirstFit) {
+    memplan::BaselineResult r;
+    uint8_t valid = 0;
+    if ((int)order.size() == g.num_nodes()) {
+      std::vector<int32_t> o(order.begin(), order.end());
+      check(mp_run_baseline(ctx_, device_graph(g), o.data(), 1,
+                            policy == memplan::FitPolicy::kBestFit ? 1 : 0, &r.mr_peak,
+                            &r.rs_at_peak, &r.fragmentation, &valid));
+    }
+    if (!valid)
+      throw memplan::InvalidOrder("sequence is not a topological order of the graph");
+    return r;
+  }
+
+  // ---- encode.hpp + lp_format.hpp: the external placement model as LP text ---------
+  std::string write_address_lp(const memplan::Graph& g, const std::vector<memplan::Interval>& lt,
+                               const std::map<memplan::EdgeIndex, std::uint64_t>& preplaced = {}) {
+    const int E = g.num_edges();
+    std::vector<int32_t> lo(E), hi(E);
+    std::vector<uint64_t> size(E), paddr(E, 0);
+    std::vector<uint8_t> pin(E, 0);
+    std::string ids;
+    std::vector<int64_t> off(E + 1, 0);
+    for (int e = 0; e < E; ++e) {
+      lo[e] = lt[e].lo;
+      hi[e] = lt[e].hi;
+      size[e] = g.edge(e).size;
+      ids += g.edge(e).id;
+      off[e + 1] = (int64_t)ids.size();
+    }
+    for (const auto& kv : preplaced) {
+      pin[kv.first] = 1;
+      paddr[kv.first] = kv.second;
+    }
+    const uint8_t* pp = preplaced.empty() ? nullptr : pin.data();
+    const uint64_t* pa = preplaced.empty() ? nullptr : paddr.data();
+    int64_t len = 0;
+    check(mp_encode_addresses_lp(ctx_, E, lo.data(), hi.data(), size.data(), pp, pa, ids.data(),
+                                 off.data(), nullptr, 0, &len, nullptr));
+    std::string text((size_t)len + 1, '\0');
+    check(mp_encode_addresses_lp(ctx_, E, lo.data(), hi.data(), size.data(), pp, pa, ids.data(),
+                                 off.data(), &text[0], len + 1, &len, nullptr));
+    text.resize((size_t)len);
+    return text;
+  }
+
   // ---- pipeline.cpp ----------------------------------------------------------------
   bool addresses_feasible(const memplan::Graph& g, const std::vector<memplan::Interval>& lt,
                           const std::map<memplan::EdgeIndex, std::uint64_t>& addresses) {
@@ -353,6 +434,38 @@ class Planner {
   }
 
  private:
+  void place(const memplan::Graph& g, const std::vector<memplan::Interval>& lt,
+             const std::map<memplan::EdgeIndex, std::uint64_t>& preplaced, uint32_t flags,
+             std::vector<uint64_t>* addr, std::vector<uint8_t>* has, uint64_t* base) {
+    const int E = g.num_edges();
+    std::vector<int32_t> lo(E), hi(E), rank(E);
+    std::vector<uint64_t> size(E), faddr(E, 0);
+    std::vector<uint8_t> fixed(E, 0);
+    std::vector<int> by_id(E);
+    for (int e = 0; e < E; ++e) {
+      lo[e] = lt[e].lo;
+      hi[e] = lt[e].hi;
+      size[e] = g.edge(e).size;
+      by_id[e] = e;
+    }
+    // the pyramid's last tie-break compares edge ids (placement.cpp:48-50)
+    std::sort(by_id.begin(), by_id.end(),
+              [&](int a, int b) { return g.edge(a).id < g.edge(b).id; });
+    for (int r = 0; r < E; ++r) rank[by_id[r]] = r;
+    for (const auto& kv : preplaced) {
+      fixed[kv.first] = 1;
+      faddr[kv.first] = kv.second;
+    }
+    addr->assign(E > 0 ? E : 1, 0);
+    has->assign(E > 0 ? E : 1, 0);
+    uint64_t peak = 0, b = 0;
+    check(mp_place(ctx_, E, 1, lo.data(), hi.data(), size.data(), rank.data(),
+                   preplaced.empty() ? nullptr : fixed.data(),
+                   preplaced.empty() ? nullptr : faddr.data(), flags, addr->data(), has->data(),
+                   &peak, &b));
+    if (base) *base = b;
+  }
+
   static std::uint64_t fingerprint(const memplan::Graph& g) {
     std::uint64_t h = 1469598103934665603ull;
     auto mix = [&h](std::uint64_t x) { h = (h ^ x) * 1099511628211ull; };

@@ -922,7 +922,8 @@ mp_status mp_run_baseline_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_ord
                             uint8_t* d_valid, void* stream) {
   if (!ctx || !g || B < 0) return invalid_arg("null argument");
   if (B == 0) return MP_OK;
-  if (!d_orders || !d_mr || !d_rs || !d_frag || !d_valid) return invalid_arg("null argument");
+  if ((!d_orders && g->n > 0) || !d_mr || !d_rs || !d_frag || !d_valid)
+    return invalid_arg("null argument");
   ArenaArgs a;
   a.n = g->n;
   a.E = g->E;
@@ -953,7 +954,7 @@ mp_status mp_run_baseline(mp_ctx* ctx, const mp_graph* g, const int32_t* orders,
                           uint8_t* valid) {
   if (!ctx || !g || B < 0) return invalid_arg("null argument");
   if (B == 0) return MP_OK;
-  if (!orders || !mr || !rs || !frag || !valid) return invalid_arg("null argument");
+  if ((!orders && g->n > 0) || !mr || !rs || !frag || !valid) return invalid_arg("null argument");
   DeviceGuard guard(ctx->device);
   cudaStream_t st = ctx->stream;
   const size_t b = (size_t)B, on = b * (size_t)g->n;

@@ -16,6 +16,7 @@
 
 #include "memplan/encode.hpp"
 #include "memplan/errors.hpp"
+#include "memplan/lp_format.hpp"
 #include "memplan/generate.hpp"
 #include "memplan/graph.hpp"
 #include "memplan/graph_io.hpp"
@@ -122,6 +123,10 @@ static void check_graph(memplan_b200::Planner& dev, const Graph& g, std::mt19937
     EXPECT(scores[c].valid == ref_err.empty(), "score verdict");
     if (!ref_err.empty()) {
       EXPECT(error_of([&] { dev.peak_resident_bytes(g, o); }) == ref_err, "peak error text");
+      if ((int)o.size() == g.num_nodes())
+        EXPECT(error_of([&] { dev.run_baseline(g, o); }) ==
+                   error_of([&] { run_baseline(g, o); }),
+               "run_baseline error text");
       continue;
     }
     const auto lt = lifetimes_from_order(g, o);
@@ -150,6 +155,25 @@ static void check_graph(memplan_b200::Planner& dev, const Graph& g, std::mt19937
     // addresses: greedy_pack is feasible; collapsing two live tensors is not
     auto packed = greedy_pack(g, lt, {});
     EXPECT(dev.addresses_feasible(g, lt, packed), "greedy_pack feasible");
+    // placement heuristics, the arena baseline and the LP text vs the reference
+    EXPECT(dev.greedy_pack(g, lt, {}) == packed, "greedy_pack");
+    const PrePlacement rp = preallocate_pyramid(g, lt);
+    const PrePlacement dp = dev.preallocate_pyramid(g, lt);
+    EXPECT(rp.assigned == dp.assigned && rp.remaining == dp.remaining &&
+               rp.reserved_base == dp.reserved_base,
+           "preallocate_pyramid");
+    EXPECT(dev.greedy_pack(g, lt, rp.assigned) == greedy_pack(g, lt, rp.assigned),
+           "greedy_pack over the pyramid");
+    for (FitPolicy pol : {FitPolicy::kFirstFit, FitPolicy::kBestFit}) {
+      const BaselineResult rb = run_baseline(g, o, pol);
+      const BaselineResult db = dev.run_baseline(g, o, pol);
+      EXPECT(rb.mr_peak == db.mr_peak && rb.rs_at_peak == db.rs_at_peak &&
+                 rb.fragmentation == db.fragmentation,
+             "run_baseline");
+    }
+    EXPECT(write_lp(encode_addresses(g, lt, {})) == dev.write_address_lp(g, lt), "LP text");
+    EXPECT(write_lp(encode_addresses(g, lt, pre)) == dev.write_address_lp(g, lt, pre),
+           "LP text, pinned");
     // realized lifetimes from the order's timesteps
     std::map<std::string, int> ts;
     for (size_t i = 0; i < o.size(); ++i) ts[g.node(o[i]).id] = (int)i + 1;
