@@ -502,6 +502,46 @@ def run_lp(args, cfg):
     return 0
 
 
+def run_joint(args, cfg):
+    """Joint-mode pair set (K8): encode_joint's pair loop with the edge_precedes
+    filter, through the public host call, beside the reference's own loop."""
+    import torch
+    import paper_2210_12924_b200 as mp
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    torch.cuda.set_device(0)
+    g = load_graph(cfg)
+    planner = mp.Planner(0)
+    pairs = planner.joint_pairs(g)            # builds the per-graph tables (once)
+    reps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        pairs = planner.joint_pairs(g)
+    t = (time.perf_counter() - t0) / reps
+    cpu = None
+    if O.ref_available():
+        rg = O.RefGraph.load(mp.save_graph(g))
+        t0 = time.perf_counter()
+        ref = rg.joint_pairs()
+        tr = time.perf_counter() - t0
+        assert np.array_equal(ref, pairs), "joint pairs differ from the reference"
+        cpu = {"value": len(ref) / tr, "unit": "pairs/s", "cores": 1, "kind": "reference",
+               "seconds": tr, "sample": "encode_joint's pair loop (compute_bounds, "
+                                       "ReachabilityCache, edge_precedes; oracle/_ref -O3)"}
+    data = int((g.edge_size > 0).sum())
+    line = {"metric": "joint-mode pairs generated/sec (edge_precedes-filtered)",
+            "value": len(pairs) / t, "unit": "pairs/s", "n_gpus": 1, "steps": reps,
+            "warmup": 1, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int32", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "edges": g.E, "pairs": int(len(pairs)),
+                       "candidate_pairs": data * (data - 1) // 2},
+            "seconds": t, "cpu_baseline": cpu,
+            "timing": "wall clock around mp_joint_pairs (count, scan, fill, D2H), tables cached"}
+    print(json.dumps(line))
+    planner.close()
+    return 0
+
+
 # ---- our arm -------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
@@ -511,7 +551,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--place-batch", type=int, default=4096)
-    ap.add_argument("--mode", default="score", choices=["score", "pairs", "place", "arena", "lp"],
+    ap.add_argument("--mode", default="score", choices=["score", "pairs", "place", "arena", "lp", "joint"],
                     help="score: candidate scoring (the headline); pairs: overlap-pair "
                          "generation (K2) + address-plan validation (K4) on one lifetime set")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -529,6 +569,8 @@ def main():
         return run_arena(args, cfg)
     if args.mode == "lp":
         return run_lp(args, cfg)
+    if args.mode == "joint":
+        return run_joint(args, cfg)
 
     import torch
     import torch.distributed as dist

@@ -258,6 +258,15 @@ mp_status mp_encode_addresses_lp(mp_ctx* ctx, int32_t num_edges, const int32_t* 
                                  const int64_t* id_off, char* out, int64_t cap, int64_t* len,
                                  int64_t* counts);
 
+/* ---- (§8f-3) joint-mode pair set ------------------------------------------------
+ * The pair loop of encode_joint (encode.cpp:401-408): data edges i < j, minus
+ * those ordered by the graph (edge_precedes either way, analysis.cpp:94-113,
+ * with compute_bounds' windows, analysis.cpp:33-62) when filter != 0. Pairs
+ * come back in the reference's (i, j) order; two-phase (pairs == NULL: count).
+ * Graphs over 32,768 nodes return MP_E_CAPACITY (host descendant bitsets). */
+mp_status mp_joint_pairs(mp_ctx* ctx, const mp_graph* g, int filter, int32_t* pairs, int64_t cap,
+                         int64_t* count);
+
 /* ---- (§8f-4) arena baseline: run_baseline over candidate orders ---------------
  * run_baseline (placement.cpp:150-180): the free-list Arena (placement.cpp:69-148,
  * first fit, or best fit when best_fit != 0) replayed over every order of

@@ -21,6 +21,7 @@
 //   memplan_b200::greedy_pack              <- memplan::greedy_pack (placement.cpp:182-204)
 //   memplan_b200::run_baseline             <- memplan::run_baseline (placement.cpp:150-180)
 //   memplan_b200::write_address_lp         <- write_lp(encode_addresses(...)) (lp_format.cpp:88-121)
+//   memplan_b200::joint_pairs              <- the pair loop of encode_joint (encode.cpp:401-408)
 //
 // One Planner per device; graphs are uploaded once per Planner and cached by
 // address (a memplan::Graph is immutable after build, graph.hpp:61).
@@ -277,6 +278,19 @@ class Planner {
     if (!valid)
       throw memplan::InvalidOrder("sequence is not a topological order of the graph");
     return r;
+  }
+
+  // ---- encode.cpp:401-408: the joint-mode pair set (edge_precedes filter) ----------
+  std::vector<std::pair<memplan::EdgeIndex, memplan::EdgeIndex>> joint_pairs(
+      const memplan::Graph& g, bool filter_pairs = true) {
+    int64_t count = 0;
+    check(mp_joint_pairs(ctx_, device_graph(g), filter_pairs ? 1 : 0, nullptr, 0, &count));
+    std::vector<int32_t> flat(2 * count);
+    check(mp_joint_pairs(ctx_, device_graph(g), filter_pairs ? 1 : 0, flat.data(), count,
+                         &count));
+    std::vector<std::pair<memplan::EdgeIndex, memplan::EdgeIndex>> out(count);
+    for (int64_t i = 0; i < count; ++i) out[i] = {flat[2 * i], flat[2 * i + 1]};
+    return out;
   }
 
   // ---- encode.hpp + lp_format.hpp: the external placement model as LP text ---------

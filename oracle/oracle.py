@@ -295,6 +295,7 @@ def rlib():
                                           C.c_uint64, C.c_int32, _vp, C.c_int64,
                                           C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
         lib.ref_greedy_pack.argtypes = [_vp, _i32p, _i32p, _u64p]
+        lib.ref_joint_pairs.argtypes = [_vp, C.c_int, _vp, C.c_int64, C.POINTER(C.c_int64)]
         lib.ref_encode_addresses_lp.argtypes = [_vp, _i32p, _i32p, _vp, _vp, C.c_int, _vp,
                                                 C.c_int64, C.POINTER(C.c_int64)]
         lib.ref_preallocate_pyramid.argtypes = [_vp, _i32p, _i32p, _u8p, _u64p,
@@ -454,6 +455,15 @@ class RefGraph:
         _check(rlib().ref_encode_address_pairs(self._h, lo, hi, _opt_ptr(pin), _opt_ptr(pa),
                                                int(filter_pairs), out.ctypes.data_as(C.c_void_p),
                                                cnt.value, C.byref(cnt)))
+        return out[: cnt.value]
+
+    def joint_pairs(self, filter_pairs=True):
+        """encode_joint's pair set (encode.cpp:401-408) from the reference -> int32[P][2]."""
+        cnt = C.c_int64()
+        _check(rlib().ref_joint_pairs(self._h, int(filter_pairs), None, 0, C.byref(cnt)))
+        out = np.zeros((max(cnt.value, 1), 2), np.int32)
+        _check(rlib().ref_joint_pairs(self._h, int(filter_pairs), out.ctypes.data_as(C.c_void_p),
+                                      cnt.value, C.byref(cnt)))
         return out[: cnt.value]
 
     def encode_addresses_lp(self, lo, hi, pinned=None, pinned_addr=None, filter_pairs=True):

@@ -338,6 +338,37 @@ int ref_encode_address_pairs(const void* gp, const int32_t* lo,
   }
 }
 
+// The pair loop of encode_joint (encode.cpp:401-408) without the model: data edges
+// a < b, skipped when filter_pairs and edge_precedes either way (analysis.cpp:94-113),
+// with the reference's compute_bounds and ReachabilityCache. Two-phase like the above.
+int ref_joint_pairs(const void* gp, int filter, int32_t* pairs, int64_t cap, int64_t* count) {
+  try {
+    const Graph& g = *static_cast<const Graph*>(gp);
+    const LifetimeBounds bounds = compute_bounds(g);
+    ReachabilityCache reach(g);
+    std::vector<EdgeIndex> data;
+    for (int e = 0; e < g.num_edges(); ++e)
+      if (g.edge(e).size > 0) data.push_back(e);
+    int64_t at = 0;
+    for (size_t a = 0; a < data.size(); ++a)
+      for (size_t b = a + 1; b < data.size(); ++b) {
+        const EdgeIndex i = data[a], j = data[b];
+        if (filter && (edge_precedes(g, bounds, i, j, &reach) ||
+                       edge_precedes(g, bounds, j, i, &reach)))
+          continue;
+        if (pairs && at < cap) {
+          pairs[2 * at] = i;
+          pairs[2 * at + 1] = j;
+        }
+        ++at;
+      }
+    *count = at;
+    return pairs && at > cap ? REF_CAPACITY : REF_OK;
+  } catch (...) {
+    return fail_from_current();
+  }
+}
+
 // write_lp(encode_addresses(...)) (lp_format.cpp:88-121): the model text
 int ref_encode_addresses_lp(const void* gp, const int32_t* lo, const int32_t* hi,
                             const uint8_t* pinned, const uint64_t* pinned_addr, int filter,

@@ -38,6 +38,7 @@ EXPORTS = [
     "mp_validate_pairs", "mp_validate_pairs_d", "mp_addresses_feasible", "mp_peak_mem",
     "mp_fragmentation", "mp_generate_graph", "mp_random_topo_orders",
     "mp_place", "mp_place_d", "mp_run_baseline", "mp_run_baseline_d", "mp_encode_addresses_lp",
+    "mp_joint_pairs",
 ]
 
 
@@ -116,6 +117,7 @@ def lib():
             "mp_addresses_feasible": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, P(i32)]),
             "mp_peak_mem": (C.c_int, [vp, i32, vp, vp, vp, P(u64)]),
             "mp_fragmentation": (C.c_double, [u64, u64]),
+            "mp_joint_pairs": (C.c_int, [vp, vp, C.c_int, vp, i64, P(i64)]),
             "mp_encode_addresses_lp": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, i64,
                                                  P(i64), vp]),
             "mp_run_baseline": (C.c_int, [vp, vp, vp, i64, C.c_int, vp, vp, vp, vp]),

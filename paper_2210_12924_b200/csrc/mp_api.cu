@@ -293,7 +293,7 @@ mp_status mp_graph_free(mp_graph* g) {
                   g->d_extra_w,  g->d_dyn_off,   g->d_dyn_sinks, g->d_dyn_size,
                   g->d_node_rec32, g->d_node_u2, g->d_extra3_packed, g->d_extra3_u,
                   g->d_extra3_w, g->d_node_dyn_off, g->d_node_dyn, g->d_tile_pos,
-                  g->d_out_off, g->d_out_edges, g->d_tile_zw, g->d_tile_rec32, g->d_tile_moff, g->d_tile_mother, g->d_tile_medge};
+                  g->d_out_off, g->d_out_edges, g->d_joint_mul, g->d_joint_ar, g->d_joint_art, g->d_tile_zw, g->d_tile_rec32, g->d_tile_moff, g->d_tile_mother, g->d_tile_medge};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete g;
@@ -699,6 +699,144 @@ mp_status mp_validate_pairs_d(mp_ctx* ctx, int32_t E, const int32_t* d_lo, const
   a.row_begin = row_begin;
   a.row_end = row_end;
   return pair_sweep_d(ctx, a, d_row_off, d_viol, cap, num_viol, st);
+}
+
+// ---- joint-mode pair set (K8) -----------------------------------------------------
+namespace {
+// compute_levels / compute_bounds (analysis.cpp:11-62) and the AR bitsets of k_joint.cu
+mp_status joint_tables(mp_graph* g) {
+  if (g->d_joint_mul) return MP_OK;
+  const int32_t n = g->n, E = g->E;
+  if (n > kJointMaxNodes) {
+    set_error("Capacity: the joint-mode pair tables support up to " +
+              std::to_string(kJointMaxNodes) + " nodes");
+    return MP_E_CAPACITY;
+  }
+  std::vector<std::vector<int32_t>> succ(n);
+  std::vector<int32_t> indeg(n, 0);
+  for (int32_t e = 0; e < E; ++e)
+    for (int64_t k = g->h_sink_off[e]; k < g->h_sink_off[e + 1]; ++k) {
+      succ[g->h_edge_src[e]].push_back(g->h_sinks[k]);
+      ++indeg[g->h_sinks[k]];
+    }
+  std::vector<int32_t> order;
+  order.reserve(n);
+  for (int32_t v = 0; v < n; ++v)
+    if (!indeg[v]) order.push_back(v);
+  for (size_t i = 0; i < order.size(); ++i)
+    for (int32_t w : succ[order[i]])
+      if (--indeg[w] == 0) order.push_back(w);
+  if ((int32_t)order.size() != n) {
+    set_error("InvalidStructure: graph has a cycle");
+    return MP_E_BAD_GRAPH;
+  }
+  std::vector<int32_t> fwd(n, 0), bwd(n, 0);
+  for (int32_t v : order)
+    for (int32_t w : succ[v]) fwd[w] = std::max(fwd[w], fwd[v] + 1);
+  for (auto it = order.rbegin(); it != order.rend(); ++it)
+    for (int32_t w : succ[*it]) bwd[*it] = std::max(bwd[*it], bwd[w] + 1);
+  std::vector<int32_t> mul(2 * (size_t)E);
+  for (int32_t e = 0; e < E; ++e) {
+    const int64_t a = g->h_sink_off[e], b = g->h_sink_off[e + 1];
+    int32_t hi = n;
+    if (b > a) {
+      hi = 0;
+      for (int64_t k = a; k < b; ++k) hi = std::max(hi, n - bwd[g->h_sinks[k]]);  // alap
+    }
+    mul[2 * e] = 1 + fwd[g->h_edge_src[e]];  // asap[src]
+    mul[2 * e + 1] = hi;
+  }
+  const int W = (n + 31) / 32, WE = (E + 31) / 32;
+  std::vector<uint32_t> desc((size_t)n * W, 0);  // proper descendants (ReachabilityCache)
+  for (auto it = order.rbegin(); it != order.rend(); ++it) {
+    uint32_t* dv = &desc[(size_t)*it * W];
+    for (int32_t w : succ[*it]) {
+      const uint32_t* dw = &desc[(size_t)w * W];
+      for (int q = 0; q < W; ++q) dv[q] |= dw[q];
+      dv[w >> 5] |= 1u << (w & 31);
+    }
+  }
+  std::vector<uint32_t> ar((size_t)E * W, 0), art((size_t)n * WE, 0);
+  for (int32_t e = 0; e < E; ++e) {
+    const int64_t a = g->h_sink_off[e], b = g->h_sink_off[e + 1];
+    if (b == a) continue;  // no sinks: edge_precedes(e, .) needs the window test alone
+    uint32_t* r = &ar[(size_t)e * W];
+    std::copy(&desc[(size_t)g->h_sinks[a] * W], &desc[(size_t)g->h_sinks[a] * W] + W, r);
+    for (int64_t k = a + 1; k < b; ++k) {
+      const uint32_t* d = &desc[(size_t)g->h_sinks[k] * W];
+      for (int q = 0; q < W; ++q) r[q] &= d[q];
+    }
+    for (int q = 0; q < W; ++q)
+      for (uint32_t m = r[q]; m; m &= m - 1) {
+        const int v = q * 32 + __builtin_ctz(m);
+        art[(size_t)v * WE + (e >> 5)] |= 1u << (e & 31);
+      }
+  }
+  cudaStream_t st = g->ctx->stream;
+  mp_status s = MP_OK;
+  auto up = [&](mp_status r) {
+    if (s == MP_OK) s = r;
+  };
+  int32_t* d_mul = nullptr;
+  up(upload(&d_mul, mul.data(), mul.size(), st));
+  up(upload(&g->d_joint_ar, ar.data(), ar.size(), st));
+  up(upload(&g->d_joint_art, art.data(), art.size(), st));
+  g->d_joint_mul = reinterpret_cast<int2*>(d_mul);
+  g->joint_ar_words = W;
+  g->joint_art_words = WE;
+  if (s == MP_OK) {
+    cudaError_t ce = cudaStreamSynchronize(st);  // host tables go out of scope
+    if (ce != cudaSuccess) s = cuda_status(ce, "joint tables");
+  }
+  return s;
+}
+}  // namespace
+
+mp_status mp_joint_pairs(mp_ctx* ctx, const mp_graph* g, int filter, int32_t* pairs, int64_t cap,
+                         int64_t* count) {
+  if (!ctx || !g || !count) return invalid_arg("null argument");
+  *count = 0;
+  DeviceGuard guard(ctx->device);
+  mp_graph* mg = const_cast<mp_graph*>(g);  // lazily built tables (graph stays immutable)
+  if (g->E == 0) return MP_OK;
+  if (filter) MP_TRY(joint_tables(mg));
+  cudaStream_t st = ctx->stream;
+  const size_t E = (size_t)g->E;
+  MP_TRY(ctx->scratch[0].reserve(Carver::size_of({8 * E, 8 * E, lp_scan_scratch(g->E), 8})));
+  Carver cv(ctx->scratch[0].ptr);
+  int64_t* d_cnt = cv.take<int64_t>(E);
+  int64_t* d_off = cv.take<int64_t>(E);
+  int64_t* d_sums = reinterpret_cast<int64_t*>(cv.take<char>(lp_scan_scratch(g->E)));
+  int64_t* d_tot = cv.take<int64_t>(1);
+  JointArgs a;
+  a.E = g->E;
+  a.filter = filter ? 1 : 0;
+  a.size = g->d_edge_size;
+  a.src = g->d_edge_src;
+  a.mul = g->d_joint_mul;
+  a.ar = g->d_joint_ar;
+  a.art = g->d_joint_art;
+  a.ar_words = g->joint_ar_words;
+  a.art_words = g->joint_art_words;
+  MP_TRY(launch_joint(a, ctx->num_sms, d_cnt, nullptr, nullptr, st));
+  MP_TRY(scan_exclusive_i64(d_cnt, g->E, d_off, d_sums, d_tot, st));
+  int64_t total = 0;
+  MP_CUDA(cudaMemcpyAsync(&total, d_tot, 8, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaStreamSynchronize(st));
+  *count = total;
+  if (!pairs) return MP_OK;
+  if (total > cap) {
+    set_error("Capacity: " + std::to_string(total) + " pairs exceed the buffer of " +
+              std::to_string(cap));
+    return MP_E_CAPACITY;
+  }
+  if (total == 0) return MP_OK;
+  MP_TRY(ctx->scratch[4].reserve(8 * (size_t)total + 256));
+  int2* d_pairs = static_cast<int2*>(ctx->scratch[4].ptr);
+  MP_TRY(launch_joint(a, ctx->num_sms, nullptr, d_off, d_pairs, st));
+  MP_CUDA(cudaMemcpyAsync(pairs, d_pairs, 8 * (size_t)total, cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaStreamSynchronize(st));
+  return MP_OK;
 }
 
 // ---- LP row emission (K7) ---------------------------------------------------------

@@ -102,6 +102,11 @@ struct mp_graph {
   int32_t* d_tile_moff = nullptr;      // [n]
   int32_t* d_tile_mother = nullptr;    // [4m]
   int32_t* d_tile_medge = nullptr;     // [m]
+  // joint-mode pair tables (built on first use, k_joint.cu)
+  int2* d_joint_mul = nullptr;
+  uint32_t* d_joint_ar = nullptr;
+  uint32_t* d_joint_art = nullptr;
+  int joint_ar_words = 0, joint_art_words = 0;
   // tile scorer: per-CTA position words (stamped) that persist across launches
   uint32_t* d_tile_pos = nullptr;      // [tile_grid * n] + [tile_grid] stamps
   int32_t tile_grid = 0;
@@ -187,6 +192,21 @@ struct PlaceArgs {
 };
 size_t place_smem_bytes(int num_edges);
 mp_status launch_place(const PlaceArgs& a, const mp_ctx* ctx, cudaStream_t st);
+// K8 joint-mode pair set (k_joint.cu): encode_joint's pair loop with edge_precedes.
+struct JointArgs {
+  int32_t E = 0;
+  int filter = 1;
+  const uint64_t* size = nullptr;
+  const int32_t* src = nullptr;
+  const int2* mul = nullptr;           // [E] compute_bounds' multiplicity windows
+  const uint32_t* ar = nullptr;        // [E][ar_words]  AR(e): nodes every sink of e reaches
+  const uint32_t* art = nullptr;       // [n][art_words] transposed
+  int ar_words = 0, art_words = 0;
+};
+mp_status launch_joint(const JointArgs& a, int num_sms, int64_t* d_row_cnt,
+                       const int64_t* d_row_off, int2* d_pairs, cudaStream_t st);
+constexpr int32_t kJointMaxNodes = 32768;  // descendant bitsets on the host: n^2 / 8 bytes
+
 // K7 LP row emission (k_lp.cu): write_lp text of encode_addresses' pair rows.
 struct LpArgs {
   int32_t E = 0;

@@ -424,6 +424,19 @@ class Planner:
                                                 has.ctypes.data, ad.ctypes.data, C.byref(out)))
         return int(out.value)
 
+    # ---- joint-mode pair set (K8, k_joint.cu) -----------------------------------------
+    def joint_pairs(self, graph: Graph, filter_pairs: bool = True) -> np.ndarray:
+        """The pair loop of encode_joint (encode.cpp:401-408) -> int32[P][2] in (i, j) order:
+        data-edge pairs not ordered by the graph (edge_precedes, analysis.cpp:94-113)."""
+        dg = self.upload(graph)
+        cnt = C.c_int64()
+        _native.check(_native.lib().mp_joint_pairs(self.ctx, dg.handle, int(filter_pairs), None,
+                                                   0, C.byref(cnt)))
+        out = np.zeros((max(cnt.value, 1), 2), np.int32)
+        _native.check(_native.lib().mp_joint_pairs(self.ctx, dg.handle, int(filter_pairs),
+                                                   out.ctypes.data, cnt.value, C.byref(cnt)))
+        return out[: cnt.value]
+
     # ---- non-overlap rows as LP text (K7, k_lp.cu) ------------------------------------
     def encode_addresses_lp(self, graph: Graph, lo, hi,
                             preplaced: Optional[Mapping[int, int]] = None,

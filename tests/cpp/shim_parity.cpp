@@ -190,6 +190,22 @@ static void check_graph(memplan_b200::Planner& dev, const Graph& g, std::mt19937
   }
   EXPECT(best == ref_best, "first-minimum argmin");
 
+  // encode_joint's pair loop (encode.cpp:401-408) with the reference's edge_precedes
+  {
+    const LifetimeBounds bounds = compute_bounds(g);
+    ReachabilityCache reach(g);
+    std::vector<std::pair<EdgeIndex, EdgeIndex>> ref;
+    std::vector<EdgeIndex> data;
+    for (int e = 0; e < g.num_edges(); ++e)
+      if (g.edge(e).size > 0) data.push_back(e);
+    for (size_t a = 0; a < data.size(); ++a)
+      for (size_t b = a + 1; b < data.size(); ++b)
+        if (!edge_precedes(g, bounds, data[a], data[b], &reach) &&
+            !edge_precedes(g, bounds, data[b], data[a], &reach))
+          ref.push_back({data[a], data[b]});
+    EXPECT(dev.joint_pairs(g) == ref, "joint pairs");
+  }
+
   // validate_plan on the reference planner's own plan, plus tampered copies
   if (g.num_nodes() <= 12) {
     MemoryPlan good = plan_graph(g).plan;

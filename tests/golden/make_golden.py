@@ -204,6 +204,9 @@ def graph_record(name, g: "O.RefGraph", rng, n_random=3, plans=True):
     for o in invalid_variants(po, g.n):
         cases.append(order_case(g, o))
     rec["orders"] = cases
+    # encode_joint's pair set (encode.cpp:401-408), filtered by edge_precedes and not
+    rec["joint_pairs"] = {"filtered": g.joint_pairs(True).tolist(),
+                          "all": len(g.joint_pairs(False))}
     # pinned (preplaced) pair sets on program order
     if g.n:
         lo, hi = g.lifetimes_from_order(po)
