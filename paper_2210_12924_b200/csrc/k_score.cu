@@ -297,7 +297,8 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
 #pragma unroll
         for (int u = 0; u < kB; ++u) {
           const int k = k0 + u * T;
-          vv[u] = k < n ? __ldg(ord + k) : 0;
+          // global-scratch variant: orders are read once, evict-first (keep the scratch in L2)
+          vv[u] = k < n ? (kSmem ? __ldg(ord + k) : __ldcs(ord + k)) : 0;
         }
 #pragma unroll
         for (int u = 0; u < kB; ++u) {
@@ -488,6 +489,29 @@ ScoreTables tables(const mp_graph* g) {
   return G;
 }
 
+// An L2 persisting access-policy window over [base, base + bytes) for one launch
+// (the per-CTA scratch of the large-graph scorers); false when unsupported.
+bool l2_persist_window(const mp_ctx* ctx, void* base, size_t bytes, cudaLaunchAttribute* at) {
+  int max_win = 0, persist_max = 0;
+  cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device);
+  cudaDeviceGetAttribute(&persist_max, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
+  if (max_win <= 0 || persist_max <= 0 || bytes == 0) return false;
+  static bool limit_set = false;  // process-wide device limit, set once
+  if (!limit_set) {
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)persist_max);
+    limit_set = true;
+  }
+  const size_t win = bytes < (size_t)max_win ? bytes : (size_t)max_win;
+  at->id = cudaLaunchAttributeAccessPolicyWindow;
+  at->val.accessPolicyWindow.base_ptr = base;
+  at->val.accessPolicyWindow.num_bytes = win;
+  const double r = (double)persist_max / (double)win;
+  at->val.accessPolicyWindow.hitRatio = (float)(r < 1.0 ? r : 1.0);
+  at->val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  at->val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  return true;
+}
+
 template <typename VT, typename PW, int J, bool kSmem>
 mp_status run(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d_peak,
               int32_t* d_step, uint8_t* d_valid, uint64_t* d_bytes, uint64_t* d_key,
@@ -522,10 +546,21 @@ mp_status run(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d
   }
   if (grid > C) grid = C;
   if (grid < 1) return MP_OK;
-  kern<<<(unsigned)grid, T, smem, st>>>(tables(g), d_orders, C, d_peak, d_step, d_valid, d_bytes,
-                                        reinterpret_cast<unsigned long long*>(d_key), index_base,
-                                        gs, gstride);
-  MP_CUDA(cudaGetLastError());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  cfg.attrs = at;
+  cfg.numAttrs = 0;
+  // An L2 persisting window over this scratch measured 2.3x SLOWER at C5 (only 79 of its
+  // 237 MB can persist; the rest turns evict-first): opt-in via MP_L2_WINDOW for tuning.
+  if (!kSmem && std::getenv("MP_L2_WINDOW"))
+    cfg.numAttrs = l2_persist_window(g->ctx, gs, gstride * (size_t)grid, &at[0]) ? 1 : 0;
+  MP_CUDA(cudaLaunchKernelEx(&cfg, kern, tables(g), d_orders, C, d_peak, d_step, d_valid, d_bytes,
+                             reinterpret_cast<unsigned long long*>(d_key), index_base, gs,
+                             gstride));
   return MP_OK;
 }
 
@@ -596,27 +631,9 @@ mp_status run_tile(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   int nat = 0;
-  int max_win = 0, persist_max = 0;
-  cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, g->ctx->device);
-  cudaDeviceGetAttribute(&persist_max, cudaDevAttrMaxPersistingL2CacheSize, g->ctx->device);
-  if (max_win > 0 && persist_max > 0 && !std::getenv("MP_NO_L2_WINDOW")) {
-    // the word slices stay in L2 (persisting); the rest of the window streams
-    static bool limit_set = false;  // process-wide device limit, set once
-    if (!limit_set) {
-      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)persist_max);
-      limit_set = true;
-    }
-    const size_t bytes = ((size_t)g->tile_grid * g->n + g->tile_grid) * 4;
-    const size_t win = bytes < (size_t)max_win ? bytes : (size_t)max_win;
-    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
-    at[0].val.accessPolicyWindow.base_ptr = g->d_tile_pos;
-    at[0].val.accessPolicyWindow.num_bytes = win;
-    const double r = (double)persist_max / (double)win;
-    at[0].val.accessPolicyWindow.hitRatio = (float)(r < 1.0 ? r : 1.0);
-    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    nat = 1;
-  }
+  if (!std::getenv("MP_NO_L2_WINDOW"))
+    nat = l2_persist_window(g->ctx, g->d_tile_pos,
+                            ((size_t)g->tile_grid * g->n + g->tile_grid) * 4, &at[0]) ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = nat;
   MP_CUDA(cudaLaunchKernelEx(&cfg, score_tile_kernel<VT, PT>, tables(g), d_orders, C, d_peak,
