@@ -116,6 +116,45 @@ struct XFPair {
   VT x, f;
 };
 
+// Storage of the per-position (x, f) scan inputs of the node-table scorer.
+template <typename VT>
+struct XFWide {  // one XFPair<VT> per position
+  using E = XFPair<VT>;
+  __device__ static void store(E* a, int i, VT x, VT f) { a[i] = E{x, f}; }
+  __device__ static void pad(E* a, int i) { a[i] = E{0, 0}; }
+  __device__ static void free_at(E* a, int i, VT sz) {  // freed after position i
+    atomicAdd(&a[i].f, sz);
+    atomicAdd(&a[i].x, (VT)0 - sz);
+  }
+  __device__ static void load(const E* a, int i, VT& x, VT& f) {
+    const E e = a[i];
+    x = e.x;
+    f = e.f;
+  }
+};
+// Graphs whose per-node values fit a byte once every order-dependent free is
+// counted (mp_prep.cpp `tiny8`, e.g. C5): 2 bytes per position, x + 128 in the
+// low byte, f in the high byte - a quarter of the wide footprint, so the per-CTA
+// scratch of the large-graph scorer stays L2-resident. A free adds 255*sz to
+// the 16-bit entry (x -= sz, f += sz): no borrow or carry leaves the entry
+// because the static bounds hold for every order.
+struct XFTiny8 {
+  using E = uint16_t;
+  __device__ static void store(E* a, int i, uint32_t x, uint32_t f) {
+    a[i] = (E)(((x + 128u) & 0xffu) | (f << 8));
+  }
+  __device__ static void pad(E* a, int i) { a[i] = 128; }
+  __device__ static void free_at(E* a, int i, uint32_t sz) {
+    const uintptr_t at = reinterpret_cast<uintptr_t>(a + i);
+    atomicAdd(reinterpret_cast<unsigned int*>(at & ~uintptr_t(3)), (sz * 255u) << ((at & 2) * 8));
+  }
+  __device__ static void load(const E* a, int i, uint32_t& x, uint32_t& f) {
+    const uint32_t e = a[i];
+    x = (e & 0xffu) - 128u;
+    f = e >> 8;
+  }
+};
+
 template <typename VT>
 __device__ __forceinline__ VT warp_sum(VT v) {
 #pragma unroll
@@ -154,7 +193,7 @@ struct BlockScratch {
   int widx[32];
 };
 
-template <typename VT, typename PW>
+template <typename VT, typename PW, typename XS = XFWide<VT>>
 struct Layout {
   // smem (or per-CTA global) layout: extra pairs, dyn tables, pos, XF
   static size_t bytes(int n, int T, int P, int nextra, int ndyn, int ndyn_sinks, bool tables) {
@@ -166,7 +205,7 @@ struct Layout {
       b += ((size_t)ndyn * sizeof(VT) + 15) & ~size_t(15);
     }
     b += ((size_t)n * sizeof(PW) + 15) & ~size_t(15);
-    b += (size_t)T * P * sizeof(XFPair<VT>);
+    b += ((size_t)T * P * sizeof(typename XS::E) + 15) & ~size_t(15);
     return b + 16;
   }
 };
@@ -175,7 +214,7 @@ struct Layout {
 //        flat tables in shared memory.
 // J == 0: node data read from global (coalesced) per candidate; buffers in
 //        shared memory (kSmem) or in a per-CTA global scratch slice.
-template <typename VT, typename PW, int J, bool kSmem>
+template <typename VT, typename PW, int J, bool kSmem, typename XS = XFWide<VT>>
 __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
     score_kernel(ScoreTables G, const int32_t* __restrict__ orders, int64_t C,
                  uint64_t* __restrict__ peak_out, int32_t* __restrict__ step_out,
@@ -227,9 +266,9 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
   }
   PW* pos = reinterpret_cast<PW*>(p);
   p += ((size_t)n * sizeof(PW) + 15) & ~size_t(15);
-  XFPair<VT>* XF = reinterpret_cast<XFPair<VT>*>(p);
+  typename XS::E* XF = reinterpret_cast<typename XS::E*>(p);
   for (int i = tid; i < n; i += T) pos[i] = 0;  // stamp 0 is never used
-  for (int i = n + tid; i < T * P; i += T) XF[i] = XFPair<VT>{0, 0};  // scan padding
+  for (int i = n + tid; i < T * P; i += T) XS::pad(XF, i);  // scan padding
 
   // ---- static per-node data in registers -------------------------------------
   constexpr int JR = J > 0 ? J : 1;
@@ -318,7 +357,7 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
       bad |= !PWT::fresh(w, tag);           // never written: not a permutation
       if (u >= 0) bad |= pos[u] >= w;       // producer not strictly before v
       const int q = PWT::pos(w);
-      if (q < n) XF[q] = XFPair<VT>{x, f};
+      if (q < n) XS::store(XF, q, x, f);
     };
     if (J > 0) {
 #pragma unroll
@@ -346,7 +385,7 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
           if (v0 + u * T < n) {
             bad |= !PWT::fresh(w[u], tag) || pu[u] >= w[u];
             const int q = PWT::pos(w[u]);
-            if (q < n) XF[q] = XFPair<VT>{xx[u], ff[u]};
+            if (q < n) XS::store(XF, q, xx[u], ff[u]);
           }
         }
       }
@@ -386,8 +425,7 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
           const int q = PWT::pos(h[u]);
           if (d < G.ndyn && q < n) {
             const VT sz = kSmem ? dy_size[d] : (VT)dy_size64[d];
-            atomicAdd(&XF[q].f, sz);
-            atomicAdd(&XF[q].x, (VT)0 - sz);
+            XS::free_at(XF, q, sz);
           }
         }
       }
@@ -402,10 +440,14 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
     }
 
     // ---- phase 3: blocked two-pass scan (chunk [tid*P, tid*P+P), P odd) ------------
-    const XFPair<VT>* mine = XF + tid * P;
+    const typename XS::E* mine = XF + tid * P;
     VT total = 0;
 #pragma unroll 8
-    for (int i = 0; i < P; ++i) total += mine[i].x;
+    for (int i = 0; i < P; ++i) {
+      VT x, f;
+      XS::load(mine, i, x, f);
+      total += x;
+    }
     const VT incl = warp_incl_scan(total, lane);
     if (lane == kWarp - 1) bs.wsum[warp] = incl;
     __syncthreads();
@@ -415,9 +457,10 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
     const int p0 = tid * P;
     const int lim = min(P, n - p0);
     for (int i = 0; i < lim; ++i) {
-      const XFPair<VT> xf = mine[i];
-      run += xf.x;
-      const VT rs = run + xf.f;
+      VT xx, ff;
+      XS::load(mine, i, xx, ff);
+      run += xx;
+      const VT rs = run + ff;
       if (bytes_out) bytes_out[c * n + p0 + i] = (uint64_t)rs * G.scale;
       if (rs > best || best_i == INT_MAX) {
         best = rs;
@@ -512,13 +555,13 @@ bool l2_persist_window(const mp_ctx* ctx, void* base, size_t bytes, cudaLaunchAt
   return true;
 }
 
-template <typename VT, typename PW, int J, bool kSmem>
+template <typename VT, typename PW, int J, bool kSmem, typename XS = XFWide<VT>>
 mp_status run(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d_peak,
               int32_t* d_step, uint8_t* d_valid, uint64_t* d_bytes, uint64_t* d_key,
               int64_t index_base, cudaStream_t st) {
-  auto kern = score_kernel<VT, PW, J, kSmem>;
+  auto kern = score_kernel<VT, PW, J, kSmem, XS>;
   const int T = g->score_threads;
-  const size_t per = Layout<VT, PW>::bytes(g->n, T, g->score_p, g->n_extra, g->n_dyn,
+  const size_t per = Layout<VT, PW, XS>::bytes(g->n, T, g->score_p, g->n_extra, g->n_dyn,
                                            g->n_dyn_sinks, kSmem);
   size_t smem = 0;
   char* gs = nullptr;
@@ -664,8 +707,12 @@ mp_status dispatch(const mp_graph* g, const int32_t* o, int64_t C, uint64_t* pk,
     default:
       if (g->smem_resident)
         return run<VT, uint32_t, 0, true>(g, o, C, pk, stp, vl, by, key, base, st);
-      if (g->n < (1 << 24) && !std::getenv("MP_SCORE_POS64"))
+      if (g->n < (1 << 24) && !std::getenv("MP_SCORE_POS64")) {
+        if constexpr (sizeof(VT) == 4)
+          if (g->tiny8 && !std::getenv("MP_SCORE_WIDE_XF"))
+            return run<VT, int32_t, 0, false, XFTiny8>(g, o, C, pk, stp, vl, by, key, base, st);
         return run<VT, int32_t, 0, false>(g, o, C, pk, stp, vl, by, key, base, st);
+      }
       return run<VT, unsigned long long, 0, false>(g, o, C, pk, stp, vl, by, key, base, st);
   }
 }

@@ -236,6 +236,7 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
   g->n_dyn_sinks = (int32_t)P.dyn_sinks.size();
   g->scale = P.scale;
   g->narrow = P.narrow;
+  g->tiny8 = P.tiny8;
   g->exact_reach = P.exact_reach;
 
   DeviceGuard guard(ctx->device);

@@ -77,6 +77,7 @@ struct mp_graph {
   int32_t n_dyn_sinks = 0;
   uint64_t scale = 1;
   bool narrow = true;
+  bool tiny8 = false;                // per-position (x, f) fit a byte each (mp_prep.h)
   bool exact_reach = false;
   uint64_t* d_node_x = nullptr;      // [n] alloc - static free (scaled, modular)
   uint64_t* d_node_f = nullptr;      // [n] static free (scaled)

@@ -165,6 +165,24 @@ void prepare_scoring(int32_t n, int32_t E, const int32_t* src, const int64_t* si
     P->node_x[v] = alloc[v] - sfree[v];  // modular; exact after the prefix sum
     P->node_f[v] = sfree[v];
   }
+  // byte-sized scan inputs? x in [-128, 127] and f <= 255 whatever the order:
+  // the order-dependent frees can only lower x and raise f at a candidate sink
+  {
+    std::vector<int64_t> xmin(n), fmax(n);
+    bool ok = P->narrow;
+    for (int32_t v = 0; v < n; ++v) {
+      xmin[v] = (int64_t)alloc[v] - (int64_t)sfree[v];
+      fmax[v] = (int64_t)sfree[v];
+      ok &= xmin[v] <= 127;
+    }
+    for (size_t d = 0; d + 1 < P->dyn_off.size(); ++d)
+      for (int32_t k = P->dyn_off[d]; k < P->dyn_off[d + 1]; ++k) {
+        xmin[P->dyn_sinks[k]] -= (int64_t)P->dyn_size[d];
+        fmax[P->dyn_sinks[k]] += (int64_t)P->dyn_size[d];
+      }
+    for (int32_t v = 0; v < n && ok; ++v) ok = xmin[v] >= -128 && fmax[v] <= 255;
+    P->tiny8 = ok;
+  }
   // second producer per node; the rest (3rd+) as a flat packed list
   P->pred2.assign(n, -1);
   {

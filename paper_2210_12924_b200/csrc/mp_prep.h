@@ -12,6 +12,7 @@ struct ScorePrep {
   int32_t n = 0;
   bool exact_reach = false;
   bool narrow = true;           // total scaled bytes < 2^32: 32-bit arithmetic
+  bool tiny8 = false;           // every node's x in [-128, 127] and f <= 255 for any order
   uint64_t scale = 1;           // gcd of data sizes
   // node tables (scaled): x = alloc - static free, f = static free
   std::vector<uint64_t> node_x, node_f;

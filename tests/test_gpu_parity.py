@@ -255,7 +255,8 @@ def test_scorer_variants_small_graphs(planner, monkeypatch, mode, kind, layers, 
 
 
 @pytest.mark.parametrize("layers,smem,mode", [(3000, 1, ""), (20000, 0, ""), (20000, 0, "tile"),
-                                              (20000, 0, "scratch64"), (3000, 1, "tile")])
+                                              (20000, 0, "scratch64"), (3000, 1, "tile"),
+                                              (20000, 0, "widexf")])
 def test_large_graph_variants(planner, monkeypatch, layers, smem, mode):
     """Graphs past the register-resident variant: node tables read per candidate,
     buffers in shared memory (n=12k); at n=80k >= 65536 the node-space kernel with
@@ -263,6 +264,8 @@ def test_large_graph_variants(planner, monkeypatch, layers, smem, mode):
     words, or the tile scorer; the tile scorer forced on the 12k graph too."""
     if mode == "scratch64":
         monkeypatch.setenv("MP_SCORE_POS64", "1")
+    if mode == "widexf":   # training_like fits the byte-packed scan inputs; force the wide ones
+        monkeypatch.setenv("MP_SCORE_WIDE_XF", "1")
     if mode == "tile":
         monkeypatch.setenv("MP_SCORE_MODE", "tile")
     g = mp.generate_graph("training_like", layers, 8)
@@ -335,6 +338,24 @@ def test_tile_scorer_model_graphs(planner, monkeypatch, name):
             assert res.valid[i] == 1 and (int(res.peak[i]), int(res.peak_step[i])) == (pr, ps), i
     rs = planner.resident_bytes_per_step(g, orders[0])
     assert (rs == orc.resident_bytes_per_step(orders[0])).all()
+
+
+def test_large_fork_join_wide_values(planner):
+    """A 100k+-node graph whose per-node values do not fit a byte (random fork-join
+    widths, 2^20-byte sizes): the global-scratch scorer with wide scan inputs."""
+    g = mp.generate_graph("fork_join", 15000, 1 << 20, 1)
+    assert g.n >= 65536
+    orc = O.Oracle.from_csr(g.csr())
+    orders = mp.random_topo_orders(g, 6, seed=4)
+    orders[2, [0, 1]] = orders[2, [1, 0]]
+    res = planner.score_orders(g, orders)
+    for i, o in enumerate(orders):
+        if not orc.is_topological_order(o):
+            assert res.valid[i] == 0
+            continue
+        rs = orc.resident_bytes_per_step(o)
+        assert res.valid[i] == 1
+        assert (int(res.peak[i]), int(res.peak_step[i])) == (int(rs.max()), int(np.argmax(rs)) + 1)
 
 
 def test_c5_full_size(golden, planner):
