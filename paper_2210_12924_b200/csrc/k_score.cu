@@ -76,6 +76,7 @@ struct ScoreTables {
   const int32_t* __restrict__ tile_moff;
   const int4* __restrict__ tile_mother;
   const int32_t* __restrict__ tile_medge;
+  const int4* __restrict__ dyn_sink4;        // [ndyn] candidate sinks, -1 padded (<= 4 each)
 };
 
 // Position word: stamp in the high half, position in the low half. Within one
@@ -412,12 +413,29 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
       constexpr int kB = 4;
       for (int d0 = tid; d0 < G.ndyn; d0 += T * kB) {
         PW h[kB];
+        if (G.dyn_sink4 != nullptr) {  // <= 4 candidate sinks each: one 16-byte load per edge
+          int4 sk[kB];
 #pragma unroll
-        for (int u = 0; u < kB; ++u) {  // gathers of kB edges before any atomic
-          const int d = d0 + u * T;
-          h[u] = 0;
-          if (d < G.ndyn)
-            for (int s = dy_off[d]; s < dy_off[d + 1]; ++s) h[u] = max(h[u], pos[dy_sinks[s]]);
+          for (int u = 0; u < kB; ++u) {
+            const int d = d0 + u * T;
+            sk[u] = d < G.ndyn ? __ldg(G.dyn_sink4 + d) : make_int4(-1, -1, -1, -1);
+          }
+#pragma unroll
+          for (int u = 0; u < kB; ++u) {  // every gather of the batch before any atomic
+            const PW a = sk[u].x >= 0 ? pos[sk[u].x] : (PW)0;
+            const PW b = sk[u].y >= 0 ? pos[sk[u].y] : (PW)0;
+            const PW c2 = sk[u].z >= 0 ? pos[sk[u].z] : (PW)0;
+            const PW d2 = sk[u].w >= 0 ? pos[sk[u].w] : (PW)0;
+            h[u] = max(max(a, b), max(c2, d2));
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < kB; ++u) {  // gathers of kB edges before any atomic
+            const int d = d0 + u * T;
+            h[u] = 0;
+            if (d < G.ndyn)
+              for (int s = dy_off[d]; s < dy_off[d + 1]; ++s) h[u] = max(h[u], pos[dy_sinks[s]]);
+          }
         }
 #pragma unroll
         for (int u = 0; u < kB; ++u) {
@@ -529,6 +547,7 @@ ScoreTables tables(const mp_graph* g) {
   G.tile_moff = g->d_tile_moff;
   G.tile_mother = reinterpret_cast<const int4*>(g->d_tile_mother);
   G.tile_medge = g->d_tile_medge;
+  G.dyn_sink4 = reinterpret_cast<const int4*>(g->d_dyn_sink4);
   return G;
 }
 

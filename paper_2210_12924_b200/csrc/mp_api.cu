@@ -234,6 +234,8 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
   g->n_extra = (int32_t)P.extra_u.size();
   g->n_dyn = (int32_t)P.dyn_size.size();
   g->n_dyn_sinks = (int32_t)P.dyn_sinks.size();
+  for (size_t d = 0; d + 1 < P.dyn_off.size(); ++d)
+    g->dyn_max_sinks = std::max(g->dyn_max_sinks, P.dyn_off[d + 1] - P.dyn_off[d]);
   g->scale = P.scale;
   g->narrow = P.narrow;
   g->tiny8 = P.tiny8;
@@ -266,6 +268,13 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
   g->n_extra3w = (int32_t)P.extra3_u.size();
   up(upload(&g->d_node_dyn_off, P.node_dyn_off.data(), P.node_dyn_off.size(), st));
   up(upload(&g->d_node_dyn, P.node_dyn.data(), P.node_dyn.size(), st));
+  if (g->dyn_max_sinks <= 4 && g->n_dyn > 0) {
+    std::vector<int32_t> s4(4 * (size_t)g->n_dyn, -1);
+    for (int32_t d = 0; d < g->n_dyn; ++d)
+      for (int32_t k = P.dyn_off[d]; k < P.dyn_off[d + 1]; ++k)
+        s4[4 * (size_t)d + (k - P.dyn_off[d])] = P.dyn_sinks[k];
+    up(upload(&g->d_dyn_sink4, s4.data(), s4.size(), st));
+  }
   up(upload(&g->d_out_off, P.out_off.data(), P.out_off.size(), st));
   up(upload(&g->d_out_edges, P.out_edges.data(), P.out_edges.size(), st));
   up(upload(&g->d_tile_zw, P.tile_zw.data(), P.tile_zw.size(), st));
@@ -294,7 +303,7 @@ mp_status mp_graph_free(mp_graph* g) {
                   g->d_extra_w,  g->d_dyn_off,   g->d_dyn_sinks, g->d_dyn_size,
                   g->d_node_rec32, g->d_node_u2, g->d_extra3_packed, g->d_extra3_u,
                   g->d_extra3_w, g->d_node_dyn_off, g->d_node_dyn, g->d_tile_pos,
-                  g->d_out_off, g->d_out_edges, g->d_joint_mul, g->d_joint_ar, g->d_joint_art, g->d_tile_zw, g->d_tile_rec32, g->d_tile_moff, g->d_tile_mother, g->d_tile_medge};
+                  g->d_out_off, g->d_out_edges, g->d_dyn_sink4, g->d_joint_mul, g->d_joint_ar, g->d_joint_art, g->d_tile_zw, g->d_tile_rec32, g->d_tile_moff, g->d_tile_mother, g->d_tile_medge};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete g;

@@ -75,6 +75,7 @@ struct mp_graph {
   int32_t n_extra = 0;               // reduced pairs beyond each node's first producer
   int32_t n_dyn = 0;                 // data edges whose last consumer depends on the order
   int32_t n_dyn_sinks = 0;
+  int32_t dyn_max_sinks = 0;         // most candidate last consumers of one dynamic edge
   uint64_t scale = 1;
   bool narrow = true;
   bool tiny8 = false;                // per-position (x, f) fit a byte each (mp_prep.h)
@@ -86,6 +87,7 @@ struct mp_graph {
   int32_t* d_extra_w = nullptr;      // [n_extra]
   int32_t* d_dyn_off = nullptr;      // [n_dyn+1]
   int32_t* d_dyn_sinks = nullptr;    // [n_dyn_sinks]
+  int32_t* d_dyn_sink4 = nullptr;    // [4 n_dyn] when every dynamic edge has <= 4 candidates
   uint64_t* d_dyn_size = nullptr;    // [n_dyn] scaled
   uint32_t* d_node_rec32 = nullptr;    // [4n] (x, f, pred1, pred2), 32-bit graphs
   int32_t* d_node_u2 = nullptr;        // [2n] (pred1, pred2)
