@@ -457,32 +457,80 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
       continue;
     }
 
-    // ---- phase 3: blocked two-pass scan (chunk [tid*P, tid*P+P), P odd) ------------
-    const typename XS::E* mine = XF + tid * P;
-    VT total = 0;
-#pragma unroll 8
-    for (int i = 0; i < P; ++i) {
-      VT x, f;
-      XS::load(mine, i, x, f);
-      total += x;
-    }
-    const VT incl = warp_incl_scan(total, lane);
-    if (lane == kWarp - 1) bs.wsum[warp] = incl;
-    __syncthreads();
-    VT run = warp_sum(lane < warp ? bs.wsum[lane] : (VT)0) + incl - total;
     VT best = 0;
     int best_i = INT_MAX;
-    const int p0 = tid * P;
-    const int lim = min(P, n - p0);
-    for (int i = 0; i < lim; ++i) {
-      VT xx, ff;
-      XS::load(mine, i, xx, ff);
-      run += xx;
-      const VT rs = run + ff;
-      if (bytes_out) bytes_out[c * n + p0 + i] = (uint64_t)rs * G.scale;
-      if (rs > best || best_i == INT_MAX) {
-        best = rs;
-        best_i = p0 + i;
+    if constexpr (kSmem) {
+      // ---- phase 3: blocked two-pass scan (chunk [tid*P, tid*P+P), P odd) ----------
+      const typename XS::E* mine = XF + tid * P;
+      VT total = 0;
+#pragma unroll 8
+      for (int i = 0; i < P; ++i) {
+        VT x, f;
+        XS::load(mine, i, x, f);
+        total += x;
+      }
+      const VT incl = warp_incl_scan(total, lane);
+      if (lane == kWarp - 1) bs.wsum[warp] = incl;
+      __syncthreads();
+      VT run = warp_sum(lane < warp ? bs.wsum[lane] : (VT)0) + incl - total;
+      const int p0 = tid * P;
+      const int lim = min(P, n - p0);
+      for (int i = 0; i < lim; ++i) {
+        VT xx, ff;
+        XS::load(mine, i, xx, ff);
+        run += xx;
+        const VT rs = run + ff;
+        if (bytes_out) bytes_out[c * n + p0 + i] = (uint64_t)rs * G.scale;
+        if (rs > best || best_i == INT_MAX) {
+          best = rs;
+          best_i = p0 + i;
+        }
+      }
+    } else {
+      // ---- phase 3, scan inputs in global scratch: warp rows -------------------------
+      // Warp w owns positions [w*32P, (w+1)*32P) and reads them 128 at a time, four
+      // consecutive per lane: each load instruction touches two lines instead of 32
+      // (the blocked layout's per-thread chunks put every lane on its own line).
+      const int wbeg = warp * kWarp * P, wend = wbeg + kWarp * P;
+      VT tot = 0;
+      for (int r = wbeg + 4 * lane; r < wend; r += 4 * kWarp)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (r + q < wend) {
+            VT xx, ff;
+            XS::load(XF, r + q, xx, ff);
+            tot += xx;
+          }
+      tot = warp_sum(tot);
+      if (lane == 0) bs.wsum[warp] = tot;
+      __syncthreads();
+      VT carry = warp_sum(lane < warp ? bs.wsum[lane] : (VT)0);  // exclusive over warps
+      for (int r0 = wbeg; r0 < wend; r0 += 4 * kWarp) {
+        const int r = r0 + 4 * lane;
+        VT xs[4], fs[4], t = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          xs[q] = 0;
+          fs[q] = 0;
+          if (r + q < wend) XS::load(XF, r + q, xs[q], fs[q]);
+          t += xs[q];
+        }
+        const VT incl = warp_incl_scan(t, lane);
+        VT run = carry + incl - t;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          run += xs[q];
+          const VT rs = run + fs[q];
+          const int k = r + q;
+          if (k < n && k < wend) {
+            if (bytes_out) bytes_out[c * n + k] = (uint64_t)rs * G.scale;
+            if (best_i == INT_MAX || rs > best) {
+              best = rs;
+              best_i = k;
+            }
+          }
+        }
+        carry += __shfl_sync(0xffffffffu, incl, kWarp - 1);
       }
     }
     warp_argmax(best, best_i);
