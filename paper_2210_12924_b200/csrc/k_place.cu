@@ -30,6 +30,7 @@
 
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "mp_internal.h"
 
@@ -99,17 +100,20 @@ __global__ void __launch_bounds__(kPT, 512 / kPT)
 
     // Place one tensor (size s, lifetime [elo, ehi]) at x, or - when `search` -
     // at greedy_pack's lowest feasible offset; returns the offset.
-    auto place = [&](bool search, unsigned long long x, unsigned long long s, int elo,
-                     int ehi) -> unsigned long long {
+    // CHT: compile-time bound on the per-thread chunk, chosen per step (2/4/8/16)
+    // so early steps do not pay for 16 predicated-off register slots.
+    auto place_ch = [&](auto cht, bool search, unsigned long long x, unsigned long long s,
+                        int elo, int ehi) -> unsigned long long {
+      constexpr int kCh = decltype(cht)::value;
       const int ch = (k + kPT - 1) / kPT;
       const int i0 = tid * ch;
-      int o[kChMax];
+      int o[kCh];
 #pragma unroll
-      for (int q = 0; q < kChMax; ++q) o[q] = (q < ch && i0 + q < k) ? ord[i0 + q] : -1;
+      for (int q = 0; q < kCh; ++q) o[q] = (q < ch && i0 + q < k) ? ord[i0 + q] : -1;
       if (search) {
         long long cm = LLONG_MIN;  // max top over this chunk's conflicting tensors
 #pragma unroll
-        for (int q = 0; q < kChMax; ++q)
+        for (int q = 0; q < kCh; ++q)
           if (o[q] >= 0) {
             const int2 l = e_life[o[q]];
             if (!disjoint(elo, ehi, l.x, l.y)) {
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(kPT, 512 / kPT)
         int stop = INT_MAX;
         long long xs = 0;
 #pragma unroll
-        for (int q = 0; q < kChMax; ++q)
+        for (int q = 0; q < kCh; ++q)
           if (stop == INT_MAX && o[q] >= 0) {
             const int2 l = e_life[o[q]];
             if (!disjoint(elo, ehi, l.x, l.y)) {
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(kPT, 512 / kPT)
       // insert at the first address-order index whose address is >= x
       int cnt = 0;
 #pragma unroll
-      for (int q = 0; q < kChMax; ++q)
+      for (int q = 0; q < kCh; ++q)
         if (o[q] >= 0) cnt += e_addr[o[q]] < x;
       if (tid == 0) ps.pos = 0;
       __syncthreads();
@@ -172,7 +176,7 @@ __global__ void __launch_bounds__(kPT, 512 / kPT)
       __syncthreads();
       const int p = ps.pos;
 #pragma unroll
-      for (int q = 0; q < kChMax; ++q)
+      for (int q = 0; q < kCh; ++q)
         if (o[q] >= 0 && i0 + q >= p) ord[i0 + q + 1] = o[q];
       if (tid == 0) {
         ord[p] = k;
@@ -183,6 +187,14 @@ __global__ void __launch_bounds__(kPT, 512 / kPT)
       __syncthreads();
       ++k;
       return x;
+    };
+    auto place = [&](bool search, unsigned long long x, unsigned long long s, int elo,
+                     int ehi) -> unsigned long long {
+      const int ch = (k + kPT - 1) / kPT;
+      if (ch <= 2) return place_ch(std::integral_constant<int, 2>{}, search, x, s, elo, ehi);
+      if (ch <= 4) return place_ch(std::integral_constant<int, 4>{}, search, x, s, elo, ehi);
+      if (ch <= 8) return place_ch(std::integral_constant<int, 8>{}, search, x, s, elo, ehi);
+      return place_ch(std::integral_constant<int, kChMax>{}, search, x, s, elo, ehi);
     };
 
     // ---- fixed tensors: caller's preplaced map, or preallocate_pyramid ------------
@@ -329,6 +341,9 @@ mp_status launch_place_t(const PlaceArgs& in, const mp_ctx* ctx, cudaStream_t st
 mp_status launch_place(const PlaceArgs& in, const mp_ctx* ctx, cudaStream_t st) {
   if (in.num_problems <= 0 || in.num_edges == 0) return MP_OK;
   // + preplaced entries never exceed num_edges: the placed set holds <= E tensors
+  // few problems (latency): the widest CTA, short chunks; many (throughput): the
+  // narrowest CTA that holds the placed set, several problems per SM
+  if (in.num_problems <= ctx->num_sms) return launch_place_t<512>(in, ctx, st);
   if (in.num_edges <= 128 * kChMax) return launch_place_t<128>(in, ctx, st);
   if (in.num_edges <= 256 * kChMax) return launch_place_t<256>(in, ctx, st);
   return launch_place_t<512>(in, ctx, st);
