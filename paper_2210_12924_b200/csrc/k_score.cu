@@ -121,6 +121,7 @@ struct XFPair {
 template <typename VT>
 struct XFWide {  // one XFPair<VT> per position
   using E = XFPair<VT>;
+  static constexpr bool kShared = false;
   __device__ static void store(E* a, int i, VT x, VT f) { a[i] = E{x, f}; }
   __device__ static void pad(E* a, int i) { a[i] = E{0, 0}; }
   __device__ static void free_at(E* a, int i, VT sz) {  // freed after position i
@@ -141,6 +142,7 @@ struct XFWide {  // one XFPair<VT> per position
 // because the static bounds hold for every order.
 struct XFTiny8 {
   using E = uint16_t;
+  static constexpr bool kShared = false;
   __device__ static void store(E* a, int i, uint32_t x, uint32_t f) {
     a[i] = (E)(((x + 128u) & 0xffu) | (f << 8));
   }
@@ -153,6 +155,28 @@ struct XFTiny8 {
     const uint32_t e = a[i];
     x = (e & 0xffu) - 128u;
     f = e >> 8;
+  }
+};
+
+// Smaller still (`tiny4`: x in [-8, 7], f <= 15 for any order, e.g. C5): one byte
+// per position, which fits the whole order-space array of the large-graph scorer
+// in SHARED memory (133 KB at C5), leaving only the position words in global
+// scratch. A free adds 15*sz to the byte through a 32-bit smem atomic.
+struct XFTiny4 {
+  using E = uint8_t;
+  static constexpr bool kShared = true;
+  __device__ static void store(E* a, int i, uint32_t x, uint32_t f) {
+    a[i] = (E)(((x + 8u) & 0xfu) | (f << 4));
+  }
+  __device__ static void pad(E* a, int i) { a[i] = 8; }
+  __device__ static void free_at(E* a, int i, uint32_t sz) {
+    const uintptr_t at = reinterpret_cast<uintptr_t>(a + i);
+    atomicAdd(reinterpret_cast<unsigned int*>(at & ~uintptr_t(3)), (sz * 15u) << ((at & 3) * 8));
+  }
+  __device__ static void load(const E* a, int i, uint32_t& x, uint32_t& f) {
+    const uint32_t e = a[i];
+    x = (e & 0xfu) - 8u;
+    f = e >> 4;
   }
 };
 
@@ -206,7 +230,7 @@ struct Layout {
       b += ((size_t)ndyn * sizeof(VT) + 15) & ~size_t(15);
     }
     b += ((size_t)n * sizeof(PW) + 15) & ~size_t(15);
-    b += ((size_t)T * P * sizeof(typename XS::E) + 15) & ~size_t(15);
+    if (!XS::kShared) b += ((size_t)T * P * sizeof(typename XS::E) + 15) & ~size_t(15);
     return b + 16;
   }
 };
@@ -267,7 +291,7 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
   }
   PW* pos = reinterpret_cast<PW*>(p);
   p += ((size_t)n * sizeof(PW) + 15) & ~size_t(15);
-  typename XS::E* XF = reinterpret_cast<typename XS::E*>(p);
+  typename XS::E* XF = reinterpret_cast<typename XS::E*>(XS::kShared ? smem : p);
   for (int i = tid; i < n; i += T) pos[i] = 0;  // stamp 0 is never used
   for (int i = n + tid; i < T * P; i += T) XS::pad(XF, i);  // scan padding
 
@@ -645,6 +669,10 @@ mp_status run(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d
     // grid of one CTA per SM keeps more of them L2-resident (MP_SCORE_GRID
     // overrides, for tuning)
     grid = (int64_t)g->ctx->num_sms;
+    if (XS::kShared) {  // the order-space scan inputs live in shared memory
+      smem = ((size_t)T * g->score_p * sizeof(typename XS::E) + 15) & ~size_t(15);
+      MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    }
     if (const char* e = std::getenv("MP_SCORE_GRID")) {
       const long v = std::atol(e);
       if (v > 0) grid = v;
@@ -775,9 +803,15 @@ mp_status dispatch(const mp_graph* g, const int32_t* o, int64_t C, uint64_t* pk,
       if (g->smem_resident)
         return run<VT, uint32_t, 0, true>(g, o, C, pk, stp, vl, by, key, base, st);
       if (g->n < (1 << 24) && !std::getenv("MP_SCORE_POS64")) {
-        if constexpr (sizeof(VT) == 4)
-          if (g->tiny8 && !std::getenv("MP_SCORE_WIDE_XF"))
+        if constexpr (sizeof(VT) == 4) {
+          const bool wide = std::getenv("MP_SCORE_WIDE_XF") != nullptr;
+          const bool no4 = std::getenv("MP_SCORE_NO_TINY4") != nullptr;
+          if (g->tiny4 && !wide && !no4 &&
+              (size_t)g->score_threads * g->score_p + 64 <= g->ctx->max_smem_optin)
+            return run<VT, int32_t, 0, false, XFTiny4>(g, o, C, pk, stp, vl, by, key, base, st);
+          if (g->tiny8 && !wide)
             return run<VT, int32_t, 0, false, XFTiny8>(g, o, C, pk, stp, vl, by, key, base, st);
+        }
         return run<VT, int32_t, 0, false>(g, o, C, pk, stp, vl, by, key, base, st);
       }
       return run<VT, unsigned long long, 0, false>(g, o, C, pk, stp, vl, by, key, base, st);

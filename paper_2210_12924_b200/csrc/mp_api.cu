@@ -239,6 +239,7 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
   g->scale = P.scale;
   g->narrow = P.narrow;
   g->tiny8 = P.tiny8;
+  g->tiny4 = P.tiny4;
   g->exact_reach = P.exact_reach;
 
   DeviceGuard guard(ctx->device);

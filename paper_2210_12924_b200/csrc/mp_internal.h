@@ -79,6 +79,7 @@ struct mp_graph {
   uint64_t scale = 1;
   bool narrow = true;
   bool tiny8 = false;                // per-position (x, f) fit a byte each (mp_prep.h)
+  bool tiny4 = false;                // ... fit 4 bits each
   bool exact_reach = false;
   uint64_t* d_node_x = nullptr;      // [n] alloc - static free (scaled, modular)
   uint64_t* d_node_f = nullptr;      // [n] static free (scaled)

@@ -180,8 +180,13 @@ void prepare_scoring(int32_t n, int32_t E, const int32_t* src, const int64_t* si
         xmin[P->dyn_sinks[k]] -= (int64_t)P->dyn_size[d];
         fmax[P->dyn_sinks[k]] += (int64_t)P->dyn_size[d];
       }
-    for (int32_t v = 0; v < n && ok; ++v) ok = xmin[v] >= -128 && fmax[v] <= 255;
+    bool ok4 = ok;
+    for (int32_t v = 0; v < n && ok; ++v) {
+      ok = xmin[v] >= -128 && fmax[v] <= 255;
+      ok4 = ok4 && xmin[v] >= -8 && xmin[v] + (fmax[v] - (int64_t)sfree[v]) <= 7 && fmax[v] <= 15;
+    }
     P->tiny8 = ok;
+    P->tiny4 = ok && ok4;
   }
   // second producer per node; the rest (3rd+) as a flat packed list
   P->pred2.assign(n, -1);

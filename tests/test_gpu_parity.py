@@ -256,7 +256,7 @@ def test_scorer_variants_small_graphs(planner, monkeypatch, mode, kind, layers, 
 
 @pytest.mark.parametrize("layers,smem,mode", [(3000, 1, ""), (20000, 0, ""), (20000, 0, "tile"),
                                               (20000, 0, "scratch64"), (3000, 1, "tile"),
-                                              (20000, 0, "widexf")])
+                                              (20000, 0, "widexf"), (20000, 0, "tiny8")])
 def test_large_graph_variants(planner, monkeypatch, layers, smem, mode):
     """Graphs past the register-resident variant: node tables read per candidate,
     buffers in shared memory (n=12k); at n=80k >= 65536 the node-space kernel with
@@ -264,8 +264,10 @@ def test_large_graph_variants(planner, monkeypatch, layers, smem, mode):
     words, or the tile scorer; the tile scorer forced on the 12k graph too."""
     if mode == "scratch64":
         monkeypatch.setenv("MP_SCORE_POS64", "1")
-    if mode == "widexf":   # training_like fits the byte-packed scan inputs; force the wide ones
+    if mode == "widexf":   # training_like fits the packed scan inputs; force the wide ones
         monkeypatch.setenv("MP_SCORE_WIDE_XF", "1")
+    if mode == "tiny8":    # ... or the byte-packed ones in global scratch (not the 4-bit smem ones)
+        monkeypatch.setenv("MP_SCORE_NO_TINY4", "1")
     if mode == "tile":
         monkeypatch.setenv("MP_SCORE_MODE", "tile")
     g = mp.generate_graph("training_like", layers, 8)
