@@ -32,19 +32,21 @@ namespace {
 constexpr int kArenaWarps = 1;  // candidates per CTA (shared memory bound)
 constexpr uint8_t kOverflow = 2;  // valid[] marker: replay again with the full block list
 
+// IT: the index type of pos / fstart / flist / block edges - 16-bit when n and E
+// are below 65535 (half the state, twice the candidates per SM), else 32-bit.
 struct ArenaLayout {
-  int n, E, cap;
+  int n, E, cap, ib;  // ib = sizeof(IT)
   __host__ __device__ size_t fstart_off() const { return 0; }
   __host__ __device__ size_t flist_off() const {
-    return align(fstart_off() + 4 * ((size_t)n + 3));
+    return align(fstart_off() + ib * ((size_t)n + 3));
   }
   // pos [n] and the block list (size [cap], edge [cap]) share this region
-  __host__ __device__ size_t pos_off() const { return align(flist_off() + 4 * (size_t)E); }
+  __host__ __device__ size_t pos_off() const { return align(flist_off() + ib * (size_t)E); }
   __host__ __device__ size_t bsize_off() const { return pos_off(); }
   __host__ __device__ size_t bedge_off() const { return align(bsize_off() + 8 * (size_t)cap); }
   __host__ __device__ size_t bytes() const {
-    const size_t blocks = align(bedge_off() + 4 * (size_t)cap);
-    const size_t p = align(pos_off() + 4 * (size_t)n);
+    const size_t blocks = align(bedge_off() + ib * (size_t)cap);
+    const size_t p = align(pos_off() + ib * (size_t)n);
     return blocks > p ? blocks : p;
   }
   __host__ __device__ static size_t align(size_t x) { return (x + 15) & ~size_t(15); }
@@ -56,19 +58,36 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// pos[v] = k + 1 unless already set (returns the previous value: nonzero = a repeat)
+__device__ __forceinline__ int set_pos(int* p, int v, int val) { return atomicExch(p + v, val); }
+__device__ __forceinline__ int set_pos(uint16_t* p, int v, int val) {
+  const uintptr_t at = reinterpret_cast<uintptr_t>(p + v);
+  const int sh = (int)(at & 2) * 8;
+  const unsigned old =
+      atomicOr(reinterpret_cast<unsigned*>(at & ~uintptr_t(3)), (unsigned)val << sh);
+  return (int)((old >> sh) & 0xffffu);
+}
+__device__ __forceinline__ void count1(int* p, int t) { atomicAdd(p + t, 1); }
+__device__ __forceinline__ void count1(uint16_t* p, int t) {
+  const uintptr_t at = reinterpret_cast<uintptr_t>(p + t);
+  atomicAdd(reinterpret_cast<unsigned*>(at & ~uintptr_t(3)), 1u << ((at & 2) * 8));
+}
+
+template <typename IT>
 __global__ void __launch_bounds__(32 * kArenaWarps)
     arena_kernel(ArenaArgs a) {
   extern __shared__ __align__(16) char smem[];
   const int n = a.n, E = a.E;
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
-  const ArenaLayout Lo{n, E, a.cap};
+  const ArenaLayout Lo{n, E, a.cap, (int)sizeof(IT)};
+  constexpr IT kFree = (IT)-1;  // block edge of a free block
   char* base = smem + (size_t)wid * Lo.bytes();
-  int* pos = reinterpret_cast<int*>(base + Lo.pos_off());
-  int* fstart = reinterpret_cast<int*>(base + Lo.fstart_off());
-  int* flist = reinterpret_cast<int*>(base + Lo.flist_off());
+  IT* pos = reinterpret_cast<IT*>(base + Lo.pos_off());
+  IT* fstart = reinterpret_cast<IT*>(base + Lo.fstart_off());
+  IT* flist = reinterpret_cast<IT*>(base + Lo.flist_off());
   unsigned long long* bsz = reinterpret_cast<unsigned long long*>(base + Lo.bsize_off());
-  int* bed = reinterpret_cast<int*>(base + Lo.bedge_off());
+  IT* bed = reinterpret_cast<IT*>(base + Lo.bedge_off());
 
   for (int64_t c = (int64_t)blockIdx.x * kArenaWarps + wid; c < a.num_orders;
        c += (int64_t)gridDim.x * kArenaWarps) {
@@ -81,7 +100,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
     for (int k = lane; k < n; k += 32) {
       const int v = order[k];
       if ((unsigned)v >= (unsigned)n) bad = true;
-      else bad |= atomicExch(&pos[v], k + 1) != 0;
+      else bad |= set_pos(pos, v, k + 1) != 0;
     }
     __syncwarp();
     // ---- lifetimes hi[e] (schedule.cpp:33-50) and validity (graph.cpp:239-254);
@@ -98,7 +117,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
         hi = ps > hi ? ps : hi;
       }
       if (s1 == s0) hi = n;
-      if (!bad && a.edge_size[e] > 0) atomicAdd(&fstart[hi + 2], 1);
+      if (!bad && a.edge_size[e] > 0) count1(fstart, hi + 2);
     }
     bad = __any_sync(0xffffffffu, bad);
     if (bad) {
@@ -163,16 +182,17 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
         const int e = flist[q];
         int b = -1;
         for (int i0 = 0; i0 < nb && b < 0; i0 += 32) {
-          const unsigned m = __ballot_sync(0xffffffffu, i0 + lane < nb && bed[i0 + lane] == e);
+          const unsigned m =
+              __ballot_sync(0xffffffffu, i0 + lane < nb && (int)bed[i0 + lane] == e);
           if (m) b = i0 + __ffs(m) - 1;
         }
         live -= a.edge_size[e];
         if (b < 0) continue;
         __syncwarp();
-        if (lane == 0) bed[b] = -1;
+        if (lane == 0) bed[b] = kFree;
         // coalesce (placement.cpp:130-139): the next block, then the previous one
         int erase = -1;
-        if (b + 1 < nb && bed[b + 1] == -1) {
+        if (b + 1 < nb && bed[b + 1] == kFree) {
           if (lane == 0) bsz[b] += bsz[b + 1];
           erase = b + 1;
         }
@@ -181,7 +201,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
           for (int i0 = erase + 1; i0 < nb; i0 += 32) {
             const int i = i0 + lane;
             unsigned long long sz = 0;
-            int ed = 0;
+            IT ed = 0;
             if (i < nb) {
               sz = bsz[i];
               ed = bed[i];
@@ -195,13 +215,13 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
           }
           --nb;
         }
-        if (b > 0 && bed[b - 1] == -1) {
+        if (b > 0 && bed[b - 1] == kFree) {
           if (lane == 0) bsz[b - 1] += bsz[b];
           __syncwarp();
           for (int i0 = b + 1; i0 < nb; i0 += 32) {
             const int i = i0 + lane;
             unsigned long long sz = 0;
-            int ed = 0;
+            IT ed = 0;
             if (i < nb) {
               sz = bsz[i];
               ed = bed[i];
@@ -229,7 +249,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
           for (int i0 = 0; i0 < nb && pick < 0; i0 += 32) {
             const int i = i0 + lane;
             const unsigned m =
-                __ballot_sync(0xffffffffu, i < nb && bed[i] == -1 && bsz[i] >= s);
+                __ballot_sync(0xffffffffu, i < nb && bed[i] == kFree && bsz[i] >= s);
             if (m) pick = i0 + __ffs(m) - 1;
           }
         } else {
@@ -237,7 +257,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
           int bi = INT_MAX;
           for (int i0 = 0; i0 < nb; i0 += 32) {
             const int i = i0 + lane;
-            if (i < nb && bed[i] == -1 && bsz[i] >= s && bsz[i] < best) {
+            if (i < nb && bed[i] == kFree && bsz[i] >= s && bsz[i] < best) {
               best = bsz[i];
               bi = i;
             }
@@ -255,7 +275,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
         }
         __syncwarp();
         if (pick < 0) {  // grow (placement.cpp:117-128)
-          if (nb > 0 && bed[nb - 1] == -1) {
+          if (nb > 0 && bed[nb - 1] == kFree) {
             const unsigned long long old = bsz[nb - 1];
             __syncwarp();
             if (lane == 0) {
@@ -287,7 +307,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
                  i0 -= 32) {
               const int i = i0 + lane;
               unsigned long long sz = 0;
-              int ed = 0;
+              IT ed = 0;
               if (i < nb) {
                 sz = bsz[i];
                 ed = bed[i];
@@ -301,7 +321,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
             }
             if (lane == 0) {
               bsz[pick + 1] = bsize - s;
-              bed[pick + 1] = -1;
+              bed[pick + 1] = kFree;
             }
             ++nb;
           }
@@ -330,23 +350,32 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
 
 }  // namespace
 
+static bool arena_narrow(int n, int E) { return n < 65535 && 2 * E + 2 < 65535; }
+
 size_t arena_smem_bytes(int n, int E, int cap) {
-  return ArenaLayout{n, E, cap}.bytes() * kArenaWarps;
+  const bool narrow = arena_narrow(n, E) && !std::getenv("MP_ARENA_WIDE");
+  return ArenaLayout{n, E, cap, narrow ? 2 : 4}.bytes() * kArenaWarps;
 }
 
-mp_status launch_arena_pass(const ArenaArgs& in, const mp_ctx* ctx, cudaStream_t st) {
+template <typename IT>
+mp_status launch_arena_t(const ArenaArgs& in, const mp_ctx* ctx, cudaStream_t st) {
   const size_t smem = arena_smem_bytes(in.n, in.E, in.cap);
-  MP_CUDA(cudaFuncSetAttribute(arena_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem));
+  auto kern = arena_kernel<IT>;
+  MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arena_kernel, 32 * kArenaWarps,
-                                                        smem));
+  MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kArenaWarps, smem));
   int64_t grid = (int64_t)ctx->num_sms * (per_sm > 0 ? per_sm : 1);
   const int64_t need = (in.num_orders + kArenaWarps - 1) / kArenaWarps;
   if (grid > need) grid = need;
-  arena_kernel<<<(unsigned)grid, 32 * kArenaWarps, smem, st>>>(in);
+  kern<<<(unsigned)grid, 32 * kArenaWarps, smem, st>>>(in);
   MP_CUDA(cudaGetLastError());
   return MP_OK;
+}
+
+mp_status launch_arena_pass(const ArenaArgs& in, const mp_ctx* ctx, cudaStream_t st) {
+  if (arena_narrow(in.n, in.E) && !std::getenv("MP_ARENA_WIDE"))
+    return launch_arena_t<uint16_t>(in, ctx, st);
+  return launch_arena_t<int>(in, ctx, st);
 }
 
 mp_status launch_arena(const ArenaArgs& in, const mp_ctx* ctx, cudaStream_t st) {

@@ -47,14 +47,17 @@ def test_golden_run_baseline(golden, planner):
         planner.run_baseline(g, [2, 1, 0])
 
 
-@pytest.mark.parametrize("name,cap", [("resnet50_b32", ""), ("bert_base_s512", ""),
-                                      ("gpt2_medium_s1024", ""), ("resnet50_b32", "6")])
-def test_batched_run_baseline_model_graphs(planner, monkeypatch, name, cap):
+@pytest.mark.parametrize("name,cap,wide", [("resnet50_b32", "", 0), ("bert_base_s512", "", 0),
+                                           ("gpt2_medium_s1024", "", 0), ("resnet50_b32", "6", 0),
+                                           ("bert_base_s512", "", 1)])
+def test_batched_run_baseline_model_graphs(planner, monkeypatch, name, cap, wide):
     """Every candidate vs the C restatement (and the reference on a few); with
     MP_ARENA_CAP=6 every block list overflows the first pass and is replayed by
-    the full-capacity second pass."""
+    the full-capacity second pass; MP_ARENA_WIDE forces 32-bit indexes."""
     if cap:
         monkeypatch.setenv("MP_ARENA_CAP", cap)
+    if wide:
+        monkeypatch.setenv("MP_ARENA_WIDE", "1")
     with gzip.open(os.path.join(ROOT, "workloads", "graphs", name + ".json.gz"), "rt") as f:
         g = mp.load_graph(f.read())
     orders = np.concatenate([g.program_order()[None], mp.random_topo_orders(g, 40, seed=8)])
