@@ -360,6 +360,35 @@ def test_large_fork_join_wide_values(planner):
         assert (int(res.peak[i]), int(res.peak_step[i])) == (int(rs.max()), int(np.argmax(rs)) + 1)
 
 
+@pytest.mark.parametrize("size", [8, 1 << 20])
+def test_large_graph_wide_dynamic_edges(planner, size, monkeypatch):
+    """>65,536 nodes whose order-dependent frees have 6 mutually unordered candidate
+    sinks (past the 4-sink table: the flat loop), with 4-bit (sizes 8 and 3, gcd 1)
+    and wide (2^20 and 3) scan inputs, valid and invalid rows, vs the oracle."""
+    groups = 10000
+    nodes, edges = [("s0", "source")], []
+    prev = "s0"
+    for g in range(groups):
+        branch = [f"b{g}_{k}" for k in range(6)]
+        nodes += [(b, "compute") for b in branch] + [(f"j{g}", "compute")]
+        edges.append((f"x{g}", prev, branch, size))                    # 6 candidate last sinks
+        edges += [(f"y{g}_{k}", branch[k], [f"j{g}"], 3) for k in range(6)]
+        prev = f"j{g}"
+    g = mp.graph_from_lists(nodes, edges)
+    assert g.n > 65536
+    orc = O.Oracle.from_csr(g.csr())
+    orders = mp.random_topo_orders(g, 4, seed=9)
+    orders[3, [5, 6]] = orders[3, [6, 5]]
+    res = planner.score_orders(g, orders)
+    for i, o in enumerate(orders):
+        if not orc.is_topological_order(o):
+            assert res.valid[i] == 0
+            continue
+        rs = orc.resident_bytes_per_step(o)
+        assert res.valid[i] == 1
+        assert (int(res.peak[i]), int(res.peak_step[i])) == (int(rs.max()), int(np.argmax(rs)) + 1)
+
+
 def test_c5_full_size(golden, planner):
     """The 100k-tensor graph at full size: KAT peak + size-independent properties."""
     g = mp.generate_graph("training_like", 33333, 8)
