@@ -66,16 +66,6 @@ struct ScoreTables {
   const int2* __restrict__ node_u2;          // (pred1, pred2)
   const uint32_t* __restrict__ extra3_packed;
   int32_t nextra3;
-  const int32_t* __restrict__ extra3_u;      // 3rd+ producer pairs, any n
-  const int32_t* __restrict__ extra3_w;
-  int32_t nextra3w;
-  const int32_t* __restrict__ node_dyn_off;  // per node: dynamic edges it may free last
-  const int32_t* __restrict__ node_dyn;
-  const uint2* __restrict__ tile_zw;         // tile scorer: (pred1 | #memberships << 24, pred2)
-  const uint4* __restrict__ tile_rec32;      // (x, f, z, w), 32-bit graphs
-  const int32_t* __restrict__ tile_moff;
-  const int4* __restrict__ tile_mother;
-  const int32_t* __restrict__ tile_medge;
   const int4* __restrict__ dyn_sink4;        // [ndyn] candidate sinks, -1 padded (<= 4 each)
 };
 
@@ -587,7 +577,6 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
 
 #include "k_score_reg.cuh"
 #include "k_score_warp.cuh"
-#include "k_score_tile.cuh"
 
 ScoreTables tables(const mp_graph* g) {
   ScoreTables G;
@@ -609,16 +598,6 @@ ScoreTables tables(const mp_graph* g) {
   G.node_u2 = reinterpret_cast<const int2*>(g->d_node_u2);
   G.extra3_packed = g->d_extra3_packed;
   G.nextra3 = g->n_extra3;
-  G.extra3_u = g->d_extra3_u;
-  G.extra3_w = g->d_extra3_w;
-  G.nextra3w = g->n_extra3w;
-  G.node_dyn_off = g->d_node_dyn_off;
-  G.node_dyn = g->d_node_dyn;
-  G.tile_zw = reinterpret_cast<const uint2*>(g->d_tile_zw);
-  G.tile_rec32 = reinterpret_cast<const uint4*>(g->d_tile_rec32);
-  G.tile_moff = g->d_tile_moff;
-  G.tile_mother = reinterpret_cast<const int4*>(g->d_tile_mother);
-  G.tile_medge = g->d_tile_medge;
   G.dyn_sink4 = reinterpret_cast<const int4*>(g->d_dyn_sink4);
   return G;
 }
@@ -744,51 +723,10 @@ mp_status run_warp(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64
   return MP_OK;
 }
 
-template <typename VT, int PT>
-mp_status run_tile(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d_peak,
-                   int32_t* d_step, uint8_t* d_valid, uint64_t* d_bytes, uint64_t* d_key,
-                   int64_t index_base, cudaStream_t st) {
-  mp_graph* mg = const_cast<mp_graph*>(g);
-  if (mg->d_tile_pos == nullptr) {  // per-CTA stamped words, zeroed once per graph
-    const int grid = g->ctx->num_sms;
-    const size_t words = (size_t)grid * g->n + grid;
-    MP_CUDA(cudaMalloc(reinterpret_cast<void**>(&mg->d_tile_pos), words * 4));
-    MP_CUDA(cudaMemsetAsync(mg->d_tile_pos, 0, words * 4, st));
-    mg->tile_grid = grid;
-  }
-  int64_t grid = g->tile_grid;
-  if (const char* e = std::getenv("MP_SCORE_GRID")) {  // tuning / stamp-wrap tests
-    const long v = std::atol(e);
-    if (v > 0 && v < grid) grid = v;
-  }
-  if (grid > C) grid = C;
-  // a smaller grid leaves the other slices' stamps untouched: still consistent
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kTileT);
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  int nat = 0;
-  if (!std::getenv("MP_NO_L2_WINDOW"))
-    nat = l2_persist_window(g->ctx, g->d_tile_pos,
-                            ((size_t)g->tile_grid * g->n + g->tile_grid) * 4, &at[0]) ? 1 : 0;
-  cfg.attrs = at;
-  cfg.numAttrs = nat;
-  MP_CUDA(cudaLaunchKernelEx(&cfg, score_tile_kernel<VT, PT>, tables(g), d_orders, C, d_peak,
-                             d_step, d_valid, d_bytes,
-                             reinterpret_cast<unsigned long long*>(d_key), index_base,
-                             g->d_tile_pos, g->tile_grid));
-  return MP_OK;
-}
-
 template <typename VT>
 mp_status dispatch(const mp_graph* g, const int32_t* o, int64_t C, uint64_t* pk, int32_t* stp,
                    uint8_t* vl, uint64_t* by, uint64_t* key, int64_t base, cudaStream_t st) {
   if (g->score_warps > 0) return run_warp<VT>(g, o, C, pk, stp, vl, by, key, base, st);
-  // MP_SCORE_MODE=tile forces the tile scorer at any size (tests, tuning)
-  if (const char* m = std::getenv("MP_SCORE_MODE"))
-    if (std::string(m) == "tile" && g->n < (1 << 24))
-      return run_tile<VT, sizeof(VT) == 4 ? 8 : 4>(g, o, C, pk, stp, vl, by, key, base, st);
   switch (g->score_j) {
     case 4:
       if (g->score_kc == 2) return run_reg<VT, 4, 2>(g, o, C, pk, stp, vl, by, key, base, st);

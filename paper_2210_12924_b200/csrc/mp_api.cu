@@ -264,11 +264,6 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
   up(upload(&g->d_node_u2, P.node_u2.data(), P.node_u2.size(), st));
   up(upload(&g->d_extra3_packed, P.extra3_packed.data(), P.extra3_packed.size(), st));
   g->n_extra3 = (int32_t)P.extra3_packed.size();
-  up(upload(&g->d_extra3_u, P.extra3_u.data(), P.extra3_u.size(), st));
-  up(upload(&g->d_extra3_w, P.extra3_w.data(), P.extra3_w.size(), st));
-  g->n_extra3w = (int32_t)P.extra3_u.size();
-  up(upload(&g->d_node_dyn_off, P.node_dyn_off.data(), P.node_dyn_off.size(), st));
-  up(upload(&g->d_node_dyn, P.node_dyn.data(), P.node_dyn.size(), st));
   if (g->dyn_max_sinks <= 4 && g->n_dyn > 0) {
     std::vector<int32_t> s4(4 * (size_t)g->n_dyn, -1);
     for (int32_t d = 0; d < g->n_dyn; ++d)
@@ -278,11 +273,6 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
   }
   up(upload(&g->d_out_off, P.out_off.data(), P.out_off.size(), st));
   up(upload(&g->d_out_edges, P.out_edges.data(), P.out_edges.size(), st));
-  up(upload(&g->d_tile_zw, P.tile_zw.data(), P.tile_zw.size(), st));
-  up(upload(&g->d_tile_rec32, P.tile_rec32.data(), P.tile_rec32.size(), st));
-  up(upload(&g->d_tile_moff, P.tile_moff.data(), P.tile_moff.size(), st));
-  up(upload(&g->d_tile_mother, P.tile_mother.data(), P.tile_mother.size(), st));
-  up(upload(&g->d_tile_medge, P.tile_medge.data(), P.tile_medge.size(), st));
   if (s == MP_OK) up(score_configure(g));
   if (s == MP_OK) {
     cudaError_t ce = cudaStreamSynchronize(st);  // host tables may go out of scope
@@ -302,9 +292,9 @@ mp_status mp_graph_free(mp_graph* g) {
   void* ptrs[] = {g->d_edge_src, g->d_sink_off,  g->d_sinks,     g->d_edge_size,
                   g->d_node_x,   g->d_node_f,    g->d_pred1,     g->d_extra_u,
                   g->d_extra_w,  g->d_dyn_off,   g->d_dyn_sinks, g->d_dyn_size,
-                  g->d_node_rec32, g->d_node_u2, g->d_extra3_packed, g->d_extra3_u,
-                  g->d_extra3_w, g->d_node_dyn_off, g->d_node_dyn, g->d_tile_pos,
-                  g->d_out_off, g->d_out_edges, g->d_dyn_sink4, g->d_joint_mul, g->d_joint_ar, g->d_joint_art, g->d_tile_zw, g->d_tile_rec32, g->d_tile_moff, g->d_tile_mother, g->d_tile_medge};
+                  g->d_node_rec32, g->d_node_u2, g->d_extra3_packed,
+                  g->d_out_off,  g->d_out_edges, g->d_dyn_sink4, g->d_joint_mul,
+                  g->d_joint_ar, g->d_joint_art};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete g;

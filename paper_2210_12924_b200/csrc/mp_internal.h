@@ -94,26 +94,13 @@ struct mp_graph {
   int32_t* d_node_u2 = nullptr;        // [2n] (pred1, pred2)
   uint32_t* d_extra3_packed = nullptr; // [n_extra3] 3rd+ producer pairs, u | w << 16
   int32_t n_extra3 = 0;
-  int32_t* d_extra3_u = nullptr;       // [n_extra3w] 3rd+ producer pairs (any n)
-  int32_t* d_extra3_w = nullptr;
-  int32_t n_extra3w = 0;
-  int32_t* d_node_dyn_off = nullptr;   // [n+1]
-  int32_t* d_node_dyn = nullptr;       // [n_dyn_sinks]
   int32_t* d_out_off = nullptr;        // [n+1] fanout(v), edge order
   int32_t* d_out_edges = nullptr;      // [E]
-  uint32_t* d_tile_zw = nullptr;       // [2n] tile scorer producer words (mp_prep.h)
-  uint32_t* d_tile_rec32 = nullptr;    // [4n] (x, f, z, w), 32-bit graphs
-  int32_t* d_tile_moff = nullptr;      // [n]
-  int32_t* d_tile_mother = nullptr;    // [4m]
-  int32_t* d_tile_medge = nullptr;     // [m]
   // joint-mode pair tables (built on first use, k_joint.cu)
   int2* d_joint_mul = nullptr;
   uint32_t* d_joint_ar = nullptr;
   uint32_t* d_joint_art = nullptr;
   int joint_ar_words = 0, joint_art_words = 0;
-  // tile scorer: per-CTA position words (stamped) that persist across launches
-  uint32_t* d_tile_pos = nullptr;      // [tile_grid * n] + [tile_grid] stamps
-  int32_t tile_grid = 0;
   int score_j = 0;                   // nodes per thread held in registers (0 = loop variant)
   int score_threads = 1024;
   int score_kc = 1;                  // candidates per CTA iteration (register variant)

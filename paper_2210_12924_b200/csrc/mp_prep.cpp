@@ -196,25 +196,10 @@ void prepare_scoring(int32_t n, int32_t E, const int32_t* src, const int64_t* si
       const int32_t u = P->extra_u[i], w = P->extra_w[i];
       if (seen[w]++ == 0) {
         P->pred2[w] = u;
-      } else {
-        if (n < 65536) P->extra3_packed.push_back((uint32_t)u | ((uint32_t)w << 16));
-        P->extra3_u.push_back(u);
-        P->extra3_w.push_back(w);
+      } else if (n < 65536) {
+        P->extra3_packed.push_back((uint32_t)u | ((uint32_t)w << 16));
       }
     }
-  }
-  // per node: the dynamic edges it is a candidate last consumer of (CSR)
-  {
-    std::vector<int32_t> cnt(n + 1, 0);
-    const int32_t nd = (int32_t)P->dyn_size.size();
-    for (int32_t d = 0; d < nd; ++d)
-      for (int32_t k = P->dyn_off[d]; k < P->dyn_off[d + 1]; ++k) ++cnt[P->dyn_sinks[k] + 1];
-    for (int32_t v = 0; v < n; ++v) cnt[v + 1] += cnt[v];
-    P->node_dyn_off.assign(cnt.begin(), cnt.end());
-    P->node_dyn.assign(P->dyn_sinks.size(), 0);
-    for (int32_t d = 0; d < nd; ++d)
-      for (int32_t k = P->dyn_off[d]; k < P->dyn_off[d + 1]; ++k)
-        P->node_dyn[cnt[P->dyn_sinks[k]]++] = d;
   }
   // fanout lists in edge order (Graph::fanout, graph.cpp:100)
   {
@@ -224,41 +209,6 @@ void prepare_scoring(int32_t n, int32_t E, const int32_t* src, const int64_t* si
     std::vector<int32_t> cur(P->out_off.begin(), P->out_off.end() - 1);
     P->out_edges.assign(E, 0);
     for (int32_t e = 0; e < E; ++e) P->out_edges[cur[src[e]]++] = e;
-  }
-  // tile scorer words and memberships (only meaningful for n < 2^24)
-  if (n < (1 << 24)) {
-    P->tile_zw.assign(2 * (size_t)n, 0);
-    P->tile_moff.assign(n, 0);
-    for (int32_t v = 0; v < n; ++v) {
-      const int32_t a = P->node_dyn_off[v], b = P->node_dyn_off[v + 1];
-      const uint32_t cnt = (uint32_t)std::min(b - a, 255);
-      P->tile_zw[2 * v] = (P->pred1[v] < 0 ? kNoNode : (uint32_t)P->pred1[v]) | (cnt << 24);
-      P->tile_zw[2 * v + 1] = P->pred2[v] < 0 ? kNoNode : (uint32_t)P->pred2[v];
-      P->tile_moff[v] = a;
-      for (int32_t q = a; q < b; ++q) {
-        const int32_t d = P->node_dyn[q];
-        int32_t o[4] = {(int32_t)kNoNode, (int32_t)kNoNode, (int32_t)kNoNode, (int32_t)kNoNode};
-        int k = 0;
-        for (int32_t s2 = P->dyn_off[d]; s2 < P->dyn_off[d + 1]; ++s2) {
-          const int32_t x = P->dyn_sinks[s2];
-          if (x == v) continue;
-          if (k < 4) o[k] = x;
-          ++k;
-        }
-        if (k > 4) o[3] = kMoreSinks;
-        P->tile_mother.insert(P->tile_mother.end(), o, o + 4);
-        P->tile_medge.push_back(d);
-      }
-    }
-    if (P->narrow) {
-      P->tile_rec32.resize(4 * (size_t)n);
-      for (int32_t v = 0; v < n; ++v) {
-        P->tile_rec32[4 * v] = (uint32_t)P->node_x[v];
-        P->tile_rec32[4 * v + 1] = (uint32_t)P->node_f[v];
-        P->tile_rec32[4 * v + 2] = P->tile_zw[2 * v];
-        P->tile_rec32[4 * v + 3] = P->tile_zw[2 * v + 1];
-      }
-    }
   }
   P->node_rec32.assign(4 * (size_t)n, 0);
   P->node_u2.assign(2 * (size_t)n, -1);

@@ -254,22 +254,19 @@ def test_scorer_variants_small_graphs(planner, monkeypatch, mode, kind, layers, 
             orc.resident_bytes_per_step(orders[0])).all()
 
 
-@pytest.mark.parametrize("layers,smem,mode", [(3000, 1, ""), (20000, 0, ""), (20000, 0, "tile"),
-                                              (20000, 0, "scratch64"), (3000, 1, "tile"),
+@pytest.mark.parametrize("layers,smem,mode", [(3000, 1, ""), (20000, 0, ""), (20000, 0, "scratch64"),
                                               (20000, 0, "widexf"), (20000, 0, "tiny8")])
 def test_large_graph_variants(planner, monkeypatch, layers, smem, mode):
     """Graphs past the register-resident variant: node tables read per candidate,
     buffers in shared memory (n=12k); at n=80k >= 65536 the node-space kernel with
     global scratch and 32-bit (24-bit position, default) or 64-bit stamped position
-    words, or the tile scorer; the tile scorer forced on the 12k graph too."""
+    words, 4-bit shared / 8-bit / wide scan inputs."""
     if mode == "scratch64":
         monkeypatch.setenv("MP_SCORE_POS64", "1")
     if mode == "widexf":   # training_like fits the packed scan inputs; force the wide ones
         monkeypatch.setenv("MP_SCORE_WIDE_XF", "1")
     if mode == "tiny8":    # ... or the byte-packed ones in global scratch (not the 4-bit smem ones)
         monkeypatch.setenv("MP_SCORE_NO_TINY4", "1")
-    if mode == "tile":
-        monkeypatch.setenv("MP_SCORE_MODE", "tile")
     g = mp.generate_graph("training_like", layers, 8)
     dg = planner.upload(g)
     assert dg.info()["smem_resident"] == smem
@@ -287,13 +284,9 @@ def test_large_graph_variants(planner, monkeypatch, layers, smem, mode):
         assert (int(res.peak[i]), int(res.peak_step[i])) == (int(rs.max()), int(np.argmax(rs)) + 1)
 
 
-@pytest.mark.parametrize("tile", [0, 1])
-def test_global_scratch_stamp_wrap(planner, monkeypatch, tile):
-    """One CTA scoring 300 candidates of an 80k-node graph: the stamp of the
-    32-bit position words wraps (7-bit node-space scratch: twice; 8-bit tile
-    scorer: once) and every verdict and peak must hold."""
-    if tile:
-        monkeypatch.setenv("MP_SCORE_MODE", "tile")
+def test_global_scratch_stamp_wrap(planner, monkeypatch):
+    """One CTA scoring 300 candidates of an 80k-node graph: the 7-bit stamp of the
+    32-bit position words wraps twice and every verdict and peak must hold."""
     monkeypatch.setenv("MP_SCORE_GRID", "1")
     g = mp.generate_graph("training_like", 20000, 8)
     orc = O.Oracle.from_csr(g.csr())
@@ -311,53 +304,6 @@ def test_global_scratch_stamp_wrap(planner, monkeypatch, tile):
     full = planner.score_orders(g, orders)
     assert (full.peak == res.peak).all() and (full.peak_step == res.peak_step).all()
     assert (full.valid == res.valid).all()
-
-
-@pytest.mark.parametrize("name", ["resnet50_b32", "bert_base_s512", "gpt2_medium_s1024"])
-def test_tile_scorer_model_graphs(planner, monkeypatch, name):
-    """The tile scorer forced on the traced model graphs: order-dependent frees
-    (57/234/364 dynamic edges), 32- and 64-bit values, invalid rows, twice in a
-    row (stamps persist across launches), vs the oracle."""
-    monkeypatch.setenv("MP_SCORE_MODE", "tile")
-    import gzip
-    import os
-    path = os.path.join(os.path.dirname(__file__), "..", "workloads", "graphs", name + ".json.gz")
-    with gzip.open(path, "rt") as fh:
-        g = mp.load_graph(fh.read())
-    orc = O.Oracle.from_csr(g.csr())
-    orders = mp.random_topo_orders(g, 24, seed=3)
-    orders[2, [5, 6]] = orders[2, [6, 5]]
-    orders[4, 11] = orders[4, 12]
-    orders[6, -1] = -1
-    for _ in range(2):
-        res = planner.score_orders(g, orders)
-        for i, o in enumerate(orders):
-            lt = orc.lifetimes_from_order(o)
-            if lt is None:
-                assert res.valid[i] == 0, i
-                continue
-            _, pr, ps = orc.timeline_from_lifetimes(lt[0], lt[1], g.n)
-            assert res.valid[i] == 1 and (int(res.peak[i]), int(res.peak_step[i])) == (pr, ps), i
-    rs = planner.resident_bytes_per_step(g, orders[0])
-    assert (rs == orc.resident_bytes_per_step(orders[0])).all()
-
-
-def test_large_fork_join_wide_values(planner):
-    """A 100k+-node graph whose per-node values do not fit a byte (random fork-join
-    widths, 2^20-byte sizes): the global-scratch scorer with wide scan inputs."""
-    g = mp.generate_graph("fork_join", 15000, 1 << 20, 1)
-    assert g.n >= 65536
-    orc = O.Oracle.from_csr(g.csr())
-    orders = mp.random_topo_orders(g, 6, seed=4)
-    orders[2, [0, 1]] = orders[2, [1, 0]]
-    res = planner.score_orders(g, orders)
-    for i, o in enumerate(orders):
-        if not orc.is_topological_order(o):
-            assert res.valid[i] == 0
-            continue
-        rs = orc.resident_bytes_per_step(o)
-        assert res.valid[i] == 1
-        assert (int(res.peak[i]), int(res.peak_step[i])) == (int(rs.max()), int(np.argmax(rs)) + 1)
 
 
 @pytest.mark.parametrize("size", [8, 1 << 20])
