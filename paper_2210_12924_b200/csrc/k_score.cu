@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
     } else {
       // batches of kB: all loads of a batch before its stores (the compiler cannot
       // reorder loads across stores to possibly aliasing buffers)
-      constexpr int kB = 8;
+      constexpr int kB = kSmem ? 8 : 16;  // more loads in flight from HBM (scratch variant)
       const int32_t* ord = orders + c * n;
       for (int k0 = tid; k0 < n; k0 += T * kB) {
         int vv[kB];

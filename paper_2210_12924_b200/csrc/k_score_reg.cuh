@@ -110,6 +110,11 @@ __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMi
     ru[j] = u1 >= 0 ? u1 : TJ + 1;
     ru2[j] = u2 >= 0 ? u2 : TJ + 1;
   }
+  // bit j: some lane of this warp has a second producer in slot j (warp-uniform),
+  // so slots without any skip the gather (most nodes have at most one)
+  uint32_t has2 = 0;
+#pragma unroll
+  for (int j = 0; j < J; ++j) has2 |= (__any_sync(0xffffffffu, ru2[j] != TJ + 1) ? 1u : 0u) << j;
 
   // Candidate groups: group g covers candidates [g*KC, g*KC + KC).
   const int64_t ngroups = (C + KC - 1) / KC;
@@ -162,7 +167,7 @@ __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMi
       for (int j = 0; j < J; ++j) {
         w[j] = pos[k][base + kWarp * j];
         pu[j] = pos[k][ru[j]];
-        pu2[j] = pos[k][ru2[j]];
+        pu2[j] = (has2 >> j & 1u) ? pos[k][ru2[j]] : 0u;
       }
 #pragma unroll
       for (int j = 0; j < J; ++j) {
