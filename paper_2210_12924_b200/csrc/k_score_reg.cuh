@@ -186,15 +186,27 @@ __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMi
     // ---- phase 2c: order-dependent last consumers -----------------------------------
     if (G.ndyn > 0) {
       __syncthreads();
-      for (int d = tid; d < G.ndyn; d += T) {
+      // edges spread over the warps (d = i*T + lane*nwarps + warp) so no warp
+      // reaches the barrier late; <= 4 candidate sinks come as one 16-byte record
+      for (int d = lane * nwarps + warp; d < G.ndyn; d += T) {
         uint32_t h[KC];
 #pragma unroll
         for (int k = 0; k < KC; ++k) h[k] = 0;
-        const int s1 = __ldg(G.dyn_off + d + 1);
-        for (int s = __ldg(G.dyn_off + d); s < s1; ++s) {
-          const int x = __ldg(G.dyn_sinks + s);
+        if (G.dyn_sink4 != nullptr) {
+          const int4 sk = __ldg(G.dyn_sink4 + d);
 #pragma unroll
-          for (int k = 0; k < KC; ++k) h[k] = max(h[k], pos[k][x]);
+          for (int k = 0; k < KC; ++k) {
+            const uint32_t a = sk.x >= 0 ? pos[k][sk.x] : 0u, b = sk.y >= 0 ? pos[k][sk.y] : 0u;
+            const uint32_t c2 = sk.z >= 0 ? pos[k][sk.z] : 0u, d2 = sk.w >= 0 ? pos[k][sk.w] : 0u;
+            h[k] = max(max(a, b), max(c2, d2));
+          }
+        } else {
+          const int s1 = __ldg(G.dyn_off + d + 1);
+          for (int s = __ldg(G.dyn_off + d); s < s1; ++s) {
+            const int x = __ldg(G.dyn_sinks + s);
+#pragma unroll
+            for (int k = 0; k < KC; ++k) h[k] = max(h[k], pos[k][x]);
+          }
         }
         const VT sz = (VT)__ldg(G.dyn_size + d);
 #pragma unroll
