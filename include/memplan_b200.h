@@ -211,6 +211,24 @@ mp_status mp_peak_mem(mp_ctx* ctx, int32_t num_edges, const uint64_t* size,
 /* fragmentation (placement.cpp:64-67): (mr - rs) / mr, 0 when mr == 0. */
 double mp_fragmentation(uint64_t mr, uint64_t rs);
 
+/* ---- (e) one process, several GPUs --------------------------------------------
+ * A set of contexts (one per entry of devices[G]; an entry may repeat) with the
+ * graph replicated on each (the CSR is replicated, candidates
+ * sharded). mp_score_orders_multi splits orders [num_orders][n] into G
+ * contiguous shards, scores each on its device from its own host thread (the
+ * fused kernel with its argmin), and combines the per-device first minima on
+ * the host: *best is the lowest index among equal minimal peaks over all
+ * shards, exactly a serial first-minimum scan (-1 when nothing is valid).
+ * Multi-process jobs use the same kernels with one NCCL allreduce(MIN) on the
+ * packed key instead (mp_score_orders_argmin_d + paper_2210_12924_b200/dist.py). */
+typedef struct mp_multi mp_multi;
+mp_status mp_multi_create(const int* devices, int num_devices, mp_multi** out);
+mp_status mp_multi_destroy(mp_multi* m);
+mp_status mp_multi_upload(mp_multi* m, const mp_csr* csr);
+mp_status mp_score_orders_multi(mp_multi* m, const int32_t* orders, int64_t num_orders,
+                                uint64_t* peak, int32_t* peak_step, uint8_t* valid,
+                                int64_t* best);
+
 /* ---- (§8f-2) placement heuristics: the producers of the plans K4 validates ----
  * preallocate_pyramid (placement.cpp:25-62) and greedy_pack
  * (placement.cpp:182-204) over num_problems lifetime vectors that share the

@@ -14,12 +14,12 @@ include/memplan_b200.h); there is no CPU fallback.
 from . import errors
 from .graph import (EdgeKind, Graph, Node, NodeRole, TensorEdge, generate_graph,
                     graph_from_lists, load_graph, load_graph_file, save_graph)
-from .planner import (BaselineResult, DeviceGraph, ExecutionSequence, Interval, MemoryPlan, Planner,
+from .planner import (BaselineResult, DeviceGraph, MultiPlanner, ExecutionSequence, Interval, MemoryPlan, Planner,
                       PrePlacement, ResidentTimeline, ScoreResult, format_report, fragmentation,
                       intervals_disjoint, load_plan, random_topo_orders)
 
 __all__ = [
-    "BaselineResult", "errors", "EdgeKind", "Graph", "Node", "NodeRole", "TensorEdge", "generate_graph",
+    "BaselineResult", "MultiPlanner", "errors", "EdgeKind", "Graph", "Node", "NodeRole", "TensorEdge", "generate_graph",
     "graph_from_lists", "load_graph", "load_graph_file", "save_graph", "DeviceGraph",
     "ExecutionSequence", "Interval", "MemoryPlan", "Planner", "PrePlacement", "ResidentTimeline",
     "ScoreResult",

@@ -38,7 +38,8 @@ EXPORTS = [
     "mp_validate_pairs", "mp_validate_pairs_d", "mp_addresses_feasible", "mp_peak_mem",
     "mp_fragmentation", "mp_generate_graph", "mp_random_topo_orders",
     "mp_place", "mp_place_d", "mp_run_baseline", "mp_run_baseline_d", "mp_encode_addresses_lp",
-    "mp_joint_pairs",
+    "mp_joint_pairs", "mp_multi_create", "mp_multi_destroy", "mp_multi_upload",
+    "mp_score_orders_multi",
 ]
 
 
@@ -117,6 +118,10 @@ def lib():
             "mp_addresses_feasible": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, P(i32)]),
             "mp_peak_mem": (C.c_int, [vp, i32, vp, vp, vp, P(u64)]),
             "mp_fragmentation": (C.c_double, [u64, u64]),
+            "mp_multi_create": (C.c_int, [vp, C.c_int, P(vp)]),
+            "mp_multi_destroy": (C.c_int, [vp]),
+            "mp_multi_upload": (C.c_int, [vp, P(MpCsr)]),
+            "mp_score_orders_multi": (C.c_int, [vp, vp, i64, vp, vp, vp, P(i64)]),
             "mp_joint_pairs": (C.c_int, [vp, vp, C.c_int, vp, i64, P(i64)]),
             "mp_encode_addresses_lp": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, i64,
                                                  P(i64), vp]),

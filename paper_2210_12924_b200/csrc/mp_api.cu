@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <thread>
 #include <unordered_set>
 #include <cctype>
 #include <climits>
@@ -700,6 +701,76 @@ mp_status mp_validate_pairs_d(mp_ctx* ctx, int32_t E, const int32_t* d_lo, const
   a.row_begin = row_begin;
   a.row_end = row_end;
   return pair_sweep_d(ctx, a, d_row_off, d_viol, cap, num_viol, st);
+}
+
+// ---- one process, several GPUs (§8e) ------------------------------------------------
+mp_status mp_multi_create(const int* devices, int G, mp_multi** out) {
+  if (!devices || G <= 0 || !out) return invalid_arg("null argument or no devices");
+  *out = nullptr;
+  auto* m = new mp_multi();
+  for (int i = 0; i < G; ++i) {
+    mp_ctx* c = nullptr;
+    const mp_status s = mp_ctx_create(devices[i], &c);
+    if (s != MP_OK) {
+      mp_multi_destroy(m);
+      return s;
+    }
+    m->ctx.push_back(c);
+  }
+  *out = m;
+  return MP_OK;
+}
+
+mp_status mp_multi_destroy(mp_multi* m) {
+  if (!m) return MP_OK;
+  for (mp_graph* g : m->graph) mp_graph_free(g);
+  for (mp_ctx* c : m->ctx) mp_ctx_destroy(c);
+  delete m;
+  return MP_OK;
+}
+
+mp_status mp_multi_upload(mp_multi* m, const mp_csr* csr) {
+  if (!m || !csr) return invalid_arg("null argument");
+  for (mp_graph* g : m->graph) mp_graph_free(g);
+  m->graph.assign(m->ctx.size(), nullptr);
+  for (size_t i = 0; i < m->ctx.size(); ++i) MP_TRY(mp_graph_upload(m->ctx[i], csr, &m->graph[i]));
+  return MP_OK;
+}
+
+mp_status mp_score_orders_multi(mp_multi* m, const int32_t* orders, int64_t C, uint64_t* peak,
+                                int32_t* step, uint8_t* valid, int64_t* best) {
+  if (!m || C < 0 || m->graph.empty() || !m->graph[0]) return invalid_arg("no graph uploaded");
+  if (best) *best = -1;
+  if (C == 0) return MP_OK;
+  const int G = (int)m->ctx.size();
+  const int64_t n = m->graph[0]->n;
+  std::vector<mp_status> st(G, MP_OK);
+  std::vector<std::string> err(G);
+  std::vector<int64_t> lbest(G, -1), beg(G + 1);
+  for (int i = 0; i <= G; ++i) beg[i] = C * i / G;  // contiguous shards, as shard_range
+  std::vector<std::thread> pool;
+  for (int i = 0; i < G; ++i)
+    pool.emplace_back([&, i] {
+      const int64_t b = beg[i], c = beg[i + 1] - beg[i];
+      st[i] = mp_score_orders_best(m->ctx[i], m->graph[i], orders ? orders + b * n : nullptr, c,
+                                   peak + b, step + b, valid + b, &lbest[i]);
+      if (st[i] != MP_OK) err[i] = mp_last_error();
+    });
+  for (std::thread& t : pool) t.join();
+  for (int i = 0; i < G; ++i)
+    if (st[i] != MP_OK) {
+      set_error(err[i]);
+      return st[i];
+    }
+  // first minimum over the shards' first minima, in index order
+  int64_t bi = -1;
+  for (int i = 0; i < G; ++i) {
+    if (lbest[i] < 0) continue;
+    const int64_t gi = beg[i] + lbest[i];
+    if (bi < 0 || peak[gi] < peak[bi]) bi = gi;
+  }
+  if (best) *best = bi;
+  return MP_OK;
 }
 
 // ---- joint-mode pair set (K8) -----------------------------------------------------

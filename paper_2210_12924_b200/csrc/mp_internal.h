@@ -51,6 +51,12 @@ struct mp_ctx {
   int64_t* d_small = nullptr;
 };
 
+// Several contexts in one process, the graph replicated on each (mp_score_orders_multi).
+struct mp_multi {
+  std::vector<mp_ctx*> ctx;
+  std::vector<mp_graph*> graph;
+};
+
 // Device-resident graph tables. Built once by mp_graph_upload from the
 // reference-shaped CSR (memplan::Graph flattened).
 //

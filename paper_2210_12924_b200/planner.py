@@ -102,6 +102,51 @@ def load_plan(text: str) -> MemoryPlan:
     return plan
 
 
+class MultiPlanner:
+    """One process, several GPUs (mp_multi_*): the graph replicated on every device,
+    candidates split into contiguous shards scored concurrently (one host thread
+    per device), the first minimum combined on the host."""
+
+    def __init__(self, devices: Sequence[int]):
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _native.check(_native.lib().mp_multi_create(devs, len(devices), C.byref(h)))
+        self.handle = h
+        self.graph = None
+
+    def upload(self, graph: Graph) -> None:
+        self._csr = graph.mp_csr()
+        _native.check(_native.lib().mp_multi_upload(self.handle, C.byref(self._csr)))
+        self.graph = graph
+
+    def score_orders(self, orders) -> tuple["ScoreResult", int]:
+        o = _i32(orders)
+        if o.ndim == 1:
+            o = o.reshape(1, -1)
+        c = o.shape[0]
+        if self.graph is None or o.shape[1] != self.graph.n:
+            raise ValueError("upload the graph first; orders must be [C][n]")
+        peak = np.zeros(max(c, 1), np.uint64)
+        step = np.zeros(max(c, 1), np.int32)
+        valid = np.zeros(max(c, 1), np.uint8)
+        best = C.c_int64()
+        _native.check(_native.lib().mp_score_orders_multi(self.handle, o.ctypes.data, c,
+                                                          peak.ctypes.data, step.ctypes.data,
+                                                          valid.ctypes.data, C.byref(best)))
+        return ScoreResult(peak[:c], step[:c], valid[:c]), best.value
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            _native.lib().mp_multi_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 @dataclass
 class BaselineResult:
     """memplan::BaselineResult (placement.hpp:44-48)."""

@@ -467,3 +467,31 @@ def test_edge_cases(planner):
     assert planner.encode_address_pairs(g, [1, 1], [0, 0]).shape == (0, 2)
     assert planner.argmin(np.array([5, 3, 3], np.uint64), np.array([1, 0, 1], np.uint8)) == 2
     assert planner.argmin(np.array([5], np.uint64), np.array([0], np.uint8)) == -1
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0]])
+def test_multi_device_scoring(devices):
+    """mp_score_orders_multi: contiguous shards on several contexts (repeated device
+    0 here: one GPU on the box) with host threads, the first minimum combined on the
+    host - identical to one context and to a serial first-minimum scan."""
+    import gzip
+    import os
+    path = os.path.join(os.path.dirname(__file__), "..", "workloads", "graphs",
+                        "resnet50_b32.json.gz")
+    with gzip.open(path, "rt") as f:
+        g = mp.load_graph(f.read())
+    orders = mp.random_topo_orders(g, 301, seed=17)
+    orders[0, [0, 1]] = orders[0, [1, 0]]
+    orders[150] = orders[77]          # a tie across shards: the lower index must win
+    mpl = mp.MultiPlanner(devices)
+    mpl.upload(g)
+    res, best = mpl.score_orders(orders)
+    p = mp.Planner(0)
+    ref = p.score_orders(g, orders)
+    assert (res.peak == ref.peak).all() and (res.peak_step == ref.peak_step).all()
+    assert (res.valid == ref.valid).all()
+    ok = np.nonzero(ref.valid)[0]
+    exp = int(ok[np.argmin(ref.peak[ok])])      # first minimum
+    assert best == exp
+    mpl.close()
+    p.close()
