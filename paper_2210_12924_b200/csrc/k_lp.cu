@@ -7,8 +7,9 @@
 // (a pinned address contributes its value v to the constant instead of a
 // term, encode.cpp:46-50), and the two binaries of each pair for the
 // "Binaries" section. One thread per pair: a length pass, an exclusive scan
-// of the lengths, and a write pass that formats the integers itself. The
-// output is byte text, so the roofline is HBM writes of the text.
+// of the lengths, and a write pass that formats the integers itself into a
+// per-warp shared stage stored out with 16-byte writes. The output is byte
+// text, so the roofline is HBM writes of the text.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -129,52 +130,127 @@ __global__ void lp_len_kernel(LpArgs a) {
   }
 }
 
-__global__ void lp_write_kernel(LpArgs a, char* __restrict__ rows, char* __restrict__ bins) {
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < a.P;
-       p += (long long)gridDim.x * blockDim.x) {
-    const int2 ij = a.pairs[p];
-    const PairText t = pair_text(a, ij.x, ij.y);
-    char* q = rows + a.row_off[p];
-    // c<3p>_live_pair: +1 below +1 above = 1
-    q = put_lit(q, " c");
-    q = put_u64(q, 3 * p);
-    q = put_lit(q, "_live_pair: +1 ");
-    q = put_pair_name(q, true, t);
-    q = put_lit(q, " +1 ");
-    q = put_pair_name(q, false, t);
-    q = put_lit(q, " = 1\n");
-    // c<3p+1>_below: ... +M below <= rhs
-    q = put_lit(q, " c");
-    q = put_u64(q, 3 * p + 1);
-    q = put_lit(q, "_below:");
-    q = put_terms(q, t);
-    q = put_lit(q, " +");
-    q = put_u64(q, (unsigned long long)a.M);
-    *q++ = ' ';
-    q = put_pair_name(q, true, t);
-    q = put_lit(q, " <= ");
-    q = put_i64(q, t.rhs_below);
-    *q++ = '\n';
-    // c<3p+2>_above: ... -M above >= rhs
-    q = put_lit(q, " c");
-    q = put_u64(q, 3 * p + 2);
-    q = put_lit(q, "_above:");
-    q = put_terms(q, t);
-    q = put_lit(q, " -");
-    q = put_u64(q, (unsigned long long)a.M);
-    *q++ = ' ';
-    q = put_pair_name(q, false, t);
-    q = put_lit(q, " >= ");
-    q = put_i64(q, t.rhs_above);
-    *q++ = '\n';
-    // Binaries section: below, then above (variable creation order, encode.cpp:263-272)
-    char* b = bins + a.bin_off[p];
-    *b++ = ' ';
-    b = put_pair_name(b, true, t);
-    *b++ = '\n';
-    *b++ = ' ';
-    b = put_pair_name(b, false, t);
-    *b++ = '\n';
+__device__ __forceinline__ char* put_rows(char* q, const LpArgs& a, const PairText& t,
+                                          long long p) {
+  // c<3p>_live_pair: +1 below +1 above = 1
+  q = put_lit(q, " c");
+  q = put_u64(q, 3 * p);
+  q = put_lit(q, "_live_pair: +1 ");
+  q = put_pair_name(q, true, t);
+  q = put_lit(q, " +1 ");
+  q = put_pair_name(q, false, t);
+  q = put_lit(q, " = 1\n");
+  // c<3p+1>_below: ... +M below <= rhs
+  q = put_lit(q, " c");
+  q = put_u64(q, 3 * p + 1);
+  q = put_lit(q, "_below:");
+  q = put_terms(q, t);
+  q = put_lit(q, " +");
+  q = put_u64(q, (unsigned long long)a.M);
+  *q++ = ' ';
+  q = put_pair_name(q, true, t);
+  q = put_lit(q, " <= ");
+  q = put_i64(q, t.rhs_below);
+  *q++ = '\n';
+  // c<3p+2>_above: ... -M above >= rhs
+  q = put_lit(q, " c");
+  q = put_u64(q, 3 * p + 2);
+  q = put_lit(q, "_above:");
+  q = put_terms(q, t);
+  q = put_lit(q, " -");
+  q = put_u64(q, (unsigned long long)a.M);
+  *q++ = ' ';
+  q = put_pair_name(q, false, t);
+  q = put_lit(q, " >= ");
+  q = put_i64(q, t.rhs_above);
+  *q++ = '\n';
+  return q;
+}
+
+// Binaries section: below, then above (variable creation order, encode.cpp:263-272)
+__device__ __forceinline__ char* put_bins(char* q, const PairText& t) {
+  *q++ = ' ';
+  q = put_pair_name(q, true, t);
+  *q++ = '\n';
+  *q++ = ' ';
+  q = put_pair_name(q, false, t);
+  *q++ = '\n';
+  return q;
+}
+
+constexpr int kLpWarps = 4;
+constexpr int kLpStage = 16384;  // bytes of staged text per warp
+
+// Copy len bytes from shared src to global dst with the warp: byte head up to a
+// 16-byte boundary of dst, then 16-byte stores whose words are funnel-shifted out
+// of aligned shared words, then a byte tail.
+__device__ __forceinline__ void warp_copy(char* __restrict__ dst, const char* src, int len,
+                                          int lane) {
+  const int head = min(len, (int)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15));
+  if (lane < head) dst[lane] = src[lane];
+  const int body = (len - head) & ~15;
+  const char* s0 = src + head;
+  const uint32_t* sw = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(s0) & ~uintptr_t(3));
+  const int sh = (int)(reinterpret_cast<uintptr_t>(s0) & 3) * 8;
+  uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+  for (int j = lane; j < body / 16; j += 32) {
+    const uint32_t* w = sw + 4 * j;
+    uint32_t x[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) x[k] = (k < 4 || sh) ? w[k] : 0u;
+    uint4 o;
+    o.x = __funnelshift_r(x[0], x[1], sh);
+    o.y = __funnelshift_r(x[1], x[2], sh);
+    o.z = __funnelshift_r(x[2], x[3], sh);
+    o.w = __funnelshift_r(x[3], x[4], sh);
+    d4[j] = o;
+  }
+  for (int k = head + body + lane; k < len; k += 32) dst[k] = src[k];
+}
+
+// One warp per 32 consecutive pairs: each lane formats its pair into a
+// contiguous shared staging area (the pairs' texts are contiguous in the
+// output), then the warp stores it with 16-byte writes - the byte-at-a-time
+// global stores of a per-thread formatter made this kernel L1-bound. Pairs
+// whose 32 texts exceed the stage are formatted straight to global memory.
+__global__ void __launch_bounds__(32 * kLpWarps)
+    lp_write_kernel(LpArgs a, char* __restrict__ rows, char* __restrict__ bins) {
+  extern __shared__ __align__(16) char stage[];  // [kLpWarps][kLpStage + 16]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  char* st = stage + (size_t)w * (kLpStage + 16);
+  const long long nwarps = (long long)gridDim.x * kLpWarps;
+  for (long long p0 = ((long long)blockIdx.x * kLpWarps + w) * 32; p0 < a.P; p0 += nwarps * 32) {
+    const long long p = p0 + lane;
+    const bool live = p < a.P;
+    const long long last = (p0 + 32 < a.P ? p0 + 32 : a.P) - 1;
+    PairText t;
+    if (live) t = pair_text(a, a.pairs[p].x, a.pairs[p].y);
+    // rows
+    {
+      const long long base = a.row_off[p0];
+      const long long span = a.row_off[last] + a.row_len[last] - base;
+      if (span <= kLpStage) {
+        if (live) put_rows(st + (a.row_off[p] - base), a, t, p);
+        __syncwarp();
+        warp_copy(rows + base, st, (int)span, lane);
+        __syncwarp();
+      } else if (live) {
+        put_rows(rows + a.row_off[p], a, t, p);
+      }
+    }
+    // binaries
+    {
+      const long long base = a.bin_off[p0];
+      const long long span = a.bin_off[last] + a.bin_len[last] - base;
+      if (span <= kLpStage) {
+        if (live) put_bins(st + (a.bin_off[p] - base), t);
+        __syncwarp();
+        warp_copy(bins + base, st, (int)span, lane);
+        __syncwarp();
+      } else if (live) {
+        put_bins(bins + a.bin_off[p], t);
+      }
+    }
   }
 }
 
@@ -284,9 +360,11 @@ mp_status launch_lp_len(const LpArgs& a, int num_sms, cudaStream_t st) {
 mp_status launch_lp_write(const LpArgs& a, char* d_rows, char* d_bins, int num_sms,
                           cudaStream_t st) {
   if (a.P <= 0) return MP_OK;
-  int64_t grid = (a.P + 255) / 256;
-  if (grid > (int64_t)num_sms * 16) grid = (int64_t)num_sms * 16;
-  lp_write_kernel<<<(unsigned)grid, 256, 0, st>>>(a, d_rows, d_bins);
+  int64_t grid = (a.P + 32 * kLpWarps - 1) / (32 * kLpWarps);
+  if (grid > (int64_t)num_sms * 3) grid = (int64_t)num_sms * 3;
+  const int smem = kLpWarps * (kLpStage + 16);
+  MP_CUDA(cudaFuncSetAttribute(lp_write_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  lp_write_kernel<<<(unsigned)grid, 32 * kLpWarps, smem, st>>>(a, d_rows, d_bins);
   MP_CUDA(cudaGetLastError());
   return MP_OK;
 }

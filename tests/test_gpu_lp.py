@@ -49,6 +49,27 @@ def test_model_graph_lp_vs_reference(planner):
         assert text == rg.encode_addresses_lp(lo, hi)
 
 
+def test_long_ids_bypass_the_stage(planner):
+    """Edge ids long enough that 32 pairs' rows overflow the per-warp shared stage
+    (the kernel then formats those pairs straight to global memory), mixed with
+    short ones, byte-identical to the reference."""
+    g = mp.generate_graph("fork_join", 6, 1000, 3)
+    ids = [("e" * (300 + 37 * (k % 5)) + str(k)) if k % 3 else f"s{k}" for k in range(g.E)]
+    text = mp.save_graph(g)
+    import json
+    doc = json.loads(text)
+    ren = dict(zip([e["id"] for e in doc["edges"]], ids))
+    for e in doc["edges"]:
+        e["id"] = ren[e["id"]]
+    g2 = mp.load_graph(json.dumps(doc))
+    o = mp.random_topo_orders(g2, 1, seed=1)[0]
+    lo, hi = planner.lifetimes_from_order(g2, o)
+    got = planner.encode_addresses_lp(g2, lo, hi)
+    assert got.count("_live_pair:") == planner.encode_address_pairs(g2, lo, hi, want_pairs=False)
+    if O.ref_available():
+        assert got == O.RefGraph.load(mp.save_graph(g2)).encode_addresses_lp(lo, hi)
+
+
 def test_sanitized_and_ambiguous_ids(planner):
     """Ids with non-alphanumeric bytes are sanitized as lp_format.cpp:30-36; ids
     whose sanitized pair names could coincide (lp_names would suffix "_2") are
