@@ -428,3 +428,129 @@ int or_run_baseline(const or_graph* g, const int32_t* order, int64_t len, int be
   free(hi);
   return 0;
 }
+
+/* ---- encode_joint's pair set (encode.cpp:401-408, analysis.cpp:11-113) ---------- */
+typedef struct {
+  const or_graph* g;
+  int32_t* fanin_off; /* per node: edges whose sink list holds it */
+  int32_t* fanin;
+  int8_t* memo;       /* [n*n]: 0 unknown, 1 reaches, 2 does not */
+} or_reach;
+
+/* ReachabilityCache::reaches (analysis.cpp:79-92): ancestor is a proper ancestor of v */
+static int or_reaches(or_reach* r, int32_t ancestor, int32_t v) {
+  if (ancestor == v) return 0;
+  int8_t* m = &r->memo[(size_t)ancestor * r->g->n + v];
+  if (*m) return *m == 1;
+  int found = 0;
+  for (int32_t q = r->fanin_off[v]; q < r->fanin_off[v + 1] && !found; ++q) {
+    const int32_t src = r->g->edge_src[r->fanin[q]];
+    if (src == ancestor || or_reaches(r, ancestor, src)) found = 1;
+  }
+  *m = found ? 1 : 2;
+  return found;
+}
+
+/* edge_precedes (analysis.cpp:94-113), literally */
+static int or_edge_precedes(const or_graph* g, const int32_t* mul_lo, const int32_t* mul_hi,
+                            or_reach* r, int32_t e1, int32_t e2) {
+  if (or_disjoint(mul_lo[e1], mul_hi[e1], mul_lo[e2], mul_hi[e2])) return 1;
+  const int64_t a = g->sink_off[e1], b = g->sink_off[e1 + 1];
+  if (a == b) return 0;
+  const int32_t src2 = g->edge_src[e2];
+  for (int64_t k = a; k < b; ++k)
+    if (!or_reaches(r, g->sinks[k], src2)) return 0;
+  /* ends1 = sinks(e1) + src(e1) */
+  if (src2 == g->edge_src[e1]) return 0;
+  for (int64_t k = a; k < b; ++k)
+    if (g->sinks[k] == src2) return 0;
+  for (int64_t q = g->sink_off[e2]; q < g->sink_off[e2 + 1]; ++q) {
+    const int32_t s = g->sinks[q];
+    if (s == g->edge_src[e1]) return 0;
+    for (int64_t k = a; k < b; ++k)
+      if (g->sinks[k] == s) return 0;
+  }
+  return 1;
+}
+
+int64_t or_joint_pairs(const or_graph* g, int filter, int32_t* pairs, int64_t cap) {
+  const int32_t n = g->n, E = g->num_edges;
+  int32_t* mul_lo = (int32_t*)malloc(sizeof(int32_t) * (E ? E : 1));
+  int32_t* mul_hi = (int32_t*)malloc(sizeof(int32_t) * (E ? E : 1));
+  or_reach r = {g, (int32_t*)calloc((size_t)n + 1, sizeof(int32_t)), NULL,
+                (int8_t*)calloc((size_t)n * (n ? n : 1), 1)};
+  /* compute_levels / compute_bounds (analysis.cpp:11-62) over a Kahn order */
+  int32_t* order = (int32_t*)malloc(sizeof(int32_t) * (n ? n : 1));
+  int32_t* indeg = (int32_t*)calloc((size_t)n + 1, sizeof(int32_t));
+  int32_t* fwd = (int32_t*)calloc((size_t)n + 1, sizeof(int32_t));
+  int32_t* bwd = (int32_t*)calloc((size_t)n + 1, sizeof(int32_t));
+  for (int64_t k = 0; k < g->sink_off[E]; ++k) ++indeg[g->sinks[k]];
+  for (int32_t e = 0; e < E; ++e)
+    for (int64_t k = g->sink_off[e]; k < g->sink_off[e + 1]; ++k) ++r.fanin_off[g->sinks[k] + 1];
+  for (int32_t v = 0; v < n; ++v) r.fanin_off[v + 1] += r.fanin_off[v];
+  r.fanin = (int32_t*)malloc(sizeof(int32_t) * (size_t)(r.fanin_off[n] ? r.fanin_off[n] : 1));
+  {
+    int32_t* cur = (int32_t*)malloc(sizeof(int32_t) * (n ? n : 1));
+    for (int32_t v = 0; v < n; ++v) cur[v] = r.fanin_off[v];
+    for (int32_t e = 0; e < E; ++e)
+      for (int64_t k = g->sink_off[e]; k < g->sink_off[e + 1]; ++k) r.fanin[cur[g->sinks[k]]++] = e;
+    free(cur);
+  }
+  int32_t head = 0, tail = 0;
+  for (int32_t v = 0; v < n; ++v)
+    if (!indeg[v]) order[tail++] = v;
+  while (head < tail) {
+    const int32_t v = order[head++];
+    for (int32_t e = 0; e < E; ++e) {
+      if (g->edge_src[e] != v) continue;
+      for (int64_t k = g->sink_off[e]; k < g->sink_off[e + 1]; ++k)
+        if (--indeg[g->sinks[k]] == 0) order[tail++] = g->sinks[k];
+    }
+  }
+  int64_t at = -1;
+  if (tail == n) {
+    for (int32_t i = 0; i < n; ++i) {  /* forward: longest edge count from a source */
+      const int32_t v = order[i];
+      for (int32_t q = r.fanin_off[v]; q < r.fanin_off[v + 1]; ++q) {
+        const int32_t src = g->edge_src[r.fanin[q]];
+        if (fwd[src] + 1 > fwd[v]) fwd[v] = fwd[src] + 1;
+      }
+    }
+    for (int32_t i = n - 1; i >= 0; --i) {  /* backward: longest edge count to a terminal */
+      const int32_t v = order[i];
+      for (int32_t e = 0; e < E; ++e) {
+        if (g->edge_src[e] != v) continue;
+        for (int64_t k = g->sink_off[e]; k < g->sink_off[e + 1]; ++k)
+          if (bwd[g->sinks[k]] + 1 > bwd[v]) bwd[v] = bwd[g->sinks[k]] + 1;
+      }
+    }
+    for (int32_t e = 0; e < E; ++e) {  /* mul = [asap(src), max alap(sinks) or n] */
+      int32_t hi = n;
+      if (g->sink_off[e + 1] > g->sink_off[e]) {
+        hi = 0;
+        for (int64_t k = g->sink_off[e]; k < g->sink_off[e + 1]; ++k)
+          if (n - bwd[g->sinks[k]] > hi) hi = n - bwd[g->sinks[k]];
+      }
+      mul_lo[e] = 1 + fwd[g->edge_src[e]];
+      mul_hi[e] = hi;
+    }
+    at = 0;
+    for (int32_t i = 0; i < E; ++i) {
+      if (g->edge_size[i] == 0) continue;
+      for (int32_t j = i + 1; j < E; ++j) {
+        if (g->edge_size[j] == 0) continue;
+        if (filter && (or_edge_precedes(g, mul_lo, mul_hi, &r, i, j) ||
+                       or_edge_precedes(g, mul_lo, mul_hi, &r, j, i)))
+          continue;
+        if (pairs && at < cap) {
+          pairs[2 * at] = i;
+          pairs[2 * at + 1] = j;
+        }
+        ++at;
+      }
+    }
+  }
+  free(mul_lo); free(mul_hi); free(order); free(indeg); free(fwd); free(bwd);
+  free(r.fanin_off); free(r.fanin); free(r.memo);
+  return at;
+}

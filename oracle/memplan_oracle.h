@@ -96,6 +96,13 @@ void or_greedy_pack(int32_t num_edges, const int32_t* lo, const int32_t* hi, con
 int or_run_baseline(const or_graph* g, const int32_t* order, int64_t len, int best_fit,
                     uint64_t* mr_peak, uint64_t* rs_at_peak, double* frag);
 
+/* The pair loop of encode_joint (encode.cpp:401-408): data edges a < b (edge
+ * order), skipped when filter != 0 and edge_precedes holds either way
+ * (analysis.cpp:94-113) with compute_bounds (analysis.cpp:11-62) and a memoised
+ * ancestor search as ReachabilityCache (analysis.cpp:79-92). Two-phase: pairs may
+ * be NULL; returns the count (-1 on a cycle). */
+int64_t or_joint_pairs(const or_graph* g, int filter, int32_t* pairs, int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -91,6 +91,8 @@ def olib():
         lib.or_preallocate_pyramid.argtypes = [C.c_int32, _i32p, _i32p, _u64p, _i32p, _u8p, _u64p]
         lib.or_preallocate_pyramid.restype = C.c_uint64
         lib.or_greedy_pack.argtypes = [C.c_int32, _i32p, _i32p, _u64p, _vp, _u64p, _u8p]
+        lib.or_joint_pairs.argtypes = [gp, C.c_int, _vp, C.c_int64]
+        lib.or_joint_pairs.restype = C.c_int64
         lib.or_run_baseline.argtypes = [gp, _i32p, C.c_int64, C.c_int, C.POINTER(C.c_uint64),
                                         C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
         _olib = lib
@@ -148,6 +150,13 @@ class Oracle:
         olib().or_timeline_from_lifetimes(C.byref(self._g), lo, hi, int(horizon), _opt_ptr(b),
                                           C.byref(pr), C.byref(ps))
         return (b[:horizon] if want_bytes else None), int(pr.value), int(ps.value)
+
+    def joint_pairs(self, filter_pairs=True):
+        """encode_joint's pair set (encode.cpp:401-408) -> int32[P][2]."""
+        cnt = olib().or_joint_pairs(C.byref(self._g), int(filter_pairs), None, 0)
+        out = np.zeros((max(cnt, 1), 2), np.int32)
+        olib().or_joint_pairs(C.byref(self._g), int(filter_pairs), out.ctypes.data, cnt)
+        return out[:cnt]
 
     def run_baseline(self, order, best_fit=False):
         """placement.cpp:150-180 -> (mr_peak, rs_at_peak, fragmentation) or None (invalid)."""
@@ -424,6 +433,13 @@ class RefGraph:
                                                   C.byref(ps)))
         return b[:horizon], int(pr.value), int(ps.value)
 
+    def joint_pairs(self, filter_pairs=True):
+        """encode_joint's pair set (encode.cpp:401-408) -> int32[P][2]."""
+        cnt = olib().or_joint_pairs(C.byref(self._g), int(filter_pairs), None, 0)
+        out = np.zeros((max(cnt, 1), 2), np.int32)
+        olib().or_joint_pairs(C.byref(self._g), int(filter_pairs), out.ctypes.data, cnt)
+        return out[:cnt]
+
     def run_baseline(self, order, best_fit=False):
         """placement.cpp:150-180 -> (mr_peak, rs_at_peak, fragmentation) or None (invalid)."""
         mr, rs, fr = C.c_uint64(), C.c_uint64(), C.c_double()
@@ -537,3 +553,78 @@ class RefGraph:
 
 def ref_fragmentation(mr, rs):
     return float(rlib().ref_fragmentation(int(mr), int(rs)))
+
+
+# ---- LP text of the address model (pure Python restatement, small graphs) -----------
+def _sanitize(name: str) -> str:
+    """lp_format.cpp:30-36: every non-alphanumeric byte becomes '_'."""
+    return "".join(c if c.isascii() and c.isalnum() else "_" for c in name)
+
+
+def address_model_lp(edge_ids, lo, hi, size, pinned=None, pinned_addr=None) -> str:
+    """write_lp(encode_addresses(graph, lifetimes, preplaced)) restated:
+    encode.cpp:320-377 (variables, the pair loop, the below/above/live_pair rows with
+    pinned addresses folded into the constant, encode.cpp:40-97 Row::emit) and
+    lp_format.cpp:75-121 (lp_names with "_2" suffixes, the section layout)."""
+    E = len(size)
+    M = int(sum(int(s) for s in size))                      # Graph::total_bytes
+    data = [e for e in range(E) if int(size[e]) > 0]
+    pin = {e: int(pinned_addr[e]) for e in data if pinned is not None and pinned[e]}
+    vars_ = [("peak_mem", "int", 0, M)]                     # objective first
+    addr = {}
+    for e in data:
+        if e not in pin:
+            addr[e] = len(vars_)
+            vars_.append((f"addr({edge_ids[e]})", "int", 0, M))
+    rows = []
+
+    def emit(tag, rel, rhs, terms):                          # terms: (coef, var or pinned edge)
+        const, out = 0, []
+        for coef, v in terms:
+            if isinstance(v, tuple):                         # ("pin", e)
+                const += coef * pin[v[1]]
+            else:
+                out.append((coef, v))
+        rows.append((tag, out, rel, rhs - const))
+
+    def slot(e):
+        return ("pin", e) if e in pin else addr[e]
+
+    for a in range(len(data)):
+        for b in range(a + 1, len(data)):
+            i, j = data[a], data[b]
+            if i in pin and j in pin:
+                continue
+            if lo[i] > hi[i] or lo[j] > hi[j] or hi[i] < lo[j] or hi[j] < lo[i]:
+                continue                                     # intervals_disjoint
+            below = len(vars_)
+            vars_.append((f"below({edge_ids[i]},{edge_ids[j]})", "bin", 0, 1))
+            above = len(vars_)
+            vars_.append((f"above({edge_ids[i]},{edge_ids[j]})", "bin", 0, 1))
+            emit("live_pair", "=", 1, [(1, below), (1, above)])
+            emit("below", "<=", M - int(size[i]), [(1, slot(i)), (-1, slot(j)), (M, below)])
+            emit("above", ">=", int(size[j]) - M, [(1, slot(i)), (-1, slot(j)), (-M, above)])
+    for e in data:
+        emit("peak_address", "<=", -int(size[e]), [(1, slot(e)), (-1, 0)])
+    names, seen = [], set()
+    for name, _, _, _ in vars_:                              # lp_names
+        base = cand = _sanitize(name)
+        k = 2
+        while cand in seen:
+            cand = f"{base}_{k}"
+            k += 1
+        seen.add(cand)
+        names.append(cand)
+    out = [f"Minimize\n obj: {names[0]}\nSubject To\n"]
+    for r, (tag, terms, rel, rhs) in enumerate(rows):
+        t = "".join(f" {'-' if c < 0 else '+'}{abs(c)} {names[v]}" for c, v in terms)
+        out.append(f" c{r}_{tag}:{t} {rel} {rhs}\n")
+    out.append("Bounds\n")
+    out += [f" {lo_} <= {names[k]} <= {hi_}\n" for k, (_, kind, lo_, hi_) in enumerate(vars_)
+            if kind == "int"]
+    out.append("Generals\n")
+    out += [f" {names[k]}\n" for k, v in enumerate(vars_) if v[1] == "int"]
+    out.append("Binaries\n")
+    out += [f" {names[k]}\n" for k, v in enumerate(vars_) if v[1] == "bin"]
+    out.append("End\n")
+    return "".join(out)

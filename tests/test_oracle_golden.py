@@ -168,3 +168,30 @@ def test_golden_run_baseline(golden):
         if rec["name"] == "chain3":
             assert o.run_baseline(rec["orders"][0]["order"])[2] == 0.0
     assert checked >= 70
+
+
+def test_golden_joint_pairs(golden):
+    """or_joint_pairs (encode_joint's pair loop + edge_precedes, restated) vs the
+    reference's own pair lists."""
+    for rec in golden["graphs"]:
+        o = _oracle(rec)
+        assert o.joint_pairs().tolist() == rec["joint_pairs"]["filtered"], rec["name"]
+        assert len(o.joint_pairs(False)) == rec["joint_pairs"]["all"]
+
+
+def test_golden_lp_text(golden):
+    """The Python restatement of write_lp(encode_addresses(...)) vs the reference's
+    own LP text, plain and with a pinned map."""
+    import paper_2210_12924_b200 as mp
+    checked = 0
+    for rec in golden["graphs"]:
+        if "lp" not in rec:
+            continue
+        ids = mp.load_graph(rec["graph_json"]).edge_ids
+        case = rec["orders"][0]
+        size = rec["csr"]["edge_size"]
+        assert O.address_model_lp(ids, case["lo"], case["hi"], size) == rec["lp"]["text"]
+        assert O.address_model_lp(ids, case["lo"], case["hi"], size, rec["pinned"]["pinned"],
+                                  rec["lp"]["pinned_addr"]) == rec["lp"]["text_pinned"]
+        checked += 1
+    assert checked >= 15
