@@ -371,6 +371,8 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
       const PW w = pos[v];
       bad |= !PWT::fresh(w, tag);           // never written: not a permutation
       if (u >= 0) bad |= pos[u] >= w;       // producer not strictly before v
+      const int u2 = __ldg(G.node_u2 + v).y;
+      if (u2 >= 0) bad |= pos[u2] >= w;
       const int q = PWT::pos(w);
       if (q < n) XS::store(XF, q, x, f);
     };
@@ -383,29 +385,32 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
     } else {
       constexpr int kB = 8;
       for (int v0 = tid; v0 < n; v0 += T * kB) {
-        PW w[kB], pu[kB];
+        // both first producers in node space: pos[v] is this node's own (coalesced)
+        // word, so each needs one random gather (the flat list below needs two)
+        PW w[kB], pu[kB], pu2[kB];
         VT xx[kB], ff[kB];
 #pragma unroll
         for (int u = 0; u < kB; ++u) {
           const int v = v0 + u * T;
           const bool in = v < n;
-          const int pr = in ? __ldg(G.pred1 + v) : -1;
+          const int2 pr = in ? __ldg(G.node_u2 + v) : make_int2(-1, -1);
           w[u] = in ? pos[v] : tag;
           xx[u] = in ? (VT)__ldg(G.node_x + v) : (VT)0;
           ff[u] = in ? (VT)__ldg(G.node_f + v) : (VT)0;
-          pu[u] = pr >= 0 ? pos[pr] : (PW)0;
+          pu[u] = pr.x >= 0 ? pos[pr.x] : (PW)0;
+          pu2[u] = pr.y >= 0 ? pos[pr.y] : (PW)0;
         }
 #pragma unroll
         for (int u = 0; u < kB; ++u) {
           if (v0 + u * T < n) {
-            bad |= !PWT::fresh(w[u], tag) || pu[u] >= w[u];
+            bad |= !PWT::fresh(w[u], tag) || pu[u] >= w[u] || pu2[u] >= w[u];
             const int q = PWT::pos(w[u]);
             if (q < n) XS::store(XF, q, xx[u], ff[u]);
           }
         }
       }
     }
-    // ---- phase 2b: remaining reduced producer pairs ----------------------------------
+    // ---- phase 2b: 3rd+ reduced producer pairs (flat) --------------------------------
     {
       constexpr int kB = 8;
       for (int i0 = tid; i0 < G.nextra; i0 += T * kB) {

@@ -232,7 +232,7 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
   prepare_scoring(n, E, g->h_edge_src.data(), g->h_sink_off.data(), g->h_sinks.data(),
                   g->h_edge_size.data(), &P);
   g->n_preds = P.num_reduced_preds;
-  g->n_extra = (int32_t)P.extra_u.size();
+  g->n_extra = (int32_t)P.extra3_u.size();
   g->n_dyn = (int32_t)P.dyn_size.size();
   g->n_dyn_sinks = (int32_t)P.dyn_sinks.size();
   for (size_t d = 0; d + 1 < P.dyn_off.size(); ++d)
@@ -256,8 +256,9 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
   up(upload(&g->d_node_x, P.node_x.data(), P.node_x.size(), st));
   up(upload(&g->d_node_f, P.node_f.data(), P.node_f.size(), st));
   up(upload(&g->d_pred1, P.pred1.data(), P.pred1.size(), st));
-  up(upload(&g->d_extra_u, P.extra_u.data(), P.extra_u.size(), st));
-  up(upload(&g->d_extra_w, P.extra_w.data(), P.extra_w.size(), st));
+  // the node-table scorer checks pred1 and pred2 in node space: its flat list is the 3rd+
+  up(upload(&g->d_extra_u, P.extra3_u.data(), P.extra3_u.size(), st));
+  up(upload(&g->d_extra_w, P.extra3_w.data(), P.extra3_w.size(), st));
   up(upload(&g->d_dyn_off, P.dyn_off.data(), P.dyn_off.size(), st));
   up(upload(&g->d_dyn_sinks, P.dyn_sinks.data(), P.dyn_sinks.size(), st));
   up(upload(&g->d_dyn_size, P.dyn_size.data(), P.dyn_size.size(), st));

@@ -196,8 +196,10 @@ void prepare_scoring(int32_t n, int32_t E, const int32_t* src, const int64_t* si
       const int32_t u = P->extra_u[i], w = P->extra_w[i];
       if (seen[w]++ == 0) {
         P->pred2[w] = u;
-      } else if (n < 65536) {
-        P->extra3_packed.push_back((uint32_t)u | ((uint32_t)w << 16));
+      } else {
+        if (n < 65536) P->extra3_packed.push_back((uint32_t)u | ((uint32_t)w << 16));
+        P->extra3_u.push_back(u);
+        P->extra3_w.push_back(w);
       }
     }
   }

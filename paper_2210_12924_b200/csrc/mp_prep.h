@@ -29,6 +29,7 @@ struct ScorePrep {
   std::vector<uint32_t> node_rec32;    // [4n] (x, f, pred1, pred2) for 32-bit graphs
   std::vector<int32_t> node_u2;        // [2n] (pred1, pred2) for 64-bit graphs
   std::vector<uint32_t> extra3_packed; // 3rd+ reduced producer pairs, u | w << 16 (n < 65536)
+  std::vector<int32_t> extra3_u, extra3_w;   // the same pairs as int32 (any n)
   std::vector<int32_t> out_off{0};           // [n+1] fanout(v) (graph.hpp:91), edge order
   std::vector<int32_t> out_edges;            // [E]
 };
