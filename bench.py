@@ -141,6 +141,22 @@ def profile_traffic(config):
         return None
 
 
+def smem_pipe_use(config, kernel_ms, sm_mhz, num_sms):
+    """The resource that actually binds the scorer: shared-memory
+    wavefronts per launch (committed ncu capture of this config) against one
+    wavefront per SM per cycle over the measured kernel time and clock."""
+    p = os.path.join(ROOT, "profiles", f"{config}_score_ncu.json")
+    try:
+        with open(p) as f:
+            raw = json.load(f)["raw"]
+        wf = float(raw["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"].split()[0])
+        cap = num_sms * kernel_ms * 1e-3 * sm_mhz * 1e6
+        return {"kind": "shared-memory wavefronts (LSU pipe)", "per_launch": wf,
+                "frac_of_one_per_sm_cycle": wf / cap, "source": f"profiles/{config}_score_ncu.json"}
+    except Exception:
+        return None
+
+
 # ---- reference arm -------------------------------------------------------------------
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
@@ -766,6 +782,11 @@ def main():
         }
         if cpu:
             line["cpu_baseline"] = cpu
+        sm_mhz = (line["clocks"] or {}).get("sm_mhz") or 1965
+        bind = smem_pipe_use(args.config, kern_graph_ms, float(sm_mhz),
+                             torch.cuda.get_device_properties(dev).multi_processor_count)
+        if bind:
+            line["roofline"]["binding_resource"] = bind
         print(json.dumps(line))
     if world > 1:
         dist.barrier()
