@@ -298,11 +298,30 @@ __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMi
     VT run[KC], best[KC];
     int best_i[KC];
     const int p0 = tid * P;
+    // KC == 1, J <= 8: pass 1 keeps the chunk (P <= J + 1 entries) in registers for
+    // pass 2 (J = 16 would spill)
+    constexpr bool kRegChunk = KC == 1 && J <= 8;
+    constexpr int PM = kRegChunk ? J + 1 : 1;
+    VT xr[PM], fr[PM];
 #pragma unroll
     for (int k = 0; k < KC; ++k) {
       const XFPair<VT>* mine = XF[k] + p0;
       VT total = 0;
-      for (int i = 0; i < P; ++i) total += mine[i].x;
+      if constexpr (kRegChunk) {
+#pragma unroll
+        for (int i = 0; i < PM; ++i) {
+          xr[i] = 0;
+          fr[i] = 0;
+          if (i < P) {
+            const XFPair<VT> e = mine[i];
+            xr[i] = e.x;
+            fr[i] = e.f;
+          }
+          total += xr[i];
+        }
+      } else {
+        for (int i = 0; i < P; ++i) total += mine[i].x;
+      }
       const VT incl = warp_incl_scan(total, lane);
       if (lane == kWarp - 1) bs.wsum[k][warp] = incl;
       run[k] = incl - total;
@@ -313,7 +332,23 @@ __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMi
     for (int k = 0; k < KC; ++k) {
       run[k] += warp_sum(lane < warp ? bs.wsum[k][lane] : (VT)0);
       const XFPair<VT>* mine = XF[k] + p0;
-      if (bytes_out == nullptr) {
+      if (kRegChunk && bytes_out == nullptr) {
+        // from the registers of pass 1 (entries past P are (0, 0) and never win:
+        // strict > keeps the first maximum)
+        VT r = run[k] + xr[0];
+        VT b = r + fr[0];
+        int bi = 0;
+#pragma unroll
+        for (int i = 1; i < PM; ++i) {
+          r += xr[i];
+          const VT rs = r + fr[i];
+          const bool better = rs > b;
+          b = better ? rs : b;
+          bi = better ? i : bi;
+        }
+        best[k] = b;
+        best_i[k] = p0 < n ? p0 + bi : INT_MAX;  // a chunk made only of padding
+      } else if (bytes_out == nullptr) {
         // First element initialises (best, index); strict > keeps the first
         // maximum. Padding entries are (0, 0): their RS equals S(n-1) <= RS(n-1),
         // so they never replace a real position.
