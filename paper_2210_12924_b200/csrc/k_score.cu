@@ -775,7 +775,7 @@ mp_status score_configure(mp_graph* g) {
   for (int j : {4, 8, 16}) {
     if (fj && j != fj) continue;
     const int t = ((n + j - 1) / j + 31) / 32 * 32;
-    if (t <= (j == 4 ? 256 : j == 8 ? 384 : 512)) {  // RegBounds<J>::kMaxT
+    if (t <= (j == 4 ? 256 : j == 8 ? MP_J8_MAXT : 512)) {  // RegBounds<J>::kMaxT
       J = j;
       T = t < 32 ? 32 : t;
       break;

@@ -35,8 +35,14 @@ struct RegLayout {
 //   J=16: T <= 512, 128.  score_configure picks T within kMaxT.
 template <int J, int KC>
 struct RegBounds {
-  static constexpr int kMaxT = J == 4 ? 256 : J == 8 ? (KC == 1 ? 384 : 320) : 512;
-  static constexpr int kMinBlocks = J == 4 ? (KC == 1 ? 4 : 3) : J == 8 ? 2 : 1;
+#ifndef MP_J8_MAXT
+#define MP_J8_MAXT 384
+#endif
+#ifndef MP_J8_MINB
+#define MP_J8_MINB 2
+#endif
+  static constexpr int kMaxT = J == 4 ? 256 : J == 8 ? (KC == 1 ? MP_J8_MAXT : 320) : 512;
+  static constexpr int kMinBlocks = J == 4 ? (KC == 1 ? 4 : 3) : J == 8 ? (KC == 1 ? MP_J8_MINB : 2) : 1;
 };
 
 template <typename VT, int KC>

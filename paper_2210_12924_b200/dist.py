@@ -93,3 +93,74 @@ def balanced_row_ranges(row_work, world: int) -> list[tuple[int, int]]:
 def triangular_row_work(num_edges: int):
     """Per-row compare work of the pairwise sweep (row i scans j > i)."""
     return np.arange(num_edges, 0, -1, dtype=np.float64)
+
+
+def _world_rank(group=None) -> tuple[int, int]:
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def exchange_counts(local: int, device=None, group=None) -> tuple[int, int, list[int]]:
+    """The one exchange of the row-sharded pair sweep: allgather
+    of the per-rank pair counts. Returns (this rank's global offset, total,
+    per-rank counts); rank r's pairs occupy [offset, offset + counts[r]) of the
+    reference's lexicographic list."""
+    import torch
+    import torch.distributed as dist
+    world, rank = _world_rank(group)
+    if world == 1:
+        return 0, int(local), [int(local)]
+    mine = torch.tensor([int(local)], dtype=torch.int64, device=device)
+    out = [torch.zeros(1, dtype=torch.int64, device=device) for _ in range(world)]
+    dist.all_gather(out, mine, group=group)
+    counts = [int(t.item()) for t in out]
+    return sum(counts[:rank]), sum(counts), counts
+
+
+def sharded_overlap_pairs(shard_fn, num_edges: int, device=None, group=None):
+    """encode_addresses' pair loop (encode.cpp:347-367) sharded by rows over the
+    ranks: rank r sweeps rows ``balanced_row_ranges(triangular_row_work(E))[r]``
+    with ``shard_fn(row_begin, row_end) -> int32 [k, 2]`` (the K2 kernel on its
+    GPU), then ONE allgather of the counts gives every rank its global offset.
+    Pairs stay rank-local; concatenated in rank order they are the reference's
+    list. Returns (local pairs, offset, total)."""
+    world, rank = _world_rank(group)
+    r0, r1 = balanced_row_ranges(triangular_row_work(num_edges), world)[rank]
+    pairs = shard_fn(r0, r1)
+    off, total, _ = exchange_counts(len(pairs), device, group)
+    return pairs, off, total
+
+
+def sharded_conflicts(shard_fn, num_edges: int, device=None, group=None, gather: bool = True):
+    """validate_plan's pairwise check (plan.cpp:390-404) sharded by rows: ONE
+    allreduce(sum) of the violation count; only when it is non-zero are the
+    violating pairs gathered (padded allgather), in rank order = (i, j) order.
+    ``shard_fn(row_begin, row_end) -> int32 [k, 2]``. Returns (total count,
+    all violating pairs as an int32 numpy [total, 2], or None with gather=False)."""
+    import torch
+    import torch.distributed as dist
+    world, rank = _world_rank(group)
+    r0, r1 = balanced_row_ranges(triangular_row_work(num_edges), world)[rank]
+    viol = shard_fn(r0, r1)
+    k = len(viol)
+    if world == 1:
+        total = k
+        allv = np.asarray(viol.cpu() if hasattr(viol, "cpu") else viol, np.int32).reshape(-1, 2)
+        return total, (allv if gather else None)
+    t = torch.tensor([k], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    total = int(t.item())
+    if not gather or total == 0:
+        return total, (np.zeros((0, 2), np.int32) if gather else None)
+    _, _, counts = exchange_counts(k, device, group)
+    width = max(counts)
+    buf = torch.full((width, 2), -1, dtype=torch.int32, device=device)
+    if k:
+        v = viol if isinstance(viol, torch.Tensor) else torch.from_numpy(np.asarray(viol))
+        buf[:k] = v.to(device=buf.device, dtype=torch.int32)
+    out = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(out, buf, group=group)
+    parts = [o[:c].cpu().numpy() for o, c in zip(out, counts)]
+    return total, np.concatenate(parts).astype(np.int32).reshape(-1, 2)

@@ -422,6 +422,23 @@ class Planner:
             _native.ptr(d_pairs), int(cap), C.byref(cnt), stream))
         return cnt.value
 
+    def overlap_pairs_rows_d(self, d_lo, d_hi, d_size, d_pinned, row_begin: int, row_end: int,
+                             stream: int | None = None):
+        """K2 over rows [row_begin, row_end) of device-resident lifetimes: count pass,
+        then a fill into a fresh int32 [k, 2] device tensor (the shard function of
+        dist.sharded_overlap_pairs)."""
+        import torch
+        E = int(d_lo.numel())
+        rows = max(0, int(row_end) - int(row_begin))
+        off = torch.empty(rows + 1, dtype=torch.int64, device=d_lo.device)
+        k = self.overlap_pairs_d(E, d_lo, d_hi, d_size, d_pinned, row_begin, row_end, off, None,
+                                 0, stream)
+        out = torch.empty((max(k, 1), 2), dtype=torch.int32, device=d_lo.device)
+        if k:
+            self.overlap_pairs_d(E, d_lo, d_hi, d_size, d_pinned, row_begin, row_end, off, out, k,
+                                 stream)
+        return out[:k]
+
     # ---- (a11/a12/a13) validation -----------------------------------------------
     def conflicting_pairs(self, lo, hi, size, has_addr, addr) -> np.ndarray:
         """Pairwise part of validate_plan (plan.cpp:390-404), in (i, j) order."""
@@ -450,6 +467,22 @@ class Planner:
             _native.ptr(d_has), _native.ptr(d_addr), int(row_begin), int(row_end),
             _native.ptr(d_row_off), _native.ptr(d_viol), int(cap), C.byref(cnt), stream))
         return cnt.value
+
+    def conflicting_pairs_rows_d(self, d_lo, d_hi, d_size, d_has, d_addr, row_begin: int,
+                                 row_end: int, stream: int | None = None):
+        """K4 over rows [row_begin, row_end): violating pairs as an int32 [k, 2]
+        device tensor (the shard function of dist.sharded_conflicts)."""
+        import torch
+        E = int(d_lo.numel())
+        rows = max(0, int(row_end) - int(row_begin))
+        off = torch.empty(rows + 1, dtype=torch.int64, device=d_lo.device)
+        k = self.validate_pairs_d(E, d_lo, d_hi, d_size, d_has, d_addr, row_begin, row_end, off,
+                                  None, 0, stream)
+        out = torch.empty((max(k, 1), 2), dtype=torch.int32, device=d_lo.device)
+        if k:
+            self.validate_pairs_d(E, d_lo, d_hi, d_size, d_has, d_addr, row_begin, row_end, off,
+                                  out, k, stream)
+        return out[:k]
 
     def addresses_feasible(self, graph: Graph, lo, hi, addresses: Mapping[int, int]) -> bool:
         """pipeline.cpp:146-160 (addresses keyed by edge index)."""

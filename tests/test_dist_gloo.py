@@ -95,3 +95,58 @@ def test_key_packing_edges():
     assert D.check_device_key(D.NO_KEY) == D.NO_KEY
     assert [D.shard_range(10, 3, r) for r in range(3)] == [(0, 3), (3, 6), (6, 10)]
     assert D.balanced_row_ranges([], 2) == [(0, 0), (0, 0)]
+
+
+def _worker_sharded(rank, world, port, lo, hi, size, has, addr, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "oracle"))
+    import oracle as O
+    full = O.overlap_pairs(lo, hi, size)
+    viol_full = O.validate_pairs(lo, hi, size, has, addr)
+
+    def rows(p, r0, r1):   # the per-GPU kernel's output for rows [r0, r1), from the C restatement
+        return p[(p[:, 0] >= r0) & (p[:, 0] < r1)] if len(p) else p.reshape(0, 2)
+
+    pairs, off, total = D.sharded_overlap_pairs(lambda a, b: rows(full, a, b), len(lo))
+    nv, viol = D.sharded_conflicts(lambda a, b: rows(viol_full, a, b), len(lo))
+    nv0, none = D.sharded_conflicts(lambda a, b: rows(viol_full[:0], a, b), len(lo))
+    out_q.put((rank, pairs.tolist(), off, total, nv, viol.tolist(), nv0, none.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_sharded_pairs_and_conflicts():
+    """Row-sharded pair sweep (one allgather of counts) and validation (one
+    allreduce(sum), violators gathered only when non-zero) reproduce the
+    serial lists in the reference's (i, j) order."""
+    rng = np.random.default_rng(3)
+    E = 400
+    lo = rng.integers(1, 300, E).astype(np.int32)
+    hi = (lo + rng.integers(-3, 60, E)).astype(np.int32)
+    size = rng.integers(0, 4, E).astype(np.uint64)
+    has = (rng.random(E) > 0.2).astype(np.uint8)
+    addr = rng.integers(0, 64, E).astype(np.uint64)
+    ctx = mp_.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_sharded,
+                         args=(r, 2, port, lo, hi, size, has, addr, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(2)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "oracle"))
+    import oracle as O
+    full = O.overlap_pairs(lo, hi, size).tolist()
+    viol = O.validate_pairs(lo, hi, size, has, addr).tolist()
+    assert len(full) > 1000 and len(viol) > 10
+    (_, p0, off0, tot0, nv, v0, nv0, z0), (_, p1, off1, tot1, _, v1, _, _) = res
+    assert off0 == 0 and off1 == len(p0) and tot0 == tot1 == len(full)
+    assert p0 + p1 == full
+    assert nv == len(viol) and v0 == v1 == viol
+    assert nv0 == 0 and z0 == []

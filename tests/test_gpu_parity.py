@@ -402,6 +402,36 @@ def test_pairs_row_sharding_concatenates(planner):
     assert (np.concatenate(parts) == full).all()
 
 
+def test_sharded_pairs_and_conflicts_device(planner):
+    """dist.sharded_overlap_pairs / sharded_conflicts with the K2 / K4 device shard
+    functions: one process (no collective), and the 3-rank balanced row ranges
+    concatenated, both equal the serial lists."""
+    import torch
+    from paper_2210_12924_b200 import dist as D
+    g = mp.generate_graph("fork_join", 300, 50, 4)
+    lo, hi = planner.lifetimes_from_order(g, mp.random_topo_orders(g, 1, seed=3)[0])
+    full = planner.encode_address_pairs(g, lo, hi)
+    rng = np.random.default_rng(1)
+    has = (rng.random(g.E) > 0.1).astype(np.uint8)
+    addr = rng.integers(0, 1 << 12, g.E).astype(np.uint64)
+    viol = O.validate_pairs(lo, hi, g.edge_size, has, addr)
+    assert len(viol) > 0
+    d = torch.device("cuda:0")
+    dlo, dhi = torch.from_numpy(lo).to(d), torch.from_numpy(hi).to(d)
+    dsz = torch.from_numpy(g.edge_size.view(np.int64)).to(d)
+    dhas = torch.from_numpy(has).to(d)
+    dad = torch.from_numpy(addr.view(np.int64)).to(d)
+    pf = lambda a, b: planner.overlap_pairs_rows_d(dlo, dhi, dsz, None, a, b)   # noqa: E731
+    vf = lambda a, b: planner.conflicting_pairs_rows_d(dlo, dhi, dsz, dhas, dad, a, b)  # noqa: E731
+    pairs, off, total = D.sharded_overlap_pairs(pf, g.E, device=d)
+    assert off == 0 and total == len(full) and (pairs.cpu().numpy() == full).all()
+    nv, allv = D.sharded_conflicts(vf, g.E, device=d)
+    assert nv == len(viol) and (allv == viol).all()
+    ranges = D.balanced_row_ranges(D.triangular_row_work(g.E), 3)
+    assert (np.concatenate([pf(a, b).cpu().numpy() for a, b in ranges]) == full).all()
+    assert (np.concatenate([vf(a, b).cpu().numpy() for a, b in ranges]) == viol).all()
+
+
 def test_validation_vs_oracle_random(planner):
     g = mp.generate_graph("fork_join", 800, 1000, 5)
     o = mp.random_topo_orders(g, 1, seed=11)[0]
