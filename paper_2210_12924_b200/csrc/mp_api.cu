@@ -140,6 +140,11 @@ mp_status mp_ctx_create(int device, mp_ctx** out) {
   ctx->max_smem_optin = (size_t)optin;
   cudaError_t ce = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
   if (ce == cudaSuccess) ce = cudaMalloc(reinterpret_cast<void**>(&ctx->d_small), 256);
+  if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+  for (int i = 0; i < mp_ctx::kPipeChunks && ce == cudaSuccess; ++i)
+    ce = cudaEventCreateWithFlags(&ctx->ev_h2d[i], cudaEventDisableTiming);
+  if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming);
+  if (ce == cudaSuccess) ce = cudaMallocHost(reinterpret_cast<void**>(&ctx->h_small), 64);
   if (ce != cudaSuccess) {
     mp_status s = cuda_status(ce, "mp_ctx_create");
     delete ctx;
@@ -155,6 +160,11 @@ mp_status mp_ctx_destroy(mp_ctx* ctx) {
   DeviceGuard guard(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->d_small) cudaFree(ctx->d_small);
+  for (cudaEvent_t e : ctx->ev_h2d)
+    if (e) cudaEventDestroy(e);
+  if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
+  if (ctx->h_small) cudaFreeHost(ctx->h_small);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return MP_OK;
@@ -520,16 +530,47 @@ mp_status mp_score_orders_best(mp_ctx* ctx, const mp_graph* g, const int32_t* or
   uint64_t* d_key = cv.take<uint64_t>(3);
   const bool fused = best && C <= (int64_t{1} << 20);
   const uint64_t kNone = 0x7fffffffffffffffull, kOverflow = 0x7ffffffffffffffeull;
-  if (fused) MP_CUDA(cudaMemcpyAsync(d_key, &kNone, 8, cudaMemcpyHostToDevice, st));
-  if (n) MP_CUDA(cudaMemcpyAsync(d_orders, orders, 4 * n * c, cudaMemcpyHostToDevice, st));
-  MP_TRY(launch_score(g, d_orders, C, d_peak, d_step, d_valid, nullptr, fused ? d_key : nullptr,
-                      0, st));
-  uint64_t key = kNone;
-  if (fused) MP_CUDA(cudaMemcpyAsync(&key, d_key, 8, cudaMemcpyDeviceToHost, st));
-  MP_CUDA(cudaMemcpyAsync(peak, d_peak, 8 * c, cudaMemcpyDeviceToHost, st));
-  MP_CUDA(cudaMemcpyAsync(step, d_step, 4 * c, cudaMemcpyDeviceToHost, st));
-  MP_CUDA(cudaMemcpyAsync(valid, d_valid, c, cudaMemcpyDeviceToHost, st));
+  uint64_t* hk = ctx->h_small;  // pinned: async copies, no staging
+  hk[0] = kNone;
+  hk[1] = kNone;
+  if (fused) MP_CUDA(cudaMemcpyAsync(d_key, hk, 8, cudaMemcpyHostToDevice, st));
+  // Pipeline: the orders go up in chunks on the copy stream while the previous
+  // chunk is scored on `st`; each chunk's results come back on `st` (the other
+  // copy direction), so only the last chunk's kernel and read-back are exposed.
+  // Chunks are >= 4 MiB of orders (at most 4 by default); the per-chunk key accumulates into one
+  // first minimum (index_base = chunk offset).
+  const size_t bytes = 4 * n * c;
+  int64_t nch = (int64_t)(bytes >> 22);
+  static const int max_ch = [] {  // MP_PIPE_CHUNKS caps the chunk count (1 = no pipeline)
+    const char* e = std::getenv("MP_PIPE_CHUNKS");
+    const int v = e ? std::atoi(e) : 4;  // 2-4 measured best at C2/C3 (8 adds launch gaps)
+    return v < 1 ? 1 : v > mp_ctx::kPipeChunks ? mp_ctx::kPipeChunks : v;
+  }();
+  if (nch > max_ch) nch = max_ch;
+  if (nch > C) nch = C;
+  if (nch < 1 || n == 0) nch = 1;
+  cudaStream_t cs = nch > 1 ? ctx->copy_stream : st;
+  if (nch > 1) {  // the copy stream starts after everything already queued on `st`
+    MP_CUDA(cudaEventRecord(ctx->ev_start, st));
+    MP_CUDA(cudaStreamWaitEvent(cs, ctx->ev_start, 0));
+  }
+  for (int64_t k = 0; k < nch; ++k) {
+    const int64_t b = C * k / nch, e = C * (k + 1) / nch, m = e - b;
+    if (n) MP_CUDA(cudaMemcpyAsync(d_orders + (size_t)b * n, orders + (size_t)b * n,
+                                   4 * n * (size_t)m, cudaMemcpyHostToDevice, cs));
+    if (nch > 1) {
+      MP_CUDA(cudaEventRecord(ctx->ev_h2d[k], cs));
+      MP_CUDA(cudaStreamWaitEvent(st, ctx->ev_h2d[k], 0));
+    }
+    MP_TRY(launch_score(g, d_orders + (size_t)b * n, m, d_peak + b, d_step + b, d_valid + b,
+                        nullptr, fused ? d_key : nullptr, b, st));
+    MP_CUDA(cudaMemcpyAsync(peak + b, d_peak + b, 8 * (size_t)m, cudaMemcpyDeviceToHost, st));
+    MP_CUDA(cudaMemcpyAsync(step + b, d_step + b, 4 * (size_t)m, cudaMemcpyDeviceToHost, st));
+    MP_CUDA(cudaMemcpyAsync(valid + b, d_valid + b, (size_t)m, cudaMemcpyDeviceToHost, st));
+  }
+  if (fused) MP_CUDA(cudaMemcpyAsync(hk + 1, d_key, 8, cudaMemcpyDeviceToHost, st));
   MP_CUDA(cudaStreamSynchronize(st));
+  const uint64_t key = hk[1];
   if (best) {
     if (fused && key == kNone) {
       *best = -1;                                   // no valid candidate

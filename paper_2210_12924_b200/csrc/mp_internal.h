@@ -49,6 +49,12 @@ struct mp_ctx {
   mpb::Scratch host_pinned_dummy;
   // small device buffer for per-call flags / counters
   int64_t* d_small = nullptr;
+  // host-buffer scoring pipeline: a copy stream, per-chunk events, a pinned word pair
+  cudaStream_t copy_stream = nullptr;
+  static constexpr int kPipeChunks = 8;
+  cudaEvent_t ev_h2d[kPipeChunks] = {};
+  cudaEvent_t ev_start = nullptr;
+  uint64_t* h_small = nullptr;  // pinned: [0] key init, [1] key read-back
 };
 
 // Several contexts in one process, the graph replicated on each (mp_score_orders_multi).

@@ -478,6 +478,37 @@ def test_device_scoring_and_argmin_key(planner):
     assert int(key.item()) == int(o3[2])
 
 
+def test_host_scoring_pipeline_chunks(planner):
+    """mp_score_orders_best with >= 4 MiB of orders runs the chunked H2D/score
+    pipeline (up to 8 chunks, per-chunk index base): results and the fused
+    first-minimum equal the device-buffer path, ties across chunks included."""
+    import torch
+    g = mp.generate_graph("fork_join", 300, 300, 5)
+    C = max(64, (20 << 20) // (4 * g.n))            # ~20 MiB of orders -> 8 chunks
+    orders = mp.random_topo_orders(g, C, seed=11)
+    orders[C - 1] = orders[C // 2]                  # tie: the earlier index must win
+    orders[7, [0, 1]] = orders[7, [1, 0]]
+    res, best = planner.score_orders_best(g, orders)
+    d = torch.device("cuda:0")
+    dg = planner.upload(g)
+    peak = torch.zeros(C, dtype=torch.int64, device=d)
+    step = torch.zeros(C, dtype=torch.int32, device=d)
+    valid = torch.zeros(C, dtype=torch.uint8, device=d)
+    planner.score_orders_d(dg, torch.from_numpy(orders).to(d), C, peak, step, valid,
+                           torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert (res.peak == peak.cpu().numpy().view(np.uint64)).all()
+    assert (res.peak_step == step.cpu().numpy()).all()
+    assert (res.valid == valid.cpu().numpy()).all() and res.valid[7] == 0
+    assert best == planner.argmin(res.peak, res.valid) and best != C - 1
+    pin = torch.from_numpy(orders).pin_memory()
+    hp = torch.zeros(C, dtype=torch.int64).pin_memory()
+    hs = torch.zeros(C, dtype=torch.int32).pin_memory()
+    hv = torch.zeros(C, dtype=torch.uint8).pin_memory()
+    assert planner.score_orders_into(dg, pin.numpy(), hp, hs, hv) == best
+    assert (hp.numpy().view(np.uint64) == res.peak).all() and (hv.numpy() == res.valid).all()
+
+
 def test_edge_cases(planner):
     empty = mp.load_graph('{"nodes": [], "edges": []}')
     assert planner.peak_resident_bytes(empty, []) == 0
