@@ -272,6 +272,35 @@ def run_pairs(args, cfg):
                                                    viol_off, None, 0), reps)
     peak_gbs, _ = measured_peak_gbs()
     pair_bytes = 8 * count + 8 * E          # write the pairs + read lo/hi
+    # parity spot check of the GPU list against the C restatement (rows [0, 64))
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    got = out[:count].cpu().numpy()
+    cnt_rows, _ = O.overlap_row_stats(lo, hi, g.edge_size, rows=(0, min(64, E)))
+    k = int(cnt_rows.sum())
+    assert (got[:k] == O.overlap_pairs(lo, hi, g.edge_size)[:k]).all()
+    # the reference beside it: memplan::encode_addresses (pair loop + its rows, one
+    # thread - the reference is sequential) where it finishes in seconds (C2/C3); on
+    # bigger graphs the C restatement of the pair predicate loop on a row subset
+    cpu = None
+    if E <= 4096 and O.ref_available():
+        rg = O.RefGraph.load(mp.save_graph(g))
+        t0 = time.perf_counter()
+        ref_count = rg.encode_address_pairs(lo, hi, want_pairs=False)
+        t_ref = time.perf_counter() - t0
+        assert ref_count == count
+        cpu = {"value": count / t_ref, "unit": "pairs/s", "cores": 1, "kind": "reference",
+               "sample": f"memplan::encode_addresses over all {E} edges ({count} pairs, "
+                         "model rows included), oracle/_ref -O3, 1 thread"}
+    else:
+        r1 = max(1, E // 16)
+        t0 = time.perf_counter()
+        sub, _ = O.overlap_row_stats(lo, hi, g.edge_size, rows=(0, r1))
+        t_port = time.perf_counter() - t0
+        cpu = {"value": float(sub.sum()) / t_port, "unit": "pairs/s", "cores": 1,
+               "kind": "port",
+               "sample": f"C restatement of the encode.cpp:347-357 predicate loop (count only) "
+                         f"over rows [0, {r1}) of {E} ({int(sub.sum())} pairs), 1 thread"}
     line = {
         "metric": "overlap pairs generated/sec (count+scan+fill) and pair checks/sec (validation)",
         "value": count / t_pairs, "unit": "pairs/s", "n_gpus": 1, "steps": reps,
@@ -285,6 +314,7 @@ def run_pairs(args, cfg):
                      "unit": "GB/s", "frac": pair_bytes / t_pairs / 1e9 / peak_gbs,
                      "traffic": None, "kernel": "pair_sweep_kernel count+fill (host-synced)"},
         "timing": "wall clock around stream-synchronous API calls (includes the count readback)",
+        "cpu_baseline": cpu,
     }
     print(json.dumps(line))
     planner.close()
