@@ -35,7 +35,7 @@ constexpr uint8_t kOverflow = 2;  // valid[] marker: replay again with the full 
 // IT: the index type of pos / fstart / flist / block edges - 16-bit when n and E
 // are below 65535 (half the state, twice the candidates per SM), else 32-bit.
 struct ArenaLayout {
-  int n, E, cap, ib;  // ib = sizeof(IT)
+  int n, E, cap, ib, sb;  // ib = sizeof(IT), sb = sizeof(ST) (block sizes)
   __host__ __device__ size_t fstart_off() const { return 0; }
   __host__ __device__ size_t flist_off() const {
     return align(fstart_off() + ib * ((size_t)n + 3));
@@ -43,7 +43,7 @@ struct ArenaLayout {
   // pos [n] and the block list (size [cap], edge [cap]) share this region
   __host__ __device__ size_t pos_off() const { return align(flist_off() + ib * (size_t)E); }
   __host__ __device__ size_t bsize_off() const { return pos_off(); }
-  __host__ __device__ size_t bedge_off() const { return align(bsize_off() + 8 * (size_t)cap); }
+  __host__ __device__ size_t bedge_off() const { return align(bsize_off() + sb * (size_t)cap); }
   __host__ __device__ size_t bytes() const {
     const size_t blocks = align(bedge_off() + ib * (size_t)cap);
     const size_t p = align(pos_off() + ib * (size_t)n);
@@ -73,20 +73,29 @@ __device__ __forceinline__ void count1(uint16_t* p, int t) {
   atomicAdd(reinterpret_cast<unsigned*>(at & ~uintptr_t(3)), 1u << ((at & 2) * 8));
 }
 
-template <typename IT>
+// ST: the block-size type - 32-bit sizes in units of the graph's gcd when the
+// scaled total fits (mp_graph::narrow), which shrinks the block list by a third
+// and raises the resident warps per SM; 64-bit byte sizes otherwise.
+template <typename ST>
+__device__ __forceinline__ ST size_of(const ArenaArgs& a, int e) {
+  if constexpr (sizeof(ST) == 4) return __ldg(a.edge_size32 + e);
+  else return __ldg(a.edge_size + e);
+}
+
+template <typename IT, typename ST>
 __global__ void __launch_bounds__(32 * kArenaWarps)
     arena_kernel(ArenaArgs a) {
   extern __shared__ __align__(16) char smem[];
   const int n = a.n, E = a.E;
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
-  const ArenaLayout Lo{n, E, a.cap, (int)sizeof(IT)};
+  const ArenaLayout Lo{n, E, a.cap, (int)sizeof(IT), (int)sizeof(ST)};
   constexpr IT kFree = (IT)-1;  // block edge of a free block
   char* base = smem + (size_t)wid * Lo.bytes();
   IT* pos = reinterpret_cast<IT*>(base + Lo.pos_off());
   IT* fstart = reinterpret_cast<IT*>(base + Lo.fstart_off());
   IT* flist = reinterpret_cast<IT*>(base + Lo.flist_off());
-  unsigned long long* bsz = reinterpret_cast<unsigned long long*>(base + Lo.bsize_off());
+  ST* bsz = reinterpret_cast<ST*>(base + Lo.bsize_off());
   IT* bed = reinterpret_cast<IT*>(base + Lo.bedge_off());
 
   for (int64_t c = (int64_t)blockIdx.x * kArenaWarps + wid; c < a.num_orders;
@@ -186,7 +195,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
               __ballot_sync(0xffffffffu, i0 + lane < nb && (int)bed[i0 + lane] == e);
           if (m) b = i0 + __ffs(m) - 1;
         }
-        live -= a.edge_size[e];
+        live -= size_of<ST>(a, e);
         if (b < 0) continue;
         __syncwarp();
         if (lane == 0) bed[b] = kFree;
@@ -200,7 +209,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
         if (erase >= 0) {  // shift [erase + 1, nb) left by one
           for (int i0 = erase + 1; i0 < nb; i0 += 32) {
             const int i = i0 + lane;
-            unsigned long long sz = 0;
+            ST sz = 0;
             IT ed = 0;
             if (i < nb) {
               sz = bsz[i];
@@ -220,7 +229,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
           __syncwarp();
           for (int i0 = b + 1; i0 < nb; i0 += 32) {
             const int i = i0 + lane;
-            unsigned long long sz = 0;
+            ST sz = 0;
             IT ed = 0;
             if (i < nb) {
               sz = bsz[i];
@@ -241,7 +250,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
       const int o0 = a.out_off[v], o1 = a.out_off[v + 1];
       for (int q = o0; q < o1; ++q) {  // fanout(v) in edge order
         const int e = a.out_edges[q];
-        const unsigned long long s = a.edge_size[e];
+        const unsigned long long s = size_of<ST>(a, e);
         if (s == 0) continue;
         // Arena::allocate (placement.cpp:80-101): first fit, or the smallest fit
         int pick = -1;
@@ -279,7 +288,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
             const unsigned long long old = bsz[nb - 1];
             __syncwarp();
             if (lane == 0) {
-              bsz[nb - 1] = s;
+              bsz[nb - 1] = (ST)s;
               bed[nb - 1] = e;
             }
             top = top - old + s;
@@ -289,7 +298,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
               break;
             }
             if (lane == 0) {
-              bsz[nb] = s;
+              bsz[nb] = (ST)s;
               bed[nb] = e;
             }
             ++nb;
@@ -306,7 +315,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
             for (int i0 = ((nb - 1 - (pick + 1)) / 32) * 32 + pick + 1; i0 >= pick + 1;
                  i0 -= 32) {
               const int i = i0 + lane;
-              unsigned long long sz = 0;
+              ST sz = 0;
               IT ed = 0;
               if (i < nb) {
                 sz = bsz[i];
@@ -320,13 +329,13 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
               __syncwarp();
             }
             if (lane == 0) {
-              bsz[pick + 1] = bsize - s;
+              bsz[pick + 1] = (ST)(bsize - s);
               bed[pick + 1] = kFree;
             }
             ++nb;
           }
           if (lane == 0) {
-            bsz[pick] = s;
+            bsz[pick] = (ST)s;
             bed[pick] = e;
           }
         }
@@ -338,6 +347,8 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
         }
       }
     }
+    mr *= a.scale;  // back to bytes (scale = 1 for 64-bit sizes)
+    rs *= a.scale;
     if (lane == 0) {
       a.mr_peak[c] = overflow ? 0 : mr;
       a.rs_at_peak[c] = overflow ? 0 : rs;
@@ -352,15 +363,15 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
 
 static bool arena_narrow(int n, int E) { return n < 65535 && 2 * E + 2 < 65535; }
 
-size_t arena_smem_bytes(int n, int E, int cap) {
+size_t arena_smem_bytes(int n, int E, int cap, int sb) {
   const bool narrow = arena_narrow(n, E) && !std::getenv("MP_ARENA_WIDE");
-  return ArenaLayout{n, E, cap, narrow ? 2 : 4}.bytes() * kArenaWarps;
+  return ArenaLayout{n, E, cap, narrow ? 2 : 4, sb}.bytes() * kArenaWarps;
 }
 
-template <typename IT>
+template <typename IT, typename ST>
 mp_status launch_arena_t(const ArenaArgs& in, const mp_ctx* ctx, cudaStream_t st) {
-  const size_t smem = arena_smem_bytes(in.n, in.E, in.cap);
-  auto kern = arena_kernel<IT>;
+  const size_t smem = arena_smem_bytes(in.n, in.E, in.cap, (int)sizeof(ST));
+  auto kern = arena_kernel<IT, ST>;
   MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kArenaWarps, smem));
@@ -373,9 +384,12 @@ mp_status launch_arena_t(const ArenaArgs& in, const mp_ctx* ctx, cudaStream_t st
 }
 
 mp_status launch_arena_pass(const ArenaArgs& in, const mp_ctx* ctx, cudaStream_t st) {
+  const bool s32 = in.edge_size32 != nullptr;
   if (arena_narrow(in.n, in.E) && !std::getenv("MP_ARENA_WIDE"))
-    return launch_arena_t<uint16_t>(in, ctx, st);
-  return launch_arena_t<int>(in, ctx, st);
+    return s32 ? launch_arena_t<uint16_t, uint32_t>(in, ctx, st)
+               : launch_arena_t<uint16_t, unsigned long long>(in, ctx, st);
+  return s32 ? launch_arena_t<int, uint32_t>(in, ctx, st)
+             : launch_arena_t<int, unsigned long long>(in, ctx, st);
 }
 
 mp_status launch_arena(const ArenaArgs& in, const mp_ctx* ctx, cudaStream_t st) {

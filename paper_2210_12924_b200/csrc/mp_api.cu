@@ -283,6 +283,12 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
         s4[4 * (size_t)d + (k - P.dyn_off[d])] = P.dyn_sinks[k];
     up(upload(&g->d_dyn_sink4, s4.data(), s4.size(), st));
   }
+  std::vector<uint32_t> size32;
+  if (g->narrow) {
+    size32.resize((size_t)E);
+    for (int32_t e = 0; e < E; ++e) size32[e] = (uint32_t)(g->h_edge_size[e] / g->scale);
+    up(upload(&g->d_edge_size32, size32.data(), size32.size(), st));
+  }
   up(upload(&g->d_out_off, P.out_off.data(), P.out_off.size(), st));
   up(upload(&g->d_out_edges, P.out_edges.data(), P.out_edges.size(), st));
   if (s == MP_OK) up(score_configure(g));
@@ -306,7 +312,7 @@ mp_status mp_graph_free(mp_graph* g) {
                   g->d_extra_w,  g->d_dyn_off,   g->d_dyn_sinks, g->d_dyn_size,
                   g->d_node_rec32, g->d_node_u2, g->d_extra3_packed,
                   g->d_out_off,  g->d_out_edges, g->d_dyn_sink4, g->d_joint_mul,
-                  g->d_joint_ar, g->d_joint_art};
+                  g->d_joint_ar, g->d_joint_art, g->d_edge_size32};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete g;
@@ -1191,6 +1197,8 @@ mp_status mp_run_baseline_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_ord
   a.sink_off = g->d_sink_off;
   a.sinks = g->d_sinks;
   a.edge_size = g->d_edge_size;
+  a.edge_size32 = std::getenv("MP_ARENA_WIDE_SIZE") ? nullptr : g->d_edge_size32;
+  a.scale = a.edge_size32 ? g->scale : 1;  // 64-bit block sizes are bytes
   a.out_off = g->d_out_off;
   a.out_edges = g->d_out_edges;
   a.best_fit = best_fit ? 1 : 0;

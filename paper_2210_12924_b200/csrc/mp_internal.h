@@ -81,6 +81,7 @@ struct mp_graph {
   int64_t* d_sink_off = nullptr;
   int32_t* d_sinks = nullptr;
   uint64_t* d_edge_size = nullptr;
+  uint32_t* d_edge_size32 = nullptr;  // size / scale when `narrow` (the arena's 32-bit blocks)
 
   // node space, derived by mp_prep.cpp (scaled by `scale`)
   int64_t n_preds = 0;               // reduced validity edges (first + extra)
@@ -243,6 +244,8 @@ struct ArenaArgs {
   const int64_t* sink_off = nullptr;
   const int32_t* sinks = nullptr;
   const uint64_t* edge_size = nullptr;
+  const uint32_t* edge_size32 = nullptr;  // size / scale (null: 64-bit block sizes)
+  uint64_t scale = 1;
   const int32_t* out_off = nullptr;    // fanout lists
   const int32_t* out_edges = nullptr;
   int best_fit = 0;
@@ -252,7 +255,7 @@ struct ArenaArgs {
   uint8_t* valid = nullptr;            // [B]
 };
 constexpr int kArenaCap = 1024;       // first-pass block-list capacity
-size_t arena_smem_bytes(int n, int E, int cap);
+size_t arena_smem_bytes(int n, int E, int cap, int size_bytes = 8);
 mp_status launch_arena(const ArenaArgs& a, const mp_ctx* ctx, cudaStream_t st);
 mp_status launch_peak_mem(int32_t num_edges, const uint64_t* d_size, const uint8_t* d_has,
                           const uint64_t* d_addr, uint64_t* d_out, cudaStream_t st);

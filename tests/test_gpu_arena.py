@@ -49,15 +49,19 @@ def test_golden_run_baseline(golden, planner):
 
 @pytest.mark.parametrize("name,cap,wide", [("resnet50_b32", "", 0), ("bert_base_s512", "", 0),
                                            ("gpt2_medium_s1024", "", 0), ("resnet50_b32", "6", 0),
-                                           ("bert_base_s512", "", 1)])
+                                           ("bert_base_s512", "", 1), ("resnet50_b32", "", 2),
+                                           ("bert_base_s512", "6", 2)])
 def test_batched_run_baseline_model_graphs(planner, monkeypatch, name, cap, wide):
     """Every candidate vs the C restatement (and the reference on a few); with
     MP_ARENA_CAP=6 every block list overflows the first pass and is replayed by
-    the full-capacity second pass; MP_ARENA_WIDE forces 32-bit indexes."""
+    the full-capacity second pass; MP_ARENA_WIDE forces 32-bit indexes and
+    MP_ARENA_WIDE_SIZE 64-bit byte block sizes (default: 32-bit gcd units)."""
     if cap:
         monkeypatch.setenv("MP_ARENA_CAP", cap)
-    if wide:
+    if wide == 1:
         monkeypatch.setenv("MP_ARENA_WIDE", "1")
+    if wide == 2:
+        monkeypatch.setenv("MP_ARENA_WIDE_SIZE", "1")
     with gzip.open(os.path.join(ROOT, "workloads", "graphs", name + ".json.gz"), "rt") as f:
         g = mp.load_graph(f.read())
     orders = np.concatenate([g.program_order()[None], mp.random_topo_orders(g, 40, seed=8)])
@@ -75,3 +79,25 @@ def test_batched_run_baseline_model_graphs(planner, monkeypatch, name, cap, wide
             assert valid[i] == 1 and (int(mr[i]), int(rs[i]), float(fr[i])) == exp, (name, bf, i)
             if rg is not None and i < 3:
                 assert rg.run_baseline(o, best_fit=bf) == exp
+
+
+def test_batched_run_baseline_unscalable_sizes(planner):
+    """Sizes with gcd 1 and a total past 2^32: the 64-bit block-size path, and
+    fragmentation from byte values above 2^53 (rounded exactly as the reference)."""
+    import json
+    rng = np.random.default_rng(4)
+    nodes = [{"id": f"v{i}"} for i in range(60)]
+    edges = []
+    for i in range(1, 60):
+        for j in rng.choice(i, size=min(i, 2), replace=False):
+            edges.append({"id": f"e{len(edges)}", "source": f"v{j}", "sinks": [f"v{i}"],
+                          "size": int(rng.integers(1, 1 << 55)) | 1})
+    g = mp.load_graph(json.dumps({"nodes": nodes, "edges": edges}))
+    assert g.edge_size.sum(dtype=object) > (1 << 32)
+    orders = mp.random_topo_orders(g, 64, seed=2)
+    orc = O.Oracle.from_csr(g.csr())
+    for bf in (False, True):
+        mr, rs, fr, valid = planner.run_baseline_batch(g, orders, best_fit=bf)
+        for i, o in enumerate(orders):
+            assert valid[i] == 1
+            assert (int(mr[i]), int(rs[i]), float(fr[i])) == orc.run_baseline(o, best_fit=bf), i
