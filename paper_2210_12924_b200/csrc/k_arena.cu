@@ -7,6 +7,10 @@
 //   pos[n]            1-based position of each node (order validity, lifetimes)
 //   fstart[n+3]       frees bucketed by timestep (hi + 1), stable in edge order,
 //   flist[E]          as placement.cpp:155-158 builds them
+//   blk[E]            (kBlk) the block index of each allocated edge, kept current
+//                     through every shift, so Arena::release finds its block in O(1)
+//                     instead of a ballot search; used when its 2E bytes do not cost
+//                     a round of resident candidates (launch_arena_t)
 //   blocks[cap]       the arena: (size, edge or -1 when free), address-sorted and
 //                     contiguous, so addresses are implicit and top() is a sum
 // The block list gets kArenaCap entries first (the live-block count is far
@@ -35,13 +39,14 @@ constexpr uint8_t kOverflow = 2;  // valid[] marker: replay again with the full 
 // IT: the index type of pos / fstart / flist / block edges - 16-bit when n and E
 // are below 65535 (half the state, twice the candidates per SM), else 32-bit.
 struct ArenaLayout {
-  int n, E, cap, ib, sb;  // ib = sizeof(IT), sb = sizeof(ST) (block sizes)
+  int n, E, cap, ib, sb, bk;  // ib = sizeof(IT), sb = sizeof(ST) (block sizes), bk = kBlk
   __host__ __device__ size_t fstart_off() const { return 0; }
   __host__ __device__ size_t flist_off() const {
     return align(fstart_off() + ib * ((size_t)n + 3));
   }
+  __host__ __device__ size_t blk_off() const { return align(flist_off() + ib * (size_t)E); }
   // pos [n] and the block list (size [cap], edge [cap]) share this region
-  __host__ __device__ size_t pos_off() const { return align(flist_off() + ib * (size_t)E); }
+  __host__ __device__ size_t pos_off() const { return align(blk_off() + bk * ib * (size_t)E); }
   __host__ __device__ size_t bsize_off() const { return pos_off(); }
   __host__ __device__ size_t bedge_off() const { return align(bsize_off() + sb * (size_t)cap); }
   __host__ __device__ size_t bytes() const {
@@ -82,19 +87,20 @@ __device__ __forceinline__ ST size_of(const ArenaArgs& a, int e) {
   else return __ldg(a.edge_size + e);
 }
 
-template <typename IT, typename ST>
+template <typename IT, typename ST, bool kBlk>
 __global__ void __launch_bounds__(32 * kArenaWarps)
     arena_kernel(ArenaArgs a) {
   extern __shared__ __align__(16) char smem[];
   const int n = a.n, E = a.E;
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
-  const ArenaLayout Lo{n, E, a.cap, (int)sizeof(IT), (int)sizeof(ST)};
+  const ArenaLayout Lo{n, E, a.cap, (int)sizeof(IT), (int)sizeof(ST), kBlk ? 1 : 0};
   constexpr IT kFree = (IT)-1;  // block edge of a free block
   char* base = smem + (size_t)wid * Lo.bytes();
   IT* pos = reinterpret_cast<IT*>(base + Lo.pos_off());
   IT* fstart = reinterpret_cast<IT*>(base + Lo.fstart_off());
   IT* flist = reinterpret_cast<IT*>(base + Lo.flist_off());
+  IT* blk = reinterpret_cast<IT*>(base + Lo.blk_off());
   ST* bsz = reinterpret_cast<ST*>(base + Lo.bsize_off());
   IT* bed = reinterpret_cast<IT*>(base + Lo.bedge_off());
 
@@ -190,10 +196,15 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
       for (int q = f0; q < f1; ++q) {  // Arena::release (placement.cpp:103-111)
         const int e = flist[q];
         int b = -1;
-        for (int i0 = 0; i0 < nb && b < 0; i0 += 32) {
-          const unsigned m =
-              __ballot_sync(0xffffffffu, i0 + lane < nb && (int)bed[i0 + lane] == e);
-          if (m) b = i0 + __ffs(m) - 1;
+        if constexpr (kBlk) {
+          b = (int)blk[e];
+          if (b < 0 || b >= nb || (int)bed[b] != e) b = -1;  // stale: never allocated
+        } else {
+          for (int i0 = 0; i0 < nb && b < 0; i0 += 32) {
+            const unsigned m =
+                __ballot_sync(0xffffffffu, i0 + lane < nb && (int)bed[i0 + lane] == e);
+            if (m) b = i0 + __ffs(m) - 1;
+          }
         }
         live -= size_of<ST>(a, e);
         if (b < 0) continue;
@@ -219,6 +230,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
             if (i < nb) {
               bsz[i - 1] = sz;
               bed[i - 1] = ed;
+              if (kBlk && ed != kFree) blk[ed] = (IT)(i - 1);
             }
             __syncwarp();
           }
@@ -239,6 +251,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
             if (i < nb) {
               bsz[i - 1] = sz;
               bed[i - 1] = ed;
+              if (kBlk && ed != kFree) blk[ed] = (IT)(i - 1);
             }
             __syncwarp();
           }
@@ -290,6 +303,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
             if (lane == 0) {
               bsz[nb - 1] = (ST)s;
               bed[nb - 1] = e;
+              if (kBlk) blk[e] = (IT)(nb - 1);
             }
             top = top - old + s;
           } else {
@@ -300,6 +314,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
             if (lane == 0) {
               bsz[nb] = (ST)s;
               bed[nb] = e;
+              if (kBlk) blk[e] = (IT)nb;
             }
             ++nb;
             top += s;
@@ -325,6 +340,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
               if (i < nb) {
                 bsz[i + 1] = sz;
                 bed[i + 1] = ed;
+                if (kBlk && ed != kFree) blk[ed] = (IT)(i + 1);
               }
               __syncwarp();
             }
@@ -337,6 +353,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
           if (lane == 0) {
             bsz[pick] = (ST)s;
             bed[pick] = e;
+            if (kBlk) blk[e] = (IT)pick;
           }
         }
         __syncwarp();
@@ -363,22 +380,51 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
 
 static bool arena_narrow(int n, int E) { return n < 65535 && 2 * E + 2 < 65535; }
 
-size_t arena_smem_bytes(int n, int E, int cap, int sb) {
+size_t arena_smem_bytes(int n, int E, int cap, int sb, int bk) {
   const bool narrow = arena_narrow(n, E) && !std::getenv("MP_ARENA_WIDE");
-  return ArenaLayout{n, E, cap, narrow ? 2 : 4, sb}.bytes() * kArenaWarps;
+  return ArenaLayout{n, E, cap, narrow ? 2 : 4, sb, bk}.bytes() * kArenaWarps;
+}
+
+template <typename IT, typename ST, bool kBlk>
+int arena_per_sm(const ArenaArgs& in, size_t* smem) {
+  *smem = arena_smem_bytes(in.n, in.E, in.cap, (int)sizeof(ST), kBlk ? 1 : 0);
+  auto kern = arena_kernel<IT, ST, kBlk>;
+  int per_sm = 0;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem) !=
+          cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kArenaWarps, *smem) !=
+          cudaSuccess) {
+    (void)cudaGetLastError();  // too big for shared memory: not an error, just not usable
+    return 0;
+  }
+  return per_sm;
 }
 
 template <typename IT, typename ST>
 mp_status launch_arena_t(const ArenaArgs& in, const mp_ctx* ctx, cudaStream_t st) {
-  const size_t smem = arena_smem_bytes(in.n, in.E, in.cap, (int)sizeof(ST));
-  auto kern = arena_kernel<IT, ST>;
-  MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kArenaWarps, smem));
+  // The edge -> block index (kBlk) removes the release search (~20% of the replay's
+  // instructions) but adds 2E bytes per candidate: use it unless the lost resident
+  // candidates cost more than that, i.e. it adds more than ~20% rounds.
+  size_t smem0 = 0, smem1 = 0;
+  const int occ0 = arena_per_sm<IT, ST, false>(in, &smem0);
+  const int occ1 = arena_per_sm<IT, ST, true>(in, &smem1);
+  const int64_t per_sm_work =
+      (in.num_orders + (int64_t)ctx->num_sms * kArenaWarps - 1) / ((int64_t)ctx->num_sms * kArenaWarps);
+  auto rounds = [&](int occ) { return occ > 0 ? (per_sm_work + occ - 1) / occ : INT64_MAX; };
+  bool blk = occ1 > 0 && 5 * rounds(occ1) <= 6 * rounds(occ0);
+  if (const char* e = std::getenv("MP_ARENA_BLK")) blk = std::atoi(e) != 0 && occ1 > 0;
+  const int per_sm = blk ? occ1 : occ0;
+  if (per_sm <= 0) {
+    set_error("Capacity: run_baseline state exceeds shared memory");
+    return MP_E_CAPACITY;
+  }
   int64_t grid = (int64_t)ctx->num_sms * (per_sm > 0 ? per_sm : 1);
   const int64_t need = (in.num_orders + kArenaWarps - 1) / kArenaWarps;
   if (grid > need) grid = need;
-  kern<<<(unsigned)grid, 32 * kArenaWarps, smem, st>>>(in);
+  if (blk)
+    arena_kernel<IT, ST, true><<<(unsigned)grid, 32 * kArenaWarps, smem1, st>>>(in);
+  else
+    arena_kernel<IT, ST, false><<<(unsigned)grid, 32 * kArenaWarps, smem0, st>>>(in);
   MP_CUDA(cudaGetLastError());
   return MP_OK;
 }

@@ -1185,7 +1185,7 @@ mp_status mp_run_baseline_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_ord
   ArenaArgs a;
   a.n = g->n;
   a.E = g->E;
-  if (arena_smem_bytes(g->n, g->E, 2 * g->E + 2) > (size_t)ctx->max_smem_optin) {
+  if (arena_smem_bytes(g->n, g->E, 2 * g->E + 2, 8, 0) > (size_t)ctx->max_smem_optin) {
     set_error("Capacity: run_baseline state for " + std::to_string(g->n) + " nodes / " +
               std::to_string(g->E) + " edges exceeds shared memory");
     return MP_E_CAPACITY;

@@ -255,7 +255,7 @@ struct ArenaArgs {
   uint8_t* valid = nullptr;            // [B]
 };
 constexpr int kArenaCap = 1024;       // first-pass block-list capacity
-size_t arena_smem_bytes(int n, int E, int cap, int size_bytes = 8);
+size_t arena_smem_bytes(int n, int E, int cap, int size_bytes = 8, int edge_index = 1);
 mp_status launch_arena(const ArenaArgs& a, const mp_ctx* ctx, cudaStream_t st);
 mp_status launch_peak_mem(int32_t num_edges, const uint64_t* d_size, const uint8_t* d_has,
                           const uint64_t* d_addr, uint64_t* d_out, cudaStream_t st);

@@ -50,18 +50,22 @@ def test_golden_run_baseline(golden, planner):
 @pytest.mark.parametrize("name,cap,wide", [("resnet50_b32", "", 0), ("bert_base_s512", "", 0),
                                            ("gpt2_medium_s1024", "", 0), ("resnet50_b32", "6", 0),
                                            ("bert_base_s512", "", 1), ("resnet50_b32", "", 2),
-                                           ("bert_base_s512", "6", 2)])
+                                           ("bert_base_s512", "6", 2), ("resnet50_b32", "", 3),
+                                           ("gpt2_medium_s1024", "6", 4)])
 def test_batched_run_baseline_model_graphs(planner, monkeypatch, name, cap, wide):
     """Every candidate vs the C restatement (and the reference on a few); with
     MP_ARENA_CAP=6 every block list overflows the first pass and is replayed by
     the full-capacity second pass; MP_ARENA_WIDE forces 32-bit indexes and
-    MP_ARENA_WIDE_SIZE 64-bit byte block sizes (default: 32-bit gcd units)."""
+    MP_ARENA_WIDE_SIZE 64-bit byte block sizes (default: 32-bit gcd units);
+    MP_ARENA_BLK forces the release search (0) or the edge -> block index (1)."""
     if cap:
         monkeypatch.setenv("MP_ARENA_CAP", cap)
     if wide == 1:
         monkeypatch.setenv("MP_ARENA_WIDE", "1")
     if wide == 2:
         monkeypatch.setenv("MP_ARENA_WIDE_SIZE", "1")
+    if wide in (3, 4):   # the edge -> block index off / on regardless of occupancy
+        monkeypatch.setenv("MP_ARENA_BLK", str(wide - 3))
     with gzip.open(os.path.join(ROOT, "workloads", "graphs", name + ".json.gz"), "rt") as f:
         g = mp.load_graph(f.read())
     orders = np.concatenate([g.program_order()[None], mp.random_topo_orders(g, 40, seed=8)])
