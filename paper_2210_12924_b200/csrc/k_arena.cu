@@ -48,9 +48,12 @@ struct ArenaLayout {
   // pos [n] and the block list (size [cap], edge [cap]) share this region
   __host__ __device__ size_t pos_off() const { return align(blk_off() + bk * ib * (size_t)E); }
   __host__ __device__ size_t bsize_off() const { return pos_off(); }
-  __host__ __device__ size_t bedge_off() const { return align(bsize_off() + sb * (size_t)cap); }
+  __host__ __device__ size_t bedge_off() const {
+    return align(bsize_off() + sb * (size_t)cap4());
+  }
+  __host__ __device__ size_t cap4() const { return ((size_t)cap + 3) & ~size_t(3); }
   __host__ __device__ size_t bytes() const {
-    const size_t blocks = align(bedge_off() + ib * (size_t)cap);
+    const size_t blocks = align(bedge_off() + ib * cap4());
     const size_t p = align(pos_off() + ib * (size_t)n);
     return blocks > p ? blocks : p;
   }
@@ -87,9 +90,37 @@ __device__ __forceinline__ ST size_of(const ArenaArgs& a, int e) {
   else return __ldg(a.edge_size + e);
 }
 
+// Fit mask of blocks [i, i + 4) (bit k: block i + k is free, below nb, and holds
+// s), for 16-bit edges and 32-bit sizes: i is a multiple of 4, so the loads are
+// aligned; entries at or past nb are masked (the list storage is padded to 4).
+__device__ __forceinline__ unsigned fit4(const uint32_t* bsz, const uint16_t* bed, int i, int nb,
+                                         uint32_t s) {
+  const uint4 z = *reinterpret_cast<const uint4*>(bsz + i);
+  const uint2 e = *reinterpret_cast<const uint2*>(bed + i);
+  unsigned f = 0;
+  f |= ((e.x & 0xffffu) == 0xffffu && z.x >= s) ? 1u : 0u;
+  f |= ((e.x >> 16) == 0xffffu && z.y >= s) ? 2u : 0u;
+  f |= ((e.y & 0xffffu) == 0xffffu && z.z >= s) ? 4u : 0u;
+  f |= ((e.y >> 16) == 0xffffu && z.w >= s) ? 8u : 0u;
+  const int left = nb - i;
+  return left >= 4 ? f : f & ((1u << left) - 1u);
+}
+__device__ __forceinline__ unsigned fit4(const unsigned long long*, const int*, int, int,
+                                         uint32_t) {
+  return 0;  // 64-bit sizes / 32-bit edges use the scalar scan
+}
+__device__ __forceinline__ unsigned fit4(const unsigned long long*, const uint16_t*, int, int,
+                                         uint32_t) {
+  return 0;
+}
+__device__ __forceinline__ unsigned fit4(const uint32_t*, const int*, int, int, uint32_t) {
+  return 0;
+}
+
 template <typename IT, typename ST, bool kBlk>
 __global__ void __launch_bounds__(32 * kArenaWarps)
     arena_kernel(ArenaArgs a) {
+  constexpr bool kVec4 = sizeof(IT) == 2 && sizeof(ST) == 4;
   extern __shared__ __align__(16) char smem[];
   const int n = a.n, E = a.E;
   const int lane = threadIdx.x & 31;
@@ -267,7 +298,20 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
         if (s == 0) continue;
         // Arena::allocate (placement.cpp:80-101): first fit, or the smallest fit
         int pick = -1;
-        if (!a.best_fit) {
+        if (!a.best_fit && kVec4) {
+          // 4 blocks per lane (one 16-byte size load + one 8-byte edge load): a
+          // 128-block window per ballot; the first lane with a fit, then its first
+          for (int i0 = 0; i0 < nb && pick < 0; i0 += 128) {
+            const int i = i0 + 4 * lane;
+            const unsigned f = i < nb ? fit4(bsz, bed, i, nb, (uint32_t)s) : 0u;
+            const unsigned m = __ballot_sync(0xffffffffu, f != 0);
+            if (m) {
+              const int src = __ffs(m) - 1;
+              const unsigned fs = __shfl_sync(0xffffffffu, f, src);
+              pick = i0 + 4 * src + __ffs(fs) - 1;
+            }
+          }
+        } else if (!a.best_fit) {
           for (int i0 = 0; i0 < nb && pick < 0; i0 += 32) {
             const int i = i0 + lane;
             const unsigned m =
