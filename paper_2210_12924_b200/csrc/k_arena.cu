@@ -91,8 +91,9 @@ __device__ __forceinline__ ST size_of(const ArenaArgs& a, int e) {
 }
 
 // Fit mask of blocks [i, i + 4) (bit k: block i + k is free, below nb, and holds
-// s), for 16-bit edges and 32-bit sizes: i is a multiple of 4, so the loads are
-// aligned; entries at or past nb are masked (the list storage is padded to 4).
+// s), for 16-bit edges: i is a multiple of 4, so the loads are aligned (16-byte
+// size loads, one 8-byte edge load); entries at or past nb are masked (the list
+// storage is padded to 4).
 __device__ __forceinline__ unsigned fit4(const uint32_t* bsz, const uint16_t* bed, int i, int nb,
                                          uint32_t s) {
   const uint4 z = *reinterpret_cast<const uint4*>(bsz + i);
@@ -106,12 +107,21 @@ __device__ __forceinline__ unsigned fit4(const uint32_t* bsz, const uint16_t* be
   return left >= 4 ? f : f & ((1u << left) - 1u);
 }
 __device__ __forceinline__ unsigned fit4(const unsigned long long*, const int*, int, int,
-                                         uint32_t) {
+                                         unsigned long long) {
   return 0;  // 64-bit sizes / 32-bit edges use the scalar scan
 }
-__device__ __forceinline__ unsigned fit4(const unsigned long long*, const uint16_t*, int, int,
-                                         uint32_t) {
-  return 0;
+__device__ __forceinline__ unsigned fit4(const unsigned long long* bsz, const uint16_t* bed,
+                                         int i, int nb, unsigned long long s) {
+  const ulonglong2 z0 = *reinterpret_cast<const ulonglong2*>(bsz + i);
+  const ulonglong2 z1 = *reinterpret_cast<const ulonglong2*>(bsz + i + 2);
+  const uint2 e = *reinterpret_cast<const uint2*>(bed + i);
+  unsigned f = 0;
+  f |= ((e.x & 0xffffu) == 0xffffu && z0.x >= s) ? 1u : 0u;
+  f |= ((e.x >> 16) == 0xffffu && z0.y >= s) ? 2u : 0u;
+  f |= ((e.y & 0xffffu) == 0xffffu && z1.x >= s) ? 4u : 0u;
+  f |= ((e.y >> 16) == 0xffffu && z1.y >= s) ? 8u : 0u;
+  const int left = nb - i;
+  return left >= 4 ? f : f & ((1u << left) - 1u);
 }
 __device__ __forceinline__ unsigned fit4(const uint32_t*, const int*, int, int, uint32_t) {
   return 0;
@@ -120,7 +130,7 @@ __device__ __forceinline__ unsigned fit4(const uint32_t*, const int*, int, int, 
 template <typename IT, typename ST, bool kBlk>
 __global__ void __launch_bounds__(32 * kArenaWarps)
     arena_kernel(ArenaArgs a) {
-  constexpr bool kVec4 = sizeof(IT) == 2 && sizeof(ST) == 4;
+  constexpr bool kVec4 = sizeof(IT) == 2;  // 16-bit edges; 32- or 64-bit sizes
   extern __shared__ __align__(16) char smem[];
   const int n = a.n, E = a.E;
   const int lane = threadIdx.x & 31;
@@ -303,7 +313,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
           // 128-block window per ballot; the first lane with a fit, then its first
           for (int i0 = 0; i0 < nb && pick < 0; i0 += 128) {
             const int i = i0 + 4 * lane;
-            const unsigned f = i < nb ? fit4(bsz, bed, i, nb, (uint32_t)s) : 0u;
+            const unsigned f = i < nb ? fit4(bsz, bed, i, nb, (ST)s) : 0u;
             const unsigned m = __ballot_sync(0xffffffffu, f != 0);
             if (m) {
               const int src = __ffs(m) - 1;
