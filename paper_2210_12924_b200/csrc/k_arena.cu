@@ -240,6 +240,22 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
         if constexpr (kBlk) {
           b = (int)blk[e];
           if (b < 0 || b >= nb || (int)bed[b] != e) b = -1;  // stale: never allocated
+        } else if constexpr (kVec4) {  // 4 edges per lane, 128 blocks per ballot
+          for (int i0 = 0; i0 < nb && b < 0; i0 += 128) {
+            const int i = i0 + 4 * lane;
+            unsigned f = 0;
+            if (i < nb) {
+              const uint2 w = *reinterpret_cast<const uint2*>(bed + i);
+              f = ((int)(w.x & 0xffffu) == e ? 1u : 0u) | ((int)(w.x >> 16) == e ? 2u : 0u) |
+                  ((int)(w.y & 0xffffu) == e ? 4u : 0u) | ((int)(w.y >> 16) == e ? 8u : 0u);
+              if (nb - i < 4) f &= (1u << (nb - i)) - 1u;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, f != 0);
+            if (m) {
+              const int src = __ffs(m) - 1;
+              b = i0 + 4 * src + __ffs(__shfl_sync(0xffffffffu, f, src)) - 1;
+            }
+          }
         } else {
           for (int i0 = 0; i0 < nb && b < 0; i0 += 32) {
             const unsigned m =
@@ -456,16 +472,21 @@ int arena_per_sm(const ArenaArgs& in, size_t* smem) {
 
 template <typename IT, typename ST>
 mp_status launch_arena_t(const ArenaArgs& in, const mp_ctx* ctx, cudaStream_t st) {
-  // The edge -> block index (kBlk) removes the release search (~20% of the replay's
-  // instructions) but adds 2E bytes per candidate: use it unless the lost resident
-  // candidates cost more than that, i.e. it adds more than ~20% rounds.
+  // The edge -> block index (kBlk) removes the release search (~20% of the scalar
+  // replay's instructions) but adds 2E bytes per candidate: use it unless the lost
+  // resident candidates cost more than that, i.e. it adds more than ~20% rounds.
   size_t smem0 = 0, smem1 = 0;
   const int occ0 = arena_per_sm<IT, ST, false>(in, &smem0);
   const int occ1 = arena_per_sm<IT, ST, true>(in, &smem1);
   const int64_t per_sm_work =
       (in.num_orders + (int64_t)ctx->num_sms * kArenaWarps - 1) / ((int64_t)ctx->num_sms * kArenaWarps);
   auto rounds = [&](int occ) { return occ > 0 ? (per_sm_work + occ - 1) / occ : INT64_MAX; };
-  bool blk = occ1 > 0 && 5 * rounds(occ1) <= 6 * rounds(occ0);
+  // with 16-bit edges the search itself is 4 blocks per lane, so the index only
+  // pays when it costs no round and <20% of the resident warps (measured: C2 +5%
+  // with it at 16 vs 19 warps/SM, C3 +4% without it at 10 vs 13)
+  bool blk = occ1 > 0 && (sizeof(IT) == 2
+                              ? rounds(occ1) <= rounds(occ0) && 5 * occ1 >= 4 * occ0
+                              : 5 * rounds(occ1) <= 6 * rounds(occ0));
   if (const char* e = std::getenv("MP_ARENA_BLK")) blk = std::atoi(e) != 0 && occ1 > 0;
   const int per_sm = blk ? occ1 : occ0;
   if (per_sm <= 0) {
