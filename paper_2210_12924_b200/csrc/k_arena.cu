@@ -267,36 +267,21 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
         if (b < 0) continue;
         __syncwarp();
         if (lane == 0) bed[b] = kFree;
-        // coalesce (placement.cpp:130-139): the next block, then the previous one
-        int erase = -1;
-        if (b + 1 < nb && bed[b + 1] == kFree) {
-          if (lane == 0) bsz[b] += bsz[b + 1];
-          erase = b + 1;
-        }
+        // coalesce (placement.cpp:130-139): the next block, then the previous one.
+        // Both merges remove up to two entries; one shift by that count replaces
+        // the reference's two successive erases (the same final list).
+        const bool nxt = b + 1 < nb && bed[b + 1] == kFree;
+        const bool prv = b > 0 && bed[b - 1] == kFree;
         __syncwarp();
-        if (erase >= 0) {  // shift [erase + 1, nb) left by one
-          for (int i0 = erase + 1; i0 < nb; i0 += 32) {
-            const int i = i0 + lane;
-            ST sz = 0;
-            IT ed = 0;
-            if (i < nb) {
-              sz = bsz[i];
-              ed = bed[i];
-            }
-            __syncwarp();
-            if (i < nb) {
-              bsz[i - 1] = sz;
-              bed[i - 1] = ed;
-              if (kBlk && ed != kFree) blk[ed] = (IT)(i - 1);
-            }
-            __syncwarp();
-          }
-          --nb;
+        if (lane == 0) {
+          if (nxt) bsz[b] += bsz[b + 1];
+          if (prv) bsz[b - 1] += bsz[b];
         }
-        if (b > 0 && bed[b - 1] == kFree) {
-          if (lane == 0) bsz[b - 1] += bsz[b];
-          __syncwarp();
-          for (int i0 = b + 1; i0 < nb; i0 += 32) {
+        const int k = (nxt ? 1 : 0) + (prv ? 1 : 0);
+        __syncwarp();
+        if (k > 0) {  // shift [keep + 1 + k, nb) left by k, keep = the surviving block
+          const int from = (prv ? b - 1 : b) + 1 + k;
+          for (int i0 = from; i0 < nb; i0 += 32) {
             const int i = i0 + lane;
             ST sz = 0;
             IT ed = 0;
@@ -306,13 +291,13 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
             }
             __syncwarp();
             if (i < nb) {
-              bsz[i - 1] = sz;
-              bed[i - 1] = ed;
-              if (kBlk && ed != kFree) blk[ed] = (IT)(i - 1);
+              bsz[i - k] = sz;
+              bed[i - k] = ed;
+              if (kBlk && ed != kFree) blk[ed] = (IT)(i - k);
             }
             __syncwarp();
           }
-          --nb;
+          nb -= k;
         }
         __syncwarp();
       }
