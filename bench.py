@@ -626,10 +626,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # MP_DIST_BACKEND=gloo: a functional check of the N>1 path with several ranks
+    # sharing the GPUs of a smaller box (never a measurement; NCCL is the product)
+    backend = os.environ.get("MP_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= max(1, torch.cuda.device_count())
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     g = load_graph(cfg)
     C = cfg["candidates"]
@@ -791,7 +799,8 @@ def main():
                        "l2": f"inputs larger than L2: {nb} rotating batches of "
                              f"{batch_bytes / 2**20:.1f} MiB ({nb * batch_bytes / 2**20:.0f} MiB"
                              " > 126 MiB L2)",
-                       "parallelism": f"dp{world} (candidates sharded, 1 allreduce-min)",
+                       "parallelism": f"dp{world} (candidates sharded, 1 allreduce-min)" +
+                       ("" if backend == "nccl" or world == 1 else f" [{backend}: functional check]"),
                        "smem_resident": bool(info["smem_resident"])},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
                          "frac": achieved / peak_gbs, "traffic": profile_traffic(args.config),
