@@ -292,6 +292,19 @@ def run_pairs(args, cfg):
         cpu = {"value": count / t_ref, "unit": "pairs/s", "cores": 1, "kind": "reference",
                "sample": f"memplan::encode_addresses over all {E} edges ({count} pairs, "
                          "model rows included), oracle/_ref -O3, 1 thread"}
+        # memplan::validate_plan on the same (valid) address plan, beside K4
+        ts = np.zeros(g.n, np.int32)
+        ts[order] = np.arange(1, g.n + 1, dtype=np.int32)
+        has = (g.edge_size > 0).astype(np.uint8)
+        pm = int(max((int(addr[e] + g.edge_size[e]) for e in range(E) if has[e]), default=0))
+        _, prs, _ = rg.timeline_from_lifetimes(lo, hi, g.n)
+        t0 = time.perf_counter()
+        viol = rg.validate_plan(order, ts, has, addr, pm, prs)
+        t_rv = time.perf_counter() - t0
+        assert viol == []
+        cpu["validate"] = {"value": E * (E - 1) / 2 / t_rv, "unit": "pair checks/s",
+                           "seconds": t_rv, "sample": "memplan::validate_plan (whole report) "
+                           "on the same valid plan, 1 thread"}
     else:
         r1 = max(1, E // 16)
         t0 = time.perf_counter()
