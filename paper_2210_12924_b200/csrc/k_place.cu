@@ -57,6 +57,10 @@ struct PlaceScratch {
   int we[kPT / 32];
 };
 
+// `ord` is stored skewed (one pad word per 32 entries): thread t's chunk starts at
+// t * ch, and with an even ch the unskewed words would sit in a few banks only.
+__device__ __forceinline__ int sk(int i) { return i + (i >> 5); }
+
 __device__ __forceinline__ bool disjoint(int alo, int ahi, int blo, int bhi) {
   return alo > ahi || blo > bhi || ahi < blo || bhi < alo;  // analysis.hpp:28-37
 }
@@ -78,11 +82,11 @@ __global__ void __launch_bounds__(kPT, 512 / kPT)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int kW = kPT / 32;
   const int cap = a.cap;
-  unsigned long long* e_addr = reinterpret_cast<unsigned long long*>(smem);  // by slot
-  unsigned long long* e_top = e_addr + cap;
-  int2* e_life = reinterpret_cast<int2*>(e_top + cap);
-  int* ord = reinterpret_cast<int*>(e_life + cap);          // slots in address order
-  uint8_t* flag = reinterpret_cast<uint8_t*>(ord + cap);    // [E] fixed / taken
+  // by slot: (address, top) together - the sweep reads both with one 16-byte load
+  ulonglong2* e_at = reinterpret_cast<ulonglong2*>(smem);
+  int2* e_life = reinterpret_cast<int2*>(e_at + cap);
+  int* ord = reinterpret_cast<int*>(e_life + cap);          // slots in address order (skewed)
+  uint8_t* flag = reinterpret_cast<uint8_t*>(ord + cap + (cap >> 5) + 1);  // [E] fixed / taken
 
   for (int64_t b = blockIdx.x; b < a.num_problems; b += gridDim.x) {
     const int32_t* lo = a.lo + b * (int64_t)E;
@@ -109,7 +113,7 @@ __global__ void __launch_bounds__(kPT, 512 / kPT)
       const int i0 = tid * ch;
       int o[kCh];
 #pragma unroll
-      for (int q = 0; q < kCh; ++q) o[q] = (q < ch && i0 + q < k) ? ord[i0 + q] : -1;
+      for (int q = 0; q < kCh; ++q) o[q] = (q < ch && i0 + q < k) ? ord[sk(i0 + q)] : -1;
       if (search) {
         long long cm = LLONG_MIN;  // max top over this chunk's conflicting tensors
 #pragma unroll
@@ -117,7 +121,7 @@ __global__ void __launch_bounds__(kPT, 512 / kPT)
           if (o[q] >= 0) {
             const int2 l = e_life[o[q]];
             if (!disjoint(elo, ehi, l.x, l.y)) {
-              const long long t = (long long)e_top[o[q]];
+              const long long t = (long long)e_at[o[q]].y;
               cm = t > cm ? t : cm;
             }
           }
@@ -143,8 +147,9 @@ __global__ void __launch_bounds__(kPT, 512 / kPT)
           if (stop == INT_MAX && o[q] >= 0) {
             const int2 l = e_life[o[q]];
             if (!disjoint(elo, ehi, l.x, l.y)) {
-              const long long L = (long long)e_addr[o[q]] - (long long)s;
-              const long long t = (long long)e_top[o[q]];
+              const ulonglong2 at = e_at[o[q]];
+              const long long L = (long long)at.x - (long long)s;
+              const long long t = (long long)at.y;
               if (L >= M) {
                 stop = i0 + q;
                 xs = M;
@@ -168,7 +173,7 @@ __global__ void __launch_bounds__(kPT, 512 / kPT)
       int cnt = 0;
 #pragma unroll
       for (int q = 0; q < kCh; ++q)
-        if (o[q] >= 0) cnt += e_addr[o[q]] < x;
+        if (o[q] >= 0) cnt += e_at[o[q]].x < x;
       if (tid == 0) ps.pos = 0;
       __syncthreads();
       cnt = __reduce_add_sync(0xffffffffu, cnt);
@@ -177,11 +182,10 @@ __global__ void __launch_bounds__(kPT, 512 / kPT)
       const int p = ps.pos;
 #pragma unroll
       for (int q = 0; q < kCh; ++q)
-        if (o[q] >= 0 && i0 + q >= p) ord[i0 + q + 1] = o[q];
+        if (o[q] >= 0 && i0 + q >= p) ord[sk(i0 + q + 1)] = o[q];
       if (tid == 0) {
-        ord[p] = k;
-        e_addr[k] = x;
-        e_top[k] = x + s;
+        ord[sk(p)] = k;
+        e_at[k] = make_ulonglong2(x, x + s);
         e_life[k] = make_int2(elo, ehi);
       }
       __syncthreads();
@@ -319,7 +323,7 @@ __global__ void __launch_bounds__(kPT, 512 / kPT)
 
 size_t place_smem_bytes(int num_edges) {
   const int cap = num_edges < kPlaceMaxEntries ? num_edges + 1 : kPlaceMaxEntries;
-  return (size_t)cap * (8 + 8 + 8 + 4) + (size_t)num_edges + 16;
+  return (size_t)cap * (8 + 8 + 8 + 4) + 4 * ((size_t)(cap >> 5) + 1) + (size_t)num_edges + 16;
 }
 
 template <int kPT>
