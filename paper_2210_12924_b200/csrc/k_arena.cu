@@ -137,6 +137,8 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
   const int wid = threadIdx.x >> 5;
   const ArenaLayout Lo{n, E, a.cap, (int)sizeof(IT), (int)sizeof(ST), kBlk ? 1 : 0};
   constexpr IT kFree = (IT)-1;  // block edge of a free block
+  constexpr IT kTomb = (IT)-2;  // an erased entry (edge ids are < E < kTomb)
+  constexpr int kTombMax = 32;  // tombstones tolerated before a compaction
   char* base = smem + (size_t)wid * Lo.bytes();
   IT* pos = reinterpret_cast<IT*>(base + Lo.pos_off());
   IT* fstart = reinterpret_cast<IT*>(base + Lo.fstart_off());
@@ -229,9 +231,56 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
     }
     // fstart[t + 1] now points past bucket t; bucket t = [fstart[t], fstart[t + 1])
     // ---- replay (placement.cpp:160-177) ------------------------------------------
-    int nb = 0;
+    // Erased entries become tombstones (edge kTomb, size 0) instead of shifting the
+    // list: they never fit, never match an edge, and are skipped when looking for a
+    // block's neighbours, so the live entries are always the reference's list in
+    // order. A split reuses the nearest tombstone after it (shifting only up to
+    // there); a compaction every kTombMax tombstones (or at the capacity) removes
+    // them, and trailing ones are trimmed at once (bed[nb - 1] is always live).
+    int nb = 0, ntomb = 0;
     bool overflow = false;  // warp-uniform
     unsigned long long top = 0, live = 0, mr = 0, rs = 0;
+    auto next_live = [&](int b) -> int {
+      for (int i0 = b + 1; i0 < nb; i0 += 32) {
+        const int i = i0 + lane;
+        const unsigned m = __ballot_sync(0xffffffffu, i < nb && bed[i] != kTomb);
+        if (m) return i0 + __ffs(m) - 1;
+      }
+      return -1;
+    };
+    auto prev_live = [&](int b) -> int {
+      for (int i1 = b - 1; i1 >= 0; i1 -= 32) {
+        const int i = i1 - lane;
+        const unsigned m = __ballot_sync(0xffffffffu, i >= 0 && bed[i] != kTomb);
+        if (m) return i1 - (__ffs(m) - 1);
+      }
+      return -1;
+    };
+    auto compact = [&]() {  // stable, in place: writes never pass the reads
+      int w = 0;
+      for (int i0 = 0; i0 < nb; i0 += 32) {
+        const int i = i0 + lane;
+        ST sz = 0;
+        IT ed = kTomb;
+        if (i < nb) {
+          sz = bsz[i];
+          ed = bed[i];
+        }
+        const bool keep = ed != kTomb;
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        const int to = w + __popc(m & lanemask_lt());
+        __syncwarp();
+        if (keep) {
+          bsz[to] = sz;
+          bed[to] = ed;
+          if (kBlk && ed != kFree) blk[ed] = (IT)to;
+        }
+        __syncwarp();
+        w += __popc(m);
+      }
+      nb = w;
+      ntomb = 0;
+    };
     for (int t = 1; t <= n && !overflow; ++t) {
       const int f0 = fstart[t], f1 = fstart[t + 1];
       for (int q = f0; q < f1; ++q) {  // Arena::release (placement.cpp:103-111)
@@ -267,39 +316,33 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
         if (b < 0) continue;
         __syncwarp();
         if (lane == 0) bed[b] = kFree;
-        // coalesce (placement.cpp:130-139): the next block, then the previous one.
-        // Both merges remove up to two entries; one shift by that count replaces
-        // the reference's two successive erases (the same final list).
-        const bool nxt = b + 1 < nb && bed[b + 1] == kFree;
-        const bool prv = b > 0 && bed[b - 1] == kFree;
         __syncwarp();
-        if (lane == 0) {
-          if (nxt) bsz[b] += bsz[b + 1];
-          if (prv) bsz[b - 1] += bsz[b];
-        }
-        const int k = (nxt ? 1 : 0) + (prv ? 1 : 0);
-        __syncwarp();
-        if (k > 0) {  // shift [keep + 1 + k, nb) left by k, keep = the surviving block
-          const int from = (prv ? b - 1 : b) + 1 + k;
-          for (int i0 = from; i0 < nb; i0 += 32) {
-            const int i = i0 + lane;
-            ST sz = 0;
-            IT ed = 0;
-            if (i < nb) {
-              sz = bsz[i];
-              ed = bed[i];
-            }
-            __syncwarp();
-            if (i < nb) {
-              bsz[i - k] = sz;
-              bed[i - k] = ed;
-              if (kBlk && ed != kFree) blk[ed] = (IT)(i - k);
-            }
-            __syncwarp();
+        // coalesce (placement.cpp:130-139): the next live block, then the previous
+        // one; a merged-away entry becomes a tombstone
+        const int nx = next_live(b);
+        if (nx >= 0 && bed[nx] == kFree) {
+          if (lane == 0) {
+            bsz[b] += bsz[nx];
+            bed[nx] = kTomb;
+            bsz[nx] = 0;
           }
-          nb -= k;
+          ++ntomb;
         }
         __syncwarp();
+        const int pv = prev_live(b);
+        if (pv >= 0 && bed[pv] == kFree) {
+          if (lane == 0) {
+            bsz[pv] += bsz[b];
+            bed[b] = kTomb;
+            bsz[b] = 0;
+          }
+          ++ntomb;
+        }
+        __syncwarp();
+        while (nb > 0 && bed[nb - 1] == kTomb) {  // keep bed[nb - 1] live
+          --nb;
+          --ntomb;
+        }
       }
       const int v = order[t - 1];
       const int o0 = a.out_off[v], o1 = a.out_off[v + 1];
@@ -307,6 +350,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
         const int e = a.out_edges[q];
         const unsigned long long s = size_of<ST>(a, e);
         if (s == 0) continue;
+        if (ntomb > kTombMax || (ntomb > 0 && nb >= a.cap - 1)) compact();
         // Arena::allocate (placement.cpp:80-101): first fit, or the smallest fit
         int pick = -1;
         if (!a.best_fit && kVec4) {
@@ -377,22 +421,29 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
         } else {
           const unsigned long long bsize = bsz[pick];
           __syncwarp();
-          if (bsize > s && nb == a.cap) {
-            overflow = true;
-            break;
-          }
-          if (bsize > s) {  // split: the rest stays free right after (shift right)
-            for (int i0 = ((nb - 1 - (pick + 1)) / 32) * 32 + pick + 1; i0 >= pick + 1;
-                 i0 -= 32) {
+          if (bsize > s) {  // split: the rest stays free right after pick
+            int tpos = -1;  // the first tombstone after pick: the shift stops there
+            for (int i0 = pick + 1; ntomb > 0 && i0 < nb && tpos < 0; i0 += 32) {
+              const unsigned m =
+                  __ballot_sync(0xffffffffu, i0 + lane < nb && bed[i0 + lane] == kTomb);
+              if (m) tpos = i0 + __ffs(m) - 1;
+            }
+            if (tpos < 0 && nb == a.cap) {  // (compacted above: no tombstone to reuse)
+              overflow = true;
+              break;
+            }
+            const int end = tpos >= 0 ? tpos : nb;  // shift [pick + 1, end) right by one
+            for (int i0 = ((end - 1 - (pick + 1)) / 32) * 32 + pick + 1;
+                 end > pick + 1 && i0 >= pick + 1; i0 -= 32) {
               const int i = i0 + lane;
               ST sz = 0;
               IT ed = 0;
-              if (i < nb) {
+              if (i < end) {
                 sz = bsz[i];
                 ed = bed[i];
               }
               __syncwarp();
-              if (i < nb) {
+              if (i < end) {
                 bsz[i + 1] = sz;
                 bed[i + 1] = ed;
                 if (kBlk && ed != kFree) blk[ed] = (IT)(i + 1);
@@ -403,7 +454,8 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
               bsz[pick + 1] = (ST)(bsize - s);
               bed[pick + 1] = kFree;
             }
-            ++nb;
+            if (tpos >= 0) --ntomb;
+            else ++nb;
           }
           if (lane == 0) {
             bsz[pick] = (ST)s;
@@ -467,11 +519,10 @@ mp_status launch_arena_t(const ArenaArgs& in, const mp_ctx* ctx, cudaStream_t st
       (in.num_orders + (int64_t)ctx->num_sms * kArenaWarps - 1) / ((int64_t)ctx->num_sms * kArenaWarps);
   auto rounds = [&](int occ) { return occ > 0 ? (per_sm_work + occ - 1) / occ : INT64_MAX; };
   // with 16-bit edges the search itself is 4 blocks per lane, so the index only
-  // pays when it costs no round and <20% of the resident warps (measured: C2 +5%
-  // with it at 16 vs 19 warps/SM, C3 +4% without it at 10 vs 13)
-  bool blk = occ1 > 0 && (sizeof(IT) == 2
-                              ? rounds(occ1) <= rounds(occ0) && 5 * occ1 >= 4 * occ0
-                              : 5 * rounds(occ1) <= 6 * rounds(occ0));
+  // pays when it costs no round (measured with tombstones: C2 +13%, C3 +12% with
+  // it; C4, one round more, 15% slower)
+  bool blk = occ1 > 0 && (sizeof(IT) == 2 ? rounds(occ1) <= rounds(occ0)
+                                          : 5 * rounds(occ1) <= 6 * rounds(occ0));
   if (const char* e = std::getenv("MP_ARENA_BLK")) blk = std::atoi(e) != 0 && occ1 > 0;
   const int per_sm = blk ? occ1 : occ0;
   if (per_sm <= 0) {
