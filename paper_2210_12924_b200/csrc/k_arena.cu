@@ -138,7 +138,10 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
   const ArenaLayout Lo{n, E, a.cap, (int)sizeof(IT), (int)sizeof(ST), kBlk ? 1 : 0};
   constexpr IT kFree = (IT)-1;  // block edge of a free block
   constexpr IT kTomb = (IT)-2;  // an erased entry (edge ids are < E < kTomb)
-  constexpr int kTombMax = 32;  // tombstones tolerated before a compaction
+#ifndef MP_TOMB_MAX
+#define MP_TOMB_MAX 96
+#endif
+  constexpr int kTombMax = MP_TOMB_MAX;  // tombstones tolerated before a compaction
   char* base = smem + (size_t)wid * Lo.bytes();
   IT* pos = reinterpret_cast<IT*>(base + Lo.pos_off());
   IT* fstart = reinterpret_cast<IT*>(base + Lo.fstart_off());
@@ -235,7 +238,7 @@ __global__ void __launch_bounds__(32 * kArenaWarps)
     // list: they never fit, never match an edge, and are skipped when looking for a
     // block's neighbours, so the live entries are always the reference's list in
     // order. A split reuses the nearest tombstone after it (shifting only up to
-    // there); a compaction every kTombMax tombstones (or at the capacity) removes
+    // there); a compaction past kTombMax (96) tombstones (or at the capacity) removes
     // them, and trailing ones are trimmed at once (bed[nb - 1] is always live).
     int nb = 0, ntomb = 0;
     bool overflow = false;  // warp-uniform
