@@ -47,7 +47,7 @@ def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(ROOT, "include", "memplan_b200.h"))
     common = ["-O3", "-std=c++17", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-              "-Xcompiler", "-fPIC,-Wall", *defines]
+              "-Xcompiler", "-fPIC,-Wall,-fopenmp", *defines]
     objs = []
     log = []
     for src in CU_SOURCES:
@@ -64,7 +64,7 @@ def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB
             log.append(_run([NVCC, *ARCH, *common, "-c", s, "-o", o]))
     if force or _stale(lib, objs):
         log.append(_run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs,
-                         "-lpthread"]))
+                         "-lpthread", "-lgomp"]))
     text = "".join(log)
     if verbose:
         print(text)

@@ -686,11 +686,11 @@ mp_status run(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d
   return MP_OK;
 }
 
-template <typename VT, int J, int KC>
-mp_status run_reg(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d_peak,
-                  int32_t* d_step, uint8_t* d_valid, uint64_t* d_bytes, uint64_t* d_key,
-                  int64_t index_base, cudaStream_t st) {
-  auto kern = score_reg_kernel<VT, J, KC>;
+template <typename VT, int J, int KC, typename OT>
+mp_status run_reg_t(const mp_graph* g, const OT* d_orders, int64_t C, uint64_t* d_peak,
+                    int32_t* d_step, uint8_t* d_valid, uint64_t* d_bytes, uint64_t* d_key,
+                    int64_t index_base, cudaStream_t st) {
+  auto kern = score_reg_kernel<VT, J, KC, OT>;
   const int T = g->score_threads;
   const size_t smem = reg_smem_bytes<VT>(g->n, T, g->score_p, J, KC);
 
@@ -704,6 +704,19 @@ mp_status run_reg(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_
                                         reinterpret_cast<unsigned long long*>(d_key), index_base);
   MP_CUDA(cudaGetLastError());
   return MP_OK;
+}
+
+template <typename VT, int J, int KC>
+mp_status run_reg(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d_peak,
+                  int32_t* d_step, uint8_t* d_valid, uint64_t* d_bytes, uint64_t* d_key,
+                  int64_t index_base, cudaStream_t st, bool o16) {
+  if (o16 && KC == 1)  // 16-bit orders (host-packed): same kernel, half the order bytes
+    return run_reg_t<VT, J, KC, uint16_t>(g, reinterpret_cast<const uint16_t*>(d_orders), C,
+                                          d_peak, d_step, d_valid, d_bytes, d_key, index_base,
+                                          st);
+  if (o16) return MP_E_INVALID_ARG;
+  return run_reg_t<VT, J, KC, int32_t>(g, d_orders, C, d_peak, d_step, d_valid, d_bytes, d_key,
+                                       index_base, st);
 }
 
 template <typename VT>
@@ -730,18 +743,20 @@ mp_status run_warp(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64
 
 template <typename VT>
 mp_status dispatch(const mp_graph* g, const int32_t* o, int64_t C, uint64_t* pk, int32_t* stp,
-                   uint8_t* vl, uint64_t* by, uint64_t* key, int64_t base, cudaStream_t st) {
+                   uint8_t* vl, uint64_t* by, uint64_t* key, int64_t base, cudaStream_t st,
+                   bool o16) {
+  if (o16 && !score_takes_u16(g)) return MP_E_INVALID_ARG;
   if (g->score_warps > 0) return run_warp<VT>(g, o, C, pk, stp, vl, by, key, base, st);
   switch (g->score_j) {
     case 4:
-      if (g->score_kc == 2) return run_reg<VT, 4, 2>(g, o, C, pk, stp, vl, by, key, base, st);
-      return run_reg<VT, 4, 1>(g, o, C, pk, stp, vl, by, key, base, st);
+      if (g->score_kc == 2) return run_reg<VT, 4, 2>(g, o, C, pk, stp, vl, by, key, base, st, o16);
+      return run_reg<VT, 4, 1>(g, o, C, pk, stp, vl, by, key, base, st, o16);
     case 8:
-      if (g->score_kc == 2) return run_reg<VT, 8, 2>(g, o, C, pk, stp, vl, by, key, base, st);
-      return run_reg<VT, 8, 1>(g, o, C, pk, stp, vl, by, key, base, st);
+      if (g->score_kc == 2) return run_reg<VT, 8, 2>(g, o, C, pk, stp, vl, by, key, base, st, o16);
+      return run_reg<VT, 8, 1>(g, o, C, pk, stp, vl, by, key, base, st, o16);
     case 16:
-      if (g->score_kc == 2) return run_reg<VT, 16, 2>(g, o, C, pk, stp, vl, by, key, base, st);
-      return run_reg<VT, 16, 1>(g, o, C, pk, stp, vl, by, key, base, st);
+      if (g->score_kc == 2) return run_reg<VT, 16, 2>(g, o, C, pk, stp, vl, by, key, base, st, o16);
+      return run_reg<VT, 16, 1>(g, o, C, pk, stp, vl, by, key, base, st, o16);
     default:
       if (g->smem_resident)
         return run<VT, uint32_t, 0, true>(g, o, C, pk, stp, vl, by, key, base, st);
@@ -838,15 +853,19 @@ mp_status score_configure(mp_graph* g) {
   return MP_OK;
 }
 
+bool score_takes_u16(const mp_graph* g) {
+  return g->n > 0 && g->n < 65535 && g->score_j > 0 && g->score_warps == 0 && g->score_kc == 1;
+}
+
 mp_status launch_score(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d_peak,
                        int32_t* d_step, uint8_t* d_valid, uint64_t* d_bytes, uint64_t* d_key,
-                       int64_t index_base, cudaStream_t st) {
+                       int64_t index_base, cudaStream_t st, bool orders16) {
   if (C <= 0) return MP_OK;
   if (g->narrow)
     return dispatch<uint32_t>(g, d_orders, C, d_peak, d_step, d_valid, d_bytes, d_key,
-                              index_base, st);
+                              index_base, st, orders16);
   return dispatch<unsigned long long>(g, d_orders, C, d_peak, d_step, d_valid, d_bytes, d_key,
-                                      index_base, st);
+                                      index_base, st, orders16);
 }
 
 // ---- argmin over candidates (single CTA; C is at most a few million) ------------

@@ -53,9 +53,12 @@ struct RegScratch {
   uint32_t bad[2];  // per-iteration-parity bitmask of invalid candidates
 };
 
-template <typename VT, int J, int KC>
+// OT: the order element type - int32 (the reference's layout) or uint16 (the host
+// call packs orders of graphs with n < 65535 to halve the PCIe bytes; values
+// outside [0, n) arrive as 0xffff, still out of range).
+template <typename VT, int J, int KC, typename OT = int32_t>
 __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMinBlocks)
-    score_reg_kernel(ScoreTables G, const int32_t* __restrict__ orders, int64_t C,
+    score_reg_kernel(ScoreTables G, const OT* __restrict__ orders, int64_t C,
                      uint64_t* __restrict__ peak_out, int32_t* __restrict__ step_out,
                      uint8_t* __restrict__ valid_out, uint64_t* __restrict__ bytes_out,
                      unsigned long long* __restrict__ best_key, int64_t index_base) {
@@ -129,10 +132,10 @@ __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMi
 #pragma unroll
     for (int k = 0; k < KC; ++k) {
       const int64_t c = g * KC + k;
-      const int32_t* row = orders + c * n + base;
+      const OT* row = orders + c * n + base;
 #pragma unroll
       for (int j = 0; j < J; ++j)
-        ov[k][j] = ((real >> j & 1) && c < C) ? __ldg(row + kWarp * j) : base + kWarp * j;
+        ov[k][j] = ((real >> j & 1) && c < C) ? (int)__ldg(row + kWarp * j) : base + kWarp * j;
     }
   };
   if ((int64_t)blockIdx.x < ngroups) load_group(blockIdx.x);

@@ -164,6 +164,7 @@ mp_status mp_ctx_destroy(mp_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
   if (ctx->h_small) cudaFreeHost(ctx->h_small);
+  if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
@@ -518,6 +519,26 @@ mp_status mp_score_orders(mp_ctx* ctx, const mp_graph* g, const int32_t* orders,
   return mp_score_orders_best(ctx, g, orders, C, peak, step, valid, nullptr);
 }
 
+namespace {
+// int32 orders -> uint16 (values outside [0, n) become 0xffff, still out of range
+// for the kernel since n < 65535), on the host cores: the packed orders halve the
+// PCIe bytes of the host-buffer call, the transfer that bounds it.
+void pack_orders16(const int32_t* src, uint16_t* dst, size_t cnt, uint32_t n) {
+  static const int nthr = [] {
+    const char* e = std::getenv("MP_PACK_THREADS");
+    const int hw = (int)std::thread::hardware_concurrency();
+    const int v = e ? std::atoi(e) : (hw < 16 ? hw : 16);
+    return v < 1 ? 1 : v;
+  }();
+  const int t = cnt < (size_t{1} << 16) ? 1 : nthr;
+#pragma omp parallel for num_threads(t) schedule(static)
+  for (int64_t i = 0; i < (int64_t)cnt; ++i) {
+    const uint32_t v = (uint32_t)src[i];
+    dst[i] = v < n ? (uint16_t)v : (uint16_t)0xffffu;
+  }
+}
+}  // namespace
+
 mp_status mp_score_orders_best(mp_ctx* ctx, const mp_graph* g, const int32_t* orders, int64_t C,
                                uint64_t* peak, int32_t* step, uint8_t* valid, int64_t* best) {
   if (!ctx || !g || C < 0) return invalid_arg("null argument or negative count");
@@ -555,6 +576,17 @@ mp_status mp_score_orders_best(mp_ctx* ctx, const mp_graph* g, const int32_t* or
   if (nch > max_ch) nch = max_ch;
   if (nch > C) nch = C;
   if (nch < 1 || n == 0) nch = 1;
+  // 16-bit orders when the graph's scorer takes them (register-slot variant, n < 65535)
+  const bool p16 = n > 0 && score_takes_u16(g) && !std::getenv("MP_NO_PACK16");
+  uint16_t* d16 = reinterpret_cast<uint16_t*>(d_orders);
+  const size_t half = n * (size_t)((C + nch - 1) / nch);
+  if (p16 && ctx->h_stage_elems < half) {
+    if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+    ctx->h_stage = nullptr;
+    ctx->h_stage_elems = 0;
+    MP_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_stage), 4 * half));
+    ctx->h_stage_elems = half;
+  }
   cudaStream_t cs = nch > 1 ? ctx->copy_stream : st;
   if (nch > 1) {  // the copy stream starts after everything already queued on `st`
     MP_CUDA(cudaEventRecord(ctx->ev_start, st));
@@ -562,14 +594,24 @@ mp_status mp_score_orders_best(mp_ctx* ctx, const mp_graph* g, const int32_t* or
   }
   for (int64_t k = 0; k < nch; ++k) {
     const int64_t b = C * k / nch, e = C * (k + 1) / nch, m = e - b;
-    if (n) MP_CUDA(cudaMemcpyAsync(d_orders + (size_t)b * n, orders + (size_t)b * n,
-                                   4 * n * (size_t)m, cudaMemcpyHostToDevice, cs));
-    if (nch > 1) {
-      MP_CUDA(cudaEventRecord(ctx->ev_h2d[k], cs));
-      MP_CUDA(cudaStreamWaitEvent(st, ctx->ev_h2d[k], 0));
+    if (p16) {  // pack chunk k while chunk k - 1 is on the wire (two staging halves)
+      uint16_t* buf = ctx->h_stage + (size_t)(k & 1) * ctx->h_stage_elems;
+      if (k >= 2) MP_CUDA(cudaEventSynchronize(ctx->ev_h2d[k - 2]));  // this half is free
+      pack_orders16(orders + (size_t)b * n, buf, n * (size_t)m, (uint32_t)n);
+      MP_CUDA(cudaMemcpyAsync(d16 + (size_t)b * n, buf, 2 * n * (size_t)m,
+                              cudaMemcpyHostToDevice, cs));
+    } else if (n) {
+      MP_CUDA(cudaMemcpyAsync(d_orders + (size_t)b * n, orders + (size_t)b * n,
+                              4 * n * (size_t)m, cudaMemcpyHostToDevice, cs));
     }
-    MP_TRY(launch_score(g, d_orders + (size_t)b * n, m, d_peak + b, d_step + b, d_valid + b,
-                        nullptr, fused ? d_key : nullptr, b, st));
+    if (nch > 1 || p16) {
+      MP_CUDA(cudaEventRecord(ctx->ev_h2d[k], cs));
+      if (nch > 1) MP_CUDA(cudaStreamWaitEvent(st, ctx->ev_h2d[k], 0));
+    }
+    const int32_t* chunk = p16 ? reinterpret_cast<const int32_t*>(d16 + (size_t)b * n)
+                               : d_orders + (size_t)b * n;
+    MP_TRY(launch_score(g, chunk, m, d_peak + b, d_step + b, d_valid + b, nullptr,
+                        fused ? d_key : nullptr, b, st, p16));
     MP_CUDA(cudaMemcpyAsync(peak + b, d_peak + b, 8 * (size_t)m, cudaMemcpyDeviceToHost, st));
     MP_CUDA(cudaMemcpyAsync(step + b, d_step + b, 4 * (size_t)m, cudaMemcpyDeviceToHost, st));
     MP_CUDA(cudaMemcpyAsync(valid + b, d_valid + b, (size_t)m, cudaMemcpyDeviceToHost, st));

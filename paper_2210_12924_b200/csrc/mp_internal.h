@@ -55,6 +55,8 @@ struct mp_ctx {
   cudaEvent_t ev_h2d[kPipeChunks] = {};
   cudaEvent_t ev_start = nullptr;
   uint64_t* h_small = nullptr;  // pinned: [0] key init, [1] key read-back
+  uint16_t* h_stage = nullptr;  // pinned: two halves of 16-bit packed orders
+  size_t h_stage_elems = 0;     // per half
 };
 
 // Several contexts in one process, the graph replicated on each (mp_score_orders_multi).
@@ -139,7 +141,10 @@ mp_status launch_score(const mp_graph* g, const int32_t* d_orders, int64_t num_o
                        uint64_t* d_peak, int32_t* d_peak_step, uint8_t* d_valid,
                        uint64_t* d_bytes /* [C][n] or null */,
                        uint64_t* d_key /* fused argmin key or null */, int64_t index_base,
-                       cudaStream_t st);
+                       cudaStream_t st,
+                       bool orders16 = false /* d_orders holds uint16 (score_takes_u16) */);
+// the fused scorer reads 16-bit orders for this graph (register-slot variant, n < 65535)
+bool score_takes_u16(const mp_graph* g);
 size_t score_scratch_bytes(const mp_graph* g, int64_t num_orders);
 mp_status score_configure(mp_graph* g);
 
