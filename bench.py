@@ -827,7 +827,11 @@ def main():
                          "kernel_ms": kern_graph_ms, "kernel_ms_eager_events": kern_ms,
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "peak_source": peak_src},
-            "e2e": {"value": e2e_value, "unit": "plans/s", "h2d_bytes_per_step": batch_bytes,
+            "e2e": {"value": e2e_value, "unit": "plans/s",
+                    "h2d_bytes_per_step": batch_bytes // 2 if info["orders16"] else batch_bytes,
+                    "host_input_bytes_per_step": batch_bytes,
+                    "orders_on_wire": "uint16 (packed on the host cores)" if info["orders16"]
+                    else "int32",
                     "d2h_bytes_per_step": C * 13 + 8,
                     "path": "Planner.score_orders_into -> mp_score_orders_best (pinned host)",
                     "torch_pinned_h2d_gbs": h2d_gbs},

@@ -72,6 +72,8 @@ typedef struct {
   int32_t num_multi_sink;  /* data edges whose last consumer depends on the order */
   int32_t smem_resident;   /* 1 when the fused scorer keeps per-candidate state in smem */
   uint64_t total_bytes;    /* Graph::total_bytes() (graph.hpp:93) */
+  int32_t orders16;        /* 1: host-buffer scoring sends orders as uint16 (half the bytes) */
+  int32_t reserved;
 } mp_graph_info;
 
 /* ---- context / graph lifetime --------------------------------------------- */

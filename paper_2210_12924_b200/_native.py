@@ -63,6 +63,8 @@ class MpGraphInfo(C.Structure):
         ("num_multi_sink", C.c_int32),
         ("smem_resident", C.c_int32),
         ("total_bytes", C.c_uint64),
+        ("orders16", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 

@@ -329,6 +329,8 @@ mp_status mp_graph_get_info(const mp_graph* g, mp_graph_info* info) {
   info->num_multi_sink = g->n_dyn;
   info->smem_resident = g->smem_resident ? 1 : 0;
   info->total_bytes = g->total_bytes;
+  info->orders16 = score_takes_u16(g) && !std::getenv("MP_NO_PACK16") ? 1 : 0;
+  info->reserved = 0;
   return MP_OK;
 }
 
