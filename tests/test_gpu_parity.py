@@ -509,6 +509,59 @@ def test_host_scoring_pipeline_chunks(planner):
     assert (hp.numpy().view(np.uint64) == res.peak).all() and (hv.numpy() == res.valid).all()
 
 
+def test_sizes_near_the_total_cap(planner):
+    """Byte sizes whose total approaches the reference's 2^62 cap (graph.cpp:122-128):
+    64-bit scan, peaks past the packed key's 2^43 (the host argmin falls back to the
+    device reduction; the device key reports MP_KEY_OVERFLOW), and the arena and
+    placement paths with 64-bit sizes - all equal to the C restatement."""
+    import json
+    import torch
+    rng = np.random.default_rng(7)
+    n = 40
+    nodes = [{"id": f"v{i}"} for i in range(n)]
+    edges = []
+    for i in range(1, n):
+        for j in rng.choice(i, size=min(i, 2), replace=False):
+            edges.append({"id": f"e{len(edges)}", "source": f"v{j}", "sinks": [f"v{i}"],
+                          "size": int(rng.integers(1 << 52, 1 << 55)) | 1})
+    g = mp.load_graph(json.dumps({"nodes": nodes, "edges": edges}))
+    total = sum(int(x) for x in g.edge_size)
+    assert (1 << 60) < total < (1 << 62)
+    orc = O.Oracle.from_csr(g.csr())
+    orders = mp.random_topo_orders(g, 300, seed=3)
+    orders[4, [0, 1]] = orders[4, [1, 0]]
+    res, best = planner.score_orders_best(g, orders)
+    peaks = []
+    for i, o in enumerate(orders):
+        lt = orc.lifetimes_from_order(o)
+        if lt is None:
+            assert res.valid[i] == 0
+            peaks.append(None)
+            continue
+        _, pr, ps = orc.timeline_from_lifetimes(lt[0], lt[1], g.n)
+        assert (int(res.peak[i]), int(res.peak_step[i])) == (pr, ps), i
+        peaks.append(pr)
+    exp = min((p, i) for i, p in enumerate(peaks) if p is not None)[1]
+    assert best == exp and int(res.peak[best]) >= (1 << 43)
+    d = torch.device("cuda:0")
+    dg = planner.upload(g)
+    key = torch.full((1,), (1 << 63) - 1, dtype=torch.int64, device=d)
+    z = [torch.zeros(300, dtype=t, device=d) for t in (torch.int64, torch.int32, torch.uint8)]
+    planner.score_orders_argmin_d(dg, torch.from_numpy(orders).to(d), 300, *z, key, 0,
+                                  torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert int(key.item()) == (1 << 63) - 2            # MP_KEY_OVERFLOW: use the fallback
+    mr, rs, fr, valid = planner.run_baseline_batch(g, orders[:20])
+    for i in range(20):
+        e = orc.run_baseline(orders[i])
+        assert (e is None and valid[i] == 0) or (int(mr[i]), int(rs[i]), float(fr[i])) == e
+    lo, hi = planner.lifetimes_from_order(g, orders[0])
+    tk, ta, _ = O.preallocate_pyramid(lo, hi, g.edge_size, g.id_rank()[:g.E])
+    ea, eh = O.greedy_pack(lo, hi, g.edge_size, tk, ta)
+    ga, gh, _, _ = planner.place_batch(g, lo[None], hi[None], pyramid=True)
+    assert (gh[0] == eh).all() and (ga[0][eh == 1] == ea[eh == 1]).all()
+
+
 def test_edge_cases(planner):
     empty = mp.load_graph('{"nodes": [], "edges": []}')
     assert planner.peak_resident_bytes(empty, []) == 0
