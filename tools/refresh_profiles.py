@@ -22,6 +22,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NCU_NOTES = {
     "ncu_c2_score": ("score_reg_kernel<u32, 8, 1>",
                      "DRAM traffic = algorithmic bytes; smem/issue-bound (DESIGN §3)"),
+    "ncu_c3_score": ("score_reg_kernel<u32, 8, 1>", "as C2: smem/issue-bound"),
+    "ncu_c4_score": ("score_reg_kernel<u64, 16, 1>", "64-bit sums, 128 registers, 2 CTAs/SM"),
     "ncu_c5_score": ("score_kernel (global scratch, 4-bit smem scan inputs)",
                      "scratch L2-resident; L1TEX random-access bound"),
     "ncu_c5_pairs": ("pair sweep fill (C5, 3.3e9 pairs)", "HBM writes of the pair list"),
