@@ -582,6 +582,8 @@ mp_status mp_score_orders_best(mp_ctx* ctx, const mp_graph* g, const int32_t* or
   const bool p16 = n > 0 && score_takes_u16(g) && !std::getenv("MP_NO_PACK16");
   uint16_t* d16 = reinterpret_cast<uint16_t*>(d_orders);
   const size_t half = n * (size_t)((C + nch - 1) / nch);
+  // a call that failed part-way may have left copies from the staging buffer queued
+  if (p16) MP_CUDA(cudaStreamSynchronize(ctx->copy_stream));
   if (p16 && ctx->h_stage_elems < half) {
     if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
     ctx->h_stage = nullptr;
