@@ -9,3 +9,8 @@ for n in 2 4; do
     > gpurun_out/mrr_$n.json 2> gpurun_out/mrr_$n.err
   echo "ref rc=$? n=$n"; tail -c 300 gpurun_out/mrr_$n.json
 done
+# the row-sharded pair sweep / validation (K2/K4) at N = 2 over gloo
+MP_DIST_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+  --master-addr 127.0.0.1 --master-port 29701 bench.py --mode pairs --config c3 --gpus 2 --steps 5 \
+  > gpurun_out/mrp_2.json 2> gpurun_out/mrp_2.err
+echo "pairs rc=$?"; tail -c 400 gpurun_out/mrp_2.json; tail -3 gpurun_out/mrp_2.err
