@@ -562,6 +562,28 @@ def test_sizes_near_the_total_cap(planner):
     assert (gh[0] == eh).all() and (ga[0][eh == 1] == ea[eh == 1]).all()
 
 
+def test_packed_orders_keep_out_of_range_ids_invalid(planner):
+    """The host call sends orders as uint16 for register-slot graphs: ids outside
+    [0, n) - negative, >= 65535, or in [n, 65535) - must still make the candidate
+    invalid (graph.cpp:241-248), and the rest must score as with int32 orders."""
+    g = mp.generate_graph("fork_join", 60, 100, 3)
+    dg = planner.upload(g)
+    assert dg.info()["orders16"] == 1
+    orders = mp.random_topo_orders(g, 40, seed=1)
+    bad_vals = {3: -5, 7: 70000, 11: 65535, 13: 65534, 17: g.n, 19: (1 << 31) - 1, 23: -(1 << 31)}
+    for r, v in bad_vals.items():
+        orders[r, r % g.n] = v
+    res = planner.score_orders(g, orders)
+    orc = O.Oracle.from_csr(g.csr())
+    for i, o in enumerate(orders):
+        if i in bad_vals:
+            assert res.valid[i] == 0, i
+            continue
+        lt = orc.lifetimes_from_order(o)
+        _, pr, ps = orc.timeline_from_lifetimes(lt[0], lt[1], g.n)
+        assert res.valid[i] == 1 and (int(res.peak[i]), int(res.peak_step[i])) == (pr, ps), i
+
+
 def test_edge_cases(planner):
     empty = mp.load_graph('{"nodes": [], "edges": []}')
     assert planner.peak_resident_bytes(empty, []) == 0
