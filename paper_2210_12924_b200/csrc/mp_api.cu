@@ -145,6 +145,8 @@ mp_status mp_ctx_create(int device, mp_ctx** out) {
     ce = cudaEventCreateWithFlags(&ctx->ev_h2d[i], cudaEventDisableTiming);
   if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming);
   if (ce == cudaSuccess) ce = cudaMallocHost(reinterpret_cast<void**>(&ctx->h_small), 64);
+  for (int i = 0; i < 2 && ce == cudaSuccess; ++i)
+    ce = cudaEventCreateWithFlags(&ctx->ev_d2h[i], cudaEventDisableTiming);
   if (ce != cudaSuccess) {
     mp_status s = cuda_status(ce, "mp_ctx_create");
     delete ctx;
@@ -165,6 +167,9 @@ mp_status mp_ctx_destroy(mp_ctx* ctx) {
   if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
   if (ctx->h_small) cudaFreeHost(ctx->h_small);
   if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+  if (ctx->h_bounce) cudaFreeHost(ctx->h_bounce);
+  for (cudaEvent_t e : ctx->ev_d2h)
+    if (e) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
@@ -541,6 +546,50 @@ void pack_orders16(const int32_t* src, uint16_t* dst, size_t cnt, uint32_t n) {
 }
 }  // namespace
 
+namespace mpb {
+// A large device result into caller (typically pageable) memory: chunks land in a
+// pinned double buffer at PCIe speed and the host cores copy each one out while
+// the next is in flight, instead of the driver's single-threaded pageable staging.
+// Synchronises `st`.
+mp_status d2h_large(mp_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  constexpr size_t kChunk = size_t{4} << 20;
+  if (bytes < 2 * kChunk) {
+    MP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+    MP_CUDA(cudaStreamSynchronize(st));
+    return MP_OK;
+  }
+  if (!ctx->h_bounce) MP_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_bounce), 2 * kChunk));
+  static const int nthr = [] {
+    const int hw = (int)std::thread::hardware_concurrency();
+    return hw < 1 ? 1 : hw < 16 ? hw : 16;
+  }();
+  const size_t nch = (bytes + kChunk - 1) / kChunk;
+  auto issue = [&](size_t i) -> mp_status {
+    const size_t off = i * kChunk, len = bytes - off < kChunk ? bytes - off : kChunk;
+    MP_CUDA(cudaMemcpyAsync(ctx->h_bounce + (i & 1) * kChunk,
+                            static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost, st));
+    MP_CUDA(cudaEventRecord(ctx->ev_d2h[i & 1], st));
+    return MP_OK;
+  };
+  MP_TRY(issue(0));
+  for (size_t i = 0; i < nch; ++i) {
+    if (i + 1 < nch) MP_TRY(issue(i + 1));  // its half was drained in iteration i - 1
+    MP_CUDA(cudaEventSynchronize(ctx->ev_d2h[i & 1]));
+    const size_t off = i * kChunk, len = bytes - off < kChunk ? bytes - off : kChunk;
+    const char* from = ctx->h_bounce + (i & 1) * kChunk;
+    char* to = static_cast<char*>(dst) + off;
+    const int64_t parts = nthr;
+#pragma omp parallel for num_threads(nthr) schedule(static)
+    for (int64_t t = 0; t < parts; ++t) {
+      const size_t b = len * (size_t)t / (size_t)parts, e = len * (size_t)(t + 1) / (size_t)parts;
+      std::memcpy(to + b, from + b, e - b);
+    }
+  }
+  MP_CUDA(cudaStreamSynchronize(st));
+  return MP_OK;
+}
+}  // namespace mpb
+
 mp_status mp_score_orders_best(mp_ctx* ctx, const mp_graph* g, const int32_t* orders, int64_t C,
                                uint64_t* peak, int32_t* step, uint8_t* valid, int64_t* best) {
   if (!ctx || !g || C < 0) return invalid_arg("null argument or negative count");
@@ -738,9 +787,7 @@ static mp_status pair_sweep_h(mp_ctx* ctx, int mode, int32_t E, const int32_t* l
   MP_TRY(ctx->scratch[1].reserve((size_t)total * 8 + 256));
   int32_t* d_out = static_cast<int32_t*>(ctx->scratch[1].ptr);
   MP_TRY(pairs_fill(a, ctx->num_sms, ctx->scratch[2].ptr, d_row_off, d_out, st));
-  MP_CUDA(cudaMemcpyAsync(out, d_out, (size_t)total * 8, cudaMemcpyDeviceToHost, st));
-  MP_CUDA(cudaStreamSynchronize(st));
-  return MP_OK;
+  return d2h_large(ctx, out, d_out, (size_t)total * 8, st);
 }
 
 mp_status mp_overlap_pairs(mp_ctx* ctx, int32_t E, const int32_t* lo, const int32_t* hi,
@@ -1000,9 +1047,7 @@ mp_status mp_joint_pairs(mp_ctx* ctx, const mp_graph* g, int filter, int32_t* pa
   MP_TRY(ctx->scratch[4].reserve(8 * (size_t)total + 256));
   int2* d_pairs = static_cast<int2*>(ctx->scratch[4].ptr);
   MP_TRY(launch_joint(a, ctx->num_sms, nullptr, d_off, d_pairs, st));
-  MP_CUDA(cudaMemcpyAsync(pairs, d_pairs, 8 * (size_t)total, cudaMemcpyDeviceToHost, st));
-  MP_CUDA(cudaStreamSynchronize(st));
-  return MP_OK;
+  return d2h_large(ctx, pairs, d_pairs, 8 * (size_t)total, st);
 }
 
 // ---- LP row emission (K7) ---------------------------------------------------------

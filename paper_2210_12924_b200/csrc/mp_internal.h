@@ -57,6 +57,8 @@ struct mp_ctx {
   uint64_t* h_small = nullptr;  // pinned: [0] key init, [1] key read-back
   uint16_t* h_stage = nullptr;  // pinned: two halves of 16-bit packed orders
   size_t h_stage_elems = 0;     // per half
+  char* h_bounce = nullptr;     // pinned: two halves for large results to pageable memory
+  cudaEvent_t ev_d2h[2] = {};
 };
 
 // Several contexts in one process, the graph replicated on each (mp_score_orders_multi).
