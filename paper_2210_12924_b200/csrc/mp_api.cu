@@ -1410,7 +1410,7 @@ mp_status mp_place(mp_ctx* ctx, int32_t E, int64_t B, const int32_t* lo, const i
   MP_TRY(mp_place_d(ctx, E, B, d_lo, d_hi, d_size, id_rank ? d_rank : nullptr,
                     fixed ? d_fixed : nullptr, fixed ? d_faddr : nullptr, flags, d_addr, d_has,
                     d_peak, d_base, st));
-  MP_CUDA(cudaMemcpyAsync(addr, d_addr, 8 * be, cudaMemcpyDeviceToHost, st));
+  MP_TRY(d2h_large(ctx, addr, d_addr, 8 * be, st));  // the address plans: B x E x 8 bytes
   MP_CUDA(cudaMemcpyAsync(has_addr, d_has, be, cudaMemcpyDeviceToHost, st));
   if (peak_mem) MP_CUDA(cudaMemcpyAsync(peak_mem, d_peak, 8 * b, cudaMemcpyDeviceToHost, st));
   if (pyramid_base)
