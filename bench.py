@@ -10,11 +10,13 @@ argmin folded in). At N>1 every rank scores its own batch (weak scaling,
 disjoint candidate index ranges) and the best plan is chosen with ONE NCCL
 allreduce(min) on a packed (peak, index) key, inside the timed region.
 
-  python bench.py [--config c2|c4|c5] [--gpus N] [--steps K] [--warmup W]
+  python bench.py [--config c2|c3|c4|c5] [--gpus N] [--steps K] [--warmup W]
   python bench.py --impl reference ...   # the reference's own CPU scorer
 
-Default config c2 = ResNet-50 fwd+bwd+SGD training graph, batch 32
-(workloads/graphs/resnet50_b32.json.gz), 4,096 candidates per GPU.
+Default config c5 = the north star's 100k-tensor graph: the reference's own
+generator, training_like L=33,333 (n=133,336 nodes, E=100,002 tensors,
+generate.cpp:101-158), 1,024 candidates per GPU. c2/c3/c4 are the traced
+ResNet-50 / BERT-base / GPT-2-medium training graphs (workloads/graphs/).
 """
 from __future__ import annotations
 
@@ -46,12 +48,31 @@ CONFIGS = {
 }
 
 
+def graph_text(cfg):
+    with gzip.open(os.path.join(ROOT, "workloads", "graphs", cfg["graph"]), "rt") as f:
+        return f.read()
+
+
 def load_graph(cfg):
     import paper_2210_12924_b200 as mp
     if "generate" in cfg:
         return mp.generate_graph(*cfg["generate"])
-    with gzip.open(os.path.join(ROOT, "workloads", "graphs", cfg["graph"]), "rt") as f:
-        return mp.load_graph(f.read())
+    return mp.load_graph(graph_text(cfg))
+
+
+def bench_config(cfg, n, E, S, C, world, backend="nccl"):
+    """The `config` object both arms print (identical keys and values)."""
+    batch_bytes = C * n * 4
+    nb = max(1, -(-2 * L2_BYTES // batch_bytes))
+    return {"workload": cfg["workload"], "nodes": n, "edges": E, "sinks": S,
+            "candidates_per_gpu": C,
+            "candidate_source": "seeded random topological orders (randomised Kahn, "
+                                "splitmix64 per candidate)",
+            "l2": f"inputs larger than L2: {nb} rotating batch(es) of "
+                  f"{batch_bytes / 2**20:.1f} MiB ({nb * batch_bytes / 2**20:.0f} MiB > 126 MiB L2)",
+            "parallelism": f"dp{world} (candidates sharded, 1 allreduce-min)" +
+                           ("" if backend == "nccl" or world == 1 else
+                            f" [{backend}: functional check]")}
 
 
 # ---- clocks (NVML, sampled in a thread during the timed region) ----------------------
@@ -159,45 +180,52 @@ def smem_pipe_use(config, kernel_ms, sm_mhz, num_sms):
 
 # ---- reference arm -------------------------------------------------------------------
 def run_reference(args, cfg):
+    """The reference's own CPU path (oracle/_ref = /root/reference/proj compiled by
+    oracle/Makefile): memplan::peak_resident_bytes per candidate + first-min argmin, on
+    all host threads. The graph comes from the reference itself (its generator, or its
+    JSON loader for the traced graphs) and the candidates from a harness function of
+    oracle/_ref: this process never loads the product library."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
-    import paper_2210_12924_b200 as mp
     if not O.ref_available():
         print(json.dumps({"impl": "reference",
                           "unavailable": "oracle/_ref/libmemplan_ref.so not built"}))
         return 0
-    g = load_graph(cfg)
-    rg = O.RefGraph.load(mp.save_graph(g))
+    if "generate" in cfg:
+        kind, layers, size = cfg["generate"]
+        rg = O.RefGraph.generate(kind, layers, size)
+    else:
+        rg = O.RefGraph.load(graph_text(cfg))
     threads = os.cpu_count() or 1
-    orders = mp.random_topo_orders(g, min(cfg["candidates"], 4096), seed=12345)
-    # calibrate: bounded sample per step so the whole run ends within a few minutes
+    C = cfg["candidates"]
+    # calibrate: a bounded sample per step so the whole run ends within a few minutes
+    probe = rg.random_topo_orders(threads, seed=12345, threads=threads)
     t = time.perf_counter()
-    rg.score_orders(orders[:threads], threads=threads)
-    per = (time.perf_counter() - t) / threads * threads  # seconds per `threads` candidates
+    rg.score_orders(probe, threads=threads)
+    per = time.perf_counter() - t              # seconds per `threads` candidates
     budget = 90.0 / max(args.steps + args.warmup, 1)
-    m = int(max(threads, min(len(orders), threads * budget / max(per, 1e-9))))
-    sample = orders[:m]
+    m = int(max(threads, min(C, threads * budget / max(per, 1e-9))))
+    sample = rg.random_topo_orders(m, seed=12345, threads=threads)
     for _ in range(args.warmup):
         rg.score_orders(sample, threads=threads)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        peak, valid, best = rg.score_orders(sample, threads=threads)
+        rg.score_orders(sample, threads=threads)
     dt = time.perf_counter() - t0
     value = m * args.steps / dt
+    S = int(rg.S)
     line = {
         "impl": "reference", "metric": METRIC, "value": value,
         "unit": "plans/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "nodes": g.n, "edges": g.E,
-                   "sinks": int(len(g.sinks)), "candidates_per_step": m,
-                   "candidate_source": "seeded random topological orders (randomised Kahn)"},
+        "config": bench_config(cfg, rg.n, rg.E, S, C, args.gpus),
         "cpu_baseline": {"value": value, "unit": "plans/s", "cores": threads, "kind": "reference",
-                         "sample": f"{m} random topological orders per step, memplan::"
-                                   f"peak_resident_bytes per order + first-min argmin, "
+                         "sample": f"{m} of the {C} candidates per step (seeded randomised Kahn), "
+                                   f"memplan::peak_resident_bytes per order + first-min argmin, "
                                    f"{threads} host threads"},
         "e2e": {"value": value, "unit": "plans/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -229,6 +257,65 @@ def cpu_baseline(g, orders, seconds=10.0):
             "sample": f"{m} of the step's candidate orders x {reps} passes ({dt:.1f} s), reference "
                       f"memplan::peak_resident_bytes (oracle/_ref, -O3) on {threads} host "
                       "threads + first-min argmin"}
+
+
+SCORERS = {1: "register slots, state in smem", 2: "node tables, state in smem",
+           3: "warp per candidate", 4: "per-CTA global position scratch",
+           5: "node-partitioned passes, positions in smem"}
+
+
+def scorer_variant(info):
+    return SCORERS.get(info.get("score_variant"), "unknown")
+
+
+def check_timed_rows(g, orders, peak, step, valid, key, base, world, rows=64):
+    """Parity of the last timed step: `rows` candidates spread over the batch (plus
+    the batch's argmin) against the reference itself (oracle/_ref:
+    memplan::peak_resident_bytes; InvalidOrder for the verdict) and the peak step
+    against the C restatement of timeline_from_lifetimes (plan.cpp:122-143); the
+    device key against the first minimum over the device results."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    import paper_2210_12924_b200 as mp
+    from paper_2210_12924_b200 import dist as D
+    pk = peak.cpu().numpy().view(np.uint64)
+    st = step.cpu().numpy()
+    vl = valid.cpu().numpy()
+    kp = key.cpu().tolist()
+    C = len(pk)
+    ok_idx = np.nonzero(vl)[0]
+    best = int(ok_idx[np.lexsort((ok_idx, pk[ok_idx]))[0]]) if len(ok_idx) else -1
+    key_ok = True
+    if world == 1 and not D.key_overflowed(kp):
+        key_ok = D.unpack_key(kp[0]) == ((int(pk[best]), best + base) if best >= 0 else (0, -1))
+    pick = sorted(set(np.linspace(0, C - 1, rows).astype(int).tolist() + ([best] if best >= 0 else [])))
+    out = {"rows": len(pick), "checked_against": "oracle/_ref (peak, verdict) + C restatement "
+           "(peak_step)", "key_consistent": bool(key_ok)}
+    if not O.ref_available():
+        out["skipped"] = "oracle/_ref not built"
+        return out
+    rg = O.RefGraph.load(mp.save_graph(g))
+    sub = np.ascontiguousarray(orders[pick])
+    rp, rv, rbest = rg.score_orders(sub, threads=os.cpu_count() or 1)
+    orc = O.Oracle.from_csr(g.csr())
+    mism = 0
+    for r, c in enumerate(pick):
+        if int(rv[r]) != int(vl[c]) or (rv[r] and int(rp[r]) != int(pk[c])):
+            mism += 1
+            continue
+        if rv[r]:
+            lo, hi = orc.lifetimes_from_order(sub[r])
+            pr, ps = O.timeline_peak(lo, hi, g.edge_size, g.n)
+            if (pr, ps) != (int(pk[c]), int(st[c])):
+                mism += 1
+    sub_best = pick[rbest] if rbest >= 0 else -1
+    dev_sub = [c for c in pick if vl[c]]
+    dev_sub_best = min(dev_sub, key=lambda c: (int(pk[c]), c)) if dev_sub else -1
+    out.update({"mismatches": mism, "argmin_of_rows_matches": sub_best == dev_sub_best,
+                "ok": mism == 0 and sub_best == dev_sub_best and key_ok})
+    if not out["ok"]:
+        raise AssertionError(f"timed-batch parity failed: {out}")
+    return out
 
 
 # ---- pairs / validation (K2, K4) ------------------------------------------------------
@@ -688,7 +775,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--place-batch", type=int, default=4096)
     ap.add_argument("--mode", default="score", choices=["score", "pairs", "place", "arena", "lp", "joint"],
                     help="score: candidate scoring (the headline); pairs: overlap-pair "
@@ -751,16 +838,15 @@ def main():
     peak = torch.zeros(C, dtype=torch.int64, device=dev)
     step = torch.zeros(C, dtype=torch.int32, device=dev)
     valid = torch.zeros(C, dtype=torch.uint8, device=dev)
-    key = torch.zeros(1, dtype=torch.int64, device=dev)
+    key = torch.zeros(2, dtype=torch.int64, device=dev)   # {key, overflow}
     base = rank * C
 
     def one_step(b):
-        key.fill_(D.NO_KEY)  # MP_KEY_NONE, the atomicMin identity
+        planner.key_reset_d(key, stream.cuda_stream)       # memset: {MP_KEY_NONE, no overflow}
         planner.score_orders_argmin_d(dg, batches[b % nb], C, peak, step, valid, key, base,
                                       stream.cuda_stream)
         if world > 1:
-            k = key.view(torch.int64)
-            dist.all_reduce(k, op=dist.ReduceOp.MIN)
+            dist.all_reduce(key, op=dist.ReduceOp.MIN)
 
     for i in range(args.warmup):
         one_step(i)
@@ -771,7 +857,7 @@ def main():
     ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     torch.cuda.synchronize()
     for i in range(args.steps):
-        key.fill_(D.NO_KEY)
+        planner.key_reset_d(key, stream.cuda_stream)
         ev_s[i].record(stream)
         planner.score_orders_argmin_d(dg, batches[i % nb], C, peak, step, valid, key, base,
                                       stream.cuda_stream)
@@ -787,7 +873,7 @@ def main():
         with torch.cuda.graph(graph, stream=stream):
             cap = torch.cuda.current_stream().cuda_stream
             for i in range(args.steps):
-                key.fill_(D.NO_KEY)
+                planner.key_reset_d(key, cap)             # a memset node, not a kernel
                 planner.score_orders_argmin_d(dg, batches[i % nb], C, peak, step, valid, key,
                                               base, cap)
         run_timed = graph.replay
@@ -796,9 +882,10 @@ def main():
         for b in range(nb):
             gb = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gb, stream=stream):
-                key.fill_(D.NO_KEY)
+                cap = torch.cuda.current_stream().cuda_stream
+                planner.key_reset_d(key, cap)
                 planner.score_orders_argmin_d(dg, batches[b], C, peak, step, valid, key, base,
-                                              torch.cuda.current_stream().cuda_stream)
+                                              cap)
             graphs.append(gb)
 
         def run_timed():
@@ -807,7 +894,6 @@ def main():
                 dist.all_reduce(key, op=dist.ReduceOp.MIN)
     run_timed()                           # warm replay (untimed)
     torch.cuda.synchronize()
-    kk = D.check_device_key(int(key.item()))  # last step's global first-minimum key
 
     clocks = ClockSampler(dev)
     clocks.start()
@@ -826,6 +912,14 @@ def main():
     t1 = time.perf_counter()
     clocks.stop()
     total_ms = start.elapsed_time(end)
+    # parity of the LAST timed step (its batch's results are still in peak/step/valid
+    # and key): rank 0 checks 64 of its rows and the batch argmin against the reference
+    last_b = (args.steps - 1) % nb
+    parity = None
+    if rank == 0:
+        parity = check_timed_rows(g, host_batches[last_b], peak, step, valid, key, base,
+                                  world)
+
     t = torch.tensor([total_ms, kern_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -859,10 +953,10 @@ def main():
     for i in range(e2e_steps):
         best = planner.score_orders_into(dg, pinned[i % len(pinned)].numpy(), h_peak, h_step, h_valid)
         if world > 1:
-            kv = D.pack_key(int(h_peak[best]), best + base) if best >= 0 else D.NO_KEY
-            bk = torch.tensor([kv], device=dev)
-            dist.all_reduce(bk, op=dist.ReduceOp.MIN)
-            bk.item()
+            kv = D.key_pair(int(h_peak[best]), best + base) if best >= 0 else [D.NO_KEY] * 2
+            bk = torch.tensor(kv, device=dev)
+            D.global_argmin(bk, int(h_peak[best]) if best >= 0 else 0,
+                            best + base if best >= 0 else -1)
     te = torch.tensor([time.perf_counter() - te0], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -876,6 +970,7 @@ def main():
     torch.cuda.synchronize()
     h2d_gbs = 5 * batch_bytes / (time.perf_counter() - th) / 1e9
 
+    wire_bytes = batch_bytes // 2 if info["orders16"] else batch_bytes
     line = None
     if rank == 0:
         cpu = None
@@ -886,15 +981,8 @@ def main():
             "value": value, "unit": "plans/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "nodes": n, "edges": g.E,
-                       "sinks": int(len(g.sinks)), "candidates_per_gpu": C,
-                       "candidate_source": "seeded random topological orders (randomised Kahn)",
-                       "l2": f"inputs larger than L2: {nb} rotating batches of "
-                             f"{batch_bytes / 2**20:.1f} MiB ({nb * batch_bytes / 2**20:.0f} MiB"
-                             " > 126 MiB L2)",
-                       "parallelism": f"dp{world} (candidates sharded, 1 allreduce-min)" +
-                       ("" if backend == "nccl" or world == 1 else f" [{backend}: functional check]"),
-                       "smem_resident": bool(info["smem_resident"])},
+            "config": bench_config(cfg, n, g.E, int(len(g.sinks)), C, world, backend),
+            "scorer": {"variant": scorer_variant(info), "smem_resident": bool(info["smem_resident"])},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
                          "frac": achieved / peak_gbs, "traffic": profile_traffic(args.config),
                          "kernel": "score_kernel (K1+K3 fused + argmin)",
@@ -908,16 +996,21 @@ def main():
                     else "int32",
                     "d2h_bytes_per_step": C * 13 + 8,
                     "path": "Planner.score_orders_into -> mp_score_orders_best (pinned host)",
-                    "torch_pinned_h2d_gbs": h2d_gbs},
+                    "torch_pinned_h2d_gbs": h2d_gbs,
+                    # PCIe roofline of the e2e leg: wire bytes per step over the e2e step
+                    # time, against torch's own pinned H2D copy rate on this box
+                    "pcie": {"achieved_gbs": wire_bytes * e2e_value / (world * C) / 1e9,
+                             "peak_gbs": h2d_gbs,
+                             "frac": wire_bytes * e2e_value / (world * C) / 1e9 / h2d_gbs}},
             "gpu_launches": args.steps,
             "timing": ("K steps captured as one CUDA graph" if world == 1 else
                        "per-batch CUDA graph per step + eager NCCL allreduce(min)") +
                       ", CUDA events on the step stream; kernel_ms = in-graph step time",
             "clocks": clocks.summary(t0, t1),
-            "best_key_check": kk != D.NO_KEY,
         }
         if cpu:
             line["cpu_baseline"] = cpu
+        line["parity_rows"] = parity
         sm_mhz = (line["clocks"] or {}).get("sm_mhz") or 1965
         bind = smem_pipe_use(args.config, kern_graph_ms, float(sm_mhz),
                              torch.cuda.get_device_properties(dev).multi_processor_count)

@@ -73,8 +73,13 @@ typedef struct {
   int32_t smem_resident;   /* 1 when the fused scorer keeps per-candidate state in smem */
   uint64_t total_bytes;    /* Graph::total_bytes() (graph.hpp:93) */
   int32_t orders16;        /* 1: host-buffer scoring sends orders as uint16 (half the bytes) */
-  int32_t reserved;
+  int32_t score_variant;   /* MP_SCORER_*: which fused-scorer formulation the graph got */
 } mp_graph_info;
+#define MP_SCORER_REG 1      /* register slots, per-candidate state in smem (n up to ~8k) */
+#define MP_SCORER_SMEM 2     /* node tables from global, state in smem (n < 65536) */
+#define MP_SCORER_WARP 3     /* warp per candidate (opt-in, n <= 2048) */
+#define MP_SCORER_SCRATCH 4  /* per-CTA global position scratch (large graphs) */
+#define MP_SCORER_PARTS 5    /* node-partitioned passes, positions in smem (large graphs) */
 
 /* ---- context / graph lifetime --------------------------------------------- */
 int mp_abi_version(void);
@@ -143,15 +148,19 @@ mp_status mp_score_orders_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_ord
 mp_status mp_score_orders_best(mp_ctx* ctx, const mp_graph* g, const int32_t* orders,
                                int64_t num_orders, uint64_t* peak, int32_t* peak_step,
                                uint8_t* valid, int64_t* best);
-/* Device variant of the fused form: every valid candidate c does
- * atomicMin(d_best_key, peak << 20 | (c + index_base)); the caller sets
- * *d_best_key = MP_KEY_NONE beforehand (stream-ordered). Keys that do not
- * fit (peak >= 2^43 or index >= 2^20) are recorded as MP_KEY_OVERFLOW,
- * telling the caller to fall back to mp_argmin_key_d. Keys are non-negative
- * int64 values, so the minimum key across GPUs (one int64 allreduce(MIN))
- * is the global first-minimum. */
-#define MP_KEY_NONE 0x7fffffffffffffffull
-#define MP_KEY_OVERFLOW 0x7ffffffffffffffeull
+/* Device variant of the fused form. d_best_key points to TWO words
+ * {key, overflow}, reset to {MP_KEY_NONE, MP_KEY_NONE} by one byte memset
+ * (mp_key_reset_d, stream-ordered; a memset node inside a CUDA graph). Every
+ * valid candidate c with peak < 2^42 and c + index_base < 2^20 does
+ * atomicMin(&key, peak << 20 | (c + index_base)); any other valid candidate
+ * sets overflow = 0, telling the caller to fall back to mp_argmin_key_d.
+ * Both words are non-negative int64 values, so one int64 allreduce(MIN) of
+ * the pair across GPUs yields the global first-minimum AND whether any shard
+ * overflowed. */
+#define MP_KEY_NONE 0x7f7f7f7f7f7f7f7full
+#define MP_KEY_OVERFLOW 0x7f7f7f7f7f7f7f7eull /* mp_argmin_key_d d_out3[2] only */
+#define MP_KEY_MAX_PEAK (1ull << 42)
+mp_status mp_key_reset_d(mp_ctx* ctx, uint64_t* d_best_key, void* stream);
 mp_status mp_score_orders_argmin_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_orders,
                                    int64_t num_orders, uint64_t* d_peak, int32_t* d_peak_step,
                                    uint8_t* d_valid, uint64_t* d_best_key, int64_t index_base,
@@ -162,7 +171,7 @@ mp_status mp_argmin(mp_ctx* ctx, const uint64_t* peak, const uint8_t* valid, int
                     int64_t* best);
 /* Device variant (one CTA): d_out3[0] = best index + index_base (or -1),
  * d_out3[1] = its peak, d_out3[2] = packed key peak << 20 | index
- * (MP_KEY_NONE when nothing is valid, MP_KEY_OVERFLOW when peak >= 2^43 or
+ * (MP_KEY_NONE when nothing is valid, MP_KEY_OVERFLOW when peak >= 2^42 or
  * index >= 2^20). index_base makes keys of different GPU shards comparable. */
 mp_status mp_argmin_key_d(mp_ctx* ctx, const uint64_t* d_peak, const uint8_t* d_valid,
                           int64_t num_orders, int64_t index_base, uint64_t* d_out3,

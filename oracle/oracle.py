@@ -177,6 +177,28 @@ class Oracle:
         return lo, hi
 
 
+def timeline_peak(lo, hi, size, horizon):
+    """(peak_rs, peak_step) of timeline_from_lifetimes (plan.cpp:122-143) in O(E + h):
+    RS(t) = sum of size over lo <= t <= hi as a difference array + prefix sum, then
+    the first strict maximum (1 when all zero and horizon > 0, 0 when horizon == 0).
+    Same definition as or_timeline_from_lifetimes (its literal O(h*E) loop is too
+    slow at 100k tensors); tests/test_oracle_golden.py checks the two agree."""
+    if horizon <= 0:
+        return 0, 0
+    lo = np.asarray(lo, np.int64)
+    hi = np.asarray(hi, np.int64)
+    sz = np.asarray(size, np.uint64).astype(np.int64)   # totals < 2^62 (graph.cpp:122-128)
+    d = np.zeros(horizon + 2, np.int64)
+    a = np.clip(lo, 1, horizon + 1)
+    b = np.clip(hi + 1, 1, horizon + 1)
+    keep = (lo <= hi) & (sz > 0) & (lo <= horizon)
+    np.add.at(d, a[keep], sz[keep])
+    np.add.at(d, b[keep], -sz[keep])
+    rs = np.cumsum(d)[1:horizon + 1]
+    best = int(rs.max())
+    return best, (int(np.argmax(rs)) + 1 if best > 0 else 1)
+
+
 def overlap_pairs(lo, hi, size, pinned=None, want_pairs=True):
     lo = np.ascontiguousarray(lo, np.int32)
     hi = np.ascontiguousarray(hi, np.int32)
@@ -295,6 +317,7 @@ def rlib():
         lib.ref_peak_resident_bytes.argtypes = [_vp, _i32p, C.c_int64, C.POINTER(C.c_uint64)]
         lib.ref_score_orders.argtypes = [_vp, _i32p, C.c_int64, C.c_int64, _u64p, _u8p, C.c_int,
                                          C.POINTER(C.c_int64)]
+        lib.ref_random_topo_orders.argtypes = [_vp, C.c_int64, C.c_uint64, C.c_int, _i32p]
         lib.ref_timeline_from_lifetimes.argtypes = [_vp, _i32p, _i32p, C.c_int32, _vp,
                                                     C.POINTER(C.c_uint64), C.POINTER(C.c_int32)]
         lib.ref_realized_lifetimes.argtypes = [_vp, _i32p, C.c_int32, _i32p, _i32p]
@@ -413,6 +436,13 @@ class RefGraph:
         p = C.c_uint64()
         _check(rlib().ref_peak_resident_bytes(self._h, o, o.size, C.byref(p)))
         return int(p.value)
+
+    def random_topo_orders(self, num_orders, seed=0, threads=1):
+        """Seeded randomised-Kahn candidates (input preparation for the reference arm;
+        the same draws as paper_2210_12924_b200.random_topo_orders)."""
+        out = np.zeros((num_orders, self.n), np.int32)
+        _check(rlib().ref_random_topo_orders(self._h, num_orders, seed, threads, out))
+        return out
 
     def score_orders(self, orders, threads=1):
         orders = np.ascontiguousarray(orders, np.int32)

@@ -254,6 +254,64 @@ int ref_score_orders(const void* gp, const int32_t* orders, int64_t num_orders,
   return status;
 }
 
+// Input preparation for bench.py's reference arm (so that arm never loads the
+// product library): seeded random topological orders of a reference Graph,
+// randomised Kahn over the (edge, sink) multigraph with one splitmix64 stream
+// per candidate - the same draws as mp_random_topo_orders, so both arms score
+// identical candidates. Not part of the reference; not timed.
+int ref_random_topo_orders(const void* gp, int64_t num_orders, uint64_t seed, int threads,
+                           int32_t* out) {
+  const Graph& g = *static_cast<const Graph*>(gp);
+  const int32_t n = g.num_nodes(), E = g.num_edges();
+  std::vector<int32_t> indeg(n, 0), off(n + 1, 0), succ;
+  for (int32_t e = 0; e < E; ++e) {
+    off[g.source_of(e) + 1] += (int32_t)g.sinks_of(e).size();
+    for (NodeIndex s : g.sinks_of(e)) ++indeg[s];
+  }
+  for (int32_t v = 0; v < n; ++v) off[v + 1] += off[v];
+  succ.resize(off[n]);
+  {
+    std::vector<int32_t> fill(off.begin(), off.end() - 1);
+    for (int32_t e = 0; e < E; ++e)
+      for (NodeIndex s : g.sinks_of(e)) succ[fill[g.source_of(e)]++] = s;
+  }
+  std::atomic<int> status{REF_OK};
+  auto work = [&](int64_t c0, int64_t c1) {
+    std::vector<int32_t> deg, ready;
+    for (int64_t c = c0; c < c1; ++c) {
+      uint64_t st = seed * 0xD1B54A32D192ED03ull + (uint64_t)c * 0x9E3779B97F4A7C15ull + 1;
+      deg = indeg;
+      ready.clear();
+      for (int32_t v = 0; v < n; ++v)
+        if (deg[v] == 0) ready.push_back(v);
+      int32_t* row = out + c * (int64_t)n;
+      int32_t k = 0;
+      while (!ready.empty()) {
+        uint64_t z = (st += 0x9E3779B97F4A7C15ull);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const size_t pick = (size_t)(z % ready.size());
+        const int32_t v = ready[pick];
+        ready[pick] = ready.back();
+        ready.pop_back();
+        row[k++] = v;
+        for (int32_t q = off[v]; q < off[v + 1]; ++q)
+          if (--deg[succ[q]] == 0) ready.push_back(succ[q]);
+      }
+      if (k != n) status = REF_UNKNOWN;
+    }
+  };
+  if (threads < 1) threads = 1;
+  if (threads > num_orders) threads = (int)std::max<int64_t>(1, num_orders);
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; ++t)
+    pool.emplace_back(work, num_orders * t / threads, num_orders * (t + 1) / threads);
+  work(0, num_orders / threads);
+  for (auto& th : pool) th.join();
+  return status;
+}
+
 int ref_timeline_from_lifetimes(const void* gp, const int32_t* lo,
                                 const int32_t* hi, int32_t horizon,
                                 uint64_t* bytes, uint64_t* peak_rs,

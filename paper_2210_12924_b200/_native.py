@@ -33,7 +33,7 @@ EXPORTS = [
     "mp_lifetimes", "mp_lifetimes_d", "mp_realized_lifetimes",
     "mp_resident_bytes", "mp_peak_resident_bytes", "mp_timeline",
     "mp_score_orders", "mp_score_orders_d", "mp_score_orders_best", "mp_score_orders_argmin_d",
-    "mp_argmin", "mp_argmin_key_d",
+    "mp_argmin", "mp_argmin_key_d", "mp_key_reset_d",
     "mp_overlap_pairs", "mp_overlap_pairs_d",
     "mp_validate_pairs", "mp_validate_pairs_d", "mp_addresses_feasible", "mp_peak_mem",
     "mp_fragmentation", "mp_generate_graph", "mp_random_topo_orders",
@@ -64,7 +64,7 @@ class MpGraphInfo(C.Structure):
         ("smem_resident", C.c_int32),
         ("total_bytes", C.c_uint64),
         ("orders16", C.c_int32),
-        ("reserved", C.c_int32),
+        ("score_variant", C.c_int32),
     ]
 
 
@@ -111,6 +111,7 @@ def lib():
             "mp_score_orders_argmin_d": (C.c_int, [vp, vp, vp, i64, vp, vp, vp, vp, i64, vp]),
             "mp_argmin": (C.c_int, [vp, vp, vp, i64, P(i64)]),
             "mp_argmin_key_d": (C.c_int, [vp, vp, vp, i64, i64, vp, vp]),
+            "mp_key_reset_d": (C.c_int, [vp, vp, vp]),
             "mp_overlap_pairs": (C.c_int, [vp, i32, vp, vp, vp, vp, vp, i64, P(i64)]),
             "mp_overlap_pairs_d": (C.c_int, [vp, i32, vp, vp, vp, vp, i64, i64, vp, vp, i64,
                                              P(i64), vp]),

@@ -49,19 +49,17 @@ def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB
     common = ["-O3", "-std=c++17", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
               "-Xcompiler", "-fPIC,-Wall,-fopenmp", *defines]
     objs = []
-    log = []
-    for src in CU_SOURCES:
+    jobs = []
+    for src in CU_SOURCES + CPP_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(objdir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            log.append(_run([NVCC, *ARCH, "-lineinfo", "-Xptxas", "-v", *common, "-c", s, "-o", o]))
-    for src in CPP_SOURCES:
-        s = os.path.join(CSRC, src)
-        o = os.path.join(objdir, src + ".o")
-        objs.append(o)
-        if force or _stale(o, [s] + headers):
-            log.append(_run([NVCC, *ARCH, *common, "-c", s, "-o", o]))
+            extra = ["-lineinfo", "-Xptxas", "-v"] if src.endswith(".cu") else []
+            jobs.append([NVCC, *ARCH, *extra, *common, "-c", s, "-o", o])
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        log = list(ex.map(_run, jobs))
     if force or _stale(lib, objs):
         log.append(_run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs,
                          "-lpthread", "-lgomp"]))

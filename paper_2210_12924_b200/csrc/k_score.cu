@@ -42,10 +42,19 @@ namespace mpb {
 namespace {
 
 constexpr int kWarp = 32;
-// Packed argmin keys stay non-negative as int64 so an NCCL int64 MIN works:
-// identity (no valid candidate) INT64_MAX, overflow marker INT64_MAX - 1.
-constexpr unsigned long long kKeyNone = 0x7fffffffffffffffull;
-constexpr unsigned long long kKeyOverflow = 0x7ffffffffffffffeull;
+// Packed argmin keys stay non-negative as int64 so an NCCL int64 MIN works.
+// The fused key is two words {key, overflow}, both reset by one byte memset
+// (0x7f): word 0 takes atomicMin(peak << 20 | index) for keys that fit (peak
+// < 2^42, index < 2^20), word 1 drops to 0 when any candidate's key did not
+// fit, so a MIN-reduction over shards can never hide an overflow.
+constexpr unsigned long long kKeyNone = 0x7f7f7f7f7f7f7f7full;
+constexpr unsigned long long kKeyOverflow = 0x7f7f7f7f7f7f7f7eull;  // mp_argmin_key_d out[2]
+constexpr uint64_t kKeyMaxPeak = 1ull << 42;
+
+__device__ __forceinline__ void record_key(unsigned long long* key, uint64_t pk, uint64_t gi) {
+  if (pk < kKeyMaxPeak && gi < (1ull << 20)) atomicMin(key, (unsigned long long)((pk << 20) | gi));
+  else atomicMin(key + 1, 0ull);
+}
 
 struct ScoreTables {
   int32_t n;
@@ -570,9 +579,7 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
         valid_out[c] = 1;
         if (best_key) {
           const uint64_t gi = (uint64_t)(c + index_base);
-          const unsigned long long key =
-              (pk < (1ull << 43) && gi < (1ull << 20)) ? ((pk << 20) | gi) : kKeyOverflow;
-          atomicMin(best_key, key);
+          record_key(best_key, pk, gi);
         }
       }
     }
@@ -914,7 +921,7 @@ __global__ void __launch_bounds__(1024)
       const int64_t gi = bi < 0 ? -1 : bi + base;
       out[0] = (uint64_t)gi;
       out[1] = bp;
-      const bool fits = gi >= 0 && gi < (1 << 20) && bp < (1ull << 43);
+      const bool fits = gi >= 0 && gi < (1 << 20) && bp < kKeyMaxPeak;
       out[2] = gi < 0 ? kKeyNone : fits ? ((bp << 20) | (uint64_t)gi) : kKeyOverflow;
     }
   }

@@ -293,9 +293,7 @@ __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMi
               valid_out[c] = ok ? 1 : 0;
               if (best_key && ok) {
                 const uint64_t gi = (uint64_t)(c + index_base);
-                const unsigned long long key =
-                    (pk < (1ull << 43) && gi < (1ull << 20)) ? ((pk << 20) | gi) : kKeyOverflow;
-                atomicMin(best_key, key);
+                record_key(best_key, pk, gi);
               }
             }
           }
@@ -416,9 +414,7 @@ __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMi
           valid_out[c] = ok ? 1 : 0;
           if (best_key && ok) {
             const uint64_t gi = (uint64_t)(c + index_base);
-            const unsigned long long key =
-                (pk < (1ull << 43) && gi < (1ull << 20)) ? ((pk << 20) | gi) : kKeyOverflow;
-            atomicMin(best_key, key);
+            record_key(best_key, pk, gi);
           }
         }
       }

@@ -221,9 +221,7 @@ __global__ void __launch_bounds__(512)
       valid_out[c] = invalid ? 0 : 1;
       if (best_key && !invalid) {
         const uint64_t gi = (uint64_t)(c + index_base);
-        const unsigned long long key =
-            (pk < (1ull << 43) && gi < (1ull << 20)) ? ((pk << 20) | gi) : kKeyOverflow;
-        atomicMin(best_key, key);
+        record_key(best_key, pk, gi);
       }
     }
     __syncwarp();  // XF reads done before the next candidate scatters

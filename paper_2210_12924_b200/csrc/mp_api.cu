@@ -335,7 +335,10 @@ mp_status mp_graph_get_info(const mp_graph* g, mp_graph_info* info) {
   info->smem_resident = g->smem_resident ? 1 : 0;
   info->total_bytes = g->total_bytes;
   info->orders16 = score_takes_u16(g) && !std::getenv("MP_NO_PACK16") ? 1 : 0;
-  info->reserved = 0;
+  info->score_variant = g->score_warps > 0 ? MP_SCORER_WARP
+                        : g->score_j > 0    ? MP_SCORER_REG
+                        : g->smem_resident  ? MP_SCORER_SMEM
+                                            : MP_SCORER_SCRATCH;
   return MP_OK;
 }
 
@@ -607,11 +610,8 @@ mp_status mp_score_orders_best(mp_ctx* ctx, const mp_graph* g, const int32_t* or
   uint8_t* d_valid = cv.take<uint8_t>(c);
   uint64_t* d_key = cv.take<uint64_t>(3);
   const bool fused = best && C <= (int64_t{1} << 20);
-  const uint64_t kNone = 0x7fffffffffffffffull, kOverflow = 0x7ffffffffffffffeull;
   uint64_t* hk = ctx->h_small;  // pinned: async copies, no staging
-  hk[0] = kNone;
-  hk[1] = kNone;
-  if (fused) MP_CUDA(cudaMemcpyAsync(d_key, hk, 8, cudaMemcpyHostToDevice, st));
+  if (fused) MP_CUDA(cudaMemsetAsync(d_key, 0x7f, 16, st));  // {MP_KEY_NONE, no overflow}
   // Pipeline: the orders go up in chunks on the copy stream while the previous
   // chunk is scored on `st`; each chunk's results come back on `st` (the other
   // copy direction), so only the last chunk's kernel and read-back are exposed.
@@ -669,22 +669,27 @@ mp_status mp_score_orders_best(mp_ctx* ctx, const mp_graph* g, const int32_t* or
     MP_CUDA(cudaMemcpyAsync(step + b, d_step + b, 4 * (size_t)m, cudaMemcpyDeviceToHost, st));
     MP_CUDA(cudaMemcpyAsync(valid + b, d_valid + b, (size_t)m, cudaMemcpyDeviceToHost, st));
   }
-  if (fused) MP_CUDA(cudaMemcpyAsync(hk + 1, d_key, 8, cudaMemcpyDeviceToHost, st));
+  if (fused) MP_CUDA(cudaMemcpyAsync(hk, d_key, 16, cudaMemcpyDeviceToHost, st));
   MP_CUDA(cudaStreamSynchronize(st));
-  const uint64_t key = hk[1];
   if (best) {
-    if (fused && key == kNone) {
-      *best = -1;                                   // no valid candidate
-    } else if (fused && key != kOverflow) {
-      *best = (int64_t)(key & ((1ull << 20) - 1));  // fused (peak, index) minimum
-    } else {                                        // key overflow: reduce on the device
+    if (fused && hk[1] != 0 && hk[0] == MP_KEY_NONE) {
+      *best = -1;                                     // no valid candidate
+    } else if (fused && hk[1] != 0) {
+      *best = (int64_t)(hk[0] & ((1ull << 20) - 1));  // fused (peak, index) minimum
+    } else {                                          // a key overflowed: reduce on the device
       MP_TRY(launch_argmin(d_peak, d_valid, C, 0, d_key, st));
-      uint64_t out0 = 0;
-      MP_CUDA(cudaMemcpyAsync(&out0, d_key, 8, cudaMemcpyDeviceToHost, st));
+      MP_CUDA(cudaMemcpyAsync(hk, d_key, 8, cudaMemcpyDeviceToHost, st));
       MP_CUDA(cudaStreamSynchronize(st));
-      *best = (int64_t)out0;
+      *best = (int64_t)hk[0];
     }
   }
+  return MP_OK;
+}
+
+mp_status mp_key_reset_d(mp_ctx* ctx, uint64_t* d_best_key, void* stream) {
+  if (!ctx || !d_best_key) return invalid_arg("null argument");
+  DeviceGuard guard(ctx->device);
+  MP_CUDA(cudaMemsetAsync(d_best_key, 0x7f, 16, static_cast<cudaStream_t>(stream)));
   return MP_OK;
 }
 

@@ -3,11 +3,12 @@
 One process per GPU (torch.distributed; NCCL on B200, gloo in CPU tests).
 
 * Candidate scoring shards by contiguous candidate ranges. Every rank's fused
-  kernel leaves the first-minimum key ``peak << 20 | global_index`` of its
-  shard; ONE ``allreduce(MIN)`` on that 8-byte key yields the global
-  first-minimum, identical to a serial first-minimum scan (lowest index wins
-  ties, oracle.cpp:78-81). Keys that cannot be packed fall back to an
-  allgather of (peak, index).
+  kernel leaves {first-minimum key ``peak << 20 | global_index``, overflow
+  flag} of its shard; ONE ``allreduce(MIN)`` on those 16 bytes yields the
+  global first-minimum, identical to a serial first-minimum scan (lowest index
+  wins ties, oracle.cpp:78-81), and tells every rank whether any shard had a
+  key that cannot be packed - then all ranks fall back to an allgather of
+  (peak, index).
 * Pair generation / validation shard by row ranges balanced on per-row work
   (the count pass); concatenating the shards in rank order reproduces the
   reference's lexicographic pair order.
@@ -17,9 +18,9 @@ from __future__ import annotations
 import numpy as np
 
 KEY_INDEX_BITS = 20
-KEY_MAX_PEAK = 1 << 43          # keeps the key a non-negative int64 for NCCL MIN
-NO_KEY = (1 << 63) - 1          # "no valid candidate" as int64
-OVERFLOW_KEY = (1 << 63) - 2    # kernel marker (MP_KEY_OVERFLOW): key does not fit
+KEY_MAX_PEAK = 1 << 42          # MP_KEY_MAX_PEAK: keys stay below NO_KEY as int64
+NO_KEY = 0x7F7F7F7F7F7F7F7F     # MP_KEY_NONE: byte-memset identity of the MIN
+OVERFLOW_KEY = 0x7F7F7F7F7F7F7F7E  # MP_KEY_OVERFLOW: mp_argmin_key_d out[2] only
 
 
 def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
@@ -35,6 +36,13 @@ def pack_key(peak: int, index: int) -> int:
     return (peak << KEY_INDEX_BITS) | index
 
 
+def key_pair(peak: int, index: int) -> list[int]:
+    """The 2-word fused key {key, overflow} one shard contributes (host side)."""
+    if index >= 0 and (peak >= KEY_MAX_PEAK or index >= (1 << KEY_INDEX_BITS)):
+        return [NO_KEY, 0]
+    return [pack_key(peak, index), NO_KEY]
+
+
 def unpack_key(key: int) -> tuple[int, int]:
     """(peak, global index), or (0, -1) when no candidate was valid."""
     if key == NO_KEY:
@@ -42,18 +50,40 @@ def unpack_key(key: int) -> tuple[int, int]:
     return key >> KEY_INDEX_BITS, key & ((1 << KEY_INDEX_BITS) - 1)
 
 
-def check_device_key(key: int) -> int:
-    """Validate a key read back from the device (MP_KEY_OVERFLOW -> fallback)."""
-    if key == OVERFLOW_KEY:
+def key_overflowed(pair) -> bool:
+    """True when any candidate behind a (reduced) {key, overflow} pair did not fit."""
+    return int(pair[1]) == 0
+
+
+def check_device_key(pair) -> int:
+    """The key of a (reduced) {key, overflow} pair read back from the device;
+    OverflowError when some shard overflowed (-> allgather_argmin fallback)."""
+    if isinstance(pair, int):
+        pair = [pair, NO_KEY]
+    if key_overflowed(pair) or int(pair[0]) == OVERFLOW_KEY:
         raise OverflowError("device argmin key overflowed; use allgather_argmin")
-    return key
+    return int(pair[0])
 
 
-def allreduce_argmin(key_tensor, group=None):
-    """In-place allreduce(MIN) of a 1-element int64 tensor holding a packed key."""
+def allreduce_argmin(key_pair_tensor, group=None):
+    """In-place allreduce(MIN) of the 2-element int64 {key, overflow} tensor: the
+    reduced key is the global first minimum, and overflow == 0 iff ANY rank had a
+    candidate whose key did not fit (that rank's key would otherwise be hidden
+    by the MIN), in which case every rank takes allgather_argmin."""
     import torch.distributed as dist
-    dist.all_reduce(key_tensor, op=dist.ReduceOp.MIN, group=group)
-    return key_tensor
+    dist.all_reduce(key_pair_tensor, op=dist.ReduceOp.MIN, group=group)
+    return key_pair_tensor
+
+
+def global_argmin(key_pair_tensor, peak: int, index: int, group=None) -> tuple[int, int]:
+    """One allreduce on the fused pair; the allgather fallback only if it reports
+    an overflow anywhere. (peak, index) is this rank's own first minimum (global
+    index, -1 if none), needed only by the fallback."""
+    allreduce_argmin(key_pair_tensor, group)
+    pair = [int(x) for x in key_pair_tensor.tolist()]
+    if key_overflowed(pair):
+        return allgather_argmin(peak, index, group)
+    return unpack_key(pair[0])
 
 
 def allgather_argmin(peak: int, index: int, group=None) -> tuple[int, int]:

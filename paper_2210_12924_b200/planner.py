@@ -200,6 +200,25 @@ def _i32(a):
     return np.ascontiguousarray(a, np.int32)
 
 
+def _check_host(a, name, itemsize, kinds, ndim):
+    """Shape of a C-contiguous host array (numpy or CPU torch) of an accepted dtype."""
+    if hasattr(a, "is_cuda"):
+        if a.is_cuda:
+            raise ValueError(f"{name} must be host memory, got a CUDA tensor")
+        if not a.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        dt, isz, shape = str(a.dtype).replace("torch.", ""), a.element_size(), tuple(a.shape)
+    elif isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"{name} must be C-contiguous")
+        dt, isz, shape = str(a.dtype), a.itemsize, a.shape
+    else:
+        raise ValueError(f"{name} must be a numpy array or a CPU torch tensor")
+    if dt not in kinds or isz != itemsize or len(shape) != ndim:
+        raise ValueError(f"{name} must be {ndim}-d {'/'.join(kinds)}, got {len(shape)}-d {dt}")
+    return shape
+
+
 class Planner:
     """One device context (mp_ctx) plus the graphs uploaded to it."""
 
@@ -344,7 +363,19 @@ class Planner:
 
     def score_orders_into(self, dg: DeviceGraph, orders_host, peak, step, valid) -> int:
         """Public host-buffer call for pre-allocated (e.g. pinned) buffers: H2D of the
-        orders, one fused scoring+argmin kernel, D2H of peak/step/valid; returns best."""
+        orders, one fused scoring+argmin kernel, D2H of peak/step/valid; returns best.
+
+        orders: C-contiguous host int32 [C, n]; peak: 8-byte [>= C]; step: int32
+        [>= C]; valid: uint8 [>= C] (numpy arrays or CPU torch tensors). Anything
+        else raises ValueError before the native call reads or writes a byte."""
+        c = _check_host(orders_host, "orders", 4, ("int32",), ndim=2)
+        if c[1] != dg.graph.n:
+            raise ValueError(f"orders must have shape [C, {dg.graph.n}], got {tuple(c)}")
+        for a, nm, isz, kinds in ((peak, "peak", 8, ("uint64", "int64")),
+                                  (step, "step", 4, ("int32",)), (valid, "valid", 1, ("uint8",))):
+            shp = _check_host(a, nm, isz, kinds, ndim=1)
+            if shp[0] < c[0]:
+                raise ValueError(f"{nm} holds {shp[0]} entries, needs {c[0]}")
         best = C.c_int64()
         _native.check(_native.lib().mp_score_orders_best(
             self.ctx, dg.handle, _native.ptr(orders_host), int(orders_host.shape[0]),
@@ -368,10 +399,15 @@ class Planner:
 
     def score_orders_argmin_d(self, dg: DeviceGraph, d_orders, num_orders, d_peak, d_step,
                               d_valid, d_best_key, index_base=0, stream: int | None = None):
+        """d_best_key: 2 int64 words {key, overflow} (reset with key_reset_d)."""
         _native.check(_native.lib().mp_score_orders_argmin_d(
             self.ctx, dg.handle, _native.ptr(d_orders), int(num_orders), _native.ptr(d_peak),
             _native.ptr(d_step), _native.ptr(d_valid), _native.ptr(d_best_key), int(index_base),
             stream))
+
+    def key_reset_d(self, d_best_key, stream: int | None = None):
+        """{MP_KEY_NONE, no overflow} into the 2-word fused key (one memset node)."""
+        _native.check(_native.lib().mp_key_reset_d(self.ctx, _native.ptr(d_best_key), stream))
 
     def argmin_key_d(self, d_peak, d_valid, num_orders, index_base, d_out3,
                      stream: int | None = None):

@@ -34,7 +34,7 @@ def _worker(rank, world, port, peaks, valid, lo, hi, size, out_q):
     for c in range(b, e):
         if valid[c] and (best < 0 or peaks[c] < peaks[best]):
             best = c
-    key = torch.tensor([D.pack_key(int(peaks[best]), best) if best >= 0 else D.NO_KEY],
+    key = torch.tensor(D.key_pair(int(peaks[best]), best) if best >= 0 else [D.NO_KEY, D.NO_KEY],
                        dtype=torch.int64)
     D.allreduce_argmin(key)
     fallback = D.allgather_argmin(int(peaks[best]) if best >= 0 else 0, best)
@@ -46,7 +46,7 @@ def _worker(rank, world, port, peaks, valid, lo, hi, size, out_q):
     gathered = [None] * world
     dist.all_gather_object(gathered, mine.tolist())
     if rank == 0:
-        out_q.put((int(key.item()), fallback, gathered, ranges))
+        out_q.put((D.check_device_key(key.tolist()), fallback, gathered, ranges))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -89,10 +89,16 @@ def test_key_packing_edges():
     assert D.unpack_key(D.NO_KEY) == (0, -1)
     assert D.pack_key(0, -1) == D.NO_KEY
     with pytest.raises(OverflowError):
-        D.pack_key(1 << 43, 0)
+        D.pack_key(1 << 42, 0)
     with pytest.raises(OverflowError):
         D.check_device_key(D.OVERFLOW_KEY)
-    assert D.check_device_key(D.NO_KEY) == D.NO_KEY
+    with pytest.raises(OverflowError):
+        D.check_device_key([D.pack_key(5, 3), 0])     # some shard overflowed
+    assert D.check_device_key([D.NO_KEY, D.NO_KEY]) == D.NO_KEY
+    assert D.key_pair(1 << 42, 7) == [D.NO_KEY, 0]
+    # every packable key sorts below the memset identity, as int64
+    assert D.pack_key(D.KEY_MAX_PEAK - 1, (1 << 20) - 1) < D.NO_KEY < (1 << 63)
+    assert int.from_bytes(b"\x7f" * 8, "little") == D.NO_KEY
     assert [D.shard_range(10, 3, r) for r in range(3)] == [(0, 3), (3, 6), (6, 10)]
     assert D.balanced_row_ranges([], 2) == [(0, 0), (0, 0)]
 
@@ -150,3 +156,51 @@ def test_two_rank_sharded_pairs_and_conflicts():
     assert p0 + p1 == full
     assert nv == len(viol) and v0 == v1 == viol
     assert nv0 == 0 and z0 == []
+
+
+def _worker_overflow(rank, world, port, out_q):
+    """Rank 1's only candidate has a peak too large to pack; rank 0's smaller
+    peak still wins, but only after every rank learned of the overflow."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = (1000, 3) if rank == 0 else (D.KEY_MAX_PEAK + 5, 10)
+    key = torch.tensor(D.key_pair(*mine), dtype=torch.int64)
+    peak, idx = D.global_argmin(key, *mine)
+    if rank == 0:
+        out_q.put((peak, idx, key.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _worker_overflow_wins(rank, world, port, out_q):
+    """The overflowing rank holds the index-order first minimum among equal huge
+    peaks: only the fallback can find it."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    big = D.KEY_MAX_PEAK + 1
+    mine = (big, 1 << 21) if rank == 0 else (big, 5)   # rank 0's index does not fit either
+    key = torch.tensor(D.key_pair(*mine), dtype=torch.int64)
+    peak, idx = D.global_argmin(key, *mine)
+    if rank == 0:
+        out_q.put((peak, idx, key.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("worker,expect", [("_worker_overflow", (1000, 3)),
+                                           ("_worker_overflow_wins", (D.KEY_MAX_PEAK + 1, 5))])
+def test_overflow_on_one_rank_reaches_every_rank(worker, expect):
+    """an overflowing rank must not be silently discarded by the MIN -
+    the 2-word {key, overflow} reduction makes every rank take the allgather."""
+    ctx = mp_.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=globals()[worker], args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    peak, idx, reduced = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert reduced[1] == 0                  # the overflow flag survived the MIN
+    assert (peak, idx) == expect

@@ -8,6 +8,7 @@ import pytest
 
 import oracle as O
 import paper_2210_12924_b200 as mp
+from paper_2210_12924_b200 import dist as D
 from paper_2210_12924_b200 import errors
 
 pytestmark = pytest.mark.gpu
@@ -472,10 +473,11 @@ def test_device_scoring_and_argmin_key(planner):
     o3 = out3.cpu().numpy().view(np.uint64)
     assert int(o3[0]) == best + 5000 and int(o3[1]) == int(host.peak[best])
     assert int(o3[2]) == (int(host.peak[best]) << 20) | (best + 5000)
-    key = torch.full((1,), (1 << 63) - 1, dtype=torch.int64, device=d)   # MP_KEY_NONE
+    key = torch.zeros(2, dtype=torch.int64, device=d)
+    planner.key_reset_d(key, s)                                  # {MP_KEY_NONE, no overflow}
     planner.score_orders_argmin_d(dg, t_orders, 1000, peak, step, valid, key, 5000, s)
     torch.cuda.synchronize()
-    assert int(key.item()) == int(o3[2])
+    assert key.tolist() == [int(o3[2]), D.NO_KEY]
 
 
 def test_host_scoring_pipeline_chunks(planner):
@@ -512,7 +514,7 @@ def test_host_scoring_pipeline_chunks(planner):
 def test_sizes_near_the_total_cap(planner):
     """Byte sizes whose total approaches the reference's 2^62 cap (graph.cpp:122-128):
     64-bit scan, peaks past the packed key's 2^43 (the host argmin falls back to the
-    device reduction; the device key reports MP_KEY_OVERFLOW), and the arena and
+    device reduction; the device key pair raises its overflow flag), and the arena and
     placement paths with 64-bit sizes - all equal to the C restatement."""
     import json
     import torch
@@ -545,12 +547,15 @@ def test_sizes_near_the_total_cap(planner):
     assert best == exp and int(res.peak[best]) >= (1 << 43)
     d = torch.device("cuda:0")
     dg = planner.upload(g)
-    key = torch.full((1,), (1 << 63) - 1, dtype=torch.int64, device=d)
+    key = torch.zeros(2, dtype=torch.int64, device=d)
     z = [torch.zeros(300, dtype=t, device=d) for t in (torch.int64, torch.int32, torch.uint8)]
+    planner.key_reset_d(key, torch.cuda.current_stream().cuda_stream)
     planner.score_orders_argmin_d(dg, torch.from_numpy(orders).to(d), 300, *z, key, 0,
                                   torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
-    assert int(key.item()) == (1 << 63) - 2            # MP_KEY_OVERFLOW: use the fallback
+    assert key.tolist()[1] == 0                        # overflow flag: use the fallback
+    with pytest.raises(OverflowError):
+        D.check_device_key(key.tolist())
     mr, rs, fr, valid = planner.run_baseline_batch(g, orders[:20])
     for i in range(20):
         e = orc.run_baseline(orders[i])

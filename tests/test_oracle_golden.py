@@ -195,3 +195,21 @@ def test_golden_lp_text(golden):
                                   rec["lp"]["pinned_addr"]) == rec["lp"]["text_pinned"]
         checked += 1
     assert checked >= 15
+
+
+def test_fast_timeline_matches_literal_restatement():
+    """oracle.timeline_peak (prefix sums, used by bench.py's timed-batch parity at
+    100k tensors) equals the literal O(h*E) restatement of plan.cpp:122-143,
+    including sinkless edges, zero sizes, all-zero timelines and horizon 0."""
+    import paper_2210_12924_b200 as mp
+    for kind, layers, seed in (("fork_join", 40, 3), ("training_like", 30, 0), ("chain", 20, 0)):
+        g = mp.generate_graph(kind, layers, 8, seed)
+        orc = O.Oracle.from_csr(g.csr())
+        for o in mp.random_topo_orders(g, 5, seed=seed):
+            lo, hi = orc.lifetimes_from_order(o)
+            _, pr, ps = orc.timeline_from_lifetimes(lo, hi, g.n, want_bytes=False)
+            assert O.timeline_peak(lo, hi, g.edge_size, g.n) == (pr, ps)
+    z = np.zeros(3, np.uint64)
+    lo, hi = np.array([1, 2, 1], np.int32), np.array([2, 3, 3], np.int32)
+    assert O.timeline_peak(lo, hi, z, 3) == (0, 1)
+    assert O.timeline_peak(lo, hi, z, 0) == (0, 0)
