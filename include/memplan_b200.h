@@ -99,6 +99,13 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out);
 mp_status mp_graph_free(mp_graph* g);
 mp_status mp_graph_get_info(const mp_graph* g, mp_graph_info* info);
 
+/* Host-only diagnostic of the node partition the large-graph scorer would use
+ * (MP_SCORER_PARTS): info[7] = {parts, max local slots per part,
+ * stash slots, cross-part validity pairs, cross-part multi-consumer tensors,
+ * shared-memory bytes, tiny4}; parts = 0 when no partition fits smem_budget. */
+mp_status mp_parts_plan_host(const mp_csr* csr, int32_t max_chunks, int64_t smem_budget,
+                             int64_t* info);
+
 /* ---- (a2/a3) lifetimes over one order ---------------------------------------
  * memplan::lifetimes_from_order (schedule.cpp:33-50) incl. the
  * is_topological_order verdict (graph.cpp:239-254): returns

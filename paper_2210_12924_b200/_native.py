@@ -39,7 +39,7 @@ EXPORTS = [
     "mp_fragmentation", "mp_generate_graph", "mp_random_topo_orders",
     "mp_place", "mp_place_d", "mp_run_baseline", "mp_run_baseline_d", "mp_encode_addresses_lp",
     "mp_joint_pairs", "mp_multi_create", "mp_multi_destroy", "mp_multi_upload",
-    "mp_score_orders_multi",
+    "mp_score_orders_multi", "mp_parts_plan_host",
 ]
 
 
@@ -137,6 +137,7 @@ def lib():
             "mp_generate_graph": (C.c_int, [C.c_int, i32, u64, u64, P(i32), P(i32), P(i64), vp,
                                             vp, vp, vp, vp]),
             "mp_random_topo_orders": (C.c_int, [P(MpCsr), i64, u64, i32, vp]),
+            "mp_parts_plan_host": (C.c_int, [P(MpCsr), i32, i64, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

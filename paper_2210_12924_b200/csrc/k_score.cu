@@ -36,6 +36,7 @@
 #include <string>
 
 #include "mp_internal.h"
+#include "mp_parts.h"
 #include "mp_prep.h"
 
 namespace mpb {
@@ -589,6 +590,7 @@ __global__ void __launch_bounds__(J > 0 ? 512 : 1024)
 
 #include "k_score_reg.cuh"
 #include "k_score_warp.cuh"
+#include "k_score_parts.cuh"
 
 ScoreTables tables(const mp_graph* g) {
   ScoreTables G;
@@ -748,11 +750,55 @@ mp_status run_warp(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64
   return MP_OK;
 }
 
+mp_status run_parts(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d_peak,
+                    int32_t* d_step, uint8_t* d_valid, uint64_t* d_key, int64_t index_base,
+                    cudaStream_t st) {
+  const auto& Q = g->parts;
+  const bool vec = g->n % 4 == 0;
+  auto kern = vec ? score_parts_kernel<true> : score_parts_kernel<false>;
+  MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q.smem));
+  int64_t grid = g->ctx->num_sms;
+  if (const char* e = std::getenv("MP_SCORE_GRID")) {
+    const long v = std::atol(e);
+    if (v > 0) grid = v;
+  }
+  if (grid > C) grid = C;
+  if (grid < 1) return MP_OK;
+  const size_t gstride = ((size_t)32 * Q.seg + 255) & ~size_t(255);
+  MP_TRY(g->ctx->scratch[3].reserve(gstride * (size_t)grid));
+  PartArgs A;
+  A.P = Q.P;
+  A.nchunks = Q.nchunks;
+  A.nb_max = Q.nb_max;
+  A.nslots = Q.nslots;
+  A.seg = Q.seg;
+  A.n_slot_init = Q.n_slot_init;
+  A.n_xfree = Q.n_xfree;
+  A.desc = static_cast<const PartDesc*>(Q.d_desc);
+  A.ctab = Q.d_ctab;
+  A.xtab = Q.d_xtab;
+  A.p1 = Q.d_p1;
+  A.intra = Q.d_intra;
+  A.xput = Q.d_xput;
+  A.xchk = Q.d_xchk;
+  A.xmax = Q.d_xmax;
+  A.dyn4 = reinterpret_cast<const uint4*>(Q.d_dyn4);
+  A.xfree = reinterpret_cast<const uint2*>(Q.d_xfree);
+  A.slot_init = Q.d_slot_init;
+  kern<<<(unsigned)grid, kPartsThreads, Q.smem, st>>>(
+      A, g->n, d_orders, C, d_peak, d_step, d_valid,
+      reinterpret_cast<unsigned long long*>(d_key), index_base, g->scale,
+      static_cast<uint8_t*>(g->ctx->scratch[3].ptr), gstride);
+  MP_CUDA(cudaGetLastError());
+  return MP_OK;
+}
+
 template <typename VT>
 mp_status dispatch(const mp_graph* g, const int32_t* o, int64_t C, uint64_t* pk, int32_t* stp,
                    uint8_t* vl, uint64_t* by, uint64_t* key, int64_t base, cudaStream_t st,
                    bool o16) {
   if (o16 && !score_takes_u16(g)) return MP_E_INVALID_ARG;
+  if (g->use_parts && by == nullptr) return run_parts(g, o, C, pk, stp, vl, key, base, st);
   if (g->score_warps > 0) return run_warp<VT>(g, o, C, pk, stp, vl, by, key, base, st);
   switch (g->score_j) {
     case 4:
@@ -851,6 +897,9 @@ mp_status score_configure(mp_graph* g) {
       }
     }
   }
+  // the node-partitioned scorer wherever per-candidate state would otherwise go
+  // through global scratch (MP_SCORE_PARTS: wherever a plan exists, for tests)
+  g->use_parts = g->parts.P > 0 && ((J == 0 && !smem) || std::getenv("MP_SCORE_PARTS"));
   g->score_j = J;
   g->score_kc = KC;
   g->score_threads = T;
@@ -861,7 +910,8 @@ mp_status score_configure(mp_graph* g) {
 }
 
 bool score_takes_u16(const mp_graph* g) {
-  return g->n > 0 && g->n < 65535 && g->score_j > 0 && g->score_warps == 0 && g->score_kc == 1;
+  return g->n > 0 && g->n < 65535 && g->score_j > 0 && g->score_warps == 0 && g->score_kc == 1 &&
+         !g->use_parts;
 }
 
 mp_status launch_score(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d_peak,

@@ -1,0 +1,337 @@
+// Node-partitioned large-graph scorer (MP_SCORER_PARTS), included by
+// k_score.cu inside namespace mpb::{anon}. Host planning: mp_parts.cpp.
+//
+// One 1024-thread CTA per SM scores one candidate at a time (persistent). The
+// candidate's positions never leave the SM: in pass b (one per node part) the
+// CTA streams the order row (coalesced int4 loads; pass 0 from HBM, the rest
+// from L2) and keeps only part b's nodes. One 32-bit shared word per local slot
+// holds the node's static scan input in its top byte ((x + 8) | f << 4, set at
+// the start of the pass) and its position in the low 24 bits (0xffffff = not
+// written this pass):
+//     w = slot[local(v)]; slot[local(v)] = (w & 0xff000000) | k;  XF[k] = w >> 24
+// Then every lookup of part b resolves in shared memory: the permutation check
+// (each local slot written this pass), the validity pairs inside the part, the
+// cross-part pairs through a stash slot written by the earlier part, and the
+// multi-consumer tensors (hi = max over the candidate sinks -> the free lands on
+// XF[hi] with one global atomic). After the last pass a blocked scan over XF
+// (global, L2-resident, 1 B per position) gives RS(p), the peak and the first
+// step attaining it, as the other variants (schedule.cpp:69-88, plan.cpp:135-141).
+//
+// Per candidate the only global traffic is the order (4n B from HBM once, then
+// from L2 per extra pass), XF (n B written, n B read), one atomic per
+// multi-consumer tensor and the static lists (shared by all CTAs, L2-resident).
+// The scratch variant instead spends a 32-byte L2 sector on each of ~3.5
+// random 4-byte position accesses per node.
+
+struct PartArgs {
+  int32_t P, nchunks, nb_max, nslots, seg;
+  int32_t n_slot_init, n_xfree;
+  const PartDesc* __restrict__ desc;
+  const uint32_t* __restrict__ ctab;
+  const uint8_t* __restrict__ xtab;
+  const uint16_t* __restrict__ p1;
+  const uint32_t* __restrict__ intra;
+  const uint32_t* __restrict__ xput;
+  const uint32_t* __restrict__ xchk;
+  const uint32_t* __restrict__ xmax;
+  const uint4* __restrict__ dyn4;
+  const uint2* __restrict__ xfree;
+  const int32_t* __restrict__ slot_init;
+};
+
+constexpr int kPartsThreads = 1024;
+#ifndef MP_PARTS_U
+#define MP_PARTS_U 4
+#endif
+constexpr int kPartsU = MP_PARTS_U;  // 16-byte order loads per thread per stream iteration
+
+__device__ __forceinline__ size_t parts_al16(size_t b) { return (b + 15) & ~size_t(15); }
+
+// The free of a multi-consumer tensor after position hi: x -= sz, f += sz on the
+// 4-bit pair, i.e. +15*sz on the byte (no carry leaves it: tiny4 bounds every
+// order); on the 32-bit word that holds it, at L2.
+__device__ __forceinline__ void parts_free_at(uint8_t* XF, int hi, uint32_t sz) {
+  atomicAdd(reinterpret_cast<unsigned int*>(XF + (hi & ~3)), (sz * 15u) << ((hi & 3) * 8));
+}
+
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
+  asm volatile("" : "+r"(v));
+  return v;
+}
+__device__ __forceinline__ uint64_t opaque_u64(uint64_t v) {
+  asm volatile("" : "+l"(v));
+  return v;
+}
+__device__ __forceinline__ void stg_u8(uint8_t* p, uint32_t v) {
+  asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// 32-bit shared-window accesses (addresses computed once, not per generic access)
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+template <bool kVec>
+__global__ void __launch_bounds__(kPartsThreads, 1)
+    score_parts_kernel(PartArgs A, int32_t n, const int32_t* __restrict__ orders, int64_t C,
+                       uint64_t* __restrict__ peak_out, int32_t* __restrict__ step_out,
+                       uint8_t* __restrict__ valid_out, unsigned long long* __restrict__ best_key,
+                       int64_t index_base, uint64_t scale, uint8_t* __restrict__ gxf,
+                       size_t gstride) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ uint32_t s_wsum[32];
+  __shared__ uint32_t s_wbest[32];
+  __shared__ int s_widx[32];
+  __shared__ uint32_t s_segadj[32];  // x removed from warp segment w by multi-consumer frees
+  __shared__ PartDesc s_desc[kPartMaxParts];  // read field by field where used (registers)
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int T = kPartsThreads;
+  constexpr uint32_t kPos = 0xffffffu;  // position bits; all ones = not written this pass
+  uint32_t* slot = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* ctab_s = reinterpret_cast<uint32_t*>(smem + parts_al16((size_t)A.nb_max * 4));
+  uint32_t* stash = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(ctab_s) +
+                                                parts_al16((size_t)(A.nchunks + 1) * 4));
+  // kept in registers (opaque to the compiler, which would otherwise rematerialise
+  // the shared window base and the scratch pointer inside every member branch)
+  const uint32_t slot_a = opaque_u32((uint32_t)__cvta_generic_to_shared(slot));
+  const uint32_t ctab_a = opaque_u32((uint32_t)__cvta_generic_to_shared(ctab_s));
+  uint8_t* XF = reinterpret_cast<uint8_t*>(
+      opaque_u64(reinterpret_cast<uint64_t>(gxf + (size_t)blockIdx.x * gstride)));
+  const int seg = A.seg;  // positions per warp segment, a multiple of 512
+  const int wbeg = warp * seg;
+
+  for (int i = tid; i <= A.nchunks; i += T) ctab_s[i] = __ldg(A.ctab + i);
+  if (tid < A.P) s_desc[tid] = A.desc[tid];
+  for (int i = n + tid; i < 32 * seg; i += T) XF[i] = 8;  // scan padding: x = 0, f = 0
+  __syncthreads();
+
+  for (int64_t c = blockIdx.x; c < C; c += gridDim.x) {
+    const int32_t* ord = orders + c * (int64_t)n;
+    bool bad = false;
+    uint32_t segx = 0;  // sum of x over this lane's positions (modular)
+    for (int i = tid; i < A.n_slot_init; i += T) stash[__ldg(A.slot_init + i)] = 0;
+    if (tid < 32) s_segadj[tid] = 0;
+
+    for (int b = 0; b < A.P; ++b) {
+      const PartDesc& D = s_desc[b];
+      {  // slot words: this part's static scan input on top, "not written" below
+        const uint4* src = reinterpret_cast<const uint4*>(A.xtab + D.xtab_off);
+        uint4* dst = reinterpret_cast<uint4*>(slot);
+        for (int i = tid; i < (D.nloc >> 4); i += T) {
+          const uint4 q = __ldg(src + i);
+          const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+          for (int h = 0; h < 4; ++h)
+            dst[4 * i + h] = make_uint4((w[h] << 24) | kPos, ((w[h] << 16) & 0xff000000u) | kPos,
+                                        ((w[h] << 8) & 0xff000000u) | kPos,
+                                        (w[h] & 0xff000000u) | kPos);
+        }
+      }
+      __syncthreads();
+
+      // ---- stream the order: keep part b's nodes -----------------------------------
+      // 16 positions per thread per iteration: their chunk-table lookups are issued
+      // together, then each member does one shared read-modify-write and one byte
+      // store. A whole iteration of real positions only tracks the max id (range
+      // check after the loop); the segment tail checks per position.
+      const bool last = b == A.P - 1;
+      const uint32_t bsel = (uint32_t)b << 24;
+      uint32_t vmax = 0;
+      for (int r0 = wbeg + 4 * lane; r0 < wbeg + seg; r0 += kPartsU * 128) {
+        uint32_t vq[4 * kPartsU];
+#pragma unroll
+        for (int u = 0; u < kPartsU; ++u) {  // kPartsU 16-byte loads in flight per thread
+          const int r = r0 + u * 128;
+          int4 q;
+          if (kVec) {
+            const int4* p4 = reinterpret_cast<const int4*>(ord + r);
+            q = r >= n ? make_int4(-1, -1, -1, -1) : last ? __ldcs(p4) : __ldg(p4);
+          } else {
+            q.x = r < n ? __ldg(ord + r) : -1;
+            q.y = r + 1 < n ? __ldg(ord + r + 1) : -1;
+            q.z = r + 2 < n ? __ldg(ord + r + 2) : -1;
+            q.w = r + 3 < n ? __ldg(ord + r + 3) : -1;
+          }
+          vq[4 * u] = (uint32_t)q.x, vq[4 * u + 1] = (uint32_t)q.y;
+          vq[4 * u + 2] = (uint32_t)q.z, vq[4 * u + 3] = (uint32_t)q.w;
+        }
+        if (r0 + (kPartsU - 1) * 128 + 3 < n) {
+#pragma unroll
+          for (int j = 0; j < 4 * kPartsU; ++j) vmax = max(vmax, vq[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4 * kPartsU; ++j)
+            bad |= vq[j] >= (uint32_t)n && r0 + (j >> 2) * 128 + (j & 3) < n;
+        }
+        // id -> local slot of part b, or ~0 (another part / out of range), in place
+#pragma unroll
+        for (int j = 0; j < 4 * kPartsU; ++j) {
+          const uint32_t e = lds_u32(ctab_a + 4u * min(vq[j] >> kPartChunkBits, (uint32_t)A.nchunks));
+          vq[j] = (e ^ bsel) < (1u << 24) ? (e & kPos) + (vq[j] & ((1u << kPartChunkBits) - 1))
+                                          : 0xffffffffu;
+        }
+        uint8_t* xrow = XF + r0;
+#pragma unroll
+        for (int j = 0; j < 4 * kPartsU; ++j) {
+          if (vq[j] != 0xffffffffu) {  // part b owns this position's node
+            const uint32_t a = slot_a + 4u * vq[j];
+            const uint32_t w = lds_u32(a);
+            sts_u32(a, (w & 0xff000000u) | (uint32_t)(r0 + (j >> 2) * 128 + (j & 3)));
+            stg_u8(xrow + (j >> 2) * 128 + (j & 3), w >> 24);
+            segx += ((w >> 24) & 0xfu) - 8u;
+          }
+        }
+      }
+      bad |= vmax >= (uint32_t)n;
+      __syncthreads();
+
+      // ---- resolve part b's lookups in shared memory ---------------------------------
+      // (a slot left unwritten keeps kPos: it fails the permutation check, so the
+      // comparisons below never need to tell it apart)
+      {  // every local node written this pass (a permutation), and its same-part
+         // first producer strictly earlier: own words in 16-byte reads, producer ids
+         // 4 x 16 bits per 8-byte load, one random slot read per node
+        const uint4* sw = reinterpret_cast<const uint4*>(slot);
+        const uint2* p1 = reinterpret_cast<const uint2*>(A.p1 + D.xtab_off);
+        const int plo = D.pad_lo, phi = D.pad_hi;
+        for (int i = tid; i < (D.nloc >> 2); i += T) {
+          const uint4 q = sw[i];
+          const uint2 pp = __ldg(p1 + i);
+          const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+          const uint32_t pr[4] = {pp.x & 0xffffu, pp.x >> 16, pp.y & 0xffffu, pp.y >> 16};
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const int l = 4 * i + h;
+            bad |= (w[h] & kPos) == kPos && (l < plo || l >= phi);
+            if (pr[h] != 0xffffu) bad |= (slot[pr[h]] & kPos) >= (w[h] & kPos);
+          }
+        }
+      }
+      // the static lists come as uint4 groups, two groups in flight per thread
+      auto groups = [&](const uint32_t* list, int off, int cnt, auto&& fn) {
+        const uint4* g4 = reinterpret_cast<const uint4*>(list) + off;
+        for (int i = tid; i < cnt; i += 2 * T) {
+          const uint4 g0 = __ldg(g4 + i);
+          const uint4 g1 = i + T < cnt ? __ldg(g4 + i + T) : make_uint4(~0u, ~0u, ~0u, ~0u);
+          const uint32_t es[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+          for (int h = 0; h < 8; ++h)
+            if (es[h] != 0xffffffffu) fn(es[h]);
+        }
+      };
+      groups(A.intra, D.intra_off, D.intra_n, [&](uint32_t e) {
+        if ((slot[e & 0xffffu] & kPos) >= (slot[e >> 16] & kPos)) bad = true;  // producer later
+      });
+      groups(A.xput, D.xput_off, D.xput_n,
+             [&](uint32_t e) { stash[e >> 16] = slot[e & 0xffffu] & kPos; });
+      groups(A.xchk, D.xchk_off, D.xchk_n, [&](uint32_t e) {
+        const uint32_t s = stash[(e >> 16) & 0x7fffu];
+        const uint32_t p = slot[e & 0xffffu] & kPos;
+        if ((e >> 31) ? p >= s : s >= p) bad = true;
+      });
+      groups(A.xmax, D.xmax_off, D.xmax_n,
+             [&](uint32_t e) { atomicMax(&stash[e >> 16], slot[e & 0xffffu] & kPos); });
+      for (int i = tid; i < D.dyn_n; i += 2 * T) {  // multi-consumer tensors inside the part
+        uint4 dd[2];
+        dd[0] = __ldg(A.dyn4 + D.dyn_off + i);
+        dd[1] = i + T < D.dyn_n ? __ldg(A.dyn4 + D.dyn_off + i + T) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint4 d = dd[u];
+          if (d.z == 0) continue;  // padding (every real record frees >= 1 unit)
+          const uint32_t l1 = d.x & 0xffffu, l2 = d.x >> 16, l3 = d.y & 0xffffu, l4 = d.y >> 16;
+          uint32_t h = slot[l1] & kPos;
+          if (l2 != 0xffffu) h = max(h, slot[l2] & kPos);
+          if (l3 != 0xffffu) h = max(h, slot[l3] & kPos);
+          if (l4 != 0xffffu) h = max(h, slot[l4] & kPos);
+          const int hi = (int)h;
+          if (hi < n) {
+            parts_free_at(XF, hi, d.z);
+            atomicAdd(&s_segadj[hi / seg], d.z);
+          }
+        }
+      }
+      __syncthreads();  // slot words are rewritten by the next pass
+    }
+    for (int i = tid; i < A.n_xfree; i += T) {  // multi-consumer tensors spanning parts
+      const uint2 f = __ldg(A.xfree + i);
+      const int hi = (int)stash[f.x];
+      if (hi < n) {
+        parts_free_at(XF, hi, f.y);
+        atomicAdd(&s_segadj[hi / seg], f.y);
+      }
+    }
+    if (__syncthreads_or(bad)) {
+      if (tid == 0) {
+        peak_out[c] = 0;
+        step_out[c] = 0;
+        valid_out[c] = 0;
+      }
+      continue;
+    }
+
+    // ---- scan over XF (L2 only: the frees above were atomics at L2) -------------------
+    uint32_t tot = warp_sum(segx);
+    if (lane == 0) s_wsum[warp] = tot - s_segadj[warp];
+    __syncthreads();
+    uint32_t carry = warp_sum(lane < warp ? s_wsum[lane] : 0u);  // exclusive over warps
+    uint32_t best = 0;
+    int best_i = INT_MAX;
+    for (int r00 = wbeg; r00 < wbeg + seg; r00 += 4 * 128) {  // seg is a 512-multiple
+      uint32_t w4s[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)  // four loads in flight, then the dependent scan
+        w4s[u] = __ldcg(reinterpret_cast<const unsigned int*>(XF + r00 + u * 128 + 4 * lane));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = r00 + u * 128 + 4 * lane;
+        const uint32_t w4 = w4s[u];
+        uint32_t xs[4], fs[4], t = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t byte = (w4 >> (8 * q)) & 0xffu;
+          xs[q] = (byte & 0xfu) - 8u;
+          fs[q] = byte >> 4;
+          t += xs[q];
+        }
+        const uint32_t incl = warp_incl_scan(t, lane);
+        uint32_t run = carry + incl - t;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          run += xs[q];
+          const uint32_t rs = run + fs[q];
+          const int k = r + q;
+          if (k < n && (best_i == INT_MAX || rs > best)) {
+            best = rs;
+            best_i = k;
+          }
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+    warp_argmax(best, best_i);
+    if (lane == 0) {
+      s_wbest[warp] = best;
+      s_widx[warp] = best_i;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      best = s_wbest[lane];
+      best_i = s_widx[lane];
+      warp_argmax(best, best_i);
+      if (lane == 0) {
+        const uint64_t pk = (uint64_t)best * scale;
+        peak_out[c] = pk;
+        step_out[c] = best_i + 1;
+        valid_out[c] = 1;
+        if (best_key) record_key(best_key, pk, (uint64_t)(c + index_base));
+      }
+    }
+    // s_wsum / s_wbest are rewritten after >= 2 barriers of the next candidate
+  }
+}

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "mp_internal.h"
+#include "mp_parts.h"
 #include "mp_prep.h"
 
 namespace mpb {
@@ -297,6 +298,45 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
   }
   up(upload(&g->d_out_off, P.out_off.data(), P.out_off.size(), st));
   up(upload(&g->d_out_edges, P.out_edges.data(), P.out_edges.size(), st));
+  // Large tiny4 graphs: plan the node partition of the shared-memory scorer
+  // (MP_SCORE_PARTS forces it on any tiny4 graph, MP_PARTS_CHUNKS caps the chunks
+  // per part - both for tests; MP_SCORE_NO_PARTS keeps the scratch scorer).
+  const bool scratch_knob = std::getenv("MP_SCORE_NO_PARTS") || std::getenv("MP_SCORE_POS64") ||
+                            std::getenv("MP_SCORE_WIDE_XF") || std::getenv("MP_SCORE_NO_TINY4");
+  if (s == MP_OK && P.tiny4 && n > 0 && !scratch_knob &&
+      (n >= kPartsMinNodes || std::getenv("MP_SCORE_PARTS"))) {
+    const char* mc = std::getenv("MP_PARTS_CHUNKS");
+    PartPlan pp;
+    if (plan_parts(P, ctx->max_smem_optin, mc ? std::atoi(mc) : 0, &pp)) {
+      auto& Q = g->parts;
+      Q.P = pp.P;
+      Q.nchunks = pp.nchunks;
+      Q.nb_max = pp.nb_max;
+      Q.nslots = pp.nslots;
+      Q.n_slot_init = (int32_t)pp.slot_init_max.size();
+      Q.n_xfree = (int32_t)(pp.xfree.size() / 2);
+      Q.n_cross_pairs = pp.n_cross_pairs;
+      Q.n_cross_dyn = pp.n_cross_dyn;
+      Q.seg = ((n + 32 * 512 - 1) / (32 * 512)) * 512;  // per-warp segment, 512-multiple
+      Q.smem = parts_smem_bytes(pp);
+      std::vector<int32_t> desc(pp.desc.size() * (sizeof(PartDesc) / 4));
+      std::memcpy(desc.data(), pp.desc.data(), desc.size() * 4);
+      int32_t* dd = nullptr;
+      up(upload(&dd, desc.data(), desc.size(), st));
+      Q.d_desc = dd;
+      up(upload(&Q.d_ctab, pp.ctab.data(), pp.ctab.size(), st));
+      up(upload(&Q.d_xtab, pp.xtab.data(), pp.xtab.size(), st));
+      up(upload(&Q.d_p1, pp.p1.data(), pp.p1.size(), st));
+      up(upload(&Q.d_intra, pp.intra.data(), pp.intra.size(), st));
+      up(upload(&Q.d_xput, pp.xput.data(), pp.xput.size(), st));
+      up(upload(&Q.d_xchk, pp.xchk.data(), pp.xchk.size(), st));
+      up(upload(&Q.d_xmax, pp.xmax.data(), pp.xmax.size(), st));
+      up(upload(&Q.d_dyn4, pp.dyn4.data(), pp.dyn4.size(), st));
+      up(upload(&Q.d_xfree, pp.xfree.data(), pp.xfree.size(), st));
+      up(upload(&Q.d_slot_init, pp.slot_init_max.data(), pp.slot_init_max.size(), st));
+      if (s == MP_OK) up(cudaStreamSynchronize(st) == cudaSuccess ? MP_OK : MP_E_CUDA);
+    }
+  }
   if (s == MP_OK) up(score_configure(g));
   if (s == MP_OK) {
     cudaError_t ce = cudaStreamSynchronize(st);  // host tables may go out of scope
@@ -310,6 +350,24 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
   return MP_OK;
 }
 
+mp_status mp_parts_plan_host(const mp_csr* csr, int32_t max_chunks, int64_t smem_budget,
+                             int64_t* info) {
+  if (!csr || !info || csr->num_nodes < 0 || csr->num_edges < 0) return invalid_arg("bad argument");
+  ScorePrep P;
+  prepare_scoring(csr->num_nodes, csr->num_edges, csr->edge_src, csr->sink_off, csr->sinks,
+                  csr->edge_size, &P);
+  PartPlan pp;
+  const bool ok = plan_parts(P, (size_t)smem_budget, max_chunks, &pp);
+  info[0] = ok ? pp.P : 0;
+  info[1] = pp.nb_max;
+  info[2] = pp.nslots;
+  info[3] = pp.n_cross_pairs;
+  info[4] = pp.n_cross_dyn;
+  info[5] = ok ? (int64_t)parts_smem_bytes(pp) : 0;
+  info[6] = P.tiny4 ? 1 : 0;
+  return MP_OK;
+}
+
 mp_status mp_graph_free(mp_graph* g) {
   if (!g) return MP_OK;
   DeviceGuard guard(g->ctx->device);
@@ -318,7 +376,10 @@ mp_status mp_graph_free(mp_graph* g) {
                   g->d_extra_w,  g->d_dyn_off,   g->d_dyn_sinks, g->d_dyn_size,
                   g->d_node_rec32, g->d_node_u2, g->d_extra3_packed,
                   g->d_out_off,  g->d_out_edges, g->d_dyn_sink4, g->d_joint_mul,
-                  g->d_joint_ar, g->d_joint_art, g->d_edge_size32};
+                  g->d_joint_ar, g->d_joint_art, g->d_edge_size32,
+                  g->parts.d_desc, g->parts.d_ctab, g->parts.d_xtab, g->parts.d_p1, g->parts.d_intra,
+                  g->parts.d_xput, g->parts.d_xchk, g->parts.d_xmax, g->parts.d_dyn4,
+                  g->parts.d_xfree, g->parts.d_slot_init};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete g;
@@ -335,7 +396,8 @@ mp_status mp_graph_get_info(const mp_graph* g, mp_graph_info* info) {
   info->smem_resident = g->smem_resident ? 1 : 0;
   info->total_bytes = g->total_bytes;
   info->orders16 = score_takes_u16(g) && !std::getenv("MP_NO_PACK16") ? 1 : 0;
-  info->score_variant = g->score_warps > 0 ? MP_SCORER_WARP
+  info->score_variant = g->use_parts        ? MP_SCORER_PARTS
+                        : g->score_warps > 0 ? MP_SCORER_WARP
                         : g->score_j > 0    ? MP_SCORER_REG
                         : g->smem_resident  ? MP_SCORER_SMEM
                                             : MP_SCORER_SCRATCH;

@@ -134,6 +134,21 @@ struct mp_graph {
 
   bool smem_resident = false;
   size_t score_smem_bytes = 0;
+
+  // node-partitioned large-graph scorer (mp_parts.cpp, k_score_parts.cuh)
+  struct Parts {
+    int32_t P = 0, nchunks = 0, nb_max = 0, nslots = 0, seg = 0;
+    int32_t n_slot_init = 0, n_xfree = 0, n_cross_pairs = 0, n_cross_dyn = 0;
+    size_t smem = 0;
+    void* d_desc = nullptr;
+    uint32_t* d_ctab = nullptr;
+    uint8_t* d_xtab = nullptr;
+    uint16_t* d_p1 = nullptr;
+    uint32_t *d_intra = nullptr, *d_xput = nullptr, *d_xchk = nullptr, *d_xmax = nullptr;
+    uint32_t *d_dyn4 = nullptr, *d_xfree = nullptr;
+    int32_t* d_slot_init = nullptr;
+  } parts;
+  bool use_parts = false;
 };
 
 namespace mpb {

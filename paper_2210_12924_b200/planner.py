@@ -778,3 +778,15 @@ def random_topo_orders(graph: Graph, num_orders: int, seed: int = 0,
     _native.check(_native.lib().mp_random_topo_orders(C.byref(csr), int(num_orders), int(seed),
                                                       int(threads), out.ctypes.data))
     return out[:num_orders, :graph.n]
+
+
+def parts_plan_info(graph: Graph, max_chunks: int = 0, smem_budget: int = 232448) -> dict:
+    """Host-only: the node partition the large-graph scorer plans for `graph`
+    (mp_parts_plan_host; no device needed)."""
+    info = np.zeros(7, np.int64)
+    csr = graph.mp_csr()
+    _native.check(_native.lib().mp_parts_plan_host(C.byref(csr), int(max_chunks),
+                                                   int(smem_budget), info.ctypes.data))
+    keys = ("parts", "slots_per_part", "stash_slots", "cross_pairs", "cross_multi_consumer",
+            "smem_bytes", "tiny4")
+    return {k: int(v) for k, v in zip(keys, info)}

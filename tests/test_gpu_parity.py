@@ -255,13 +255,17 @@ def test_scorer_variants_small_graphs(planner, monkeypatch, mode, kind, layers, 
             orc.resident_bytes_per_step(orders[0])).all()
 
 
-@pytest.mark.parametrize("layers,smem,mode", [(3000, 1, ""), (20000, 0, ""), (20000, 0, "scratch64"),
-                                              (20000, 0, "widexf"), (20000, 0, "tiny8")])
+@pytest.mark.parametrize("layers,smem,mode", [(3000, 1, ""), (20000, 0, ""), (20000, 0, "scratch"),
+                                              (20000, 0, "scratch64"), (20000, 0, "widexf"),
+                                              (20000, 0, "tiny8")])
 def test_large_graph_variants(planner, monkeypatch, layers, smem, mode):
     """Graphs past the register-resident variant: node tables read per candidate,
-    buffers in shared memory (n=12k); at n=80k >= 65536 the node-space kernel with
-    global scratch and 32-bit (24-bit position, default) or 64-bit stamped position
-    words, 4-bit shared / 8-bit / wide scan inputs."""
+    buffers in shared memory (n=12k); at n=80k the node-partitioned scorer
+    (default), and the node-space kernel with global scratch and 32-bit (24-bit
+    position) or 64-bit stamped position words, 4-bit shared / 8-bit / wide scan
+    inputs."""
+    if mode == "scratch":
+        monkeypatch.setenv("MP_SCORE_NO_PARTS", "1")
     if mode == "scratch64":
         monkeypatch.setenv("MP_SCORE_POS64", "1")
     if mode == "widexf":   # training_like fits the packed scan inputs; force the wide ones
@@ -271,6 +275,8 @@ def test_large_graph_variants(planner, monkeypatch, layers, smem, mode):
     g = mp.generate_graph("training_like", layers, 8)
     dg = planner.upload(g)
     assert dg.info()["smem_resident"] == smem
+    if not smem:
+        assert dg.info()["score_variant"] == (5 if mode == "" else 4)   # MP_SCORER_PARTS / SCRATCH
     orc = O.Oracle.from_csr(g.csr())
     orders = np.concatenate([g.program_order()[None, :], mp.random_topo_orders(g, 4, seed=2)])
     bad = orders[1:3].copy()
@@ -285,9 +291,13 @@ def test_large_graph_variants(planner, monkeypatch, layers, smem, mode):
         assert (int(res.peak[i]), int(res.peak_step[i])) == (int(rs.max()), int(np.argmax(rs)) + 1)
 
 
-def test_global_scratch_stamp_wrap(planner, monkeypatch):
+@pytest.mark.parametrize("variant", ["parts", "scratch"])
+def test_global_scratch_stamp_wrap(planner, monkeypatch, variant):
     """One CTA scoring 300 candidates of an 80k-node graph: the 7-bit stamp of the
-    32-bit position words wraps twice and every verdict and peak must hold."""
+    32-bit position words (per candidate in the scratch scorer, per pass in the
+    node-partitioned one) wraps several times and every verdict and peak must hold."""
+    if variant == "scratch":
+        monkeypatch.setenv("MP_SCORE_NO_PARTS", "1")
     monkeypatch.setenv("MP_SCORE_GRID", "1")
     g = mp.generate_graph("training_like", 20000, 8)
     orc = O.Oracle.from_csr(g.csr())
@@ -305,6 +315,41 @@ def test_global_scratch_stamp_wrap(planner, monkeypatch):
     full = planner.score_orders(g, orders)
     assert (full.peak == res.peak).all() and (full.peak_step == res.peak_step).all()
     assert (full.valid == res.valid).all()
+
+
+@pytest.mark.parametrize("kind,layers,chunks", [("training_like", 300, 2), ("training_like", 200, 1),
+                                                ("training_like", 1000, 6), ("chain", 3000, 4),
+                                                ("training_like", 40, 1), ("training_like", 40, 0)])
+def test_node_partitioned_scorer_small(planner, monkeypatch, kind, layers, chunks):
+    """The node-partitioned scorer forced onto small graphs with tiny parts
+    (MP_PARTS_CHUNKS 64-node chunks per part, 0 = no cap): many passes, validity pairs and
+    multi-consumer tensors across parts through stash slots, n not a multiple of
+    4 (scalar order loads) and of 256 (padding slots); valid, swapped,
+    duplicated and out-of-range candidates vs the C restatement."""
+    monkeypatch.setenv("MP_SCORE_PARTS", "1")
+    monkeypatch.setenv("MP_PARTS_CHUNKS", str(chunks))
+    g = mp.generate_graph(kind, layers, 8)
+    info = mp.planner.parts_plan_info(g, max_chunks=chunks)
+    assert info["parts"] >= 1 and info["tiny4"] == 1
+    dg = planner.upload(g)
+    assert dg.info()["score_variant"] == 5
+    orc = O.Oracle.from_csr(g.csr())
+    orders = np.concatenate([g.program_order()[None, :], mp.random_topo_orders(g, 40, seed=4)])
+    orders[3, [1, 2]] = orders[3, [2, 1]]
+    orders[7, 4] = orders[7, 9]
+    orders[9, 0] = g.n
+    orders[11, -1] = -5
+    res = planner.score_orders(g, orders)
+    for i, o in enumerate(orders):
+        lt = orc.lifetimes_from_order(o)
+        if lt is None:
+            assert res.valid[i] == 0, i
+            continue
+        pr, ps = O.timeline_peak(lt[0], lt[1], g.edge_size, g.n)
+        assert res.valid[i] == 1 and (int(res.peak[i]), int(res.peak_step[i])) == (pr, ps), i
+    _, best = planner.score_orders_best(g, orders)
+    ok = [i for i in range(len(orders)) if res.valid[i]]
+    assert best == min(ok, key=lambda i: (int(res.peak[i]), i))
 
 
 @pytest.mark.parametrize("size", [8, 1 << 20])

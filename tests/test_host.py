@@ -109,3 +109,15 @@ def test_random_topo_orders_are_valid(built):
             assert len({tuple(x) for x in orders.tolist()}) > 1
         again = mp.random_topo_orders(g, 64, seed=5, threads=2)
         assert (again == orders).all()   # deterministic for any thread count
+
+
+def test_node_partitioned_plan_c5_host():
+    """Host planning of the large-graph scorer at the 100k-tensor graph: a handful of
+    parts whose positions, static bytes and stash fit one SM's shared memory; graphs
+    whose per-position values do not fit 4 bits get no plan (the scratch scorer)."""
+    import paper_2210_12924_b200 as mp
+    g = mp.generate_graph("training_like", 33333, 8)
+    info = mp.planner.parts_plan_info(g)
+    assert 2 <= info["parts"] <= 6 and info["smem_bytes"] <= 232448
+    assert info["stash_slots"] == info["cross_pairs"] + info["cross_multi_consumer"]
+    assert mp.planner.parts_plan_info(mp.generate_graph("fork_join", 3000, 8, 1))["parts"] == 0
