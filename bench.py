@@ -318,6 +318,173 @@ def check_timed_rows(g, orders, peak, step, valid, key, base, world, rows=64):
     return out
 
 
+# ---- candidate plans (schedule + addresses + check): the metric read literally ----------
+PLAN_METRIC = "candidate plans scored/sec (peak bytes + addr check)"
+
+
+def run_plan(args, cfg):
+    """BASELINE.json's metric read literally: one step scores C candidate PLANS. Per
+    candidate order (inputs resident in HBM): the schedule score (validity, peak
+    resident bytes, its step), the order's lifetimes, its address plan by
+    preallocate_pyramid + greedy_pack (plan_once's preplacement + greedy placement,
+    pipeline.cpp:101-109, 248-249), peak_mem, and the address check (validate_plan's
+    below_above pairs, plan.cpp:390-404 = addresses_feasible when 0); the best plan
+    (first minimum peak_mem over feasible plans) by a fused key. mp_score_plans_d."""
+    import torch
+    import paper_2210_12924_b200 as mp
+    from paper_2210_12924_b200 import dist as D
+    from concurrent.futures import ThreadPoolExecutor
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    g = load_graph(cfg)
+    planner = mp.Planner(0)
+    dg = planner.upload(g)
+    C = min(cfg["candidates"], args.place_batch)
+    n, E = g.n, g.E
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    st = stream.cuda_stream
+    host = [mp.random_topo_orders(g, C, seed=500 + b) for b in range(2)]
+    d_orders = [torch.from_numpy(h).to(dev) for h in host]
+    rank = torch.from_numpy(g.id_rank()[:max(E, 1)].copy()).to(dev)
+    z = lambda shape, dt: torch.zeros(shape, dtype=dt, device=dev)  # noqa: E731
+    o = {"peak_rs": z(C, torch.int64), "peak_step": z(C, torch.int32), "valid": z(C, torch.uint8),
+         "peak_mem": z(C, torch.int64), "nviol": z(C, torch.int32),
+         "addr": z((C, E), torch.int64), "has": z((C, E), torch.uint8)}
+    key = z(2, torch.int64)
+
+    def step(b):
+        planner.key_reset_d(key, st)
+        planner.score_plans_d(dg, d_orders[b % 2], C, rank, True, o["peak_rs"], o["peak_step"],
+                              o["valid"], o["peak_mem"], o["nviol"], o["addr"], o["has"], key, 0,
+                              st)
+
+    for i in range(max(args.warmup, 3)):
+        step(i)
+    torch.cuda.synchronize()
+    reps = max(1, min(args.steps, 10))
+    clocks = ClockSampler(dev)
+    clocks.start()
+    a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    a.record(stream)
+    for i in range(reps):
+        step(i)
+    b_.record(stream)
+    b_.synchronize()
+    t1 = time.perf_counter()
+    clocks.stop()
+    ms = a.elapsed_time(b_) / reps
+    last = (reps - 1) % 2
+    # parity: 8 candidates of the last step against the reference's own functions
+    res = {k: v.cpu().numpy() for k, v in o.items()}
+    kp = key.cpu().tolist()
+    ok_idx = [i for i in range(C) if res["valid"][i] and res["nviol"][i] == 0]
+    best = min(ok_idx, key=lambda i: (int(res["peak_mem"][i].view(np.uint64)), i)) if ok_idx else -1
+    parity = {"rows": 8, "key_consistent": D.unpack_key(kp[0])[1] == best if best >= 0 else
+              kp[0] == D.NO_KEY, "checked_against": "oracle/_ref lifetimes_from_order, "
+              "preallocate_pyramid, greedy_pack; C restatement of validate_plan's pair loop"}
+    cpu = None
+    if O.ref_available():
+        rg = O.RefGraph.load(mp.save_graph(g))
+        mism = 0
+        for i in np.linspace(0, C - 1, 8).astype(int):
+            od = host[last][i]
+            try:
+                lo, hi = rg.lifetimes_from_order(od)
+            except O.RefError:
+                mism += int(res["valid"][i] != 0)
+                continue
+            tk, ta, _ = rg.preallocate_pyramid(lo, hi)
+            ea, eh = rg.greedy_pack_fixed(lo, hi, tk, ta)
+            pm = max((int(ea[e]) + int(g.edge_size[e]) for e in range(E) if eh[e]), default=0)
+            nv = len(O.validate_pairs(lo, hi, g.edge_size, eh, ea))
+            got_a = res["addr"][i].view(np.uint64)
+            mism += int(not ((res["has"][i] == eh).all() and (got_a[eh == 1] == ea[eh == 1]).all()
+                             and int(res["peak_mem"][i].view(np.uint64)) == pm
+                             and int(res["nviol"][i]) == nv))
+        parity.update({"mismatches": mism, "ok": mism == 0 and parity["key_consistent"]})
+        if not parity["ok"]:
+            raise AssertionError(f"plan parity failed: {parity}")
+        # the reference on the host cores: the same composition with its public check
+        cores = os.cpu_count() or 1
+        ts_cache = {}
+
+        def ref_one(i):
+            od = host[0][i]
+            lo, hi = rg.lifetimes_from_order(od)
+            tk, ta, _ = rg.preallocate_pyramid(lo, hi)
+            ea, eh = rg.greedy_pack_fixed(lo, hi, tk, ta)
+            pm = max((int(ea[e]) + int(g.edge_size[e]) for e in range(E) if eh[e]), default=0)
+            prs = rg.peak_resident_bytes(od)
+            ts = np.zeros(n, np.int32)
+            ts[od] = np.arange(1, n + 1, dtype=np.int32)
+            ts_cache[i] = rg.validate_plan(od, ts, eh, ea, pm, prs)
+            return pm
+
+        t_one0 = time.perf_counter()
+        ref_one(0)
+        per = time.perf_counter() - t_one0
+        sample = int(min(C, max(cores, cores * 20.0 / max(per, 1e-9) / 2)))
+        tc = time.perf_counter()
+        with ThreadPoolExecutor(cores) as ex:
+            list(ex.map(ref_one, range(sample)))
+        tr = time.perf_counter() - tc
+        assert not any(t == "below_above" for v in ts_cache.values() for t, _ in v), \
+            "reference validate_plan found an address conflict in a greedy plan"
+        cpu = {"value": sample / tr, "unit": "plans/s", "cores": cores, "kind": "reference",
+               "single_plan_s": per,
+               "sample": f"{sample} candidate orders: memplan::lifetimes_from_order + "
+                         "preallocate_pyramid + greedy_pack + peak_resident_bytes + validate_plan "
+                         f"(oracle/_ref -O3) on {cores} host threads (python thread pool; the "
+                         "reference releases the GIL inside each call)"}
+    # e2e through the public API: pinned orders in, per-plan results back, every step
+    pin = torch.from_numpy(host[0]).pin_memory()
+    hres = {k: torch.zeros(C, dtype=o[k].dtype).pin_memory()
+            for k in ("peak_rs", "valid", "peak_mem", "nviol")}
+    torch.cuda.synchronize()
+    te0 = time.perf_counter()
+    for i in range(reps):
+        d_orders[0].copy_(pin, non_blocking=True)
+        step(0)
+        for k, v in hres.items():
+            v.copy_(o[k], non_blocking=True)
+        stream.synchronize()
+    te = (time.perf_counter() - te0) / reps
+    peak_gbs, peak_src = measured_peak_gbs()
+    alg = C * (4 * n + 8 + 4 + 1 + 8 + 4 + 9 * E)   # orders in; scores, plan, check out
+    line = {
+        "metric": PLAN_METRIC, "value": C / (ms / 1e3), "unit": "plans/s", "n_gpus": 1,
+        "steps": reps, "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "nodes": n, "edges": E, "candidates_per_gpu": C,
+                   "candidate_source": "seeded random topological orders (randomised Kahn)",
+                   "plan": "lifetimes_from_order -> preallocate_pyramid -> greedy_pack -> "
+                           "peak_mem -> validate_plan below_above pairs; best = first-min peak_mem "
+                           "over feasible plans"},
+        "roofline": {"bound": "latency (placement: sequential over edges per plan)",
+                     "achieved": alg / (ms / 1e3) / 1e9, "peak": peak_gbs, "unit": "GB/s",
+                     "frac": alg / (ms / 1e3) / 1e9 / peak_gbs, "traffic": None,
+                     "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
+                     "kernel": "score + lifetimes_batch + place (K5) + plan_check + key"},
+        "e2e": {"value": C / te, "unit": "plans/s", "h2d_bytes_per_step": C * n * 4,
+                "d2h_bytes_per_step": C * (8 + 1 + 8 + 4),
+                "path": "Planner.score_plans_d with pinned H2D of the orders and D2H of "
+                        "peak_rs/valid/peak_mem/nviol"},
+        "gpu_launches": reps * 6,
+        "feasible_plans": len(ok_idx), "best_plan": best,
+        "parity_rows": parity, "clocks": clocks.summary(t0, t1),
+        "timing": "CUDA events around stream-ordered mp_score_plans_d calls",
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line))
+    planner.close()
+    return 0
+
+
 # ---- pairs / validation (K2, K4) ------------------------------------------------------
 def run_pairs_sharded(args, cfg):
     """N > 1: the pair sweep and the validation sharded by rows over the ranks
@@ -777,7 +944,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--place-batch", type=int, default=4096)
-    ap.add_argument("--mode", default="score", choices=["score", "pairs", "place", "arena", "lp", "joint"],
+    ap.add_argument("--mode", default="score",
+                    choices=["score", "plan", "pairs", "place", "arena", "lp", "joint"],
                     help="score: candidate scoring (the headline); pairs: overlap-pair "
                          "generation (K2) + address-plan validation (K4) on one lifetime set")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -791,6 +959,8 @@ def main():
         return run_pairs(args, cfg)
     if args.mode == "place":
         return run_place(args, cfg)
+    if args.mode == "plan":
+        return run_plan(args, cfg)
     if args.mode == "arena":
         return run_arena(args, cfg)
     if args.mode == "lp":

@@ -276,6 +276,42 @@ mp_status mp_place_d(mp_ctx* ctx, int32_t num_edges, int64_t num_problems, const
                      uint64_t* d_addr, uint8_t* d_has_addr, uint64_t* d_peak_mem,
                      uint64_t* d_pyramid_base, void* stream);
 
+/* ---- batched candidate PLANS: plan_once's placement half per candidate order ----
+ * For each candidate order c (row c of [num_orders][num_nodes]):
+ *   schedule score  valid[c], peak_rs[c], peak_step[c] as mp_score_orders;
+ *   lifetimes_from_order (schedule.cpp:33-50) of the order;
+ *   addresses       preallocate_pyramid (flags & MP_PLACE_PYRAMID) then greedy_pack
+ *                   (placement.cpp:25-62, 182-204) over those lifetimes, as plan_once's
+ *                   preplacement + greedy placement (pipeline.cpp:101-109, 248-249);
+ *   peak_mem[c]     max(addr + size) (pipeline.cpp:270-275);
+ *   nviol[c]        the address check: pairs validate_plan reports as below_above
+ *                   (plan.cpp:390-404; addresses_feasible, pipeline.cpp:146-160, is
+ *                   nviol == 0). Invalid orders get nviol = 0, peak_mem = 0.
+ * d_addr / d_has_addr [num_orders][num_edges] may be NULL (context scratch).
+ * d_best_key (optional, 2 words as mp_score_orders_argmin_d): first minimum of
+ * peak_mem over feasible plans (valid order, nviol == 0). Stream-ordered; the
+ * placement bounds apply (num_edges <= 8192). */
+mp_status mp_score_plans_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_orders,
+                           int64_t num_orders, const int32_t* d_id_rank, uint32_t flags,
+                           uint64_t* d_peak_rs, int32_t* d_peak_step, uint8_t* d_valid,
+                           uint64_t* d_peak_mem, uint32_t* d_nviol, uint64_t* d_addr,
+                           uint8_t* d_has_addr, uint64_t* d_best_key, int64_t index_base,
+                           void* stream);
+/* The address check alone, for caller-supplied plans: per plan c the number of
+ * pairs validate_plan reports as below_above (plan.cpp:390-404) given the plan's
+ * lifetimes lo/hi and addresses addr/has_addr ([num_plans][num_edges] each; size
+ * [num_edges] shared). Plans with valid[c] == 0 (optional) are skipped (nviol 0,
+ * peak_mem untouched when d_peak_mem is NULL). num_edges <= 8192. */
+mp_status mp_validate_plans_d(mp_ctx* ctx, int32_t num_edges, int64_t num_plans,
+                              const int32_t* d_lo, const int32_t* d_hi, const uint64_t* d_size,
+                              const uint8_t* d_has_addr, const uint64_t* d_addr,
+                              const uint8_t* d_valid, uint32_t* d_nviol, void* stream);
+/* lifetimes_from_order for many orders at once (schedule.cpp:33-50): lo/hi
+ * [num_orders][num_edges] int32 (1-based), valid[c] = is_topological_order. */
+mp_status mp_lifetimes_batch_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_orders,
+                               int64_t num_orders, int32_t* d_lo, int32_t* d_hi,
+                               uint8_t* d_valid, void* stream);
+
 /* ---- (§8f-1) non-overlap rows: the external-ILP model text from the GPU pair list ----
  * write_lp(encode_addresses(graph, lifetimes, preplaced)) (lp_format.cpp:88-121,
  * encode.cpp:320-377) as text: per overlapping pair (the K2 pair set, i.e.

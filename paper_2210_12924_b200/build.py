@@ -18,7 +18,7 @@ LIB = os.path.join(LIBDIR, "libmemplan_b200.so")
 OBJDIR = os.path.join(ROOT, "build", "obj")
 
 CU_SOURCES = ["mp_api.cu", "k_score.cu", "k_lifetimes.cu", "k_pairs.cu", "k_place.cu",
-              "k_arena.cu", "k_lp.cu", "k_joint.cu"]
+              "k_arena.cu", "k_lp.cu", "k_joint.cu", "k_plans.cu"]
 CPP_SOURCES = ["mp_workloads.cpp", "mp_prep.cpp", "mp_parts.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

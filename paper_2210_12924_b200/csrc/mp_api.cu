@@ -1435,6 +1435,86 @@ mp_status mp_place_d(mp_ctx* ctx, int32_t E, int64_t B, const int32_t* d_lo, con
   return launch_place(a, ctx, static_cast<cudaStream_t>(stream));
 }
 
+mp_status mp_lifetimes_batch_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_orders,
+                               int64_t C, int32_t* d_lo, int32_t* d_hi, uint8_t* d_valid,
+                               void* stream) {
+  if (!ctx || !g || C < 0) return invalid_arg("null argument or negative count");
+  if (g->ctx != ctx) return invalid_arg("graph belongs to another context");
+  if (C > 0 && ((g->n > 0 && !d_orders) || !d_valid || (g->E > 0 && (!d_lo || !d_hi))))
+    return invalid_arg("null buffer");
+  DeviceGuard guard(ctx->device);
+  const mp_status s = launch_lifetimes_batch(g, d_orders, C, d_lo, d_hi, d_valid,
+                                             static_cast<cudaStream_t>(stream));
+  if (s == MP_E_CAPACITY) set_error("Capacity: graph too large for the batched lifetimes kernel");
+  return s;
+}
+
+mp_status mp_validate_plans_d(mp_ctx* ctx, int32_t E, int64_t C, const int32_t* d_lo,
+                              const int32_t* d_hi, const uint64_t* d_size, const uint8_t* d_has,
+                              const uint64_t* d_addr, const uint8_t* d_valid, uint32_t* d_nviol,
+                              void* stream) {
+  if (!ctx || E < 0 || C < 0) return invalid_arg("null argument or negative count");
+  if (C > 0 && (!d_nviol || (E > 0 && (!d_lo || !d_hi || !d_size || !d_has || !d_addr))))
+    return invalid_arg("null buffer");
+  if (E > kPlaceMaxEntries) {
+    set_error("Capacity: the batched address check handles at most 8192 edges per plan");
+    return MP_E_CAPACITY;
+  }
+  DeviceGuard guard(ctx->device);
+  return launch_plan_check(ctx, C, E, d_lo, d_hi, d_size, d_has, d_addr, d_valid, d_nviol, nullptr,
+                           static_cast<cudaStream_t>(stream));
+}
+
+mp_status mp_score_plans_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_orders, int64_t C,
+                           const int32_t* d_id_rank, uint32_t flags, uint64_t* d_peak_rs,
+                           int32_t* d_peak_step, uint8_t* d_valid, uint64_t* d_peak_mem,
+                           uint32_t* d_nviol, uint64_t* d_addr, uint8_t* d_has,
+                           uint64_t* d_best_key, int64_t index_base, void* stream) {
+  if (!ctx || !g || C < 0 || index_base < 0) return invalid_arg("null argument or negative count");
+  if (g->ctx != ctx) return invalid_arg("graph belongs to another context");
+  if (flags & ~MP_PLACE_PYRAMID) return invalid_arg("flags: only MP_PLACE_PYRAMID is accepted");
+  if (C > 0 && (!d_peak_rs || !d_peak_step || !d_valid || !d_peak_mem || !d_nviol ||
+                (g->n > 0 && !d_orders)))
+    return invalid_arg("null buffer");
+  if (g->E > kPlaceMaxEntries) {
+    set_error("Capacity: placement handles at most 8192 edges per problem");
+    return MP_E_CAPACITY;
+  }
+  if (C == 0) return MP_OK;
+  DeviceGuard guard(ctx->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t E = (size_t)g->E, c = (size_t)C;
+  MP_TRY(ctx->scratch[6].reserve(Carver::size_of({4 * E * c, 4 * E * c, c, d_addr ? 0 : 8 * E * c,
+                                                  d_has ? 0 : E * c})));
+  Carver cv(ctx->scratch[6].ptr);
+  int32_t* d_lo = cv.take<int32_t>(E * c);
+  int32_t* d_hi = cv.take<int32_t>(E * c);
+  uint8_t* d_lv = cv.take<uint8_t>(c);
+  if (!d_addr) d_addr = cv.take<uint64_t>(E * c);
+  if (!d_has) d_has = cv.take<uint8_t>(E * c);
+  // the schedules (K3), their lifetimes, their placements, the address check, the key
+  MP_TRY(launch_score(g, d_orders, C, d_peak_rs, d_peak_step, d_valid, nullptr, nullptr, 0, st));
+  mp_status s = launch_lifetimes_batch(g, d_orders, C, d_lo, d_hi, d_lv, st);
+  if (s == MP_E_CAPACITY) set_error("Capacity: graph too large for the batched lifetimes kernel");
+  MP_TRY(s);
+  PlaceArgs a;
+  a.num_edges = g->E;
+  a.num_problems = C;
+  a.lo = d_lo;
+  a.hi = d_hi;
+  a.size = g->d_edge_size;
+  a.id_rank = d_id_rank;
+  a.pyramid = (flags & MP_PLACE_PYRAMID) ? 1 : 0;
+  a.addr = d_addr;
+  a.has_addr = d_has;
+  a.peak_mem = d_peak_mem;
+  MP_TRY(launch_place(a, ctx, st));
+  MP_TRY(launch_plan_check(ctx, C, g->E, d_lo, d_hi, g->d_edge_size, d_has, d_addr, d_lv, d_nviol,
+                           d_peak_mem, st));
+  if (d_best_key) MP_TRY(launch_plan_key(C, d_lv, d_nviol, d_peak_mem, index_base, d_best_key, st));
+  return MP_OK;
+}
+
 mp_status mp_place(mp_ctx* ctx, int32_t E, int64_t B, const int32_t* lo, const int32_t* hi,
                    const uint64_t* size, const int32_t* id_rank, const uint8_t* fixed,
                    const uint64_t* fixed_addr, uint32_t flags, uint64_t* addr, uint8_t* has_addr,

@@ -45,7 +45,7 @@ struct mp_ctx {
   size_t max_smem_optin = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;  // own_stream unless mp_ctx_set_stream
-  mpb::Scratch scratch[6];        // independent scratch slots per call site
+  mpb::Scratch scratch[8];        // independent scratch slots per call site
   mpb::Scratch host_pinned_dummy;
   // small device buffer for per-call flags / counters
   int64_t* d_small = nullptr;
@@ -218,6 +218,19 @@ struct PlaceArgs {
 };
 size_t place_smem_bytes(int num_edges);
 mp_status launch_place(const PlaceArgs& a, const mp_ctx* ctx, cudaStream_t st);
+// Batched plans (k_plans.cu): lifetimes per candidate order, the pairwise
+// address check per plan, the first-minimum key over feasible plans.
+size_t lifetimes_batch_smem(int32_t n);
+size_t plan_check_smem(int32_t E);
+mp_status launch_lifetimes_batch(const mp_graph* g, const int32_t* d_orders, int64_t C,
+                                 int32_t* d_lo, int32_t* d_hi, uint8_t* d_valid, cudaStream_t st);
+mp_status launch_plan_check(const mp_ctx* ctx, int64_t C, int32_t E, const int32_t* d_lo,
+                            const int32_t* d_hi, const uint64_t* d_size, const uint8_t* d_has,
+                            const uint64_t* d_addr, const uint8_t* d_valid, uint32_t* d_nviol,
+                            uint64_t* d_peak_mem, cudaStream_t st);
+mp_status launch_plan_key(int64_t C, const uint8_t* d_valid, const uint32_t* d_nviol,
+                          const uint64_t* d_peak_mem, int64_t index_base, uint64_t* d_key,
+                          cudaStream_t st);
 // K8 joint-mode pair set (k_joint.cu): encode_joint's pair loop with edge_precedes.
 struct JointArgs {
   int32_t E = 0;

@@ -409,6 +409,69 @@ class Planner:
         """{MP_KEY_NONE, no overflow} into the 2-word fused key (one memset node)."""
         _native.check(_native.lib().mp_key_reset_d(self.ctx, _native.ptr(d_best_key), stream))
 
+    # ---- batched candidate plans (plan_once's placement half per order) -----------
+    def score_plans_d(self, dg: DeviceGraph, d_orders, num_orders, d_id_rank, pyramid: bool,
+                      d_peak_rs, d_peak_step, d_valid, d_peak_mem, d_nviol, d_addr=None,
+                      d_has=None, d_best_key=None, index_base=0, stream: int | None = None):
+        """mp_score_plans_d: per candidate order the schedule score, its lifetimes,
+        preallocate_pyramid + greedy_pack addresses, peak_mem and the number of
+        below_above pairs (0 = addresses_feasible); optional fused first-minimum key
+        of peak_mem over feasible plans."""
+        _native.check(_native.lib().mp_score_plans_d(
+            self.ctx, dg.handle, _native.ptr(d_orders), int(num_orders), _native.ptr(d_id_rank),
+            self.PLACE_PYRAMID if pyramid else 0, _native.ptr(d_peak_rs), _native.ptr(d_peak_step),
+            _native.ptr(d_valid), _native.ptr(d_peak_mem), _native.ptr(d_nviol),
+            _native.ptr(d_addr), _native.ptr(d_has), _native.ptr(d_best_key), int(index_base),
+            stream))
+
+    def score_plans(self, graph: Graph, orders, pyramid: bool = True):
+        """Host convenience over score_plans_d: returns dict of numpy arrays (peak_rs,
+        peak_step, valid, peak_mem, nviol, addr, has_addr) and the best plan index
+        (first minimum peak_mem over feasible plans, -1 if none)."""
+        import torch
+        dg = self.upload(graph)
+        o = np.ascontiguousarray(orders, np.int32).reshape(-1, graph.n)
+        c, E = o.shape[0], graph.E
+        dev = torch.device("cuda", self.device)
+        t = lambda shape, dt: torch.zeros(shape, dtype=dt, device=dev)  # noqa: E731
+        d_o = torch.from_numpy(o).to(dev)
+        rank = torch.from_numpy(graph.id_rank()[:max(E, 1)].copy()).to(dev)
+        out = {"peak_rs": t(max(c, 1), torch.int64), "peak_step": t(max(c, 1), torch.int32),
+               "valid": t(max(c, 1), torch.uint8), "peak_mem": t(max(c, 1), torch.int64),
+               "nviol": t(max(c, 1), torch.int32), "addr": t((max(c, 1), max(E, 1)), torch.int64),
+               "has_addr": t((max(c, 1), max(E, 1)), torch.uint8)}
+        key = t(2, torch.int64)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        self.key_reset_d(key, st)
+        self.score_plans_d(dg, d_o, c, rank, pyramid, out["peak_rs"], out["peak_step"],
+                           out["valid"], out["peak_mem"], out["nviol"], out["addr"],
+                           out["has_addr"], key, 0, st)
+        torch.cuda.synchronize(dev)
+        res = {k: v.cpu().numpy()[:c] for k, v in out.items()}
+        for k in ("peak_rs", "peak_mem", "addr"):
+            res[k] = res[k].view(np.uint64)
+        from . import dist as D
+        kp = key.cpu().tolist()
+        best = -1 if D.key_overflowed(kp) or kp[0] == D.NO_KEY else D.unpack_key(kp[0])[1]
+        if D.key_overflowed(kp):    # a peak past the packed range: reduce on the host
+            ok = [i for i in range(c) if res["valid"][i] and res["nviol"][i] == 0]
+            best = min(ok, key=lambda i: (int(res["peak_mem"][i]), i)) if ok else -1
+        return res, best
+
+    def validate_plans_d(self, num_edges, num_plans, d_lo, d_hi, d_size, d_has, d_addr, d_valid,
+                         d_nviol, stream: int | None = None):
+        """mp_validate_plans_d: below_above pair count per caller-supplied plan."""
+        _native.check(_native.lib().mp_validate_plans_d(
+            self.ctx, int(num_edges), int(num_plans), _native.ptr(d_lo), _native.ptr(d_hi),
+            _native.ptr(d_size), _native.ptr(d_has), _native.ptr(d_addr), _native.ptr(d_valid),
+            _native.ptr(d_nviol), stream))
+
+    def lifetimes_batch_d(self, dg: DeviceGraph, d_orders, num_orders, d_lo, d_hi, d_valid,
+                          stream: int | None = None):
+        _native.check(_native.lib().mp_lifetimes_batch_d(
+            self.ctx, dg.handle, _native.ptr(d_orders), int(num_orders), _native.ptr(d_lo),
+            _native.ptr(d_hi), _native.ptr(d_valid), stream))
+
     def argmin_key_d(self, d_peak, d_valid, num_orders, index_base, d_out3,
                      stream: int | None = None):
         _native.check(_native.lib().mp_argmin_key_d(
