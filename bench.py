@@ -264,6 +264,24 @@ SCORERS = {1: "register slots, state in smem", 2: "node tables, state in smem",
            5: "node-partitioned passes, positions in smem"}
 
 
+def alu_roofline(checks_per_s, config):
+    """K4 is issue-bound (O(E^2) compares on O(E) bytes): its roofline is
+    the warp-instruction issue rate, 4 per SM per cycle, over the measured warp
+    instructions per 32 pair checks of the validation sweep (ncu capture under
+    profiles/r2/, inst_executed / (pairs / 32))."""
+    p = os.path.join(ROOT, "profiles", "r2", f"ncu_{config}_validate.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        ipc32 = float(d["warp_instructions_per_32_checks"])
+    except Exception:
+        return None
+    peak = 148 * 4 * 1.965e9 * 32 / ipc32
+    return {"bound": "issue (ALU)", "achieved_checks_per_s": checks_per_s,
+            "peak_checks_per_s": peak, "frac": checks_per_s / peak,
+            "warp_instructions_per_32_checks": ipc32, "source": f"profiles/r2/ncu_{config}_validate.json"}
+
+
 def scorer_variant(info):
     return SCORERS.get(info.get("score_variant"), "unknown")
 
@@ -577,10 +595,26 @@ def run_pairs(args, cfg):
     row_off = torch.zeros(E + 1, dtype=torch.int64, device=dev)
     count = planner.overlap_pairs_d(E, d_lo, d_hi, d_size, None, 0, E, row_off, None, 0)
     out = torch.empty((max(count, 1), 2), dtype=torch.int32, device=dev)
-    # a valid address plan: every data tensor at its own offset (prefix sums)
-    addr = (np.cumsum(g.edge_size) - g.edge_size).astype(np.uint64)
+    # the address plans validated: the reference's placement for these
+    # lifetimes - preallocate_pyramid + greedy_pack (placement.cpp:25-62, 182-204), run
+    # on the GPU (K5) - and a seeded tampered copy (tensors moved onto live neighbours)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    if E <= 8192:
+        ga, gh, _, _ = planner.place_batch(g, lo[None], hi[None], pyramid=True)
+        addr, has = ga[0].astype(np.uint64), gh[0].astype(np.uint8)
+        plan_src = "preallocate_pyramid + greedy_pack (K5 on the GPU)"
+    else:  # beyond K5's placed-set bound: the prefix-sum plan (every tensor private)
+        addr = (np.cumsum(g.edge_size) - g.edge_size).astype(np.uint64)
+        has = (g.edge_size > 0).astype(np.uint8)
+        plan_src = "prefix sums (every tensor at its own offset; K5 holds <= 8192 edges)"
+    rng = np.random.default_rng(1234)
+    tam = addr.copy()
+    movers = rng.choice(np.nonzero(has)[0], size=min(64, int(has.sum())), replace=False)
+    tam[movers] = addr[rng.choice(np.nonzero(has)[0], size=len(movers))]
     d_addr = torch.from_numpy(addr.view(np.int64)).to(dev)
-    d_has = torch.from_numpy((g.edge_size > 0).astype(np.uint8)).to(dev)
+    d_tam = torch.from_numpy(tam.view(np.int64)).to(dev)
+    d_has = torch.from_numpy(has).to(dev)
     viol_off = torch.zeros(E + 1, dtype=torch.int64, device=dev)
 
     def timed(fn, reps):
@@ -598,11 +632,20 @@ def run_pairs(args, cfg):
                                                     out, count), reps)
     t_val = timed(lambda: planner.validate_pairs_d(E, d_lo, d_hi, d_size, d_has, d_addr, 0, E,
                                                    viol_off, None, 0), reps)
+    n_ok = planner.validate_pairs_d(E, d_lo, d_hi, d_size, d_has, d_addr, 0, E, viol_off, None, 0)
+    # the tampered plan: count, then the violating pairs themselves (count + fill)
+    n_tam = planner.validate_pairs_d(E, d_lo, d_hi, d_size, d_has, d_tam, 0, E, viol_off, None, 0)
+    vbuf = torch.empty((max(n_tam, 1), 2), dtype=torch.int32, device=dev)
+
+    def val_tampered():
+        planner.validate_pairs_d(E, d_lo, d_hi, d_size, d_has, d_tam, 0, E, viol_off, None, 0)
+        planner.validate_pairs_d(E, d_lo, d_hi, d_size, d_has, d_tam, 0, E, viol_off, vbuf, n_tam)
+    t_tam = timed(val_tampered, reps)
+    exp_tam = O.validate_pairs(lo, hi, g.edge_size, has, tam)
+    assert n_ok == 0 and n_tam == len(exp_tam) and (vbuf[:n_tam].cpu().numpy() == exp_tam).all()
     peak_gbs, _ = measured_peak_gbs()
     pair_bytes = 8 * count + 8 * E          # write the pairs + read lo/hi
     # parity spot check of the GPU list against the C restatement (rows [0, 64))
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
     got = out[:count].cpu().numpy()
     cnt_rows, _ = O.overlap_row_stats(lo, hi, g.edge_size, rows=(0, min(64, E)))
     k = int(cnt_rows.sum())
@@ -651,6 +694,12 @@ def run_pairs(args, cfg):
                    "order": "one seeded random topological order"},
         "pairs_ms": t_pairs * 1e3, "validate_ms": t_val * 1e3,
         "validate_checks_per_s": E * (E - 1) / 2 / t_val,
+        "validation": {"plan": plan_src, "valid_plan_violations": int(n_ok),
+                       "tampered": f"{len(movers)} tensors moved onto other tensors' offsets "
+                                   f"(seed 1234): {n_tam} below_above pairs, listed in (i, j) "
+                                   "order = the C restatement's", "tampered_ms": t_tam * 1e3,
+                       "checks_per_s_valid": E * (E - 1) / 2 / t_val,
+                       "roofline": alu_roofline(E * (E - 1) / 2 / t_val, args.config)},
         "roofline": {"bound": "hbm", "achieved": pair_bytes / t_pairs / 1e9, "peak": peak_gbs,
                      "unit": "GB/s", "frac": pair_bytes / t_pairs / 1e9 / peak_gbs,
                      "traffic": None, "kernel": "pair_sweep_kernel count+fill (host-synced)"},

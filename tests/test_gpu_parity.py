@@ -681,3 +681,72 @@ def test_multi_device_scoring(devices):
     assert best == exp
     mpl.close()
     p.close()
+
+
+def test_pairs_and_lp_on_multi_node_schedules(planner):
+    """The drop-in site place_external (pipeline.cpp:119) feeds encode_addresses with
+    lifetimes realized from decode_sequence's multi-node-per-step schedules: GPU
+    realized lifetimes -> K2 pair list -> K7 LP text against the reference's own
+    realized_lifetimes + encode_addresses (filter on) + write_lp."""
+    from schedules import multi_node_schedules
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(1)
+    for kind, layers, seed in (("training_like", 10, 0), ("fork_join", 14, 2)):
+        g = mp.generate_graph(kind, layers, 8, seed)
+        rg = O.RefGraph.load(mp.save_graph(g))
+        for o in mp.random_topo_orders(g, 2, seed=seed + 7):
+            for name, ts, horizon in multi_node_schedules(g, o, rng):
+                lo, hi = planner.realized_lifetimes(g, ts, horizon)
+                rlo, rhi = rg.realized_lifetimes(ts, horizon)
+                assert (lo == rlo).all() and (hi == rhi).all(), name
+                ref = rg.encode_address_pairs(rlo, rhi, filter_pairs=True)
+                got = planner.encode_address_pairs(g, lo, hi)
+                assert got.shape == ref.shape and (got == ref).all(), name
+                assert planner.encode_addresses_lp(g, lo, hi) == rg.encode_addresses_lp(rlo, rhi)
+
+
+@pytest.mark.parametrize("name", ["resnet50_b32", "bert_base_s512", "gpt2_medium_s1024"])
+def test_model_graphs_vs_reference(planner, name):
+    """C2/C3/C4 graphs scored against the compiled reference itself (oracle/_ref:
+    memplan::peak_resident_bytes and its InvalidOrder verdict) on 512 candidates,
+    the batch first-minimum included; peak steps against the restatement."""
+    import gzip
+    import os
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    path = os.path.join(os.path.dirname(__file__), "..", "workloads", "graphs", name + ".json.gz")
+    with gzip.open(path, "rt") as f:
+        text = f.read()
+    g = mp.load_graph(text)
+    rg = O.RefGraph.load(text)
+    orders = mp.random_topo_orders(g, 512, seed=29)
+    orders[10, [2, 3]] = orders[10, [3, 2]]
+    orders[20, 4] = orders[20, 5]
+    res, best = planner.score_orders_best(g, orders)
+    rp, rv, rbest = rg.score_orders(orders, threads=os.cpu_count() or 1)
+    assert (res.valid == rv).all() and (res.peak == rp).all() and best == rbest
+    for i in range(0, 512, 37):
+        if rv[i]:
+            lo, hi = rg.lifetimes_from_order(orders[i])
+            assert O.timeline_peak(lo, hi, g.edge_size, g.n) == (int(res.peak[i]),
+                                                                  int(res.peak_step[i]))
+
+
+def test_c5_random_orders_vs_reference(planner):
+    """The 100k-tensor graph: 16 random candidates' peaks and verdicts against the
+    compiled reference (memplan::peak_resident_bytes on all host threads) and the
+    peak steps against the restatement (replaces a GPU-vs-GPU comparison)."""
+    import os
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    g = mp.generate_graph("training_like", 33333, 8)
+    rg = O.RefGraph.generate("training_like", 33333, 8)
+    orders = mp.random_topo_orders(g, 16, seed=41)
+    orders[3, 100] = orders[3, 200]                   # a duplicated node: not a permutation
+    res = planner.score_orders(g, orders)
+    rp, rv, _ = rg.score_orders(orders, threads=os.cpu_count() or 1)
+    assert (res.valid == rv).all() and (res.peak == rp).all() and rv[3] == 0
+    for i in (0, 7, 15):
+        lo, hi = rg.lifetimes_from_order(orders[i])
+        assert O.timeline_peak(lo, hi, g.edge_size, g.n) == (int(res.peak[i]), int(res.peak_step[i]))

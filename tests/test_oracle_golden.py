@@ -213,3 +213,30 @@ def test_fast_timeline_matches_literal_restatement():
     lo, hi = np.array([1, 2, 1], np.int32), np.array([2, 3, 3], np.int32)
     assert O.timeline_peak(lo, hi, z, 3) == (0, 1)
     assert O.timeline_peak(lo, hi, z, 0) == (0, 0)
+
+
+def test_pair_filter_is_a_no_op_on_multi_node_schedules():
+    """SURVEY F4 beyond topological orders: on lifetimes realized from schedules with
+    several nodes per timestep (ASAP layering, random delays, tail nodes at the
+    horizon - decode_sequence's shapes, plan.cpp:28-77), the reference's
+    encode_addresses pair set WITH its edge_precedes filter (encode.cpp:347-357)
+    equals the unfiltered interval-intersection set the K2 kernel emits, pair for
+    pair and in order; so does its LP text."""
+    import paper_2210_12924_b200 as mp
+    from schedules import multi_node_schedules
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(0)
+    cases = 0
+    for kind, layers, seed in (("training_like", 8, 0), ("fork_join", 12, 1), ("chain", 10, 0),
+                               ("fork_join", 25, 5)):
+        g = mp.generate_graph(kind, layers, 8, seed)
+        rg = O.RefGraph.load(mp.save_graph(g))
+        for o in mp.random_topo_orders(g, 3, seed=seed + 3):
+            for name, ts, horizon in multi_node_schedules(g, o, rng):
+                lo, hi = rg.realized_lifetimes(ts, horizon)
+                ref = rg.encode_address_pairs(lo, hi, filter_pairs=True)
+                got = O.overlap_pairs(lo, hi, g.edge_size)
+                assert got.shape == ref.shape and (got == ref).all(), (kind, name)
+                cases += 1
+    assert cases == 4 * 3 * 6
