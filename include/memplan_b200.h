@@ -237,12 +237,18 @@ double mp_fragmentation(uint64_t mr, uint64_t rs);
  * fused kernel with its argmin), and combines the per-device first minima on
  * the host: *best is the lowest index among equal minimal peaks over all
  * shards, exactly a serial first-minimum scan (-1 when nothing is valid).
+ * With distinct devices and NCCL present (loaded at run time), mp_multi_create
+ * makes one communicator per device (ncclCommInitAll) and the shards' fused
+ * {key, overflow} pairs meet in ONE device-side ncclAllReduce(MIN);
+ * the host combine remains only for repeated devices, a missing NCCL, or a key
+ * that does not fit (mp_multi_nccl tells which path is active).
  * Multi-process jobs use the same kernels with one NCCL allreduce(MIN) on the
  * packed key instead (mp_score_orders_argmin_d + paper_2210_12924_b200/dist.py). */
 typedef struct mp_multi mp_multi;
 mp_status mp_multi_create(const int* devices, int num_devices, mp_multi** out);
 mp_status mp_multi_destroy(mp_multi* m);
 mp_status mp_multi_upload(mp_multi* m, const mp_csr* csr);
+int mp_multi_nccl(const mp_multi* m);
 mp_status mp_score_orders_multi(mp_multi* m, const int32_t* orders, int64_t num_orders,
                                 uint64_t* peak, int32_t* peak_step, uint8_t* valid,
                                 int64_t* best);

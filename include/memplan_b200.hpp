@@ -82,18 +82,36 @@ class Planner {
   mp_ctx* ctx() const { return ctx_; }
 
   // The device copy of `g` (uploaded on first use). Cached by address AND a
-  // structural fingerprint: a destroyed graph's address can be reused by the
-  // next one, which must not hit the stale upload.
+  // fingerprint: a destroyed graph's address can be reused by the next one, which
+  // must not hit the stale upload. memplan::Graph is immutable once built
+  // (SPEC.md:86-87), so a hit compares a cheap fingerprint (dimensions, total
+  // bytes and 64 sampled edges); the full O(E + S) one is taken at upload. At
+  // most kMaxGraphs uploads stay cached (least recently used evicted first);
+  // release() drops one explicitly.
+  static constexpr size_t kMaxGraphs = 16;
   mp_graph* device_graph(const memplan::Graph& g) {
-    const std::uint64_t fp = fingerprint(g);
+    const std::uint64_t quick = quick_fingerprint(g);
     auto it = graphs_.find(&g);
     if (it != graphs_.end()) {
-      if (it->second.fp == fp) return it->second.handle;
+      if (it->second.quick == quick) {
+        it->second.last_use = ++clock_;
+        return it->second.handle;
+      }
       mp_graph_free(it->second.handle);
       graphs_.erase(it);
     }
+    if (graphs_.size() >= kMaxGraphs) {
+      auto lru = graphs_.begin();
+      for (auto j = graphs_.begin(); j != graphs_.end(); ++j)
+        if (j->second.last_use < lru->second.last_use) lru = j;
+      mp_graph_free(lru->second.handle);
+      graphs_.erase(lru);
+    }
+    const std::uint64_t fp = fingerprint(g);
     Uploaded u;
     u.fp = fp;
+    u.quick = quick;
+    u.last_use = ++clock_;
     const int E = g.num_edges();
     u.src.resize(E);
     u.off.resize(E + 1, 0);
@@ -480,6 +498,32 @@ class Planner {
     if (base) *base = b;
   }
 
+  // Drops the cached device copy of `g` (e.g. before destroying the graph).
+ public:
+  void release(const memplan::Graph& g) {
+    auto it = graphs_.find(&g);
+    if (it == graphs_.end()) return;
+    mp_graph_free(it->second.handle);
+    graphs_.erase(it);
+  }
+
+ private:
+  static std::uint64_t quick_fingerprint(const memplan::Graph& g) {
+    std::uint64_t h = 1469598103934665603ull;
+    auto mix = [&h](std::uint64_t x) { h = (h ^ x) * 1099511628211ull; };
+    const int E = g.num_edges();
+    mix((std::uint64_t)g.num_nodes());
+    mix((std::uint64_t)E);
+    mix(g.total_bytes());
+    for (int k = 0; k < 64 && E > 0; ++k) {
+      const int e = (int)((int64_t)k * E / 64);
+      mix((std::uint64_t)g.source_of(e));
+      mix(g.edge(e).size);
+      mix((std::uint64_t)g.sinks_of(e).size());
+    }
+    return h;
+  }
+
   static std::uint64_t fingerprint(const memplan::Graph& g) {
     std::uint64_t h = 1469598103934665603ull;
     auto mix = [&h](std::uint64_t x) { h = (h ^ x) * 1099511628211ull; };
@@ -494,7 +538,7 @@ class Planner {
   }
 
   struct Uploaded {
-    std::uint64_t fp = 0;
+    std::uint64_t fp = 0, quick = 0, last_use = 0;
     mp_graph* handle = nullptr;
     std::vector<int32_t> src, sinks;
     std::vector<int64_t> off;
@@ -502,6 +546,7 @@ class Planner {
   };
   mp_ctx* ctx_ = nullptr;
   std::unordered_map<const memplan::Graph*, Uploaded> graphs_;
+  std::uint64_t clock_ = 0;
 };
 
 }  // namespace memplan_b200

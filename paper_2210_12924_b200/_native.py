@@ -40,7 +40,7 @@ EXPORTS = [
     "mp_place", "mp_place_d", "mp_run_baseline", "mp_run_baseline_d", "mp_encode_addresses_lp",
     "mp_joint_pairs", "mp_multi_create", "mp_multi_destroy", "mp_multi_upload",
     "mp_score_orders_multi", "mp_parts_plan_host", "mp_score_plans_d", "mp_lifetimes_batch_d",
-    "mp_validate_plans_d",
+    "mp_validate_plans_d", "mp_multi_nccl",
 ]
 
 
@@ -124,6 +124,7 @@ def lib():
             "mp_fragmentation": (C.c_double, [u64, u64]),
             "mp_multi_create": (C.c_int, [vp, C.c_int, P(vp)]),
             "mp_multi_destroy": (C.c_int, [vp]),
+            "mp_multi_nccl": (C.c_int, [vp]),
             "mp_multi_upload": (C.c_int, [vp, P(MpCsr)]),
             "mp_score_orders_multi": (C.c_int, [vp, vp, i64, vp, vp, vp, P(i64)]),
             "mp_joint_pairs": (C.c_int, [vp, vp, C.c_int, vp, i64, P(i64)]),

@@ -2,6 +2,8 @@
 // with the derived scoring tables, and the host-buffer / device-buffer entry
 // points that launch the kernels in k_score.cu, k_lifetimes.cu, k_pairs.cu.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <thread>
@@ -92,6 +94,15 @@ mp_status upload(T** dst, const T* src, size_t count, cudaStream_t st) {
 }  // namespace mpb
 
 using namespace mpb;
+
+namespace {
+// A graph is bound to the context (device) it was uploaded to: a graph
+// from another context would launch kernels on one device over another's tables.
+mp_status same_ctx(const mp_ctx* ctx, const mp_graph* g) {
+  if (ctx && g && g->ctx != ctx) return invalid_arg("graph belongs to another context");
+  return MP_OK;
+}
+}  // namespace
 
 extern "C" {
 
@@ -407,6 +418,7 @@ mp_status mp_graph_get_info(const mp_graph* g, mp_graph_info* info) {
 // ---- lifetimes ------------------------------------------------------------------
 mp_status mp_lifetimes_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_order, int64_t len,
                          int32_t* d_lo, int32_t* d_hi, int32_t* d_valid, void* stream) {
+  MP_TRY(same_ctx(ctx, g));
   if (!ctx || !g || (len > 0 && !d_order) || !d_valid) return invalid_arg("null argument");
   DeviceGuard guard(ctx->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL: default stream
@@ -417,6 +429,7 @@ mp_status mp_lifetimes_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_order,
 
 mp_status mp_lifetimes(mp_ctx* ctx, const mp_graph* g, const int32_t* order, int64_t len,
                        int32_t* lo, int32_t* hi) {
+  MP_TRY(same_ctx(ctx, g));
   if (!ctx || !g || (len > 0 && !order) || (g->E > 0 && (!lo || !hi)))
     return invalid_arg("null argument");
   if (len != g->n) return invalid_order();
@@ -446,6 +459,7 @@ mp_status mp_lifetimes(mp_ctx* ctx, const mp_graph* g, const int32_t* order, int
 mp_status mp_realized_lifetimes(mp_ctx* ctx, const mp_graph* g, const int32_t* timestep_of,
                                 int32_t horizon, int32_t* lo, int32_t* hi,
                                 int32_t* missing_node) {
+  MP_TRY(same_ctx(ctx, g));
   if (!ctx || !g || (g->n > 0 && !timestep_of) || (g->E > 0 && (!lo || !hi)))
     return invalid_arg("null argument");
   if (missing_node) *missing_node = -1;
@@ -526,18 +540,21 @@ static mp_status score_one(mp_ctx* ctx, const mp_graph* g, const int32_t* order,
 
 mp_status mp_resident_bytes(mp_ctx* ctx, const mp_graph* g, const int32_t* order, int64_t len,
                             uint64_t* bytes) {
+  MP_TRY(same_ctx(ctx, g));
   if (g && g->n > 0 && !bytes) return invalid_arg("bytes is null");
   return score_one(ctx, g, order, len, bytes, nullptr);
 }
 
 mp_status mp_peak_resident_bytes(mp_ctx* ctx, const mp_graph* g, const int32_t* order,
                                  int64_t len, uint64_t* peak) {
+  MP_TRY(same_ctx(ctx, g));
   if (!peak) return invalid_arg("peak is null");
   return score_one(ctx, g, order, len, nullptr, peak);
 }
 
 mp_status mp_timeline(mp_ctx* ctx, const mp_graph* g, const int32_t* lo, const int32_t* hi,
                       int32_t horizon, uint64_t* bytes, uint64_t* peak_rs, int32_t* peak_step) {
+  MP_TRY(same_ctx(ctx, g));
   if (!ctx || !g || (g->E > 0 && (!lo || !hi)) || !peak_rs || !peak_step)
     return invalid_arg("null argument");
   if (horizon < 0) return invalid_arg("negative horizon");
@@ -577,6 +594,7 @@ mp_status mp_score_orders_argmin_d(mp_ctx* ctx, const mp_graph* g, const int32_t
                                    int64_t C, uint64_t* d_peak, int32_t* d_step,
                                    uint8_t* d_valid, uint64_t* d_best_key, int64_t index_base,
                                    void* stream) {
+  MP_TRY(same_ctx(ctx, g));
   if (!ctx || !g || C < 0 || index_base < 0) return invalid_arg("null argument or negative count");
   if (C > 0 && (!d_peak || !d_step || !d_valid || (g->n > 0 && !d_orders)))
     return invalid_arg("null output");
@@ -655,12 +673,34 @@ mp_status d2h_large(mp_ctx* ctx, void* dst, const void* src, size_t bytes, cudaS
 }
 }  // namespace mpb
 
+namespace mpb {
+// Reduces the fused {key, overflow} pair on the device across shards (NCCL), on
+// the scoring stream, before the key is read back. Null: single shard.
+struct KeyReduce {
+  mp_status (*fn)(void* arg, uint64_t* d_key, cudaStream_t st) = nullptr;
+  void* arg = nullptr;
+  int64_t index_base = 0;  // global index of this shard's first candidate
+};
+mp_status score_best_impl(mp_ctx* ctx, const mp_graph* g, const int32_t* orders, int64_t C,
+                          uint64_t* peak, int32_t* step, uint8_t* valid, int64_t* best,
+                          const KeyReduce* kr, bool* key_overflow);
+}  // namespace mpb
+
 mp_status mp_score_orders_best(mp_ctx* ctx, const mp_graph* g, const int32_t* orders, int64_t C,
                                uint64_t* peak, int32_t* step, uint8_t* valid, int64_t* best) {
+  return score_best_impl(ctx, g, orders, C, peak, step, valid, best, nullptr, nullptr);
+}
+
+mp_status mpb::score_best_impl(mp_ctx* ctx, const mp_graph* g, const int32_t* orders, int64_t C,
+                               uint64_t* peak, int32_t* step, uint8_t* valid, int64_t* best,
+                               const KeyReduce* kr, bool* key_overflow) {
   if (!ctx || !g || C < 0) return invalid_arg("null argument or negative count");
+  if (g->ctx != ctx) return invalid_arg("graph belongs to another context");
   if (best) *best = -1;
-  if (C == 0) return MP_OK;
-  if (!peak || !step || !valid || (g->n > 0 && !orders)) return invalid_arg("null buffer");
+  if (key_overflow) *key_overflow = false;
+  const int64_t gbase = kr ? kr->index_base : 0;
+  if (C == 0 && !kr) return MP_OK;
+  if (C > 0 && (!peak || !step || !valid || (g->n > 0 && !orders))) return invalid_arg("null buffer");
   DeviceGuard guard(ctx->device);
   cudaStream_t st = ctx->stream;
   const size_t n = (size_t)g->n, c = (size_t)C;
@@ -671,7 +711,7 @@ mp_status mp_score_orders_best(mp_ctx* ctx, const mp_graph* g, const int32_t* or
   int32_t* d_step = cv.take<int32_t>(c);
   uint8_t* d_valid = cv.take<uint8_t>(c);
   uint64_t* d_key = cv.take<uint64_t>(3);
-  const bool fused = best && C <= (int64_t{1} << 20);
+  const bool fused = (best || kr) && gbase + C <= (int64_t{1} << 20);
   uint64_t* hk = ctx->h_small;  // pinned: async copies, no staging
   if (fused) MP_CUDA(cudaMemsetAsync(d_key, 0x7f, 16, st));  // {MP_KEY_NONE, no overflow}
   // Pipeline: the orders go up in chunks on the copy stream while the previous
@@ -726,13 +766,25 @@ mp_status mp_score_orders_best(mp_ctx* ctx, const mp_graph* g, const int32_t* or
     const int32_t* chunk = p16 ? reinterpret_cast<const int32_t*>(d16 + (size_t)b * n)
                                : d_orders + (size_t)b * n;
     MP_TRY(launch_score(g, chunk, m, d_peak + b, d_step + b, d_valid + b, nullptr,
-                        fused ? d_key : nullptr, b, st, p16));
+                        fused ? d_key : nullptr, gbase + b, st, p16));
     MP_CUDA(cudaMemcpyAsync(peak + b, d_peak + b, 8 * (size_t)m, cudaMemcpyDeviceToHost, st));
     MP_CUDA(cudaMemcpyAsync(step + b, d_step + b, 4 * (size_t)m, cudaMemcpyDeviceToHost, st));
     MP_CUDA(cudaMemcpyAsync(valid + b, d_valid + b, (size_t)m, cudaMemcpyDeviceToHost, st));
   }
-  if (fused) MP_CUDA(cudaMemcpyAsync(hk, d_key, 16, cudaMemcpyDeviceToHost, st));
+  if (kr) {  // every shard takes part in the reduction, overflowed or not
+    if (!fused) MP_CUDA(cudaMemsetAsync(d_key, 0, 16, st));  // {0, overflow}: forces the fallback
+    MP_TRY(kr->fn(kr->arg, d_key, st));
+  }
+  if (fused || kr) MP_CUDA(cudaMemcpyAsync(hk, d_key, 16, cudaMemcpyDeviceToHost, st));
   MP_CUDA(cudaStreamSynchronize(st));
+  if (kr) {  // the reduced pair: global first minimum, or every shard falls back
+    if (hk[1] == 0) {
+      if (key_overflow) *key_overflow = true;
+    } else if (best) {
+      *best = hk[0] == MP_KEY_NONE ? -1 : (int64_t)(hk[0] & ((1ull << 20) - 1));
+    }
+    return MP_OK;
+  }
   if (best) {
     if (fused && hk[1] != 0 && hk[0] == MP_KEY_NONE) {
       *best = -1;                                     // no valid candidate
@@ -912,6 +964,55 @@ mp_status mp_validate_pairs_d(mp_ctx* ctx, int32_t E, const int32_t* d_lo, const
 }
 
 // ---- one process, several GPUs (§8e) ------------------------------------------------
+// NCCL is loaded at run time (the library does not link it, so a process without
+// NCCL still scores on one GPU); its few entry points are resolved by name.
+namespace {
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*comm_init_all)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    if (std::getenv("MP_NO_NCCL")) {
+      a.why = "MP_NO_NCCL set";
+      return a;
+    }
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.why = "libnccl.so.2 not found";
+      return a;
+    }
+    a.comm_init_all = reinterpret_cast<decltype(a.comm_init_all)>(dlsym(h, "ncclCommInitAll"));
+    a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.comm_init_all && a.all_reduce && a.comm_destroy && a.error_string;
+    if (!a.ok) a.why = "libnccl lacks ncclCommInitAll/ncclAllReduce";
+    return a;
+  }();
+  return api;
+}
+
+// one shard's part of the single allreduce(MIN) over the 16-byte {key, overflow}
+mp_status nccl_min_key(void* comm, uint64_t* d_key, cudaStream_t st) {
+  const ncclResult_t r = nccl().all_reduce(d_key, d_key, 2, ncclInt64, ncclMin,
+                                           static_cast<ncclComm_t>(comm), st);
+  if (r != ncclSuccess) {
+    set_error(std::string("ncclAllReduce: ") + nccl().error_string(r));
+    return MP_E_CUDA;
+  }
+  return MP_OK;
+}
+}  // namespace
+
 mp_status mp_multi_create(const int* devices, int G, mp_multi** out) {
   if (!devices || G <= 0 || !out) return invalid_arg("null argument or no devices");
   *out = nullptr;
@@ -925,17 +1026,38 @@ mp_status mp_multi_create(const int* devices, int G, mp_multi** out) {
     }
     m->ctx.push_back(c);
   }
+  // one communicator per device when the devices are distinct (NCCL cannot put
+  // two ranks of one communicator on one GPU); otherwise the host combine
+  std::vector<int> devs(devices, devices + G);
+  std::vector<int> sorted = devs;
+  std::sort(sorted.begin(), sorted.end());
+  if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end()) {
+    m->nccl_note = "repeated device entries";
+  } else if (!nccl().ok) {
+    m->nccl_note = nccl().why;
+  } else {
+    std::vector<ncclComm_t> comms(G);
+    const ncclResult_t r = nccl().comm_init_all(comms.data(), G, devs.data());
+    if (r == ncclSuccess) {
+      m->comm.assign(comms.begin(), comms.end());
+    } else {
+      m->nccl_note = std::string("ncclCommInitAll: ") + nccl().error_string(r);
+    }
+  }
   *out = m;
   return MP_OK;
 }
 
 mp_status mp_multi_destroy(mp_multi* m) {
   if (!m) return MP_OK;
+  for (void* c : m->comm) nccl().comm_destroy(static_cast<ncclComm_t>(c));
   for (mp_graph* g : m->graph) mp_graph_free(g);
   for (mp_ctx* c : m->ctx) mp_ctx_destroy(c);
   delete m;
   return MP_OK;
 }
+
+int mp_multi_nccl(const mp_multi* m) { return m && !m->comm.empty() ? 1 : 0; }
 
 mp_status mp_multi_upload(mp_multi* m, const mp_csr* csr) {
   if (!m || !csr) return invalid_arg("null argument");
@@ -952,16 +1074,28 @@ mp_status mp_score_orders_multi(mp_multi* m, const int32_t* orders, int64_t C, u
   if (C == 0) return MP_OK;
   const int G = (int)m->ctx.size();
   const int64_t n = m->graph[0]->n;
+  const bool use_nccl = !m->comm.empty();
   std::vector<mp_status> st(G, MP_OK);
   std::vector<std::string> err(G);
-  std::vector<int64_t> lbest(G, -1), beg(G + 1);
+  std::vector<int64_t> lbest(G, -1), gbest(G, -1), beg(G + 1);
+  std::vector<char> over(G, 0);
   for (int i = 0; i <= G; ++i) beg[i] = C * i / G;  // contiguous shards, as shard_range
   std::vector<std::thread> pool;
   for (int i = 0; i < G; ++i)
     pool.emplace_back([&, i] {
       const int64_t b = beg[i], c = beg[i + 1] - beg[i];
-      st[i] = mp_score_orders_best(m->ctx[i], m->graph[i], orders ? orders + b * n : nullptr, c,
-                                   peak + b, step + b, valid + b, &lbest[i]);
+      KeyReduce kr;
+      kr.fn = [](void* comm, uint64_t* d_key, cudaStream_t s) { return nccl_min_key(comm, d_key, s); };
+      kr.arg = use_nccl ? m->comm[i] : nullptr;
+      kr.index_base = b;
+      bool ovf = false;
+      // NCCL: every shard's fused key goes through ONE allreduce(MIN) on the device
+      // and each thread reads back the global first minimum; otherwise each shard's
+      // own first minimum comes back and the host combines them.
+      st[i] = score_best_impl(m->ctx[i], m->graph[i], orders ? orders + b * n : nullptr, c,
+                              peak + b, step + b, valid + b, use_nccl ? &gbest[i] : &lbest[i],
+                              use_nccl ? &kr : nullptr, &ovf);
+      over[i] = ovf ? 1 : 0;
       if (st[i] != MP_OK) err[i] = mp_last_error();
     });
   for (std::thread& t : pool) t.join();
@@ -970,12 +1104,22 @@ mp_status mp_score_orders_multi(mp_multi* m, const int32_t* orders, int64_t C, u
       set_error(err[i]);
       return st[i];
     }
-  // first minimum over the shards' first minima, in index order
+  if (use_nccl && !over[0]) {  // the reduced key is the same on every device
+    if (best) *best = gbest[0];
+    return MP_OK;
+  }
+  // host combine: first minimum over the scores, in index order (also the NCCL
+  // path's fallback when some shard's key did not fit)
   int64_t bi = -1;
-  for (int i = 0; i < G; ++i) {
-    if (lbest[i] < 0) continue;
-    const int64_t gi = beg[i] + lbest[i];
-    if (bi < 0 || peak[gi] < peak[bi]) bi = gi;
+  if (use_nccl) {
+    for (int64_t c = 0; c < C; ++c)
+      if (valid[c] && (bi < 0 || peak[c] < peak[bi])) bi = c;
+  } else {
+    for (int i = 0; i < G; ++i) {
+      if (lbest[i] < 0) continue;
+      const int64_t gi = beg[i] + lbest[i];
+      if (bi < 0 || peak[gi] < peak[bi]) bi = gi;
+    }
   }
   if (best) *best = bi;
   return MP_OK;
@@ -1074,6 +1218,7 @@ mp_status joint_tables(mp_graph* g) {
 
 mp_status mp_joint_pairs(mp_ctx* ctx, const mp_graph* g, int filter, int32_t* pairs, int64_t cap,
                          int64_t* count) {
+  MP_TRY(same_ctx(ctx, g));
   if (!ctx || !g || !count) return invalid_arg("null argument");
   *count = 0;
   DeviceGuard guard(ctx->device);
@@ -1336,6 +1481,7 @@ mp_status mp_encode_addresses_lp(mp_ctx* ctx, int32_t E, const int32_t* lo, cons
 mp_status mp_run_baseline_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_orders, int64_t B,
                             int best_fit, uint64_t* d_mr, uint64_t* d_rs, double* d_frag,
                             uint8_t* d_valid, void* stream) {
+  MP_TRY(same_ctx(ctx, g));
   if (!ctx || !g || B < 0) return invalid_arg("null argument");
   if (B == 0) return MP_OK;
   if ((!d_orders && g->n > 0) || !d_mr || !d_rs || !d_frag || !d_valid)
@@ -1370,6 +1516,7 @@ mp_status mp_run_baseline_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_ord
 mp_status mp_run_baseline(mp_ctx* ctx, const mp_graph* g, const int32_t* orders, int64_t B,
                           int best_fit, uint64_t* mr, uint64_t* rs, double* frag,
                           uint8_t* valid) {
+  MP_TRY(same_ctx(ctx, g));
   if (!ctx || !g || B < 0) return invalid_arg("null argument");
   if (B == 0) return MP_OK;
   if ((!orders && g->n > 0) || !mr || !rs || !frag || !valid) return invalid_arg("null argument");

@@ -62,9 +62,13 @@ struct mp_ctx {
 };
 
 // Several contexts in one process, the graph replicated on each (mp_score_orders_multi).
+// With distinct devices and libnccl available, one NCCL communicator per device
+// (ncclCommInitAll) reduces the fused argmin key on the devices.
 struct mp_multi {
   std::vector<mp_ctx*> ctx;
   std::vector<mp_graph*> graph;
+  std::vector<void*> comm;  // ncclComm_t per context, empty without NCCL
+  std::string nccl_note;    // why NCCL is not used (empty when it is)
 };
 
 // Device-resident graph tables. Built once by mp_graph_upload from the

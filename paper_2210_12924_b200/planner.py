@@ -105,7 +105,9 @@ def load_plan(text: str) -> MemoryPlan:
 class MultiPlanner:
     """One process, several GPUs (mp_multi_*): the graph replicated on every device,
     candidates split into contiguous shards scored concurrently (one host thread
-    per device), the first minimum combined on the host."""
+    per device), the shards' first minima meeting in ONE device-side NCCL
+    allreduce(MIN) on the fused key when the devices are distinct and NCCL loads
+    (``nccl`` is True), else combined on the host."""
 
     def __init__(self, devices: Sequence[int]):
         devs = (C.c_int * len(devices))(*devices)
@@ -113,6 +115,7 @@ class MultiPlanner:
         _native.check(_native.lib().mp_multi_create(devs, len(devices), C.byref(h)))
         self.handle = h
         self.graph = None
+        self.nccl = bool(_native.lib().mp_multi_nccl(h))
 
     def upload(self, graph: Graph) -> None:
         self._csr = graph.mp_csr()

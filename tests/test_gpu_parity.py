@@ -658,8 +658,10 @@ def test_edge_cases(planner):
 @pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0]])
 def test_multi_device_scoring(devices):
     """mp_score_orders_multi: contiguous shards on several contexts (repeated device
-    0 here: one GPU on the box) with host threads, the first minimum combined on the
-    host - identical to one context and to a serial first-minimum scan."""
+    0 here: one GPU on the box) with host threads - through ONE NCCL allreduce(MIN)
+    of the fused key for distinct devices ([0]: a one-rank communicator), the host
+    combine for repeated ones - identical to one context and to a serial
+    first-minimum scan."""
     import gzip
     import os
     path = os.path.join(os.path.dirname(__file__), "..", "workloads", "graphs",
@@ -670,6 +672,7 @@ def test_multi_device_scoring(devices):
     orders[0, [0, 1]] = orders[0, [1, 0]]
     orders[150] = orders[77]          # a tie across shards: the lower index must win
     mpl = mp.MultiPlanner(devices)
+    assert mpl.nccl == (len(set(devices)) == len(devices))
     mpl.upload(g)
     res, best = mpl.score_orders(orders)
     p = mp.Planner(0)
