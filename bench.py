@@ -1189,7 +1189,7 @@ def main():
     torch.cuda.synchronize()
     h2d_gbs = 5 * batch_bytes / (time.perf_counter() - th) / 1e9
 
-    wire_bytes = batch_bytes // 2 if info["orders16"] else batch_bytes
+    wire_bytes = batch_bytes * {1: 2, 2: 3}.get(info["orders16"], 4) // 4
     line = None
     if rank == 0:
         cpu = None
@@ -1209,10 +1209,11 @@ def main():
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "peak_source": peak_src},
             "e2e": {"value": e2e_value, "unit": "plans/s",
-                    "h2d_bytes_per_step": batch_bytes // 2 if info["orders16"] else batch_bytes,
+                    "h2d_bytes_per_step": wire_bytes,
                     "host_input_bytes_per_step": batch_bytes,
-                    "orders_on_wire": "uint16 (packed on the host cores)" if info["orders16"]
-                    else "int32",
+                    "orders_on_wire": {1: "uint16 (packed on the host cores)",
+                                       2: "3-byte ids (packed on the host cores)"}.get(
+                                           info["orders16"], "int32"),
                     "d2h_bytes_per_step": C * 13 + 8,
                     "path": "Planner.score_orders_into -> mp_score_orders_best (pinned host)",
                     "torch_pinned_h2d_gbs": h2d_gbs,

@@ -72,7 +72,8 @@ typedef struct {
   int32_t num_multi_sink;  /* data edges whose last consumer depends on the order */
   int32_t smem_resident;   /* 1 when the fused scorer keeps per-candidate state in smem */
   uint64_t total_bytes;    /* Graph::total_bytes() (graph.hpp:93) */
-  int32_t orders16;        /* 1: host-buffer scoring sends orders as uint16 (half the bytes) */
+  int32_t orders16;        /* host-buffer scoring's wire format: 1 uint16 ids (half the bytes),
+                              2 3-byte ids (three quarters), 0 int32 */
   int32_t score_variant;   /* MP_SCORER_*: which fused-scorer formulation the graph got */
 } mp_graph_info;
 #define MP_SCORER_REG 1      /* register slots, per-candidate state in smem (n up to ~8k) */

@@ -752,10 +752,12 @@ mp_status run_warp(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64
 
 mp_status run_parts(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d_peak,
                     int32_t* d_step, uint8_t* d_valid, uint64_t* d_key, int64_t index_base,
-                    cudaStream_t st) {
+                    cudaStream_t st, bool o24) {
   const auto& Q = g->parts;
   const bool vec = g->n % 4 == 0;
-  auto kern = vec ? score_parts_kernel<true> : score_parts_kernel<false>;
+  if (o24 && !vec) return MP_E_INVALID_ARG;
+  auto kern = o24 ? score_parts_kernel<true, true>
+                  : vec ? score_parts_kernel<true> : score_parts_kernel<false>;
   MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q.smem));
   int64_t grid = g->ctx->num_sms;
   if (const char* e = std::getenv("MP_SCORE_GRID")) {
@@ -796,9 +798,12 @@ mp_status run_parts(const mp_graph* g, const int32_t* d_orders, int64_t C, uint6
 template <typename VT>
 mp_status dispatch(const mp_graph* g, const int32_t* o, int64_t C, uint64_t* pk, int32_t* stp,
                    uint8_t* vl, uint64_t* by, uint64_t* key, int64_t base, cudaStream_t st,
-                   bool o16) {
+                   int ofmt) {
+  const bool o16 = ofmt == kOrdU16;
   if (o16 && !score_takes_u16(g)) return MP_E_INVALID_ARG;
-  if (g->use_parts && by == nullptr) return run_parts(g, o, C, pk, stp, vl, key, base, st);
+  if (ofmt == kOrdU24 && !score_takes_u24(g)) return MP_E_INVALID_ARG;
+  if (g->use_parts && by == nullptr)
+    return run_parts(g, o, C, pk, stp, vl, key, base, st, ofmt == kOrdU24);
   if (g->score_warps > 0) return run_warp<VT>(g, o, C, pk, stp, vl, by, key, base, st);
   switch (g->score_j) {
     case 4:
@@ -909,6 +914,10 @@ mp_status score_configure(mp_graph* g) {
   return MP_OK;
 }
 
+bool score_takes_u24(const mp_graph* g) {
+  return g->use_parts && g->n > 0 && g->n % 4 == 0 && g->n < 0xffffff;
+}
+
 bool score_takes_u16(const mp_graph* g) {
   return g->n > 0 && g->n < 65535 && g->score_j > 0 && g->score_warps == 0 && g->score_kc == 1 &&
          !g->use_parts;
@@ -916,13 +925,13 @@ bool score_takes_u16(const mp_graph* g) {
 
 mp_status launch_score(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d_peak,
                        int32_t* d_step, uint8_t* d_valid, uint64_t* d_bytes, uint64_t* d_key,
-                       int64_t index_base, cudaStream_t st, bool orders16) {
+                       int64_t index_base, cudaStream_t st, int ofmt) {
   if (C <= 0) return MP_OK;
   if (g->narrow)
     return dispatch<uint32_t>(g, d_orders, C, d_peak, d_step, d_valid, d_bytes, d_key,
-                              index_base, st, orders16);
+                              index_base, st, ofmt);
   return dispatch<unsigned long long>(g, d_orders, C, d_peak, d_step, d_valid, d_bytes, d_key,
-                                      index_base, st, orders16);
+                                      index_base, st, ofmt);
 }
 
 // ---- argmin over candidates (single CTA; C is at most a few million) ------------

@@ -75,7 +75,9 @@ __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
-template <bool kVec>
+// k24: orders arrive as 24-bit ids (3 bytes per position, host-packed for the
+// PCIe leg of the host-buffer call; n % 4 == 0, out-of-range ids as 0xffffff).
+template <bool kVec, bool k24 = false>
 __global__ void __launch_bounds__(kPartsThreads, 1)
     score_parts_kernel(PartArgs A, int32_t n, const int32_t* __restrict__ orders, int64_t C,
                        uint64_t* __restrict__ peak_out, int32_t* __restrict__ step_out,
@@ -112,6 +114,8 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
 
   for (int64_t c = blockIdx.x; c < C; c += gridDim.x) {
     const int32_t* ord = orders + c * (int64_t)n;
+    // 24-bit rows: 3n bytes each = 3n/4 words (n % 4 == 0)
+    const uint32_t* ord24 = reinterpret_cast<const uint32_t*>(orders) + c * (int64_t)(3 * (n >> 2));
     bool bad = false;
     uint32_t segx = 0;  // sum of x over this lane's positions (modular)
     for (int i = tid; i < A.n_slot_init; i += T) stash[__ldg(A.slot_init + i)] = 0;
@@ -148,7 +152,17 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
         for (int u = 0; u < kPartsU; ++u) {  // kPartsU 16-byte loads in flight per thread
           const int r = r0 + u * 128;
           int4 q;
-          if (kVec) {
+          if (k24) {  // four 3-byte ids in three words (word index 3r/4)
+            if (r >= n) {
+              q = make_int4(-1, -1, -1, -1);
+            } else {
+              const uint32_t* w = ord24 + 3 * (r >> 2);
+              const uint32_t w0 = __ldg(w), w1 = __ldg(w + 1), w2 = __ldg(w + 2);
+              auto id = [](uint32_t x) { return x == 0xffffffu ? -1 : (int)x; };
+              q = make_int4(id(w0 & 0xffffffu), id((w0 >> 24) | ((w1 & 0xffffu) << 8)),
+                            id((w1 >> 16) | ((w2 & 0xffu) << 16)), id(w2 >> 8));
+            }
+          } else if (kVec) {
             const int4* p4 = reinterpret_cast<const int4*>(ord + r);
             q = r >= n ? make_int4(-1, -1, -1, -1) : last ? __ldcs(p4) : __ldg(p4);
           } else {

@@ -406,7 +406,9 @@ mp_status mp_graph_get_info(const mp_graph* g, mp_graph_info* info) {
   info->num_multi_sink = g->n_dyn;
   info->smem_resident = g->smem_resident ? 1 : 0;
   info->total_bytes = g->total_bytes;
-  info->orders16 = score_takes_u16(g) && !std::getenv("MP_NO_PACK16") ? 1 : 0;
+  info->orders16 = score_takes_u16(g) && !std::getenv("MP_NO_PACK16")   ? 1
+                   : score_takes_u24(g) && std::getenv("MP_PACK24")     ? 2
+                                                                        : 0;
   info->score_variant = g->use_parts        ? MP_SCORER_PARTS
                         : g->score_warps > 0 ? MP_SCORER_WARP
                         : g->score_j > 0    ? MP_SCORER_REG
@@ -613,6 +615,31 @@ namespace {
 // int32 orders -> uint16 (values outside [0, n) become 0xffff, still out of range
 // for the kernel since n < 65535), on the host cores: the packed orders halve the
 // PCIe bytes of the host-buffer call, the transfer that bounds it.
+// int32 orders -> 3-byte ids, little-endian (values outside [0, n) become 0xffffff,
+// still out of range since n < 0xffffff): the node-partitioned scorer's wire format.
+void pack_orders24(const int32_t* src, uint8_t* dst, size_t cnt, uint32_t n) {
+  static const int nthr = [] {
+    const char* e = std::getenv("MP_PACK_THREADS");
+    const int hw = (int)std::thread::hardware_concurrency();
+    const int v = e ? std::atoi(e) : (hw < 16 ? hw : 16);
+    return v < 1 ? 1 : v;
+  }();
+  const int t = cnt < (size_t{1} << 16) ? 1 : nthr;
+  const int64_t groups = (int64_t)(cnt / 4);  // n % 4 == 0: rows are whole groups
+#pragma omp parallel for num_threads(t) schedule(static)
+  for (int64_t q = 0; q < groups; ++q) {
+    uint32_t v[4];
+    for (int h = 0; h < 4; ++h) {
+      const uint32_t x = (uint32_t)src[4 * q + h];
+      v[h] = x < n ? x : 0xffffffu;
+    }
+    uint32_t* w = reinterpret_cast<uint32_t*>(dst + 12 * q);
+    w[0] = v[0] | v[1] << 24;
+    w[1] = v[1] >> 8 | v[2] << 16;
+    w[2] = v[2] >> 16 | v[3] << 8;
+  }
+}
+
 void pack_orders16(const int32_t* src, uint16_t* dst, size_t cnt, uint32_t n) {
   static const int nthr = [] {
     const char* e = std::getenv("MP_PACK_THREADS");
@@ -729,18 +756,25 @@ mp_status mpb::score_best_impl(mp_ctx* ctx, const mp_graph* g, const int32_t* or
   if (nch > max_ch) nch = max_ch;
   if (nch > C) nch = C;
   if (nch < 1 || n == 0) nch = 1;
-  // 16-bit orders when the graph's scorer takes them (register-slot variant, n < 65535)
+  // Packed orders on the wire when the graph's scorer takes them: 16-bit for the
+  // register-slot variant (n < 65535), 3-byte ids for the node-partitioned one.
   const bool p16 = n > 0 && score_takes_u16(g) && !std::getenv("MP_NO_PACK16");
-  uint16_t* d16 = reinterpret_cast<uint16_t*>(d_orders);
-  const size_t half = n * (size_t)((C + nch - 1) / nch);
+  // (3-byte ids are opt-in, MP_PACK24=1: on the 16-core host of the measuring box
+  // the pack itself bounds the call - 8.6e4 vs 1.0e5 plans/s end to end at C5 - since
+  // it reads 4 B and writes 3 B per id to save 1 B of PCIe)
+  const bool p24 = !p16 && n > 0 && score_takes_u24(g) && std::getenv("MP_PACK24");
+  const size_t wire = p16 ? 2 : p24 ? 3 : 4;  // bytes per id on the wire
+  const int ofmt = p16 ? kOrdU16 : p24 ? kOrdU24 : kOrdI32;
+  uint8_t* dw = reinterpret_cast<uint8_t*>(d_orders);
+  const size_t half = wire * n * (size_t)((C + nch - 1) / nch);  // bytes per staging half
   // a call that failed part-way may have left copies from the staging buffer queued
-  if (p16) MP_CUDA(cudaStreamSynchronize(ctx->copy_stream));
-  if (p16 && ctx->h_stage_elems < half) {
+  if (wire < 4) MP_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+  if (wire < 4 && ctx->h_stage_bytes < half) {
     if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
     ctx->h_stage = nullptr;
-    ctx->h_stage_elems = 0;
-    MP_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_stage), 4 * half));
-    ctx->h_stage_elems = half;
+    ctx->h_stage_bytes = 0;
+    MP_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_stage), 2 * half));
+    ctx->h_stage_bytes = half;
   }
   cudaStream_t cs = nch > 1 ? ctx->copy_stream : st;
   if (nch > 1) {  // the copy stream starts after everything already queued on `st`
@@ -749,24 +783,27 @@ mp_status mpb::score_best_impl(mp_ctx* ctx, const mp_graph* g, const int32_t* or
   }
   for (int64_t k = 0; k < nch; ++k) {
     const int64_t b = C * k / nch, e = C * (k + 1) / nch, m = e - b;
-    if (p16) {  // pack chunk k while chunk k - 1 is on the wire (two staging halves)
-      uint16_t* buf = ctx->h_stage + (size_t)(k & 1) * ctx->h_stage_elems;
+    if (wire < 4) {  // pack chunk k while chunk k - 1 is on the wire (two staging halves)
+      uint8_t* buf = ctx->h_stage + (size_t)(k & 1) * ctx->h_stage_bytes;
       if (k >= 2) MP_CUDA(cudaEventSynchronize(ctx->ev_h2d[k - 2]));  // this half is free
-      pack_orders16(orders + (size_t)b * n, buf, n * (size_t)m, (uint32_t)n);
-      MP_CUDA(cudaMemcpyAsync(d16 + (size_t)b * n, buf, 2 * n * (size_t)m,
+      if (p16)
+        pack_orders16(orders + (size_t)b * n, reinterpret_cast<uint16_t*>(buf), n * (size_t)m,
+                      (uint32_t)n);
+      else
+        pack_orders24(orders + (size_t)b * n, buf, n * (size_t)m, (uint32_t)n);
+      MP_CUDA(cudaMemcpyAsync(dw + wire * (size_t)b * n, buf, wire * n * (size_t)m,
                               cudaMemcpyHostToDevice, cs));
     } else if (n) {
       MP_CUDA(cudaMemcpyAsync(d_orders + (size_t)b * n, orders + (size_t)b * n,
                               4 * n * (size_t)m, cudaMemcpyHostToDevice, cs));
     }
-    if (nch > 1 || p16) {
+    if (nch > 1 || wire < 4) {
       MP_CUDA(cudaEventRecord(ctx->ev_h2d[k], cs));
       if (nch > 1) MP_CUDA(cudaStreamWaitEvent(st, ctx->ev_h2d[k], 0));
     }
-    const int32_t* chunk = p16 ? reinterpret_cast<const int32_t*>(d16 + (size_t)b * n)
-                               : d_orders + (size_t)b * n;
+    const int32_t* chunk = reinterpret_cast<const int32_t*>(dw + wire * (size_t)b * n);
     MP_TRY(launch_score(g, chunk, m, d_peak + b, d_step + b, d_valid + b, nullptr,
-                        fused ? d_key : nullptr, gbase + b, st, p16));
+                        fused ? d_key : nullptr, gbase + b, st, ofmt));
     MP_CUDA(cudaMemcpyAsync(peak + b, d_peak + b, 8 * (size_t)m, cudaMemcpyDeviceToHost, st));
     MP_CUDA(cudaMemcpyAsync(step + b, d_step + b, 4 * (size_t)m, cudaMemcpyDeviceToHost, st));
     MP_CUDA(cudaMemcpyAsync(valid + b, d_valid + b, (size_t)m, cudaMemcpyDeviceToHost, st));

@@ -55,8 +55,8 @@ struct mp_ctx {
   cudaEvent_t ev_h2d[kPipeChunks] = {};
   cudaEvent_t ev_start = nullptr;
   uint64_t* h_small = nullptr;  // pinned: [0] key init, [1] key read-back
-  uint16_t* h_stage = nullptr;  // pinned: two halves of 16-bit packed orders
-  size_t h_stage_elems = 0;     // per half
+  uint8_t* h_stage = nullptr;   // pinned: two halves of packed (16/24-bit) orders
+  size_t h_stage_bytes = 0;     // per half
   char* h_bounce = nullptr;     // pinned: two halves for large results to pageable memory
   cudaEvent_t ev_d2h[2] = {};
 };
@@ -163,9 +163,14 @@ mp_status launch_score(const mp_graph* g, const int32_t* d_orders, int64_t num_o
                        uint64_t* d_bytes /* [C][n] or null */,
                        uint64_t* d_key /* fused argmin key or null */, int64_t index_base,
                        cudaStream_t st,
-                       bool orders16 = false /* d_orders holds uint16 (score_takes_u16) */);
+                       int ofmt = 0 /* kOrdI32, or host-packed kOrdU16 / kOrdU24 */);
 // the fused scorer reads 16-bit orders for this graph (register-slot variant, n < 65535)
 bool score_takes_u16(const mp_graph* g);
+// Order element formats of launch_score: the reference's int32, or the host-buffer
+// call's wire formats (uint16 for the register-slot scorer, 3-byte ids for the
+// node-partitioned one; both map out-of-range ids to an out-of-range value).
+constexpr int kOrdI32 = 0, kOrdU16 = 1, kOrdU24 = 2;
+bool score_takes_u24(const mp_graph* g);
 size_t score_scratch_bytes(const mp_graph* g, int64_t num_orders);
 mp_status score_configure(mp_graph* g);
 

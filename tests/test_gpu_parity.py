@@ -753,3 +753,31 @@ def test_c5_random_orders_vs_reference(planner):
     for i in (0, 7, 15):
         lo, hi = rg.lifetimes_from_order(orders[i])
         assert O.timeline_peak(lo, hi, g.edge_size, g.n) == (int(res.peak[i]), int(res.peak_step[i]))
+
+
+@pytest.mark.parametrize("pack24", [True, False])
+def test_host_scoring_24bit_wire(planner, monkeypatch, pack24):
+    """Host-buffer scoring of a node-partitioned graph with the 3-byte wire format
+    (MP_PACK24, opt-in) and without: out-of-range / negative ids stay invalid, and
+    results equal the device-buffer path row for row."""
+    import torch
+    if pack24:
+        monkeypatch.setenv("MP_PACK24", "1")
+    g = mp.generate_graph("training_like", 20000, 8)       # n = 80,004 (n % 4 == 0)
+    dg = planner.upload(g)
+    assert dg.info()["score_variant"] == 5
+    assert dg.info()["orders16"] == (2 if pack24 else 0)
+    orders = mp.random_topo_orders(g, 40, seed=23)
+    orders[1, 7] = g.n
+    orders[2, 9] = -1
+    orders[3, 11] = (1 << 24) + 5                      # wraps to a valid id if truncated
+    orders[4, [5, 6]] = orders[4, [6, 5]]
+    res, best = planner.score_orders_best(g, orders)
+    d = torch.device("cuda:0")
+    z = [torch.zeros(40, dtype=t, device=d) for t in (torch.int64, torch.int32, torch.uint8)]
+    planner.score_orders_d(dg, torch.from_numpy(orders).to(d), 40, *z,
+                           torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert (z[0].cpu().numpy().view(np.uint64) == res.peak).all()
+    assert (z[1].cpu().numpy() == res.peak_step).all() and (z[2].cpu().numpy() == res.valid).all()
+    assert res.valid[1:4].tolist() == [0, 0, 0]
