@@ -39,7 +39,7 @@ EXPORTS = [
     "mp_fragmentation", "mp_generate_graph", "mp_random_topo_orders",
     "mp_place", "mp_place_d", "mp_run_baseline", "mp_run_baseline_d", "mp_encode_addresses_lp",
     "mp_joint_pairs", "mp_multi_create", "mp_multi_destroy", "mp_multi_upload",
-    "mp_score_orders_multi", "mp_parts_plan_host", "mp_score_plans_d", "mp_lifetimes_batch_d",
+    "mp_score_orders_multi", "mp_parts_plan_host", "mp_prep_host", "mp_score_plans_d", "mp_lifetimes_batch_d",
     "mp_validate_plans_d", "mp_multi_nccl",
 ]
 
@@ -140,6 +140,7 @@ def lib():
                                             vp, vp, vp, vp]),
             "mp_random_topo_orders": (C.c_int, [P(MpCsr), i64, u64, i32, vp]),
             "mp_parts_plan_host": (C.c_int, [P(MpCsr), i32, i64, vp]),
+            "mp_prep_host": (C.c_int, [P(MpCsr), vp, vp, i64]),
             "mp_score_plans_d": (C.c_int, [vp, vp, vp, i64, vp, C.c_uint32, vp, vp, vp, vp, vp,
                                            vp, vp, vp, i64, vp]),
             "mp_lifetimes_batch_d": (C.c_int, [vp, vp, vp, i64, vp, vp, vp, vp]),

@@ -88,7 +88,6 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
   __shared__ uint32_t s_wsum[32];
   __shared__ uint32_t s_wbest[32];
   __shared__ int s_widx[32];
-  __shared__ uint32_t s_segadj[32];  // x removed from warp segment w by multi-consumer frees
   __shared__ PartDesc s_desc[kPartMaxParts];  // read field by field where used (registers)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -117,9 +116,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
     // 24-bit rows: 3n bytes each = 3n/4 words (n % 4 == 0)
     const uint32_t* ord24 = reinterpret_cast<const uint32_t*>(orders) + c * (int64_t)(3 * (n >> 2));
     bool bad = false;
-    uint32_t segx = 0;  // sum of x over this lane's positions (modular)
     for (int i = tid; i < A.n_slot_init; i += T) stash[__ldg(A.slot_init + i)] = 0;
-    if (tid < 32) s_segadj[tid] = 0;
 
     for (int b = 0; b < A.P; ++b) {
       const PartDesc& D = s_desc[b];
@@ -197,7 +194,6 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
             const uint32_t w = lds_u32(a);
             sts_u32(a, (w & 0xff000000u) | (uint32_t)(r0 + (j >> 2) * 128 + (j & 3)));
             stg_u8(xrow + (j >> 2) * 128 + (j & 3), w >> 24);
-            segx += ((w >> 24) & 0xfu) - 8u;
           }
         }
       }
@@ -264,10 +260,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
           if (l3 != 0xffffu) h = max(h, slot[l3] & kPos);
           if (l4 != 0xffffu) h = max(h, slot[l4] & kPos);
           const int hi = (int)h;
-          if (hi < n) {
-            parts_free_at(XF, hi, d.z);
-            atomicAdd(&s_segadj[hi / seg], d.z);
-          }
+          if (hi < n) parts_free_at(XF, hi, d.z);
         }
       }
       __syncthreads();  // slot words are rewritten by the next pass
@@ -275,10 +268,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
     for (int i = tid; i < A.n_xfree; i += T) {  // multi-consumer tensors spanning parts
       const uint2 f = __ldg(A.xfree + i);
       const int hi = (int)stash[f.x];
-      if (hi < n) {
-        parts_free_at(XF, hi, f.y);
-        atomicAdd(&s_segadj[hi / seg], f.y);
-      }
+      if (hi < n) parts_free_at(XF, hi, f.y);
     }
     if (__syncthreads_or(bad)) {
       if (tid == 0) {
@@ -290,8 +280,21 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
     }
 
     // ---- scan over XF (L2 only: the frees above were atomics at L2) -------------------
-    uint32_t tot = warp_sum(segx);
-    if (lane == 0) s_wsum[warp] = tot - s_segadj[warp];
+    // pass 1: the x total of this warp's segment (4 nibbles per word: x + 8 in the
+    // low nibble of each byte, padding bytes are 8 = (x 0, f 0))
+    {
+      uint32_t tot = 0;
+      for (int r00 = wbeg; r00 < wbeg + seg; r00 += 4 * 128) {
+        uint32_t w4s[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          w4s[u] = __ldcg(reinterpret_cast<const unsigned int*>(XF + r00 + u * 128 + 4 * lane));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) tot += (((w4s[u] & 0x0f0f0f0fu) * 0x01010101u) >> 24) - 32u;
+      }
+      tot = warp_sum(tot);
+      if (lane == 0) s_wsum[warp] = tot;
+    }
     __syncthreads();
     uint32_t carry = warp_sum(lane < warp ? s_wsum[lane] : 0u);  // exclusive over warps
     uint32_t best = 0;

@@ -379,6 +379,34 @@ mp_status mp_parts_plan_host(const mp_csr* csr, int32_t max_chunks, int64_t smem
   return MP_OK;
 }
 
+mp_status mp_prep_host(const mp_csr* csr, int64_t* info, int32_t* pairs, int64_t cap) {
+  if (!csr || !info || csr->num_nodes < 0 || csr->num_edges < 0 || cap < 0)
+    return invalid_arg("bad argument");
+  ScorePrep P;
+  prepare_scoring(csr->num_nodes, csr->num_edges, csr->edge_src, csr->sink_off, csr->sinks,
+                  csr->edge_size, &P);
+  info[0] = P.num_reduced_preds;
+  info[1] = (int64_t)P.dyn_size.size();
+  info[2] = P.exact_reach ? 1 : 0;
+  info[3] = P.tiny4 ? 1 : 0;
+  info[4] = P.tiny8 ? 1 : 0;
+  info[5] = P.narrow ? 1 : 0;
+  if (pairs) {
+    int64_t k = 0;
+    for (int32_t w = 0; w < P.n && k < cap; ++w)
+      if (P.pred1[w] >= 0) {
+        pairs[2 * k] = P.pred1[w];
+        pairs[2 * k + 1] = w;
+        ++k;
+      }
+    for (size_t i = 0; i < P.extra_u.size() && k < cap; ++i, ++k) {
+      pairs[2 * k] = P.extra_u[i];
+      pairs[2 * k + 1] = P.extra_w[i];
+    }
+  }
+  return MP_OK;
+}
+
 mp_status mp_graph_free(mp_graph* g) {
   if (!g) return MP_OK;
   DeviceGuard guard(g->ctx->device);

@@ -7,7 +7,8 @@
 // pair; a pair implied by a path of other pairs cannot fail alone).
 //
 //   preds      per consumer node, its producer nodes minus redundant ones
-//              (u -> w is dropped when another successor x of u reaches w)
+//              (u -> w is dropped when another successor x of u reaches w;
+//              exact bitsets up to kExactReachMaxNodes, a chain index above)
 //   alloc      bytes a node creates at its timestep: sum of its data fanout
 //              (lo = pos[src], schedule.cpp:37)
 //   sfree      bytes freed after a node: data edges whose last consumer is
@@ -19,6 +20,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <climits>
+#include <cstdlib>
 #include <numeric>
 
 namespace mpb {
@@ -72,7 +75,11 @@ void prepare_scoring(int32_t n, int32_t E, const int32_t* src, const int64_t* si
   const bool acyclic = topo(n, succ, &order);
 
   // Reachability: exact bitset closure for moderate n, 2-hop rule above.
-  const bool exact = acyclic && n <= kExactReachMaxNodes;
+  // MP_PREP_EXACT_MAX lowers the bitset limit (tests compare the chain index
+  // against the exact closure on small graphs)
+  int64_t exact_max = kExactReachMaxNodes;
+  if (const char* e = std::getenv("MP_PREP_EXACT_MAX")) exact_max = std::atoll(e);
+  const bool exact = acyclic && n <= exact_max;
   const size_t words = ((size_t)n + 63) / 64;
   std::vector<uint64_t> reach;  // reach[v*words + w/64] bit: v reaches w (v != w)
   if (exact) {
@@ -87,11 +94,69 @@ void prepare_scoring(int32_t n, int32_t E, const int32_t* src, const int64_t* si
       }
     }
   }
+  // Above the bitset limit: a chain index. Greedy chain cover along the Kahn
+  // order (each node extends the longest chain ending at one of its producers),
+  // then for the K longest chains c, minidx[v][c] = lowest chain index of a node of
+  // c that v reaches (itself included). a reaches b on such a chain iff
+  // minidx[a][c] <= idx(b): exact. Other targets are decided through their
+  // producers (one level) and otherwise answered "no" - sound: a pair kept or a
+  // sink kept as a candidate last consumer only costs a redundant check.
+  std::vector<int32_t> chain_of, chain_idx, minidx;
+  int32_t K = 0;
+  if (acyclic && !exact && n > 0) {
+    chain_of.assign(n, -1);
+    chain_idx.assign(n, 0);
+    std::vector<int32_t> tail, len;
+    for (int32_t v : order) {
+      int32_t best = -1;
+      for (int32_t p : pred[v]) {
+        const int32_t c = chain_of[p];
+        if (tail[c] == p && (best < 0 || len[c] > len[best])) best = c;
+      }
+      if (best < 0) {
+        best = (int32_t)tail.size();
+        tail.push_back(v);
+        len.push_back(0);
+      }
+      chain_of[v] = best;
+      chain_idx[v] = len[best]++;
+      tail[best] = v;
+    }
+    std::vector<int32_t> ids(len.size());
+    std::iota(ids.begin(), ids.end(), 0);
+    std::stable_sort(ids.begin(), ids.end(), [&](int32_t a, int32_t b) { return len[a] > len[b]; });
+    const int32_t kmax = (int32_t)std::max<int64_t>(1, std::min<int64_t>(64, (int64_t{1} << 26) / n));
+    std::vector<int32_t> slot(len.size(), -1);
+    for (int32_t i = 0; i < (int32_t)ids.size() && K < kmax && len[ids[i]] >= 2; ++i) slot[ids[i]] = K++;
+    for (int32_t v = 0; v < n; ++v) chain_of[v] = slot[chain_of[v]];  // -1: not indexed
+    if (K > 0) {
+      minidx.assign((size_t)n * K, INT32_MAX);
+      for (int32_t i = n - 1; i >= 0; --i) {
+        const int32_t v = order[i];
+        int32_t* mv = &minidx[(size_t)v * K];
+        for (int32_t x : succ[v]) {
+          const int32_t* mx = &minidx[(size_t)x * K];
+          for (int32_t c = 0; c < K; ++c) mv[c] = std::min(mv[c], mx[c]);
+        }
+        if (chain_of[v] >= 0) mv[chain_of[v]] = std::min(mv[chain_of[v]], chain_idx[v]);
+      }
+    }
+  }
+  auto reaches_idx = [&](int32_t a, int32_t b) -> int {  // 1 yes, 0 no, -1 unknown
+    if (K == 0 || chain_of[b] < 0) return -1;
+    return minidx[(size_t)a * K + chain_of[b]] <= chain_idx[b] && a != b ? 1 : 0;
+  };
   auto reaches = [&](int32_t a, int32_t b) -> bool {
     if (exact) return (reach[(size_t)a * words + (b >> 6)] >> (b & 63)) & 1;
-    // 2-hop: a -> b directly or a -> x -> b
+    if (a == b) return false;
+    const int r = reaches_idx(a, b);
+    if (r >= 0) return r == 1;
     if (std::binary_search(succ[a].begin(), succ[a].end(), b)) return true;
-    for (int32_t x : succ[a])
+    for (int32_t p : pred[b]) {  // a reaches b iff a reaches (or is) one of b's producers
+      if (p == a) return true;
+      if (reaches_idx(a, p) == 1) return true;
+    }
+    for (int32_t x : succ[a])  // 2-hop
       if (std::binary_search(succ[x].begin(), succ[x].end(), b)) return true;
     return false;
   };
@@ -107,8 +172,7 @@ void prepare_scoring(int32_t n, int32_t E, const int32_t* src, const int64_t* si
       if (acyclic && u != w) {
         for (int32_t x : succ[u]) {
           if (x == w) continue;
-          if (exact ? reaches(x, w)
-                    : std::binary_search(succ[x].begin(), succ[x].end(), w)) {
+          if (reaches(x, w)) {
             redundant = true;
             break;
           }

@@ -856,3 +856,20 @@ def parts_plan_info(graph: Graph, max_chunks: int = 0, smem_budget: int = 232448
     keys = ("parts", "slots_per_part", "stash_slots", "cross_pairs", "cross_multi_consumer",
             "smem_bytes", "tiny4")
     return {k: int(v) for k, v in zip(keys, info)}
+
+
+def prep_info(graph: Graph, with_pairs: bool = False):
+    """Host-only: the scorer's derived tables for `graph` (mp_prep_host; no device):
+    reduced validity pairs, order-dependent frees, which reachability was used.
+    With with_pairs, also the reduced pairs as an int32 [m, 2] array (u before w)."""
+    info = np.zeros(6, np.int64)
+    csr = graph.mp_csr()
+    _native.check(_native.lib().mp_prep_host(C.byref(csr), info.ctypes.data, None, 0))
+    keys = ("reduced_pairs", "multi_consumer", "exact_reach", "tiny4", "tiny8", "narrow")
+    out = {k: int(v) for k, v in zip(keys, info)}
+    if with_pairs:
+        pairs = np.zeros((max(out["reduced_pairs"], 1), 2), np.int32)
+        _native.check(_native.lib().mp_prep_host(C.byref(csr), info.ctypes.data,
+                                                 pairs.ctypes.data, out["reduced_pairs"]))
+        return out, pairs[:out["reduced_pairs"]]
+    return out

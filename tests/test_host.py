@@ -121,3 +121,50 @@ def test_node_partitioned_plan_c5_host():
     assert 2 <= info["parts"] <= 6 and info["smem_bytes"] <= 232448
     assert info["stash_slots"] == info["cross_pairs"] + info["cross_multi_consumer"]
     assert mp.planner.parts_plan_info(mp.generate_graph("fork_join", 3000, 8, 1))["parts"] == 0
+
+
+def _random_dag(n, E, seed, max_sinks=4):
+    rng = np.random.default_rng(seed)
+    src, off, sinks, size = [], [0], [], []
+    for _ in range(E):
+        u = int(rng.integers(0, n - 1))
+        k = int(rng.integers(0, max_sinks + 1))
+        s = sorted(set(int(x) for x in rng.integers(u + 1, min(n, u + 1 + 40), size=k)))
+        src.append(u)
+        sinks.extend(s)
+        off.append(len(sinks))
+        size.append(int(rng.integers(1, 5)) * 16)
+    return mp.Graph.from_csr(n, src, off, sinks, size)
+
+
+def test_prep_chain_index_reduction_is_sound(monkeypatch):
+    """Above the bitset limit the validity pairs are reduced with a chain index
+    (mp_prep.cpp). Forced onto small graphs it must keep every pair the exact
+    transitive reduction keeps (it may only drop implied pairs), and on the
+    ladder-shaped training graphs it finds the exact reduction: n - 1 pairs and
+    the same order-dependent frees as the exact closure."""
+    graphs = [mp.generate_graph("training_like", 300, 8), mp.generate_graph("fork_join", 120, 8, 3),
+              mp.generate_graph("chain", 50, 8), _random_dag(600, 900, 1), _random_dag(400, 1200, 2)]
+    for i, g in enumerate(graphs):
+        monkeypatch.delenv("MP_PREP_EXACT_MAX", raising=False)
+        ex, pe = mp.planner.prep_info(g, with_pairs=True)
+        monkeypatch.setenv("MP_PREP_EXACT_MAX", "0")
+        ch, pc = mp.planner.prep_info(g, with_pairs=True)
+        assert ex["exact_reach"] == 1 and ch["exact_reach"] == 0
+        se, sc = set(map(tuple, pe.tolist())), set(map(tuple, pc.tolist()))
+        allp = {(int(g.edge_src[e]), int(s)) for e in range(g.E)
+                for s in g.sinks[g.sink_off[e]:g.sink_off[e + 1]]}
+        assert se <= sc <= allp, i
+        assert ex["multi_consumer"] <= ch["multi_consumer"]
+        if i == 0:   # training_like: the chain index is exact
+            assert sc == se and len(sc) == g.n - 1
+            assert ch["multi_consumer"] == ex["multi_consumer"] == 300
+
+
+def test_prep_c5_reduction():
+    """The 100k-tensor graph (n > the bitset limit): n - 1 reduced validity pairs
+    (was 200,001 with the 2-hop rule) and one order-dependent free per layer."""
+    g = mp.generate_graph("training_like", 33333, 8)
+    info = mp.planner.prep_info(g)
+    assert info["exact_reach"] == 0 and info["tiny4"] == 1
+    assert info["reduced_pairs"] == g.n - 1 and info["multi_consumer"] == 33333
