@@ -756,8 +756,11 @@ mp_status run_parts(const mp_graph* g, const int32_t* d_orders, int64_t C, uint6
   const auto& Q = g->parts;
   const bool vec = g->n % 4 == 0;
   if (o24 && !vec) return MP_E_INVALID_ARG;
-  auto kern = o24 ? score_parts_kernel<true, true>
-                  : vec ? score_parts_kernel<true> : score_parts_kernel<false>;
+  // deferred positions (one stream of the order) unless MP_PARTS_NO_DEFER
+  const bool defer = vec && Q.P >= 2 && Q.P <= 7 && Q.seg <= 8192 && !std::getenv("MP_PARTS_NO_DEFER");
+  auto kern = o24 ? (defer ? score_parts_kernel<true, true, true> : score_parts_kernel<true, true>)
+              : vec ? (defer ? score_parts_kernel<true, false, true> : score_parts_kernel<true>)
+                    : score_parts_kernel<false>;
   MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q.smem));
   int64_t grid = g->ctx->num_sms;
   if (const char* e = std::getenv("MP_SCORE_GRID")) {
@@ -766,7 +769,9 @@ mp_status run_parts(const mp_graph* g, const int32_t* d_orders, int64_t C, uint6
   }
   if (grid > C) grid = C;
   if (grid < 1) return MP_OK;
-  const size_t gstride = ((size_t)32 * Q.seg + 255) & ~size_t(255);
+  // per CTA: XF (1 byte per position) then, when deferring, 32 warp lists of seg words
+  const size_t xf_bytes = ((size_t)32 * Q.seg + 255) & ~size_t(255);
+  const size_t gstride = xf_bytes + (defer ? (size_t)32 * Q.seg * 4 : 0);
   MP_TRY(g->ctx->scratch[3].reserve(gstride * (size_t)grid));
   PartArgs A;
   A.P = Q.P;
@@ -790,7 +795,7 @@ mp_status run_parts(const mp_graph* g, const int32_t* d_orders, int64_t C, uint6
   kern<<<(unsigned)grid, kPartsThreads, Q.smem, st>>>(
       A, g->n, d_orders, C, d_peak, d_step, d_valid,
       reinterpret_cast<unsigned long long*>(d_key), index_base, g->scale,
-      static_cast<uint8_t*>(g->ctx->scratch[3].ptr), gstride);
+      static_cast<uint8_t*>(g->ctx->scratch[3].ptr), gstride, xf_bytes);
   MP_CUDA(cudaGetLastError());
   return MP_OK;
 }

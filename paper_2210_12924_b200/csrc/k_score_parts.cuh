@@ -77,13 +77,18 @@ __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
 
 // k24: orders arrive as 24-bit ids (3 bytes per position, host-packed for the
 // PCIe leg of the host-buffer call; n % 4 == 0, out-of-range ids as 0xffffff).
-template <bool kVec, bool k24 = false>
+// kDefer: the order is streamed ONCE. Pass 0 keeps part 0's positions and
+// appends every other in-range position to the warp's deferred list in global
+// scratch (L2-resident), one word {local slot, position - segment start, part};
+// pass b >= 1 reads the warp's own list instead of the order and the chunk table
+// (needs P <= 7 - part 7 marks nothing - and a warp segment of at most 8192 positions).
+template <bool kVec, bool k24 = false, bool kDefer = false>
 __global__ void __launch_bounds__(kPartsThreads, 1)
     score_parts_kernel(PartArgs A, int32_t n, const int32_t* __restrict__ orders, int64_t C,
                        uint64_t* __restrict__ peak_out, int32_t* __restrict__ step_out,
                        uint8_t* __restrict__ valid_out, unsigned long long* __restrict__ best_key,
                        int64_t index_base, uint64_t scale, uint8_t* __restrict__ gxf,
-                       size_t gstride) {
+                       size_t gstride, size_t xf_bytes) {
   extern __shared__ __align__(16) char smem[];
   __shared__ uint32_t s_wsum[32];
   __shared__ uint32_t s_wbest[32];
@@ -105,6 +110,10 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
       opaque_u64(reinterpret_cast<uint64_t>(gxf + (size_t)blockIdx.x * gstride)));
   const int seg = A.seg;  // positions per warp segment, a multiple of 512
   const int wbeg = warp * seg;
+  uint32_t* dlist = reinterpret_cast<uint32_t*>(
+      opaque_u64(reinterpret_cast<uint64_t>(gxf + (size_t)blockIdx.x * gstride + xf_bytes))) +
+                    (size_t)warp * seg;  // this warp's deferred list (kDefer)
+  uint32_t dcnt = 0;                     // its length (warp-uniform)
 
   for (int i = tid; i <= A.nchunks; i += T) ctab_s[i] = __ldg(A.ctab + i);
   if (tid < A.P) s_desc[tid] = A.desc[tid];
@@ -116,21 +125,30 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
     // 24-bit rows: 3n bytes each = 3n/4 words (n % 4 == 0)
     const uint32_t* ord24 = reinterpret_cast<const uint32_t*>(orders) + c * (int64_t)(3 * (n >> 2));
     bool bad = false;
+    dcnt = 0;
     for (int i = tid; i < A.n_slot_init; i += T) stash[__ldg(A.slot_init + i)] = 0;
 
     for (int b = 0; b < A.P; ++b) {
       const PartDesc& D = s_desc[b];
       {  // slot words: this part's static scan input on top, "not written" below
-        const uint4* src = reinterpret_cast<const uint4*>(A.xtab + D.xtab_off);
+        // one xtab word -> four consecutive slot words per thread: 16-byte stores
+        // of consecutive lanes are contiguous (no bank conflicts)
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(A.xtab + D.xtab_off);
         uint4* dst = reinterpret_cast<uint4*>(slot);
-        for (int i = tid; i < (D.nloc >> 4); i += T) {
-          const uint4 q = __ldg(src + i);
-          const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-          for (int h = 0; h < 4; ++h)
-            dst[4 * i + h] = make_uint4((w[h] << 24) | kPos, ((w[h] << 16) & 0xff000000u) | kPos,
-                                        ((w[h] << 8) & 0xff000000u) | kPos,
-                                        (w[h] & 0xff000000u) | kPos);
+        // slots past the last node ([pad_lo, pad_hi), never written) start at position 0
+        // so the permutation check below needs no range test
+        const int plo = D.pad_lo, phi = D.pad_hi;
+        for (int i = tid; i < (D.nloc >> 2); i += T) {
+          const uint32_t w = __ldg(src + i);
+          uint4 o = make_uint4((w << 24) | kPos, ((w << 16) & 0xff000000u) | kPos,
+                               ((w << 8) & 0xff000000u) | kPos, (w & 0xff000000u) | kPos);
+          if (4 * i + 3 >= plo && 4 * i < phi) {
+            if (4 * i >= plo && 4 * i < phi) o.x &= 0xff000000u;
+            if (4 * i + 1 >= plo && 4 * i + 1 < phi) o.y &= 0xff000000u;
+            if (4 * i + 2 >= plo && 4 * i + 2 < phi) o.z &= 0xff000000u;
+            if (4 * i + 3 >= plo && 4 * i + 3 < phi) o.w &= 0xff000000u;
+          }
+          dst[i] = o;
         }
       }
       __syncthreads();
@@ -143,6 +161,31 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
       const bool last = b == A.P - 1;
       const uint32_t bsel = (uint32_t)b << 24;
       uint32_t vmax = 0;
+      if (kDefer && b > 0) {
+        // the warp's own deferred positions: 4 words per 16-byte load, part b's kept
+        for (uint32_t i0 = 4 * lane; i0 < dcnt; i0 += 4 * 128) {
+          uint4 q[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            q[u] = i0 + u * 128 < dcnt ? __ldcg(reinterpret_cast<const uint4*>(dlist + i0 + u * 128))
+                                       : make_uint4(~0u, ~0u, ~0u, ~0u);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t ev[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const uint32_t e = ev[h];
+              if ((e >> 29) == (uint32_t)b && i0 + u * 128 + h < dcnt) {
+                const uint32_t a = slot_a + 4u * (e & 0xffffu);
+                const uint32_t w = lds_u32(a);
+                const uint32_t k = (uint32_t)wbeg + ((e >> 16) & 0x1fffu);
+                sts_u32(a, (w & 0xff000000u) | k);
+                stg_u8(XF + k, w >> 24);
+              }
+            }
+          }
+        }
+      } else
       for (int r0 = wbeg + 4 * lane; r0 < wbeg + seg; r0 += kPartsU * 128) {
         uint32_t vq[4 * kPartsU];
 #pragma unroll
@@ -161,7 +204,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
             }
           } else if (kVec) {
             const int4* p4 = reinterpret_cast<const int4*>(ord + r);
-            q = r >= n ? make_int4(-1, -1, -1, -1) : last ? __ldcs(p4) : __ldg(p4);
+            q = r >= n ? make_int4(-1, -1, -1, -1) : (last || kDefer) ? __ldcs(p4) : __ldg(p4);
           } else {
             q.x = r < n ? __ldg(ord + r) : -1;
             q.y = r + 1 < n ? __ldg(ord + r + 1) : -1;
@@ -179,12 +222,38 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
           for (int j = 0; j < 4 * kPartsU; ++j)
             bad |= vq[j] >= (uint32_t)n && r0 + (j >> 2) * 128 + (j & 3) < n;
         }
-        // id -> local slot of part b, or ~0 (another part / out of range), in place
+        if (kDefer) {
+          // pass 0: part 0 now, parts 1.. appended to the deferred list. One word per
+          // position either way: {local, position - segment start, part}, ~0 out of range
 #pragma unroll
-        for (int j = 0; j < 4 * kPartsU; ++j) {
-          const uint32_t e = lds_u32(ctab_a + 4u * min(vq[j] >> kPartChunkBits, (uint32_t)A.nchunks));
-          vq[j] = (e ^ bsel) < (1u << 24) ? (e & kPos) + (vq[j] & ((1u << kPartChunkBits) - 1))
-                                          : 0xffffffffu;
+          for (int j = 0; j < 4 * kPartsU; ++j) {
+            const uint32_t e = lds_u32(ctab_a + 4u * min(vq[j] >> kPartChunkBits, (uint32_t)A.nchunks));
+            const uint32_t pt = e >> 24;  // 0xff: out of range
+            vq[j] = pt < (uint32_t)A.P
+                        ? ((e & kPos) + (vq[j] & ((1u << kPartChunkBits) - 1))) |
+                              ((uint32_t)(r0 - wbeg + (j >> 2) * 128 + (j & 3)) << 16) | pt << 29
+                        : 0xffffffffu;
+          }
+          // appended in (j, lane) order with ballot ranks: each store instruction
+          // writes one contiguous run of the list (coalesced)
+          const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+          for (int j = 0; j < 4 * kPartsU; ++j) {
+            const uint32_t w = vq[j];
+            const bool d = w != 0xffffffffu && (w >> 29) != 0;
+            const uint32_t bal = __ballot_sync(0xffffffffu, d);
+            if (d) __stcg(dlist + dcnt + __popc(bal & lt), w);
+            dcnt += __popc(bal);
+            vq[j] = w != 0xffffffffu && (w >> 29) == 0 ? w & 0xffffu : 0xffffffffu;
+          }
+        } else {
+          // id -> local slot of part b, or ~0 (another part / out of range), in place
+#pragma unroll
+          for (int j = 0; j < 4 * kPartsU; ++j) {
+            const uint32_t e = lds_u32(ctab_a + 4u * min(vq[j] >> kPartChunkBits, (uint32_t)A.nchunks));
+            vq[j] = (e ^ bsel) < (1u << 24) ? (e & kPos) + (vq[j] & ((1u << kPartChunkBits) - 1))
+                                            : 0xffffffffu;
+          }
         }
         uint8_t* xrow = XF + r0;
 #pragma unroll
@@ -208,7 +277,6 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
          // 4 x 16 bits per 8-byte load, one random slot read per node
         const uint4* sw = reinterpret_cast<const uint4*>(slot);
         const uint2* p1 = reinterpret_cast<const uint2*>(A.p1 + D.xtab_off);
-        const int plo = D.pad_lo, phi = D.pad_hi;
         for (int i = tid; i < (D.nloc >> 2); i += T) {
           const uint4 q = sw[i];
           const uint2 pp = __ldg(p1 + i);
@@ -216,8 +284,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
           const uint32_t pr[4] = {pp.x & 0xffffu, pp.x >> 16, pp.y & 0xffffu, pp.y >> 16};
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
-            const int l = 4 * i + h;
-            bad |= (w[h] & kPos) == kPos && (l < plo || l >= phi);
+            bad |= (w[h] & kPos) == kPos;
             if (pr[h] != 0xffffu) bad |= (slot[pr[h]] & kPos) >= (w[h] & kPos);
           }
         }
@@ -298,7 +365,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
     __syncthreads();
     uint32_t carry = warp_sum(lane < warp ? s_wsum[lane] : 0u);  // exclusive over warps
     uint32_t best = 0;
-    int best_i = INT_MAX;
+    int best_i = wbeg;  // (0, first position): an all-zero segment reports its first step
     for (int r00 = wbeg; r00 < wbeg + seg; r00 += 4 * 128) {  // seg is a 512-multiple
       uint32_t w4s[4];
 #pragma unroll
@@ -322,11 +389,11 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
         for (int q = 0; q < 4; ++q) {
           run += xs[q];
           const uint32_t rs = run + fs[q];
-          const int k = r + q;
-          if (k < n && (best_i == INT_MAX || rs > best)) {
-            best = rs;
-            best_i = k;
-          }
+          // padding positions (k >= n) carry RS <= RS(n-1): they never beat a real
+          // position (strict >, and the smaller index wins ties across lanes)
+          const bool better = rs > best;
+          best = better ? rs : best;
+          best_i = better ? r + q : best_i;
         }
         carry += __shfl_sync(0xffffffffu, incl, 31);
       }
