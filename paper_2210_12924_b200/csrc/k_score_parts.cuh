@@ -138,15 +138,17 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
         // slots past the last node ([pad_lo, pad_hi), never written) start at position 0
         // so the permutation check below needs no range test
         const int plo = D.pad_lo, phi = D.pad_hi;
+        const int qlo = plo >> 2, qhi = (phi + 3) >> 2;  // uint4 words touching the pad
         for (int i = tid; i < (D.nloc >> 2); i += T) {
           const uint32_t w = __ldg(src + i);
           uint4 o = make_uint4((w << 24) | kPos, ((w << 16) & 0xff000000u) | kPos,
                                ((w << 8) & 0xff000000u) | kPos, (w & 0xff000000u) | kPos);
-          if (4 * i + 3 >= plo && 4 * i < phi) {
-            if (4 * i >= plo && 4 * i < phi) o.x &= 0xff000000u;
-            if (4 * i + 1 >= plo && 4 * i + 1 < phi) o.y &= 0xff000000u;
-            if (4 * i + 2 >= plo && 4 * i + 2 < phi) o.z &= 0xff000000u;
-            if (4 * i + 3 >= plo && 4 * i + 3 < phi) o.w &= 0xff000000u;
+          if (i >= qlo && i < qhi) {
+            const int l = 4 * i;
+            if (l >= plo && l < phi) o.x &= 0xff000000u;
+            if (l + 1 >= plo && l + 1 < phi) o.y &= 0xff000000u;
+            if (l + 2 >= plo && l + 2 < phi) o.z &= 0xff000000u;
+            if (l + 3 >= plo && l + 3 < phi) o.w &= 0xff000000u;
           }
           dst[i] = o;
         }
@@ -277,15 +279,25 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
          // 4 x 16 bits per 8-byte load, one random slot read per node
         const uint4* sw = reinterpret_cast<const uint4*>(slot);
         const uint2* p1 = reinterpret_cast<const uint2*>(A.p1 + D.xtab_off);
-        for (int i = tid; i < (D.nloc >> 2); i += T) {
-          const uint4 q = sw[i];
-          const uint2 pp = __ldg(p1 + i);
-          const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-          const uint32_t pr[4] = {pp.x & 0xffffu, pp.x >> 16, pp.y & 0xffffu, pp.y >> 16};
+        const int nq = D.nloc >> 2;
+        for (int i0 = tid; i0 < nq; i0 += 4 * T) {  // four groups' loads in flight
+          uint2 pp[4];
 #pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            bad |= (w[h] & kPos) == kPos;
-            if (pr[h] != 0xffffu) bad |= (slot[pr[h]] & kPos) >= (w[h] & kPos);
+          for (int u = 0; u < 4; ++u)
+            pp[u] = i0 + u * T < nq ? __ldg(p1 + i0 + u * T) : make_uint2(~0u, ~0u);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * T;
+            if (i >= nq) break;
+            const uint4 q = sw[i];
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+            const uint32_t pr[4] = {pp[u].x & 0xffffu, pp[u].x >> 16, pp[u].y & 0xffffu,
+                                    pp[u].y >> 16};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              bad |= (w[h] & kPos) == kPos;
+              if (pr[h] != 0xffffu) bad |= (slot[pr[h]] & kPos) >= (w[h] & kPos);
+            }
           }
         }
       }
