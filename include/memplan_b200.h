@@ -205,8 +205,10 @@ mp_status mp_overlap_pairs(mp_ctx* ctx, int32_t num_edges, const int32_t* lo, co
                            int64_t cap, int64_t* count);
 /* Device variant over a row range [row_begin, row_end) (for sharding rows
  * across GPUs): d_row_off[row_end-row_begin+1] (int64) receives the
- * exclusive offsets (relative to the range), pairs are written when d_pairs
- * != NULL and the range total fits cap. */
+ * exclusive offsets (relative to the range). With d_pairs != NULL the count,
+ * scan and fill run back to back on the stream (one read-back of the total at
+ * the end): at most cap pairs are written, MP_E_CAPACITY when the total exceeds
+ * cap (*count still receives the total). */
 mp_status mp_overlap_pairs_d(mp_ctx* ctx, int32_t num_edges, const int32_t* d_lo,
                              const int32_t* d_hi, const uint64_t* d_size,
                              const uint8_t* d_pinned, int64_t row_begin, int64_t row_end,

@@ -15,6 +15,7 @@
 
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
 
 #include "mp_internal.h"
 
@@ -59,7 +60,7 @@ constexpr int kTileCols = 1024;
 template <int MODE, bool PINNED, bool FILL, int RPW>
 __global__ void __launch_bounds__(kThreads)
     pair_tile_kernel(int32_t E, PairRec R, int64_t row_begin, int64_t row_end,
-                     int64_t* __restrict__ row_off, int2* __restrict__ out) {
+                     int64_t* __restrict__ row_off, int2* __restrict__ out, int64_t cap) {
   __shared__ int2 slh[kTileCols];
   __shared__ ulonglong2 sas[MODE == 1 ? kTileCols : 1];
   __shared__ uint8_t spin[PINNED ? kTileCols : 1];
@@ -112,7 +113,10 @@ __global__ void __launch_bounds__(kThreads)
           if (MODE == 1) p = p && aa[t].x < bb.x + bb.y && bb.x < aa[t].x + aa[t].y;
           const unsigned m = __ballot_sync(0xffffffffu, p);
           if (FILL) {
-            if (p) out[acc[t] + __popc(m & lt_mask)] = make_int2(ri[t], j);
+            if (p) {
+              const int64_t o = acc[t] + __popc(m & lt_mask);
+              if (o < cap) out[o] = make_int2(ri[t], j);  // capacity: the first cap pairs
+            }
           }
           acc[t] += __popc(m);
         }
@@ -127,6 +131,123 @@ __global__ void __launch_bounds__(kThreads)
       if (i < row_end) row_off[i - row_begin + 1] = acc[t];
     }
   }
+}
+
+// ---- mode 0 count without the O(E^2) sweep ------------------------------------
+// For row i and a column tile lying entirely after i, the overlapping eligible j are
+//   #{lo_j <= hi_i} - #{hi_j < lo_i}
+// (hi_j < lo_i <= hi_i implies lo_j <= hi_i, so the second set is inside the first):
+// two binary searches in the tile's sorted lo and hi arrays (ineligible columns sort
+// to the end as INT_MAX and are never counted). Only the tile holding row i itself
+// is swept column by column (j > i). The per-row totals are identical to the
+// sweep's; the fill pass still walks every tile to emit the pairs in (i, j) order.
+constexpr int kSortT = 512;
+constexpr int32_t kSortedCountMinEdges = 8 * kTileCols;  // C2-C4 (<= 4,180 edges) sweep
+
+// One CTA per column tile: sorted lo / hi of the eligible columns (and, for pinned
+// mode, of the eligible UNPINNED columns), bitonic in shared memory.
+template <bool PINNED>
+__global__ void __launch_bounds__(kSortT)
+    tile_sort_kernel(int32_t E, PairRec R, int32_t* __restrict__ sorted) {
+  constexpr int NA = PINNED ? 4 : 2;
+  __shared__ int32_t s[NA][kTileCols];
+  const int t = blockIdx.x;
+  for (int q = threadIdx.x; q < kTileCols; q += kSortT) {
+    const int64_t j = (int64_t)t * kTileCols + q;
+    const int2 b = j < E ? R.lh[j] : make_int2(INT_MAX, INT_MIN);
+    const bool el = b.x <= b.y;
+    s[0][q] = el ? b.x : INT_MAX;
+    s[1][q] = el ? b.y : INT_MAX;
+    if (PINNED) {
+      const bool up = el && !(j < E && R.pin[j] != 0);
+      s[2][q] = up ? b.x : INT_MAX;
+      s[3][q] = up ? b.y : INT_MAX;
+    }
+  }
+  __syncthreads();
+  for (int k = 2; k <= kTileCols; k <<= 1)
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      for (int i = threadIdx.x; i < kTileCols; i += kSortT) {
+        const int ixj = i ^ jj;
+        if (ixj > i) {
+          const bool asc = (i & k) == 0;
+#pragma unroll
+          for (int a = 0; a < NA; ++a) {
+            const int x = s[a][i], y = s[a][ixj];
+            if ((x > y) == asc) {
+              s[a][i] = y;
+              s[a][ixj] = x;
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+  int32_t* out = sorted + (size_t)t * NA * kTileCols;
+  for (int a = 0; a < NA; ++a)
+    for (int q = threadIdx.x; q < kTileCols; q += kSortT) out[a * kTileCols + q] = s[a][q];
+}
+
+// entries <= x (LE) or < x (!LE) in a sorted 1024-entry shared array
+template <bool LE>
+__device__ __forceinline__ int rank_in(const int32_t* S, int x) {
+  int pos = 0;
+#pragma unroll
+  for (int step = kTileCols / 2; step > 0; step >>= 1)
+    if (LE ? S[pos + step - 1] <= x : S[pos + step - 1] < x) pos += step;
+  // the steps sum to 1023: a tile whose every entry qualifies ends at 1023
+  if (LE ? S[pos] <= x : S[pos] < x) ++pos;
+  return pos;
+}
+
+constexpr int kCountT = 256;
+
+template <bool PINNED>
+__global__ void __launch_bounds__(kCountT)
+    pair_count_sorted_kernel(int32_t E, PairRec R, const int32_t* __restrict__ sorted,
+                             int64_t row_begin, int64_t row_end, int64_t* __restrict__ row_off) {
+  constexpr int NA = PINNED ? 4 : 2;
+  __shared__ int32_t ss[NA][kTileCols];
+  __shared__ int2 slh[kTileCols];
+  __shared__ uint8_t spin[PINNED ? kTileCols : 1];
+  const int64_t b0 = row_begin + (int64_t)blockIdx.x * kCountT;
+  const int64_t r = b0 + threadIdx.x;
+  const bool in = r < row_end;
+  const int2 a = in ? R.lh[r] : make_int2(INT_MAX, INT_MIN);
+  const bool pin = PINNED && in && R.pin[r] != 0;
+  const bool el = a.x <= a.y;
+  const int tr = (int)(r / kTileCols);
+  const int64_t blast = min(row_end, b0 + kCountT) - 1;
+  const int ntiles = (E + kTileCols - 1) / kTileCols;
+  int64_t cnt = 0;
+  for (int t = (int)(b0 / kTileCols); t < ntiles; ++t) {
+    const bool diag = t <= (int)(blast / kTileCols);  // some row of this CTA lies in tile t
+    __syncthreads();
+    const int32_t* src = sorted + (size_t)t * NA * kTileCols;
+    for (int q = threadIdx.x; q < NA * kTileCols; q += kCountT) (&ss[0][0])[q] = __ldg(src + q);
+    if (diag)
+      for (int q = threadIdx.x; q < kTileCols; q += kCountT) {
+        const int64_t j = (int64_t)t * kTileCols + q;
+        slh[q] = j < E ? R.lh[j] : make_int2(INT_MAX, INT_MIN);
+        if (PINNED) spin[q] = j < E ? R.pin[j] : 0;
+      }
+    __syncthreads();
+    if (!el || !in) continue;
+    if (t > tr) {
+      const int32_t* SL = ss[pin ? 2 : 0];
+      const int32_t* SH = ss[pin ? 3 : 1];
+      cnt += rank_in<true>(SL, a.y) - rank_in<false>(SH, a.x);
+    } else if (t == tr) {
+      const int cols = (int)min((int64_t)kTileCols, (int64_t)E - (int64_t)t * kTileCols);
+      for (int q = (int)(r - (int64_t)t * kTileCols) + 1; q < cols; ++q) {
+        const int2 b = slh[q];
+        bool p = b.x <= a.y && a.x <= b.y;
+        if (PINNED) p = p && !(pin && spin[q] != 0);
+        cnt += p ? 1 : 0;
+      }
+    }
+  }
+  if (in) row_off[r - row_begin + 1] = cnt;
 }
 
 // In-place inclusive scan of row_off[1..rows] with row_off[0] = 0 (one CTA).
@@ -186,7 +307,7 @@ PairRec carve(const PairArgs& a, void* scratch) {
   PairRec R;
   R.lh = reinterpret_cast<int2*>(p);
   p += ((size_t)a.num_edges * sizeof(int2) + 255) & ~size_t(255);
-  R.as = reinterpret_cast<ulonglong2*>(p);
+  R.as = reinterpret_cast<ulonglong2*>(p);  // mode 1; the sorted tiles follow it
   R.pin = const_cast<uint8_t*>(a.mask);
   return R;
 }
@@ -203,32 +324,32 @@ mp_status pack(const PairArgs& a, const PairRec& R, cudaStream_t st) {
 
 template <int MODE, bool PINNED, bool FILL, int RPW>
 void launch_tile(const PairArgs& a, const PairRec& R, int64_t* row_off, int2* out,
-                 cudaStream_t st) {
+                 int64_t cap, cudaStream_t st) {
   const int64_t rows = a.row_end - a.row_begin;
   const int64_t per_block = (int64_t)kWarpsPerBlock * RPW;
   const unsigned grid = (unsigned)((rows + per_block - 1) / per_block);
   pair_tile_kernel<MODE, PINNED, FILL, RPW>
-      <<<grid, kThreads, 0, st>>>(a.num_edges, R, a.row_begin, a.row_end, row_off, out);
+      <<<grid, kThreads, 0, st>>>(a.num_edges, R, a.row_begin, a.row_end, row_off, out, cap);
 }
 
 template <bool FILL>
 mp_status sweep(const PairArgs& a, int num_sms, const PairRec& R, int64_t* row_off, int2* out,
-                cudaStream_t st) {
+                int64_t cap, cudaStream_t st) {
   const int64_t rows = a.row_end - a.row_begin;
   if (rows <= 0) return MP_OK;
   // 8 rows per warp once there are enough rows to fill the GPU twice over
   const bool big = rows >= (int64_t)num_sms * kWarpsPerBlock * 8 * 2;
   if (a.mode == 0) {
     if (a.mask) {
-      big ? launch_tile<0, true, FILL, 8>(a, R, row_off, out, st)
-          : launch_tile<0, true, FILL, 1>(a, R, row_off, out, st);
+      big ? launch_tile<0, true, FILL, 8>(a, R, row_off, out, cap, st)
+          : launch_tile<0, true, FILL, 1>(a, R, row_off, out, cap, st);
     } else {
-      big ? launch_tile<0, false, FILL, 8>(a, R, row_off, out, st)
-          : launch_tile<0, false, FILL, 1>(a, R, row_off, out, st);
+      big ? launch_tile<0, false, FILL, 8>(a, R, row_off, out, cap, st)
+          : launch_tile<0, false, FILL, 1>(a, R, row_off, out, cap, st);
     }
   } else {
-    big ? launch_tile<1, false, FILL, 8>(a, R, row_off, out, st)
-        : launch_tile<1, false, FILL, 1>(a, R, row_off, out, st);
+    big ? launch_tile<1, false, FILL, 8>(a, R, row_off, out, cap, st)
+        : launch_tile<1, false, FILL, 1>(a, R, row_off, out, cap, st);
   }
   MP_CUDA(cudaGetLastError());
   return MP_OK;
@@ -236,9 +357,16 @@ mp_status sweep(const PairArgs& a, int num_sms, const PairRec& R, int64_t* row_o
 
 }  // namespace
 
+// scratch: packed {lo,hi} | {addr,size} | mode-0 sorted tiles | 256 B (device total)
+size_t sorted_bytes(const PairArgs& a) {
+  if (a.mode != 0) return 0;
+  const size_t tiles = ((size_t)a.num_edges + kTileCols - 1) / kTileCols;
+  return tiles * (a.mask ? 4 : 2) * kTileCols * sizeof(int32_t);
+}
 size_t pairs_scratch_bytes(const PairArgs& a, int) {
   return (((size_t)a.num_edges * sizeof(int2) + 255) & ~size_t(255)) +
-         (size_t)a.num_edges * sizeof(ulonglong2) + 512;
+         (((size_t)a.num_edges * sizeof(ulonglong2) + 255) & ~size_t(255)) + sorted_bytes(a) +
+         512;
 }
 
 mp_status pairs_count(const PairArgs& a, int num_sms, void* scratch, int64_t* d_row_off,
@@ -246,21 +374,49 @@ mp_status pairs_count(const PairArgs& a, int num_sms, void* scratch, int64_t* d_
   PairRec R = carve(a, scratch);
   MP_TRY(pack(a, R, st));
   const int64_t rows = a.row_end - a.row_begin;
-  MP_TRY(sweep<false>(a, num_sms, R, d_row_off, nullptr, st));
-  int64_t* d_total = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(scratch) +
-                                                pairs_scratch_bytes(a, num_sms) - 256);
+  // per-row totals from sorted column tiles (no O(E^2) sweep) once there are enough
+  // tiles to amortise the sort and the serial in-tile count; small graphs sweep
+  const bool force_sorted = std::getenv("MP_PAIRS_SORTED") != nullptr;  // tests
+  if (a.mode == 0 && rows > 0 && (a.num_edges >= kSortedCountMinEdges || force_sorted)) {
+    int32_t* sorted = reinterpret_cast<int32_t*>(
+        reinterpret_cast<char*>(scratch) +
+        (((size_t)a.num_edges * sizeof(int2) + 255) & ~size_t(255)) +
+        (((size_t)a.num_edges * sizeof(ulonglong2) + 255) & ~size_t(255)));
+    const unsigned tiles = (unsigned)((a.num_edges + kTileCols - 1) / kTileCols);
+    const unsigned grid = (unsigned)((rows + kCountT - 1) / kCountT);
+    if (a.mask) {
+      tile_sort_kernel<true><<<tiles, kSortT, 0, st>>>(a.num_edges, R, sorted);
+      pair_count_sorted_kernel<true>
+          <<<grid, kCountT, 0, st>>>(a.num_edges, R, sorted, a.row_begin, a.row_end, d_row_off);
+    } else {
+      tile_sort_kernel<false><<<tiles, kSortT, 0, st>>>(a.num_edges, R, sorted);
+      pair_count_sorted_kernel<false>
+          <<<grid, kCountT, 0, st>>>(a.num_edges, R, sorted, a.row_begin, a.row_end, d_row_off);
+    }
+    MP_CUDA(cudaGetLastError());
+  } else {
+    MP_TRY(sweep<false>(a, num_sms, R, d_row_off, nullptr, 0, st));
+  }
+  int64_t* d_total = pairs_device_total(a, num_sms, scratch);
   offsets_scan_kernel<<<1, 1024, 0, st>>>(d_row_off, rows > 0 ? rows : 0, d_total);
   MP_CUDA(cudaGetLastError());
-  MP_CUDA(cudaMemcpyAsync(h_total, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  MP_CUDA(cudaStreamSynchronize(st));
+  if (h_total) {
+    MP_CUDA(cudaMemcpyAsync(h_total, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    MP_CUDA(cudaStreamSynchronize(st));
+  }
   return MP_OK;
 }
 
+int64_t* pairs_device_total(const PairArgs& a, int num_sms, void* scratch) {
+  return reinterpret_cast<int64_t*>(reinterpret_cast<char*>(scratch) +
+                                    pairs_scratch_bytes(a, num_sms) - 256);
+}
+
 mp_status pairs_fill(const PairArgs& a, int num_sms, void* scratch, const int64_t* d_row_off,
-                     int32_t* d_pairs, cudaStream_t st) {
+                     int32_t* d_pairs, cudaStream_t st, int64_t cap) {
   PairRec R = carve(a, scratch);  // packed by pairs_count
   return sweep<true>(a, num_sms, R, const_cast<int64_t*>(d_row_off),
-                     reinterpret_cast<int2*>(d_pairs), st);
+                     reinterpret_cast<int2*>(d_pairs), cap, st);
 }
 
 mp_status launch_peak_mem(int32_t E, const uint64_t* d_size, const uint8_t* d_has,

@@ -81,7 +81,9 @@ __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
 // appends every other in-range position to the warp's deferred list in global
 // scratch (L2-resident), one word {local slot, position - segment start, part};
 // pass b >= 1 reads the warp's own list instead of the order and the chunk table
-// (needs P <= 7 - part 7 marks nothing - and a warp segment of at most 8192 positions).
+// and keeps part b's words (needs P <= 7 - part 7 marks nothing - and a warp
+// segment of at most 8192 positions). Measured: one list read by every later pass
+// beats one list per part (two ballots per position to append) at C5.
 template <bool kVec, bool k24 = false, bool kDefer = false>
 __global__ void __launch_bounds__(kPartsThreads, 1)
     score_parts_kernel(PartArgs A, int32_t n, const int32_t* __restrict__ orders, int64_t C,
@@ -139,8 +141,16 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
         // so the permutation check below needs no range test
         const int plo = D.pad_lo, phi = D.pad_hi;
         const int qlo = plo >> 2, qhi = (phi + 3) >> 2;  // uint4 words touching the pad
-        for (int i = tid; i < (D.nloc >> 2); i += T) {
-          const uint32_t w = __ldg(src + i);
+        const int nq = D.nloc >> 2;
+        for (int i0 = tid; i0 < nq; i0 += 4 * T) {
+          uint32_t ws[4];  // four words' loads in flight
+#pragma unroll
+          for (int u = 0; u < 4; ++u) ws[u] = i0 + u * T < nq ? __ldg(src + i0 + u * T) : 0u;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * T;
+          if (i >= nq) break;
+          const uint32_t w = ws[u];
           uint4 o = make_uint4((w << 24) | kPos, ((w << 16) & 0xff000000u) | kPos,
                                ((w << 8) & 0xff000000u) | kPos, (w & 0xff000000u) | kPos);
           if (i >= qlo && i < qhi) {
@@ -151,6 +161,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
             if (l + 3 >= plo && l + 3 < phi) o.w &= 0xff000000u;
           }
           dst[i] = o;
+          }
         }
       }
       __syncthreads();
@@ -325,12 +336,13 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
       });
       groups(A.xmax, D.xmax_off, D.xmax_n,
              [&](uint32_t e) { atomicMax(&stash[e >> 16], slot[e & 0xffffu] & kPos); });
-      for (int i = tid; i < D.dyn_n; i += 2 * T) {  // multi-consumer tensors inside the part
-        uint4 dd[2];
-        dd[0] = __ldg(A.dyn4 + D.dyn_off + i);
-        dd[1] = i + T < D.dyn_n ? __ldg(A.dyn4 + D.dyn_off + i + T) : make_uint4(0, 0, 0, 0);
+      for (int i = tid; i < D.dyn_n; i += 4 * T) {  // multi-consumer tensors inside the part
+        uint4 dd[4];  // four records' loads in flight
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < 4; ++u)
+          dd[u] = i + u * T < D.dyn_n ? __ldg(A.dyn4 + D.dyn_off + i + u * T) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
           const uint4 d = dd[u];
           if (d.z == 0) continue;  // padding (every real record frees >= 1 unit)
           const uint32_t l1 = d.x & 0xffffu, l2 = d.x >> 16, l3 = d.y & 0xffffu, l4 = d.y >> 16;

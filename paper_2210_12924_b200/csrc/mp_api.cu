@@ -911,15 +911,28 @@ static mp_status pair_sweep_d(mp_ctx* ctx, PairArgs a, int64_t* d_row_off, int32
     return invalid_arg("row range out of bounds");
   MP_TRY(ctx->scratch[2].reserve(pairs_scratch_bytes(a, ctx->num_sms)));
   int64_t total = 0;
-  MP_TRY(pairs_count(a, ctx->num_sms, ctx->scratch[2].ptr, d_row_off, &total, st));
+  if (!d_out || cap <= 0) {
+    MP_TRY(pairs_count(a, ctx->num_sms, ctx->scratch[2].ptr, d_row_off, &total, st));
+    *count = total;
+    if (d_out && total > 0) {
+      set_error("Capacity: " + std::to_string(total) + " pairs exceed the buffer of 0");
+      return MP_E_CAPACITY;
+    }
+    return MP_OK;
+  }
+  // count -> scan -> fill back to back (the fill writes at most `cap` pairs), one
+  // read-back of the total at the end
+  MP_TRY(pairs_count(a, ctx->num_sms, ctx->scratch[2].ptr, d_row_off, nullptr, st));
+  MP_TRY(pairs_fill(a, ctx->num_sms, ctx->scratch[2].ptr, d_row_off, d_out, st, cap));
+  MP_CUDA(cudaMemcpyAsync(&total, pairs_device_total(a, ctx->num_sms, ctx->scratch[2].ptr),
+                          sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  MP_CUDA(cudaStreamSynchronize(st));
   *count = total;
-  if (!d_out) return MP_OK;
   if (total > cap) {
     set_error("Capacity: " + std::to_string(total) + " pairs exceed the buffer of " +
-              std::to_string(cap));
+              std::to_string(cap) + " (the first " + std::to_string(cap) + " were written)");
     return MP_E_CAPACITY;
   }
-  if (total > 0) MP_TRY(pairs_fill(a, ctx->num_sms, ctx->scratch[2].ptr, d_row_off, d_out, st));
   return MP_OK;
 }
 

@@ -200,12 +200,15 @@ struct PairArgs {
   int64_t row_end = 0;
 };
 size_t pairs_scratch_bytes(const PairArgs& a, int num_sms);
-// Count pass + scan: d_row_off[rows+1]; total copied to *h_total (sync).
+// Count pass + scan: d_row_off[rows+1]; the total stays in device memory
+// (pairs_device_total) and is also copied to *h_total (sync) when h_total != NULL.
+// Mode 0 counts from sorted column tiles (no O(E^2) sweep), mode 1 sweeps.
 mp_status pairs_count(const PairArgs& a, int num_sms, void* d_scratch, int64_t* d_row_off,
                       int64_t* h_total, cudaStream_t st);
-// Fill pass using d_row_off from pairs_count.
+int64_t* pairs_device_total(const PairArgs& a, int num_sms, void* d_scratch);
+// Fill pass using d_row_off from pairs_count; writes only the first `cap` pairs.
 mp_status pairs_fill(const PairArgs& a, int num_sms, void* d_scratch, const int64_t* d_row_off,
-                     int32_t* d_pairs, cudaStream_t st);
+                     int32_t* d_pairs, cudaStream_t st, int64_t cap = INT64_MAX);
 // K5 placement (k_place.cu): preallocate_pyramid / greedy_pack / peak_mem per problem.
 constexpr int kPlaceMaxEntries = 8192;  // placed tensors per problem (shared memory)
 struct PlaceArgs {

@@ -781,3 +781,47 @@ def test_host_scoring_24bit_wire(planner, monkeypatch, pack24):
     assert (z[0].cpu().numpy().view(np.uint64) == res.peak).all()
     assert (z[1].cpu().numpy() == res.peak_step).all() and (z[2].cpu().numpy() == res.valid).all()
     assert res.valid[1:4].tolist() == [0, 0, 0]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,layers,size,seed,pinned", [
+    ("fork_join", 300, 50, 4, False), ("fork_join", 1200, 8, 2, True),
+    ("training_like", 900, 8, 0, False), ("training_like", 900, 8, 0, True)])
+def test_pairs_sorted_tile_count(planner, monkeypatch, kind, layers, size, seed, pinned):
+    """K2's count from sorted column tiles (used from 8,192 edges up, forced here with
+    MP_PAIRS_SORTED) gives the same per-row totals, hence the same pair list, as the
+    ballot sweep and the C restatement - full tiles, the diagonal tile, pinned rows,
+    row shards - and the single-sync device call writes the first `cap` pairs and
+    reports MP_E_CAPACITY when the total exceeds cap."""
+    import torch
+    g = mp.generate_graph(kind, layers, size, seed)
+    lo, hi = planner.lifetimes_from_order(g, mp.random_topo_orders(g, 1, seed=seed + 7)[0])
+    pin = None
+    if pinned:
+        rng = np.random.default_rng(seed)
+        pin = {int(e): 0 for e in rng.choice(g.E, size=g.E // 3, replace=False)}
+    monkeypatch.delenv("MP_PAIRS_SORTED", raising=False)
+    ref = planner.encode_address_pairs(g, lo, hi, pin)
+    monkeypatch.setenv("MP_PAIRS_SORTED", "1")
+    got = planner.encode_address_pairs(g, lo, hi, pin)
+    assert got.shape == ref.shape and (got == ref).all()
+    if pin is None:
+        assert (ref == O.overlap_pairs(lo, hi, g.edge_size)).all()
+        d = torch.device("cuda:0")
+        dlo, dhi = torch.from_numpy(lo).to(d), torch.from_numpy(hi).to(d)
+        dsz = torch.from_numpy(g.edge_size.view(np.int64)).to(d)
+        parts = []
+        bounds = [0, 5, 1100, g.E // 2 + 3, g.E]
+        for r0, r1 in zip(bounds[:-1], bounds[1:]):
+            off = torch.zeros(r1 - r0 + 1, dtype=torch.int64, device=d)
+            cnt = planner.overlap_pairs_d(g.E, dlo, dhi, dsz, None, r0, r1, off, None, 0)
+            out = torch.zeros((max(cnt, 1), 2), dtype=torch.int32, device=d)
+            assert planner.overlap_pairs_d(g.E, dlo, dhi, dsz, None, r0, r1, off, out, cnt) == cnt
+            parts.append(out[:cnt].cpu().numpy())
+        assert (np.concatenate(parts) == ref).all()
+        off = torch.zeros(g.E + 1, dtype=torch.int64, device=d)
+        cap = len(ref) // 2
+        out = torch.full((cap, 2), -1, dtype=torch.int32, device=d)
+        with pytest.raises(errors.Capacity):
+            planner.overlap_pairs_d(g.E, dlo, dhi, dsz, None, 0, g.E, off, out, cap)
+        assert (out.cpu().numpy() == ref[:cap]).all()
