@@ -110,8 +110,10 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
   const uint32_t ctab_a = opaque_u32((uint32_t)__cvta_generic_to_shared(ctab_s));
   uint8_t* XF = reinterpret_cast<uint8_t*>(
       opaque_u64(reinterpret_cast<uint64_t>(gxf + (size_t)blockIdx.x * gstride)));
-  const int seg = A.seg;  // positions per warp segment, a multiple of 512
+  const int seg = A.seg;  // positions per warp segment, a multiple of 128
   const int wbeg = warp * seg;
+  const int wend = wbeg + seg;   // loops run in 512-position steps and stop at wend
+  const int wlim = min(n, wend);  // this warp's real positions end here
   uint32_t* dlist = reinterpret_cast<uint32_t*>(
       opaque_u64(reinterpret_cast<uint64_t>(gxf + (size_t)blockIdx.x * gstride + xf_bytes))) +
                     (size_t)warp * seg;  // this warp's deferred list (kDefer)
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
           const int r = r0 + u * 128;
           int4 q;
           if (k24) {  // four 3-byte ids in three words (word index 3r/4)
-            if (r >= n) {
+            if (r >= wlim) {
               q = make_int4(-1, -1, -1, -1);
             } else {
               const uint32_t* w = ord24 + 3 * (r >> 2);
@@ -217,23 +219,23 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
             }
           } else if (kVec) {
             const int4* p4 = reinterpret_cast<const int4*>(ord + r);
-            q = r >= n ? make_int4(-1, -1, -1, -1) : (last || kDefer) ? __ldcs(p4) : __ldg(p4);
+            q = r >= wlim ? make_int4(-1, -1, -1, -1) : (last || kDefer) ? __ldcs(p4) : __ldg(p4);
           } else {
-            q.x = r < n ? __ldg(ord + r) : -1;
-            q.y = r + 1 < n ? __ldg(ord + r + 1) : -1;
-            q.z = r + 2 < n ? __ldg(ord + r + 2) : -1;
-            q.w = r + 3 < n ? __ldg(ord + r + 3) : -1;
+            q.x = r < wlim ? __ldg(ord + r) : -1;
+            q.y = r + 1 < wlim ? __ldg(ord + r + 1) : -1;
+            q.z = r + 2 < wlim ? __ldg(ord + r + 2) : -1;
+            q.w = r + 3 < wlim ? __ldg(ord + r + 3) : -1;
           }
           vq[4 * u] = (uint32_t)q.x, vq[4 * u + 1] = (uint32_t)q.y;
           vq[4 * u + 2] = (uint32_t)q.z, vq[4 * u + 3] = (uint32_t)q.w;
         }
-        if (r0 + (kPartsU - 1) * 128 + 3 < n) {
+        if (r0 + (kPartsU - 1) * 128 + 3 < wlim) {
 #pragma unroll
           for (int j = 0; j < 4 * kPartsU; ++j) vmax = max(vmax, vq[j]);
         } else {
 #pragma unroll
           for (int j = 0; j < 4 * kPartsU; ++j)
-            bad |= vq[j] >= (uint32_t)n && r0 + (j >> 2) * 128 + (j & 3) < n;
+            bad |= vq[j] >= (uint32_t)n && r0 + (j >> 2) * 128 + (j & 3) < wlim;
         }
         if (kDefer) {
           // pass 0: part 0 now, parts 1.. appended to the deferred list. One word per
@@ -378,8 +380,10 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
       for (int r00 = wbeg; r00 < wbeg + seg; r00 += 4 * 128) {
         uint32_t w4s[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          w4s[u] = __ldcg(reinterpret_cast<const unsigned int*>(XF + r00 + u * 128 + 4 * lane));
+        for (int u = 0; u < 4; ++u)  // the next warp's positions read as padding
+          w4s[u] = r00 + u * 128 < wend
+                       ? __ldcg(reinterpret_cast<const unsigned int*>(XF + r00 + u * 128 + 4 * lane))
+                       : 0x08080808u;
 #pragma unroll
         for (int u = 0; u < 4; ++u) tot += (((w4s[u] & 0x0f0f0f0fu) * 0x01010101u) >> 24) - 32u;
       }
@@ -390,11 +394,13 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
     uint32_t carry = warp_sum(lane < warp ? s_wsum[lane] : 0u);  // exclusive over warps
     uint32_t best = 0;
     int best_i = wbeg;  // (0, first position): an all-zero segment reports its first step
-    for (int r00 = wbeg; r00 < wbeg + seg; r00 += 4 * 128) {  // seg is a 512-multiple
+    for (int r00 = wbeg; r00 < wend; r00 += 4 * 128) {
       uint32_t w4s[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u)  // four loads in flight, then the dependent scan
-        w4s[u] = __ldcg(reinterpret_cast<const unsigned int*>(XF + r00 + u * 128 + 4 * lane));
+        w4s[u] = r00 + u * 128 < wend
+                     ? __ldcg(reinterpret_cast<const unsigned int*>(XF + r00 + u * 128 + 4 * lane))
+                     : 0x08080808u;  // the next warp's positions: padding (x 0, f 0)
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int r = r00 + u * 128 + 4 * lane;
