@@ -108,9 +108,10 @@ mp_status mp_parts_plan_host(const mp_csr* csr, int32_t max_chunks, int64_t smem
                              int64_t* info);
 
 /* Host-only (no device): the scorer's derived validity and free tables for a
- * graph (mp_prep.cpp, run by mp_graph_upload). info[6] = {reduced validity pairs,
+ * graph (mp_prep.cpp, run by mp_graph_upload). info[7] = {reduced validity pairs,
  * multi-consumer (order-dependent free) tensors, exact reachability (1) or the
- * chain index (0), tiny4, tiny8, narrow (32-bit sums)}. When pairs != NULL it
+ * chain index (0), tiny4, tiny8, narrow (32-bit sums), mid32 (32-bit per-node
+ * values, 64-bit sums)}. When pairs != NULL it
  * receives up to `cap` reduced pairs as (u, w) int32 couples: u must run before w. */
 mp_status mp_prep_host(const mp_csr* csr, int64_t* info, int32_t* pairs, int64_t cap);
 

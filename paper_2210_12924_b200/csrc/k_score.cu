@@ -695,11 +695,11 @@ mp_status run(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d
   return MP_OK;
 }
 
-template <typename VT, int J, int KC, typename OT>
+template <typename VT, int J, int KC, typename OT, typename AT = VT>
 mp_status run_reg_t(const mp_graph* g, const OT* d_orders, int64_t C, uint64_t* d_peak,
                     int32_t* d_step, uint8_t* d_valid, uint64_t* d_bytes, uint64_t* d_key,
                     int64_t index_base, cudaStream_t st) {
-  auto kern = score_reg_kernel<VT, J, KC, OT>;
+  auto kern = score_reg_kernel<VT, J, KC, OT, AT>;
   const int T = g->score_threads;
   const size_t smem = reg_smem_bytes<VT>(g->n, T, g->score_p, J, KC);
 
@@ -715,17 +715,17 @@ mp_status run_reg_t(const mp_graph* g, const OT* d_orders, int64_t C, uint64_t* 
   return MP_OK;
 }
 
-template <typename VT, int J, int KC>
+template <typename VT, int J, int KC, typename AT = VT>
 mp_status run_reg(const mp_graph* g, const int32_t* d_orders, int64_t C, uint64_t* d_peak,
                   int32_t* d_step, uint8_t* d_valid, uint64_t* d_bytes, uint64_t* d_key,
                   int64_t index_base, cudaStream_t st, bool o16) {
   if (o16 && KC == 1)  // 16-bit orders (host-packed): same kernel, half the order bytes
-    return run_reg_t<VT, J, KC, uint16_t>(g, reinterpret_cast<const uint16_t*>(d_orders), C,
-                                          d_peak, d_step, d_valid, d_bytes, d_key, index_base,
-                                          st);
+    return run_reg_t<VT, J, KC, uint16_t, AT>(g, reinterpret_cast<const uint16_t*>(d_orders), C,
+                                              d_peak, d_step, d_valid, d_bytes, d_key,
+                                              index_base, st);
   if (o16) return MP_E_INVALID_ARG;
-  return run_reg_t<VT, J, KC, int32_t>(g, d_orders, C, d_peak, d_step, d_valid, d_bytes, d_key,
-                                       index_base, st);
+  return run_reg_t<VT, J, KC, int32_t, AT>(g, d_orders, C, d_peak, d_step, d_valid, d_bytes,
+                                           d_key, index_base, st);
 }
 
 template <typename VT>
@@ -932,6 +932,28 @@ mp_status launch_score(const mp_graph* g, const int32_t* d_orders, int64_t C, ui
                        int32_t* d_step, uint8_t* d_valid, uint64_t* d_bytes, uint64_t* d_key,
                        int64_t index_base, cudaStream_t st, int ofmt) {
   if (C <= 0) return MP_OK;
+  // mid32 graphs (64-bit totals, 32-bit per-node values): the register-slot kernel with
+  // 32-bit scan inputs and 64-bit sums; per-step bytes and the other variants take the
+  // 64-bit path
+  if (g->mid32 && d_bytes == nullptr && g->score_warps == 0 && !g->use_parts &&
+      ofmt != kOrdU24) {
+    const bool o16 = ofmt == kOrdU16;
+    if (o16 && !score_takes_u16(g)) return MP_E_INVALID_ARG;
+    using U = unsigned long long;
+    switch (g->score_j) {
+      case 4:
+        if (g->score_kc == 2) return run_reg<uint32_t, 4, 2, U>(g, d_orders, C, d_peak, d_step, d_valid, d_bytes, d_key, index_base, st, o16);
+        return run_reg<uint32_t, 4, 1, U>(g, d_orders, C, d_peak, d_step, d_valid, d_bytes, d_key, index_base, st, o16);
+      case 8:
+        if (g->score_kc == 2) return run_reg<uint32_t, 8, 2, U>(g, d_orders, C, d_peak, d_step, d_valid, d_bytes, d_key, index_base, st, o16);
+        return run_reg<uint32_t, 8, 1, U>(g, d_orders, C, d_peak, d_step, d_valid, d_bytes, d_key, index_base, st, o16);
+      case 16:
+        if (g->score_kc == 2) return run_reg<uint32_t, 16, 2, U>(g, d_orders, C, d_peak, d_step, d_valid, d_bytes, d_key, index_base, st, o16);
+        return run_reg<uint32_t, 16, 1, U>(g, d_orders, C, d_peak, d_step, d_valid, d_bytes, d_key, index_base, st, o16);
+      default:
+        break;
+    }
+  }
   if (g->narrow)
     return dispatch<uint32_t>(g, d_orders, C, d_peak, d_step, d_valid, d_bytes, d_key,
                               index_base, st, ofmt);

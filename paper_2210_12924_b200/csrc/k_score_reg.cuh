@@ -53,17 +53,25 @@ struct RegScratch {
   uint32_t bad[2];  // per-iteration-parity bitmask of invalid candidates
 };
 
+// x as a signed 64-bit value: 32-bit scan inputs are int32 bit patterns
+__device__ __forceinline__ long long sx64(uint32_t v) { return (long long)(int32_t)v; }
+__device__ __forceinline__ long long sx64(unsigned long long v) { return (long long)v; }
+
 // OT: the order element type - int32 (the reference's layout) or uint16 (the host
 // call packs orders of graphs with n < 65535 to halve the PCIe bytes; values
 // outside [0, n) arrive as 0xffff, still out of range).
-template <typename VT, int J, int KC, typename OT = int32_t>
+// AT: the sum type. AT = VT, or VT = uint32 with AT = uint64 ("mid32" graphs:
+// total bytes past 2^32 in gcd units, but every node's x fits int32 and f uint32
+// for any order) - half the registers and shared bytes of the 64-bit variant,
+// exact 64-bit sums in the one-pass scan (peak/step only; no per-step bytes).
+template <typename VT, int J, int KC, typename OT = int32_t, typename AT = VT>
 __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMinBlocks)
     score_reg_kernel(ScoreTables G, const OT* __restrict__ orders, int64_t C,
                      uint64_t* __restrict__ peak_out, int32_t* __restrict__ step_out,
                      uint8_t* __restrict__ valid_out, uint64_t* __restrict__ bytes_out,
                      unsigned long long* __restrict__ best_key, int64_t index_base) {
   extern __shared__ __align__(16) char smem[];
-  __shared__ RegScratch<VT, KC> bs;
+  __shared__ RegScratch<AT, KC> bs;
 
   const int n = G.n;
   const int T = blockDim.x;
@@ -239,8 +247,8 @@ __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMi
     const uint32_t badmask = bs.bad[parity];
     const int64_t c0 = g * KC;
 
-    if constexpr (sizeof(VT) == 8) {
-      if (bytes_out == nullptr) {
+    if constexpr (sizeof(AT) == 8) {
+      if (bytes_out == nullptr || sizeof(VT) != sizeof(AT)) {  // the mid variant: never bytes
         // ---- phase 3, 64-bit values: ONE pass over the chunk [p0, p0 + P) -----------
         // x = alloc - free is exact as int64 (|x| <= total < 2^62), so chunk-relative
         // RS values are exact: each thread finds its chunk's first maximum relative to
@@ -251,13 +259,13 @@ __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMi
         for (int k = 0; k < KC; ++k) {
           const XFPair<VT>* mine = XF[k] + p0;
           XFPair<VT> xf = mine[0];
-          long long l = (long long)xf.x;
-          long long lb = l + (long long)xf.f;
+          long long l = sx64(xf.x);
+          long long lb = l + (long long)(AT)xf.f;
           int li = 0;
           for (int i = 1; i < P; ++i) {
             xf = mine[i];
-            l += (long long)xf.x;
-            const long long rs = l + (long long)xf.f;
+            l += sx64(xf.x);
+            const long long rs = l + (long long)(AT)xf.f;
             const bool better = rs > lb;
             lb = better ? rs : lb;
             li = better ? i : li;
@@ -267,10 +275,10 @@ __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMi
           int ci = p0 < n ? p0 + li : INT_MAX;  // a chunk made only of padding
           warp_argmax(cand, ci);
           if (lane == 0) {
-            bs.wbest[k][warp] = (VT)cand;
+            bs.wbest[k][warp] = (AT)cand;
             bs.widx[k][warp] = ci;
           }
-          if (lane == kWarp - 1) bs.wsum[k][warp] = (VT)incl;
+          if (lane == kWarp - 1) bs.wsum[k][warp] = (AT)incl;
         }
         __syncthreads();
         if (tid == 0) bs.bad[parity ^ 1] = 0;  // next iteration's flags

@@ -267,6 +267,7 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
     g->dyn_max_sinks = std::max(g->dyn_max_sinks, P.dyn_off[d + 1] - P.dyn_off[d]);
   g->scale = P.scale;
   g->narrow = P.narrow;
+  g->mid32 = P.mid32 && !std::getenv("MP_SCORE_NO_MID");
   g->tiny8 = P.tiny8;
   g->tiny4 = P.tiny4;
   g->exact_reach = P.exact_reach;
@@ -391,6 +392,7 @@ mp_status mp_prep_host(const mp_csr* csr, int64_t* info, int32_t* pairs, int64_t
   info[3] = P.tiny4 ? 1 : 0;
   info[4] = P.tiny8 ? 1 : 0;
   info[5] = P.narrow ? 1 : 0;
+  info[6] = P.mid32 ? 1 : 0;
   if (pairs) {
     int64_t k = 0;
     for (int32_t w = 0; w < P.n && k < cap; ++w)

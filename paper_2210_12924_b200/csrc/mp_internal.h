@@ -99,6 +99,7 @@ struct mp_graph {
   int32_t dyn_max_sinks = 0;         // most candidate last consumers of one dynamic edge
   uint64_t scale = 1;
   bool narrow = true;
+  bool mid32 = false;                // 32-bit scan inputs, 64-bit sums (mp_prep.h)
   bool tiny8 = false;                // per-position (x, f) fit a byte each (mp_prep.h)
   bool tiny4 = false;                // ... fit 4 bits each
   bool exact_reach = false;

@@ -251,6 +251,13 @@ void prepare_scoring(int32_t n, int32_t E, const int32_t* src, const int64_t* si
     }
     P->tiny8 = ok;
     P->tiny4 = ok && ok4;
+    bool m = !P->narrow;
+    for (int32_t v = 0; v < n && m; ++v) {
+      const int64_t xmax = (int64_t)alloc[v] - (int64_t)sfree[v];
+      m = xmin[v] >= INT32_MIN && xmax <= INT32_MAX && fmax[v] <= (int64_t)UINT32_MAX &&
+          alloc[v] <= (uint64_t)INT64_MAX / 2;
+    }
+    P->mid32 = m;
   }
   // second producer per node; the rest (3rd+) as a flat packed list
   P->pred2.assign(n, -1);

@@ -14,6 +14,9 @@ struct ScorePrep {
   bool narrow = true;           // total scaled bytes < 2^32: 32-bit arithmetic
   bool tiny8 = false;           // every node's x in [-128, 127] and f <= 255 for any order
   bool tiny4 = false;           // ... x in [-8, 7] and f <= 15
+  bool mid32 = false;           // not narrow, but every node's x fits int32 and f (with the
+                                // order-dependent frees) uint32 for any order: 32-bit
+                                // scan inputs, 64-bit sums
   uint64_t scale = 1;           // gcd of data sizes
   // node tables (scaled): x = alloc - static free, f = static free
   std::vector<uint64_t> node_x, node_f;

@@ -862,10 +862,11 @@ def prep_info(graph: Graph, with_pairs: bool = False):
     """Host-only: the scorer's derived tables for `graph` (mp_prep_host; no device):
     reduced validity pairs, order-dependent frees, which reachability was used.
     With with_pairs, also the reduced pairs as an int32 [m, 2] array (u before w)."""
-    info = np.zeros(6, np.int64)
+    info = np.zeros(7, np.int64)
     csr = graph.mp_csr()
     _native.check(_native.lib().mp_prep_host(C.byref(csr), info.ctypes.data, None, 0))
-    keys = ("reduced_pairs", "multi_consumer", "exact_reach", "tiny4", "tiny8", "narrow")
+    keys = ("reduced_pairs", "multi_consumer", "exact_reach", "tiny4", "tiny8", "narrow",
+            "mid32")
     out = {k: int(v) for k, v in zip(keys, info)}
     if with_pairs:
         pairs = np.zeros((max(out["reduced_pairs"], 1), 2), np.int32)

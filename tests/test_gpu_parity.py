@@ -825,3 +825,48 @@ def test_pairs_sorted_tile_count(planner, monkeypatch, kind, layers, size, seed,
         with pytest.raises(errors.Capacity):
             planner.overlap_pairs_d(g.E, dlo, dhi, dsz, None, 0, g.E, off, out, cap)
         assert (out.cpu().numpy() == ref[:cap]).all()
+
+
+@pytest.mark.parametrize("name", ["gpt2_medium_s1024", "random_dag_wide"])
+def test_mid32_scorer_matches_64bit(planner, monkeypatch, name):
+    """Graphs whose totals pass 2^32 gcd units while every node's x fits int32 and
+    f uint32 (C4) are scored with 32-bit scan inputs and 64-bit sums; the results
+    equal the 64-bit kernel's (MP_SCORE_NO_MID) and the reference's, on the device
+    and the host (16-bit wire) paths."""
+    import gzip
+    import os
+    if name == "random_dag_wide":   # gcd 1, sizes up to 2^27: total past 2^32 units
+        rng = np.random.default_rng(5)
+        n, src, off, sinks, size = 900, [], [0], [], []
+        for u in range(n - 1):
+            for _ in range(int(rng.integers(1, 3))):
+                src.append(u)
+                sinks.extend(sorted(set(int(x) for x in rng.integers(u + 1, min(n, u + 30),
+                                                                      size=int(rng.integers(1, 4))))))
+                off.append(len(sinks))
+                size.append(int(rng.integers(1, 1 << 27)))
+        g = mp.Graph.from_csr(n, src, off, sinks, size)
+        text = mp.save_graph(g)
+    else:
+        path = os.path.join(os.path.dirname(__file__), "..", "workloads", "graphs",
+                            name + ".json.gz")
+        with gzip.open(path, "rt") as f:
+            text = f.read()
+        g = mp.load_graph(text)
+    info = mp.planner.prep_info(g)
+    assert info["narrow"] == 0 and info["mid32"] == 1
+    orders = mp.random_topo_orders(g, 300, seed=31)
+    orders[7, [1, 2]] = orders[7, [2, 1]]
+    monkeypatch.delenv("MP_SCORE_NO_MID", raising=False)
+    mid, best_mid = planner.score_orders_best(g, orders)
+    mid_d = planner.score_orders(g, orders)
+    monkeypatch.setenv("MP_SCORE_NO_MID", "1")
+    wide, best_wide = planner.score_orders_best(g, orders)
+    for a in (mid, mid_d):
+        assert (a.valid == wide.valid).all() and (a.peak == wide.peak).all()
+        assert (a.peak_step == wide.peak_step).all()
+    assert best_mid == best_wide
+    if O.ref_available():
+        rg = O.RefGraph.load(text)
+        rp, rv, rbest = rg.score_orders(orders, threads=os.cpu_count() or 1)
+        assert (mid.valid == rv).all() and (mid.peak == rp).all() and best_mid == rbest
