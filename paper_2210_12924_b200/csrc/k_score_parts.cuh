@@ -198,6 +198,10 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
                 stg_u8(XF + k, w >> 24);
               }
             }
+            // last reader: drop the consumed 128-byte lines from L2 without a write-back
+            if (last && (lane & 7) == 0 && i0 + u * 128 < dcnt)
+              asm volatile("discard.global.L2 [%0], 128;" ::"l"(dlist + ((i0 + u * 128) & ~31u))
+                           : "memory");
           }
         }
       } else
@@ -429,6 +433,10 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
       }
     }
     warp_argmax(best, best_i);
+    // XF is rewritten by the next candidate: drop this segment's lines from L2 without
+    // a write-back (not the line holding position n - its padding bytes persist)
+    for (int l0 = wbeg + 128 * lane; l0 + 128 <= min(wend, n & ~127); l0 += 128 * 32)
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(XF + l0) : "memory");
     if (lane == 0) {
       s_wbest[warp] = best;
       s_widx[warp] = best_i;
