@@ -178,8 +178,8 @@ def smem_pipe_use(config, kernel_ms, sm_mhz, num_sms):
         return None
 
 
-def pinned_h2d_gbs(dev, nbytes=256 * 2**20, reps=3):
-    """The PCIe roofline denominator: torch's pinned host->device copy rate on this box,
+def pinned_h2d_gbs(dev, nbytes=256 * 2**20, reps=10):
+    """The PCIe roofline denominator: the pinned host->device copy rate on this box,
     one 256 MiB copy timed with CUDA events (best of `reps`, after one warm-up)."""
     import torch
     src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
