@@ -28,15 +28,6 @@ struct RegLayout {
     return ((size_t)(T * P + 1) * sizeof(XFPair<VT>) + 15) & ~size_t(15);
   }
   __host__ __device__ size_t per_candidate() const { return pos_bytes() + xf_bytes(); }
-  // MP_REG_SMEM_NODES (tuning variant, 32-bit graphs): the slots' node records
-  // {x, f, pos index of producer 1, of producer 2} in shared memory, not registers
-  __host__ __device__ size_t node_bytes() const {
-#ifdef MP_REG_SMEM_NODES
-    return sizeof(VT) == 4 ? (size_t)T * J * 16 : 0;
-#else
-    return 0;
-#endif
-  }
 };
 
 // Register budgets (65536 / (kMaxT * kMinBlocks) per thread):
@@ -141,19 +132,6 @@ __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMi
   uint32_t has2 = 0;
 #pragma unroll
   for (int j = 0; j < J; ++j) has2 |= (__any_sync(0xffffffffu, ru2[j] != TJ + 1) ? 1u : 0u) << j;
-#ifdef MP_REG_SMEM_NODES
-  constexpr bool kSmemNodes = sizeof(VT) == 4 && KC == 1;
-  uint4* NT = reinterpret_cast<uint4*>(smem + KC * L.per_candidate());
-  if constexpr (kSmemNodes) {
-#pragma unroll
-    for (int j = 0; j < J; ++j)
-      NT[base + kWarp * j] = make_uint4((uint32_t)rx[j], (uint32_t)rf[j], (uint32_t)ru[j],
-                                        (uint32_t)ru2[j]);
-  }
-#else
-  constexpr bool kSmemNodes = false;
-  const uint4* NT = nullptr;
-#endif
 
   // Candidate groups: group g covers candidates [g*KC, g*KC + KC).
   const int64_t ngroups = (C + KC - 1) / KC;
@@ -202,27 +180,17 @@ __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMi
 #pragma unroll
     for (int k = 0; k < KC; ++k) {
       uint32_t w[J], pu[J], pu2[J];
-      uint4 nr[kSmemNodes ? J : 1];
 #pragma unroll
       for (int j = 0; j < J; ++j) {
         w[j] = pos[k][base + kWarp * j];
-        if constexpr (kSmemNodes) {
-          nr[j] = NT[base + kWarp * j];
-          pu[j] = pos[k][nr[j].z];
-          pu2[j] = (has2 >> j & 1u) ? pos[k][nr[j].w] : 0u;
-        } else {
-          pu[j] = pos[k][ru[j]];
-          pu2[j] = (has2 >> j & 1u) ? pos[k][ru2[j]] : 0u;
-        }
+        pu[j] = pos[k][ru[j]];
+        pu2[j] = (has2 >> j & 1u) ? pos[k][ru2[j]] : 0u;
       }
 #pragma unroll
       for (int j = 0; j < J; ++j) {
         // stale word (not a permutation) / a producer not strictly earlier
         bad |= ((w[j] < tag || pu[j] >= w[j] || pu2[j] >= w[j]) ? 1u : 0u) << k;
-        if constexpr (kSmemNodes)
-          XF[k][min((int)(w[j] & 0xffffu), TP)] = XFPair<VT>{(VT)nr[j].x, (VT)nr[j].y};
-        else
-          XF[k][min((int)(w[j] & 0xffffu), TP)] = XFPair<VT>{rx[j], rf[j]};
+        XF[k][min((int)(w[j] & 0xffffu), TP)] = XFPair<VT>{rx[j], rf[j]};
       }
     }
     // ---- phase 2b: 3rd+ reduced producer pairs (flat) ----------------------------------
@@ -464,6 +432,5 @@ __global__ void __launch_bounds__(RegBounds<J, KC>::kMaxT, RegBounds<J, KC>::kMi
 
 template <typename VT>
 size_t reg_smem_bytes(int n, int T, int P, int J, int KC) {
-  const RegLayout<VT> L{n, T, P, J};
-  return L.per_candidate() * KC + (KC == 1 ? L.node_bytes() : 0) + 16;
+  return RegLayout<VT>{n, T, P, J}.per_candidate() * KC + 16;
 }
