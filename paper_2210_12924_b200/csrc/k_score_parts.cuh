@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
               const uint32_t e = ev[h];
-              if ((e >> 29) == (uint32_t)b && i0 + u * 128 + h < dcnt) {
+              if ((e >> 29) == (uint32_t)b) {  // groups past the end read as ~0
                 const uint32_t a = slot_a + 4u * (e & 0xffffu);
                 const uint32_t w = lds_u32(a);
                 const uint32_t k = (uint32_t)wbeg + ((e >> 16) & 0x1fffu);
@@ -286,6 +286,9 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
         }
       }
       bad |= vmax >= (uint32_t)n;
+      // pad the deferred list to whole 16-byte groups with ~0 (part 7: no pass keeps
+      // it), so the readers test only the group, not every word, against the length
+      if (kDefer && b == 0 && lane < ((4u - (dcnt & 3u)) & 3u)) __stcg(dlist + dcnt + lane, ~0u);
       __syncthreads();
 
       // ---- resolve part b's lookups in shared memory ---------------------------------
