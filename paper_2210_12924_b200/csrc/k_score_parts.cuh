@@ -119,7 +119,12 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
                     (size_t)warp * seg;  // this warp's deferred list (kDefer)
   uint32_t dcnt = 0;                     // its length (warp-uniform)
 
-  for (int i = tid; i <= A.nchunks; i += T) ctab_s[i] = __ldg(A.ctab + i);
+  // kDefer keeps the chunk table pre-formatted as a deferred word: part << 29 | local base
+  // (parts past P - out-of-range ids - become part 7, which no pass keeps)
+  for (int i = tid; i <= A.nchunks; i += T) {
+    const uint32_t e = __ldg(A.ctab + i);
+    ctab_s[i] = !kDefer ? e : ((e >> 24) < (uint32_t)A.P ? (e >> 24) : 7u) << 29 | (e & 0xffffffu);
+  }
   if (tid < A.P) s_desc[tid] = A.desc[tid];
   for (int i = n + tid; i < 32 * seg; i += T) XF[i] = 8;  // scan padding: x = 0, f = 0
   __syncthreads();
@@ -244,26 +249,28 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
         if (kDefer) {
           // pass 0: part 0 now, parts 1.. appended to the deferred list. One word per
           // position either way: {local, position - segment start, part}, ~0 out of range
+          // the table word already is part << 29 | local base: add the id's offset in
+          // its chunk and the position's offset in the segment (no carries: local
+          // < 2^16, offset < 2^13)
+          const uint32_t k16 = (uint32_t)(r0 - wbeg) << 16;
 #pragma unroll
           for (int j = 0; j < 4 * kPartsU; ++j) {
             const uint32_t e = lds_u32(ctab_a + 4u * min(vq[j] >> kPartChunkBits, (uint32_t)A.nchunks));
-            const uint32_t pt = e >> 24;  // 0xff: out of range
-            vq[j] = pt < (uint32_t)A.P
-                        ? ((e & kPos) + (vq[j] & ((1u << kPartChunkBits) - 1))) |
-                              ((uint32_t)(r0 - wbeg + (j >> 2) * 128 + (j & 3)) << 16) | pt << 29
-                        : 0xffffffffu;
+            vq[j] = e + (vq[j] & ((1u << kPartChunkBits) - 1)) +
+                    (k16 + ((uint32_t)((j >> 2) * 128 + (j & 3)) << 16));
           }
           // appended in (j, lane) order with ballot ranks: each store instruction
           // writes one contiguous run of the list (coalesced)
           const uint32_t lt = (1u << lane) - 1u;
+          const uint32_t nd = (uint32_t)(A.P - 1) << 29;  // parts 1 .. P-1
 #pragma unroll
           for (int j = 0; j < 4 * kPartsU; ++j) {
             const uint32_t w = vq[j];
-            const bool d = w != 0xffffffffu && (w >> 29) != 0;
+            const bool d = w - (1u << 29) < nd;
             const uint32_t bal = __ballot_sync(0xffffffffu, d);
             if (d) __stcg(dlist + dcnt + __popc(bal & lt), w);
             dcnt += __popc(bal);
-            vq[j] = w != 0xffffffffu && (w >> 29) == 0 ? w & 0xffffu : 0xffffffffu;
+            vq[j] = w < (1u << 29) ? w & 0xffffu : 0xffffffffu;  // part 0: this pass
           }
         } else {
           // id -> local slot of part b, or ~0 (another part / out of range), in place
