@@ -93,6 +93,9 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
                        size_t gstride, size_t xf_bytes) {
   extern __shared__ __align__(16) char smem[];
   __shared__ uint32_t s_wsum[32];
+  __shared__ uint32_t s_dcnt[32];   // kDefer: each warp's deferred-list length
+  __shared__ uint32_t s_uoff[33];   // kDefer: exclusive prefix of 512-word units per list
+  __shared__ uint32_t s_next[kPartMaxParts];  // kDefer: next unit to take, per pass
   __shared__ uint32_t s_wbest[32];
   __shared__ int s_widx[32];
   __shared__ PartDesc s_desc[kPartMaxParts];  // read field by field where used (registers)
@@ -139,6 +142,13 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
 
     for (int b = 0; b < A.P; ++b) {
       const PartDesc& D = s_desc[b];
+      if (kDefer && b == 1 && warp == 0) {  // s_dcnt is a barrier old: units per list
+        const uint32_t units = (s_dcnt[lane] + 511u) >> 9;
+        const uint32_t incl = warp_incl_scan(units, lane);
+        s_uoff[lane] = incl - units;
+        if (lane == 31) s_uoff[32] = incl;
+        if (lane < kPartMaxParts) s_next[lane] = 0;
+      }
       {  // slot words: this part's static scan input on top, "not written" below
         // one xtab word -> four consecutive slot words per thread: 16-byte stores
         // of consecutive lanes are contiguous (no bank conflicts)
@@ -182,13 +192,25 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
       const uint32_t bsel = (uint32_t)b << 24;
       uint32_t vmax = 0;
       if (kDefer && b > 0) {
-        // the warp's own deferred positions: 4 words per 16-byte load, part b's kept
-        for (uint32_t i0 = 4 * lane; i0 < dcnt; i0 += 4 * 128) {
+        // the deferred positions of all warps in 512-word units taken from a shared
+        // counter (the warps finish together); 4 words per 16-byte load, part b's kept
+        const uint32_t total = s_uoff[32];
+        const uint32_t my_uoff = s_uoff[lane];
+        for (;;) {
+          uint32_t t = 0;
+          if (lane == 0) t = atomicAdd(&s_next[b], 1u);
+          t = __shfl_sync(0xffffffffu, t, 0);
+          if (t >= total) break;
+          const int ow = 31 - __clz(__ballot_sync(0xffffffffu, my_uoff <= t));  // the list's warp
+          const uint32_t cnt = s_dcnt[ow];
+          const uint32_t* dl = dlist + (ow - warp) * seg;  // that warp's list
+          const uint32_t obeg = (uint32_t)(ow * seg);
+          const uint32_t i0 = ((t - s_uoff[ow]) << 9) + 4 * lane;
           uint4 q[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            q[u] = i0 + u * 128 < dcnt ? __ldcg(reinterpret_cast<const uint4*>(dlist + i0 + u * 128))
-                                       : make_uint4(~0u, ~0u, ~0u, ~0u);
+            q[u] = i0 + u * 128 < cnt ? __ldcg(reinterpret_cast<const uint4*>(dl + i0 + u * 128))
+                                      : make_uint4(~0u, ~0u, ~0u, ~0u);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const uint32_t ev[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
@@ -198,14 +220,14 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
               if ((e >> 29) == (uint32_t)b) {  // groups past the end read as ~0
                 const uint32_t a = slot_a + 4u * (e & 0xffffu);
                 const uint32_t w = lds_u32(a);
-                const uint32_t k = (uint32_t)wbeg + ((e >> 16) & 0x1fffu);
+                const uint32_t k = obeg + ((e >> 16) & 0x1fffu);
                 sts_u32(a, (w & 0xff000000u) | k);
                 stg_u8(XF + k, w >> 24);
               }
             }
             // last reader: drop the consumed 128-byte lines from L2 without a write-back
-            if (last && (lane & 7) == 0 && i0 + u * 128 < dcnt)
-              asm volatile("discard.global.L2 [%0], 128;" ::"l"(dlist + ((i0 + u * 128) & ~31u))
+            if (last && (lane & 7) == 0 && i0 + u * 128 < cnt)
+              asm volatile("discard.global.L2 [%0], 128;" ::"l"(dl + ((i0 + u * 128) & ~31u))
                            : "memory");
           }
         }
@@ -296,6 +318,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
       // pad the deferred list to whole 16-byte groups with ~0 (part 7: no pass keeps
       // it), so the readers test only the group, not every word, against the length
       if (kDefer && b == 0 && lane < ((4u - (dcnt & 3u)) & 3u)) __stcg(dlist + dcnt + lane, ~0u);
+      if (kDefer && b == 0 && lane == 0) s_dcnt[warp] = dcnt;
       __syncthreads();
 
       // ---- resolve part b's lookups in shared memory ---------------------------------
