@@ -6,9 +6,9 @@
 // CTA streams the order row (coalesced int4 loads; pass 0 from HBM, the rest
 // from L2) and keeps only part b's nodes. One 32-bit shared word per local slot
 // holds the node's static scan input in its top byte ((x + 8) | f << 4, set at
-// the start of the pass) and its position in the low 24 bits (0xffffff = not
+// the start of the pass) and its 1-based position in the low 24 bits (0xffffff = not
 // written this pass):
-//     w = slot[local(v)]; slot[local(v)] = (w & 0xff000000) | k;  XF[k] = w >> 24
+//     w = slot[local(v)]; slot[local(v)] = (w & 0xff000000) | (k + 1);  XF[k] = w >> 24
 // Then every lookup of part b resolves in shared memory: the permutation check
 // (each local slot written this pass), the validity pairs inside the part, the
 // cross-part pairs through a stash slot written by the earlier part, and the
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
   constexpr int T = kPartsThreads;
   constexpr uint32_t kPos = 0xffffffu;  // position bits; all ones = not written this pass
   uint32_t* slot = reinterpret_cast<uint32_t*>(smem);
-  uint32_t* ctab_s = reinterpret_cast<uint32_t*>(smem + parts_al16((size_t)A.nb_max * 4));
+  uint32_t* ctab_s = reinterpret_cast<uint32_t*>(smem + parts_al16((size_t)(A.nb_max + 2) * 4));
   uint32_t* stash = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(ctab_s) +
                                                 parts_al16((size_t)(A.nchunks + 1) * 4));
   // kept in registers (opaque to the compiler, which would otherwise rematerialise
@@ -130,6 +130,12 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
   }
   if (tid < A.P) s_desc[tid] = A.desc[tid];
   for (int i = n + tid; i < 32 * seg; i += T) XF[i] = 8;  // scan padding: x = 0, f = 0
+  // sentinel slots (positions are 1-based): nb_max reads position 0 ("no producer",
+  // "no sink"), nb_max + 1 reads unwritten (the padding pair of the intra lists)
+  if (tid == 0) {
+    slot[A.nb_max] = 0;
+    slot[A.nb_max + 1] = kPos;
+  }
   __syncthreads();
 
   for (int64_t c = blockIdx.x; c < C; c += gridDim.x) {
@@ -154,7 +160,8 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
         // of consecutive lanes are contiguous (no bank conflicts)
         const uint32_t* src = reinterpret_cast<const uint32_t*>(A.xtab + D.xtab_off);
         uint4* dst = reinterpret_cast<uint4*>(slot);
-        // slots past the last node ([pad_lo, pad_hi), never written) start at position 0
+        // slots past the last node ([pad_lo, pad_hi), never written) start at position 1
+        // (written, and after the position-0 sentinel of "no producer")
         // so the permutation check below needs no range test
         const int plo = D.pad_lo, phi = D.pad_hi;
         const int qlo = plo >> 2, qhi = (phi + 3) >> 2;  // uint4 words touching the pad
@@ -172,10 +179,10 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
                                ((w << 8) & 0xff000000u) | kPos, (w & 0xff000000u) | kPos);
           if (i >= qlo && i < qhi) {
             const int l = 4 * i;
-            if (l >= plo && l < phi) o.x &= 0xff000000u;
-            if (l + 1 >= plo && l + 1 < phi) o.y &= 0xff000000u;
-            if (l + 2 >= plo && l + 2 < phi) o.z &= 0xff000000u;
-            if (l + 3 >= plo && l + 3 < phi) o.w &= 0xff000000u;
+            if (l >= plo && l < phi) o.x = (o.x & 0xff000000u) | 1u;
+            if (l + 1 >= plo && l + 1 < phi) o.y = (o.y & 0xff000000u) | 1u;
+            if (l + 2 >= plo && l + 2 < phi) o.z = (o.z & 0xff000000u) | 1u;
+            if (l + 3 >= plo && l + 3 < phi) o.w = (o.w & 0xff000000u) | 1u;
           }
           dst[i] = o;
           }
@@ -221,7 +228,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
                 const uint32_t a = slot_a + 4u * (e & 0xffffu);
                 const uint32_t w = lds_u32(a);
                 const uint32_t k = obeg + ((e >> 16) & 0x1fffu);
-                sts_u32(a, (w & 0xff000000u) | k);
+                sts_u32(a, (w & 0xff000000u) | (k + 1));  // 1-based
                 stg_u8(XF + k, w >> 24);
               }
             }
@@ -309,7 +316,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
           if (vq[j] != 0xffffffffu) {  // part b owns this position's node
             const uint32_t a = slot_a + 4u * vq[j];
             const uint32_t w = lds_u32(a);
-            sts_u32(a, (w & 0xff000000u) | (uint32_t)(r0 + (j >> 2) * 128 + (j & 3)));
+            sts_u32(a, (w & 0xff000000u) | (uint32_t)(r0 + (j >> 2) * 128 + (j & 3) + 1));  // 1-based
             stg_u8(xrow + (j >> 2) * 128 + (j & 3), w >> 24);
           }
         }
@@ -346,7 +353,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
               bad |= (w[h] & kPos) == kPos;
-              if (pr[h] != 0xffffu) bad |= (slot[pr[h]] & kPos) >= (w[h] & kPos);
+              bad |= (slot[pr[h]] & kPos) >= (w[h] & kPos);  // none: the position-0 sentinel
             }
           }
         }
@@ -363,9 +370,18 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
             if (es[h] != 0xffffffffu) fn(es[h]);
         }
       };
-      groups(A.intra, D.intra_off, D.intra_n, [&](uint32_t e) {
-        if ((slot[e & 0xffffu] & kPos) >= (slot[e >> 16] & kPos)) bad = true;  // producer later
-      });
+      {  // same-part validity pairs beyond p1, padded with the sentinel pair (no test)
+        const uint4* g4 = reinterpret_cast<const uint4*>(A.intra) + D.intra_off;
+        const uint32_t sp = (uint32_t)A.nb_max | (uint32_t)(A.nb_max + 1) << 16;
+        for (int i = tid; i < D.intra_n; i += 2 * T) {
+          const uint4 g0 = __ldg(g4 + i);
+          const uint4 g1 = i + T < D.intra_n ? __ldg(g4 + i + T) : make_uint4(sp, sp, sp, sp);
+          const uint32_t es[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+          for (int h = 0; h < 8; ++h)  // producer later
+            bad |= (slot[es[h] & 0xffffu] & kPos) >= (slot[es[h] >> 16] & kPos);
+        }
+      }
       groups(A.xput, D.xput_off, D.xput_n,
              [&](uint32_t e) { stash[e >> 16] = slot[e & 0xffffu] & kPos; });
       groups(A.xchk, D.xchk_off, D.xchk_n, [&](uint32_t e) {
@@ -385,20 +401,19 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
           const uint4 d = dd[u];
           if (d.z == 0) continue;  // padding (every real record frees >= 1 unit)
           const uint32_t l1 = d.x & 0xffffu, l2 = d.x >> 16, l3 = d.y & 0xffffu, l4 = d.y >> 16;
-          uint32_t h = slot[l1] & kPos;
-          if (l2 != 0xffffu) h = max(h, slot[l2] & kPos);
-          if (l3 != 0xffffu) h = max(h, slot[l3] & kPos);
-          if (l4 != 0xffffu) h = max(h, slot[l4] & kPos);
-          const int hi = (int)h;
-          if (hi < n) parts_free_at(XF, hi, d.z);
+          // missing sinks read the position-0 sentinel
+          const uint32_t h = max(max(slot[l1] & kPos, slot[l2] & kPos),
+                                 max(slot[l3] & kPos, slot[l4] & kPos));
+          const uint32_t hi = h - 1u;  // 1-based; unwritten (invalid orders) or 0 -> skipped
+          if (hi < (uint32_t)n) parts_free_at(XF, (int)hi, d.z);
         }
       }
       __syncthreads();  // slot words are rewritten by the next pass
     }
     for (int i = tid; i < A.n_xfree; i += T) {  // multi-consumer tensors spanning parts
       const uint2 f = __ldg(A.xfree + i);
-      const int hi = (int)stash[f.x];
-      if (hi < n) parts_free_at(XF, hi, f.y);
+      const uint32_t hi = stash[f.x] - 1u;  // 1-based positions
+      if (hi < (uint32_t)n) parts_free_at(XF, (int)hi, f.y);
     }
     if (__syncthreads_or(bad)) {
       if (tid == 0) {

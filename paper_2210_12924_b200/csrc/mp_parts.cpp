@@ -81,7 +81,7 @@ std::vector<int32_t> bfs_order(const std::vector<std::vector<std::pair<int32_t, 
 
 size_t parts_smem_bytes(const PartPlan& p) {
   auto al = [](size_t b) { return (b + 15) & ~size_t(15); };
-  return al((size_t)p.nb_max * 4) + al((size_t)(p.nchunks + 1) * 4) + al((size_t)p.nslots * 4) +
+  return al((size_t)(p.nb_max + 2) * 4) + al((size_t)(p.nchunks + 1) * 4) + al((size_t)p.nslots * 4) +
          kPartsMiscSmem;
 }
 
@@ -102,7 +102,8 @@ bool plan_parts(const ScorePrep& S, size_t smem_budget, int32_t max_chunks, Part
 
   for (int32_t P = 1; P <= kPartMaxParts; ++P) {
     const int32_t per = (nchunks + P - 1) / P;  // chunks per part (the last may have fewer)
-    if ((int64_t)per * kChunk > 65536) continue;  // 16-bit local indices in the lists
+    // 16-bit local indices in the lists, two sentinel slots past the table
+    if ((int64_t)per * kChunk > 65536 - kChunk) continue;
     if (per * kChunk % 16) continue;               // whole 16-byte groups of static bytes
     if (max_chunks > 0 && per > max_chunks) continue;
     PartPlan p;
@@ -143,13 +144,14 @@ bool plan_parts(const ScorePrep& S, size_t smem_budget, int32_t max_chunks, Part
     // one same-part producer per node is checked in node order beside the
     // permutation check (own slot read sequentially, one random read); the rest
     // go to the part's pair list, sorted by consumer so its reads run in order
-    p.p1.assign((size_t)p.P * p.nb_max, 0xffff);
+    const uint32_t s0 = (uint32_t)p.nb_max, s1 = s0 + 1;  // sentinel slots: position 0 / kPos
+    p.p1.assign((size_t)p.P * p.nb_max, (uint16_t)s0);
     int32_t slot = 0;
     for (const auto& [u, w] : pairs) {
       const int32_t a = pt(u), b = pt(w);
       if (a == b) {
         uint16_t& f = p.p1[(size_t)a * p.nb_max + loc(w)];
-        if (f == 0xffff) f = (uint16_t)loc(u);
+        if (f == (uint16_t)s0) f = (uint16_t)loc(u);
         else intra[a].push_back(loc(u) | loc(w) << 16);
         continue;
       }
@@ -168,7 +170,7 @@ bool plan_parts(const ScorePrep& S, size_t smem_budget, int32_t max_chunks, Part
       for (int32_t k = a + 1; k < b && same; ++k) same = pt(S.dyn_sinks[k]) == pt(S.dyn_sinks[a]);
       const uint32_t sz = (uint32_t)S.dyn_size[d];
       if (same) {
-        uint32_t l[4] = {0xffff, 0xffff, 0xffff, 0xffff};
+        uint32_t l[4] = {s0, s0, s0, s0};  // missing sinks read position 0
         for (int32_t k = a; k < b; ++k) l[k - a] = loc(S.dyn_sinks[k]);
         auto& L = dyn[pt(S.dyn_sinks[a])];
         L.push_back(l[0] | l[1] << 16);
@@ -211,6 +213,9 @@ bool plan_parts(const ScorePrep& S, size_t smem_budget, int32_t max_chunks, Part
         (void)unit;
       };
       put(p.intra, intra[b], &D.intra_off, &D.intra_n, 1);
+      // intra pairs are checked without a padding test: pad with (s0, s1), never "later"
+      for (size_t q = p.intra.size(); q > 0 && p.intra[q - 1] == 0xffffffffu; --q)
+        p.intra[q - 1] = s0 | s1 << 16;
       put(p.xput, xput[b], &D.xput_off, &D.xput_n, 1);
       put(p.xchk, xchk[b], &D.xchk_off, &D.xchk_n, 1);
       put(p.xmax, xmax[b], &D.xmax_off, &D.xmax_n, 1);

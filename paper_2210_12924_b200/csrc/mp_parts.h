@@ -27,18 +27,20 @@ constexpr int kPartMaxParts = 16;
 constexpr int32_t kPartsMinNodes = 16384;  // planned above this; used where smem variants do not fit
 
 // Per-part descriptor read by the kernel. List offsets and counts are in uint4
-// groups of four entries; padding entries are 0xffffffff (skipped).
+// groups of four entries; padding entries are 0xffffffff (skipped), except in the
+// intra list, padded with the sentinel pair (nb_max, nb_max + 1). Slots nb_max and
+// nb_max + 1 are sentinels holding position 0 and "unwritten" (positions are 1-based).
 struct PartDesc {
   int32_t nloc;       // local slots (64 per chunk)
   int32_t pad_lo;     // [pad_lo, pad_hi): local slots past the last node (never written)
   int32_t pad_hi;
   int32_t xtab_off;   // part-local static (x, f) bytes in the flat xtab; also the offset of
-                      // the part's first-producer table p1 (uint16 local slot, 0xffff none)
+                      // the part's first-producer table p1 (uint16 local slot, nb_max none)
   int32_t intra_off, intra_n;  // u32 lu | lw << 16: pos[lu] < pos[lw] (beyond p1), by lw
   int32_t xput_off, xput_n;    // u32 l | slot << 16: stash[slot] = pos[l]
   int32_t xchk_off, xchk_n;    // u32 l | slot << 16 | dir << 31: compare with stash[slot]
   int32_t xmax_off, xmax_n;    // u32 l | slot << 16: stash[slot] = max(stash[slot], pos[l])
-  int32_t dyn_off, dyn_n;      // uint4 {l1 | l2 << 16, l3 | l4 << 16, size, 0}, 0xffff = none
+  int32_t dyn_off, dyn_n;      // uint4 {l1 | l2 << 16, l3 | l4 << 16, size, 0}, nb_max = none
 };
 
 struct PartPlan {
