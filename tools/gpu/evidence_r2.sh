@@ -1,6 +1,6 @@
 # Round-2 evidence: smoke, GPU tests, bench lines (all modes), reference arm, launch list, ncu.
 # usage: bash tools/gpu/evidence_r2.sh   (outputs under gpurun_out/ev2/)
-O=gpurun_out/ev2; mkdir -p $O
+O=${EV:-gpurun_out/ev2}; mkdir -p $O
 nproc > $O/host.txt; lscpu | grep -i "model name" >> $O/host.txt; nvidia-smi -L >> $O/host.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
 timeout 1500 python -m pytest tests -q -m gpu > $O/gpu_tests.log 2>&1; tail -1 $O/gpu_tests.log
@@ -18,4 +18,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c2.csv python bench.py --config c2 --steps 20 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:score -s 5 -c 1 -o $O/ncu_c5_score python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:score -s 5 -c 1 -o $O/ncu_c2_score python bench.py --config c2 --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:score -s 5 -c 1 -o $O/ncu_c4_score python bench.py --config c4 --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:count_sorted -s 2 -c 1 -o $O/ncu_c5_pairs_count python bench.py --mode pairs --config c5 --steps 2 > /dev/null 2>&1
 ls -la $O
