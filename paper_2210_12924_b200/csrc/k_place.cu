@@ -28,7 +28,9 @@
 // order index), so up to kPlaceMaxEntries tensors per problem.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstdint>
 #include <type_traits>
 
@@ -319,6 +321,236 @@ __global__ void __launch_bounds__(kPT, 512 / kPT)
   }
 }
 
+// ---- warp per problem (many problems, E <= kPlaceWarpMaxEdges) -------------------
+// The same heuristics with the placed set kept IN ADDRESS ORDER as three arrays in
+// the warp's shared-memory slice (address, top, lifetime: 24 bytes per tensor), so
+// the search reads 32 consecutive tensors per step with no index indirection and no
+// bank conflicts, and no block barrier is ever needed:
+//   search   rounds of 32 tensors in address order; pm = max(0, tops of the
+//            lifetime-overlapping tensors before this one) is a carried value plus a
+//            warp exclusive prefix-max; the first overlapping tensor with
+//            addr - size >= pm leaves the gap at pm (ballot + ffs); if none, x = the
+//            final pm. Rounds stop at the gap.
+//   insert   the first index whose address is >= x (32-ary warp search), then the
+//            tail shifts right by one, 32 tensors per step from the end.
+// The CTA variant above keeps append-only slots and shifts a 4-byte index instead;
+// its indirect random reads made half its shared-memory wavefronts bank conflicts.
+// One warp per problem is latency-bound (a shuffle scan per 32 tensors): it wins
+// only where many problems fit an SM (C2: 1.68e5 vs 1.51e5 placements/s).
+constexpr int kPlaceWarpMaxEdges = 4096;
+
+__device__ __forceinline__ long long wmax_ll(long long v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const long long o = __shfl_xor_sync(0xffffffffu, v, d);
+    v = o > v ? o : v;
+  }
+  return v;
+}
+
+template <int W>
+__global__ void __launch_bounds__(32 * W) place_warp_kernel(PlaceArgs a, size_t slice) {
+  extern __shared__ __align__(16) char smem[];
+  const int E = a.num_edges;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cap = a.cap;
+  char* base_p = smem + (size_t)warp * slice;
+  unsigned long long* P_addr = reinterpret_cast<unsigned long long*>(base_p);
+  unsigned long long* P_top = P_addr + cap;
+  int2* P_life = reinterpret_cast<int2*>(P_top + cap);
+  uint8_t* flag = reinterpret_cast<uint8_t*>(P_life + cap);
+  const unsigned lt = (1u << lane) - 1u;
+
+  for (int64_t b = (int64_t)blockIdx.x * W + warp; b < a.num_problems;
+       b += (int64_t)gridDim.x * W) {
+    const int32_t* lo = a.lo + b * (int64_t)E;
+    const int32_t* hi = a.hi + b * (int64_t)E;
+    uint64_t* out_addr = a.addr + b * (int64_t)E;
+    uint8_t* out_has = a.has_addr + b * (int64_t)E;
+    int k = 0;
+    unsigned long long peak = 0;
+    for (int e = lane; e < E; e += 32) {
+      flag[e] = 0;
+      out_has[e] = 0;
+      out_addr[e] = 0;
+    }
+    __syncwarp();
+
+    // insert (x, x + s, [elo, ehi]) at its address-order index
+    auto insert = [&](unsigned long long x, unsigned long long s, int elo, int ehi) {
+      // first index p with P_addr[p] >= x: 32-ary narrowing over [0, k)
+      int lo_i = 0, n_i = k;
+      while (n_i > 32) {
+        const int step = (n_i + 31) / 32;
+        const int probe = lo_i + lane * step;
+        const bool below = probe < lo_i + n_i && P_addr[probe] < x;
+        const int c = __popc(__ballot_sync(0xffffffffu, below));  // probes below x
+        if (c == 0) {
+          n_i = 0;
+          break;
+        }
+        const int nlo = lo_i + (c - 1) * step;  // last probe below x: p is after it
+        const int nhi = min(lo_i + c * step, lo_i + n_i);
+        lo_i = nlo + 1;
+        n_i = nhi - lo_i;
+        if (n_i < 0) n_i = 0;
+      }
+      const bool below = lane < n_i && P_addr[lo_i + lane] < x;
+      const int p = lo_i + __popc(__ballot_sync(0xffffffffu, below));
+      // shift [p, k) right by one, 32 tensors per step from the end
+      for (int r = k - 32; r > p - 32; r -= 32) {
+        const int i = r + lane;
+        const bool mv = i >= p && i >= 0 && i < k;
+        unsigned long long ad = 0, tp = 0;
+        int2 lf = make_int2(0, 0);
+        if (mv) {
+          ad = P_addr[i];
+          tp = P_top[i];
+          lf = P_life[i];
+        }
+        __syncwarp();
+        if (mv) {
+          P_addr[i + 1] = ad;
+          P_top[i + 1] = tp;
+          P_life[i + 1] = lf;
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        P_addr[p] = x;
+        P_top[p] = x + s;
+        P_life[p] = make_int2(elo, ehi);
+      }
+      __syncwarp();
+      ++k;
+    };
+    // greedy_pack's lowest feasible offset for (s, [elo, ehi]) (placement.cpp:187-200)
+    auto search = [&](unsigned long long s, int elo, int ehi) -> unsigned long long {
+      long long pm = 0;  // max(0, tops of the overlapping tensors before this round)
+      for (int r = 0; r < k; r += 32) {
+        const int i = r + lane;
+        bool conf = false;
+        long long t = LLONG_MIN, L = 0;
+        if (i < k) {
+          const int2 l = P_life[i];
+          conf = !disjoint(elo, ehi, l.x, l.y);
+          t = conf ? (long long)P_top[i] : LLONG_MIN;
+          L = (long long)P_addr[i] - (long long)s;
+        }
+        long long incl = t;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const long long v = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= d && v > incl) incl = v;
+        }
+        long long ex = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) ex = LLONG_MIN;
+        const long long m = ex > pm ? ex : pm;
+        const unsigned gap = __ballot_sync(0xffffffffu, conf && L >= m);
+        if (gap) return (unsigned long long)__shfl_sync(0xffffffffu, m, __ffs(gap) - 1);
+        const long long rm = __shfl_sync(0xffffffffu, incl, 31);
+        pm = rm > pm ? rm : pm;
+      }
+      return (unsigned long long)pm;
+    };
+
+    // ---- fixed tensors: caller's preplaced map, or preallocate_pyramid ------------
+    if (a.pyramid) {
+      long long min_start = 0, max_end = LLONG_MAX;
+      unsigned long long pbase = 0;
+      while (max_end > min_start) {
+        int bd = INT_MIN, br = INT_MAX, be = -1;
+        unsigned long long bsz = 0;
+        for (int e = lane; e < E; e += 32) {
+          const unsigned long long sz = a.size[e];
+          if (flag[e] || sz == 0) continue;
+          const int l = lo[e], h = hi[e];
+          if (l <= min_start || h >= max_end) continue;
+          const int d = h - l, rk = a.id_rank ? a.id_rank[e] : e;
+          if (be < 0 || pyr_better(d, sz, rk, bd, bsz, br)) {
+            bd = d;
+            bsz = sz;
+            br = rk;
+            be = e;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const int d2 = __shfl_xor_sync(0xffffffffu, bd, o);
+          const unsigned long long s2 = __shfl_xor_sync(0xffffffffu, bsz, o);
+          const int r2 = __shfl_xor_sync(0xffffffffu, br, o);
+          const int e2 = __shfl_xor_sync(0xffffffffu, be, o);
+          if (e2 >= 0 && (be < 0 || pyr_better(d2, s2, r2, bd, bsz, br))) {
+            bd = d2;
+            bsz = s2;
+            br = r2;
+            be = e2;
+          }
+        }
+        const int pick = be;  // warp-uniform after the butterfly
+        if (pick < 0) break;
+        const unsigned long long sz = a.size[pick];
+        const int pl = lo[pick], ph = hi[pick];
+        if (lane == 0) {
+          flag[pick] = 1;
+          out_addr[pick] = pbase;
+          out_has[pick] = 1;
+        }
+        insert(pbase, sz, pl, ph);
+        pbase += sz;
+        peak = pbase > peak ? pbase : peak;
+        min_start = pl;
+        max_end = ph;
+      }
+      if (lane == 0 && a.pyramid_base) a.pyramid_base[b] = pbase;
+    } else if (a.fixed) {
+      for (int e = 0; e < E; ++e) {
+        if (!a.fixed[e]) continue;
+        const unsigned long long x = a.fixed_addr[e], sz = a.size[e];
+        if (lane == 0) {
+          flag[e] = 1;
+          out_addr[e] = x;
+          out_has[e] = 1;
+        }
+        insert(x, sz, lo[e], hi[e]);
+        peak = x + sz > peak ? x + sz : peak;
+      }
+    }
+    __syncwarp();
+
+    // ---- greedy_pack over the remaining data edges, in edge order -----------------
+    if (!a.pyramid_only) {
+      // the next edge's (size, lifetime) is loaded one step ahead
+      unsigned long long s_nx = a.size[0];
+      int lo_nx = lo[0], hi_nx = hi[0];
+      for (int e = 0; e < E; ++e) {
+        const unsigned long long sz = s_nx;
+        const int elo = lo_nx, ehi = hi_nx;
+        if (e + 1 < E) {
+          s_nx = a.size[e + 1];
+          lo_nx = lo[e + 1];
+          hi_nx = hi[e + 1];
+        }
+        if (sz == 0 || flag[e]) continue;
+        const unsigned long long x = search(sz, elo, ehi);
+        insert(x, sz, elo, ehi);
+        if (lane == 0) {
+          out_addr[e] = x;
+          out_has[e] = 1;
+        }
+        peak = x + sz > peak ? x + sz : peak;
+      }
+    }
+    if (lane == 0 && a.peak_mem) a.peak_mem[b] = peak;
+    __syncwarp();
+  }
+}
+
+size_t place_warp_slice(int num_edges) {
+  const size_t cap = (size_t)num_edges + 1;
+  return ((cap * (8 + 8 + 8) + (size_t)num_edges) + 15) & ~size_t(15);
+}
+
 }  // namespace
 
 size_t place_smem_bytes(int num_edges) {
@@ -344,6 +576,32 @@ mp_status launch_place_t(const PlaceArgs& in, const mp_ctx* ctx, cudaStream_t st
 
 mp_status launch_place(const PlaceArgs& in, const mp_ctx* ctx, cudaStream_t st) {
   if (in.num_problems <= 0 || in.num_edges == 0) return MP_OK;
+  // many problems of a modest graph: one warp per problem, placed set in address order
+  // (MP_PLACE_CTA forces the CTA variant, MP_PLACE_WARP the warp variant)
+  const bool force_cta = std::getenv("MP_PLACE_CTA") != nullptr;
+  const bool force_warp = std::getenv("MP_PLACE_WARP") != nullptr;
+  const size_t slice = place_warp_slice(in.num_edges);
+  // measured: +11% at C2 (7 warps per SM), 2x slower at C3 (3 warps per SM): only where
+  // at least six problems' placed sets fit one SM
+  const bool warp_ok = force_warp || (in.num_problems > ctx->num_sms && slice * 6 <= 228 * 1024);
+  if (!force_cta && in.num_edges <= kPlaceWarpMaxEdges && warp_ok &&
+      slice <= (size_t)ctx->max_smem_optin) {
+    PlaceArgs a = in;
+    a.cap = in.num_edges + 1;
+    // one-warp CTAs: as many per SM as their placed sets fit (up to 32)
+    auto kern = place_warp_kernel<1>;
+    constexpr int W = 1;
+    const size_t sm = slice;
+    MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int per_sm = 0;
+    MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * W, sm));
+    int64_t grid = (int64_t)ctx->num_sms * (per_sm > 0 ? per_sm : 1);
+    const int64_t need = (in.num_problems + W - 1) / W;
+    if (grid > need) grid = need;
+    kern<<<(unsigned)grid, 32 * W, sm, st>>>(a, slice);
+    MP_CUDA(cudaGetLastError());
+    return MP_OK;
+  }
   // + preplaced entries never exceed num_edges: the placed set holds <= E tensors
   // few problems (latency): the widest CTA, short chunks; many (throughput): the
   // narrowest CTA that holds the placed set, several problems per SM

@@ -26,7 +26,17 @@ def _masked(addr, has):
     return [int(a) if h else 0 for a, h in zip(addr, has)]
 
 
-def test_golden_placement(golden, planner):
+@pytest.fixture(params=["cta", "warp"])
+def variant(request, monkeypatch):
+    """K5 has a CTA-per-problem variant (few problems) and a warp-per-problem
+    variant (many problems, placed set in address order); both are forced here."""
+    monkeypatch.delenv("MP_PLACE_CTA", raising=False)
+    monkeypatch.delenv("MP_PLACE_WARP", raising=False)
+    monkeypatch.setenv("MP_PLACE_CTA" if request.param == "cta" else "MP_PLACE_WARP", "1")
+    return request.param
+
+
+def test_golden_placement(golden, planner, variant):
     checked = 0
     for rec in golden["graphs"]:
         g = mp.load_graph(rec["graph_json"])
@@ -57,7 +67,7 @@ def test_golden_placement(golden, planner):
 
 
 @pytest.mark.parametrize("name", ["resnet50_b32", "bert_base_s512", "gpt2_medium_s1024"])
-def test_batched_placement_model_graphs(planner, name):
+def test_batched_placement_model_graphs(planner, name, variant):
     """One CTA per candidate: 12 candidate orders' realized lifetimes at once,
     pyramid + greedy and plain greedy, every row vs the C restatement."""
     g = _model(name)
@@ -81,7 +91,7 @@ def test_batched_placement_model_graphs(planner, name):
                                           {e: int(addr[0, e]) for e in np.nonzero(has[0])[0]})
 
 
-def test_preplaced_map_and_edge_cases(planner):
+def test_preplaced_map_and_edge_cases(planner, variant):
     """A caller's preplaced map (incl. a zero-size entry, which can block per
     placement.cpp:196), empty lifetimes (lo > hi: disjoint from everything,
     analysis.hpp:28-37), control edges, the empty graph, capacity."""

@@ -34,7 +34,11 @@ def _expected(g, orc, order, pyramid=True):
 @pytest.mark.parametrize("kind,layers,size,seed,pyramid", [
     ("fork_join", 30, 1000, 3, True), ("training_like", 20, 8, 0, True),
     ("training_like", 25, 1 << 33, 0, False), ("chain", 40, 8, 0, True)])
-def test_score_plans_matches_restatement(planner, kind, layers, size, seed, pyramid):
+@pytest.mark.parametrize("k5", ["auto", "warp"])
+def test_score_plans_matches_restatement(planner, monkeypatch, kind, layers, size, seed, pyramid,
+                                         k5):
+    if k5 == "warp":   # the warp-per-problem placement variant (default for big batches)
+        monkeypatch.setenv("MP_PLACE_WARP", "1")
     g = mp.generate_graph(kind, layers, size, seed)
     orc = O.Oracle.from_csr(g.csr())
     orders = mp.random_topo_orders(g, 48, seed=seed + 1)
