@@ -319,7 +319,10 @@ def test_global_scratch_stamp_wrap(planner, monkeypatch, variant):
 
 @pytest.mark.parametrize("kind,layers,chunks", [("training_like", 300, 2), ("training_like", 200, 1),
                                                 ("training_like", 1000, 6), ("chain", 3000, 4),
-                                                ("training_like", 40, 1), ("training_like", 40, 0)])
+                                                ("training_like", 40, 1), ("training_like", 40, 0),
+                                                # 2-7 parts, n % 4 == 0: the deferred lists
+                                                ("training_like", 300, 8), ("training_like", 1000, 20),
+                                                ("training_like", 2000, 63)])
 def test_node_partitioned_scorer_small(planner, monkeypatch, kind, layers, chunks):
     """The node-partitioned scorer forced onto small graphs with tiny parts
     (MP_PARTS_CHUNKS 64-node chunks per part, 0 = no cap): many passes, validity pairs and
