@@ -65,7 +65,39 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// One warp per 32 x 32 bit block: lane r holds AR row (eb*32 + r), word vb; ballot
+// of bit c across the lanes is ARt row (vb*32 + c), word eb.
+__global__ void __launch_bounds__(256)
+    joint_transpose_kernel(const uint32_t* __restrict__ ar, int32_t E, int32_t n, int ar_words,
+                           int art_words, uint32_t* __restrict__ art) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nblk_e = (E + 31) / 32;
+  const int64_t nblocks = nblk_e * ar_words;
+  for (int64_t blk = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); blk < nblocks;
+       blk += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const int64_t eb = blk % nblk_e, vb = blk / nblk_e;
+    const int64_t e = eb * 32 + lane;
+    const uint32_t w = e < E ? __ldg(ar + (size_t)e * ar_words + vb) : 0u;
+    uint32_t mine = 0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, (w >> c) & 1u);
+      if (lane == c) mine = bal;
+    }
+    const int64_t v = vb * 32 + lane;
+    if (v < n) art[(size_t)v * art_words + eb] = mine;
+  }
+}
+
 }  // namespace
+
+mp_status launch_joint_transpose(const uint32_t* d_ar, int32_t E, int32_t n, int ar_words,
+                                 int art_words, uint32_t* d_art, cudaStream_t st) {
+  if (E <= 0 || n <= 0) return MP_OK;
+  joint_transpose_kernel<<<148 * 16, 256, 0, st>>>(d_ar, E, n, ar_words, art_words, d_art);
+  MP_CUDA(cudaGetLastError());
+  return MP_OK;
+}
 
 mp_status launch_joint(const JointArgs& a, int num_sms, int64_t* d_row_cnt,
                        const int64_t* d_row_off, int2* d_pairs, cudaStream_t st) {

@@ -1211,9 +1211,13 @@ namespace {
 mp_status joint_tables(mp_graph* g) {
   if (g->d_joint_mul) return MP_OK;
   const int32_t n = g->n, E = g->E;
-  if (n > kJointMaxNodes) {
+  const size_t Wn = ((size_t)n + 31) / 32, WEn = ((size_t)E + 31) / 32;
+  const size_t host_bytes = 4 * Wn * ((size_t)n + (size_t)E);   // desc + AR
+  const size_t dev_bytes = 4 * (Wn * (size_t)E + WEn * (size_t)n);  // AR + ARt
+  if (n > kJointMaxNodes || host_bytes > kJointMaxTableBytes || dev_bytes > kJointMaxTableBytes) {
     set_error("Capacity: the joint-mode pair tables support up to " +
-              std::to_string(kJointMaxNodes) + " nodes");
+              std::to_string(kJointMaxNodes) + " nodes and " +
+              std::to_string(kJointMaxTableBytes >> 30) + " GiB of bitsets");
     return MP_E_CAPACITY;
   }
   std::vector<std::vector<int32_t>> succ(n);
@@ -1260,7 +1264,8 @@ mp_status joint_tables(mp_graph* g) {
       dv[w >> 5] |= 1u << (w & 31);
     }
   }
-  std::vector<uint32_t> ar((size_t)E * W, 0), art((size_t)n * WE, 0);
+  std::vector<uint32_t> ar((size_t)E * W, 0);  // the transpose ARt is built on the device
+#pragma omp parallel for schedule(dynamic, 64)
   for (int32_t e = 0; e < E; ++e) {
     const int64_t a = g->h_sink_off[e], b = g->h_sink_off[e + 1];
     if (b == a) continue;  // no sinks: edge_precedes(e, .) needs the window test alone
@@ -1270,12 +1275,8 @@ mp_status joint_tables(mp_graph* g) {
       const uint32_t* d = &desc[(size_t)g->h_sinks[k] * W];
       for (int q = 0; q < W; ++q) r[q] &= d[q];
     }
-    for (int q = 0; q < W; ++q)
-      for (uint32_t m = r[q]; m; m &= m - 1) {
-        const int v = q * 32 + __builtin_ctz(m);
-        art[(size_t)v * WE + (e >> 5)] |= 1u << (e & 31);
-      }
   }
+  std::vector<uint32_t>().swap(desc);
   cudaStream_t st = g->ctx->stream;
   mp_status s = MP_OK;
   auto up = [&](mp_status r) {
@@ -1284,7 +1285,16 @@ mp_status joint_tables(mp_graph* g) {
   int32_t* d_mul = nullptr;
   up(upload(&d_mul, mul.data(), mul.size(), st));
   up(upload(&g->d_joint_ar, ar.data(), ar.size(), st));
-  up(upload(&g->d_joint_art, art.data(), art.size(), st));
+  if (s == MP_OK) {
+    void* d_art = nullptr;
+    const cudaError_t ce = cudaMalloc(&d_art, 4 * (size_t)n * WE);
+    if (ce != cudaSuccess) {
+      s = cuda_status(ce, "joint tables (ARt)");
+    } else {
+      g->d_joint_art = static_cast<uint32_t*>(d_art);
+      up(launch_joint_transpose(g->d_joint_ar, E, n, W, WE, g->d_joint_art, st));
+    }
+  }
   g->d_joint_mul = reinterpret_cast<int2*>(d_mul);
   g->joint_ar_words = W;
   g->joint_art_words = WE;

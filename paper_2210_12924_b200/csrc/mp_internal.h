@@ -257,7 +257,13 @@ struct JointArgs {
 };
 mp_status launch_joint(const JointArgs& a, int num_sms, int64_t* d_row_cnt,
                        const int64_t* d_row_off, int2* d_pairs, cudaStream_t st);
-constexpr int32_t kJointMaxNodes = 32768;  // descendant bitsets on the host: n^2 / 8 bytes
+// Descendant bitsets are built on the host (n^2 / 8 bytes), AR uploaded and
+// transposed on the device; both bounded by kJointMaxTableBytes.
+constexpr int32_t kJointMaxNodes = 1 << 18;
+constexpr size_t kJointMaxTableBytes = size_t{6} << 30;
+// ARt[v][e / 32] bit e % 32 = AR[e][v / 32] bit v % 32, 32 x 32 blocks by ballots
+mp_status launch_joint_transpose(const uint32_t* d_ar, int32_t E, int32_t n, int ar_words,
+                                 int art_words, uint32_t* d_art, cudaStream_t st);
 
 // K7 LP row emission (k_lp.cu): write_lp text of encode_addresses' pair rows.
 struct LpArgs {
