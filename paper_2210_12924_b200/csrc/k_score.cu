@@ -757,7 +757,8 @@ mp_status run_parts(const mp_graph* g, const int32_t* d_orders, int64_t C, uint6
   const bool vec = g->n % 4 == 0;
   if (o24 && !vec) return MP_E_INVALID_ARG;
   // deferred positions (one stream of the order) unless MP_PARTS_NO_DEFER
-  const bool defer = vec && Q.P >= 2 && Q.P <= 7 && Q.seg <= 8192 && !std::getenv("MP_PARTS_NO_DEFER");
+  const bool defer = vec && Q.P >= 2 && Q.P <= 7 && g->n <= 512 * kPartsMaxBlocks &&
+                     !std::getenv("MP_PARTS_NO_DEFER");
   auto kern = o24 ? (defer ? score_parts_kernel<true, true, true> : score_parts_kernel<true, true>)
               : vec ? (defer ? score_parts_kernel<true, false, true> : score_parts_kernel<true>)
                     : score_parts_kernel<false>;
@@ -769,9 +770,9 @@ mp_status run_parts(const mp_graph* g, const int32_t* d_orders, int64_t C, uint6
   }
   if (grid > C) grid = C;
   if (grid < 1) return MP_OK;
-  // per CTA: XF (1 byte per position) then, when deferring, 32 warp lists of seg words
+  // per CTA: XF (1 byte per position) then, when deferring, 512 words per 512-position block
   const size_t xf_bytes = ((size_t)32 * Q.seg + 255) & ~size_t(255);
-  const size_t gstride = xf_bytes + (defer ? (size_t)32 * Q.seg * 4 : 0);
+  const size_t gstride = xf_bytes + (defer ? (((size_t)g->n + 511) / 512) * 512 * 4 : 0);
   MP_TRY(g->ctx->scratch[3].reserve(gstride * (size_t)grid));
   PartArgs A;
   A.P = Q.P;

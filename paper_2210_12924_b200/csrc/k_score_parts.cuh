@@ -44,6 +44,7 @@ constexpr int kPartsThreads = 1024;
 #define MP_PARTS_U 4
 #endif
 constexpr int kPartsU = MP_PARTS_U;  // 16-byte order loads per thread per stream iteration
+constexpr int kPartsMaxBlocks = 512;  // kDefer: 512-position blocks (n <= 262,144)
 
 __device__ __forceinline__ size_t parts_al16(size_t b) { return (b + 15) & ~size_t(15); }
 
@@ -77,13 +78,14 @@ __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
 
 // k24: orders arrive as 24-bit ids (3 bytes per position, host-packed for the
 // PCIe leg of the host-buffer call; n % 4 == 0, out-of-range ids as 0xffffff).
-// kDefer: the order is streamed ONCE. Pass 0 keeps part 0's positions and
-// appends every other in-range position to the warp's deferred list in global
-// scratch (L2-resident), one word {local slot, position - segment start, part};
-// pass b >= 1 reads the warp's own list instead of the order and the chunk table
-// and keeps part b's words (needs P <= 7 - part 7 marks nothing - and a warp
-// segment of at most 8192 positions). Measured: one list read by every later pass
-// beats one list per part (two ballots per position to append) at C5.
+// kDefer: the order is streamed ONCE, in 512-position blocks that the warps take
+// from a shared counter. Pass 0 keeps part 0's positions and appends every other
+// in-range position to its block's deferred list in global scratch (L2-resident),
+// one word {local slot, position - block start, part}; pass b >= 1 takes the blocks'
+// lists the same way instead of the order and the chunk table, and keeps part b's
+// words (needs P <= 7 - part 7 marks nothing - and n <= 512 * kPartsMaxBlocks).
+// Measured: one list read by every later pass beats one list per part (two ballots
+// per position to append) at C5.
 template <bool kVec, bool k24 = false, bool kDefer = false>
 __global__ void __launch_bounds__(kPartsThreads, 1)
     score_parts_kernel(PartArgs A, int32_t n, const int32_t* __restrict__ orders, int64_t C,
@@ -93,9 +95,8 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
                        size_t gstride, size_t xf_bytes) {
   extern __shared__ __align__(16) char smem[];
   __shared__ uint32_t s_wsum[32];
-  __shared__ uint32_t s_dcnt[32];   // kDefer: each warp's deferred-list length
-  __shared__ uint32_t s_uoff[33];   // kDefer: exclusive prefix of 512-word units per list
-  __shared__ uint32_t s_next[kPartMaxParts];  // kDefer: next unit to take, per pass
+  __shared__ uint32_t s_bcnt[kPartsMaxBlocks];  // kDefer: deferred words per 512-position block
+  __shared__ uint32_t s_next[kPartMaxParts];    // kDefer: next block to take, per pass
   __shared__ uint32_t s_wbest[32];
   __shared__ int s_widx[32];
   __shared__ PartDesc s_desc[kPartMaxParts];  // read field by field where used (registers)
@@ -117,10 +118,10 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
   const int wbeg = warp * seg;
   const int wend = wbeg + seg;   // loops run in 512-position steps and stop at wend
   const int wlim = min(n, wend);  // this warp's real positions end here
-  uint32_t* dlist = reinterpret_cast<uint32_t*>(
-      opaque_u64(reinterpret_cast<uint64_t>(gxf + (size_t)blockIdx.x * gstride + xf_bytes))) +
-                    (size_t)warp * seg;  // this warp's deferred list (kDefer)
-  uint32_t dcnt = 0;                     // its length (warp-uniform)
+  // kDefer: block t's deferred words (at most 512) at dbase + 512 t
+  uint32_t* dbase = reinterpret_cast<uint32_t*>(
+      opaque_u64(reinterpret_cast<uint64_t>(gxf + (size_t)blockIdx.x * gstride + xf_bytes)));
+  const uint32_t nblk = (uint32_t)(n + 511) >> 9;
 
   // kDefer keeps the chunk table pre-formatted as a deferred word: part << 29 | local base
   // (parts past P - out-of-range ids - become part 7, which no pass keeps)
@@ -143,18 +144,11 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
     // 24-bit rows: 3n bytes each = 3n/4 words (n % 4 == 0)
     const uint32_t* ord24 = reinterpret_cast<const uint32_t*>(orders) + c * (int64_t)(3 * (n >> 2));
     bool bad = false;
-    dcnt = 0;
+    if (kDefer && tid < kPartMaxParts) s_next[tid] = 0;  // read after pass 0's slot init barrier
     for (int i = tid; i < A.n_slot_init; i += T) stash[__ldg(A.slot_init + i)] = 0;
 
     for (int b = 0; b < A.P; ++b) {
       const PartDesc& D = s_desc[b];
-      if (kDefer && b == 1 && warp == 0) {  // s_dcnt is a barrier old: units per list
-        const uint32_t units = (s_dcnt[lane] + 511u) >> 9;
-        const uint32_t incl = warp_incl_scan(units, lane);
-        s_uoff[lane] = incl - units;
-        if (lane == 31) s_uoff[32] = incl;
-        if (lane < kPartMaxParts) s_next[lane] = 0;
-      }
       {  // slot words: this part's static scan input on top, "not written" below
         // one xtab word -> four consecutive slot words per thread: 16-byte stores
         // of consecutive lanes are contiguous (no bank conflicts)
@@ -199,25 +193,22 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
       const uint32_t bsel = (uint32_t)b << 24;
       uint32_t vmax = 0;
       if (kDefer && b > 0) {
-        // the deferred positions of all warps in 512-word units taken from a shared
-        // counter (the warps finish together); 4 words per 16-byte load, part b's kept
-        const uint32_t total = s_uoff[32];
-        const uint32_t my_uoff = s_uoff[lane];
+        // the deferred words block by block, blocks taken from a shared counter (the
+        // warps finish together); 4 words per 16-byte load, part b's kept
         for (;;) {
           uint32_t t = 0;
           if (lane == 0) t = atomicAdd(&s_next[b], 1u);
           t = __shfl_sync(0xffffffffu, t, 0);
-          if (t >= total) break;
-          const int ow = 31 - __clz(__ballot_sync(0xffffffffu, my_uoff <= t));  // the list's warp
-          const uint32_t cnt = s_dcnt[ow];
-          const uint32_t* dl = dlist + (ow - warp) * seg;  // that warp's list
-          const uint32_t obeg = (uint32_t)(ow * seg);
-          const uint32_t i0 = ((t - s_uoff[ow]) << 9) + 4 * lane;
+          if (t >= nblk) break;
+          const uint32_t cnt = s_bcnt[t];
+          const uint32_t* dl = dbase + ((size_t)t << 9);
+          const uint32_t kb = t << 9;
           uint4 q[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            q[u] = i0 + u * 128 < cnt ? __ldcg(reinterpret_cast<const uint4*>(dl + i0 + u * 128))
-                                      : make_uint4(~0u, ~0u, ~0u, ~0u);
+            q[u] = 4 * lane + u * 128 < cnt
+                       ? __ldcg(reinterpret_cast<const uint4*>(dl + 4 * lane + u * 128))
+                       : make_uint4(~0u, ~0u, ~0u, ~0u);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const uint32_t ev[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
@@ -227,26 +218,41 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
               if ((e >> 29) == (uint32_t)b) {  // groups past the end read as ~0
                 const uint32_t a = slot_a + 4u * (e & 0xffffu);
                 const uint32_t w = lds_u32(a);
-                const uint32_t k = obeg + ((e >> 16) & 0x1fffu);
+                const uint32_t k = kb + ((e >> 16) & 0x1ffu);
                 sts_u32(a, (w & 0xff000000u) | (k + 1));  // 1-based
                 stg_u8(XF + k, w >> 24);
               }
             }
             // last reader: drop the consumed 128-byte lines from L2 without a write-back
-            if (last && (lane & 7) == 0 && i0 + u * 128 < cnt)
-              asm volatile("discard.global.L2 [%0], 128;" ::"l"(dl + ((i0 + u * 128) & ~31u))
+            if (last && (lane & 7) == 0 && 4 * lane + u * 128 < cnt)
+              asm volatile("discard.global.L2 [%0], 128;" ::"l"(dl + ((4 * lane + u * 128) & ~31u))
                            : "memory");
           }
         }
       } else
-      for (int r0 = wbeg + 4 * lane; r0 < wbeg + seg; r0 += kPartsU * 128) {
+      for (int it = 0;; ++it) {
+        // kDefer (pass 0): 512-position blocks from a shared counter (the warps finish
+        // together); otherwise the warp's own segment in 512-position steps
+        int r0, wlim_it;
+        uint32_t t = 0;
+        if (kDefer) {
+          if (lane == 0) t = atomicAdd(&s_next[0], 1u);
+          t = __shfl_sync(0xffffffffu, t, 0);
+          if (t >= nblk) break;
+          r0 = (int)(t << 9) + 4 * lane;
+          wlim_it = n;
+        } else {
+          r0 = wbeg + 4 * lane + it * (kPartsU * 128);
+          if (r0 >= wbeg + seg) break;
+          wlim_it = wlim;
+        }
         uint32_t vq[4 * kPartsU];
 #pragma unroll
         for (int u = 0; u < kPartsU; ++u) {  // kPartsU 16-byte loads in flight per thread
           const int r = r0 + u * 128;
           int4 q;
           if (k24) {  // four 3-byte ids in three words (word index 3r/4)
-            if (r >= wlim) {
+            if (r >= wlim_it) {
               q = make_int4(-1, -1, -1, -1);
             } else {
               const uint32_t* w = ord24 + 3 * (r >> 2);
@@ -257,23 +263,23 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
             }
           } else if (kVec) {
             const int4* p4 = reinterpret_cast<const int4*>(ord + r);
-            q = r >= wlim ? make_int4(-1, -1, -1, -1) : (last || kDefer) ? __ldcs(p4) : __ldg(p4);
+            q = r >= wlim_it ? make_int4(-1, -1, -1, -1) : (last || kDefer) ? __ldcs(p4) : __ldg(p4);
           } else {
-            q.x = r < wlim ? __ldg(ord + r) : -1;
-            q.y = r + 1 < wlim ? __ldg(ord + r + 1) : -1;
-            q.z = r + 2 < wlim ? __ldg(ord + r + 2) : -1;
-            q.w = r + 3 < wlim ? __ldg(ord + r + 3) : -1;
+            q.x = r < wlim_it ? __ldg(ord + r) : -1;
+            q.y = r + 1 < wlim_it ? __ldg(ord + r + 1) : -1;
+            q.z = r + 2 < wlim_it ? __ldg(ord + r + 2) : -1;
+            q.w = r + 3 < wlim_it ? __ldg(ord + r + 3) : -1;
           }
           vq[4 * u] = (uint32_t)q.x, vq[4 * u + 1] = (uint32_t)q.y;
           vq[4 * u + 2] = (uint32_t)q.z, vq[4 * u + 3] = (uint32_t)q.w;
         }
-        if (r0 + (kPartsU - 1) * 128 + 3 < wlim) {
+        if (r0 + (kPartsU - 1) * 128 + 3 < wlim_it) {
 #pragma unroll
           for (int j = 0; j < 4 * kPartsU; ++j) vmax = max(vmax, vq[j]);
         } else {
 #pragma unroll
           for (int j = 0; j < 4 * kPartsU; ++j)
-            bad |= vq[j] >= (uint32_t)n && r0 + (j >> 2) * 128 + (j & 3) < wlim;
+            bad |= vq[j] >= (uint32_t)n && r0 + (j >> 2) * 128 + (j & 3) < wlim_it;
         }
         if (kDefer) {
           // pass 0: part 0 now, parts 1.. appended to the deferred list. One word per
@@ -281,7 +287,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
           // the table word already is part << 29 | local base: add the id's offset in
           // its chunk and the position's offset in the segment (no carries: local
           // < 2^16, offset < 2^13)
-          const uint32_t k16 = (uint32_t)(r0 - wbeg) << 16;
+          const uint32_t k16 = (uint32_t)(4 * lane) << 16;  // position - block start
 #pragma unroll
           for (int j = 0; j < 4 * kPartsU; ++j) {
             const uint32_t e = lds_u32(ctab_a + 4u * min(vq[j] >> kPartChunkBits, (uint32_t)A.nchunks));
@@ -292,15 +298,20 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
           // writes one contiguous run of the list (coalesced)
           const uint32_t lt = (1u << lane) - 1u;
           const uint32_t nd = (uint32_t)(A.P - 1) << 29;  // parts 1 .. P-1
+          uint32_t bc = 0;                                // this block's deferred words
 #pragma unroll
           for (int j = 0; j < 4 * kPartsU; ++j) {
             const uint32_t w = vq[j];
             const bool d = w - (1u << 29) < nd;
             const uint32_t bal = __ballot_sync(0xffffffffu, d);
-            if (d) __stcg(dlist + dcnt + __popc(bal & lt), w);
-            dcnt += __popc(bal);
+            if (d) __stcg(dbase + ((size_t)t << 9) + bc + __popc(bal & lt), w);
+            bc += __popc(bal);
             vq[j] = w < (1u << 29) ? w & 0xffffu : 0xffffffffu;  // part 0: this pass
           }
+          // padded to whole 16-byte groups with ~0 (part 7: no pass keeps it), so the
+          // readers test only the group, not every word, against the count
+          if (lane < ((4u - (bc & 3u)) & 3u)) __stcg(dbase + ((size_t)t << 9) + bc + lane, ~0u);
+          if (lane == 0) s_bcnt[t] = bc;
         } else {
           // id -> local slot of part b, or ~0 (another part / out of range), in place
 #pragma unroll
@@ -322,10 +333,6 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
         }
       }
       bad |= vmax >= (uint32_t)n;
-      // pad the deferred list to whole 16-byte groups with ~0 (part 7: no pass keeps
-      // it), so the readers test only the group, not every word, against the length
-      if (kDefer && b == 0 && lane < ((4u - (dcnt & 3u)) & 3u)) __stcg(dlist + dcnt + lane, ~0u);
-      if (kDefer && b == 0 && lane == 0) s_dcnt[warp] = dcnt;
       __syncthreads();
 
       // ---- resolve part b's lookups in shared memory ---------------------------------

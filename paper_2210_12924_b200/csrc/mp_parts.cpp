@@ -10,7 +10,7 @@ namespace mpb {
 namespace {
 
 constexpr int32_t kChunk = 1 << kPartChunkBits;
-constexpr size_t kPartsMiscSmem = 2048;  // block scratch + alignment (k_score_parts.cuh)
+constexpr size_t kPartsMiscSmem = 4096;  // static shared memory (~3.4 KB) + alignment (k_score_parts.cuh)
 constexpr int32_t kMaxSlots = 32767;     // 15-bit slot field of xchk
 
 // Weighted chunk graph: adjacency lists (neighbour, weight), merged duplicates.
