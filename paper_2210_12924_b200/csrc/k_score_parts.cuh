@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
           const uint32_t cnt = s_bcnt[t];
           const uint32_t* dl = dbase + ((size_t)t << 9);
           const uint32_t kb = t << 9;
+          const uint32_t nu = (cnt + 127u) >> 7;  // 128-word rows holding words (uniform)
           uint4 q[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u)
@@ -211,6 +212,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
                        : make_uint4(~0u, ~0u, ~0u, ~0u);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
+            if ((uint32_t)u >= nu) break;
             const uint32_t ev[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
