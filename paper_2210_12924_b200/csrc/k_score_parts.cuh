@@ -434,27 +434,14 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
     }
 
     // ---- scan over XF (L2 only: the frees above were atomics at L2) -------------------
-    // pass 1: the x total of this warp's segment (4 nibbles per word: x + 8 in the
-    // low nibble of each byte, padding bytes are 8 = (x 0, f 0))
-    {
-      uint32_t tot = 0;
-      for (int r00 = wbeg; r00 < wbeg + seg; r00 += 4 * 128) {
-        uint32_t w4s[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)  // the next warp's positions read as padding
-          w4s[u] = r00 + u * 128 < wend
-                       ? __ldcg(reinterpret_cast<const unsigned int*>(XF + r00 + u * 128 + 4 * lane))
-                       : 0x08080808u;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) tot += (((w4s[u] & 0x0f0f0f0fu) * 0x01010101u) >> 24) - 32u;
-      }
-      tot = warp_sum(tot);
-      if (lane == 0) s_wsum[warp] = tot;
-    }
-    __syncthreads();
-    uint32_t carry = warp_sum(lane < warp ? s_wsum[lane] : 0u);  // exclusive over warps
-    uint32_t best = 0;
-    int best_i = wbeg;  // (0, first position): an all-zero segment reports its first step
+    // One pass: each warp scans its segment relative to the segment start (signed local
+    // sums, |x| <= 8 per position), keeping its total and its first local maximum
+    // (adding the segment's true starting RS moves every local value by the same
+    // amount, so the arg-max is the same); warp 0 then adds the exclusive prefix of the
+    // totals and takes the first maximum over the warps.
+    int32_t carry = 0;
+    int32_t best = INT32_MIN;
+    int best_i = wbeg;
     for (int r00 = wbeg; r00 < wend; r00 += 4 * 128) {
       uint32_t w4s[4];
 #pragma unroll
@@ -466,20 +453,20 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
       for (int u = 0; u < 4; ++u) {
         const int r = r00 + u * 128 + 4 * lane;
         const uint32_t w4 = w4s[u];
-        uint32_t xs[4], fs[4], t = 0;
+        int32_t xs[4], fs[4], t = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const uint32_t byte = (w4 >> (8 * q)) & 0xffu;
-          xs[q] = (byte & 0xfu) - 8u;
-          fs[q] = byte >> 4;
+          xs[q] = (int32_t)(byte & 0xfu) - 8;
+          fs[q] = (int32_t)(byte >> 4);
           t += xs[q];
         }
-        const uint32_t incl = warp_incl_scan(t, lane);
-        uint32_t run = carry + incl - t;
+        const int32_t incl = warp_incl_scan(t, lane);
+        int32_t run = carry + incl - t;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           run += xs[q];
-          const uint32_t rs = run + fs[q];
+          const int32_t rs = run + fs[q];
           // padding positions (k >= n) carry RS <= RS(n-1): they never beat a real
           // position (strict >, and the smaller index wins ties across lanes)
           const bool better = rs > best;
@@ -495,18 +482,20 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
     for (int l0 = wbeg + 128 * lane; l0 + 128 <= min(wend, n & ~127); l0 += 128 * 32)
       asm volatile("discard.global.L2 [%0], 128;" ::"l"(XF + l0) : "memory");
     if (lane == 0) {
-      s_wbest[warp] = best;
+      s_wsum[warp] = (uint32_t)carry;  // the segment's x total
+      s_wbest[warp] = (uint32_t)best;
       s_widx[warp] = best_i;
     }
     __syncthreads();
     if (warp == 0) {
-      best = s_wbest[lane];
-      best_i = s_widx[lane];
-      warp_argmax(best, best_i);
+      const uint32_t tot = s_wsum[lane];
+      uint32_t v = warp_incl_scan(tot, lane) - tot + s_wbest[lane];  // RS at the local max
+      int vi = s_widx[lane];
+      warp_argmax(v, vi);
       if (lane == 0) {
-        const uint64_t pk = (uint64_t)best * scale;
+        const uint64_t pk = (uint64_t)v * scale;
         peak_out[c] = pk;
-        step_out[c] = best_i + 1;
+        step_out[c] = vi + 1;
         valid_out[c] = 1;
         if (best_key) record_key(best_key, pk, (uint64_t)(c + index_base));
       }
