@@ -178,23 +178,30 @@ def smem_pipe_use(config, kernel_ms, sm_mhz, num_sms):
         return None
 
 
-def pinned_h2d_gbs(dev, nbytes=256 * 2**20, reps=10):
+def pinned_h2d_gbs(dev, nbytes=512 * 2**20, reps=6):
     """The PCIe roofline denominator: the pinned host->device copy rate on this box,
-    one 256 MiB copy timed with CUDA events (best of `reps`, after one warm-up)."""
+    512 MiB copied as one copy and as four back-to-back 128 MiB copies (the e2e
+    pipeline's shape), timed with CUDA events; the best of `reps` of either."""
     import torch
     src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
     dst = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     s = torch.cuda.Stream(dev)
     best = 0.0
+    q = nbytes // 4
     with torch.cuda.stream(s):
         dst.copy_(src, non_blocking=True)
         for _ in range(reps):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(s)
-            dst.copy_(src, non_blocking=True)
-            b.record(s)
-            b.synchronize()
-            best = max(best, nbytes / (a.elapsed_time(b) / 1e3) / 1e9)
+            for chunks in (1, 4):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                if chunks == 1:
+                    dst.copy_(src, non_blocking=True)
+                else:
+                    for k in range(4):
+                        dst[k * q:(k + 1) * q].copy_(src[k * q:(k + 1) * q], non_blocking=True)
+                b.record(s)
+                b.synchronize()
+                best = max(best, nbytes / (a.elapsed_time(b) / 1e3) / 1e9)
     del src, dst
     return best
 
@@ -1267,7 +1274,7 @@ def main():
                     "path": "Planner.score_orders_into -> mp_score_orders_best (pinned host)",
                     "torch_pinned_h2d_gbs": h2d_gbs,
                     # PCIe roofline of the e2e leg: wire bytes per step over the e2e step
-                    # time, against one 256 MiB pinned H2D copy on this box (pinned_h2d_gbs)
+                    # time, against the best pinned H2D copy rate on this box (pinned_h2d_gbs)
                     "pcie": {"achieved_gbs": wire_bytes * e2e_value / (world * C) / 1e9,
                              "peak_gbs": h2d_gbs,
                              "frac": wire_bytes * e2e_value / (world * C) / 1e9 / h2d_gbs}},
