@@ -191,7 +191,6 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
       // check after the loop); the segment tail checks per position.
       const bool last = b == A.P - 1;
       const uint32_t bsel = (uint32_t)b << 24;
-      uint32_t vmax = 0;
       if (kDefer && b > 0) {
         // the deferred words block by block, blocks taken from a shared counter (the
         // warps finish together); 4 words per 16-byte load, part b's kept
@@ -275,14 +274,9 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
           vq[4 * u] = (uint32_t)q.x, vq[4 * u + 1] = (uint32_t)q.y;
           vq[4 * u + 2] = (uint32_t)q.z, vq[4 * u + 3] = (uint32_t)q.w;
         }
-        if (r0 + (kPartsU - 1) * 128 + 3 < wlim_it) {
-#pragma unroll
-          for (int j = 0; j < 4 * kPartsU; ++j) vmax = max(vmax, vq[j]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 4 * kPartsU; ++j)
-            bad |= vq[j] >= (uint32_t)n && r0 + (j >> 2) * 128 + (j & 3) < wlim_it;
-        }
+        // no range check: an id outside [0, n) maps to the chunk table's "no part" entry,
+        // so no pass writes it, and with n positions some node then stays unwritten - the
+        // permutation check below rejects the order
         if (kDefer) {
           // pass 0: part 0 now, parts 1.. appended to the deferred list. One word per
           // position either way: {local, position - segment start, part}, ~0 out of range
@@ -334,7 +328,6 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
           }
         }
       }
-      bad |= vmax >= (uint32_t)n;
       __syncthreads();
 
       // ---- resolve part b's lookups in shared memory ---------------------------------
