@@ -410,6 +410,21 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
           if (hi < (uint32_t)n) parts_free_at(XF, (int)hi, d.z);
         }
       }
+      const uint32_t s2 = (uint32_t)A.nb_max * 0x10001u;  // both sinks: position 0
+      for (int i = tid; i < D.dyn2_n; i += 4 * T) {  // two-sink tensors, two per 16 bytes
+        uint4 dd[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)  // past the end: the sentinel pair (no free)
+          dd[u] = i + u * T < D.dyn2_n ? __ldg(A.dyn4 + D.dyn2_off + i + u * T)
+                                       : make_uint4(s2, 0, s2, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t ha = max(slot[dd[u].x & 0xffffu] & kPos, slot[dd[u].x >> 16] & kPos) - 1u;
+          const uint32_t hb = max(slot[dd[u].z & 0xffffu] & kPos, slot[dd[u].z >> 16] & kPos) - 1u;
+          if (ha < (uint32_t)n) parts_free_at(XF, (int)ha, dd[u].y);
+          if (hb < (uint32_t)n) parts_free_at(XF, (int)hb, dd[u].w);
+        }
+      }
       __syncthreads();  // slot words are rewritten by the next pass
     }
     for (int i = tid; i < A.n_xfree; i += T) {  // multi-consumer tensors spanning parts

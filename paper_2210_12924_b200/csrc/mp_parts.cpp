@@ -140,7 +140,8 @@ bool plan_parts(const ScorePrep& S, size_t smem_budget, int32_t max_chunks, Part
     for (int32_t c = 0; c < nchunks; ++c) p.ctab[c] = (uint32_t)part[c] << 24 | (uint32_t)base[c];
     p.ctab[nchunks] = 0xffu << 24;  // out-of-range ids: a part no pass owns
     // per-part lists, built in part order
-    std::vector<std::vector<uint32_t>> intra(p.P), xput(p.P), xchk(p.P), xmax(p.P), dyn(p.P);
+    std::vector<std::vector<uint32_t>> intra(p.P), xput(p.P), xchk(p.P), xmax(p.P), dyn(p.P),
+        dyn2(p.P);
     // one same-part producer per node is checked in node order beside the
     // permutation check (own slot read sequentially, one random read); the rest
     // go to the part's pair list, sorted by consumer so its reads run in order
@@ -169,6 +170,12 @@ bool plan_parts(const ScorePrep& S, size_t smem_budget, int32_t max_chunks, Part
       bool same = b - a <= 4;
       for (int32_t k = a + 1; k < b && same; ++k) same = pt(S.dyn_sinks[k]) == pt(S.dyn_sinks[a]);
       const uint32_t sz = (uint32_t)S.dyn_size[d];
+      if (same && b - a == 2) {  // the common case (a forward value read twice): 8 bytes
+        auto& L = dyn2[pt(S.dyn_sinks[a])];
+        L.push_back(loc(S.dyn_sinks[a]) | loc(S.dyn_sinks[a + 1]) << 16);
+        L.push_back(sz);
+        continue;
+      }
       if (same) {
         uint32_t l[4] = {s0, s0, s0, s0};  // missing sinks read position 0
         for (int32_t k = a; k < b; ++k) l[k - a] = loc(S.dyn_sinks[k]);
@@ -220,6 +227,15 @@ bool plan_parts(const ScorePrep& S, size_t smem_budget, int32_t max_chunks, Part
       put(p.xchk, xchk[b], &D.xchk_off, &D.xchk_n, 1);
       put(p.xmax, xmax[b], &D.xmax_off, &D.xmax_n, 1);
       put(p.dyn4, dyn[b], &D.dyn_off, &D.dyn_n, 4);
+      // two-sink records after the part's four-sink ones, padded with the sentinel pair
+      // (position 0: no free) so the kernel tests nothing per record
+      D.dyn2_off = (int32_t)(p.dyn4.size() / 4);
+      D.dyn2_n = (int32_t)((dyn2[b].size() + 3) / 4);
+      p.dyn4.insert(p.dyn4.end(), dyn2[b].begin(), dyn2[b].end());
+      while (p.dyn4.size() % 4) {
+        p.dyn4.push_back(s0 | s0 << 16);
+        p.dyn4.push_back(0);
+      }
     }
     if (n % kChunk) {  // the chunk holding the last node has unwritten tail slots
       const int32_t c = nchunks - 1;

@@ -41,6 +41,8 @@ struct PartDesc {
   int32_t xchk_off, xchk_n;    // u32 l | slot << 16 | dir << 31: compare with stash[slot]
   int32_t xmax_off, xmax_n;    // u32 l | slot << 16: stash[slot] = max(stash[slot], pos[l])
   int32_t dyn_off, dyn_n;      // uint4 {l1 | l2 << 16, l3 | l4 << 16, size, 0}, nb_max = none
+  int32_t dyn2_off, dyn2_n;    // two-sink tensors, two per uint4 {l1 | l2 << 16, size}
+                               // (in the dyn4 array; padded with the sentinel pair, size 0)
 };
 
 struct PartPlan {
@@ -55,7 +57,7 @@ struct PartPlan {
   std::vector<uint16_t> p1;    // per part, per local slot: one producer in the same part
   std::vector<PartDesc> desc;  // [P]
   std::vector<uint32_t> intra, xput, xchk, xmax;
-  std::vector<uint32_t> dyn4;  // 4 words per record
+  std::vector<uint32_t> dyn4;  // 4 words per record; the two-sink lists, 2 words per record
   std::vector<uint32_t> xfree; // 2 words per record: slot, size (after the last pass)
   std::vector<int32_t> slot_init_max;  // slots that accumulate a max (reset to 0 per candidate)
 };
