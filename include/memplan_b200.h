@@ -278,8 +278,10 @@ mp_status mp_score_orders_multi(mp_multi* m, const int32_t* orders, int64_t num_
  * Outputs: addr / has_addr [num_problems][num_edges] (has_addr = the edge is in
  * the returned map), peak_mem [num_problems] and pyramid_base
  * [num_problems] (PrePlacement.reserved_base), both optional.
- * At most 8192 edges per problem (the placed set lives in shared memory):
- * larger graphs return MP_E_CAPACITY. */
+ * Up to 8192 edges per problem the placed set lives in shared memory (many
+ * problems per SM); larger graphs (up to 2^18 - 1 edges, e.g. the 100k-tensor
+ * graph) keep it in a per-CTA global slice, one problem per SM. Past that:
+ * MP_E_CAPACITY. */
 #define MP_PLACE_PYRAMID 1u
 #define MP_PLACE_PYRAMID_ONLY 2u
 mp_status mp_place(mp_ctx* ctx, int32_t num_edges, int64_t num_problems, const int32_t* lo,

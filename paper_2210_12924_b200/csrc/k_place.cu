@@ -546,6 +546,310 @@ __global__ void __launch_bounds__(32 * W) place_warp_kernel(PlaceArgs a, size_t 
   }
 }
 
+// ---- one CTA per problem, placed set in global memory (E > kPlaceMaxEntries) -------
+// The warp variant's address-ordered arrays (address, top, lifetime: 24 bytes per
+// tensor) in a per-CTA global slice, L2-resident for one problem, scanned by 512
+// threads in 4096-tensor tiles (8 consecutive tensors per thread, 16-byte loads):
+//   search   per tile a block prefix-max of the overlapping tops (warp shuffles + one
+//            word per warp), each thread's sweep of its 8 tensors from that prefix,
+//            and a block min of the first gap; the scan stops at the tile holding it
+//   insert   the first index whose address is >= x by a two-level 512-ary count
+//            (__syncthreads_count), then the tail shifts right by one, 2048 tensors
+//            per tile from the end
+// Same results as the other variants (the placed set is the same set in the same
+// order); for the 100k-tensor graph, whose placed sets do not fit shared memory.
+constexpr int kBigT = 512, kBigR = 8, kBigTile = kBigT * kBigR;
+constexpr int kBigW = kBigT / 32;
+
+struct BigShared {
+  long long wmax[32];
+  int stop[2];
+  long long x;
+};
+struct BigSet {  // the placed set in address order (a per-CTA global slice) and its size
+  unsigned long long* addr;
+  unsigned long long* top;
+  int2* life;
+  BigShared* s;
+  int k;
+  int gi;  // tiles scanned so far (selects the stop buffer)
+};
+
+// greedy_pack's lowest feasible offset for (s, [elo, ehi]) (placement.cpp:187-200)
+__device__ __forceinline__ unsigned long long big_search(BigSet& P, unsigned long long s, int elo,
+                                                         int ehi) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = P.k;
+  long long carry = 0;  // max(0, overlapping tops of the earlier tiles)
+  for (int b0 = 0; b0 < k; b0 += kBigTile, ++P.gi) {
+    const int j0 = b0 + kBigR * tid;
+    unsigned long long ad[kBigR], tp[kBigR];
+    int2 lf[kBigR];
+    if (j0 < k) {  // the slice is padded to whole tiles: no partial vectors
+#pragma unroll
+      for (int q = 0; q < kBigR; q += 2) {
+        const ulonglong2 u = __ldcg(reinterpret_cast<const ulonglong2*>(P.addr + j0 + q));
+        const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(P.top + j0 + q));
+        const int4 l = __ldcg(reinterpret_cast<const int4*>(P.life + j0 + q));
+        ad[q] = u.x, ad[q + 1] = u.y, tp[q] = v.x, tp[q + 1] = v.y;
+        lf[q] = make_int2(l.x, l.y), lf[q + 1] = make_int2(l.z, l.w);
+      }
+    }
+    bool cf[kBigR];
+    long long cm = LLONG_MIN;  // max top over this thread's overlapping tensors
+#pragma unroll
+    for (int q = 0; q < kBigR; ++q) {
+      cf[q] = j0 + q < k && !disjoint(elo, ehi, lf[q].x, lf[q].y);
+      if (cf[q] && (long long)tp[q] > cm) cm = (long long)tp[q];
+    }
+    long long incl = cm;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const long long v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d && v > incl) incl = v;
+    }
+    if (lane == 31) P.s->wmax[warp] = incl;
+    __syncthreads();
+    // the other buffer was last read before this barrier: reset it for the next tile
+    if (tid == 0) P.s->stop[(P.gi + 1) & 1] = INT_MAX;
+    long long before = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) before = LLONG_MIN;
+    long long tmax = LLONG_MIN;
+    for (int w = 0; w < kBigW; ++w) {
+      const long long v = P.s->wmax[w];
+      if (w < warp && v > before) before = v;
+      if (v > tmax) tmax = v;
+    }
+    long long M = before > carry ? before : carry;
+    int stop = INT_MAX;
+    long long xs = 0;
+#pragma unroll
+    for (int q = 0; q < kBigR; ++q)
+      if (stop == INT_MAX && cf[q]) {
+        const long long L = (long long)ad[q] - (long long)s;
+        if (L >= M) {
+          stop = j0 + q;
+          xs = M;
+        } else if ((long long)tp[q] > M) {
+          M = (long long)tp[q];
+        }
+      }
+    if (stop != INT_MAX) atomicMin(&P.s->stop[P.gi & 1], stop);
+    __syncthreads();
+    const int gs = P.s->stop[P.gi & 1];
+    if (gs != INT_MAX) {
+      if (stop == gs) P.s->x = xs;
+      __syncthreads();
+      ++P.gi;
+      return (unsigned long long)P.s->x;  // rewritten only after two more barriers
+    }
+    if (tmax > carry) carry = tmax;
+  }
+  return (unsigned long long)carry;
+}
+
+// insert (x, x + s, [elo, ehi]) at the first index whose address is >= x
+__device__ __forceinline__ void big_insert(BigSet& P, unsigned long long x, unsigned long long s,
+                                           int elo, int ehi) {
+  const int tid = threadIdx.x;
+  const int k = P.k;
+  int p = 0;
+  if (k > 0) {
+    const int step = (k + kBigT - 1) / kBigT;
+    const int j = tid * step;
+    const int c1 = __syncthreads_count(j < k && __ldcg(P.addr + j) < x);
+    if (c1 > 0) {  // p in [(c1 - 1) * step + 1, min(c1 * step, k)]
+      const int lo_i = (c1 - 1) * step + 1, hi_i = min(c1 * step, k);
+      const int j2 = lo_i + tid;
+      p = lo_i + __syncthreads_count(j2 < hi_i && __ldcg(P.addr + j2) < x);
+    }
+  }
+  // [p, k) right by one, 2048 tensors per tile (4 per thread: the 8 of the search
+  // would keep 48 addresses live across the barrier)
+  constexpr int kShiftR = 4, kShiftTile = kBigT * kShiftR;
+  for (int t_hi = k; t_hi > p; t_hi -= kShiftTile) {
+    const int t_lo = max(p, t_hi - kShiftTile);
+    unsigned long long ad[kShiftR], tp[kShiftR];
+    int2 lf[kShiftR];
+#pragma unroll
+    for (int q = 0; q < kShiftR; ++q) {
+      const int i = t_lo + tid + q * kBigT;
+      if (i < t_hi) {
+        ad[q] = __ldcg(P.addr + i);
+        tp[q] = __ldcg(P.top + i);
+        lf[q] = __ldcg(P.life + i);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kShiftR; ++q) {
+      const int i = t_lo + tid + q * kBigT;
+      if (i < t_hi) {
+        __stcg(P.addr + i + 1, ad[q]);
+        __stcg(P.top + i + 1, tp[q]);
+        __stcg(P.life + i + 1, lf[q]);
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    __stcg(P.addr + p, x);
+    __stcg(P.top + p, x + s);
+    __stcg(P.life + p, make_int2(elo, ehi));
+  }
+  __syncthreads();
+  ++P.k;
+}
+
+__global__ void __launch_bounds__(kBigT, 1)
+    place_big_kernel(PlaceArgs a, char* __restrict__ scratch, size_t stride, int cap) {
+  __shared__ BigShared sh;
+  __shared__ int s_wd[32], s_wr[32], s_we[32];
+  __shared__ unsigned long long s_ws[32];
+  __shared__ int s_pick;
+  const int E = a.num_edges;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  char* base_p = scratch + (size_t)blockIdx.x * stride;
+  BigSet P;
+  P.addr = reinterpret_cast<unsigned long long*>(base_p);
+  P.top = P.addr + cap;
+  P.life = reinterpret_cast<int2*>(P.top + cap);
+  P.s = &sh;
+  P.gi = 0;
+  uint8_t* flag = reinterpret_cast<uint8_t*>(P.life + cap);
+  if (tid < 2) sh.stop[tid] = INT_MAX;
+
+  for (int64_t b = blockIdx.x; b < a.num_problems; b += gridDim.x) {
+    const int32_t* lo = a.lo + b * (int64_t)E;
+    const int32_t* hi = a.hi + b * (int64_t)E;
+    uint64_t* out_addr = a.addr + b * (int64_t)E;
+    uint8_t* out_has = a.has_addr + b * (int64_t)E;
+    P.k = 0;
+    unsigned long long peak = 0;
+    for (int e = tid; e < E; e += kBigT) {
+      flag[e] = 0;
+      out_has[e] = 0;
+      out_addr[e] = 0;
+    }
+    __syncthreads();
+
+    // ---- fixed tensors: caller's preplaced map, or preallocate_pyramid ------------
+    if (a.pyramid) {
+      long long min_start = 0, max_end = LLONG_MAX;
+      unsigned long long pbase = 0;
+      while (max_end > min_start) {
+        int bd = INT_MIN, br = INT_MAX, be = -1;
+        unsigned long long bsz = 0;
+        for (int e = tid; e < E; e += kBigT) {
+          const unsigned long long sz = a.size[e];
+          if (flag[e] || sz == 0) continue;
+          const int l = lo[e], h = hi[e];
+          if (l <= min_start || h >= max_end) continue;
+          const int d = h - l, rk = a.id_rank ? a.id_rank[e] : e;
+          if (be < 0 || pyr_better(d, sz, rk, bd, bsz, br)) {
+            bd = d;
+            bsz = sz;
+            br = rk;
+            be = e;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const int d2 = __shfl_xor_sync(0xffffffffu, bd, o);
+          const unsigned long long s2 = __shfl_xor_sync(0xffffffffu, bsz, o);
+          const int r2 = __shfl_xor_sync(0xffffffffu, br, o);
+          const int e2 = __shfl_xor_sync(0xffffffffu, be, o);
+          if (e2 >= 0 && (be < 0 || pyr_better(d2, s2, r2, bd, bsz, br))) {
+            bd = d2;
+            bsz = s2;
+            br = r2;
+            be = e2;
+          }
+        }
+        if (lane == 0) {
+          s_wd[warp] = bd;
+          s_ws[warp] = bsz;
+          s_wr[warp] = br;
+          s_we[warp] = be;
+        }
+        __syncthreads();
+        if (warp == 0) {
+          bd = lane < kBigW ? s_wd[lane] : INT_MIN;
+          bsz = lane < kBigW ? s_ws[lane] : 0;
+          br = lane < kBigW ? s_wr[lane] : INT_MAX;
+          be = lane < kBigW ? s_we[lane] : -1;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const int d2 = __shfl_xor_sync(0xffffffffu, bd, o);
+            const unsigned long long s2 = __shfl_xor_sync(0xffffffffu, bsz, o);
+            const int r2 = __shfl_xor_sync(0xffffffffu, br, o);
+            const int e2 = __shfl_xor_sync(0xffffffffu, be, o);
+            if (e2 >= 0 && (be < 0 || pyr_better(d2, s2, r2, bd, bsz, br))) {
+              bd = d2;
+              bsz = s2;
+              br = r2;
+              be = e2;
+            }
+          }
+          if (lane == 0) s_pick = be;
+        }
+        __syncthreads();
+        const int pick = s_pick;
+        if (pick < 0) break;
+        const unsigned long long sz = a.size[pick];
+        if (tid == 0) {
+          flag[pick] = 1;
+          out_addr[pick] = pbase;
+          out_has[pick] = 1;
+        }
+        big_insert(P, pbase, sz, lo[pick], hi[pick]);  // its barriers also publish flag[pick]
+        pbase += sz;
+        peak = pbase > peak ? pbase : peak;
+        min_start = lo[pick];
+        max_end = hi[pick];
+      }
+      if (tid == 0 && a.pyramid_base) a.pyramid_base[b] = pbase;
+    } else if (a.fixed) {
+      for (int e = 0; e < E; ++e) {  // uniform loop: preplaced maps are small
+        if (!a.fixed[e]) continue;
+        const unsigned long long x = a.fixed_addr[e], sz = a.size[e];
+        if (tid == 0) {
+          flag[e] = 1;
+          out_addr[e] = x;
+          out_has[e] = 1;
+        }
+        big_insert(P, x, sz, lo[e], hi[e]);
+        peak = x + sz > peak ? x + sz : peak;
+      }
+    }
+    __syncthreads();
+
+    // ---- greedy_pack over the remaining data edges, in edge order -----------------
+    if (!a.pyramid_only) {
+      for (int e = 0; e < E; ++e) {
+        const unsigned long long sz = a.size[e];
+        if (sz == 0 || flag[e]) continue;  // uniform: flags were fixed before this loop
+        const int elo = lo[e], ehi = hi[e];
+        const unsigned long long x = big_search(P, sz, elo, ehi);
+        big_insert(P, x, sz, elo, ehi);
+        if (tid == 0) {
+          out_addr[e] = x;
+          out_has[e] = 1;
+        }
+        peak = x + sz > peak ? x + sz : peak;
+      }
+    }
+    if (tid == 0 && a.peak_mem) a.peak_mem[b] = peak;
+    __syncthreads();
+  }
+}
+
+size_t place_big_stride(int num_edges, int* cap) {
+  // whole tiles (search loads 8 tensors per thread unguarded) plus the one-past shift
+  *cap = ((num_edges + 1 + kBigTile - 1) / kBigTile) * kBigTile;
+  return ((size_t)*cap * (8 + 8 + 8) + (size_t)num_edges + 255) & ~size_t(255);
+}
+
 size_t place_warp_slice(int num_edges) {
   const size_t cap = (size_t)num_edges + 1;
   return ((cap * (8 + 8 + 8) + (size_t)num_edges) + 15) & ~size_t(15);
@@ -559,7 +863,7 @@ size_t place_smem_bytes(int num_edges) {
 }
 
 template <int kPT>
-mp_status launch_place_t(const PlaceArgs& in, const mp_ctx* ctx, cudaStream_t st) {
+mp_status launch_place_t(const PlaceArgs& in, mp_ctx* ctx, cudaStream_t st) {
   PlaceArgs a = in;
   a.cap = in.num_edges < kPlaceMaxEntries ? in.num_edges + 1 : kPlaceMaxEntries;
   const size_t smem = place_smem_bytes(in.num_edges);
@@ -574,8 +878,21 @@ mp_status launch_place_t(const PlaceArgs& in, const mp_ctx* ctx, cudaStream_t st
   return MP_OK;
 }
 
-mp_status launch_place(const PlaceArgs& in, const mp_ctx* ctx, cudaStream_t st) {
+mp_status launch_place(const PlaceArgs& in, mp_ctx* ctx, cudaStream_t st) {
   if (in.num_problems <= 0 || in.num_edges == 0) return MP_OK;
+  // placed sets past shared memory (MP_PLACE_BIG forces it: tests)
+  if (in.num_edges > kPlaceMaxEntries || std::getenv("MP_PLACE_BIG")) {
+    int cap = 0;
+    const size_t stride = place_big_stride(in.num_edges, &cap);
+    int64_t grid = in.num_problems < ctx->num_sms ? in.num_problems : ctx->num_sms;
+    MP_TRY(ctx->scratch[7].reserve(stride * (size_t)grid));
+    PlaceArgs a = in;
+    a.cap = cap;
+    place_big_kernel<<<(unsigned)grid, kBigT, 0, st>>>(a, static_cast<char*>(ctx->scratch[7].ptr),
+                                                        stride, cap);
+    MP_CUDA(cudaGetLastError());
+    return MP_OK;
+  }
   // many problems of a modest graph: one warp per problem, placed set in address order
   // (MP_PLACE_CTA forces the CTA variant, MP_PLACE_WARP the warp variant)
   const bool force_cta = std::getenv("MP_PLACE_CTA") != nullptr;

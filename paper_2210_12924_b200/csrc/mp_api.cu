@@ -1635,9 +1635,9 @@ static mp_status place_check(int32_t E, int64_t B, uint32_t flags, const void* f
   if (E < 0 || B < 0) return invalid_arg("negative size");
   if ((flags & (MP_PLACE_PYRAMID | MP_PLACE_PYRAMID_ONLY)) && fixed)
     return invalid_arg("a preplaced map and MP_PLACE_PYRAMID are exclusive");
-  if (E > kPlaceMaxEntries) {
-    set_error("Capacity: " + std::to_string(E) + " edges exceed the placement kernel's " +
-              std::to_string(kPlaceMaxEntries) + " per problem");
+  if (E > kPlaceBigMaxEdges) {
+    set_error("Capacity: " + std::to_string(E) + " edges exceed the placement kernels' " +
+              std::to_string(kPlaceBigMaxEdges) + " per problem");
     return MP_E_CAPACITY;
   }
   return MP_OK;

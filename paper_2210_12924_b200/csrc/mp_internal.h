@@ -212,6 +212,7 @@ mp_status pairs_fill(const PairArgs& a, int num_sms, void* d_scratch, const int6
                      int32_t* d_pairs, cudaStream_t st, int64_t cap = INT64_MAX);
 // K5 placement (k_place.cu): preallocate_pyramid / greedy_pack / peak_mem per problem.
 constexpr int kPlaceMaxEntries = 8192;  // placed tensors per problem (shared memory)
+constexpr int kPlaceBigMaxEdges = (1 << 18) - 1;  // global-memory variant (two 512-ary levels)
 struct PlaceArgs {
   int32_t num_edges = 0;
   int64_t num_problems = 0;
@@ -230,7 +231,7 @@ struct PlaceArgs {
   int cap = 0;                         // set by launch_place
 };
 size_t place_smem_bytes(int num_edges);
-mp_status launch_place(const PlaceArgs& a, const mp_ctx* ctx, cudaStream_t st);
+mp_status launch_place(const PlaceArgs& a, mp_ctx* ctx, cudaStream_t st);
 // Batched plans (k_plans.cu): lifetimes per candidate order, the pairwise
 // address check per plan, the first-minimum key over feasible plans.
 size_t lifetimes_batch_smem(int32_t n);

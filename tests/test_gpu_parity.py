@@ -355,6 +355,39 @@ def test_node_partitioned_scorer_small(planner, monkeypatch, kind, layers, chunk
     assert best == min(ok, key=lambda i: (int(res.peak[i]), i))
 
 
+@pytest.mark.parametrize("chunks", [2, 5, 0])
+def test_node_partitioned_scorer_sink_counts(planner, monkeypatch, chunks):
+    """The partitioned scorer's three multi-consumer record kinds: 2-sink tensors (8-byte
+    records), 3- and 4-sink tensors (16-byte records) and 5-sink ones (stash max), inside
+    one part and across parts, vs the C restatement."""
+    monkeypatch.setenv("MP_SCORE_PARTS", "1")
+    monkeypatch.setenv("MP_PARTS_CHUNKS", str(chunks))
+    nodes, edges, prev = [("s0", "source")], [], "s0"
+    for gi in range(300):
+        width = 2 + gi % 4 if gi % 7 else 5
+        branch = [f"b{gi}_{k}" for k in range(width)]
+        nodes += [(b, "compute") for b in branch] + [(f"j{gi}", "compute")]
+        edges.append((f"x{gi}", prev, branch, 1 + gi % 3))
+        edges += [(f"y{gi}_{k}", branch[k], [f"j{gi}"], 1) for k in range(width)]
+        prev = f"j{gi}"
+    g = mp.graph_from_lists(nodes, edges)
+    info = mp.planner.parts_plan_info(g, max_chunks=chunks)
+    assert info["parts"] >= 1 and info["tiny4"] == 1
+    assert planner.upload(g).info()["score_variant"] == 5
+    orc = O.Oracle.from_csr(g.csr())
+    orders = mp.random_topo_orders(g, 64, seed=5)
+    orders[2, [3, 4]] = orders[2, [4, 3]]
+    orders[6, 10] = orders[6, 11]
+    res = planner.score_orders(g, orders)
+    for i, o in enumerate(orders):
+        lt = orc.lifetimes_from_order(o)
+        if lt is None:
+            assert res.valid[i] == 0, i
+            continue
+        pr, ps = O.timeline_peak(lt[0], lt[1], g.edge_size, g.n)
+        assert res.valid[i] == 1 and (int(res.peak[i]), int(res.peak_step[i])) == (pr, ps), i
+
+
 @pytest.mark.parametrize("size", [8, 1 << 20])
 def test_large_graph_wide_dynamic_edges(planner, size, monkeypatch):
     """>65,536 nodes whose order-dependent frees have 6 mutually unordered candidate

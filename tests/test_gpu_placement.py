@@ -26,13 +26,15 @@ def _masked(addr, has):
     return [int(a) if h else 0 for a, h in zip(addr, has)]
 
 
-@pytest.fixture(params=["cta", "warp"])
+@pytest.fixture(params=["cta", "warp", "big"])
 def variant(request, monkeypatch):
-    """K5 has a CTA-per-problem variant (few problems) and a warp-per-problem
-    variant (many problems, placed set in address order); both are forced here."""
-    monkeypatch.delenv("MP_PLACE_CTA", raising=False)
-    monkeypatch.delenv("MP_PLACE_WARP", raising=False)
-    monkeypatch.setenv("MP_PLACE_CTA" if request.param == "cta" else "MP_PLACE_WARP", "1")
+    """K5 has a CTA-per-problem variant (few problems), a warp-per-problem variant
+    (many problems, placed set in address order) and a global-memory variant (graphs
+    past 8,192 edges); each is forced here."""
+    for k in ("MP_PLACE_CTA", "MP_PLACE_WARP", "MP_PLACE_BIG"):
+        monkeypatch.delenv(k, raising=False)
+    monkeypatch.setenv({"cta": "MP_PLACE_CTA", "warp": "MP_PLACE_WARP",
+                        "big": "MP_PLACE_BIG"}[request.param], "1")
     return request.param
 
 
@@ -128,8 +130,29 @@ def test_preplaced_map_and_edge_cases(planner, variant):
     assert planner.greedy_pack(eg, np.zeros(0, np.int32), np.zeros(0, np.int32)) == {}
     assert planner.preallocate_pyramid(eg, np.zeros(0, np.int32),
                                        np.zeros(0, np.int32)).reserved_base == 0
-    # capacity: more edges than the shared-memory placed set holds
-    big = mp.generate_graph("training_like", 3000, 8)
-    blo, bhi = planner.lifetimes_from_order(big, big.program_order())
+    # capacity: past the global-memory variant's 2^18 - 1 edges (checked before any launch)
+    huge = mp.generate_graph("chain", 1 << 18, 8)
     with pytest.raises(errors.Error):
-        planner.greedy_pack(big, blo, bhi)
+        planner.greedy_pack(huge, np.zeros(huge.E, np.int32), np.zeros(huge.E, np.int32))
+
+
+@pytest.mark.parametrize("pyramid", [True, False])
+def test_placement_past_shared_memory(planner, pyramid):
+    """A graph past the shared-memory placed set (8,192 edges): the global-memory
+    variant, two candidates' lifetimes, vs the C restatement bit for bit."""
+    g = mp.generate_graph("training_like", 3000, 8)
+    assert g.E > 8192
+    orders = np.concatenate([g.program_order()[None], mp.random_topo_orders(g, 1, seed=3)])
+    lo = np.stack([planner.lifetimes_from_order(g, o)[0] for o in orders])
+    hi = np.stack([planner.lifetimes_from_order(g, o)[1] for o in orders])
+    addr, has, peak, base = planner.place_batch(g, lo, hi, pyramid=pyramid)
+    for b in range(len(orders)):
+        if pyramid:
+            tk, ta, tb = O.preallocate_pyramid(lo[b], hi[b], g.edge_size, g.id_rank()[:g.E])
+            assert int(base[b]) == tb
+            ea, eh = O.greedy_pack(lo[b], hi[b], g.edge_size, tk, ta)
+        else:
+            ea, eh = O.greedy_pack(lo[b], hi[b], g.edge_size)
+        assert (has[b] == eh).all(), b
+        assert (addr[b][eh == 1] == ea[eh == 1]).all(), b
+        assert int(peak[b]) == O.peak_mem(g.edge_size, eh, ea)
