@@ -614,12 +614,16 @@ __device__ __forceinline__ unsigned long long big_search(BigSet& P, unsigned lon
     if (tid == 0) P.s->stop[(P.gi + 1) & 1] = INT_MAX;
     long long before = __shfl_up_sync(0xffffffffu, incl, 1);
     if (lane == 0) before = LLONG_MIN;
-    long long tmax = LLONG_MIN;
-    for (int w = 0; w < kBigW; ++w) {
-      const long long v = P.s->wmax[w];
-      if (w < warp && v > before) before = v;
-      if (v > tmax) tmax = v;
+    // the warps' totals: an inclusive max-scan over lanes 0 .. kBigW - 1
+    long long wv = lane < kBigW ? P.s->wmax[lane] : LLONG_MIN;
+#pragma unroll
+    for (int d = 1; d < kBigW; d <<= 1) {
+      const long long v = __shfl_up_sync(0xffffffffu, wv, d);
+      if (lane >= d && v > wv) wv = v;
     }
+    const long long wprev = __shfl_sync(0xffffffffu, wv, warp > 0 ? warp - 1 : 0);
+    if (warp > 0 && wprev > before) before = wprev;
+    const long long tmax = __shfl_sync(0xffffffffu, wv, kBigW - 1);
     long long M = before > carry ? before : carry;
     int stop = INT_MAX;
     long long xs = 0;
