@@ -34,6 +34,8 @@
 #include <cstdint>
 #include <type_traits>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "mp_internal.h"
 
 namespace mpb {
@@ -708,9 +710,7 @@ __device__ __forceinline__ void big_insert(BigSet& P, unsigned long long x, unsi
 __global__ void __launch_bounds__(kBigT, 1)
     place_big_kernel(PlaceArgs a, char* __restrict__ scratch, size_t stride, int cap) {
   __shared__ BigShared sh;
-  __shared__ int s_wd[32], s_wr[32], s_we[32];
-  __shared__ unsigned long long s_ws[32];
-  __shared__ int s_pick;
+  __shared__ int s_wd[32];
   const int E = a.num_edges;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   char* base_p = scratch + (size_t)blockIdx.x * stride;
@@ -738,68 +738,35 @@ __global__ void __launch_bounds__(kBigT, 1)
     __syncthreads();
 
     // ---- fixed tensors: caller's preplaced map, or preallocate_pyramid ------------
+    // The pyramid walks this problem's edges in preference order (duration desc, size
+    // desc, id rank asc: pyr_order, sorted by the launcher): the pick is the first edge
+    // from the cursor inside the window. The window only shrinks (min_start rises to the
+    // pick's lo, max_end falls to its hi), so the edges skipped on the way never qualify
+    // again and the cursor only moves forward: O(E) checks for all picks together.
     if (a.pyramid) {
+      const int32_t* po = a.pyr_order + b * (int64_t)E;
       long long min_start = 0, max_end = LLONG_MAX;
       unsigned long long pbase = 0;
-      while (max_end > min_start) {
-        int bd = INT_MIN, br = INT_MAX, be = -1;
-        unsigned long long bsz = 0;
-        for (int e = tid; e < E; e += kBigT) {
-          const unsigned long long sz = a.size[e];
-          if (flag[e] || sz == 0) continue;
-          const int l = lo[e], h = hi[e];
-          if (l <= min_start || h >= max_end) continue;
-          const int d = h - l, rk = a.id_rank ? a.id_rank[e] : e;
-          if (be < 0 || pyr_better(d, sz, rk, bd, bsz, br)) {
-            bd = d;
-            bsz = sz;
-            br = rk;
-            be = e;
-          }
+      int cur = 0;
+      while (max_end > min_start && cur < E) {
+        const int i = cur + tid;
+        bool ok = false;
+        if (i < E) {
+          const int e = po[i];
+          ok = a.size[e] != 0 && lo[e] > min_start && hi[e] < max_end;
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const int d2 = __shfl_xor_sync(0xffffffffu, bd, o);
-          const unsigned long long s2 = __shfl_xor_sync(0xffffffffu, bsz, o);
-          const int r2 = __shfl_xor_sync(0xffffffffu, br, o);
-          const int e2 = __shfl_xor_sync(0xffffffffu, be, o);
-          if (e2 >= 0 && (be < 0 || pyr_better(d2, s2, r2, bd, bsz, br))) {
-            bd = d2;
-            bsz = s2;
-            br = r2;
-            be = e2;
-          }
-        }
-        if (lane == 0) {
-          s_wd[warp] = bd;
-          s_ws[warp] = bsz;
-          s_wr[warp] = br;
-          s_we[warp] = be;
-        }
+        const int f = __reduce_min_sync(0xffffffffu, ok ? i : INT_MAX);
+        if (lane == 0) s_wd[warp] = f;
         __syncthreads();
-        if (warp == 0) {
-          bd = lane < kBigW ? s_wd[lane] : INT_MIN;
-          bsz = lane < kBigW ? s_ws[lane] : 0;
-          br = lane < kBigW ? s_wr[lane] : INT_MAX;
-          be = lane < kBigW ? s_we[lane] : -1;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const int d2 = __shfl_xor_sync(0xffffffffu, bd, o);
-            const unsigned long long s2 = __shfl_xor_sync(0xffffffffu, bsz, o);
-            const int r2 = __shfl_xor_sync(0xffffffffu, br, o);
-            const int e2 = __shfl_xor_sync(0xffffffffu, be, o);
-            if (e2 >= 0 && (be < 0 || pyr_better(d2, s2, r2, bd, bsz, br))) {
-              bd = d2;
-              bsz = s2;
-              br = r2;
-              be = e2;
-            }
-          }
-          if (lane == 0) s_pick = be;
+        int fm = INT_MAX;
+        for (int w = 0; w < kBigW; ++w) fm = min(fm, s_wd[w]);
+        __syncthreads();  // s_wd is rewritten by the next round
+        if (fm == INT_MAX) {
+          cur += kBigT;
+          continue;
         }
-        __syncthreads();
-        const int pick = s_pick;
-        if (pick < 0) break;
+        const int pick = po[fm];
+        cur = fm + 1;
         const unsigned long long sz = a.size[pick];
         if (tid == 0) {
           flag[pick] = 1;
@@ -848,6 +815,38 @@ __global__ void __launch_bounds__(kBigT, 1)
   }
 }
 
+// pyramid preference order for the global-memory variant (sorted by the launcher with
+// stable radix sorts): edges by id rank, then by size descending (static), then per
+// problem by duration descending
+__global__ void pyr_key_rank(int E, const int32_t* __restrict__ id_rank, uint32_t* key,
+                             int32_t* val) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x) {
+    key[i] = id_rank ? (uint32_t)id_rank[i] : (uint32_t)i;
+    val[i] = i;
+  }
+}
+__global__ void pyr_key_size(int E, const uint64_t* __restrict__ size,
+                             const int32_t* __restrict__ by_rank, uint64_t* key, int32_t* val) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x) {
+    const int e = by_rank[i];
+    key[i] = ~size[e];  // ascending sort = size descending
+    val[i] = e;
+  }
+}
+__global__ void pyr_key_dur(int E, int64_t nb, const int32_t* __restrict__ lo,
+                            const int32_t* __restrict__ hi, const int32_t* __restrict__ order0,
+                            uint64_t* key, int32_t* val) {
+  const int64_t N = nb * (int64_t)E;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < N;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = x / E;
+    const int e = order0[x - b * E];
+    const uint32_t d = (uint32_t)(hi[b * E + e] - lo[b * E + e]) ^ 0x80000000u;  // signed order
+    key[x] = (uint64_t)b << 32 | (0xffffffffu - d);  // by problem, then duration descending
+    val[x] = e;
+  }
+}
+
 size_t place_big_stride(int num_edges, int* cap) {
   // whole tiles (search loads 8 tensors per thread unguarded) plus the one-past shift
   *cap = ((num_edges + 1 + kBigTile - 1) / kBigTile) * kBigTile;
@@ -886,15 +885,86 @@ mp_status launch_place(const PlaceArgs& in, mp_ctx* ctx, cudaStream_t st) {
   if (in.num_problems <= 0 || in.num_edges == 0) return MP_OK;
   // placed sets past shared memory (MP_PLACE_BIG forces it: tests)
   if (in.num_edges > kPlaceMaxEntries || std::getenv("MP_PLACE_BIG")) {
+    const int E = in.num_edges;
     int cap = 0;
-    const size_t stride = place_big_stride(in.num_edges, &cap);
-    int64_t grid = in.num_problems < ctx->num_sms ? in.num_problems : ctx->num_sms;
-    MP_TRY(ctx->scratch[7].reserve(stride * (size_t)grid));
-    PlaceArgs a = in;
-    a.cap = cap;
-    place_big_kernel<<<(unsigned)grid, kBigT, 0, st>>>(a, static_cast<char*>(ctx->scratch[7].ptr),
-                                                        stride, cap);
-    MP_CUDA(cudaGetLastError());
+    const size_t stride = place_big_stride(E, &cap);
+    const int64_t group = in.num_problems < ctx->num_sms ? in.num_problems : ctx->num_sms;
+    const size_t slices = stride * (size_t)group;
+    // pyramid: the preference order per problem, `group` problems per launch
+    const size_t ng = (size_t)group * E;
+    size_t temp = 0;
+    if (in.pyramid) {
+      size_t t1 = 0, t2 = 0;
+      MP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t1, (const uint64_t*)nullptr,
+                                              (uint64_t*)nullptr, (const int32_t*)nullptr,
+                                              (int32_t*)nullptr, (int64_t)ng, 0, 64, st));
+      MP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t2, (const uint32_t*)nullptr,
+                                              (uint32_t*)nullptr, (const int32_t*)nullptr,
+                                              (int32_t*)nullptr, E, 0, 32, st));
+      temp = (std::max(t1, t2) + 255) & ~size_t(255);
+    }
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t sort_bytes = in.pyramid ? 3 * al(4 * (size_t)E) + 2 * al(8 * (size_t)E) +
+                                               2 * al(8 * ng) + 2 * al(4 * ng) + temp
+                                         : 0;
+    MP_TRY(ctx->scratch[7].reserve(slices + sort_bytes));
+    char* cur = static_cast<char*>(ctx->scratch[7].ptr);
+    char* slice_base = cur;
+    cur += al(slices);
+    auto take = [&](size_t b) {
+      char* r = cur;
+      cur += al(b);
+      return r;
+    };
+    int32_t* order0 = nullptr;
+    uint64_t *keys = nullptr, *keys_o = nullptr;
+    int32_t *vals = nullptr, *porder = nullptr;
+    void* tmp = nullptr;
+    if (in.pyramid) {
+      order0 = reinterpret_cast<int32_t*>(take(4 * (size_t)E));
+      uint32_t* k32 = reinterpret_cast<uint32_t*>(take(4 * (size_t)E));
+      int32_t* v32 = reinterpret_cast<int32_t*>(take(4 * (size_t)E));
+      uint64_t* k64 = reinterpret_cast<uint64_t*>(take(8 * (size_t)E));
+      uint64_t* k64o = reinterpret_cast<uint64_t*>(take(8 * (size_t)E));
+      keys = reinterpret_cast<uint64_t*>(take(8 * ng));
+      keys_o = reinterpret_cast<uint64_t*>(take(8 * ng));
+      vals = reinterpret_cast<int32_t*>(take(4 * ng));
+      porder = reinterpret_cast<int32_t*>(take(4 * ng));
+      tmp = take(temp);
+      // static part: by id rank, then (stable) by size descending
+      const int eb = (int)std::min<int64_t>((E + 255) / 256, 4096);
+      pyr_key_rank<<<eb, 256, 0, st>>>(E, in.id_rank, k32, v32);
+      size_t tb = temp;
+      MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k32, reinterpret_cast<uint32_t*>(keys),
+                                              v32, vals, E, 0, 32, st));
+      pyr_key_size<<<eb, 256, 0, st>>>(E, in.size, vals, k64, v32);
+      tb = temp;
+      MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k64, k64o, v32, order0, E, 0, 64, st));
+    }
+    for (int64_t g0 = 0; g0 < in.num_problems; g0 += group) {
+      const int64_t nb = std::min<int64_t>(group, in.num_problems - g0);
+      PlaceArgs a = in;
+      a.num_problems = nb;
+      a.lo = in.lo + g0 * E;
+      a.hi = in.hi + g0 * E;
+      a.addr = in.addr + g0 * E;
+      a.has_addr = in.has_addr + g0 * E;
+      if (in.peak_mem) a.peak_mem = in.peak_mem + g0;
+      if (in.pyramid_base) a.pyramid_base = in.pyramid_base + g0;
+      if (in.pyramid) {  // per problem: (problem, duration descending), stable over order0
+        const int64_t n_items = nb * (int64_t)E;
+        int bits = 1;
+        while ((int64_t(1) << bits) < nb) ++bits;
+        const int kb = (int)std::min<int64_t>((n_items + 255) / 256, 8192);
+        pyr_key_dur<<<kb, 256, 0, st>>>(E, nb, a.lo, a.hi, order0, keys, vals);
+        size_t tb = temp;
+        MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys_o, vals, porder, n_items, 0,
+                                                32 + bits, st));
+        a.pyr_order = porder;
+      }
+      place_big_kernel<<<(unsigned)nb, kBigT, 0, st>>>(a, slice_base, stride, cap);
+      MP_CUDA(cudaGetLastError());
+    }
     return MP_OK;
   }
   // many problems of a modest graph: one warp per problem, placed set in address order

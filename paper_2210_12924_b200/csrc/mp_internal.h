@@ -229,6 +229,7 @@ struct PlaceArgs {
   uint64_t* peak_mem = nullptr;        // [B] or null
   uint64_t* pyramid_base = nullptr;    // [B] or null
   int cap = 0;                         // set by launch_place
+  const int32_t* pyr_order = nullptr;  // [B][E] set by launch_place (global-memory variant)
 };
 size_t place_smem_bytes(int num_edges);
 mp_status launch_place(const PlaceArgs& a, mp_ctx* ctx, cudaStream_t st);
