@@ -21,8 +21,9 @@
 // thread shifts from its registers (4 bytes per entry). Per edge: O(placed/T)
 // work and five barriers.
 //
-// preallocate_pyramid is a block-wide arg-max per pick (duration, then size,
-// then the edge id's rank in byte order), the window narrowing each time.
+// preallocate_pyramid walks the problem's edges in preference order (duration, then
+// size, then the edge id's rank in byte order; sorted by the launcher) with a cursor
+// that only moves forward, since the window only narrows.
 //
 // Shared memory: the placed set, 28 bytes per tensor (address, top, lifetime,
 // order index), so up to kPlaceMaxEntries tensors per problem.
@@ -53,12 +54,7 @@ struct PlaceScratch {
   int pos;
   long long x;
   long long allmax;
-  int pick;
-  // pyramid arg-max per warp
-  int wd[kPT / 32];
-  unsigned long long ws[kPT / 32];
-  int wr[kPT / 32];
-  int we[kPT / 32];
+  int we[kPT / 32];  // pyramid: first qualifying index per warp
 };
 
 // `ord` is stored skewed (one pad word per 32 entries): thread t's chunk starts at
@@ -67,14 +63,6 @@ __device__ __forceinline__ int sk(int i) { return i + (i >> 5); }
 
 __device__ __forceinline__ bool disjoint(int alo, int ahi, int blo, int bhi) {
   return alo > ahi || blo > bhi || ahi < blo || bhi < alo;  // analysis.hpp:28-37
-}
-
-// pyramid order: longer lifetime, then larger size, then smaller id rank
-__device__ __forceinline__ bool pyr_better(int d, unsigned long long s, int r, int d2,
-                                           unsigned long long s2, int r2) {
-  if (d != d2) return d > d2;
-  if (s != s2) return s > s2;
-  return r < r2;
 }
 
 template <int kPT>
@@ -206,68 +194,29 @@ __global__ void __launch_bounds__(kPT, 512 / kPT)
     };
 
     // ---- fixed tensors: caller's preplaced map, or preallocate_pyramid ------------
-    if (a.pyramid) {
+    if (a.pyramid) {  // preference order with a forward-only cursor (see place_big_kernel)
+      const int32_t* po = a.pyr_order + b * (int64_t)E;
       long long min_start = 0, max_end = LLONG_MAX;
       unsigned long long base = 0;
-      while (max_end > min_start) {
-        int bd = INT_MIN, br = INT_MAX, be = -1;
-        unsigned long long bsz = 0;
-        for (int e = tid; e < E; e += kPT) {
-          const unsigned long long s = a.size[e];
-          if (flag[e] || s == 0) continue;
-          const int l = lo[e], h = hi[e];
-          if (l <= min_start || h >= max_end) continue;
-          const int d = h - l, r = a.id_rank ? a.id_rank[e] : e;
-          if (be < 0 || pyr_better(d, s, r, bd, bsz, br)) {
-            bd = d;
-            bsz = s;
-            br = r;
-            be = e;
-          }
+      for (int cur = 0; max_end > min_start && cur < E;) {
+        const int i = cur + tid;
+        bool ok = false;
+        if (i < E) {
+          const int e = po[i];
+          ok = a.size[e] != 0 && lo[e] > min_start && hi[e] < max_end;
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const int d2 = __shfl_xor_sync(0xffffffffu, bd, o);
-          const unsigned long long s2 = __shfl_xor_sync(0xffffffffu, bsz, o);
-          const int r2 = __shfl_xor_sync(0xffffffffu, br, o);
-          const int e2 = __shfl_xor_sync(0xffffffffu, be, o);
-          if (e2 >= 0 && (be < 0 || pyr_better(d2, s2, r2, bd, bsz, br))) {
-            bd = d2;
-            bsz = s2;
-            br = r2;
-            be = e2;
-          }
-        }
-        if (lane == 0) {
-          ps.wd[warp] = bd;
-          ps.ws[warp] = bsz;
-          ps.wr[warp] = br;
-          ps.we[warp] = be;
-        }
+        const int f = __reduce_min_sync(0xffffffffu, ok ? i : INT_MAX);
+        if (lane == 0) ps.we[warp] = f;
         __syncthreads();
-        if (warp == 0) {
-          bd = lane < kW ? ps.wd[lane] : INT_MIN;
-          bsz = lane < kW ? ps.ws[lane] : 0;
-          br = lane < kW ? ps.wr[lane] : INT_MAX;
-          be = lane < kW ? ps.we[lane] : -1;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const int d2 = __shfl_xor_sync(0xffffffffu, bd, o);
-            const unsigned long long s2 = __shfl_xor_sync(0xffffffffu, bsz, o);
-            const int r2 = __shfl_xor_sync(0xffffffffu, br, o);
-            const int e2 = __shfl_xor_sync(0xffffffffu, be, o);
-            if (e2 >= 0 && (be < 0 || pyr_better(d2, s2, r2, bd, bsz, br))) {
-              bd = d2;
-              bsz = s2;
-              br = r2;
-              be = e2;
-            }
-          }
-          if (lane == 0) ps.pick = be;
+        int fm = INT_MAX;
+        for (int w = 0; w < kW; ++w) fm = min(fm, ps.we[w]);
+        __syncthreads();  // ps.we is rewritten by the next round
+        if (fm == INT_MAX) {
+          cur += kPT;
+          continue;
         }
-        __syncthreads();
-        const int pick = ps.pick;
-        if (pick < 0) break;
+        cur = fm + 1;
+        const int pick = po[fm];
         const unsigned long long s = a.size[pick];
         if (tid == 0) {
           flag[pick] = 1;
@@ -341,15 +290,6 @@ __global__ void __launch_bounds__(kPT, 512 / kPT)
 // only where many problems fit an SM (C2: 1.68e5 vs 1.51e5 placements/s).
 constexpr int kPlaceWarpMaxEdges = 4096;
 
-__device__ __forceinline__ long long wmax_ll(long long v) {
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) {
-    const long long o = __shfl_xor_sync(0xffffffffu, v, d);
-    v = o > v ? o : v;
-  }
-  return v;
-}
-
 template <int W>
 __global__ void __launch_bounds__(32 * W) place_warp_kernel(PlaceArgs a, size_t slice) {
   extern __shared__ __align__(16) char smem[];
@@ -361,7 +301,6 @@ __global__ void __launch_bounds__(32 * W) place_warp_kernel(PlaceArgs a, size_t 
   unsigned long long* P_top = P_addr + cap;
   int2* P_life = reinterpret_cast<int2*>(P_top + cap);
   uint8_t* flag = reinterpret_cast<uint8_t*>(P_life + cap);
-  const unsigned lt = (1u << lane) - 1u;
 
   for (int64_t b = (int64_t)blockIdx.x * W + warp; b < a.num_problems;
        b += (int64_t)gridDim.x * W) {
@@ -457,40 +396,25 @@ __global__ void __launch_bounds__(32 * W) place_warp_kernel(PlaceArgs a, size_t 
     };
 
     // ---- fixed tensors: caller's preplaced map, or preallocate_pyramid ------------
-    if (a.pyramid) {
+    if (a.pyramid) {  // preference order with a forward-only cursor (see place_big_kernel)
+      const int32_t* po = a.pyr_order + b * (int64_t)E;
       long long min_start = 0, max_end = LLONG_MAX;
       unsigned long long pbase = 0;
-      while (max_end > min_start) {
-        int bd = INT_MIN, br = INT_MAX, be = -1;
-        unsigned long long bsz = 0;
-        for (int e = lane; e < E; e += 32) {
-          const unsigned long long sz = a.size[e];
-          if (flag[e] || sz == 0) continue;
-          const int l = lo[e], h = hi[e];
-          if (l <= min_start || h >= max_end) continue;
-          const int d = h - l, rk = a.id_rank ? a.id_rank[e] : e;
-          if (be < 0 || pyr_better(d, sz, rk, bd, bsz, br)) {
-            bd = d;
-            bsz = sz;
-            br = rk;
-            be = e;
-          }
+      for (int cur = 0; max_end > min_start && cur < E;) {
+        const int i = cur + lane;
+        bool ok = false;
+        if (i < E) {
+          const int e = po[i];
+          ok = a.size[e] != 0 && lo[e] > min_start && hi[e] < max_end;
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const int d2 = __shfl_xor_sync(0xffffffffu, bd, o);
-          const unsigned long long s2 = __shfl_xor_sync(0xffffffffu, bsz, o);
-          const int r2 = __shfl_xor_sync(0xffffffffu, br, o);
-          const int e2 = __shfl_xor_sync(0xffffffffu, be, o);
-          if (e2 >= 0 && (be < 0 || pyr_better(d2, s2, r2, bd, bsz, br))) {
-            bd = d2;
-            bsz = s2;
-            br = r2;
-            be = e2;
-          }
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        if (!m) {
+          cur += 32;
+          continue;
         }
-        const int pick = be;  // warp-uniform after the butterfly
-        if (pick < 0) break;
+        const int f = cur + __ffs(m) - 1;
+        cur = f + 1;
+        const int pick = po[f];
         const unsigned long long sz = a.size[pick];
         const int pl = lo[pick], ph = hi[pick];
         if (lane == 0) {
@@ -881,125 +805,155 @@ mp_status launch_place_t(const PlaceArgs& in, mp_ctx* ctx, cudaStream_t st) {
   return MP_OK;
 }
 
-mp_status launch_place(const PlaceArgs& in, mp_ctx* ctx, cudaStream_t st) {
-  if (in.num_problems <= 0 || in.num_edges == 0) return MP_OK;
-  // placed sets past shared memory (MP_PLACE_BIG forces it: tests)
-  if (in.num_edges > kPlaceMaxEntries || std::getenv("MP_PLACE_BIG")) {
-    const int E = in.num_edges;
-    int cap = 0;
-    const size_t stride = place_big_stride(E, &cap);
-    const int64_t group = in.num_problems < ctx->num_sms ? in.num_problems : ctx->num_sms;
-    const size_t slices = stride * (size_t)group;
-    // pyramid: the preference order per problem, `group` problems per launch
-    const size_t ng = (size_t)group * E;
-    size_t temp = 0;
-    if (in.pyramid) {
-      size_t t1 = 0, t2 = 0;
-      MP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t1, (const uint64_t*)nullptr,
-                                              (uint64_t*)nullptr, (const int32_t*)nullptr,
-                                              (int32_t*)nullptr, (int64_t)ng, 0, 64, st));
-      MP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t2, (const uint32_t*)nullptr,
-                                              (uint32_t*)nullptr, (const int32_t*)nullptr,
-                                              (int32_t*)nullptr, E, 0, 32, st));
-      temp = (std::max(t1, t2) + 255) & ~size_t(255);
-    }
-    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-    const size_t sort_bytes = in.pyramid ? 3 * al(4 * (size_t)E) + 2 * al(8 * (size_t)E) +
-                                               2 * al(8 * ng) + 2 * al(4 * ng) + temp
-                                         : 0;
-    MP_TRY(ctx->scratch[7].reserve(slices + sort_bytes));
-    char* cur = static_cast<char*>(ctx->scratch[7].ptr);
-    char* slice_base = cur;
-    cur += al(slices);
+// The pyramid's preference order per problem (every K5 variant walks it with a cursor):
+// stable radix sorts by id rank and by size descending once per call, then per group of
+// problems by (problem, duration descending). Buffers are carved from one scratch slot.
+struct PyrSort {
+  int E = 0;
+  int64_t group = 0;
+  size_t temp = 0;
+  int32_t* order0 = nullptr;
+  uint32_t *k32 = nullptr, *k32o = nullptr;
+  int32_t* v32 = nullptr;
+  uint64_t *k64 = nullptr, *keys = nullptr, *keys_o = nullptr;
+  int32_t *vals = nullptr, *porder = nullptr;
+  void* tmp = nullptr;
+  static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
+  mp_status size(int e, int64_t g, size_t* bytes, cudaStream_t st) {
+    E = e;
+    group = g;
+    const size_t ng = (size_t)g * e;
+    size_t t1 = 0, t2 = 0;
+    MP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t1, (const uint64_t*)nullptr,
+                                            (uint64_t*)nullptr, (const int32_t*)nullptr,
+                                            (int32_t*)nullptr, (int64_t)std::max<size_t>(ng, e),
+                                            0, 64, st));
+    MP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t2, (const uint32_t*)nullptr,
+                                            (uint32_t*)nullptr, (const int32_t*)nullptr,
+                                            (int32_t*)nullptr, e, 0, 32, st));
+    temp = al(std::max(t1, t2));
+    *bytes = 4 * al(4 * (size_t)e) + al(8 * (size_t)e) + 2 * al(8 * ng) + 2 * al(4 * ng) + temp;
+    return MP_OK;
+  }
+  void carve(char* p) {
     auto take = [&](size_t b) {
-      char* r = cur;
-      cur += al(b);
+      char* r = p;
+      p += al(b);
       return r;
     };
-    int32_t* order0 = nullptr;
-    uint64_t *keys = nullptr, *keys_o = nullptr;
-    int32_t *vals = nullptr, *porder = nullptr;
-    void* tmp = nullptr;
-    if (in.pyramid) {
-      order0 = reinterpret_cast<int32_t*>(take(4 * (size_t)E));
-      uint32_t* k32 = reinterpret_cast<uint32_t*>(take(4 * (size_t)E));
-      int32_t* v32 = reinterpret_cast<int32_t*>(take(4 * (size_t)E));
-      uint64_t* k64 = reinterpret_cast<uint64_t*>(take(8 * (size_t)E));
-      uint64_t* k64o = reinterpret_cast<uint64_t*>(take(8 * (size_t)E));
-      keys = reinterpret_cast<uint64_t*>(take(8 * ng));
-      keys_o = reinterpret_cast<uint64_t*>(take(8 * ng));
-      vals = reinterpret_cast<int32_t*>(take(4 * ng));
-      porder = reinterpret_cast<int32_t*>(take(4 * ng));
-      tmp = take(temp);
-      // static part: by id rank, then (stable) by size descending
-      const int eb = (int)std::min<int64_t>((E + 255) / 256, 4096);
-      pyr_key_rank<<<eb, 256, 0, st>>>(E, in.id_rank, k32, v32);
-      size_t tb = temp;
-      MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k32, reinterpret_cast<uint32_t*>(keys),
-                                              v32, vals, E, 0, 32, st));
-      pyr_key_size<<<eb, 256, 0, st>>>(E, in.size, vals, k64, v32);
-      tb = temp;
-      MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k64, k64o, v32, order0, E, 0, 64, st));
-    }
-    for (int64_t g0 = 0; g0 < in.num_problems; g0 += group) {
-      const int64_t nb = std::min<int64_t>(group, in.num_problems - g0);
-      PlaceArgs a = in;
-      a.num_problems = nb;
-      a.lo = in.lo + g0 * E;
-      a.hi = in.hi + g0 * E;
-      a.addr = in.addr + g0 * E;
-      a.has_addr = in.has_addr + g0 * E;
-      if (in.peak_mem) a.peak_mem = in.peak_mem + g0;
-      if (in.pyramid_base) a.pyramid_base = in.pyramid_base + g0;
-      if (in.pyramid) {  // per problem: (problem, duration descending), stable over order0
-        const int64_t n_items = nb * (int64_t)E;
-        int bits = 1;
-        while ((int64_t(1) << bits) < nb) ++bits;
-        const int kb = (int)std::min<int64_t>((n_items + 255) / 256, 8192);
-        pyr_key_dur<<<kb, 256, 0, st>>>(E, nb, a.lo, a.hi, order0, keys, vals);
-        size_t tb = temp;
-        MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys_o, vals, porder, n_items, 0,
-                                                32 + bits, st));
-        a.pyr_order = porder;
-      }
-      place_big_kernel<<<(unsigned)nb, kBigT, 0, st>>>(a, slice_base, stride, cap);
-      MP_CUDA(cudaGetLastError());
-    }
+    const size_t ng = (size_t)group * E;
+    order0 = reinterpret_cast<int32_t*>(take(4 * (size_t)E));
+    k32 = reinterpret_cast<uint32_t*>(take(4 * (size_t)E));
+    k32o = reinterpret_cast<uint32_t*>(take(4 * (size_t)E));
+    v32 = reinterpret_cast<int32_t*>(take(4 * (size_t)E));
+    k64 = reinterpret_cast<uint64_t*>(take(8 * (size_t)E));
+    keys = reinterpret_cast<uint64_t*>(take(8 * ng));
+    keys_o = reinterpret_cast<uint64_t*>(take(8 * ng));
+    vals = reinterpret_cast<int32_t*>(take(4 * ng));
+    porder = reinterpret_cast<int32_t*>(take(4 * ng));
+    tmp = take(temp);
+  }
+  mp_status statics(const int32_t* id_rank, const uint64_t* size, cudaStream_t st) {
+    const int eb = (int)std::min<int64_t>((E + 255) / 256, 4096);
+    pyr_key_rank<<<eb, 256, 0, st>>>(E, id_rank, k32, v32);
+    size_t tb = temp;
+    MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k32, k32o, v32, vals, E, 0, 32, st));
+    pyr_key_size<<<eb, 256, 0, st>>>(E, size, vals, k64, v32);
+    tb = temp;
+    MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k64, keys_o, v32, order0, E, 0, 64, st));
+    return MP_OK;
+  }
+  mp_status problems(const int32_t* lo, const int32_t* hi, int64_t nb, cudaStream_t st) {
+    const int64_t n_items = nb * (int64_t)E;
+    int bits = 1;
+    while ((int64_t(1) << bits) < nb) ++bits;
+    const int kb = (int)std::min<int64_t>((n_items + 255) / 256, 8192);
+    pyr_key_dur<<<kb, 256, 0, st>>>(E, nb, lo, hi, order0, keys, vals);
+    size_t tb = temp;
+    MP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys_o, vals, porder, n_items, 0,
+                                            32 + bits, st));
+    return MP_OK;
+  }
+};
+
+static mp_status launch_group(const PlaceArgs& a, mp_ctx* ctx, cudaStream_t st, char* slices,
+                              size_t stride, int cap) {
+  if (slices) {  // placed sets past shared memory: one 512-thread CTA per problem
+    place_big_kernel<<<(unsigned)a.num_problems, kBigT, 0, st>>>(a, slices, stride, cap);
+    MP_CUDA(cudaGetLastError());
     return MP_OK;
   }
   // many problems of a modest graph: one warp per problem, placed set in address order
   // (MP_PLACE_CTA forces the CTA variant, MP_PLACE_WARP the warp variant)
   const bool force_cta = std::getenv("MP_PLACE_CTA") != nullptr;
   const bool force_warp = std::getenv("MP_PLACE_WARP") != nullptr;
-  const size_t slice = place_warp_slice(in.num_edges);
+  const size_t slice = place_warp_slice(a.num_edges);
   // measured: +11% at C2 (7 warps per SM), 2x slower at C3 (3 warps per SM): only where
   // at least six problems' placed sets fit one SM
-  const bool warp_ok = force_warp || (in.num_problems > ctx->num_sms && slice * 6 <= 228 * 1024);
-  if (!force_cta && in.num_edges <= kPlaceWarpMaxEdges && warp_ok &&
+  const bool warp_ok = force_warp || (a.num_problems > ctx->num_sms && slice * 6 <= 228 * 1024);
+  if (!force_cta && a.num_edges <= kPlaceWarpMaxEdges && warp_ok &&
       slice <= (size_t)ctx->max_smem_optin) {
-    PlaceArgs a = in;
-    a.cap = in.num_edges + 1;
+    PlaceArgs w = a;
+    w.cap = a.num_edges + 1;
     // one-warp CTAs: as many per SM as their placed sets fit (up to 32)
     auto kern = place_warp_kernel<1>;
-    constexpr int W = 1;
-    const size_t sm = slice;
-    MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)slice));
     int per_sm = 0;
-    MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * W, sm));
+    MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, slice));
     int64_t grid = (int64_t)ctx->num_sms * (per_sm > 0 ? per_sm : 1);
-    const int64_t need = (in.num_problems + W - 1) / W;
-    if (grid > need) grid = need;
-    kern<<<(unsigned)grid, 32 * W, sm, st>>>(a, slice);
+    if (grid > a.num_problems) grid = a.num_problems;
+    kern<<<(unsigned)grid, 32, slice, st>>>(w, slice);
     MP_CUDA(cudaGetLastError());
     return MP_OK;
   }
   // + preplaced entries never exceed num_edges: the placed set holds <= E tensors
   // few problems (latency): the widest CTA, short chunks; many (throughput): the
   // narrowest CTA that holds the placed set, several problems per SM
-  if (in.num_problems <= ctx->num_sms) return launch_place_t<512>(in, ctx, st);
-  if (in.num_edges <= 128 * kChMax) return launch_place_t<128>(in, ctx, st);
-  if (in.num_edges <= 256 * kChMax) return launch_place_t<256>(in, ctx, st);
-  return launch_place_t<512>(in, ctx, st);
+  if (a.num_problems <= ctx->num_sms) return launch_place_t<512>(a, ctx, st);
+  if (a.num_edges <= 128 * kChMax) return launch_place_t<128>(a, ctx, st);
+  if (a.num_edges <= 256 * kChMax) return launch_place_t<256>(a, ctx, st);
+  return launch_place_t<512>(a, ctx, st);
+}
+
+mp_status launch_place(const PlaceArgs& in, mp_ctx* ctx, cudaStream_t st) {
+  if (in.num_problems <= 0 || in.num_edges == 0) return MP_OK;
+  const int E = in.num_edges;
+  // placed sets past shared memory (MP_PLACE_BIG forces it: tests)
+  const bool big = E > kPlaceMaxEntries || std::getenv("MP_PLACE_BIG");
+  int cap = 0;
+  const size_t stride = big ? place_big_stride(E, &cap) : 0;
+  // problems per launch: one per SM for the global-memory variant; otherwise as many as
+  // keep the pyramid's sort buffers (24 bytes per edge and problem) under ~1.5 GB
+  const int64_t group =
+      big ? std::min<int64_t>(in.num_problems, ctx->num_sms)
+          : std::min<int64_t>(in.num_problems, std::max<int64_t>(1, (int64_t(1) << 26) / E));
+  const size_t slices = PyrSort::al(stride * (size_t)group);
+  PyrSort ps;
+  size_t sort_bytes = 0;
+  if (in.pyramid) MP_TRY(ps.size(E, group, &sort_bytes, st));
+  if (slices + sort_bytes > 0) MP_TRY(ctx->scratch[7].reserve(slices + sort_bytes));
+  char* base = static_cast<char*>(ctx->scratch[7].ptr);
+  if (in.pyramid) {
+    ps.carve(base + slices);
+    MP_TRY(ps.statics(in.id_rank, in.size, st));
+  }
+  for (int64_t g0 = 0; g0 < in.num_problems; g0 += group) {
+    const int64_t nb = std::min<int64_t>(group, in.num_problems - g0);
+    PlaceArgs a = in;
+    a.num_problems = nb;
+    a.lo = in.lo + g0 * E;
+    a.hi = in.hi + g0 * E;
+    a.addr = in.addr + g0 * E;
+    a.has_addr = in.has_addr + g0 * E;
+    if (in.peak_mem) a.peak_mem = in.peak_mem + g0;
+    if (in.pyramid_base) a.pyramid_base = in.pyramid_base + g0;
+    if (in.pyramid) {
+      MP_TRY(ps.problems(a.lo, a.hi, nb, st));
+      a.pyr_order = ps.porder;
+    }
+    MP_TRY(launch_group(a, ctx, st, big ? base : nullptr, stride, cap));
+  }
+  return MP_OK;
 }
 
 }  // namespace mpb
