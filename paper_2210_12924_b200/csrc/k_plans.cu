@@ -12,6 +12,8 @@
 // plan by peak_mem over the feasible ones (a fused atomicMin key).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include <climits>
 #include <cstdint>
 
@@ -132,6 +134,24 @@ __global__ void plan_key_kernel(int64_t C, const uint8_t* __restrict__ valid,
   }
 }
 
+// Large graphs (launch_plans_large): one plan's conflict count, read from the K4 sweep's
+// device total, clamped to 32 bits; an invalid order has no plan (count 0, peak_mem 0).
+__global__ void plan_store_count_kernel(const int64_t* __restrict__ total,
+                                        const uint8_t* __restrict__ valid, int64_t c,
+                                        uint32_t* __restrict__ nviol, uint64_t* __restrict__ peak_mem) {
+  if (threadIdx.x != 0) return;
+  const bool ok = valid[c] != 0;
+  const int64_t t = *total;
+  nviol[c] = ok ? (uint32_t)(t < 0xffffffffll ? t : 0xffffffffll) : 0u;
+  if (!ok && peak_mem) peak_mem[c] = 0;
+}
+__global__ void valid_narrow_kernel(const int32_t* __restrict__ v32, int64_t C,
+                                    uint8_t* __restrict__ v8) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
+       c += (int64_t)gridDim.x * blockDim.x)
+    v8[c] = v32[c] != 0 ? 1 : 0;
+}
+
 }  // namespace
 
 size_t lifetimes_batch_smem(int32_t n) { return (size_t)n * 4; }
@@ -181,6 +201,48 @@ mp_status launch_plan_key(int64_t C, const uint8_t* d_valid, const uint32_t* d_n
   plan_key_kernel<<<(unsigned)(blocks < 1024 ? blocks : 1024), 256, 0, st>>>(
       C, d_valid, d_nviol, d_peak_mem, index_base, reinterpret_cast<unsigned long long*>(d_key));
   MP_CUDA(cudaGetLastError());
+  return MP_OK;
+}
+
+// Candidate plans on graphs past the shared-memory kernels (the 100k-tensor graph):
+// lifetimes per candidate with K1 (positions in global scratch), and each plan's address
+// check with the K4 sweep over the whole GPU (validate_plan's below_above pairs),
+// counted on the device. Placement (K5's global-memory variant) runs in between.
+mp_status launch_lifetimes_large(const mp_graph* g, const int32_t* d_orders, int64_t C,
+                                 int32_t* d_lo, int32_t* d_hi, int32_t* d_valid32,
+                                 uint8_t* d_valid, int32_t* d_pos, cudaStream_t st) {
+  const int64_t n = g->n, E = g->E;
+  for (int64_t c = 0; c < C; ++c)
+    MP_TRY(launch_lifetimes(g, d_orders + c * n, n, d_lo + c * E, d_hi + c * E, d_valid32 + c,
+                            d_pos, st));
+  valid_narrow_kernel<<<(unsigned)std::min<int64_t>((C + 255) / 256, 1024), 256, 0, st>>>(
+      d_valid32, C, d_valid);
+  MP_CUDA(cudaGetLastError());
+  return MP_OK;
+}
+
+mp_status launch_plan_check_large(mp_ctx* ctx, int64_t C, int32_t E, const int32_t* d_lo,
+                                  const int32_t* d_hi, const uint64_t* d_size,
+                                  const uint8_t* d_has, const uint64_t* d_addr,
+                                  const uint8_t* d_valid, uint32_t* d_nviol, uint64_t* d_peak_mem,
+                                  int64_t* d_row_off, cudaStream_t st) {
+  PairArgs a;
+  a.num_edges = E;
+  a.size = d_size;
+  a.mode = 1;
+  a.row_begin = 0;
+  a.row_end = E;
+  MP_TRY(ctx->scratch[2].reserve(pairs_scratch_bytes(a, ctx->num_sms)));
+  for (int64_t c = 0; c < C; ++c) {
+    a.lo = d_lo + c * E;
+    a.hi = d_hi + c * E;
+    a.mask = d_has + c * E;
+    a.addr = d_addr + c * E;
+    MP_TRY(pairs_count(a, ctx->num_sms, ctx->scratch[2].ptr, d_row_off, nullptr, st));
+    plan_store_count_kernel<<<1, 32, 0, st>>>(pairs_device_total(a, ctx->num_sms, ctx->scratch[2].ptr),
+                                              d_valid, c, d_nviol, d_peak_mem);
+    MP_CUDA(cudaGetLastError());
+  }
   return MP_OK;
 }
 

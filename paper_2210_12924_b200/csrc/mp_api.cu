@@ -1713,16 +1713,22 @@ mp_status mp_score_plans_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_orde
   if (C > 0 && (!d_peak_rs || !d_peak_step || !d_valid || !d_peak_mem || !d_nviol ||
                 (g->n > 0 && !d_orders)))
     return invalid_arg("null buffer");
-  if (g->E > kPlaceMaxEntries) {
-    set_error("Capacity: placement handles at most 8192 edges per problem");
+  if (g->E > kPlaceBigMaxEdges) {
+    set_error("Capacity: placement handles at most " + std::to_string(kPlaceBigMaxEdges) +
+              " edges per problem");
     return MP_E_CAPACITY;
   }
   if (C == 0) return MP_OK;
   DeviceGuard guard(ctx->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const size_t E = (size_t)g->E, c = (size_t)C;
-  MP_TRY(ctx->scratch[6].reserve(Carver::size_of({4 * E * c, 4 * E * c, c, d_addr ? 0 : 8 * E * c,
-                                                  d_has ? 0 : E * c})));
+  const size_t E = (size_t)g->E, c = (size_t)C, n = (size_t)g->n;
+  // graphs past the shared-memory kernels (lifetimes, placed set, pair records): K1 per
+  // candidate, K5's global-memory variant, the K4 sweep per plan
+  const bool large = g->E > kPlaceMaxEntries || lifetimes_batch_smem(g->n) > ctx->max_smem_optin ||
+                     plan_check_smem(g->E) > ctx->max_smem_optin;
+  MP_TRY(ctx->scratch[6].reserve(Carver::size_of(
+      {4 * E * c, 4 * E * c, c, d_addr ? 0 : 8 * E * c, d_has ? 0 : E * c, large ? 4 * c : 0,
+       large ? 4 * (n + 1) : 0, large ? 8 * (E + 1) : 0})));
   Carver cv(ctx->scratch[6].ptr);
   int32_t* d_lo = cv.take<int32_t>(E * c);
   int32_t* d_hi = cv.take<int32_t>(E * c);
@@ -1731,6 +1737,29 @@ mp_status mp_score_plans_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_orde
   if (!d_has) d_has = cv.take<uint8_t>(E * c);
   // the schedules (K3), their lifetimes, their placements, the address check, the key
   MP_TRY(launch_score(g, d_orders, C, d_peak_rs, d_peak_step, d_valid, nullptr, nullptr, 0, st));
+  if (large) {
+    int32_t* d_lv32 = cv.take<int32_t>(c);
+    int32_t* d_pos = cv.take<int32_t>(n + 1);
+    int64_t* d_row_off = cv.take<int64_t>(E + 1);
+    MP_TRY(launch_lifetimes_large(g, d_orders, C, d_lo, d_hi, d_lv32, d_lv, d_pos, st));
+    PlaceArgs a;
+    a.num_edges = g->E;
+    a.num_problems = C;
+    a.lo = d_lo;
+    a.hi = d_hi;
+    a.size = g->d_edge_size;
+    a.id_rank = d_id_rank;
+    a.pyramid = (flags & MP_PLACE_PYRAMID) ? 1 : 0;
+    a.addr = d_addr;
+    a.has_addr = d_has;
+    a.peak_mem = d_peak_mem;
+    MP_TRY(launch_place(a, ctx, st));
+    MP_TRY(launch_plan_check_large(ctx, C, g->E, d_lo, d_hi, g->d_edge_size, d_has, d_addr, d_lv,
+                                   d_nviol, d_peak_mem, d_row_off, st));
+    if (d_best_key)
+      MP_TRY(launch_plan_key(C, d_lv, d_nviol, d_peak_mem, index_base, d_best_key, st));
+    return MP_OK;
+  }
   mp_status s = launch_lifetimes_batch(g, d_orders, C, d_lo, d_hi, d_lv, st);
   if (s == MP_E_CAPACITY) set_error("Capacity: graph too large for the batched lifetimes kernel");
   MP_TRY(s);

@@ -236,6 +236,15 @@ mp_status launch_place(const PlaceArgs& a, mp_ctx* ctx, cudaStream_t st);
 // Batched plans (k_plans.cu): lifetimes per candidate order, the pairwise
 // address check per plan, the first-minimum key over feasible plans.
 size_t lifetimes_batch_smem(int32_t n);
+// ... and for graphs past the shared-memory kernels (per-candidate K1, per-plan K4 sweep)
+mp_status launch_lifetimes_large(const mp_graph* g, const int32_t* d_orders, int64_t C,
+                                 int32_t* d_lo, int32_t* d_hi, int32_t* d_valid32,
+                                 uint8_t* d_valid, int32_t* d_pos, cudaStream_t st);
+mp_status launch_plan_check_large(mp_ctx* ctx, int64_t C, int32_t E, const int32_t* d_lo,
+                                  const int32_t* d_hi, const uint64_t* d_size,
+                                  const uint8_t* d_has, const uint64_t* d_addr,
+                                  const uint8_t* d_valid, uint32_t* d_nviol, uint64_t* d_peak_mem,
+                                  int64_t* d_row_off, cudaStream_t st);
 size_t plan_check_smem(int32_t E);
 mp_status launch_lifetimes_batch(const mp_graph* g, const int32_t* d_orders, int64_t C,
                                  int32_t* d_lo, int32_t* d_hi, uint8_t* d_valid, cudaStream_t st);

@@ -62,6 +62,31 @@ def test_score_plans_matches_restatement(planner, monkeypatch, kind, layers, siz
     assert best == min(feas)[1]
 
 
+@pytest.mark.parametrize("pyramid", [True, False])
+def test_score_plans_past_shared_memory(planner, pyramid):
+    """A graph past the shared-memory kernels (9,003 edges > 8,192): lifetimes per
+    candidate (K1), K5's global-memory placement and each plan's address check by the
+    K4 sweep, vs the C restatement; an invalid row gets no plan."""
+    g = mp.generate_graph("training_like", 3000, 8)
+    assert g.E > 8192
+    orc = O.Oracle.from_csr(g.csr())
+    orders = mp.random_topo_orders(g, 4, seed=13)
+    orders[2, [0, 1]] = orders[2, [1, 0]]
+    res, best = planner.score_plans(g, orders, pyramid=pyramid)
+    feas = []
+    for i, o in enumerate(orders):
+        exp = _expected(g, orc, o, pyramid)
+        if exp is None:
+            assert res["valid"][i] == 0 and res["nviol"][i] == 0 and res["peak_mem"][i] == 0
+            continue
+        lo, hi, ea, eh, pm, nv = exp
+        assert (res["has_addr"][i] == eh).all(), i
+        assert (res["addr"][i][eh == 1] == ea[eh == 1]).all(), i
+        assert int(res["peak_mem"][i]) == pm and int(res["nviol"][i]) == nv == 0, i
+        feas.append((pm, i))
+    assert best == min(feas)[1]
+
+
 def test_validate_plans_counts_tampered_conflicts(planner):
     """Caller-supplied plans: a greedy plan (no conflict) and seeded tampered copies
     (addresses moved onto live neighbours) - counts equal the restatement's pair
