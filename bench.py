@@ -444,10 +444,10 @@ def run_plan(args, cfg):
         # no same-run rows; parity at this size is tests/ + profiles/r2/c5_plan/
         parity.update({"rows": 0, "ok": parity["key_consistent"],
                        "note": "C5 greedy_pack/pyramid parity: tools/gpu/big_place.py vs "
-                               "tools/c5_greedy_check.py (committed result under profiles/r2/)"})
+                               "tools/c5_greedy_check.py (profiles/r2/c5_plan/greedy_check.json)"})
         cpu = {"value": None, "unit": "plans/s", "cores": 1, "kind": "port",
                "sample": "not timed in this run: one C5 plan's greedy_pack alone runs for minutes "
-                         "on one host thread (profiles/r2/c5_plan/README.md)"}
+                         "on one host thread (profiles/r2/c5_plan/greedy_check.json)"}
     elif O.ref_available():
         rg = O.RefGraph.load(mp.save_graph(g))
         mism = 0

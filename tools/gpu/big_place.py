@@ -12,7 +12,7 @@ for pyr in (True, False):
         print('c5 E', g.E, 'pyramid' if pyr else 'plain', 'one problem', round(time.time() - t, 3), 's peak', int(peak[0]), flush=True)
     ok = p.addresses_feasible(g, lo, hi, {int(e): int(addr[0, e]) for e in np.nonzero(has[0])[0]})
     print('feasible', ok, flush=True)
-np.save('gpurun_out/c5_greedy_addr.npy', addr[0]); np.save('gpurun_out/c5_greedy_has.npy', has[0])
+os.makedirs("gpurun_out", exist_ok=True); np.save("gpurun_out/c5_greedy_addr.npy", addr[0]); np.save("gpurun_out/c5_greedy_has.npy", has[0])
 B = 148
 LO = np.repeat(lo[None], B, 0); HI = np.repeat(hi[None], B, 0)
 t = time.time()

@@ -9,6 +9,8 @@ timeout 900 python bench.py --impl reference > $O/ref_c5.json 2> $O/ref_c5.err
 for c in c2 c3 c4; do timeout 600 python bench.py --config $c --steps 100 --warmup 10 > $O/bench_$c.json 2> $O/bench_$c.err; done
 timeout 600 python bench.py --impl reference --config c2 > $O/ref_c2.json 2> $O/ref_c2.err
 for c in c2 c3; do timeout 600 python bench.py --mode plan --config $c --steps 5 > $O/plan_$c.json 2> $O/plan_$c.err; done
+timeout 900 python bench.py --mode plan --config c5 --steps 2 --warmup 3 > $O/plan_c5.json 2> $O/plan_c5.err
+timeout 600 python tools/gpu/big_place.py > $O/big_place_c5.txt 2>&1
 for c in c2 c3 c5; do timeout 600 python bench.py --mode pairs --config $c --steps 10 > $O/pairs_$c.json 2> $O/pairs_$c.err; done
 for c in c2 c3 c4; do timeout 600 python bench.py --mode place --config $c --steps 5 --place-batch 2048 > $O/place_$c.json 2> $O/place_$c.err; done
 for c in c2 c3 c4; do timeout 600 python bench.py --mode joint --config $c --steps 3 > $O/joint_$c.json 2> $O/joint_$c.err; done
