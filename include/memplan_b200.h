@@ -309,7 +309,9 @@ mp_status mp_place_d(mp_ctx* ctx, int32_t num_edges, int64_t num_problems, const
  * d_addr / d_has_addr [num_orders][num_edges] may be NULL (context scratch).
  * d_best_key (optional, 2 words as mp_score_orders_argmin_d): first minimum of
  * peak_mem over feasible plans (valid order, nviol == 0). Stream-ordered; the
- * placement bounds apply (num_edges <= 8192). */
+ * placement bounds apply (num_edges <= 2^18 - 1). Past the shared-memory kernels
+ * (8192 edges, or positions / pair records beyond shared memory) the lifetimes run
+ * per candidate, the placement one problem per SM, the check as a K4 sweep per plan. */
 mp_status mp_score_plans_d(mp_ctx* ctx, const mp_graph* g, const int32_t* d_orders,
                            int64_t num_orders, const int32_t* d_id_rank, uint32_t flags,
                            uint64_t* d_peak_rs, int32_t* d_peak_step, uint8_t* d_valid,
