@@ -178,12 +178,18 @@ def smem_pipe_use(config, kernel_ms, sm_mhz, num_sms):
         return None
 
 
-def pinned_h2d_gbs(dev, nbytes=512 * 2**20, reps=6):
+def pinned_h2d_gbs(dev, nbytes=512 * 2**20, reps=6, src=None):
     """The PCIe roofline denominator: the pinned host->device copy rate on this box,
-    512 MiB copied as one copy and as four back-to-back 128 MiB copies (the e2e
-    pipeline's shape), timed with CUDA events; the best of `reps` of either."""
+    512 MiB (or the given pinned tensor: the e2e leg's own host buffer, so the copy
+    reads the same host memory) copied as one copy and as four back-to-back copies (the
+    e2e pipeline's shape), timed with CUDA events; the best of `reps` of either."""
     import torch
-    src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    if src is None:
+        src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    else:
+        src = src.reshape(-1).view(torch.uint8)
+        nbytes = src.numel() & ~15
+        src = src[:nbytes]
     dst = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     s = torch.cuda.Stream(dev)
     best = 0.0
@@ -1259,7 +1265,7 @@ def main():
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * C * e2e_steps / float(te[0])
-    h2d_gbs = pinned_h2d_gbs(dev)
+    h2d_gbs = pinned_h2d_gbs(dev, src=pinned[0])
 
     wire_bytes = batch_bytes * {1: 2, 2: 3}.get(info["orders16"], 4) // 4
     line = None
