@@ -542,7 +542,9 @@ def run_plan(args, cfg):
                 "d2h_bytes_per_step": C * (8 + 1 + 8 + 4),
                 "path": "Planner.score_plans_d with pinned H2D of the orders and D2H of "
                         "peak_rs/valid/peak_mem/nviol"},
-        "gpu_launches": reps * (6 + 5 * C) if large else reps * 6,
+        # per step: score, lifetimes, the pyramid's three radix sorts (~26 kernels), place,
+        # check, key; past shared memory 3 lifetimes + 4 check kernels per candidate
+        "gpu_launches": reps * (7 * C + 30) if large else reps * 31,
         "feasible_plans": len(ok_idx), "best_plan": best,
         "parity_rows": parity, "clocks": clocks.summary(t0, t1),
         "timing": "CUDA events around stream-ordered mp_score_plans_d calls",
