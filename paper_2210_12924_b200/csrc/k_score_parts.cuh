@@ -6,9 +6,11 @@
 // CTA streams the order row (coalesced int4 loads; pass 0 from HBM, the rest
 // from L2) and keeps only part b's nodes. One 32-bit shared word per local slot
 // holds the node's static scan input in its top byte ((x + 8) | f << 4, set at
-// the start of the pass) and its 1-based position in the low 24 bits (0xffffff = not
-// written this pass):
-//     w = slot[local(v)]; slot[local(v)] = (w & 0xff000000) | (k + 1);  XF[k] = w >> 24
+// the start of the pass) in its low byte and its 1-based position in the top 24 bits
+// (0xffffff = not written this pass):
+//     w = slot[local(v)]; slot[local(v)] = (k + 1) << 8 | (w & 0xff);  XF[k] = (uint8_t)w
+// Position on top lets every lookup compare or max whole words: two written slots
+// differ in position, and an unwritten one fails the permutation check anyway.
 // Then every lookup of part b resolves in shared memory: the permutation check
 // (each local slot written this pass), the validity pairs inside the part, the
 // cross-part pairs through a stash slot written by the earlier part, and the
@@ -103,7 +105,8 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int T = kPartsThreads;
-  constexpr uint32_t kPos = 0xffffffu;  // position bits; all ones = not written this pass
+  constexpr uint32_t kPos = 0xffffffu;  // chunk-table local base bits
+  constexpr uint32_t kUnw = 0xffffff00u;  // slot words >= this: not written this pass
   uint32_t* slot = reinterpret_cast<uint32_t*>(smem);
   uint32_t* ctab_s = reinterpret_cast<uint32_t*>(smem + parts_al16((size_t)(A.nb_max + 2) * 4));
   uint32_t* stash = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(ctab_s) +
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
   // "no sink"), nb_max + 1 reads unwritten (the padding pair of the intra lists)
   if (tid == 0) {
     slot[A.nb_max] = 0;
-    slot[A.nb_max + 1] = kPos;
+    slot[A.nb_max + 1] = kUnw;
   }
   __syncthreads();
 
@@ -169,14 +172,14 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
           const int i = i0 + u * T;
           if (i >= nq) break;
           const uint32_t w = ws[u];
-          uint4 o = make_uint4((w << 24) | kPos, ((w << 16) & 0xff000000u) | kPos,
-                               ((w << 8) & 0xff000000u) | kPos, (w & 0xff000000u) | kPos);
+          uint4 o = make_uint4(kUnw | (w & 0xffu), kUnw | ((w >> 8) & 0xffu),
+                               kUnw | ((w >> 16) & 0xffu), kUnw | (w >> 24));
           if (i >= qlo && i < qhi) {
             const int l = 4 * i;
-            if (l >= plo && l < phi) o.x = (o.x & 0xff000000u) | 1u;
-            if (l + 1 >= plo && l + 1 < phi) o.y = (o.y & 0xff000000u) | 1u;
-            if (l + 2 >= plo && l + 2 < phi) o.z = (o.z & 0xff000000u) | 1u;
-            if (l + 3 >= plo && l + 3 < phi) o.w = (o.w & 0xff000000u) | 1u;
+            if (l >= plo && l < phi) o.x = (o.x & 0xffu) | 0x100u;
+            if (l + 1 >= plo && l + 1 < phi) o.y = (o.y & 0xffu) | 0x100u;
+            if (l + 2 >= plo && l + 2 < phi) o.z = (o.z & 0xffu) | 0x100u;
+            if (l + 3 >= plo && l + 3 < phi) o.w = (o.w & 0xffu) | 0x100u;
           }
           dst[i] = o;
           }
@@ -220,8 +223,8 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
                 const uint32_t a = slot_a + 4u * (e & 0xffffu);
                 const uint32_t w = lds_u32(a);
                 const uint32_t k = kb + ((e >> 16) & 0x1ffu);
-                sts_u32(a, (w & 0xff000000u) | (k + 1));  // 1-based
-                stg_u8(XF + k, w >> 24);
+                sts_u32(a, (k + 1) << 8 | (w & 0xffu));  // 1-based
+                stg_u8(XF + k, w);
               }
             }
             // last reader: drop the consumed 128-byte lines from L2 without a write-back
@@ -323,15 +326,15 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
           if (vq[j] != 0xffffffffu) {  // part b owns this position's node
             const uint32_t a = slot_a + 4u * vq[j];
             const uint32_t w = lds_u32(a);
-            sts_u32(a, (w & 0xff000000u) | (uint32_t)(r0 + (j >> 2) * 128 + (j & 3) + 1));  // 1-based
-            stg_u8(xrow + (j >> 2) * 128 + (j & 3), w >> 24);
+            sts_u32(a, (uint32_t)(r0 + (j >> 2) * 128 + (j & 3) + 1) << 8 | (w & 0xffu));  // 1-based
+            stg_u8(xrow + (j >> 2) * 128 + (j & 3), w);
           }
         }
       }
       __syncthreads();
 
       // ---- resolve part b's lookups in shared memory ---------------------------------
-      // (a slot left unwritten keeps kPos: it fails the permutation check, so the
+      // (a slot left unwritten stays >= kUnw: it fails the permutation check, so the
       // comparisons below never need to tell it apart)
       {  // every local node written this pass (a permutation), and its same-part
          // first producer strictly earlier: own words in 16-byte reads, producer ids
@@ -354,8 +357,8 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
                                     pp[u].y >> 16};
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
-              bad |= (w[h] & kPos) == kPos;
-              bad |= (slot[pr[h]] & kPos) >= (w[h] & kPos);  // none: the position-0 sentinel
+              bad |= w[h] >= kUnw;
+              bad |= slot[pr[h]] >= w[h];  // none: the position-0 sentinel (word 0)
             }
           }
         }
@@ -381,18 +384,18 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
           const uint32_t es[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
           for (int h = 0; h < 8; ++h)  // producer later
-            bad |= (slot[es[h] & 0xffffu] & kPos) >= (slot[es[h] >> 16] & kPos);
+            bad |= slot[es[h] & 0xffffu] >= slot[es[h] >> 16];
         }
       }
       groups(A.xput, D.xput_off, D.xput_n,
-             [&](uint32_t e) { stash[e >> 16] = slot[e & 0xffffu] & kPos; });
+             [&](uint32_t e) { stash[e >> 16] = slot[e & 0xffffu] >> 8; });
       groups(A.xchk, D.xchk_off, D.xchk_n, [&](uint32_t e) {
         const uint32_t s = stash[(e >> 16) & 0x7fffu];
-        const uint32_t p = slot[e & 0xffffu] & kPos;
+        const uint32_t p = slot[e & 0xffffu] >> 8;
         if ((e >> 31) ? p >= s : s >= p) bad = true;
       });
       groups(A.xmax, D.xmax_off, D.xmax_n,
-             [&](uint32_t e) { atomicMax(&stash[e >> 16], slot[e & 0xffffu] & kPos); });
+             [&](uint32_t e) { atomicMax(&stash[e >> 16], slot[e & 0xffffu] >> 8); });
       for (int i = tid; i < D.dyn_n; i += 4 * T) {  // multi-consumer tensors inside the part
         uint4 dd[4];  // four records' loads in flight
 #pragma unroll
@@ -404,8 +407,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
           if (d.z == 0) continue;  // padding (every real record frees >= 1 unit)
           const uint32_t l1 = d.x & 0xffffu, l2 = d.x >> 16, l3 = d.y & 0xffffu, l4 = d.y >> 16;
           // missing sinks read the position-0 sentinel
-          const uint32_t h = max(max(slot[l1] & kPos, slot[l2] & kPos),
-                                 max(slot[l3] & kPos, slot[l4] & kPos));
+          const uint32_t h = max(max(slot[l1], slot[l2]), max(slot[l3], slot[l4])) >> 8;
           const uint32_t hi = h - 1u;  // 1-based; unwritten (invalid orders) or 0 -> skipped
           if (hi < (uint32_t)n) parts_free_at(XF, (int)hi, d.z);
         }
@@ -419,8 +421,8 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
                                        : make_uint4(s2, 0, s2, 0);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const uint32_t ha = max(slot[dd[u].x & 0xffffu] & kPos, slot[dd[u].x >> 16] & kPos) - 1u;
-          const uint32_t hb = max(slot[dd[u].z & 0xffffu] & kPos, slot[dd[u].z >> 16] & kPos) - 1u;
+          const uint32_t ha = (max(slot[dd[u].x & 0xffffu], slot[dd[u].x >> 16]) >> 8) - 1u;
+          const uint32_t hb = (max(slot[dd[u].z & 0xffffu], slot[dd[u].z >> 16]) >> 8) - 1u;
           if (ha < (uint32_t)n) parts_free_at(XF, (int)ha, dd[u].y);
           if (hb < (uint32_t)n) parts_free_at(XF, (int)hb, dd[u].w);
         }
