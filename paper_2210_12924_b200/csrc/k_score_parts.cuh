@@ -88,6 +88,22 @@ __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
 // words (needs P <= 7 - part 7 marks nothing - and n <= 512 * kPartsMaxBlocks).
 // Measured: one list read by every later pass beats one list per part (two ballots
 // per position to append) at C5.
+// MP_PARTS_PROF (a profiling build only): thread 0 of CTA 0 accumulates the clock cycles
+// between the phase barriers and prints them at exit
+#ifdef MP_PARTS_PROF
+#define MP_PARTS_T0() \
+  unsigned long long prof_acc[15] = {}, prof_last = clock64();
+#define MP_PARTS_T(i)                                  \
+  if (tid == 0) {                                      \
+    const unsigned long long t_ = clock64();           \
+    prof_acc[(i)] += t_ - prof_last;                   \
+    prof_last = t_;                                    \
+  }
+#else
+#define MP_PARTS_T0()
+#define MP_PARTS_T(i)
+#endif
+
 template <bool kVec, bool k24 = false, bool kDefer = false>
 __global__ void __launch_bounds__(kPartsThreads, 1)
     score_parts_kernel(PartArgs A, int32_t n, const int32_t* __restrict__ orders, int64_t C,
@@ -141,6 +157,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
     slot[A.nb_max + 1] = kUnw;
   }
   __syncthreads();
+  MP_PARTS_T0();
 
   for (int64_t c = blockIdx.x; c < C; c += gridDim.x) {
     const int32_t* ord = orders + c * (int64_t)n;
@@ -186,6 +203,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
         }
       }
       __syncthreads();
+      MP_PARTS_T(3 * min(b, 3));
 
       // ---- stream the order: keep part b's nodes -----------------------------------
       // 16 positions per thread per iteration: their chunk-table lookups are issued
@@ -332,6 +350,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
         }
       }
       __syncthreads();
+      MP_PARTS_T(3 * min(b, 3) + 1);
 
       // ---- resolve part b's lookups in shared memory ---------------------------------
       // (a slot left unwritten stays >= kUnw: it fails the permutation check, so the
@@ -428,13 +447,16 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
         }
       }
       __syncthreads();  // slot words are rewritten by the next pass
+      MP_PARTS_T(3 * min(b, 3) + 2);
     }
     for (int i = tid; i < A.n_xfree; i += T) {  // multi-consumer tensors spanning parts
       const uint2 f = __ldg(A.xfree + i);
       const uint32_t hi = stash[f.x] - 1u;  // 1-based positions
       if (hi < (uint32_t)n) parts_free_at(XF, (int)hi, f.y);
     }
-    if (__syncthreads_or(bad)) {
+    const bool any_bad = __syncthreads_or(bad);
+    MP_PARTS_T(12);
+    if (any_bad) {
       if (tid == 0) {
         peak_out[c] = 0;
         step_out[c] = 0;
@@ -497,6 +519,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
       s_widx[warp] = best_i;
     }
     __syncthreads();
+    MP_PARTS_T(13);
     if (warp == 0) {
       const uint32_t tot = s_wsum[lane];
       uint32_t v = warp_incl_scan(tot, lane) - tot + s_wbest[lane];  // RS at the local max
@@ -512,4 +535,8 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
     }
     // s_wsum / s_wbest are rewritten after >= 2 barriers of the next candidate
   }
+#ifdef MP_PARTS_PROF
+  if (tid == 0 && blockIdx.x == 0)
+    for (int i = 0; i < 15; ++i) printf("MP_PARTS_PROF phase %d cycles %llu\n", i, prof_acc[i]);
+#endif
 }
