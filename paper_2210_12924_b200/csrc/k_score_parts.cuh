@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
   const uint32_t ctab_a = opaque_u32((uint32_t)__cvta_generic_to_shared(ctab_s));
   uint8_t* XF = reinterpret_cast<uint8_t*>(
       opaque_u64(reinterpret_cast<uint64_t>(gxf + (size_t)blockIdx.x * gstride)));
-  const int seg = A.seg;  // positions per warp segment, a multiple of 128
+  const int seg = A.seg;  // positions per warp segment, a multiple of 512 (lane chunks of 16-byte multiples)
   const int wbeg = warp * seg;
   const int wend = wbeg + seg;   // loops run in 512-position steps and stop at wend
   const int wlim = min(n, wend);  // this warp's real positions end here
@@ -471,43 +471,41 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
     // (adding the segment's true starting RS moves every local value by the same
     // amount, so the arg-max is the same); warp 0 then adds the exclusive prefix of the
     // totals and takes the first maximum over the warps.
-    int32_t carry = 0;
+    // Lane chunks: lane L scans its own cs = seg / 32 consecutive positions of the warp's
+    // segment sequentially (16-byte L2 loads, three in flight), keeping its local total and
+    // its first local maximum (strict >: a padding position, x = f = 0, never beats the
+    // positions before it). One warp scan of the lane totals then shifts each lane's maximum
+    // by the lane's exclusive prefix (the same shift for all of a lane's positions, so its
+    // arg-max stands), and the warp arg-max (smallest index on ties) takes the first.
+    // Against one warp scan per 128 positions this has no shuffle chain per row.
+    const int cs = seg >> 5;  // a multiple of 16 (seg % 512 == 0)
+    const int l0 = wbeg + lane * cs;
+    int32_t run = 0;
     int32_t best = INT32_MIN;
-    int best_i = wbeg;
-    for (int r00 = wbeg; r00 < wend; r00 += 4 * 128) {
-      uint32_t w4s[4];
+    int best_i = l0;
+    for (int r = 0; r < cs; r += 48) {
+      uint4 q[3];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)  // four loads in flight, then the dependent scan
-        w4s[u] = r00 + u * 128 < wend
-                     ? __ldcg(reinterpret_cast<const unsigned int*>(XF + r00 + u * 128 + 4 * lane))
-                     : 0x08080808u;  // the next warp's positions: padding (x 0, f 0)
+      for (int u = 0; u < 3; ++u)  // past the chunk: padding (x 0, f 0)
+        q[u] = r + 16 * u < cs ? __ldcg(reinterpret_cast<const uint4*>(XF + l0 + r + 16 * u))
+                               : make_uint4(0x08080808u, 0x08080808u, 0x08080808u, 0x08080808u);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int r = r00 + u * 128 + 4 * lane;
-        const uint32_t w4 = w4s[u];
-        int32_t xs[4], fs[4], t = 0;
+      for (int u = 0; u < 3; ++u) {
+        const uint32_t ws[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t byte = (w4 >> (8 * q)) & 0xffu;
-          xs[q] = (int32_t)(byte & 0xfu) - 8;
-          fs[q] = (int32_t)(byte >> 4);
-          t += xs[q];
-        }
-        const int32_t incl = warp_incl_scan(t, lane);
-        int32_t run = carry + incl - t;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          run += xs[q];
-          const int32_t rs = run + fs[q];
-          // padding positions (k >= n) carry RS <= RS(n-1): they never beat a real
-          // position (strict >, and the smaller index wins ties across lanes)
+        for (int h = 0; h < 16; ++h) {
+          const uint32_t byte = (ws[h >> 2] >> (8 * (h & 3))) & 0xffu;
+          run += (int32_t)(byte & 0xfu) - 8;
+          const int32_t rs = run + (int32_t)(byte >> 4);
           const bool better = rs > best;
           best = better ? rs : best;
-          best_i = better ? r + q : best_i;
+          best_i = better ? l0 + r + 16 * u + h : best_i;
         }
-        carry += __shfl_sync(0xffffffffu, incl, 31);
       }
     }
+    const int32_t incl = warp_incl_scan(run, lane);
+    const int32_t carry = __shfl_sync(0xffffffffu, incl, 31);  // the segment's x total
+    best += incl - run;  // RS relative to the segment start at the lane's maximum
     warp_argmax(best, best_i);
     // XF is rewritten by the next candidate: drop this segment's lines from L2 without
     // a write-back (not the line holding position n - its padding bytes persist)

@@ -329,7 +329,7 @@ mp_status mp_graph_upload(mp_ctx* ctx, const mp_csr* csr, mp_graph** out) {
       Q.n_xfree = (int32_t)(pp.xfree.size() / 2);
       Q.n_cross_pairs = pp.n_cross_pairs;
       Q.n_cross_dyn = pp.n_cross_dyn;
-      Q.seg = ((n + 32 * 128 - 1) / (32 * 128)) * 128;  // per-warp segment, 128-multiple
+      Q.seg = ((n + 32 * 512 - 1) / (32 * 512)) * 512;  // per-warp segment: 32 lane chunks of 16-byte multiples
       Q.smem = parts_smem_bytes(pp);
       std::vector<int32_t> desc(pp.desc.size() * (sizeof(PartDesc) / 4));
       std::memcpy(desc.data(), pp.desc.data(), desc.size() * 4);
