@@ -47,6 +47,10 @@ constexpr int kPartsThreads = 1024;
 #endif
 constexpr int kPartsU = MP_PARTS_U;  // 16-byte order loads per thread per stream iteration
 constexpr int kPartsMaxBlocks = 512;  // kDefer: 512-position blocks (n <= 262,144)
+#ifndef MP_SCAN_U
+#define MP_SCAN_U 3
+#endif
+constexpr int kScanU = MP_SCAN_U;  // 16-byte XF loads in flight per lane in the scan
 
 __device__ __forceinline__ size_t parts_al16(size_t b) { return (b + 15) & ~size_t(15); }
 
@@ -472,7 +476,7 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
     // amount, so the arg-max is the same); warp 0 then adds the exclusive prefix of the
     // totals and takes the first maximum over the warps.
     // Lane chunks: lane L scans its own cs = seg / 32 consecutive positions of the warp's
-    // segment sequentially (16-byte L2 loads, three in flight), keeping its local total and
+    // segment sequentially (16-byte L2 loads, kScanU in flight), keeping its local total and
     // its first local maximum (strict >: a padding position, x = f = 0, never beats the
     // positions before it). One warp scan of the lane totals then shifts each lane's maximum
     // by the lane's exclusive prefix (the same shift for all of a lane's positions, so its
@@ -483,14 +487,14 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
     int32_t run = 0;
     int32_t best = INT32_MIN;
     int best_i = l0;
-    for (int r = 0; r < cs; r += 48) {
-      uint4 q[3];
+    for (int r = 0; r < cs; r += 16 * kScanU) {
+      uint4 q[kScanU];
 #pragma unroll
-      for (int u = 0; u < 3; ++u)  // past the chunk: padding (x 0, f 0)
+      for (int u = 0; u < kScanU; ++u)  // past the chunk: padding (x 0, f 0)
         q[u] = r + 16 * u < cs ? __ldcg(reinterpret_cast<const uint4*>(XF + l0 + r + 16 * u))
                                : make_uint4(0x08080808u, 0x08080808u, 0x08080808u, 0x08080808u);
 #pragma unroll
-      for (int u = 0; u < 3; ++u) {
+      for (int u = 0; u < kScanU; ++u) {
         const uint32_t ws[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
 #pragma unroll
         for (int h = 0; h < 16; ++h) {
