@@ -51,6 +51,10 @@ constexpr int kPartsMaxBlocks = 512;  // kDefer: 512-position blocks (n <= 262,1
 #define MP_SCAN_U 3
 #endif
 constexpr int kScanU = MP_SCAN_U;  // 16-byte XF loads in flight per lane in the scan
+#ifndef MP_LOOK_U
+#define MP_LOOK_U 4
+#endif
+constexpr int kLookU = MP_LOOK_U;  // first-producer / two-sink groups' loads in flight
 
 __device__ __forceinline__ size_t parts_al16(size_t b) { return (b + 15) & ~size_t(15); }
 
@@ -365,13 +369,13 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
         const uint4* sw = reinterpret_cast<const uint4*>(slot);
         const uint2* p1 = reinterpret_cast<const uint2*>(A.p1 + D.xtab_off);
         const int nq = D.nloc >> 2;
-        for (int i0 = tid; i0 < nq; i0 += 4 * T) {  // four groups' loads in flight
-          uint2 pp[4];
+        for (int i0 = tid; i0 < nq; i0 += kLookU * T) {  // kLookU groups' loads in flight
+          uint2 pp[kLookU];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int u = 0; u < kLookU; ++u)
             pp[u] = i0 + u * T < nq ? __ldg(p1 + i0 + u * T) : make_uint2(~0u, ~0u);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < kLookU; ++u) {
             const int i = i0 + u * T;
             if (i >= nq) break;
             const uint4 q = sw[i];
@@ -436,14 +440,14 @@ __global__ void __launch_bounds__(kPartsThreads, 1)
         }
       }
       const uint32_t s2 = (uint32_t)A.nb_max * 0x10001u;  // both sinks: position 0
-      for (int i = tid; i < D.dyn2_n; i += 4 * T) {  // two-sink tensors, two per 16 bytes
-        uint4 dd[4];
+      for (int i = tid; i < D.dyn2_n; i += kLookU * T) {  // two-sink tensors, two per 16 bytes
+        uint4 dd[kLookU];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)  // past the end: the sentinel pair (no free)
+        for (int u = 0; u < kLookU; ++u)  // past the end: the sentinel pair (no free)
           dd[u] = i + u * T < D.dyn2_n ? __ldg(A.dyn4 + D.dyn2_off + i + u * T)
                                        : make_uint4(s2, 0, s2, 0);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kLookU; ++u) {
           const uint32_t ha = (max(slot[dd[u].x & 0xffffu], slot[dd[u].x >> 16]) >> 8) - 1u;
           const uint32_t hb = (max(slot[dd[u].z & 0xffffu], slot[dd[u].z >> 16]) >> 8) - 1u;
           if (ha < (uint32_t)n) parts_free_at(XF, (int)ha, dd[u].y);
