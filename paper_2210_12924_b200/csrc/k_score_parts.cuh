@@ -5,8 +5,8 @@
 // candidate's positions never leave the SM: in pass b (one per node part) the
 // CTA streams the order row (coalesced int4 loads; pass 0 from HBM, the rest
 // from L2) and keeps only part b's nodes. One 32-bit shared word per local slot
-// holds the node's static scan input in its top byte ((x + 8) | f << 4, set at
-// the start of the pass) in its low byte and its 1-based position in the top 24 bits
+// holds the node's static scan input ((x + 8) | f << 4, set at the start of the
+// pass) in its low byte and its 1-based position in the top 24 bits
 // (0xffffff = not written this pass):
 //     w = slot[local(v)]; slot[local(v)] = (k + 1) << 8 | (w & 0xff);  XF[k] = (uint8_t)w
 // Position on top lets every lookup compare or max whole words: two written slots
